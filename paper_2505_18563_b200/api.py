@@ -1,0 +1,547 @@
+"""Python host mirror of the reference operator API for the hot path.
+
+Same names, argument meaning and error behaviour as the reference C++ API
+(/root/reference/proj/include/pact/{tensor,sparsity,codec,collective}.hpp),
+but tensors are CUDA fp32 ``torch.Tensor``s and every computation runs in
+the sm_100a kernels behind include/pact_c.h. torch is used only for device
+memory, streams and torch.distributed plumbing.
+
+Deviations, all deliberate:
+  * ``FlatTensor`` is a 1-D CUDA float32 torch.Tensor.
+  * ``masked_allreduce`` / ``full_allreduce`` take a :class:`Comm` backed by
+    NCCL (one process per GPU) instead of a ring ``Transport``; passing
+    ``comm=None`` runs the single-GPU path (pack -> unpack, no exchange),
+    which the reference cannot express (it rejects n < 2).
+  * ``SyncStats.seconds`` is measured device time, not a virtual clock;
+    ``bytes_on_wire`` keeps the reference's ring accounting exactly.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import torch
+
+from . import _lib
+from ._lib import check, lib
+
+# ------------------------------------------------------------------ errors
+
+
+class Errc(enum.IntEnum):  # error.hpp:10-26, same order
+    DuplicateParam = 0
+    InvalidView = 1
+    InvalidRatio = 2
+    InvalidRate = 3
+    NumericalFailure = 4
+    ShapeMismatch = 5
+    MaskMismatch = 6
+    CorruptPayload = 7
+    LinkError = 8
+    UndefinedMetric = 9
+    MissingFile = 10
+    ParseError = 11
+    UnknownKey = 12
+    BadTopology = 13
+    RunFailure = 14
+
+
+class Error(RuntimeError):
+    """error.hpp:51-62. ``code`` is an :class:`Errc` (None for CUDA/NCCL
+    failures, whose C status is in ``status``)."""
+
+    def __init__(self, code: Optional[Errc], what: str, status: int = 0):
+        super().__init__(what)
+        self.code = code
+        self.status = status
+
+
+def _call(fn, *args):
+    st = fn(*args)
+    if st != 0:
+        msg = lib.pact_last_error().decode(errors="replace")
+        code = Errc(st - 1) if 1 <= st <= 15 else None
+        raise Error(code, msg, st)
+
+
+def _stream() -> C.c_void_p:
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _ptr(t: Optional[torch.Tensor]) -> C.c_void_p:
+    return C.c_void_p(t.data_ptr() if t is not None else 0)
+
+
+def _as_grad(x: torch.Tensor, name: str = "tensor") -> torch.Tensor:
+    if not isinstance(x, torch.Tensor) or not x.is_cuda or x.dtype != torch.float32:
+        raise TypeError(f"{name} must be a CUDA float32 tensor")
+    return x.contiguous().view(-1)
+
+
+# ---------------------------------------------------------------- context
+
+
+class Context:
+    """One pact_ctx per CUDA device (workspace, streams)."""
+
+    _by_device: dict = {}
+
+    def __init__(self, device: int):
+        h = C.c_void_p()
+        _call(lib.pact_ctx_create, device, C.byref(h))
+        self.handle = h
+        self.device = device
+
+    @classmethod
+    def get(cls, device: Optional[int] = None) -> "Context":
+        if device is None:
+            device = torch.cuda.current_device()
+        if device not in cls._by_device:
+            cls._by_device[device] = Context(device)
+        return cls._by_device[device]
+
+    def kernel_launches(self) -> int:
+        return int(lib.pact_ctx_kernel_launches(self.handle))
+
+
+# ------------------------------------------------------------------ masks
+
+
+class _CudaArray:
+    """__cuda_array_interface__ shim so torch can view library-owned memory."""
+
+    def __init__(self, ptr: int, n: int, typestr: str, owner):
+        self.__cuda_array_interface__ = {
+            "shape": (n,), "typestr": typestr, "data": (ptr, False), "version": 3, "strides": None,
+        }
+        self._owner = owner
+
+
+class SparsityMask:
+    """tensor.hpp:78-106, device resident. Words use the reference layout
+    (bit i at words[i>>6] bit i&63, tail bits zero)."""
+
+    def __init__(self, length: int, ctx: Optional[Context] = None):
+        self.ctx = ctx or Context.get()
+        h = C.c_void_p()
+        _call(lib.pact_mask_create, self.ctx.handle, int(length), C.byref(h))
+        self.handle = h
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and h.value:
+            lib.pact_mask_destroy(h)
+            self.handle = None
+
+    # -- constructors (tensor.cpp:87-105)
+    @staticmethod
+    def all_ones(length: int) -> "SparsityMask":
+        m = SparsityMask(length)
+        _call(lib.pact_mask_fill, m.handle, 1, _stream())
+        return m
+
+    @staticmethod
+    def all_zeros(length: int) -> "SparsityMask":
+        m = SparsityMask(length)
+        _call(lib.pact_mask_fill, m.handle, 0, _stream())
+        return m
+
+    @staticmethod
+    def from_words(words: torch.Tensor, length: int) -> "SparsityMask":
+        m = SparsityMask(length)
+        w = words.to(device=f"cuda:{m.ctx.device}", dtype=torch.int64).contiguous().view(-1)
+        if w.numel() != (length + 63) // 64:
+            raise Error(Errc.ShapeMismatch, f"{w.numel()} words for {length} bits")
+        _call(lib.pact_mask_set_words, m.handle, _ptr(w), _stream())
+        return m
+
+    @staticmethod
+    def from_bits(bits) -> "SparsityMask":
+        b = torch.as_tensor(bits, dtype=torch.bool).view(-1).cpu()
+        n = b.numel()
+        padded = torch.zeros(((n + 63) // 64) * 64, dtype=torch.bool)
+        padded[:n] = b
+        import numpy as np
+
+        words = np.packbits(padded.numpy().reshape(-1, 8), axis=1, bitorder="little").reshape(-1).view(np.int64)
+        return SparsityMask.from_words(torch.from_numpy(words.copy()), n)
+
+    # -- accessors
+    def _info(self) -> _lib.MaskInfo:
+        info = _lib.MaskInfo()
+        _call(lib.pact_mask_info_get, self.handle, C.byref(info))
+        return info
+
+    def size(self) -> int:
+        return int(self._info().len)
+
+    def nnz(self) -> int:
+        return int(self._info().nnz)
+
+    def digest(self) -> int:
+        d = C.c_uint64()
+        _call(lib.pact_mask_digest, self.handle, _stream(), C.byref(d))
+        return int(d.value)
+
+    @property
+    def changed(self) -> bool:
+        return bool(self._info().changed)
+
+    def words(self) -> torch.Tensor:
+        """Zero-copy int64 view of the device words (valid while self lives)."""
+        info = self._info()
+        n = (int(info.len) + 63) // 64
+        return torch.as_tensor(_CudaArray(int(info.words or 0), n, "<i8", self), device=f"cuda:{self.ctx.device}")
+
+    def tile_offsets(self) -> torch.Tensor:
+        info = self._info()
+        return torch.as_tensor(_CudaArray(int(info.tile_off), int(info.ntiles) + 1, "<u4", self),
+                               device=f"cuda:{self.ctx.device}")
+
+    def words_host(self):
+        return self.words().cpu().numpy().view("uint64").copy()
+
+    def test(self, i: int) -> bool:
+        w = int(self.words()[i >> 6].item()) & 0xFFFFFFFFFFFFFFFF
+        return bool((w >> (i & 63)) & 1)
+
+    def with_bit(self, i: int, keep: bool) -> "SparsityMask":  # tensor.cpp:107-115
+        w = self.words().clone()
+        word = int(w[i >> 6].item()) & 0xFFFFFFFFFFFFFFFF
+        word = word | (1 << (i & 63)) if keep else word & ~(1 << (i & 63))
+        if word >= 1 << 63:
+            word -= 1 << 64
+        w[i >> 6] = word
+        return SparsityMask.from_words(w, self.size())
+
+    def __eq__(self, other) -> bool:
+        return isinstance(other, SparsityMask) and self.size() == other.size() and bool(
+            torch.equal(self.words(), other.words()))
+
+    __hash__ = None
+
+
+def mask_digest(mask: SparsityMask) -> int:  # tensor.hpp:110
+    return mask.digest()
+
+
+# ------------------------------------------------------------------ prune
+
+
+@dataclass
+class PruneConfig:  # sparsity.hpp:24-31 (magnitude method only)
+    ratio: float = 0.0
+
+    def validate(self) -> None:
+        if not (0.0 <= self.ratio < 1.0):
+            raise Error(Errc.InvalidRatio, f"prune ratio {self.ratio} outside [0, 1)")
+
+
+def drop_count(ratio: float, length: int) -> int:  # sparsity.cpp:33-40
+    k = C.c_uint64()
+    _call(lib.pact_drop_count, C.c_float(ratio), int(length), C.byref(k))
+    return int(k.value)
+
+
+def magnitude_prune(weights: torch.Tensor, ratio: float, out: Optional[SparsityMask] = None,
+                    stats: Optional[dict] = None) -> SparsityMask:
+    """sparsity.cpp:44-59: keep all but the k smallest |w| (ties drop the lower
+    index first). ``out`` reuses a mask (its ``changed`` flag then reports
+    whether the words moved, which feeds the tracker without a digest)."""
+    w = _as_grad(weights, "weights")
+    m = out if out is not None else SparsityMask(w.numel())
+    ps = _lib.PruneStats()
+    _call(lib.pact_prune_magnitude, m.ctx.handle, _ptr(w), w.numel(), C.c_float(ratio), m.handle,
+          _stream(), C.byref(ps))
+    if stats is not None:
+        stats.update(k=ps.k, threshold=ps.threshold, c_lt=ps.c_lt, path=ps.path, candidates=ps.candidates)
+    return m
+
+
+def build_prune_mask(weights: torch.Tensor, cfg: PruneConfig) -> SparsityMask:  # sparsity.cpp:121-128
+    cfg.validate()
+    return magnitude_prune(weights, cfg.ratio)
+
+
+def enforce_gradient_sparsity(grad: torch.Tensor, mask: SparsityMask, out: Optional[torch.Tensor] = None
+                              ) -> torch.Tensor:
+    """sparsity.cpp:112-119 (out may be grad for the in-place variant)."""
+    g = _as_grad(grad, "grad")
+    o = torch.empty_like(g) if out is None else out
+    _call(lib.pact_gse, mask.ctx.handle, _ptr(g), g.numel(), mask.handle, _ptr(o), _stream())
+    return o
+
+
+class TrackerStatus(enum.Enum):  # sparsity.hpp:33
+    Stable = 0
+    Unstable = 1
+
+
+class MaskTracker:
+    """sparsity.hpp:37-54 / sparsity.cpp:17-25 (host state machine)."""
+
+    def __init__(self, stability_threshold: int = 3):
+        self._t = _lib.Tracker()
+        lib.pact_tracker_init(C.byref(self._t), int(stability_threshold))
+
+    def observe(self, mask: SparsityMask) -> TrackerStatus:
+        return self.observe_digest(mask.digest())
+
+    def observe_digest(self, digest: int) -> TrackerStatus:
+        s = lib.pact_tracker_observe(C.byref(self._t), int(digest) & 0xFFFFFFFFFFFFFFFF)
+        return TrackerStatus.Stable if s else TrackerStatus.Unstable
+
+    def status(self) -> TrackerStatus:
+        return TrackerStatus.Stable if lib.pact_tracker_status(C.byref(self._t)) else TrackerStatus.Unstable
+
+    def stable_count(self) -> int:
+        return int(self._t.stable_count)
+
+    def last_digest(self) -> Optional[int]:
+        return int(self._t.last_digest) if self._t.has_last else None
+
+
+def tracker_observe(tracker: MaskTracker, mask: SparsityMask) -> TrackerStatus:
+    return tracker.observe(mask)
+
+
+# ------------------------------------------------------------------ codec
+
+
+@dataclass
+class PackedGradient:  # codec.hpp:19-23
+    mask_digest: int = 0
+    epoch: int = 0
+    values: Optional[torch.Tensor] = None
+
+
+def pack(grad: torch.Tensor, mask: SparsityMask, epoch: int) -> PackedGradient:  # codec.cpp:14-25
+    g = _as_grad(grad, "grad")
+    if g.numel() != mask.size():
+        raise Error(Errc.ShapeMismatch, f"gradient length {g.numel()} != mask length {mask.size()}")
+    vals = torch.empty(max(1, mask.nnz()), dtype=torch.float32, device=g.device)[: mask.nnz()]
+    _call(lib.pact_pack, mask.ctx.handle, _ptr(g), g.numel(), mask.handle, _ptr(vals), 0,
+          C.c_uint64(0xFFFFFFFFFFFFFFFF), _stream())
+    return PackedGradient(mask.digest(), int(epoch), vals)
+
+
+def unpack(packed: PackedGradient, mask: SparsityMask, scale: float = 1.0,
+           out: Optional[torch.Tensor] = None) -> torch.Tensor:  # codec.cpp:27-38
+    vals = packed.values if packed.values is not None else torch.empty(0, device="cuda")
+    o = torch.empty(mask.size(), dtype=torch.float32, device=f"cuda:{mask.ctx.device}") if out is None else out
+    _call(lib.pact_unpack, mask.ctx.handle, _ptr(vals), vals.numel(),
+          C.c_uint64(int(packed.mask_digest) & 0xFFFFFFFFFFFFFFFF), 1, mask.handle,
+          C.c_float(scale), _ptr(o), 0, C.c_uint64(0xFFFFFFFFFFFFFFFF), _stream())
+    return o
+
+
+def unpack_sgd(packed_values: torch.Tensor, mask: SparsityMask, scale: float, lr: float,
+               weights: torch.Tensor, grad_out: Optional[torch.Tensor] = None) -> None:
+    """Fused unpack + to_mean + masked SGD step (trainer.cpp:202-214, 268-273)."""
+    _call(lib.pact_unpack_sgd, mask.ctx.handle, _ptr(packed_values), packed_values.numel(),
+          mask.handle, C.c_float(scale), C.c_float(lr), _ptr(grad_out), _ptr(weights), _stream())
+
+
+class PayloadKind(enum.IntEnum):  # codec.hpp:80-86
+    Full = 0
+    Packed = 1
+    Ternary = 2
+    Fp16 = 3
+    TopK = 4
+
+
+@dataclass
+class FrameHeader:  # codec.hpp:93-98
+    kind: PayloadKind = PayloadKind.Full
+    epoch: int = 0
+    mask_digest: int = 0
+    value_count: int = 0
+
+
+def encode_header(h: FrameHeader) -> bytes:  # codec.cpp:257-259
+    ch = _lib.FrameHeader(int(h.kind), h.epoch, h.mask_digest & 0xFFFFFFFFFFFFFFFF, h.value_count)
+    out = (C.c_uint8 * 26)()
+    _call(lib.pact_header_encode, C.byref(ch), out)
+    return bytes(out)
+
+
+def decode_header(frame: bytes) -> FrameHeader:  # codec.cpp:261-275
+    buf = (C.c_uint8 * max(1, len(frame))).from_buffer_copy(bytes(frame) or b"\0")
+    ch = _lib.FrameHeader()
+    _call(lib.pact_header_decode, buf, len(frame), C.byref(ch))
+    return FrameHeader(PayloadKind(ch.kind), ch.epoch, ch.mask_digest, ch.value_count)
+
+
+# -------------------------------------------------------------- collective
+
+
+class SyncMode(enum.IntEnum):  # collective.hpp:58-64
+    FullAllReduce = 0
+    PackedAllReduce = 1
+    TernaryAllGather = 2
+    TopKAllGather = 3
+    Fp16AllReduce = 4
+
+
+def decide_sync_mode(requested: SyncMode, tracker: TrackerStatus) -> SyncMode:  # collective.cpp:62-67
+    return SyncMode(lib.pact_decide_sync_mode(int(requested), int(tracker == TrackerStatus.Stable)))
+
+
+def vote_decide(frames: Sequence[bytes], mine: FrameHeader, stable: bool) -> bool:
+    """collective.cpp:285-293 unanimity rule (host scalar logic)."""
+    blob = b"".join(frames)
+    buf = (C.c_uint8 * max(1, len(blob))).from_buffer_copy(blob or b"\0")
+    ch = _lib.FrameHeader(int(mine.kind), mine.epoch, mine.mask_digest & 0xFFFFFFFFFFFFFFFF, mine.value_count)
+    agree = C.c_int()
+    _call(lib.pact_vote_decide, buf, len(frames), C.byref(ch), int(bool(stable)), C.byref(agree))
+    return bool(agree.value)
+
+
+def ring_bytes(n: int, position: int, count: int) -> int:
+    return int(lib.pact_ring_bytes(n, position, count))
+
+
+def masked_bytes(n: int, position: int, count: int) -> int:
+    return int(lib.pact_masked_bytes(n, position, count))
+
+
+@dataclass
+class SyncStats:  # collective.hpp:73-77
+    bytes_on_wire: int = 0
+    seconds: float = 0.0
+    mode_used: SyncMode = SyncMode.FullAllReduce
+    buckets: int = 0
+    value_count: int = 0
+    fallback_reason: int = 0
+
+
+@dataclass
+class AggregateResult:  # collective.hpp:130-133
+    tensor: Optional[torch.Tensor] = None
+    stats: SyncStats = field(default_factory=SyncStats)
+
+
+@dataclass
+class SyncPolicy:
+    """Adaptive knobs. Defaults == reference policy."""
+
+    density_threshold: float = 0.0   # fall back to dense above this agreed density (0: never)
+    bucket_bytes: int = 0            # packed bytes per overlapped bucket (0: one bucket)
+    scale: float = 1.0               # fused into unpack (1/n gives the mean)
+    time_stages: bool = False
+
+    def c(self) -> _lib.PolicyC:
+        return _lib.PolicyC(self.density_threshold, self.bucket_bytes, self.scale, int(self.time_stages))
+
+
+def _stats(s: _lib.SyncStatsC) -> SyncStats:
+    return SyncStats(int(s.bytes_on_wire), float(s.seconds), SyncMode(s.mode_used), int(s.buckets),
+                     int(s.value_count), int(s.fallback_reason))
+
+
+class Comm:
+    """NCCL-backed worker endpoint (collective.hpp:89-116), one per GPU."""
+
+    def __init__(self, rank: int, world_size: int, unique_id: bytes, ctx: Optional[Context] = None):
+        self.ctx = ctx or Context.get()
+        buf = (C.c_uint8 * 128).from_buffer_copy(unique_id)
+        h = C.c_void_p()
+        _call(lib.pact_comm_create, self.ctx.handle, buf, int(world_size), int(rank), C.byref(h))
+        self.handle = h
+
+    @staticmethod
+    def unique_id() -> bytes:
+        out = (C.c_uint8 * 128)()
+        _call(lib.pact_comm_unique_id, out)
+        return bytes(out)
+
+    @staticmethod
+    def from_process_group(group=None, ctx: Optional[Context] = None) -> "Comm":
+        """Rendezvous over an initialised torch.distributed group (gloo or nccl)."""
+        import torch.distributed as dist
+
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        obj = [Comm.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        return Comm(rank, world, obj[0], ctx)
+
+    def rank(self) -> int:
+        return int(lib.pact_comm_rank(self.handle))
+
+    def world_size(self) -> int:
+        return int(lib.pact_comm_size(self.handle))
+
+    def close(self) -> None:
+        if getattr(self, "handle", None) is not None and self.handle.value:
+            lib.pact_comm_destroy(self.handle)
+            self.handle = None
+
+
+def ring_allreduce(local: torch.Tensor, comm: Comm, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """collective.cpp:165-216 semantics (SUM); NCCL chooses the reduction order."""
+    g = _as_grad(local, "local")
+    o = torch.empty_like(g) if out is None else out
+    _call(lib.pact_allreduce_sum, comm.handle, _ptr(g), _ptr(o), g.numel(), _stream())
+    return o
+
+
+def allgather(payload: bytes, comm: Comm) -> list:
+    """collective.cpp:222-247 for equal-size frames; result indexed by rank."""
+    n = comm.world_size()
+    src = (C.c_uint8 * max(1, len(payload))).from_buffer_copy(payload or b"\0")
+    dst = (C.c_uint8 * max(1, len(payload) * n))()
+    _call(lib.pact_allgather_frames, comm.handle, src, len(payload), dst, _stream())
+    raw = bytes(dst)
+    return [raw[i * len(payload):(i + 1) * len(payload)] for i in range(n)]
+
+
+def full_allreduce(grad: torch.Tensor, comm: Comm, scale: float = 1.0,
+                   out: Optional[torch.Tensor] = None) -> AggregateResult:  # collective.cpp:253-259
+    g = _as_grad(grad, "grad")
+    o = torch.empty_like(g) if out is None else out
+    st = _lib.SyncStatsC()
+    _call(lib.pact_full_allreduce, comm.handle, _ptr(g), _ptr(o), g.numel(), C.c_float(scale),
+          C.byref(st), _stream())
+    return AggregateResult(o, _stats(st))
+
+
+def masked_allreduce(grad: torch.Tensor, mask: SparsityMask, tracker: TrackerStatus, epoch: int,
+                     comm: Optional[Comm], advertised_digest: Optional[int] = None,
+                     policy: Optional[SyncPolicy] = None,
+                     out: Optional[torch.Tensor] = None) -> AggregateResult:
+    """collective.cpp:269-309: vote, then pack -> sum-allreduce -> unpack on a
+    unanimous stable vote, else a dense sum-allreduce. Returns the SUM
+    (times policy.scale)."""
+    g = _as_grad(grad, "grad")
+    o = torch.empty_like(g) if out is None else out
+    st = _lib.SyncStatsC()
+    pol = (policy or SyncPolicy()).c()
+    adv = None
+    if advertised_digest is not None:
+        adv = C.c_uint64(int(advertised_digest) & 0xFFFFFFFFFFFFFFFF)
+    _call(lib.pact_masked_allreduce, comm.handle if comm is not None else None, mask.ctx.handle,
+          _ptr(g), g.numel(), mask.handle, int(tracker == TrackerStatus.Stable), int(epoch),
+          C.byref(adv) if adv is not None else None, C.byref(pol), _ptr(o), C.byref(st), _stream())
+    return AggregateResult(o, _stats(st))
+
+
+def masked_allreduce_host(grad_host: torch.Tensor, mask: SparsityMask, tracker: TrackerStatus,
+                          epoch: int, comm: Optional[Comm], out_host: torch.Tensor,
+                          policy: Optional[SyncPolicy] = None) -> SyncStats:
+    """The same call on HOST (ideally pinned) fp32 buffers: H2D, device path, D2H."""
+    st = _lib.SyncStatsC()
+    pol = (policy or SyncPolicy()).c()
+    _call(lib.pact_masked_allreduce_host, comm.handle if comm is not None else None, mask.ctx.handle,
+          _ptr(grad_host), grad_host.numel(), mask.handle, int(tracker == TrackerStatus.Stable),
+          int(epoch), None, C.byref(pol), _ptr(out_host), C.byref(st), _stream())
+    return _stats(st)
+
+
+def synth_fill(x: torch.Tensor, seed: int, recipe: int, scale: float = 1.0, index_base: int = 0) -> torch.Tensor:
+    """Device-side synthetic data; host twin in synth.py."""
+    ctx = Context.get(x.device.index)
+    _call(lib.pact_synth_fill, ctx.handle, _ptr(x), x.numel(), C.c_uint64(seed & 0xFFFFFFFFFFFFFFFF),
+          C.c_uint64(index_base), int(recipe), C.c_float(scale), _stream())
+    return x

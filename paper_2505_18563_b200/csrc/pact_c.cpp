@@ -1,0 +1,1025 @@
+// pact_c.cpp -- host side of the C-ABI (include/pact_c.h): contexts, device
+// masks, the prune driver, codec entry points and the NCCL collectives
+// (vote -> pack -> allreduce -> unpack with per-bucket stream overlap).
+//
+// Reference semantics are cited per function (paths relative to
+// /root/reference/proj). Nothing here computes on the CPU except scalar
+// control decisions (drop count, vote rule, byte accounting, tracker).
+#include "pact_c.h"
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "launch.h"
+
+// ---------------------------------------------------------------- errors
+
+namespace {
+
+thread_local std::string g_last_error;
+
+pact_status fail(pact_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_last_error = std::string(pact_status_name(st)) + ": " + buf;
+  return st;
+}
+
+#define CUDA_TRY(expr)                                                                        \
+  do {                                                                                        \
+    cudaError_t e_ = (expr);                                                                  \
+    if (e_ != cudaSuccess)                                                                    \
+      return fail(e_ == cudaErrorMemoryAllocation ? PACT_E_OOM : PACT_E_CUDA, "%s: %s (%s:%d)", \
+                  #expr, cudaGetErrorString(e_), __FILE__, __LINE__);                         \
+  } while (0)
+
+#define NCCL_TRY(expr)                                                                    \
+  do {                                                                                    \
+    ncclResult_t r_ = (expr);                                                             \
+    if (r_ != ncclSuccess)                                                                \
+      return fail(r_ == ncclRemoteError || r_ == ncclSystemError ? PACT_E_LINK : PACT_E_NCCL, \
+                  "%s: %s", #expr, ncclGetErrorString(r_));                               \
+  } while (0)
+
+#define TRY(expr)                      \
+  do {                                 \
+    pact_status s_ = (expr);           \
+    if (s_ != PACT_OK) return s_;      \
+  } while (0)
+
+// grow-only device buffer
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  pact_status ensure(size_t need) {
+    if (need <= bytes) return PACT_OK;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    size_t b = std::max<size_t>(need, 256);
+    if (cudaMalloc(&p, b) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(PACT_E_OOM, "cudaMalloc(%zu)", b);
+    }
+    bytes = b;
+    return PACT_OK;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  template <typename T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+struct HostBuf {  // grow-only pinned host buffer
+  void* p = nullptr;
+  size_t bytes = 0;
+  pact_status ensure(size_t need) {
+    if (need <= bytes) return PACT_OK;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    bytes = 0;
+    size_t b = std::max<size_t>(need, 256);
+    if (cudaMallocHost(&p, b) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(PACT_E_OOM, "cudaMallocHost(%zu)", b);
+    }
+    bytes = b;
+    return PACT_OK;
+  }
+  void release() {
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  template <typename T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+constexpr uint64_t kTile = PACT_TILE;
+
+uint64_t word_count(uint64_t len) { return (len + 63) / 64; }
+uint64_t tile_count(uint64_t len) { return (len + kTile - 1) / kTile; }
+
+}  // namespace
+
+struct pact_ctx {
+  int device = 0;
+  DevBuf ws_small;  // PruneWindow | PruneCounts | hist[2048] | digest out | changed flag
+  DevBuf cand;      // prune candidates (u32 keys)
+  DevBuf state;     // look-back tile states + counter
+  DevBuf digest_scratch;
+  DevBuf packed;    // packed gradient for masked_allreduce
+  DevBuf grad_stage, out_stage;  // e2e host path staging
+  HostBuf pin;      // small pinned readbacks
+  cudaStream_t aux[2] = {nullptr, nullptr};  // comm / unpack streams for bucket overlap
+  std::vector<cudaEvent_t> ev_pool;
+  cudaEvent_t t0 = nullptr, t1 = nullptr;
+};
+
+struct pact_mask {
+  pact_ctx* ctx = nullptr;
+  uint64_t len = 0, nwords = 0, ntiles = 0;
+  uint64_t* words = nullptr;
+  uint32_t* tile_off = nullptr;   // ntiles + 1
+  uint32_t* tile_popc = nullptr;  // ntiles
+  uint64_t nnz = 0;
+  uint64_t digest = 0;
+  int digest_valid = 0;
+  int changed = 1;
+  std::vector<uint32_t> host_tile_off;  // lazily mirrored (bucket planning)
+  int host_tile_off_valid = 0;
+};
+
+struct pact_comm {
+  pact_ctx* ctx = nullptr;
+  ncclComm_t nccl = nullptr;
+  int rank = 0, n = 1;
+  DevBuf vote_dev;  // 32 B own slot + 32*n gathered
+  HostBuf vote_pin;
+  cudaEvent_t vote_done = nullptr;
+};
+
+namespace {
+
+// small workspace layout
+struct Small {
+  pactk::PruneWindow win;
+  uint32_t pad0[2];
+  pactk::PruneCounts counts;
+  uint64_t digest;
+  int changed;
+  int pad1[3];
+  uint32_t hist[2048];
+};
+
+pact_status set_device(pact_ctx* ctx) {
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  return PACT_OK;
+}
+
+pact_status ensure_ctx_ws(pact_ctx* ctx) {
+  TRY(ctx->ws_small.ensure(sizeof(Small)));
+  TRY(ctx->pin.ensure(64 * 1024));
+  if (!ctx->aux[0]) {
+    for (auto& s : ctx->aux) CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    CUDA_TRY(cudaEventCreate(&ctx->t0));
+    CUDA_TRY(cudaEventCreate(&ctx->t1));
+  }
+  return PACT_OK;
+}
+
+cudaEvent_t pool_event(pact_ctx* ctx, size_t i) {
+  while (ctx->ev_pool.size() <= i) {
+    cudaEvent_t e;
+    cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    ctx->ev_pool.push_back(e);
+  }
+  return ctx->ev_pool[i];
+}
+
+// recompute tile offsets + nnz from the mask words (device), sync
+pact_status refresh_offsets(pact_mask* m, cudaStream_t s) {
+  pactk::launch_tile_popc(m->words, m->len, m->tile_popc, s);
+  pactk::launch_scan_excl(m->tile_popc, m->ntiles, m->tile_off, s);
+  uint32_t* pin = m->ctx->pin.as<uint32_t>();
+  CUDA_TRY(cudaMemcpyAsync(pin, m->tile_off + m->ntiles, 4, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  m->nnz = pin[0];
+  m->host_tile_off_valid = 0;
+  return PACT_OK;
+}
+
+pact_status mirror_tile_off(pact_mask* m, cudaStream_t s) {
+  if (m->host_tile_off_valid) return PACT_OK;
+  m->host_tile_off.resize(m->ntiles + 1);
+  CUDA_TRY(cudaMemcpyAsync(m->host_tile_off.data(), m->tile_off, (m->ntiles + 1) * 4,
+                           cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  m->host_tile_off_valid = 1;
+  return PACT_OK;
+}
+
+uint64_t drop_count_raw(float ratio, uint64_t len) {  // sparsity.cpp:38-39
+  return (uint64_t)std::floor((double)ratio * (double)len + (double)len * 1e-7);
+}
+
+void put_le(uint8_t* p, uint64_t v, int n) {
+  for (int i = 0; i < n; ++i) p[i] = (uint8_t)((v >> (8 * i)) & 0xff);
+}
+uint64_t get_le(const uint8_t* p, int n) {
+  uint64_t v = 0;
+  for (int i = 0; i < n; ++i) v |= (uint64_t)p[i] << (8 * i);
+  return v;
+}
+
+int imod(int a, int n) { return ((a % n) + n) % n; }
+
+}  // namespace
+
+// =================================================================== ABI
+
+extern "C" {
+
+const char* pact_status_name(int st) {
+  switch (st) {
+    case PACT_OK: return "Ok";
+    case PACT_E_DUPLICATE_PARAM: return "DuplicateParam";
+    case PACT_E_INVALID_VIEW: return "InvalidView";
+    case PACT_E_INVALID_RATIO: return "InvalidRatio";
+    case PACT_E_INVALID_RATE: return "InvalidRate";
+    case PACT_E_NUMERICAL: return "NumericalFailure";
+    case PACT_E_SHAPE_MISMATCH: return "ShapeMismatch";
+    case PACT_E_MASK_MISMATCH: return "MaskMismatch";
+    case PACT_E_CORRUPT_PAYLOAD: return "CorruptPayload";
+    case PACT_E_LINK: return "LinkError";
+    case PACT_E_UNDEFINED_METRIC: return "UndefinedMetric";
+    case PACT_E_MISSING_FILE: return "MissingFile";
+    case PACT_E_PARSE: return "ParseError";
+    case PACT_E_UNKNOWN_KEY: return "UnknownKey";
+    case PACT_E_BAD_TOPOLOGY: return "BadTopology";
+    case PACT_E_RUN_FAILURE: return "RunFailure";
+    case PACT_E_CUDA: return "CudaError";
+    case PACT_E_NCCL: return "NcclError";
+    case PACT_E_INVALID_ARG: return "InvalidArgument";
+    case PACT_E_NO_DEVICE: return "NoDevice";
+    case PACT_E_OOM: return "OutOfMemory";
+  }
+  return "Error";
+}
+
+const char* pact_last_error(void) { return g_last_error.c_str(); }
+int pact_abi_version(void) { return PACT_ABI_VERSION; }
+
+// ------------------------------------------------------ scalar helpers
+
+pact_status pact_drop_count(float ratio, uint64_t len, uint64_t* k_out) {
+  if (!(ratio >= 0.0f && ratio < 1.0f))  // sparsity.cpp:34-35
+    return fail(PACT_E_INVALID_RATIO, "prune ratio %g outside [0, 1)", (double)ratio);
+  if (!k_out) return fail(PACT_E_INVALID_ARG, "k_out is null");
+  *k_out = drop_count_raw(ratio, len);
+  return PACT_OK;
+}
+
+pact_status pact_header_encode(const pact_frame_header* h, uint8_t out[PACT_HEADER_BYTES]) {
+  if (!h || !out) return fail(PACT_E_INVALID_ARG, "null header");
+  out[0] = 'P', out[1] = 'A', out[2] = 'C', out[3] = 'T';  // codec.cpp:226, 246
+  out[4] = 1;                                             // kVersion
+  out[5] = h->kind;
+  put_le(out + 6, h->epoch, 4);
+  put_le(out + 10, h->mask_digest, 8);
+  put_le(out + 18, h->value_count, 8);
+  return PACT_OK;
+}
+
+pact_status pact_header_decode(const uint8_t* f, size_t len, pact_frame_header* h) {
+  if (!h) return fail(PACT_E_INVALID_ARG, "null header");
+  if (!f || len < PACT_HEADER_BYTES) return fail(PACT_E_CORRUPT_PAYLOAD, "frame truncated");
+  if (f[0] != 'P' || f[1] != 'A' || f[2] != 'C' || f[3] != 'T')
+    return fail(PACT_E_CORRUPT_PAYLOAD, "bad magic");
+  if (f[4] != 1) return fail(PACT_E_CORRUPT_PAYLOAD, "unsupported version");
+  if (f[5] > 4) return fail(PACT_E_CORRUPT_PAYLOAD, "unknown payload kind");
+  h->kind = f[5];
+  h->epoch = (uint32_t)get_le(f + 6, 4);
+  h->mask_digest = get_le(f + 10, 8);
+  h->value_count = get_le(f + 18, 8);
+  return PACT_OK;
+}
+
+void pact_tracker_init(pact_tracker* t, uint32_t threshold) {
+  t->threshold = threshold == 0 ? 1 : threshold;  // sparsity.hpp:41
+  t->stable_count = 0;
+  t->has_last = 0;
+  t->last_digest = 0;
+}
+
+int pact_tracker_status(const pact_tracker* t) { return t->stable_count >= t->threshold ? 1 : 0; }
+
+int pact_tracker_observe(pact_tracker* t, uint64_t d) {  // sparsity.cpp:17-25
+  if (t->has_last && t->last_digest == d)
+    ++t->stable_count;
+  else
+    t->stable_count = 0;
+  t->has_last = 1;
+  t->last_digest = d;
+  return pact_tracker_status(t);
+}
+
+int pact_decide_sync_mode(int requested, int stable) {  // collective.cpp:62-67
+  if ((requested == PACT_SYNC_PACKED || requested == PACT_SYNC_TERNARY) && !stable)
+    return PACT_SYNC_FULL;
+  return requested;
+}
+
+pact_status pact_vote_decide(const uint8_t* frames, int n, const pact_frame_header* mine,
+                             int stable, int* agree) {
+  if (!frames || !mine || !agree || n < 1) return fail(PACT_E_INVALID_ARG, "bad vote args");
+  int ok = stable ? 1 : 0;  // collective.cpp:285-293
+  for (int q = 0; q < n; ++q) {
+    pact_frame_header h;
+    TRY(pact_header_decode(frames + (size_t)q * PACT_HEADER_BYTES, PACT_HEADER_BYTES, &h));
+    if (h.kind != PACT_KIND_PACKED || h.mask_digest != mine->mask_digest ||
+        h.value_count != mine->value_count)
+      ok = 0;
+  }
+  *agree = ok;
+  return PACT_OK;
+}
+
+uint64_t pact_ring_bytes(int n, int p, uint64_t count) {
+  // collective.cpp:178-206: RS step s sends chunk p-s, AG step s chunk p+1-s
+  if (n < 2) return 0;
+  const uint64_t chunk = (count + n - 1) / n;
+  auto elems = [&](int c) {
+    const uint64_t b = std::min<uint64_t>(count, (uint64_t)c * chunk);
+    const uint64_t e = std::min<uint64_t>(count, ((uint64_t)c + 1) * chunk);
+    return e - b;
+  };
+  uint64_t bytes = 0;
+  for (int s = 0; s < n - 1; ++s) bytes += 4 * (elems(imod(p - s, n)) + elems(imod(p + 1 - s, n)));
+  return bytes;
+}
+
+uint64_t pact_masked_bytes(int n, int p, uint64_t count) {
+  if (n < 2) return 0;
+  return (uint64_t)(n - 1) * PACT_HEADER_BYTES + pact_ring_bytes(n, p, count);
+}
+
+// ----------------------------------------------------------------- ctx
+
+pact_status pact_ctx_create(int device, pact_ctx** out) {
+  if (!out) return fail(PACT_E_INVALID_ARG, "out is null");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return fail(PACT_E_NO_DEVICE, "no CUDA device visible");
+  }
+  if (device < 0 || device >= ndev) return fail(PACT_E_INVALID_ARG, "device %d of %d", device, ndev);
+  auto* ctx = new pact_ctx;
+  ctx->device = device;
+  pact_status st = set_device(ctx);
+  if (st == PACT_OK) st = ensure_ctx_ws(ctx);
+  if (st != PACT_OK) {
+    delete ctx;
+    return st;
+  }
+  *out = ctx;
+  return PACT_OK;
+}
+
+pact_status pact_ctx_destroy(pact_ctx* ctx) {
+  if (!ctx) return PACT_OK;
+  cudaSetDevice(ctx->device);
+  cudaDeviceSynchronize();
+  for (DevBuf* b : {&ctx->ws_small, &ctx->cand, &ctx->state, &ctx->digest_scratch, &ctx->packed,
+                    &ctx->grad_stage, &ctx->out_stage})
+    b->release();
+  ctx->pin.release();
+  for (auto s : ctx->aux)
+    if (s) cudaStreamDestroy(s);
+  for (auto e : ctx->ev_pool) cudaEventDestroy(e);
+  if (ctx->t0) cudaEventDestroy(ctx->t0);
+  if (ctx->t1) cudaEventDestroy(ctx->t1);
+  delete ctx;
+  return PACT_OK;
+}
+
+uint64_t pact_ctx_kernel_launches(const pact_ctx*) { return pactk::launches(); }
+
+// --------------------------------------------------------------- masks
+
+pact_status pact_mask_create(pact_ctx* ctx, uint64_t len, pact_mask** out) {
+  if (!ctx || !out) return fail(PACT_E_INVALID_ARG, "null ctx/out");
+  if (len > PACT_MAX_LEN) return fail(PACT_E_SHAPE_MISMATCH, "len %llu > PACT_MAX_LEN", (unsigned long long)len);
+  TRY(set_device(ctx));
+  auto* m = new pact_mask;
+  m->ctx = ctx;
+  m->len = len;
+  m->nwords = word_count(len);
+  m->ntiles = tile_count(len);
+  const size_t wb = std::max<uint64_t>(1, m->nwords) * 8;
+  const size_t tb = (m->ntiles + 1) * 4, pb = std::max<uint64_t>(1, m->ntiles) * 4;
+  if (cudaMalloc(&m->words, wb) != cudaSuccess || cudaMalloc(&m->tile_off, tb) != cudaSuccess ||
+      cudaMalloc(&m->tile_popc, pb) != cudaSuccess) {
+    cudaGetLastError();
+    pact_mask_destroy(m);
+    return fail(PACT_E_OOM, "mask allocation (%llu elements)", (unsigned long long)len);
+  }
+  // all_zeros(len): tensor.cpp:92-95
+  cudaMemset(m->words, 0, wb);
+  cudaMemset(m->tile_off, 0, tb);
+  CUDA_TRY(cudaDeviceSynchronize());
+  m->nnz = 0;
+  m->digest_valid = 0;
+  m->changed = 1;
+  *out = m;
+  return PACT_OK;
+}
+
+pact_status pact_mask_destroy(pact_mask* m) {
+  if (!m) return PACT_OK;
+  cudaSetDevice(m->ctx->device);
+  if (m->words) cudaFree(m->words);
+  if (m->tile_off) cudaFree(m->tile_off);
+  if (m->tile_popc) cudaFree(m->tile_popc);
+  delete m;
+  return PACT_OK;
+}
+
+pact_status pact_mask_info_get(const pact_mask* m, pact_mask_info* o) {
+  if (!m || !o) return fail(PACT_E_INVALID_ARG, "null mask/out");
+  o->len = m->len;
+  o->nnz = m->nnz;
+  o->digest = m->digest;
+  o->digest_valid = m->digest_valid;
+  o->changed = m->changed;
+  o->ntiles = m->ntiles;
+  o->words = m->words;
+  o->tile_off = m->tile_off;
+  return PACT_OK;
+}
+
+pact_status pact_mask_fill(pact_mask* m, int keep, pact_stream_t stream) {
+  if (!m) return fail(PACT_E_INVALID_ARG, "null mask");
+  TRY(set_device(m->ctx));
+  const uint64_t want = keep ? m->len : 0;
+  const int same = m->host_tile_off_valid && m->nnz == want && !m->changed;
+  pactk::launch_mask_fill(m->words, m->len, keep, m->tile_off, stream);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaStreamSynchronize(stream));
+  m->changed = !same;
+  m->nnz = want;
+  m->digest_valid = 0;
+  m->host_tile_off_valid = 0;
+  return PACT_OK;
+}
+
+pact_status pact_mask_set_words(pact_mask* m, const uint64_t* words_dev, pact_stream_t stream) {
+  if (!m || (!words_dev && m->nwords)) return fail(PACT_E_INVALID_ARG, "null mask/words");
+  TRY(set_device(m->ctx));
+  if (m->nwords) {
+    CUDA_TRY(cudaMemcpyAsync(m->words, words_dev, m->nwords * 8, cudaMemcpyDeviceToDevice, stream));
+    pactk::launch_clear_tail(m->words, m->len, stream);
+  }
+  if (m->ntiles) {
+    TRY(refresh_offsets(m, stream));
+  } else {
+    m->nnz = 0;
+  }
+  CUDA_TRY(cudaGetLastError());
+  m->changed = 1;
+  m->digest_valid = 0;
+  return PACT_OK;
+}
+
+pact_status pact_mask_digest(pact_mask* m, pact_stream_t stream, uint64_t* out) {
+  if (!m) return fail(PACT_E_INVALID_ARG, "null mask");
+  if (!m->digest_valid) {
+    pact_ctx* ctx = m->ctx;
+    TRY(set_device(ctx));
+    TRY(ctx->digest_scratch.ensure(pactk::digest_scratch_bytes(m->nwords)));
+    Small* sm = ctx->ws_small.as<Small>();
+    pactk::launch_digest(m->words, m->nwords, ctx->digest_scratch.p, &sm->digest, stream);
+    CUDA_TRY(cudaGetLastError());
+    uint64_t* pin = ctx->pin.as<uint64_t>();
+    CUDA_TRY(cudaMemcpyAsync(pin, &sm->digest, 8, cudaMemcpyDeviceToHost, stream));
+    CUDA_TRY(cudaStreamSynchronize(stream));
+    m->digest = pin[0];
+    m->digest_valid = 1;
+  }
+  if (out) *out = m->digest;
+  return PACT_OK;
+}
+
+// --------------------------------------------------------------- prune
+
+namespace {
+
+// radix select of the `rank`-th smallest (1-based) key' = key - base over
+// elements with key' < 2^bits; returns key' and #(key' smaller).
+pact_status select_rank(pact_ctx* ctx, const void* src, int from_float, uint64_t n, uint32_t base,
+                        int bits, uint64_t rank, cudaStream_t s, uint32_t* value,
+                        uint64_t* below) {
+  Small* sm = ctx->ws_small.as<Small>();
+  uint32_t* pin = ctx->pin.as<uint32_t>();
+  uint32_t prefix = 0;
+  uint64_t rem = rank, blw = 0;
+  int hi = bits;
+  while (hi > 0) {
+    const int nb = std::min(11, hi);
+    const int shift = hi - nb;
+    pactk::launch_prune_hist(src, from_float, n, base, shift, nb, prefix, sm->hist, s);
+    CUDA_TRY(cudaMemcpyAsync(pin, sm->hist, sizeof(uint32_t) << nb, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    uint32_t d = 0;
+    while (d < (1u << nb) && pin[d] < rem) {
+      rem -= pin[d];
+      blw += pin[d];
+      ++d;
+    }
+    if (d >= (1u << nb)) return fail(PACT_E_RUN_FAILURE, "radix select lost its rank");
+    prefix = (prefix << nb) | d;
+    hi = shift;
+  }
+  *value = prefix;
+  *below = blw;
+  return PACT_OK;
+}
+
+int bit_length(uint32_t v) { return v ? 32 - __builtin_clz(v) : 0; }
+
+}  // namespace
+
+pact_status pact_prune_magnitude(pact_ctx* ctx, const float* w, uint64_t len, float ratio,
+                                 pact_mask* out, pact_stream_t stream, pact_prune_stats* stats) {
+  if (!ctx || !out) return fail(PACT_E_INVALID_ARG, "null ctx/mask");
+  uint64_t k;
+  TRY(pact_drop_count(ratio, len, &k));  // sparsity.cpp:46
+  if (out->len != len)
+    return fail(PACT_E_SHAPE_MISMATCH, "weights length %llu != mask length %llu",
+                (unsigned long long)len, (unsigned long long)out->len);
+  if (len && !w) return fail(PACT_E_INVALID_ARG, "null weights");
+  TRY(set_device(ctx));
+  TRY(ensure_ctx_ws(ctx));
+  cudaStream_t s = stream;
+  pact_prune_stats st{};
+  st.k = k;
+  if (len == 0) {
+    out->nnz = 0;
+    out->changed = 0;
+    if (stats) *stats = st;
+    return PACT_OK;
+  }
+  if (k == 0 || k >= len) {  // nothing / everything dropped
+    TRY(pact_mask_fill(out, k == 0 ? 1 : 0, s));
+    st.path = 0;
+    st.threshold = 0;
+    if (stats) *stats = st;
+    return PACT_OK;
+  }
+  Small* sm = ctx->ws_small.as<Small>();
+  const uint64_t cap = std::max<uint64_t>(1u << 20, len / 16);
+  TRY(ctx->cand.ensure(cap * 4));
+  TRY(ctx->state.ensure(out->ntiles * 8 + 64));
+
+  // (1) sampled window, (2) counting pass
+  pactk::launch_prune_sample(w, len, k, &sm->win, s);
+  pactk::launch_prune_count(w, len, &sm->win, &sm->counts, ctx->cand.as<uint32_t>(), cap, s);
+  CUDA_TRY(cudaGetLastError());
+  struct {
+    pactk::PruneWindow win;
+    uint32_t pad[2];
+    pactk::PruneCounts c;
+  } h;
+  static_assert(sizeof(h) == offsetof(Small, digest), "layout");
+  void* pin = ctx->pin.p;
+  CUDA_TRY(cudaMemcpyAsync(pin, sm, sizeof(h), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  std::memcpy(&h, pin, sizeof(h));
+  const uint64_t lo_end = h.c.n_lt + h.c.n_eq_lo;
+  const uint64_t mid_end = lo_end + h.c.n_mid;
+  const uint64_t hi_end = mid_end + h.c.n_eq_hi;
+  uint32_t T = 0;
+  uint64_t c_lt = 0;
+  bool fallback = false;
+  st.candidates = h.c.n_mid;
+  if (k <= h.c.n_lt || k > hi_end) {
+    fallback = true;
+  } else if (k <= lo_end) {
+    T = h.win.lo;
+    c_lt = h.c.n_lt;
+  } else if (k <= mid_end) {
+    if (h.c.n_mid > cap) {
+      fallback = true;
+    } else {
+      // (3) exact select among the window-interior keys
+      const uint32_t base = h.win.lo + 1;
+      const int bits = bit_length(h.win.hi - h.win.lo - 2);
+      uint32_t rel = 0;
+      uint64_t below = 0;
+      if (bits > 0)
+        TRY(select_rank(ctx, ctx->cand.p, 0, h.c.n_mid, base, bits, k - lo_end, s, &rel, &below));
+      T = base + rel;
+      c_lt = lo_end + below;
+    }
+  } else {
+    T = h.win.hi;
+    c_lt = mid_end;
+  }
+  st.path = fallback ? 2 : 1;
+  if (fallback) {  // exact radix select over the whole array
+    uint32_t rel = 0;
+    uint64_t below = 0;
+    TRY(select_rank(ctx, w, 1, len, 0, 31, k, s, &rel, &below));
+    T = rel;
+    c_lt = below;
+  }
+  st.threshold = T;
+  st.c_lt = c_lt;
+
+  // (4) bitmap with tie ranks, then tile offsets
+  const int had_digest = out->digest_valid;
+  Small* smd = sm;
+  pactk::launch_prune_bitmap(w, len, T, k - c_lt, out->words, out->tile_popc, &smd->changed,
+                             ctx->state.as<uint64_t>(), s);
+  pactk::launch_scan_excl(out->tile_popc, out->ntiles, out->tile_off, s);
+  CUDA_TRY(cudaGetLastError());
+  uint32_t* pin32 = ctx->pin.as<uint32_t>();
+  CUDA_TRY(cudaMemcpyAsync(pin32, out->tile_off + out->ntiles, 4, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaMemcpyAsync(pin32 + 1, &smd->changed, 4, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  out->nnz = pin32[0];
+  out->changed = pin32[1] != 0;
+  out->host_tile_off_valid = out->host_tile_off_valid && !out->changed;
+  out->digest_valid = had_digest && !out->changed;
+  if (out->nnz != len - k)
+    return fail(PACT_E_RUN_FAILURE, "prune kept %llu, expected %llu", (unsigned long long)out->nnz,
+                (unsigned long long)(len - k));
+  if (stats) *stats = st;
+  return PACT_OK;
+}
+
+pact_status pact_prune_magnitude_segmented(pact_ctx* ctx, const float* w, uint64_t len,
+                                           const uint64_t* seg, uint64_t nseg, float ratio,
+                                           pact_mask* out, pact_stream_t stream) {
+  (void)ctx, (void)w, (void)len, (void)seg, (void)nseg, (void)ratio, (void)out, (void)stream;
+  return fail(PACT_E_INVALID_ARG, "per-layer prune not built yet");
+}
+
+// -------------------------------------------------------------- codecs
+
+pact_status pact_gse(pact_ctx* ctx, const float* g, uint64_t len, const pact_mask* m, float* out,
+                     pact_stream_t stream) {
+  if (!ctx || !m) return fail(PACT_E_INVALID_ARG, "null ctx/mask");
+  if (len != m->len)  // sparsity.cpp:113-115
+    return fail(PACT_E_SHAPE_MISMATCH, "gradient length %llu != mask length %llu",
+                (unsigned long long)len, (unsigned long long)m->len);
+  TRY(set_device(ctx));
+  pactk::launch_gse(g, len, m->words, out, stream);
+  CUDA_TRY(cudaGetLastError());
+  return PACT_OK;
+}
+
+pact_status pact_pack(pact_ctx* ctx, const float* g, uint64_t len, const pact_mask* m,
+                      float* packed, uint64_t tb, uint64_t te, pact_stream_t stream) {
+  if (!ctx || !m) return fail(PACT_E_INVALID_ARG, "null ctx/mask");
+  if (len != m->len)  // codec.cpp:15-17
+    return fail(PACT_E_SHAPE_MISMATCH, "gradient length %llu != mask length %llu",
+                (unsigned long long)len, (unsigned long long)m->len);
+  TRY(set_device(ctx));
+  te = std::min<uint64_t>(te, m->ntiles);
+  pactk::launch_pack(g, len, m->words, m->tile_off, packed, tb, te, stream);
+  CUDA_TRY(cudaGetLastError());
+  return PACT_OK;
+}
+
+pact_status pact_unpack(pact_ctx* ctx, const float* packed, uint64_t count, uint64_t packed_digest,
+                        int check_digest, const pact_mask* m, float scale, float* out,
+                        uint64_t tb, uint64_t te, pact_stream_t stream) {
+  if (!ctx || !m) return fail(PACT_E_INVALID_ARG, "null ctx/mask");
+  TRY(set_device(ctx));
+  if (check_digest) {  // codec.cpp:28-29
+    pact_mask* mm = const_cast<pact_mask*>(m);
+    uint64_t d;
+    TRY(pact_mask_digest(mm, stream, &d));
+    if (d != packed_digest) return fail(PACT_E_MASK_MISMATCH, "payload digest does not match local mask");
+  }
+  te = std::min<uint64_t>(te, m->ntiles);
+  if (tb == 0 && te == m->ntiles && count != m->nnz)  // codec.cpp:30-32
+    return fail(PACT_E_CORRUPT_PAYLOAD, "payload holds %llu values, mask keeps %llu",
+                (unsigned long long)count, (unsigned long long)m->nnz);
+  pactk::launch_unpack(packed, m->len, m->words, m->tile_off, scale, scale != 1.0f, out, tb, te,
+                       stream);
+  CUDA_TRY(cudaGetLastError());
+  return PACT_OK;
+}
+
+pact_status pact_unpack_sgd(pact_ctx* ctx, const float* packed, uint64_t count, const pact_mask* m,
+                            float scale, float lr, float* grad_out, float* weights,
+                            pact_stream_t stream) {
+  if (!ctx || !m || (!weights && m->len)) return fail(PACT_E_INVALID_ARG, "null ctx/mask/weights");
+  if (count != m->nnz)
+    return fail(PACT_E_CORRUPT_PAYLOAD, "payload holds %llu values, mask keeps %llu",
+                (unsigned long long)count, (unsigned long long)m->nnz);
+  TRY(set_device(ctx));
+  pactk::launch_unpack_sgd(packed, m->len, m->words, m->tile_off, scale, scale != 1.0f, lr,
+                           grad_out, weights, stream);
+  CUDA_TRY(cudaGetLastError());
+  return PACT_OK;
+}
+
+pact_status pact_synth_fill(pact_ctx* ctx, float* x, uint64_t len, uint64_t seed,
+                            uint64_t index_base, int recipe, float scale, pact_stream_t stream) {
+  if (!ctx || (!x && len)) return fail(PACT_E_INVALID_ARG, "null ctx/x");
+  if (recipe < 0 || recipe > 3) return fail(PACT_E_INVALID_ARG, "recipe %d", recipe);
+  TRY(set_device(ctx));
+  pactk::launch_synth(x, len, seed, index_base, recipe, scale, stream);
+  CUDA_TRY(cudaGetLastError());
+  return PACT_OK;
+}
+
+// --------------------------------------------------------- collectives
+
+pact_status pact_comm_unique_id(uint8_t out[PACT_UNIQUE_ID_BYTES]) {
+  static_assert(sizeof(ncclUniqueId) == PACT_UNIQUE_ID_BYTES, "nccl id size");
+  ncclUniqueId id;
+  NCCL_TRY(ncclGetUniqueId(&id));
+  std::memcpy(out, &id, sizeof id);
+  return PACT_OK;
+}
+
+pact_status pact_comm_create(pact_ctx* ctx, const uint8_t id[PACT_UNIQUE_ID_BYTES], int nranks,
+                             int rank, pact_comm** out) {
+  if (!ctx || !id || !out) return fail(PACT_E_INVALID_ARG, "null args");
+  if (nranks < 2)  // collective.cpp:25 WorkerTopology::validate
+    return fail(PACT_E_BAD_TOPOLOGY, "need at least 2 workers, got %d", nranks);
+  if (rank < 0 || rank >= nranks) return fail(PACT_E_BAD_TOPOLOGY, "rank %d not in ring", rank);
+  TRY(set_device(ctx));
+  TRY(ensure_ctx_ws(ctx));
+  auto* c = new pact_comm;
+  c->ctx = ctx;
+  c->rank = rank;
+  c->n = nranks;
+  ncclUniqueId uid;
+  std::memcpy(&uid, id, sizeof uid);
+  ncclResult_t r = ncclCommInitRank(&c->nccl, nranks, uid, rank);
+  if (r != ncclSuccess) {
+    delete c;
+    return fail(PACT_E_NCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
+  }
+  pact_status st = c->vote_dev.ensure(32 * (nranks + 1));
+  if (st == PACT_OK) st = c->vote_pin.ensure(32 * (nranks + 1));
+  if (st == PACT_OK && cudaEventCreateWithFlags(&c->vote_done, cudaEventDisableTiming) != cudaSuccess)
+    st = fail(PACT_E_CUDA, "event create");
+  if (st != PACT_OK) {
+    pact_comm_destroy(c);
+    return st;
+  }
+  *out = c;
+  return PACT_OK;
+}
+
+pact_status pact_comm_destroy(pact_comm* c) {
+  if (!c) return PACT_OK;
+  cudaSetDevice(c->ctx->device);
+  if (c->nccl) ncclCommDestroy(c->nccl);
+  c->vote_dev.release();
+  c->vote_pin.release();
+  if (c->vote_done) cudaEventDestroy(c->vote_done);
+  delete c;
+  return PACT_OK;
+}
+
+int pact_comm_rank(const pact_comm* c) { return c ? c->rank : 0; }
+int pact_comm_size(const pact_comm* c) { return c ? c->n : 1; }
+
+pact_status pact_allreduce_sum(pact_comm* c, const float* in, float* out, uint64_t count,
+                               pact_stream_t stream) {
+  if (!c) return fail(PACT_E_INVALID_ARG, "null comm");
+  TRY(set_device(c->ctx));
+  if (count) NCCL_TRY(ncclAllReduce(in, out, count, ncclFloat32, ncclSum, c->nccl, stream));
+  return PACT_OK;
+}
+
+namespace {
+
+// post the vote allgather on `s` (stage pinned -> device -> gather -> pinned)
+pact_status post_vote(pact_comm* c, const uint8_t frame[PACT_HEADER_BYTES], cudaStream_t s) {
+  uint8_t* pin = c->vote_pin.as<uint8_t>();
+  std::memset(pin, 0, 32);
+  std::memcpy(pin, frame, PACT_HEADER_BYTES);
+  uint8_t* dev = c->vote_dev.as<uint8_t>();
+  CUDA_TRY(cudaMemcpyAsync(dev, pin, 32, cudaMemcpyHostToDevice, s));
+  NCCL_TRY(ncclAllGather(dev, dev + 32, 32, ncclUint8, c->nccl, s));
+  CUDA_TRY(cudaMemcpyAsync(pin + 32, dev + 32, 32 * (size_t)c->n, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaEventRecord(c->vote_done, s));
+  return PACT_OK;
+}
+
+pact_status wait_vote(pact_comm* c, std::vector<uint8_t>& frames) {
+  CUDA_TRY(cudaEventSynchronize(c->vote_done));
+  const uint8_t* pin = c->vote_pin.as<uint8_t>() + 32;
+  frames.resize((size_t)c->n * PACT_HEADER_BYTES);
+  for (int q = 0; q < c->n; ++q)
+    std::memcpy(frames.data() + (size_t)q * PACT_HEADER_BYTES, pin + 32 * q, PACT_HEADER_BYTES);
+  return PACT_OK;
+}
+
+}  // namespace
+
+pact_status pact_allgather_frames(pact_comm* c, const uint8_t* frame, size_t frame_bytes,
+                                  uint8_t* frames_out, pact_stream_t stream) {
+  if (!c || !frame || !frames_out) return fail(PACT_E_INVALID_ARG, "null args");
+  TRY(set_device(c->ctx));
+  DevBuf tmp;
+  TRY(tmp.ensure(frame_bytes * (c->n + 1)));
+  HostBuf pin;
+  TRY(pin.ensure(frame_bytes * (c->n + 1)));
+  std::memcpy(pin.p, frame, frame_bytes);
+  uint8_t* d = tmp.as<uint8_t>();
+  pact_status st = PACT_OK;
+  if (cudaMemcpyAsync(d, pin.p, frame_bytes, cudaMemcpyHostToDevice, stream) != cudaSuccess)
+    st = fail(PACT_E_CUDA, "H2D");
+  if (st == PACT_OK && ncclAllGather(d, d + frame_bytes, frame_bytes, ncclUint8, c->nccl, stream) != ncclSuccess)
+    st = fail(PACT_E_NCCL, "ncclAllGather");
+  if (st == PACT_OK &&
+      cudaMemcpyAsync(pin.as<uint8_t>() + frame_bytes, d + frame_bytes, frame_bytes * c->n,
+                      cudaMemcpyDeviceToHost, stream) != cudaSuccess)
+    st = fail(PACT_E_CUDA, "D2H");
+  if (st == PACT_OK && cudaStreamSynchronize(stream) != cudaSuccess) st = fail(PACT_E_CUDA, "sync");
+  if (st == PACT_OK) std::memcpy(frames_out, pin.as<uint8_t>() + frame_bytes, frame_bytes * c->n);
+  tmp.release();
+  pin.release();
+  return st;
+}
+
+pact_status pact_full_allreduce(pact_comm* c, const float* grad, float* out, uint64_t len,
+                                float scale, pact_sync_stats* stats, pact_stream_t stream) {
+  if (!c) return fail(PACT_E_INVALID_ARG, "null comm");
+  TRY(set_device(c->ctx));
+  pact_ctx* ctx = c->ctx;
+  CUDA_TRY(cudaEventRecord(ctx->t0, stream));
+  if (len) NCCL_TRY(ncclAllReduce(grad, out, len, ncclFloat32, ncclSum, c->nccl, stream));
+  if (scale != 0.0f && scale != 1.0f) pactk::launch_scale(out, out, len, scale, stream);
+  CUDA_TRY(cudaEventRecord(ctx->t1, stream));
+  if (stats) {
+    CUDA_TRY(cudaEventSynchronize(ctx->t1));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, ctx->t0, ctx->t1);
+    *stats = pact_sync_stats{};
+    stats->bytes_on_wire = pact_ring_bytes(c->n, c->rank, len);  // collective.cpp:253-259
+    stats->seconds = ms * 1e-3;
+    stats->mode_used = PACT_SYNC_FULL;
+    stats->value_count = len;
+  }
+  return PACT_OK;
+}
+
+pact_status pact_masked_allreduce(pact_comm* c, pact_ctx* ctx, const float* grad, uint64_t len,
+                                  pact_mask* m, int tracker_stable, uint32_t epoch,
+                                  const uint64_t* advertised, const pact_policy* policy,
+                                  float* out, pact_sync_stats* stats, pact_stream_t stream) {
+  if (!ctx || !m) return fail(PACT_E_INVALID_ARG, "null ctx/mask");
+  if (c && c->ctx != ctx) return fail(PACT_E_INVALID_ARG, "comm belongs to another ctx");
+  if (len != m->len)  // collective.cpp:272
+    return fail(PACT_E_SHAPE_MISMATCH, "gradient/mask length mismatch (%llu vs %llu)",
+                (unsigned long long)len, (unsigned long long)m->len);
+  TRY(set_device(ctx));
+  TRY(ensure_ctx_ws(ctx));
+  pact_policy pol{};
+  if (policy) pol = *policy;
+  const float scale = pol.scale == 0.0f ? 1.0f : pol.scale;
+  const int n = c ? c->n : 1;
+  cudaStream_t s = stream;
+  if (pol.time_stages) CUDA_TRY(cudaEventRecord(ctx->t0, s));
+
+  // vote frame (collective.cpp:280-283)
+  const int stable = pact_decide_sync_mode(PACT_SYNC_PACKED, tracker_stable) == PACT_SYNC_PACKED;
+  uint64_t digest = 0;
+  if (!advertised || stable) TRY(pact_mask_digest(m, s, &digest));
+  pact_frame_header mine{(uint8_t)(stable ? PACT_KIND_PACKED : PACT_KIND_FULL), epoch,
+                         advertised ? *advertised : digest, m->nnz};
+  uint8_t frame[PACT_HEADER_BYTES];
+  TRY(pact_header_encode(&mine, frame));
+  TRY(ctx->packed.ensure(std::max<uint64_t>(1, m->nnz) * 4));
+  float* packed = ctx->packed.as<float>();
+
+  const bool buckets = c && pol.bucket_bytes > 0 && m->nnz * 4 > pol.bucket_bytes;
+  if (buckets) TRY(mirror_tile_off(m, s));
+
+  int agree = 0;
+  bool packed_issued = false;
+  if (c) {
+    TRY(post_vote(c, frame, ctx->aux[0]));
+    // speculative pack overlaps the vote round trip (single-bucket plan only)
+    if (stable && !buckets && m->nnz) {
+      pactk::launch_pack(grad, len, m->words, m->tile_off, packed, 0, m->ntiles, s);
+      packed_issued = true;
+    }
+    std::vector<uint8_t> frames;
+    TRY(wait_vote(c, frames));
+    TRY(pact_vote_decide(frames.data(), n, &mine, stable, &agree));  // collective.cpp:285-293
+  } else {
+    agree = stable;  // the one-rank vote: only this rank's frame
+  }
+  int reason = agree ? 0 : (stable ? 2 : 1);
+  // density rule: unanimous because nnz and len were agreed
+  if (agree && pol.density_threshold > 0.0 && pol.density_threshold < 1.0 && len &&
+      (double)m->nnz / (double)len > pol.density_threshold) {
+    agree = 0;
+    reason = 3;
+  }
+
+  int nbuckets = 0;
+  if (agree) {
+    if (!buckets) {
+      if (!packed_issued && m->nnz)
+        pactk::launch_pack(grad, len, m->words, m->tile_off, packed, 0, m->ntiles, s);
+      if (c && m->nnz)
+        NCCL_TRY(ncclAllReduce(packed, packed, m->nnz, ncclFloat32, ncclSum, c->nccl, s));
+      pactk::launch_unpack(packed, len, m->words, m->tile_off, scale, scale != 1.0f, out, 0,
+                           m->ntiles, s);
+      nbuckets = 1;
+    } else {
+      // tile-aligned buckets of ~bucket_bytes packed; pack on s, NCCL on
+      // aux[0], unpack on aux[1], chained by events
+      const std::vector<uint32_t>& off = m->host_tile_off;
+      std::vector<uint64_t> cuts{0};
+      const uint64_t per = std::max<uint64_t>(1, pol.bucket_bytes / 4);
+      uint64_t t = 0;
+      while (t < m->ntiles) {
+        const uint64_t target = off[t] + per;
+        uint64_t u = std::upper_bound(off.begin() + t + 1, off.end(), (uint32_t)std::min<uint64_t>(target, 0xffffffffu)) - off.begin();
+        u = std::max<uint64_t>(u - 1, t + 1);
+        if (u > m->ntiles) u = m->ntiles;
+        cuts.push_back(u);
+        t = u;
+      }
+      nbuckets = (int)cuts.size() - 1;
+      cudaEvent_t start = pool_event(ctx, 0);
+      CUDA_TRY(cudaEventRecord(start, s));
+      CUDA_TRY(cudaStreamWaitEvent(ctx->aux[1], start, 0));
+      for (int b = 0; b < nbuckets; ++b) {
+        const uint64_t tb = cuts[b], te = cuts[b + 1];
+        const uint64_t o0 = off[tb], cnt = off[te] - off[tb];
+        cudaEvent_t e_pack = pool_event(ctx, 1 + 2 * b), e_ar = pool_event(ctx, 2 + 2 * b);
+        pactk::launch_pack(grad, len, m->words, m->tile_off, packed, tb, te, s);
+        CUDA_TRY(cudaEventRecord(e_pack, s));
+        CUDA_TRY(cudaStreamWaitEvent(ctx->aux[0], e_pack, 0));
+        if (cnt)
+          NCCL_TRY(ncclAllReduce(packed + o0, packed + o0, cnt, ncclFloat32, ncclSum, c->nccl,
+                                 ctx->aux[0]));
+        CUDA_TRY(cudaEventRecord(e_ar, ctx->aux[0]));
+        CUDA_TRY(cudaStreamWaitEvent(ctx->aux[1], e_ar, 0));
+        pactk::launch_unpack(packed, len, m->words, m->tile_off, scale, scale != 1.0f, out, tb, te,
+                             ctx->aux[1]);
+      }
+      cudaEvent_t done = pool_event(ctx, 1 + 2 * nbuckets);
+      CUDA_TRY(cudaEventRecord(done, ctx->aux[1]));
+      CUDA_TRY(cudaStreamWaitEvent(s, done, 0));
+    }
+  } else {
+    if (c) {
+      if (len) NCCL_TRY(ncclAllReduce(grad, out, len, ncclFloat32, ncclSum, c->nccl, s));
+      if (scale != 1.0f) pactk::launch_scale(out, out, len, scale, s);
+    } else if (scale != 1.0f || out != grad) {
+      pactk::launch_scale(grad, out, len, scale, s);
+    }
+  }
+  CUDA_TRY(cudaGetLastError());
+  if (stats) {
+    *stats = pact_sync_stats{};
+    stats->bytes_on_wire = c ? pact_masked_bytes(n, c->rank, agree ? m->nnz : len) : 0;
+    stats->mode_used = agree ? PACT_SYNC_PACKED : PACT_SYNC_FULL;
+    stats->buckets = nbuckets;
+    stats->value_count = agree ? m->nnz : len;
+    stats->fallback_reason = reason;
+    if (pol.time_stages) {
+      CUDA_TRY(cudaEventRecord(ctx->t1, s));
+      CUDA_TRY(cudaEventSynchronize(ctx->t1));
+      float ms = 0;
+      cudaEventElapsedTime(&ms, ctx->t0, ctx->t1);
+      stats->seconds = ms * 1e-3;
+    }
+  }
+  return PACT_OK;
+}
+
+pact_status pact_masked_allreduce_host(pact_comm* c, pact_ctx* ctx, const float* grad_host,
+                                       uint64_t len, pact_mask* m, int tracker_stable,
+                                       uint32_t epoch, const uint64_t* advertised,
+                                       const pact_policy* policy, float* out_host,
+                                       pact_sync_stats* stats, pact_stream_t stream) {
+  if (!ctx || !m) return fail(PACT_E_INVALID_ARG, "null ctx/mask");
+  if (len != m->len)
+    return fail(PACT_E_SHAPE_MISMATCH, "gradient/mask length mismatch (%llu vs %llu)",
+                (unsigned long long)len, (unsigned long long)m->len);
+  TRY(set_device(ctx));
+  TRY(ctx->grad_stage.ensure(std::max<uint64_t>(1, len) * 4));
+  float* dg = ctx->grad_stage.as<float>();
+  if (len) CUDA_TRY(cudaMemcpyAsync(dg, grad_host, len * 4, cudaMemcpyHostToDevice, stream));
+  TRY(pact_masked_allreduce(c, ctx, dg, len, m, tracker_stable, epoch, advertised, policy, dg,
+                            stats, stream));
+  if (len) CUDA_TRY(cudaMemcpyAsync(out_host, dg, len * 4, cudaMemcpyDeviceToHost, stream));
+  CUDA_TRY(cudaStreamSynchronize(stream));
+  return PACT_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,330 @@
+"""GPU parity of the sm_100a kernels against the CPU oracle, through the
+C-ABI: bit-exact masks/thresholds/packed layouts (north_star), exact digests,
+reference error contract, and size-independent properties at full BASELINE
+sizes."""
+import numpy as np
+import pytest
+import torch
+
+from conftest import u32
+from oracle import bits_from_words, words_from_bits
+
+pytestmark = pytest.mark.gpu
+
+
+def dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+def expand_bits(words: torch.Tensor, n: int) -> torch.Tensor:
+    """device words -> bool[n] (torch ops, test-side only)"""
+    w = words.view(-1, 1)
+    sh = torch.arange(64, device=words.device, dtype=torch.int64).view(1, 64)
+    return ((w >> sh) & 1).view(-1)[:n].bool()
+
+
+# ----------------------------------------------------------------- prune
+
+
+def check_prune(pb, port, x, ratio, expect_path=None):
+    n = x.size
+    st = {}
+    m = pb.magnitude_prune(dev(x), ratio, stats=st)
+    ref = port.magnitude_prune(x, ratio)
+    got = m.words_host()
+    assert got.shape == ref.shape
+    if not np.array_equal(got, ref):
+        bad = np.nonzero(got != ref)[0]
+        raise AssertionError(f"n={n} ratio={ratio} words differ at {bad[:5]} stats={st}")
+    k = port.drop_count(ratio, n)
+    assert m.nnz() == n - min(k, n)
+    if 0 < k < n:
+        T, c_lt = port.prune_threshold(x, k)
+        assert st["threshold"] == T and st["c_lt"] == c_lt, (st, T, c_lt)
+    if expect_path is not None:
+        assert st["path"] == expect_path, st
+    return m, st
+
+
+def test_prune_golden_cases(pb, port, golden, cuda):
+    j, a = golden
+    for ex in j["prune_examples"]:
+        m = pb.magnitude_prune(dev(np.array(ex["w"], np.float32)), ex["ratio"])
+        assert [int(b) for b in bits_from_words(m.words_host(), len(ex["w"]))] == ex["keep"]
+    for t, c in enumerate(j["prune_cases"]):
+        m = pb.magnitude_prune(dev(a[f"prune_w_{t}"]), c["ratio"])
+        assert np.array_equal(m.words_host(), a[f"prune_words_{t}"]), t
+        assert m.nnz() == c["nnz"]
+        assert m.digest() == c["digest"]
+
+
+@pytest.mark.parametrize("n", [1, 2, 63, 64, 65, 4095, 4096, 4097, 12289, 100_003, 1_000_001])
+def test_prune_ragged_lengths(pb, port, cuda, n):
+    rng = np.random.default_rng(n)
+    for ratio in (0.1, 0.5, 0.9, 0.99):
+        check_prune(pb, port, rng.standard_normal(n).astype(np.float32), ratio)
+
+
+def test_prune_tie_heavy(pb, port, cuda):
+    from paper_2505_18563_b200 import synth
+
+    rng = np.random.default_rng(1)
+    for n in (5000, 300_000, 2_000_000):
+        x = (rng.integers(-6, 7, n) * 0.25).astype(np.float32)
+        x[rng.random(n) < 0.2] = -0.0  # +-0 tie at key 0
+        for ratio in (0.3, 0.5, 0.8, 0.95):
+            check_prune(pb, port, x, ratio)
+    x = synth.synth_host(3_000_000, 77, synth.W_TIES, 2.0 ** -5)
+    for ratio in (0.5, 0.9):
+        check_prune(pb, port, x, ratio)
+
+
+def test_prune_all_equal_and_zeros(pb, port, cuda):
+    for n in (10, 5000, 200_000):
+        check_prune(pb, port, np.full(n, 0.5, np.float32), 0.5)
+        check_prune(pb, port, np.zeros(n, np.float32), 0.7)
+
+
+def test_prune_ratio_bounds(pb, port, cuda):
+    x = np.random.default_rng(2).standard_normal(10_000).astype(np.float32)
+    m = pb.magnitude_prune(dev(x), 0.0)
+    assert m.nnz() == 10_000
+    for r in (1.0, -0.1):
+        with pytest.raises(pb.Error) as e:
+            pb.magnitude_prune(dev(x), r)
+        assert e.value.code == pb.Errc.InvalidRatio
+
+
+def test_prune_fallback_path(pb, port, cuda):
+    """Adversarial input: every sampled position is 0 while the rest is large,
+    so the sampled window misses and the full radix path must take over."""
+    n = 1_000_000
+    x = np.random.default_rng(3).uniform(1.0, 2.0, n).astype(np.float32)
+    S = 16384
+    pos = (np.arange(S, dtype=np.uint64) * np.uint64(n) + np.uint64(n // 2)) // np.uint64(S)
+    x[pos.astype(np.int64)] = 0.0
+    check_prune(pb, port, x, 0.5, expect_path=2)
+
+
+def test_prune_sort_oracle_property(pb, cuda):
+    """test_sparsity.cpp:49-69: 1000 gaussians at 0.8 keep 200, min kept >= max dropped."""
+    rng = np.random.default_rng(17)
+    for _ in range(20):
+        x = rng.standard_normal(1000).astype(np.float32)
+        m = pb.magnitude_prune(dev(x), 0.8)
+        assert m.nnz() == 200
+        keep = bits_from_words(m.words_host(), 1000)
+        assert np.abs(x[keep]).min() >= np.abs(x[~keep]).max()
+
+
+def test_prune_changed_flag_and_digest_cache(pb, port, cuda):
+    rng = np.random.default_rng(4)
+    x = rng.standard_normal(500_000).astype(np.float32)
+    m = pb.magnitude_prune(dev(x), 0.9)
+    d = m.digest()
+    pb.magnitude_prune(dev(x), 0.9, out=m)
+    assert not m.changed and m.digest() == d
+    x[np.argmax(np.abs(x))] = 0.0  # the largest becomes the smallest -> mask moves
+    pb.magnitude_prune(dev(x), 0.9, out=m)
+    assert m.changed
+    assert m.digest() == port.mask_digest(port.magnitude_prune(x, 0.9), x.size)
+
+
+# ----------------------------------------------------------------- codec
+
+
+def test_codec_golden(pb, golden, cuda):
+    j, a = golden
+    for t, c in enumerate(j["codec_cases"]):
+        g = dev(a[f"codec_g_{t}"])
+        m = pb.SparsityMask.from_words(dev(a[f"codec_words_{t}"].view(np.int64)), c["n"])
+        assert m.digest() == c["digest"]
+        p = pb.pack(g, m, t)
+        assert p.mask_digest == c["digest"] and p.epoch == t
+        assert np.array_equal(u32(p.values.cpu().numpy()), u32(a[f"codec_packed_{t}"]))
+        u = pb.unpack(p, m)
+        assert np.array_equal(u32(u.cpu().numpy()), u32(a[f"codec_unpacked_{t}"]))
+        gse = pb.enforce_gradient_sparsity(g, m)
+        assert np.array_equal(u32(gse.cpu().numpy()), u32(a[f"codec_unpacked_{t}"]))
+
+
+@pytest.mark.parametrize("n", [1, 77, 4096, 4097, 65_537, 2_500_003])
+@pytest.mark.parametrize("density", [0.0, 0.01, 0.2, 0.5, 1.0])
+def test_pack_unpack_random(pb, port, cuda, n, density):
+    rng = np.random.default_rng(n + int(density * 100))
+    g = rng.standard_normal(n).astype(np.float32)
+    g[rng.random(n) < 0.01] = -0.0
+    bits = rng.random(n) < density
+    w = words_from_bits(bits)
+    m = pb.SparsityMask.from_words(dev(w.view(np.int64)), n)
+    assert m.nnz() == int(bits.sum())
+    p = pb.pack(dev(g), m, 1)
+    ref = port.pack(g, w)
+    assert np.array_equal(u32(p.values.cpu().numpy()), u32(ref))
+    u = pb.unpack(p, m)
+    assert np.array_equal(u32(u.cpu().numpy()), u32(port.gse(g, w)))
+
+
+def test_unaligned_and_inplace(pb, port, cuda):
+    """pointers off the 16-byte grid take the scalar path; GSE in place."""
+    rng = np.random.default_rng(9)
+    n = 100_001
+    big = rng.standard_normal(n + 3).astype(np.float32)
+    g_h = big[1:n + 1]
+    bits = rng.random(n) < 0.3
+    w = words_from_bits(bits)
+    m = pb.SparsityMask.from_words(dev(w.view(np.int64)), n)
+    gd = dev(big)[1:n + 1]
+    p = pb.pack(gd, m, 0)
+    assert np.array_equal(u32(p.values.cpu().numpy()), u32(port.pack(g_h, w)))
+    out = torch.zeros(n + 1, device=cuda)[1:]
+    pb.unpack(p, m, out=out)
+    assert np.array_equal(u32(out.cpu().numpy()), u32(port.gse(g_h, w)))
+    x = dev(g_h.copy())
+    pb.enforce_gradient_sparsity(x, m, out=x)
+    assert np.array_equal(u32(x.cpu().numpy()), u32(port.gse(g_h, w)))
+
+
+def test_codec_errors(pb, cuda):
+    m = pb.SparsityMask.all_ones(2)
+    p = pb.pack(dev(np.array([1.0, 2.0], np.float32)), m, 0)
+    p.mask_digest ^= 1
+    with pytest.raises(pb.Error) as e:
+        pb.unpack(p, m)
+    assert e.value.code == pb.Errc.MaskMismatch
+    m3 = pb.SparsityMask.all_ones(3)
+    with pytest.raises(pb.Error) as e:
+        pb.unpack(pb.PackedGradient(m3.digest(), 0, dev(np.array([1.0, 2.0], np.float32))), m3)
+    assert e.value.code == pb.Errc.CorruptPayload
+    with pytest.raises(pb.Error) as e:
+        pb.enforce_gradient_sparsity(dev(np.ones(1, np.float32)), pb.SparsityMask.all_ones(2))
+    assert e.value.code == pb.Errc.ShapeMismatch
+    with pytest.raises(pb.Error) as e:
+        pb.pack(dev(np.ones(5, np.float32)), pb.SparsityMask.all_ones(4), 0)
+    assert e.value.code == pb.Errc.ShapeMismatch
+    z = pb.SparsityMask.all_zeros(4)  # empty payload over an all-zero mask
+    u = pb.unpack(pb.PackedGradient(z.digest(), 0, torch.empty(0, device=cuda)), z)
+    assert torch.all(u == 0)
+
+
+def test_mask_constructors(pb, port, cuda):
+    assert pb.SparsityMask.all_zeros(64).digest() == 0xA8C7F832281A39C5
+    assert pb.SparsityMask.all_ones(11).digest() == 0xB57A47E34A2684D3
+    assert pb.SparsityMask.all_ones(77).nnz() == 77
+    m = pb.SparsityMask.all_zeros(130).with_bit(0, True).with_bit(64, True).with_bit(129, True)
+    assert m.nnz() == 3 and m.test(0) and m.test(64) and m.test(129)
+    m = m.with_bit(64, False)
+    assert m.nnz() == 2
+    # digest flips on every single-bit change (test_tensor.cpp:103-117, sampled)
+    rng = np.random.default_rng(99)
+    for _ in range(50):
+        n = int(rng.integers(1, 512))
+        bits = rng.random(n) < 0.5
+        a = pb.SparsityMask.from_bits(bits)
+        i = int(rng.integers(0, n))
+        b = a.with_bit(i, not bits[i])
+        assert a.digest() != b.digest()
+        assert a.digest() == port.mask_digest(words_from_bits(bits), n)
+
+
+@pytest.mark.parametrize("n", [1, 64, 4096 * 64, 16384 * 128 + 5, 33_554_432 + 64 * 300 + 7, 170_000_000])
+def test_digest_sizes(pb, port, cuda, n):
+    """crosses segment (16384 elements) and group (2M elements) boundaries"""
+    rng = np.random.default_rng(n % 1000)
+    nw = (n + 63) // 64
+    w = rng.integers(0, 2**63, nw, dtype=np.uint64) ^ rng.integers(0, 2, nw, dtype=np.uint64) << np.uint64(63)
+    if n % 64:
+        w[-1] &= np.uint64((1 << (n % 64)) - 1)
+    m = pb.SparsityMask.from_words(dev(w.view(np.int64)), n)
+    assert m.digest() == port.mask_digest(w, n)
+    assert m.nnz() == port.mask_nnz(w, n)
+
+
+def test_single_gpu_masked_allreduce(pb, port, cuda):
+    rng = np.random.default_rng(12)
+    n = 1_234_567
+    g = rng.standard_normal(n).astype(np.float32)
+    bits = rng.random(n) < 0.2
+    w = words_from_bits(bits)
+    m = pb.SparsityMask.from_words(dev(w.view(np.int64)), n)
+    r = pb.masked_allreduce(dev(g), m, pb.TrackerStatus.Stable, 5, None)
+    assert r.stats.mode_used == pb.SyncMode.PackedAllReduce and r.stats.bytes_on_wire == 0
+    assert np.array_equal(u32(r.tensor.cpu().numpy()), u32(port.gse(g, w)))
+    r = pb.masked_allreduce(dev(g), m, pb.TrackerStatus.Unstable, 5, None)
+    assert r.stats.mode_used == pb.SyncMode.FullAllReduce
+    assert np.array_equal(u32(r.tensor.cpu().numpy()), u32(g))
+    pol = pb.SyncPolicy(density_threshold=0.1)
+    r = pb.masked_allreduce(dev(g), m, pb.TrackerStatus.Stable, 5, None, policy=pol)
+    assert r.stats.mode_used == pb.SyncMode.FullAllReduce and r.stats.fallback_reason == 3
+    pol = pb.SyncPolicy(scale=0.5)
+    r = pb.masked_allreduce(dev(g), m, pb.TrackerStatus.Stable, 5, None, policy=pol)
+    assert np.array_equal(u32(r.tensor.cpu().numpy()), u32(port.to_mean(port.gse(g, w), 2)))
+    with pytest.raises(pb.Error) as e:
+        pb.masked_allreduce(dev(g[:-1]), m, pb.TrackerStatus.Stable, 5, None)
+    assert e.value.code == pb.Errc.ShapeMismatch
+    # host-buffer (e2e) entry point
+    gh = torch.from_numpy(g).pin_memory()
+    oh = torch.empty(n, dtype=torch.float32).pin_memory()
+    st = pb.masked_allreduce_host(gh, m, pb.TrackerStatus.Stable, 5, None, oh)
+    assert st.mode_used == pb.SyncMode.PackedAllReduce
+    assert np.array_equal(u32(oh.numpy()), u32(port.gse(g, w)))
+
+
+def test_unpack_sgd_matches_trainer(pb, port, cuda):
+    rng = np.random.default_rng(13)
+    n = 300_001
+    s = rng.standard_normal(n).astype(np.float32)
+    wts = rng.standard_normal(n).astype(np.float32)
+    bits = rng.random(n) < 0.4
+    w = words_from_bits(bits)
+    m = pb.SparsityMask.from_words(dev(w.view(np.int64)), n)
+    p = pb.pack(dev(s), m, 0)
+    wd = dev(wts.copy())
+    gout = torch.empty(n, device=cuda)
+    pb.unpack_sgd(p.values, m, 1.0 / 8, 0.05, wd, gout)
+    mean = port.to_mean(port.gse(s, w), 8)
+    assert np.array_equal(u32(gout.cpu().numpy()), u32(mean))
+    assert np.array_equal(u32(wd.cpu().numpy()), u32(port.sgd_step(wts, mean, 0.05, w)))
+
+
+# ------------------------------------------------- full BASELINE sizes
+
+
+def test_prune_resnet50_full_size_bitexact(pb, port, cuda):
+    """C2: ResNet-50 shape (25,557,032) at 80%: words bit-exact vs the oracle."""
+    from paper_2505_18563_b200 import synth
+
+    shape = synth.model_shape("resnet50")
+    for recipe in (synth.W_REAL, synth.W_TIES):
+        wd = synth.weights_device(shape, 21, recipe)
+        m = pb.magnitude_prune(wd, 0.8)
+        assert m.nnz() == 5_111_404
+        ref = port.magnitude_prune(wd.cpu().numpy(), 0.8)
+        assert np.array_equal(m.words_host(), ref)
+        assert m.digest() == port.mask_digest(ref, shape.total)
+
+
+@pytest.mark.parametrize("model,ratio,nnz", [("vgg19", 0.95, 7_183_350), ("gpt2-medium", 0.9, 35_482_290)])
+def test_full_size_properties(pb, cuda, model, ratio, nnz):
+    """C3/C5 sizes: exact kept count, threshold property, pack->unpack == GSE,
+    checksum of the packed values == checksum of the GSE'd gradient."""
+    from paper_2505_18563_b200 import synth
+
+    shape = synth.model_shape(model)
+    wd = synth.weights_device(shape, 31, synth.W_TIES)
+    st = {}
+    m = pb.magnitude_prune(wd, ratio, stats=st)
+    assert m.nnz() == nnz
+    keep = expand_bits(m.words(), shape.total)
+    key = wd.view(torch.int32) & 0x7FFFFFFF
+    assert int(key[keep].min()) >= st["threshold"] >= int(key[~keep].max())
+    del key
+    g = torch.empty_like(wd)
+    pb.synth_fill(g, 5, synth.G_FULL)
+    del wd
+    p = pb.pack(g, m, 0)
+    assert p.values.numel() == nnz
+    ref_sum = torch.where(keep, g, torch.zeros((), device=g.device)).double().sum()
+    assert float(p.values.double().sum()) == float(ref_sum)
+    u = pb.unpack(p, m)
+    assert torch.equal(u, torch.where(keep, g, torch.zeros((), device=g.device)))
