@@ -1,0 +1,401 @@
+"""Benchmark of the PacTrain gradient-sync hot path on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+
+Metric (BASELINE.json): dense-equivalent gradient-sync GB/s
+    = 4 * len bytes of fp32 gradient per rank / t_step,
+where a step is one pass of the hot path over one synthetic gradient:
+vote -> pack -> NCCL allreduce -> unpack (N > 1), pack -> unpack (N = 1,
+no exchange), plus the magnitude re-prune for config c5. `value` is
+the whole-job aggregate: N ranks x 4*len / t_step (weak scaling: every rank
+syncs a full model-sized gradient). Inputs are HBM resident; the L2 is
+flushed (a 512 MiB write) before every timed step; timing is CUDA events on
+the launching stream, max over ranks. `e2e` is the same metric through the
+host-buffer C-ABI call (pinned H2D of the gradient, D2H of the result inside
+the timed region).
+
+Multi-GPU: launched by the driver under torch.distributed.run, one process per
+GPU; torch.distributed (nccl) carries the barrier / max-over-ranks plumbing and
+the NCCL unique id; the collective itself is the library's own NCCL comm.
+
+--impl reference times the reference's own CPU implementation (oracle/_ref,
+compiled from /root/reference by oracle/Makefile) on the host cores, on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (model shape, prune ratio, re-prune per step, bucket bytes)
+    "c1": ("resnet18", 0.9, False, 0),
+    "c2": ("resnet50", 0.8, False, 0),
+    "c3": ("vgg19", 0.95, False, 16 << 20),
+    "c4": ("bert-base", 0.5, False, 0),
+    "c5": ("gpt2-medium", 0.9, True, 32 << 20),
+}
+L2_FLUSH_BYTES = 512 << 20
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """NVML sampling of SM clock and throttle reasons during the timed region."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+        0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+        0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, device: int):
+        self.samples = []
+        self.reasons = 0
+        self._stop = threading.Event()
+        self.ok = False
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max_mhz = None
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                self.reasons |= nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.ok:
+            self.t.join()
+
+    def summary(self):
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml_unavailable"]}
+        names = [n for b, n in self.REASONS.items() if self.reasons & b and n != "gpu_idle"]
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": names, "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------ reference
+
+
+def run_reference(args, cfg):
+    """The reference's own CPU path (oracle/_ref) on this host's cores."""
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    import numpy as np
+
+    import oracle
+    from paper_2505_18563_b200 import synth
+
+    model, ratio, _, _ = CONFIGS[cfg]
+    shape = synth.model_shape(model)
+    n = shape.total
+    R = oracle.ref()
+    w = synth.weights_host(shape, 1234, synth.W_REAL)
+    words, nnz, _ = R.magnitude_prune(w, ratio)
+    nthreads = os.cpu_count() or 1
+    nworkers = max(2, args.gpus)
+    grads = [R.gse(synth.synth_host(n, synth.grad_seed(r, 0), synth.G_FULL), words) for r in range(max(1, args.gpus))]
+    if args.gpus == 1:
+        h = R.bench_create(grads[:1], words, slices=nthreads)
+        fn = lambda: R.bench_pack_unpack(h)  # noqa: E731
+        what = f"reference pack->unpack on {nthreads} thread slices of the full gradient"
+        cores = nthreads
+    else:
+        h = R.bench_create(grads, words, slices=0)
+        fn = lambda: R.bench_masked(h)  # noqa: E731
+        what = f"reference masked_allreduce (tracker Stable) over SimCluster, {nworkers} worker threads"
+        cores = nworkers
+    for _ in range(args.warmup):
+        fn()
+    ts = [fn() for _ in range(args.steps)]
+    R.bench_destroy(h)
+    t = sum(ts) / len(ts)
+    per_rank = 4.0 * n / t / 1e9
+    value = per_rank * args.gpus
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GB/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t * 1e3, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic", "config": {"workload": f"{cfg}:{model}", "len": n, "nnz": nnz, "ratio": ratio},
+        "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": cores, "kind": "reference",
+                         "sample": what + f"; {args.steps} steps, full {model} gradient per step"},
+        "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+METRIC = "dense-equiv. gradient sync GB/s (prune+pack+allreduce+unpack)"
+
+
+# ------------------------------------------------------------------ ours
+
+
+def cpu_baseline_sample(shape, ratio, words_np, n):
+    """Reference CPU path on this host, bounded sample (rank 0, N=1 only)."""
+    try:
+        import oracle
+        from paper_2505_18563_b200 import synth
+
+        R = oracle.ref()
+        kind = "reference"
+    except Exception as e:  # pragma: no cover
+        return {"value": None, "unit": "GB/s", "cores": 0, "kind": "unavailable", "sample": str(e)}
+    nthreads = os.cpu_count() or 1
+    g = R.gse(synth.synth_host(n, synth.grad_seed(0, 0), synth.G_FULL), words_np)
+    h = R.bench_create([g], words_np, slices=nthreads)
+    R.bench_pack_unpack(h)
+    ts = []
+    t0 = time.time()
+    while time.time() - t0 < 10.0 and len(ts) < 50:
+        ts.append(R.bench_pack_unpack(h))
+    R.bench_destroy(h)
+    t = statistics.median(ts)
+    return {"value": round(4.0 * n / t / 1e9, 4), "unit": "GB/s", "cores": nthreads, "kind": kind,
+            "sample": f"reference pack->unpack (codec.cpp:14-38) over the full {shape.name} gradient, "
+                      f"{nthreads} thread slices, median of {len(ts)} runs (~10 s)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--ratio", type=float, default=None, help="override the config's prune ratio")
+    ap.add_argument("--bucket-mb", type=float, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    cfg = args.config
+    if args.ratio is not None:
+        m, _, rp, bb = CONFIGS[cfg]
+        CONFIGS[cfg] = (m, args.ratio, rp, bb)
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+
+    import numpy as np
+    import torch
+
+    import paper_2505_18563_b200 as pb
+    from paper_2505_18563_b200 import synth
+
+    rank, world, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    comm = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+        comm = pb.Comm.from_process_group()
+
+    model, ratio, reprune, bucket = CONFIGS[cfg]
+    if args.bucket_mb is not None:
+        bucket = int(args.bucket_mb * (1 << 20))
+    shape = synth.model_shape(model)
+    n = shape.total
+    ctx = pb.Context.get(local)
+    stream = torch.cuda.current_stream()
+
+    # inputs: identical weights on every rank (same seed) -> identical global mask
+    weights = synth.weights_device(shape, 1234, synth.W_REAL, device=dev)
+    mask = pb.magnitude_prune(weights, ratio)
+    nnz = mask.nnz()
+    tracker = pb.MaskTracker(3)
+    for _ in range(4):
+        tracker.observe(mask)
+    assert tracker.status() == pb.TrackerStatus.Stable
+    grad = torch.empty(n, dtype=torch.float32, device=dev)
+    pb.synth_fill(grad, synth.grad_seed(rank, 0), synth.G_FULL)
+    pb.enforce_gradient_sparsity(grad, mask, out=grad)
+    out = torch.empty_like(grad)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+    policy = pb.SyncPolicy(bucket_bytes=bucket if world > 1 else 0)
+    w_cur = weights.clone() if reprune else None
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    def step(e):
+        if reprune:  # c5: regenerate the mask from the current weights every step
+            pb.magnitude_prune(w_cur, ratio, out=mask)
+            tracker.observe(mask)
+        return pb.masked_allreduce(grad, mask, tracker.status(), e, comm, policy=policy, out=out)
+
+    def timed(fn, k):
+        """k device-timed calls, L2 flushed before each; returns seconds list."""
+        evs = []
+        for i in range(k):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            fn(i)
+            b.record(stream)
+            evs.append((a, b))
+        torch.cuda.synchronize()
+        return [a.elapsed_time(b) * 1e-3 for a, b in evs]
+
+    # ---- headline: device-resident step
+    for i in range(args.warmup):
+        r = step(i)
+    assert r.stats.mode_used == pb.SyncMode.PackedAllReduce, r.stats
+    barrier()
+    l0 = ctx.kernel_launches()
+    with ClockSampler(local) as clk:
+        barrier()
+        ts = timed(step, args.steps)
+        barrier()
+    launches = ctx.kernel_launches() - l0
+    t_step = sum(ts) / len(ts)
+    if world > 1:
+        tt = torch.tensor([t_step], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        t_step = float(tt.item())
+    per_rank_gbs = 4.0 * n / t_step / 1e9
+    value = per_rank_gbs * world
+
+    # ---- dominant kernel roofline: pack and unpack timed alone (flushed)
+    packed = torch.empty(max(1, nnz), dtype=torch.float32, device=dev)
+    pk = pb.PackedGradient(mask.digest(), 0, packed[:nnz])
+    t_pack = statistics.median(timed(lambda i: pb.api._call(
+        pb.api.lib.pact_pack, ctx.handle, pb.api._ptr(grad), n, mask.handle, pb.api._ptr(packed), 0,
+        pb.api.C.c_uint64(2**64 - 1), pb.api._stream()), max(10, args.steps)))
+    t_unpack = statistics.median(timed(lambda i: pb.unpack(pk, mask, out=out), max(10, args.steps)))
+    alg_pack = 4 * n + n / 8 + 4 * nnz
+    alg_unpack = 4 * nnz + n / 8 + 4 * n
+    stages = {"pack_us": round(t_pack * 1e6, 2), "unpack_us": round(t_unpack * 1e6, 2),
+              "pack_gbs": round(alg_pack / t_pack / 1e9, 1), "unpack_gbs": round(alg_unpack / t_unpack / 1e9, 1)}
+    if reprune:
+        t_prune = statistics.median(timed(lambda i: pb.magnitude_prune(w_cur, ratio, out=mask), 5))
+        stages["prune_us"] = round(t_prune * 1e6, 1)
+        stages["prune_gbs"] = round((4 * n + n / 8) / t_prune / 1e9, 1)
+    if t_pack >= t_unpack:
+        dom, alg, tdom = "pack_kernel", alg_pack, t_pack
+    else:
+        dom, alg, tdom = "unpack_kernel", alg_unpack, t_unpack
+    peak, peak_kind = peaks()
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get(f"{cfg}:{dom}")
+        except Exception:
+            traffic = None
+    achieved = alg / tdom / 1e9
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": traffic, "peak_kind": peak_kind,
+                "algorithmic_bytes": int(alg)}
+
+    # ---- allreduce context (N > 1): dense NCCL busbw in the same run
+    extra = {}
+    if world > 1:
+        t_dense = statistics.median(timed(lambda i: pb.full_allreduce(grad, comm, out=out), 10))
+        t_packed_ar = statistics.median(timed(lambda i: pb.ring_allreduce(packed, comm, out=packed), 10))
+        f = 2 * (world - 1) / world
+        extra = {"dense_allreduce_us": round(t_dense * 1e6, 1),
+                 "dense_busbw_gbs": round(4 * n * f / t_dense / 1e9, 1),
+                 "packed_allreduce_us": round(t_packed_ar * 1e6, 1),
+                 "packed_busbw_gbs": round(4 * nnz * f / t_packed_ar / 1e9, 1),
+                 "dense_sync_equiv_gbs_per_rank": round(4 * n / t_dense / 1e9, 1)}
+
+    # ---- e2e through the host-buffer C-ABI entry point
+    e2e = None
+    if not args.no_e2e:
+        gh = grad.cpu().pin_memory()
+        oh = torch.empty(n, dtype=torch.float32).pin_memory()
+        for i in range(2):
+            pb.masked_allreduce_host(gh, mask, tracker.status(), i, comm, oh, policy=policy)
+        barrier()
+        te = []
+        for i in range(max(5, min(args.steps, 20))):
+            flush.zero_()
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            pb.masked_allreduce_host(gh, mask, tracker.status(), i, comm, oh, policy=policy)
+            b.record(stream)
+            b.synchronize()
+            te.append(a.elapsed_time(b) * 1e-3)
+        t_e2e = sum(te) / len(te)
+        if world > 1:
+            tt = torch.tensor([t_e2e], dtype=torch.float64, device=dev)
+            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+            t_e2e = float(tt.item())
+        e2e = {"value": round(4.0 * n / t_e2e / 1e9 * world, 3), "unit": "GB/s",
+               "h2d_bytes_per_step": 4 * n, "d2h_bytes_per_step": 4 * n, "ms_per_step": round(t_e2e * 1e3, 3)}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline_sample(shape, ratio, mask.words_host(), n)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t_step * 1e3, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": f"{cfg}:{model} fp32 grads, {int(round(ratio * 100))}% magnitude-pruned mask",
+                       "len": n, "nnz": nnz, "ratio": ratio, "reprune_per_step": reprune,
+                       "l2": "flushed (512 MiB write) before every timed step",
+                       "parallelism": f"dp{world}", "bucket_bytes": policy.bucket_bytes,
+                       "per_rank_gbs": round(per_rank_gbs, 2)},
+            "roofline": roofline, "stages": stages, **({"allreduce": extra} if extra else {}),
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if comm is not None:
+        torch.distributed.barrier()
+        comm.close()
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -30,7 +30,7 @@ extern "C" {
 #endif
 
 #define PACT_ABI_VERSION 1
-#define PACT_TILE 4096              /* elements per mask tile (64 words)     */
+#define PACT_TILE 1024              /* elements per offset tile (16 words)   */
 #define PACT_MAX_LEN ((1ull << 30) - 1)
 #define PACT_HEADER_BYTES 26        /* codec.hpp:90 kHeaderSize              */
 #define PACT_UNIQUE_ID_BYTES 128    /* NCCL unique id                        */

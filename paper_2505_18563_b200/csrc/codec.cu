@@ -1,22 +1,28 @@
 // codec.cu -- mask-indexed stream compaction (pack), scatter-expand (unpack,
 // optionally fused with to_mean and the masked SGD step), GSE, and the
-// mask bookkeeping kernels (fill, tile popcounts, exclusive scan).
+// mask bookkeeping kernels (fill, chunk popcounts, exclusive scan).
 //
 // Reference semantics: codec.cpp:14-38 (pack/unpack), sparsity.cpp:112-119
 // (GSE), trainer.cpp:202-214 and 268-273 (to_mean + sgd_step), tensor.cpp
 // 83-129 (mask layout, nnz).
 //
-// Layout: the gradient is split into 4096-element tiles (64 mask words). A
-// mask carries tile_off[t] = kept elements before tile t, so every tile's
-// packed range is known up front and tiles are independent: pack/unpack are
-// one streaming pass with no inter-CTA communication. Each thread owns four
-// float4 slots of the tile (coalesced 128-bit accesses), reads its 4-bit mask
-// nibble per slot and skips the load entirely when the nibble is zero (pack
-// and GSE only fetch the 32-byte sectors that hold kept values). Compacted
-// values are staged in shared memory and written out as one contiguous,
-// coalesced run per tile.
-#include <cstdio>
-
+// Layout: the gradient is cut into 1024-element chunks (16 mask words; the
+// word array is padded to whole chunks). A mask carries chunk_off[c] = kept
+// elements before chunk c, so one WARP owns one chunk end to end with no
+// inter-warp communication and no shared memory. Lane l's eight float4 slots
+// cover elements 128*j + 4*l (coalesced 512-byte warp accesses); slot j's two
+// mask words arrive as one broadcast 16-byte load (L1 resident: the next
+// chunk's 128-byte word line is prefetched into L1 one iteration ahead), and
+// the lane's rank inside the chunk is a popcount of the bits below it, so no
+// shuffles or scans are needed. Pack skips a slot's gradient load when its
+// 4-bit nibble is zero (only sectors holding kept values are read) and
+// stores kept values straight to their packed positions; unpack gathers them
+// with predicated loads and writes full float4s. All loads of a chunk are
+// issued before any use. Persistent grids; warps stride over chunks.
+//
+// The kernels are issue-bound, not bandwidth-bound, at the sizes of interest
+// (ncu: ~480 warp-instructions per chunk in the smem-staged version), so the
+// formulation minimises instructions per element.
 #include "common.cuh"
 #include "launch.h"
 
@@ -24,9 +30,10 @@ namespace pactk {
 
 namespace {
 
+constexpr int kCodecWarps = 8;  // 256-thread CTAs
 unsigned long long g_launches = 0;
 
-int grid_for(uint64_t tiles, int per_sm) {
+int sm_count() {
   static int sms = 0;
   if (!sms) {
     int dev = 0;
@@ -34,147 +41,264 @@ int grid_for(uint64_t tiles, int per_sm) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (sms <= 0) sms = 148;
   }
-  const uint64_t cap = (uint64_t)sms * per_sm;
-  return (int)(tiles < cap ? tiles : cap);
+  return sms;
+}
+
+template <typename K>
+int persistent_grid(K kernel, int warps = kCodecWarps) {
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, warps * 32, 0);
+  if (per_sm <= 0) per_sm = 1;
+  return sm_count() * per_sm;
+}
+
+unsigned grid_for(int cap, uint64_t chunks, int warps = kCodecWarps) {
+  const uint64_t need = (chunks + warps - 1) / warps;
+  return (unsigned)(need < (uint64_t)cap ? need : (uint64_t)cap);
+}
+
+// Per-warp double buffer of the next chunk's 16 mask words + its offset,
+// filled with cp.async one iteration ahead (no registers held in flight).
+constexpr int kWbuf = kChunkWords + 2;  // 16 words, chunk_off in [16]
+__device__ __forceinline__ void words_issue(uint64_t* dst, const uint64_t* __restrict__ words,
+                                            const uint32_t* __restrict__ chunk_off, uint64_t c) {
+  const int lane = threadIdx.x & 31;
+  if (lane < 8) {
+    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(dst + 2 * lane);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa),
+                 "l"(words + c * kChunkWords + 2 * lane)
+                 : "memory");
+  } else if (lane == 8 && chunk_off) {
+    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(dst + kChunkWords);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(chunk_off + c) : "memory");
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void words_wait_prev() {
+  asm volatile("cp.async.wait_group 1;" ::: "memory");
+  __syncwarp();
+}
+
+// Slot j of the current chunk: nibble and in-chunk rank of lane's first
+// element. `run` accumulates the kept count of the slots before (uniform).
+struct Slot {
+  uint32_t nib, pos;
+};
+__device__ __forceinline__ Slot chunk_slot(const uint64_t* wc, int j, uint32_t& run) {
+  const int lane = threadIdx.x & 31;
+  const ulonglong2 ab = reinterpret_cast<const ulonglong2*>(wc)[j];
+  const uint64_t w = lane < 16 ? ab.x : ab.y;
+  const int sh = 4 * (lane & 15);
+  Slot s;
+  s.nib = (uint32_t)(w >> sh) & 0xFu;
+  const uint32_t pa = (uint32_t)__popcll(ab.x);
+  s.pos = run + (uint32_t)__popcll(w & ((1ull << sh) - 1ull)) + (lane < 16 ? 0u : pa);
+  run += pa + (uint32_t)__popcll(ab.y);
+  return s;
 }
 
 // ------------------------------------------------------------------ pack
-__global__ void __launch_bounds__(kThreads, 6)
+// One warp per chunk; kept values are staged in a 4 KiB per-warp buffer and
+// leave as one coalesced run (full-line writes of the packed buffer).
+constexpr int kPuWarps = 4;  // 128-thread CTAs
+
+__global__ void __launch_bounds__(kPuWarps * 32)
     pack_kernel(const float* __restrict__ g, uint64_t len, const uint64_t* __restrict__ words,
-                uint64_t nwords, const uint32_t* __restrict__ tile_off, float* __restrict__ packed,
-                uint64_t tb, uint64_t te) {
-  __shared__ uint64_t sw[kTileWords];
-  __shared__ uint32_t wpre[kTileWords + 1];
-  __shared__ float stage[kTile];
-  const int tid = threadIdx.x;
+                const uint32_t* __restrict__ chunk_off, float* __restrict__ packed, uint64_t cb,
+                uint64_t ce) {
+  __shared__ float stage_all[kPuWarps][kChunk];
+  __shared__ __align__(16) uint64_t wsm[kPuWarps][2][kWbuf];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  float* stage = stage_all[warp];
   const bool vec_ok = (((uintptr_t)g) & 15) == 0;
-  for (uint64_t t = tb + blockIdx.x; t < te; t += gridDim.x) {
-    load_tile_words(words, nwords, t, sw, wpre);
-    const uint64_t e0 = t * (uint64_t)kTile;
-    float4 v[kVecPerThread];
-    uint32_t nib[kVecPerThread];
+  const uint64_t nwt = (uint64_t)gridDim.x * kPuWarps;
+  uint64_t c = cb + (uint64_t)blockIdx.x * kPuWarps + warp;
+  if (c >= ce) return;
+  words_issue(wsm[warp][0], words, chunk_off, c);
+  for (int cur = 0; c < ce; c += nwt, cur ^= 1) {
+    if (c + nwt < ce) words_issue(wsm[warp][cur ^ 1], words, chunk_off, c + nwt);
+    else asm volatile("cp.async.commit_group;" ::: "memory");
+    words_wait_prev();
+    const uint64_t* wc = wsm[warp][cur];
+    const uint32_t base = (uint32_t)wc[kChunkWords];
+    const uint64_t e0 = c * (uint64_t)kChunk + 4 * lane;
+    uint32_t run = 0;
+    float4 v[kVecPerLane];
 #pragma unroll
-    for (int j = 0; j < kVecPerThread; ++j) {
-      const int e = (j * kThreads + tid) * 4;
-      nib[j] = nibble_at(sw, e);
+    for (int j = 0; j < kVecPerLane; ++j) {
+      const Slot s = chunk_slot(wc, j, run);
+      const uint64_t ge = e0 + 128 * j;
       v[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (nib[j]) {
-        const uint64_t ge = e0 + e;
+      if (s.nib) {
         if (vec_ok && ge + 4 <= len) {
           v[j] = ld_stream_f4(reinterpret_cast<const float4*>(g + ge));
         } else {  // unaligned base or ragged tail: only kept (hence in-range) lanes
-          if (nib[j] & 1) v[j].x = g[ge];
-          if (nib[j] & 2) v[j].y = g[ge + 1];
-          if (nib[j] & 4) v[j].z = g[ge + 2];
-          if (nib[j] & 8) v[j].w = g[ge + 3];
+          if (s.nib & 1) v[j].x = g[ge];
+          if (s.nib & 2) v[j].y = g[ge + 1];
+          if (s.nib & 4) v[j].z = g[ge + 2];
+          if (s.nib & 8) v[j].w = g[ge + 3];
         }
       }
     }
+    run = 0;  // positions recomputed from the (smem) words: fewer live registers
 #pragma unroll
-    for (int j = 0; j < kVecPerThread; ++j) {
-      if (!nib[j]) continue;
-      const int e = (j * kThreads + tid) * 4;
-      uint32_t pos = rank_before(sw, wpre, e);
-      if (nib[j] & 1) stage[pos++] = v[j].x;
-      if (nib[j] & 2) stage[pos++] = v[j].y;
-      if (nib[j] & 4) stage[pos++] = v[j].z;
-      if (nib[j] & 8) stage[pos++] = v[j].w;
+    for (int j = 0; j < kVecPerLane; ++j) {
+      const Slot s = chunk_slot(wc, j, run);
+      const uint32_t nib = s.nib, p = s.pos;
+      const uint32_t b0 = nib & 1, b1 = (nib >> 1) & 1, b2 = (nib >> 2) & 1;
+      if (b0) stage[p] = v[j].x;
+      if (b1) stage[p + b0] = v[j].y;
+      if (b2) stage[p + b0 + b1] = v[j].z;
+      if (nib & 8) stage[p + b0 + b1 + b2] = v[j].w;
     }
-    __syncthreads();
-    const uint32_t cnt = wpre[kTileWords];
-    float* dst = packed + tile_off[t];
-    for (uint32_t i = tid; i < cnt; i += kThreads) dst[i] = stage[i];
-    __syncthreads();
+    __syncwarp();
+    float* dst = packed + base;
+#pragma unroll 4
+    for (uint32_t i = lane; i < run; i += 32) dst[i] = stage[i];
+    __syncwarp();  // stage and buffer `cur` are reused
   }
 }
 
 // ---------------------------------------------------------------- unpack
-// kSgd: fused to_mean (scale) + masked SGD on weights; grad_out optional.
+// kSgd: fused to_mean (scale) + masked SGD on weights; out (grad) optional.
+// Three-stage cp.async pipeline per warp: mask words + offsets of chunk i+2,
+// the packed run of chunk i+1 (exact length, from the offsets), expansion of
+// chunk i with full-float4 streaming stores.
+__device__ __forceinline__ void offs_words_issue(uint64_t* dst, const uint64_t* __restrict__ words,
+                                                 const uint32_t* __restrict__ chunk_off, uint64_t c) {
+  const int lane = threadIdx.x & 31;
+  if (lane < 8) {
+    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(dst + 2 * lane);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa),
+                 "l"(words + c * kChunkWords + 2 * lane)
+                 : "memory");
+  } else if (lane < 10) {  // chunk_off[c], chunk_off[c+1] -> low halves of dst[16], dst[17]
+    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(dst + kChunkWords + (lane - 8));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(chunk_off + c + (lane - 8))
+                 : "memory");
+  }
+}
+__device__ __forceinline__ void run_issue(float* dst, const float* __restrict__ src, uint32_t cnt) {
+  const int lane = threadIdx.x & 31;
+  for (uint32_t i = lane; i < cnt; i += 32) {
+    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(dst + i);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(src + i) : "memory");
+  }
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+
 template <bool kSgd>
-__global__ void __launch_bounds__(kThreads, 8)
+__global__ void __launch_bounds__(kPuWarps * 32)
     unpack_kernel(const float* __restrict__ packed, uint64_t len, const uint64_t* __restrict__ words,
-                  uint64_t nwords, const uint32_t* __restrict__ tile_off, float scale, int do_scale,
-                  float* __restrict__ out, float lr, float* __restrict__ weights, uint64_t tb,
-                  uint64_t te) {
-  __shared__ uint64_t sw[kTileWords];
-  __shared__ uint32_t wpre[kTileWords + 1];
-  __shared__ float stage[kTile];
-  const int tid = threadIdx.x;
+                  const uint32_t* __restrict__ chunk_off, float scale, int do_scale,
+                  float* __restrict__ out, float lr, float* __restrict__ weights, uint64_t cb,
+                  uint64_t ce) {
+  __shared__ __align__(16) float psm[kPuWarps][2][kChunk];
+  __shared__ __align__(16) uint64_t wsm[kPuWarps][3][kWbuf];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const bool vec_ok = ((((uintptr_t)out) | (kSgd ? (uintptr_t)weights : 0)) & 15) == 0;
-  for (uint64_t t = tb + blockIdx.x; t < te; t += gridDim.x) {
-    load_tile_words(words, nwords, t, sw, wpre);
-    const uint32_t cnt = wpre[kTileWords];
-    const float* src = packed + tile_off[t];
-    for (uint32_t i = tid; i < cnt; i += kThreads) stage[i] = src[i];
-    __syncthreads();
-    const uint64_t e0 = t * (uint64_t)kTile;
+  const uint64_t nwt = (uint64_t)gridDim.x * kPuWarps;
+  uint64_t c = cb + (uint64_t)blockIdx.x * kPuWarps + warp;
+  if (c >= ce) return;
+  auto offs = [&](int slot, uint32_t& b, uint32_t& n) {
+    const uint32_t* o = reinterpret_cast<const uint32_t*>(wsm[warp][slot] + kChunkWords);
+    b = o[0];
+    n = o[2] - o[0];
+  };
+  // prologue: words(c0), words(c1), run(c0)
+  offs_words_issue(wsm[warp][0], words, chunk_off, c);
+  cp_commit();
+  if (c + nwt < ce) offs_words_issue(wsm[warp][1], words, chunk_off, c + nwt);
+  cp_commit();
+  asm volatile("cp.async.wait_group 1;" ::: "memory");
+  __syncwarp();
+  {
+    uint32_t b, n;
+    offs(0, b, n);
+    run_issue(psm[warp][0], packed + b, n);
+  }
+  cp_commit();
+  int wi = 0, pi = 0;
+  for (; c < ce; c += nwt) {
+    const int w1 = wi == 2 ? 0 : wi + 1, w2 = w1 == 2 ? 0 : w1 + 1;
+    if (c + 2 * nwt < ce) offs_words_issue(wsm[warp][w2], words, chunk_off, c + 2 * nwt);
+    cp_commit();
+    asm volatile("cp.async.wait_group 1;" ::: "memory");  // words(c+nwt), run(c) landed
+    __syncwarp();
+    if (c + nwt < ce) {
+      uint32_t b, n;
+      offs(w1, b, n);
+      run_issue(psm[warp][pi ^ 1], packed + b, n);
+    }
+    cp_commit();
+    const uint64_t* wc = wsm[warp][wi];
+    const float* stage = psm[warp][pi];
+    const uint64_t e0 = c * (uint64_t)kChunk + 4 * lane;
+    uint32_t run = 0;
 #pragma unroll
-    for (int j = 0; j < kVecPerThread; ++j) {
-      const int e = (j * kThreads + tid) * 4;
-      const uint64_t ge = e0 + e;
+    for (int j = 0; j < kVecPerLane; ++j) {
+      const Slot s = chunk_slot(wc, j, run);
+      const uint64_t ge = e0 + 128 * j;
       if (ge >= len) continue;
-      const uint32_t nib = nibble_at(sw, e);
-      uint32_t pos = nib ? rank_before(sw, wpre, e) : 0;
+      const uint32_t nib = s.nib;
+      const uint32_t b0 = nib & 1, b1 = (nib >> 1) & 1, b2 = (nib >> 2) & 1;
       float o[4];
+      o[0] = b0 ? stage[s.pos] : 0.0f;
+      o[1] = b1 ? stage[s.pos + b0] : 0.0f;
+      o[2] = b2 ? stage[s.pos + b0 + b1] : 0.0f;
+      o[3] = (nib & 8) ? stage[s.pos + b0 + b1 + b2] : 0.0f;
+      if (do_scale) {
 #pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        if (nib & (1u << b)) {
-          const float x = stage[pos++];
-          o[b] = do_scale ? __fmul_rn(x, scale) : x;
-        } else {
-          o[b] = 0.0f;
-        }
+        for (int b = 0; b < 4; ++b)
+          if ((nib >> b) & 1) o[b] = __fmul_rn(o[b], scale);
       }
       const bool full = vec_ok && ge + 4 <= len;
       if (!kSgd || out != nullptr) {
-        if (full) {
+        if (full)
           st_stream_f4(reinterpret_cast<float4*>(out + ge), make_float4(o[0], o[1], o[2], o[3]));
-        } else {
+        else
           for (int b = 0; b < 4 && ge + b < len; ++b) out[ge + b] = o[b];
-        }
       }
       if (kSgd) {
-        float p[4];
+        float q[4];
         if (full) {
           const float4 w4 = *reinterpret_cast<const float4*>(weights + ge);
-          p[0] = w4.x, p[1] = w4.y, p[2] = w4.z, p[3] = w4.w;
+          q[0] = w4.x, q[1] = w4.y, q[2] = w4.z, q[3] = w4.w;
         } else {
-          for (int b = 0; b < 4; ++b) p[b] = ge + b < len ? weights[ge + b] : 0.f;
+          for (int b = 0; b < 4; ++b) q[b] = ge + b < len ? weights[ge + b] : 0.f;
         }
 #pragma unroll
         for (int b = 0; b < 4; ++b)  // trainer.cpp:208-212, no FMA contraction
-          p[b] = (nib & (1u << b)) ? __fsub_rn(p[b], __fmul_rn(lr, o[b])) : 0.0f;
-        if (full) {
-          *reinterpret_cast<float4*>(weights + ge) = make_float4(p[0], p[1], p[2], p[3]);
-        } else {
-          for (int b = 0; b < 4 && ge + b < len; ++b) weights[ge + b] = p[b];
-        }
+          q[b] = ((nib >> b) & 1) ? __fsub_rn(q[b], __fmul_rn(lr, o[b])) : 0.0f;
+        if (full)
+          *reinterpret_cast<float4*>(weights + ge) = make_float4(q[0], q[1], q[2], q[3]);
+        else
+          for (int b = 0; b < 4 && ge + b < len; ++b) weights[ge + b] = q[b];
       }
     }
-    __syncthreads();
+    __syncwarp();  // run buffer `pi` and word buffer `wi` are refilled next
+    wi = w1;
+    pi ^= 1;
   }
+  asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
 // ------------------------------------------------------------------- GSE
-__global__ void __launch_bounds__(kThreads, 8)
-    gse_kernel(const float* g, uint64_t len, const uint64_t* __restrict__ words, uint64_t nwords,
-               float* out, uint64_t ntiles) {  // out may alias g (in-place GSE)
-  __shared__ uint64_t sw[kTileWords];
-  const int tid = threadIdx.x;
+__global__ void __launch_bounds__(kCodecWarps * 32)
+    gse_kernel(const float* g, uint64_t len, const uint64_t* __restrict__ words, float* out,
+               uint64_t nchunks) {  // out may alias g (in-place GSE)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const bool vec_ok = ((((uintptr_t)g) | ((uintptr_t)out)) & 15) == 0;
-  for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    if (tid < kTileWords) {
-      const uint64_t wi = t * kTileWords + tid;
-      sw[tid] = wi < nwords ? __ldg(words + wi) : 0ull;
-    }
-    __syncthreads();
-    const uint64_t e0 = t * (uint64_t)kTile;
+  const uint64_t nwt = (uint64_t)gridDim.x * kCodecWarps;
+  for (uint64_t c = (uint64_t)blockIdx.x * kCodecWarps + warp; c < nchunks; c += nwt) {
+    const uint64_t* wc = words + c * kChunkWords;
+    const uint64_t e0 = c * (uint64_t)kChunk + 4 * lane;
+    uint32_t run = 0;
 #pragma unroll
-    for (int j = 0; j < kVecPerThread; ++j) {
-      const int e = (j * kThreads + tid) * 4;
-      const uint64_t ge = e0 + e;
+    for (int j = 0; j < kVecPerLane; ++j) {
+      const uint32_t nib = chunk_slot(wc, j, run).nib;
+      const uint64_t ge = e0 + 128 * j;
       if (ge >= len) continue;
-      const uint32_t nib = nibble_at(sw, e);
       float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
       if (vec_ok && ge + 4 <= len) {
         if (nib) {
@@ -189,80 +313,7 @@ __global__ void __launch_bounds__(kThreads, 8)
         for (int b = 0; b < 4 && ge + b < len; ++b) out[ge + b] = (nib >> b) & 1 ? g[ge + b] : 0.0f;
       }
     }
-    __syncthreads();
   }
-}
-
-// ------------------------------------------------------- mask bookkeeping
-__global__ void mask_fill_kernel(uint64_t* words, uint64_t nwords, uint64_t len, int keep,
-                                 uint32_t* tile_off, uint64_t ntiles) {
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nwords; i += stride) {
-    uint64_t w = keep ? ~0ull : 0ull;
-    if (keep && i == nwords - 1 && (len & 63)) w = (1ull << (len & 63)) - 1ull;
-    words[i] = w;
-  }
-  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t <= ntiles; t += stride) {
-    const uint64_t e = t * (uint64_t)kTile;
-    tile_off[t] = keep ? (uint32_t)(e < len ? e : len) : 0u;
-  }
-}
-
-__global__ void clear_tail_kernel(uint64_t* words, uint64_t len) {
-  const uint64_t last = (len - 1) >> 6;
-  words[last] &= (1ull << (len & 63)) - 1ull;
-}
-
-// one warp per tile: popcount of its 64 words
-__global__ void tile_popc_kernel(const uint64_t* __restrict__ words, uint64_t nwords,
-                                 uint32_t* __restrict__ tile_popc, uint64_t ntiles) {
-  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (warp >= ntiles) return;
-  const uint64_t w0 = warp * kTileWords + 2 * lane;
-  uint32_t c = 0;
-  if (w0 < nwords) c += __popcll(words[w0]);
-  if (w0 + 1 < nwords) c += __popcll(words[w0 + 1]);
-  c = warp_sum(c);
-  if (lane == 0) tile_popc[warp] = c;
-}
-
-// single-CTA exclusive scan, 1024 threads x 8 items per chunk
-__global__ void __launch_bounds__(1024) scan_excl_kernel(const uint32_t* __restrict__ in, uint64_t n,
-                                                         uint32_t* __restrict__ out) {
-  __shared__ uint32_t warp_tot[33];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  uint32_t carry = 0;
-  for (uint64_t base = 0; base < n; base += 8192) {
-    uint32_t v[8];
-    uint32_t s = 0;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const uint64_t idx = base + (uint64_t)tid * 8 + i;
-      v[i] = idx < n ? in[idx] : 0u;
-      s += v[i];
-    }
-    const uint32_t inc = warp_incl_scan(s);
-    if (lane == 31) warp_tot[warp] = inc;
-    __syncthreads();
-    if (warp == 0) {
-      const uint32_t x = warp_tot[lane];
-      const uint32_t xi = warp_incl_scan(x);
-      warp_tot[lane] = xi - x;
-      if (lane == 31) warp_tot[32] = xi;
-    }
-    __syncthreads();
-    uint32_t run = carry + warp_tot[warp] + inc - s;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const uint64_t idx = base + (uint64_t)tid * 8 + i;
-      if (idx < n) out[idx] = run;
-      run += v[i];
-    }
-    carry += warp_tot[32];
-    __syncthreads();
-  }
-  if (tid == 0) out[n] = carry;
 }
 
 // out[i] = in[i] * scale (dense-fallback epilogue of to_mean, trainer.cpp:268-273)
@@ -273,52 +324,166 @@ __global__ void __launch_bounds__(256) scale_kernel(const float* __restrict__ in
     out[i] = __fmul_rn(in[i], scale);
 }
 
+// ------------------------------------------------------- mask bookkeeping
+__global__ void mask_fill_kernel(uint64_t* words, uint64_t nwords, uint64_t len, int keep,
+                                 uint32_t* chunk_off, uint64_t nchunks) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nwords; i += stride) {
+    uint64_t w = keep ? ~0ull : 0ull;
+    if (keep && i == nwords - 1 && (len & 63)) w = (1ull << (len & 63)) - 1ull;
+    words[i] = w;
+  }
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t <= nchunks; t += stride) {
+    const uint64_t e = t * (uint64_t)kChunk;
+    chunk_off[t] = keep ? (uint32_t)(e < len ? e : len) : 0u;
+  }
+}
+
+__global__ void clear_tail_kernel(uint64_t* words, uint64_t len) {
+  const uint64_t last = (len - 1) >> 6;
+  words[last] &= (1ull << (len & 63)) - 1ull;
+}
+
+// half a warp per chunk: popcount of its 16 words
+__global__ void chunk_popc_kernel(const uint64_t* __restrict__ words, uint64_t nwords,
+                                  uint32_t* __restrict__ popc, uint64_t nchunks) {
+  const uint64_t gt = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  const uint64_t c = gt >> 4;
+  const uint64_t wi = c * kChunkWords + (gt & 15);
+  uint32_t v = (c < nchunks && wi < nwords) ? (uint32_t)__popcll(words[wi]) : 0u;
+#pragma unroll
+  for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((gt & 15) == 0 && c < nchunks) popc[c] = v;
+}
+
+// Single-pass exclusive scan (decoupled look-back): 8192 values per CTA,
+// tiles ordered by a ticket so every CTA's predecessors are running or done.
+constexpr uint64_t kStAgg = 1ull << 62, kStIncl = 2ull << 62, kStMask = 3ull << 62;
+constexpr int kScanItems = 8192;
+
+__global__ void __launch_bounds__(1024) scan_excl_kernel(const uint32_t* __restrict__ in, uint64_t n,
+                                                         uint32_t* __restrict__ out,
+                                                         uint64_t* __restrict__ state,
+                                                         unsigned* __restrict__ ticket) {
+  __shared__ uint32_t warp_tot[33];
+  __shared__ uint32_t s_tile;
+  __shared__ uint64_t s_prefix;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) s_tile = atomicAdd(ticket, 1u);
+  __syncthreads();
+  const uint64_t t = s_tile;
+  const uint64_t base = t * kScanItems;
+  uint32_t v[8];
+  uint32_t s = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const uint64_t idx = base + (uint64_t)tid * 8 + i;
+    v[i] = idx < n ? in[idx] : 0u;
+    s += v[i];
+  }
+  const uint32_t inc = warp_incl_scan(s);
+  if (lane == 31) warp_tot[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    const uint32_t x = warp_tot[lane];
+    const uint32_t xi = warp_incl_scan(x);
+    warp_tot[lane] = xi - x;
+    const uint64_t total = __shfl_sync(0xffffffffu, xi, 31);
+    uint64_t before = 0;
+    if (t == 0) {
+      if (lane == 0) st_relaxed_u64(state, kStIncl | total);
+    } else {
+      if (lane == 0) st_relaxed_u64(state + t, kStAgg | total);
+      int64_t look = (int64_t)t - 1;
+      while (true) {
+        const int64_t p = look - lane;
+        uint64_t st = p >= 0 ? ld_relaxed_u64(state + p) : kStIncl;
+        while (__any_sync(0xffffffffu, (st & kStMask) == 0))
+          if ((st & kStMask) == 0) st = ld_relaxed_u64(state + p);
+        const unsigned incl = __ballot_sync(0xffffffffu, (st & kStMask) == kStIncl);
+        const int L = incl ? __ffs(incl) - 1 : 31;
+        before += warp_sum(lane <= L ? (st & ~kStMask) : 0ull);
+        if (incl) break;
+        look -= 32;
+      }
+      if (lane == 0) st_relaxed_u64(state + t, kStIncl | (before + total));
+    }
+    if (lane == 0) {
+      s_prefix = before;
+      if (base + kScanItems >= n) out[n] = (uint32_t)(before + total);
+    }
+  }
+  __syncthreads();
+  uint32_t run = (uint32_t)s_prefix + warp_tot[warp] + inc - s;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const uint64_t idx = base + (uint64_t)tid * 8 + i;
+    if (idx < n) out[idx] = run;
+    run += v[i];
+  }
+}
+
 }  // namespace
 
 uint64_t launches() { return g_launches; }
 void note_launch(uint64_t n) { g_launches += n; }
 
-void launch_pack(const float* g, uint64_t len, const uint64_t* words, const uint32_t* tile_off,
-                 float* packed, uint64_t tb, uint64_t te, cudaStream_t s) {
-  if (te <= tb) return;
-  pack_kernel<<<grid_for(te - tb, 8), kThreads, 0, s>>>(g, len, words, (len + 63) / 64, tile_off,
-                                                        packed, tb, te);
+void launch_pack(const float* g, uint64_t len, const uint64_t* words, const uint32_t* chunk_off,
+                 float* packed, uint64_t cb, uint64_t ce, cudaStream_t s) {
+  if (ce <= cb) return;
+  static int cap = 0;
+  if (!cap) cap = persistent_grid(pack_kernel, kPuWarps);
+  pack_kernel<<<grid_for(cap, ce - cb, kPuWarps), kPuWarps * 32, 0, s>>>(g, len, words, chunk_off, packed,
+                                                                   cb, ce);
   note_launch();
 }
 
 void launch_unpack(const float* packed, uint64_t len, const uint64_t* words,
-                   const uint32_t* tile_off, float scale, int do_scale, float* out, uint64_t tb,
-                   uint64_t te, cudaStream_t s) {
-  if (te <= tb) return;
-  unpack_kernel<false><<<grid_for(te - tb, 8), kThreads, 0, s>>>(
-      packed, len, words, (len + 63) / 64, tile_off, scale, do_scale, out, 0.f, nullptr, tb, te);
+                   const uint32_t* chunk_off, float scale, int do_scale, float* out, uint64_t cb,
+                   uint64_t ce, cudaStream_t s) {
+  if (ce <= cb) return;
+  static int cap = 0;
+  if (!cap) cap = persistent_grid(unpack_kernel<false>, kPuWarps);
+  unpack_kernel<false><<<grid_for(cap, ce - cb, kPuWarps), kPuWarps * 32, 0, s>>>(
+      packed, len, words, chunk_off, scale, do_scale, out, 0.f, nullptr, cb, ce);
   note_launch();
 }
 
 void launch_unpack_sgd(const float* packed, uint64_t len, const uint64_t* words,
-                       const uint32_t* tile_off, float scale, int do_scale, float lr,
+                       const uint32_t* chunk_off, float scale, int do_scale, float lr,
                        float* grad_out, float* weights, cudaStream_t s) {
-  const uint64_t nt = (len + kTile - 1) / kTile;
-  if (!nt) return;
-  unpack_kernel<true><<<grid_for(nt, 8), kThreads, 0, s>>>(packed, len, words, (len + 63) / 64,
-                                                           tile_off, scale, do_scale, grad_out, lr,
-                                                           weights, 0, nt);
+  const uint64_t nc = (len + kChunk - 1) / kChunk;
+  if (!nc) return;
+  static int cap = 0;
+  if (!cap) cap = persistent_grid(unpack_kernel<true>, kPuWarps);
+  unpack_kernel<true><<<grid_for(cap, nc, kPuWarps), kPuWarps * 32, 0, s>>>(
+      packed, len, words, chunk_off, scale, do_scale, grad_out, lr, weights, 0, nc);
   note_launch();
 }
 
 void launch_gse(const float* g, uint64_t len, const uint64_t* words, float* out, cudaStream_t s) {
-  const uint64_t nt = (len + kTile - 1) / kTile;
-  if (!nt) return;
-  gse_kernel<<<grid_for(nt, 8), kThreads, 0, s>>>(g, len, words, (len + 63) / 64, out, nt);
+  const uint64_t nc = (len + kChunk - 1) / kChunk;
+  if (!nc) return;
+  static int cap = 0;
+  if (!cap) cap = persistent_grid(gse_kernel);
+  gse_kernel<<<grid_for(cap, nc), kCodecWarps * 32, 0, s>>>(g, len, words, out, nc);
   note_launch();
 }
 
-void launch_mask_fill(uint64_t* words, uint64_t len, int keep, uint32_t* tile_off, cudaStream_t s) {
-  const uint64_t nw = (len + 63) / 64, nt = (len + kTile - 1) / kTile;
-  const uint64_t work = nw > nt + 1 ? nw : nt + 1;
+void launch_scale(const float* in, float* out, uint64_t len, float scale, cudaStream_t s) {
+  if (!len) return;
+  uint64_t blocks = (len + 255) / 256;
+  if (blocks > (uint64_t)sm_count() * 16) blocks = (uint64_t)sm_count() * 16;
+  scale_kernel<<<(unsigned)blocks, 256, 0, s>>>(in, out, len, scale);
+  note_launch();
+}
+
+void launch_mask_fill(uint64_t* words, uint64_t len, int keep, uint32_t* chunk_off, cudaStream_t s) {
+  const uint64_t nw = (len + 63) / 64, nc = (len + kChunk - 1) / kChunk;
+  const uint64_t work = nw > nc + 1 ? nw : nc + 1;
   int grid = (int)((work + 255) / 256);
   if (grid > 4096) grid = 4096;
-  mask_fill_kernel<<<grid, 256, 0, s>>>(words, nw, len, keep, tile_off, nt);
+  mask_fill_kernel<<<grid, 256, 0, s>>>(words, nw, len, keep, chunk_off, nc);
   note_launch();
 }
 
@@ -328,24 +493,21 @@ void launch_clear_tail(uint64_t* words, uint64_t len, cudaStream_t s) {
   note_launch();
 }
 
-void launch_tile_popc(const uint64_t* words, uint64_t len, uint32_t* tile_popc, cudaStream_t s) {
-  const uint64_t nt = (len + kTile - 1) / kTile;
-  if (!nt) return;
-  tile_popc_kernel<<<(unsigned)((nt * 32 + 255) / 256), 256, 0, s>>>(words, (len + 63) / 64,
-                                                                    tile_popc, nt);
+void launch_tile_popc(const uint64_t* words, uint64_t len, uint32_t* popc, cudaStream_t s) {
+  const uint64_t nc = (len + kChunk - 1) / kChunk;
+  if (!nc) return;
+  chunk_popc_kernel<<<(unsigned)((nc * 16 + 255) / 256), 256, 0, s>>>(words, (len + 63) / 64, popc, nc);
   note_launch();
 }
 
-void launch_scan_excl(const uint32_t* in, uint64_t n, uint32_t* out, cudaStream_t s) {
-  scan_excl_kernel<<<1, 1024, 0, s>>>(in, n, out);
-  note_launch();
-}
+size_t scan_scratch_bytes(uint64_t n) { return ((n + kScanItems - 1) / kScanItems + 1) * 8 + 8; }
 
-void launch_scale(const float* in, float* out, uint64_t len, float scale, cudaStream_t s) {
-  if (!len) return;
-  uint64_t blocks = (len + 255) / 256;
-  if (blocks > 148 * 16) blocks = 148 * 16;
-  scale_kernel<<<(unsigned)blocks, 256, 0, s>>>(in, out, len, scale);
+void launch_scan_excl(const uint32_t* in, uint64_t n, uint32_t* out, void* scratch, cudaStream_t s) {
+  const uint64_t tiles = n ? (n + kScanItems - 1) / kScanItems : 1;
+  cudaMemsetAsync(scratch, 0, tiles * 8 + 8, s);
+  uint64_t* state = static_cast<uint64_t*>(scratch);
+  scan_excl_kernel<<<(unsigned)tiles, 1024, 0, s>>>(in, n, out, state,
+                                                    reinterpret_cast<unsigned*>(state + tiles));
   note_launch();
 }
 

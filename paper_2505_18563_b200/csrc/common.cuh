@@ -6,9 +6,15 @@
 
 namespace pactk {
 
-constexpr int kTile = 4096;            // elements per mask tile (= PACT_TILE)
-constexpr int kTileWords = kTile / 64; // 64 words
-constexpr int kThreads = 256;          // CTA size of the streaming kernels
+// Offset granularity of a mask: one warp work unit of pack/unpack.
+constexpr int kChunk = 1024;             // elements (= PACT_TILE)
+constexpr int kChunkWords = kChunk / 64; // 16 words
+constexpr int kVecPerLane = kChunk / (4 * 32);  // 8 float4 per lane
+
+// CTA tile of the prune kernels (4 chunks).
+constexpr int kTile = 4096;
+constexpr int kTileWords = kTile / 64;
+constexpr int kThreads = 256;
 constexpr int kVecPerThread = kTile / (4 * kThreads);  // 4 float4 per thread
 
 // |w| ordering of finite floats == unsigned ordering of bits & 0x7fffffff
@@ -24,7 +30,7 @@ __device__ __forceinline__ void st_relaxed_u64(uint64_t* p, uint64_t v) {
   asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-// streaming (evict-first) 128-bit load: the dense gradient is touched once
+// streaming (evict-first) 128-bit accesses: the dense gradient is touched once
 __device__ __forceinline__ float4 ld_stream_f4(const float4* p) {
   float4 v;
   asm volatile("ld.global.cs.v4.f32 {%0,%1,%2,%3}, [%4];"
@@ -37,19 +43,10 @@ __device__ __forceinline__ void st_stream_f4(float4* p, float4 v) {
                "f"(v.w)
                : "memory");
 }
-
-__device__ __forceinline__ float f4_get(const float4& v, int i) {
-  return i == 0 ? v.x : (i == 1 ? v.y : (i == 2 ? v.z : v.w));
-}
-
-// 4-bit slice of the tile mask covering elements [e, e+4) (e multiple of 4)
-__device__ __forceinline__ uint32_t nibble_at(const uint64_t* sw, int e) {
-  return (uint32_t)(sw[e >> 6] >> (e & 63)) & 0xFu;
-}
-// kept elements of the tile strictly before element e
-__device__ __forceinline__ uint32_t rank_before(const uint64_t* sw, const uint32_t* wpre, int e) {
-  const uint64_t below = (e & 63) ? (sw[e >> 6] & ((1ull << (e & 63)) - 1ull)) : 0ull;
-  return wpre[e >> 6] + (uint32_t)__popcll(below);
+__device__ __forceinline__ uint64_t ld_nc_u64(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.global.nc.u64 %0, [%1];" : "=l"(v) : "l"(p));
+  return v;
 }
 
 template <typename T>
@@ -92,25 +89,37 @@ __device__ __forceinline__ T block_excl_scan(T v, T* scratch, T* total) {
   return r;
 }
 
-// Load the 64 words of tile t and their exclusive popcount prefix into smem.
-// Must be called by all threads; ends with a barrier.
-__device__ __forceinline__ void load_tile_words(const uint64_t* __restrict__ words, uint64_t nwords,
-                                                uint64_t t, uint64_t* sw, uint32_t* wpre) {
-  const int tid = threadIdx.x;
-  if (tid < kTileWords) {
-    const uint64_t wi = t * kTileWords + tid;
-    sw[tid] = wi < nwords ? __ldg(words + wi) : 0ull;
-  }
-  __syncthreads();
-  if (tid < 32) {
-    const uint32_t c0 = __popcll(sw[2 * tid]), c1 = __popcll(sw[2 * tid + 1]);
-    const uint32_t s = c0 + c1;
-    const uint32_t inc = warp_incl_scan(s);
-    wpre[2 * tid] = inc - s;
-    wpre[2 * tid + 1] = inc - s + c0;
-    if (tid == 31) wpre[64] = inc;
-  }
-  __syncthreads();
+// A warp's view of one 1024-element chunk: lane l < 16 holds word l and its
+// exclusive popcount prefix; lane l's j-th float4 slot covers elements
+// 128*j + 4*l .. +3, i.e. nibble 4*(l&15) of word 2*j + (l>>4).
+struct ChunkMask {
+  uint64_t w;      // lane's own word (lanes 0..15)
+  uint32_t excl;   // exclusive prefix of popcounts (lanes 0..15)
+  uint32_t total;  // kept elements in the chunk (all lanes)
+};
+
+__device__ __forceinline__ ChunkMask load_chunk_mask(const uint64_t* __restrict__ words,
+                                                     uint64_t nwords, uint64_t c) {
+  const int lane = threadIdx.x & 31;
+  ChunkMask m;
+  const uint64_t wi = c * kChunkWords + lane;
+  m.w = (lane < kChunkWords && wi < nwords) ? ld_nc_u64(words + wi) : 0ull;
+  const uint32_t pc = (uint32_t)__popcll(m.w);
+  const uint32_t inc = warp_incl_scan(pc);
+  m.excl = inc - pc;
+  m.total = __shfl_sync(0xffffffffu, inc, 31);
+  return m;
+}
+
+// nibble and in-chunk rank of lane's slot j
+__device__ __forceinline__ void slot_of(const ChunkMask& m, int j, uint32_t& nib, uint32_t& pos) {
+  const int lane = threadIdx.x & 31;
+  const int wi = 2 * j + (lane >> 4);
+  const uint64_t w = __shfl_sync(0xffffffffu, m.w, wi);
+  const uint32_t ex = __shfl_sync(0xffffffffu, m.excl, wi);
+  const int sh = 4 * (lane & 15);
+  nib = (uint32_t)(w >> sh) & 0xFu;
+  pos = ex + (uint32_t)__popcll(sh ? (w & ((1ull << sh) - 1ull)) : 0ull);
 }
 
 }  // namespace pactk

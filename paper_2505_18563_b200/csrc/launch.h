@@ -1,28 +1,30 @@
 // launch.h -- host-callable launchers of the sm_100a kernels (internal).
 #pragma once
 
+#include <cstddef>
 #include <cstdint>
 #include <cuda_runtime.h>
 
 namespace pactk {
 
 // ---- codec.cu --------------------------------------------------------------
-// tile range [tb, te) of ntiles; all pointers device.
-void launch_pack(const float* g, uint64_t len, const uint64_t* words, const uint32_t* tile_off,
-                 float* packed, uint64_t tb, uint64_t te, cudaStream_t s);
+// chunk range [cb, ce) of 1024-element chunks; all pointers device.
+void launch_pack(const float* g, uint64_t len, const uint64_t* words, const uint32_t* chunk_off,
+                 float* packed, uint64_t cb, uint64_t ce, cudaStream_t s);
 void launch_unpack(const float* packed, uint64_t len, const uint64_t* words,
-                   const uint32_t* tile_off, float scale, int do_scale, float* out, uint64_t tb,
-                   uint64_t te, cudaStream_t s);
+                   const uint32_t* chunk_off, float scale, int do_scale, float* out, uint64_t cb,
+                   uint64_t ce, cudaStream_t s);
 void launch_unpack_sgd(const float* packed, uint64_t len, const uint64_t* words,
-                       const uint32_t* tile_off, float scale, int do_scale, float lr,
+                       const uint32_t* chunk_off, float scale, int do_scale, float lr,
                        float* grad_out, float* weights, cudaStream_t s);
 void launch_scale(const float* in, float* out, uint64_t len, float scale, cudaStream_t s);
 void launch_gse(const float* g, uint64_t len, const uint64_t* words, float* out, cudaStream_t s);
-void launch_mask_fill(uint64_t* words, uint64_t len, int keep, uint32_t* tile_off, cudaStream_t s);
+void launch_mask_fill(uint64_t* words, uint64_t len, int keep, uint32_t* chunk_off, cudaStream_t s);
 void launch_clear_tail(uint64_t* words, uint64_t len, cudaStream_t s);
-void launch_tile_popc(const uint64_t* words, uint64_t len, uint32_t* tile_popc, cudaStream_t s);
-// exclusive scan of n u32 -> out[0..n], out[n] = total
-void launch_scan_excl(const uint32_t* in, uint64_t n, uint32_t* out, cudaStream_t s);
+void launch_tile_popc(const uint64_t* words, uint64_t len, uint32_t* chunk_popc, cudaStream_t s);
+// exclusive scan of n u32 -> out[0..n], out[n] = total (single pass, look-back)
+size_t scan_scratch_bytes(uint64_t n);
+void launch_scan_excl(const uint32_t* in, uint64_t n, uint32_t* out, void* scratch, cudaStream_t s);
 // count of kernels launched by these launchers (process-wide, for gpu_launches)
 uint64_t launches();
 void note_launch(uint64_t n = 1);
@@ -33,6 +35,10 @@ struct PruneWindow {
 };
 struct PruneCounts {  // device-side accumulators (zeroed by the launcher)
   unsigned long long n_lt, n_eq_lo, n_eq_hi, n_mid;
+};
+struct BitmapCounts {  // zeroed by launch_prune_bitmap
+  unsigned long long n_lt, n_eq;
+  int changed, tie_mismatch;
 };
 // 1 CTA: strided sample of keys, sorted; writes the [lo, hi] window.
 void launch_prune_sample(const float* w, uint64_t len, uint64_t k, PruneWindow* win_dev,
@@ -46,12 +52,18 @@ void launch_prune_count(const float* w, uint64_t len, const PruneWindow* win_dev
 // u32 keys. hist (1<<nbits u32) is zeroed by the launcher.
 void launch_prune_hist(const void* src, int from_float, uint64_t n, uint32_t base, int shift,
                        int nbits, uint32_t prefix, uint32_t* hist, cudaStream_t s);
-// final pass: words (in place, compared to their old content), per-tile kept
-// counts, changed flag; ties at T dropped lowest-index-first via a decoupled
-// look-back over the tie counts. ws_state: ntiles u64 + 1 u32 counter, zeroed
-// by the launcher.
-void launch_prune_bitmap(const float* w, uint64_t len, uint32_t T, uint64_t r, uint64_t* words,
-                         uint32_t* tile_popc, int* changed, uint64_t* ws_state, cudaStream_t s);
+// full read: words (written only where they change) + per-chunk kept counts;
+// ties resolved against tie_prefix (per chunk) or all dropped if it is null;
+// per-chunk tie counts -> ties_out (compared with ties_prev when given), tie
+// bits of chunks with ties -> tie_words; global #(key<T), #(key==T).
+void launch_prune_bitmap(const float* w, uint64_t len, uint32_t T, uint64_t r,
+                         const uint32_t* tie_prefix, uint64_t* words, uint32_t* chunk_popc,
+                         uint32_t* ties_out, const uint32_t* ties_prev, uint64_t* tie_words,
+                         BitmapCounts* counts, cudaStream_t s);
+// exact tie bits from the exact tie prefix; updates chunk_popc of tie chunks
+void launch_prune_tiefix(uint64_t* words, uint64_t len, const uint64_t* tie_words,
+                         const uint32_t* ties, const uint32_t* tie_prefix, uint64_t r,
+                         uint32_t* chunk_popc, cudaStream_t s);
 
 // ---- digest.cu -------------------------------------------------------------
 // FNV-1a-64 over the LE bytes of nwords words; scratch sized by

@@ -146,6 +146,14 @@ struct pact_mask {
   int changed = 1;
   std::vector<uint32_t> host_tile_off;  // lazily mirrored (bucket planning)
   int host_tile_off_valid = 0;
+  // prune state kept for the next call (temporal reuse of the threshold)
+  DevBuf tie_words;   // nwords u64: tie bits of chunks that had ties
+  DevBuf ties[2];     // per-chunk tie counts, double buffered
+  DevBuf tie_prefix;  // nchunks + 1 exclusive prefix of ties[cur]
+  int ties_cur = 0;
+  int spec_valid = 0;
+  uint64_t spec_k = 0, spec_c_lt = 0;
+  uint32_t spec_T = 0;
 };
 
 struct pact_comm {
@@ -168,6 +176,7 @@ struct Small {
   int changed;
   int pad1[3];
   uint32_t hist[2048];
+  pactk::BitmapCounts bcounts;
 };
 
 pact_status set_device(pact_ctx* ctx) {
@@ -196,9 +205,15 @@ cudaEvent_t pool_event(pact_ctx* ctx, size_t i) {
 }
 
 // recompute tile offsets + nnz from the mask words (device), sync
+pact_status scan(pact_ctx* ctx, const uint32_t* in, uint64_t n, uint32_t* out, cudaStream_t s) {
+  TRY(ctx->state.ensure(pactk::scan_scratch_bytes(n)));
+  pactk::launch_scan_excl(in, n, out, ctx->state.p, s);
+  return PACT_OK;
+}
+
 pact_status refresh_offsets(pact_mask* m, cudaStream_t s) {
   pactk::launch_tile_popc(m->words, m->len, m->tile_popc, s);
-  pactk::launch_scan_excl(m->tile_popc, m->ntiles, m->tile_off, s);
+  TRY(scan(m->ctx, m->tile_popc, m->ntiles, m->tile_off, s));
   uint32_t* pin = m->ctx->pin.as<uint32_t>();
   CUDA_TRY(cudaMemcpyAsync(pin, m->tile_off + m->ntiles, 4, cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaStreamSynchronize(s));
@@ -414,7 +429,9 @@ pact_status pact_mask_create(pact_ctx* ctx, uint64_t len, pact_mask** out) {
   m->len = len;
   m->nwords = word_count(len);
   m->ntiles = tile_count(len);
-  const size_t wb = std::max<uint64_t>(1, m->nwords) * 8;
+  // words padded (zero) to whole 16-word chunks: the codec kernels read a
+  // chunk's words as 16-byte pairs without bounds checks
+  const size_t wb = std::max<uint64_t>(1, m->ntiles) * (PACT_TILE / 64) * 8;
   const size_t tb = (m->ntiles + 1) * 4, pb = std::max<uint64_t>(1, m->ntiles) * 4;
   if (cudaMalloc(&m->words, wb) != cudaSuccess || cudaMalloc(&m->tile_off, tb) != cudaSuccess ||
       cudaMalloc(&m->tile_popc, pb) != cudaSuccess) {
@@ -439,6 +456,10 @@ pact_status pact_mask_destroy(pact_mask* m) {
   if (m->words) cudaFree(m->words);
   if (m->tile_off) cudaFree(m->tile_off);
   if (m->tile_popc) cudaFree(m->tile_popc);
+  m->tie_words.release();
+  m->ties[0].release();
+  m->ties[1].release();
+  m->tie_prefix.release();
   delete m;
   return PACT_OK;
 }
@@ -467,6 +488,7 @@ pact_status pact_mask_fill(pact_mask* m, int keep, pact_stream_t stream) {
   m->changed = !same;
   m->nnz = want;
   m->digest_valid = 0;
+  m->spec_valid = 0;
   m->host_tile_off_valid = 0;
   return PACT_OK;
 }
@@ -486,6 +508,7 @@ pact_status pact_mask_set_words(pact_mask* m, const uint64_t* words_dev, pact_st
   CUDA_TRY(cudaGetLastError());
   m->changed = 1;
   m->digest_valid = 0;
+  m->spec_valid = 0;
   return PACT_OK;
 }
 
@@ -569,86 +592,149 @@ pact_status pact_prune_magnitude(pact_ctx* ctx, const float* w, uint64_t len, fl
   }
   if (k == 0 || k >= len) {  // nothing / everything dropped
     TRY(pact_mask_fill(out, k == 0 ? 1 : 0, s));
-    st.path = 0;
-    st.threshold = 0;
     if (stats) *stats = st;
     return PACT_OK;
   }
+  const uint64_t nc = out->ntiles;
+  TRY(out->tie_words.ensure(out->nwords * 8));
+  TRY(out->ties[0].ensure(nc * 4));
+  TRY(out->ties[1].ensure(nc * 4));
+  TRY(out->tie_prefix.ensure((nc + 1) * 4));
   Small* sm = ctx->ws_small.as<Small>();
-  const uint64_t cap = std::max<uint64_t>(1u << 20, len / 16);
-  TRY(ctx->cand.ensure(cap * 4));
-  TRY(ctx->state.ensure(out->ntiles * 8 + 64));
+  pactk::BitmapCounts* bc = &sm->bcounts;
+  pactk::BitmapCounts hb{};
+  const int had_digest = out->digest_valid;
+  int changed = 0;
+  bool done = false;
 
-  // (1) sampled window, (2) counting pass
-  pactk::launch_prune_sample(w, len, k, &sm->win, s);
-  pactk::launch_prune_count(w, len, &sm->win, &sm->counts, ctx->cand.as<uint32_t>(), cap, s);
-  CUDA_TRY(cudaGetLastError());
-  struct {
-    pactk::PruneWindow win;
-    uint32_t pad[2];
-    pactk::PruneCounts c;
-  } h;
-  static_assert(sizeof(h) == offsetof(Small, digest), "layout");
-  void* pin = ctx->pin.p;
-  CUDA_TRY(cudaMemcpyAsync(pin, sm, sizeof(h), cudaMemcpyDeviceToHost, s));
-  CUDA_TRY(cudaStreamSynchronize(s));
-  std::memcpy(&h, pin, sizeof(h));
-  const uint64_t lo_end = h.c.n_lt + h.c.n_eq_lo;
-  const uint64_t mid_end = lo_end + h.c.n_mid;
-  const uint64_t hi_end = mid_end + h.c.n_eq_hi;
-  uint32_t T = 0;
-  uint64_t c_lt = 0;
-  bool fallback = false;
-  st.candidates = h.c.n_mid;
-  if (k <= h.c.n_lt || k > hi_end) {
-    fallback = true;
-  } else if (k <= lo_end) {
-    T = h.win.lo;
-    c_lt = h.c.n_lt;
-  } else if (k <= mid_end) {
-    if (h.c.n_mid > cap) {
-      fallback = true;
+  // one bitmap pass at (T, r); tie prefix from the previous call (spec) or
+  // "all ties dropped" (prefix null); returns the pass's own counts
+  auto bitmap = [&](uint32_t T, uint64_t r, bool use_prefix, bool compare_prev) -> pact_status {
+    const int nxt = out->ties_cur ^ 1;
+    pactk::launch_prune_bitmap(w, len, T, r, use_prefix ? out->tie_prefix.as<uint32_t>() : nullptr,
+                               out->words, out->tile_popc, out->ties[nxt].as<uint32_t>(),
+                               compare_prev ? out->ties[out->ties_cur].as<uint32_t>() : nullptr,
+                               out->tie_words.as<uint64_t>(), bc, s);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaMemcpyAsync(ctx->pin.p, bc, sizeof hb, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    std::memcpy(&hb, ctx->pin.p, sizeof hb);
+    out->ties_cur = nxt;
+    changed |= hb.changed;
+    return PACT_OK;
+  };
+  // exact tie bits once the true (T, r) and per-chunk tie counts are known
+  auto fix_ties = [&](uint64_t r) -> pact_status {
+    const uint32_t* ties = out->ties[out->ties_cur].as<uint32_t>();
+    TRY(scan(ctx, ties, nc, out->tie_prefix.as<uint32_t>(), s));
+    pactk::launch_prune_tiefix(out->words, len, out->tie_words.as<uint64_t>(), ties,
+                               out->tie_prefix.as<uint32_t>(), r, out->tile_popc, s);
+    CUDA_TRY(cudaGetLastError());
+    changed = 1;  // conservative: the digest is recomputed on demand
+    return PACT_OK;
+  };
+
+  // (0) temporal reuse: previous threshold, verified by the pass itself
+  if (out->spec_valid && out->spec_k == k) {
+    const uint64_t r0 = k - out->spec_c_lt;
+    TRY(bitmap(out->spec_T, r0, true, true));
+    if (hb.n_lt < k && k <= hb.n_lt + hb.n_eq) {  // threshold still the k-th key
+      const uint64_t r = k - hb.n_lt;
+      if (r != r0 || hb.tie_mismatch) TRY(fix_ties(r));
+      st.path = 3;
+      st.threshold = out->spec_T;
+      st.c_lt = hb.n_lt;
+      out->spec_c_lt = hb.n_lt;
+      done = true;
     } else {
-      // (3) exact select among the window-interior keys
-      const uint32_t base = h.win.lo + 1;
-      const int bits = bit_length(h.win.hi - h.win.lo - 2);
+      changed = 1;
+    }
+  }
+
+  if (!done) {
+    const uint64_t cap = std::max<uint64_t>(1u << 20, len / 16);
+    TRY(ctx->cand.ensure(cap * 4));
+    // (1) sampled window, (2) counting pass
+    pactk::launch_prune_sample(w, len, k, &sm->win, s);
+    pactk::launch_prune_count(w, len, &sm->win, &sm->counts, ctx->cand.as<uint32_t>(), cap, s);
+    CUDA_TRY(cudaGetLastError());
+    struct {
+      pactk::PruneWindow win;
+      uint32_t pad[2];
+      pactk::PruneCounts c;
+    } h;
+    static_assert(sizeof(h) == offsetof(Small, digest), "layout");
+    CUDA_TRY(cudaMemcpyAsync(ctx->pin.p, sm, sizeof(h), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    std::memcpy(&h, ctx->pin.p, sizeof(h));
+    const uint64_t lo_end = h.c.n_lt + h.c.n_eq_lo;
+    const uint64_t mid_end = lo_end + h.c.n_mid;
+    const uint64_t hi_end = mid_end + h.c.n_eq_hi;
+    uint32_t T = 0;
+    uint64_t c_lt = 0;
+    bool fallback = false;
+    st.candidates = h.c.n_mid;
+    if (k <= h.c.n_lt || k > hi_end) {
+      fallback = true;
+    } else if (k <= lo_end) {
+      T = h.win.lo;
+      c_lt = h.c.n_lt;
+    } else if (k <= mid_end) {
+      if (h.c.n_mid > cap) {
+        fallback = true;
+      } else {  // (3) exact select among the window-interior keys
+        const uint32_t base = h.win.lo + 1;
+        const int bits = bit_length(h.win.hi - h.win.lo - 2);
+        uint32_t rel = 0;
+        uint64_t below = 0;
+        if (bits > 0)
+          TRY(select_rank(ctx, ctx->cand.p, 0, h.c.n_mid, base, bits, k - lo_end, s, &rel, &below));
+        T = base + rel;
+        c_lt = lo_end + below;
+      }
+    } else {
+      T = h.win.hi;
+      c_lt = mid_end;
+    }
+    st.path = fallback ? 2 : 1;
+    if (fallback) {  // exact radix select over the whole array
       uint32_t rel = 0;
       uint64_t below = 0;
-      if (bits > 0)
-        TRY(select_rank(ctx, ctx->cand.p, 0, h.c.n_mid, base, bits, k - lo_end, s, &rel, &below));
-      T = base + rel;
-      c_lt = lo_end + below;
+      TRY(select_rank(ctx, w, 1, len, 0, 31, k, s, &rel, &below));
+      T = rel;
+      c_lt = below;
     }
-  } else {
-    T = h.win.hi;
-    c_lt = mid_end;
+    st.threshold = T;
+    st.c_lt = c_lt;
+    // (4) bitmap, ties provisionally all dropped; exact when r == E
+    const uint64_t r = k - c_lt;
+    TRY(bitmap(T, r, false, false));
+    if (hb.n_lt != c_lt || !(c_lt < k && k <= hb.n_lt + hb.n_eq))
+      return fail(PACT_E_RUN_FAILURE, "prune threshold inconsistent (T=%u c_lt=%llu n_lt=%llu n_eq=%llu k=%llu)",
+                  T, (unsigned long long)c_lt, (unsigned long long)hb.n_lt,
+                  (unsigned long long)hb.n_eq, (unsigned long long)k);
+    if (r < hb.n_eq) {
+      TRY(fix_ties(r));  // ties straddle r
+    } else {
+      TRY(scan(ctx, out->ties[out->ties_cur].as<uint32_t>(), nc, out->tie_prefix.as<uint32_t>(), s));
+    }
+    out->spec_valid = 1;
+    out->spec_k = k;
+    out->spec_T = T;
+    out->spec_c_lt = c_lt;
   }
-  st.path = fallback ? 2 : 1;
-  if (fallback) {  // exact radix select over the whole array
-    uint32_t rel = 0;
-    uint64_t below = 0;
-    TRY(select_rank(ctx, w, 1, len, 0, 31, k, s, &rel, &below));
-    T = rel;
-    c_lt = below;
-  }
-  st.threshold = T;
-  st.c_lt = c_lt;
 
-  // (4) bitmap with tie ranks, then tile offsets
-  const int had_digest = out->digest_valid;
-  Small* smd = sm;
-  pactk::launch_prune_bitmap(w, len, T, k - c_lt, out->words, out->tile_popc, &smd->changed,
-                             ctx->state.as<uint64_t>(), s);
-  pactk::launch_scan_excl(out->tile_popc, out->ntiles, out->tile_off, s);
-  CUDA_TRY(cudaGetLastError());
-  uint32_t* pin32 = ctx->pin.as<uint32_t>();
-  CUDA_TRY(cudaMemcpyAsync(pin32, out->tile_off + out->ntiles, 4, cudaMemcpyDeviceToHost, s));
-  CUDA_TRY(cudaMemcpyAsync(pin32 + 1, &smd->changed, 4, cudaMemcpyDeviceToHost, s));
-  CUDA_TRY(cudaStreamSynchronize(s));
-  out->nnz = pin32[0];
-  out->changed = pin32[1] != 0;
-  out->host_tile_off_valid = out->host_tile_off_valid && !out->changed;
-  out->digest_valid = had_digest && !out->changed;
+  // (5) chunk offsets (unchanged words keep their offsets)
+  out->changed = changed;
+  if (changed || out->nnz != len - k) {
+    TRY(scan(ctx, out->tile_popc, nc, out->tile_off, s));
+    uint32_t* pin32 = ctx->pin.as<uint32_t>();
+    CUDA_TRY(cudaMemcpyAsync(pin32, out->tile_off + nc, 4, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    out->nnz = pin32[0];
+    out->host_tile_off_valid = 0;
+  }
+  out->digest_valid = had_digest && !changed;
   if (out->nnz != len - k)
     return fail(PACT_E_RUN_FAILURE, "prune kept %llu, expected %llu", (unsigned long long)out->nnz,
                 (unsigned long long)(len - k));

@@ -3,24 +3,29 @@
 // The reference stable-sorts an index array by |w| and drops the first k
 // positions: the k smallest (|w_i|, i) pairs, ties at the threshold dropped
 // lowest-index first. With key = bits(w) & 0x7fffffff (monotone in |w| for
-// finite values, +0/-0 tie) that is:
+// finite values, +0/-0 tie) that is exactly:
 //
-//   T    = k-th smallest key,  c_lt = #(key < T),  r = k - c_lt
+//   T = k-th smallest key,  c_lt = #(key < T),  r = k - c_lt  (1 <= r <= E)
 //   bit_i = key_i > T  ||  (key_i == T  &&  tierank_i >= r)
 //
-// where tierank_i = #{j < i : key_j == T}. The selection of T is
-// sample-guided so the dense array is streamed only twice:
-//   1. prune_sample  (1 CTA): 16384 strided keys, bitonic-sorted in smem;
-//      a [lo, hi] window of +-6 sigma around the expected rank of the k-th key.
-//   2. prune_count   (full read): #(key<lo), #(key==lo), #(key==hi), and the
-//      window-interior keys compacted to a small candidate buffer.
-//   3. prune_hist    (only if T is strictly inside the window): radix-select
-//      digits over the candidate buffer (L2 resident).
-//   4. prune_bitmap  (full read): mask words + per-tile kept counts; the
-//      tie ranks come from a decoupled look-back over per-tile tie counts.
-// If the window misses (sample unrepresentative) or the candidate buffer
-// overflows, step 3 runs over the full array instead (3 digit passes); the
-// result is identical, only slower.
+// with E = #(key == T) and tierank_i = #{j < i : key_j == T}.
+//
+// Kernels (one warp owns one 1024-element chunk; persistent grids):
+//   prune_sample   1 CTA: 16384 strided keys, register bitonic sort, a
+//                  +-6 sigma window [lo, hi] around the k-th key's rank.
+//   prune_count    full read: #(key<lo), #(key==lo), #(key==hi); keys strictly
+//                  inside the window go to a small candidate buffer.
+//   prune_hist     radix-select digits over the candidates (L2 resident) or,
+//                  if the window missed, over the whole array.
+//   prune_bitmap   full read: mask words with ties resolved against a given
+//                  per-chunk tie prefix (or all ties dropped when r == E);
+//                  records per-chunk tie counts, the tie bits, #(key<T),
+//                  #(key==T), and whether any word changed.
+//   prune_tiefix   only when ties straddle r: rewrites the tie bits from the
+//                  exact prefix (reads the small tie bitmap, never w).
+// Temporal reuse (C5 re-pruning): the previous call's (T, c_lt, tie prefix)
+// is tried first; the bitmap pass verifies it from its own counts, so an
+// unchanged threshold costs ONE read of w. On a miss the full path runs.
 #include "common.cuh"
 #include "launch.h"
 
@@ -29,6 +34,7 @@ namespace pactk {
 namespace {
 
 constexpr int kSample = 16384;
+constexpr int kPruneWarps = 8;  // 256-thread CTAs for count / bitmap
 
 int num_sms() {
   static int sms = 0;
@@ -41,34 +47,122 @@ int num_sms() {
   return sms;
 }
 
+template <typename K>
+unsigned persistent_grid(K kernel, int threads, size_t smem, uint64_t work_units, int units_per_cta) {
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem);
+  if (per_sm <= 0) per_sm = 1;
+  const uint64_t cap = (uint64_t)num_sms() * per_sm;
+  const uint64_t need = (work_units + units_per_cta - 1) / units_per_cta;
+  return (unsigned)(need < cap ? (need ? need : 1) : cap);
+}
+
+// load lane's 8 float4 slots of chunk c (keys), in-range mask per slot
+__device__ __forceinline__ void load_chunk_keys(const float* __restrict__ w, uint64_t len, uint64_t c,
+                                                bool vec_ok, uint32_t key[kVecPerLane][4],
+                                                uint32_t inr[kVecPerLane]) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t e0 = c * (uint64_t)kChunk + 4 * lane;
+  float4 v[kVecPerLane];
+#pragma unroll
+  for (int j = 0; j < kVecPerLane; ++j) {
+    const uint64_t ge = e0 + 128 * j;
+    v[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (vec_ok && ge + 4 <= len) {
+      v[j] = ld_stream_f4(reinterpret_cast<const float4*>(w + ge));
+      inr[j] = 0xF;
+    } else {
+      inr[j] = 0;
+      for (int b = 0; b < 4; ++b)
+        if (ge + b < len) {
+          (&v[j].x)[b] = w[ge + b];
+          inr[j] |= 1u << b;
+        }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < kVecPerLane; ++j) {
+    key[j][0] = mag_key(v[j].x);
+    key[j][1] = mag_key(v[j].y);
+    key[j][2] = mag_key(v[j].z);
+    key[j][3] = mag_key(v[j].w);
+  }
+}
+
 // ---------------------------------------------------------------- sample
+// 16384 keys, 16 per thread in registers; bitonic network: in-register for
+// strides < 16, warp shuffles for strides < 512, shared memory above.
+__device__ __forceinline__ void cswap(uint32_t& a, uint32_t& b, bool asc) {
+  const uint32_t lo = min(a, b), hi = max(a, b);
+  a = asc ? lo : hi;
+  b = asc ? hi : lo;
+}
+
 __global__ void __launch_bounds__(1024, 1)
     prune_sample_kernel(const float* __restrict__ w, uint64_t len, uint64_t k,
                         PruneWindow* __restrict__ win) {
   extern __shared__ uint32_t s[];
-  const int tid = threadIdx.x;
-  for (int i = tid; i < kSample; i += 1024) {
-    const uint64_t idx = ((uint64_t)i * len + len / 2) / kSample;  // < len
-    s[i] = mag_key(w[idx]);
+  const int t = threadIdx.x;
+  uint32_t r[16];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    const uint64_t i = (uint64_t)t * 16 + q;
+    r[q] = mag_key(w[(i * len + len / 2) / kSample]);
   }
-  __syncthreads();
-  for (int kk = 2; kk <= kSample; kk <<= 1) {
+  // stages with k <= 16: entirely in registers
+#pragma unroll
+  for (int kk = 2; kk <= 16; kk <<= 1) {
+#pragma unroll
     for (int j = kk >> 1; j > 0; j >>= 1) {
-      for (int i = tid; i < kSample; i += 1024) {
-        const int ixj = i ^ j;
-        if (ixj > i) {
-          const uint32_t a = s[i], b = s[ixj];
-          const bool asc = (i & kk) == 0;
-          if ((a > b) == asc) {
-            s[i] = b;
-            s[ixj] = a;
-          }
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        if ((q & j) == 0) {
+          const uint32_t i = (uint32_t)t * 16 + q;
+          cswap(r[q], r[q | j], (i & kk) == 0);
         }
       }
-      __syncthreads();
     }
   }
-  if (tid == 0) {
+  for (int kk = 32; kk <= kSample; kk <<= 1) {
+    for (int j = kk >> 1; j >= 16; j >>= 1) {
+      if (j >= 512) {
+#pragma unroll
+        for (int q = 0; q < 16; ++q) s[t * 16 + q] = r[q];
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          const uint32_t i = (uint32_t)t * 16 + q;
+          const uint32_t o = s[i ^ j];
+          const bool asc = (i & kk) == 0, lower = (i & j) == 0;
+          r[q] = (lower == asc) ? min(r[q], o) : max(r[q], o);
+        }
+        __syncthreads();
+      } else {
+        const int lanemask = j >> 4;
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          const uint32_t i = (uint32_t)t * 16 + q;
+          const uint32_t o = __shfl_xor_sync(0xffffffffu, r[q], lanemask);
+          const bool asc = (i & kk) == 0, lower = (i & j) == 0;
+          r[q] = (lower == asc) ? min(r[q], o) : max(r[q], o);
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 8; j > 0; j >>= 1) {
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        if ((q & j) == 0) {
+          const uint32_t i = (uint32_t)t * 16 + q;
+          cswap(r[q], r[q | j], (i & kk) == 0);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 16; ++q) s[t * 16 + q] = r[q];
+  __syncthreads();
+  if (t == 0) {
     const double p = (double)k / (double)len;
     const double center = ((double)k - 0.5) / (double)len * kSample;
     const double margin = 6.0 * sqrt(kSample * p * (1.0 - p)) + 8.0;
@@ -82,70 +176,70 @@ __global__ void __launch_bounds__(1024, 1)
 }
 
 // ----------------------------------------------------------------- count
-__global__ void __launch_bounds__(kThreads)
+__device__ __forceinline__ void flush_cands(uint32_t* buf, uint32_t fill, PruneCounts* counts,
+                                            uint32_t* __restrict__ cand, uint64_t cap) {
+  const int lane = threadIdx.x & 31;
+  unsigned long long base = 0;
+  if (lane == 0) base = atomicAdd(&counts->n_mid, (unsigned long long)fill);
+  base = __shfl_sync(0xffffffffu, base, 0);
+  for (uint32_t i = lane; i < fill; i += 32)
+    if (base + i < cap) cand[base + i] = buf[i];
+  __syncwarp();
+}
+
+__global__ void __launch_bounds__(kPruneWarps * 32)
     prune_count_kernel(const float* __restrict__ w, uint64_t len, const PruneWindow* __restrict__ win,
                        PruneCounts* __restrict__ counts, uint32_t* __restrict__ cand,
-                       uint64_t cap, uint64_t ntiles) {
-  __shared__ unsigned long long scratch[kThreads / 32 + 1];
-  __shared__ unsigned long long s_base;
-  const int tid = threadIdx.x;
+                       uint64_t cap, uint64_t nchunks) {
+  __shared__ uint32_t cbuf_all[kPruneWarps][kChunk];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t* buf = cbuf_all[warp];
   const uint32_t lo = win->lo, hi = win->hi;
   const bool vec_ok = (((uintptr_t)w) & 15) == 0;
-  uint32_t c_lt = 0, c_eqlo = 0, c_eqhi = 0;
-  for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    const uint64_t e0 = t * (uint64_t)kTile;
-    uint32_t key[kVecPerThread * 4];
-    uint32_t inr = 0;  // in-range bits
+  uint32_t c_lt = 0, c_eqlo = 0, c_eqhi = 0, fill = 0;
+  const uint64_t nw_total = (uint64_t)gridDim.x * kPruneWarps;
+  for (uint64_t c = (uint64_t)blockIdx.x * kPruneWarps + warp; c < nchunks; c += nw_total) {
+    uint32_t key[kVecPerLane][4], inr[kVecPerLane];
+    load_chunk_keys(w, len, c, vec_ok, key, inr);
+    uint32_t nmid = 0;
 #pragma unroll
-    for (int j = 0; j < kVecPerThread; ++j) {
-      const uint64_t ge = e0 + (uint64_t)(j * kThreads + tid) * 4;
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (vec_ok && ge + 4 <= len) {
-        v = ld_stream_f4(reinterpret_cast<const float4*>(w + ge));
-        inr |= 0xFu << (4 * j);
-      } else {
-        for (int b = 0; b < 4; ++b)
-          if (ge + b < len) {
-            (&v.x)[b] = w[ge + b];
-            inr |= 1u << (4 * j + b);
-          }
+    for (int j = 0; j < kVecPerLane; ++j)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const bool in = (inr[j] >> b) & 1;
+        const uint32_t kq = key[j][b];
+        c_lt += in && kq < lo;
+        c_eqlo += in && kq == lo;
+        c_eqhi += in && kq == hi && hi != lo;
+        nmid += in && kq > lo && kq < hi;
       }
-      key[4 * j + 0] = mag_key(v.x);
-      key[4 * j + 1] = mag_key(v.y);
-      key[4 * j + 2] = mag_key(v.z);
-      key[4 * j + 3] = mag_key(v.w);
+    const uint32_t inc = warp_incl_scan(nmid);
+    const uint32_t tot = __shfl_sync(0xffffffffu, inc, 31);
+    if (tot == 0) continue;
+    if (fill + tot > kChunk) {
+      flush_cands(buf, fill, counts, cand, cap);
+      fill = 0;
     }
-    uint32_t mid = 0;
+    uint32_t o = fill + inc - nmid;
 #pragma unroll
-    for (int q = 0; q < kVecPerThread * 4; ++q) {
-      const bool in = (inr >> q) & 1;
-      const uint32_t kq = key[q];
-      c_lt += in && kq < lo;
-      c_eqlo += in && kq == lo;
-      c_eqhi += in && kq == hi && hi != lo;
-      if (in && kq > lo && kq < hi) mid |= 1u << q;
-    }
-    unsigned long long tot;
-    const unsigned long long off = block_excl_scan<unsigned long long>(__popc(mid), scratch, &tot);
-    if (tot) {
-      if (tid == 0) s_base = atomicAdd(&counts->n_mid, tot);
-      __syncthreads();
-      unsigned long long o = s_base + off;
-      for (int q = 0; q < kVecPerThread * 4; ++q)
-        if ((mid >> q) & 1) {
-          if (o < cap) cand[o] = key[q];
-          ++o;
-        }
-      __syncthreads();
-    }
+    for (int j = 0; j < kVecPerLane; ++j)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const uint32_t kq = key[j][b];
+        if (((inr[j] >> b) & 1) && kq > lo && kq < hi) buf[o++] = kq;
+      }
+    __syncwarp();
+    fill += tot;
   }
-  unsigned long long tot;
-  block_excl_scan<unsigned long long>(c_lt, scratch, &tot);
-  if (tid == 0 && tot) atomicAdd(&counts->n_lt, tot);
-  block_excl_scan<unsigned long long>(c_eqlo, scratch, &tot);
-  if (tid == 0 && tot) atomicAdd(&counts->n_eq_lo, tot);
-  block_excl_scan<unsigned long long>(c_eqhi, scratch, &tot);
-  if (tid == 0 && tot) atomicAdd(&counts->n_eq_hi, tot);
+  if (fill) flush_cands(buf, fill, counts, cand, cap);
+  c_lt = warp_sum(c_lt);
+  c_eqlo = warp_sum(c_eqlo);
+  c_eqhi = warp_sum(c_eqhi);
+  if (lane == 0) {
+    if (c_lt) atomicAdd(&counts->n_lt, (unsigned long long)c_lt);
+    if (c_eqlo) atomicAdd(&counts->n_eq_lo, (unsigned long long)c_eqlo);
+    if (c_eqhi) atomicAdd(&counts->n_eq_hi, (unsigned long long)c_eqhi);
+  }
 }
 
 // ------------------------------------------------------------------ hist
@@ -176,145 +270,157 @@ __global__ void __launch_bounds__(256)
 }
 
 // ---------------------------------------------------------------- bitmap
-constexpr uint64_t kStAgg = 1ull << 62;
-constexpr uint64_t kStIncl = 2ull << 62;
-constexpr uint64_t kStMask = 3ull << 62;
-
-__global__ void __launch_bounds__(kThreads, 4)
-    prune_bitmap_kernel(const float* __restrict__ w, uint64_t len, uint32_t T, uint64_t r,
-                        uint64_t* __restrict__ words, uint64_t nwords,
-                        uint32_t* __restrict__ tile_popc, int* __restrict__ changed,
-                        uint64_t* __restrict__ state, unsigned* __restrict__ tile_counter) {
-  __shared__ unsigned long long scratch[kThreads / 32 + 1];
-  __shared__ uint64_t sw[kTileWords];
-  __shared__ uint32_t s_tile;
-  __shared__ unsigned long long s_before;
-  __shared__ uint32_t s_pc[2];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) s_tile = atomicAdd(tile_counter, 1u);
-  __syncthreads();
-  const uint64_t t = s_tile;
-  const uint64_t e0 = t * (uint64_t)kTile;
-  const bool vec_ok = (((uintptr_t)w) & 15) == 0;
-
-  uint32_t gt = 0, eq = 0;  // bit q = 4*j + b
+// Gather the 32-bit halves of the chunk's 16 words into lanes (lane h holds
+// half h) from per-slot 4-bit nibbles (slot j of lane l -> half
+// 4j + (l >> 3), bits 4*(l & 7)).
+__device__ __forceinline__ uint32_t gather_halves(const uint32_t nib[kVecPerLane]) {
+  const int lane = threadIdx.x & 31;
+  uint32_t mine = 0;
 #pragma unroll
-  for (int j = 0; j < kVecPerThread; ++j) {
-    const uint64_t ge = e0 + (uint64_t)(j * kThreads + tid) * 4;
-    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-    uint32_t inr = 0;
-    if (vec_ok && ge + 4 <= len) {
-      v = ld_stream_f4(reinterpret_cast<const float4*>(w + ge));
-      inr = 0xF;
-    } else {
-      for (int b = 0; b < 4; ++b)
-        if (ge + b < len) {
-          (&v.x)[b] = w[ge + b];
-          inr |= 1u << b;
-        }
-    }
-#pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      const uint32_t kq = mag_key((&v.x)[b]);
-      if ((inr >> b) & 1) {
-        gt |= (uint32_t)(kq > T) << (4 * j + b);
-        eq |= (uint32_t)(kq == T) << (4 * j + b);
-      }
-    }
-  }
-  // tie counts per float4 slot j, packed in 16-bit lanes of a u64, scanned
-  // in (j, tid) order = element order within the tile
-  unsigned long long packed_cnt = 0;
-#pragma unroll
-  for (int j = 0; j < kVecPerThread; ++j)
-    packed_cnt |= (unsigned long long)__popc((eq >> (4 * j)) & 0xF) << (16 * j);
-  unsigned long long tot;
-  const unsigned long long excl = block_excl_scan<unsigned long long>(packed_cnt, scratch, &tot);
-  uint32_t slot_base[kVecPerThread];
-  uint32_t run = 0;
-#pragma unroll
-  for (int j = 0; j < kVecPerThread; ++j) {
-    slot_base[j] = run + (uint32_t)((excl >> (16 * j)) & 0xFFFF);
-    run += (uint32_t)((tot >> (16 * j)) & 0xFFFF);
-  }
-  const uint64_t E = run;  // ties in this tile
-
-  // decoupled look-back over the tie counts (plain sum; identity = 0)
-  if (warp == 0) {
-    uint64_t before = 0;
-    if (t == 0) {
-      if (lane == 0) st_relaxed_u64(state, kStIncl | E);
-    } else {
-      if (lane == 0) st_relaxed_u64(state + t, kStAgg | E);
-      int64_t base = (int64_t)t - 1;
-      while (true) {
-        const int64_t p = base - lane;
-        uint64_t s = p >= 0 ? ld_relaxed_u64(state + p) : kStIncl;
-        while (__any_sync(0xffffffffu, (s & kStMask) == 0)) {
-          if ((s & kStMask) == 0) s = ld_relaxed_u64(state + p);
-        }
-        const unsigned incl = __ballot_sync(0xffffffffu, (s & kStMask) == kStIncl);
-        const int L = incl ? __ffs(incl) - 1 : 31;
-        uint64_t v = lane <= L ? (s & ~kStMask) : 0ull;
-        v = warp_sum(v);
-        before += v;
-        if (incl) break;
-        base -= 32;
-      }
-      if (lane == 0) st_relaxed_u64(state + t, kStIncl | (before + E));
-    }
-    if (lane == 0) s_before = before;
-  }
-  __syncthreads();
-  const uint64_t before = s_before;
-
-  // final bits: keep = key > T || (key == T && tierank >= r)
-  uint32_t keep = gt;
-  if (eq) {
-#pragma unroll
-    for (int j = 0; j < kVecPerThread; ++j) {
-      uint32_t rk = slot_base[j];
-#pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        const int q = 4 * j + b;
-        if ((eq >> q) & 1) {
-          if (before + rk >= r) keep |= 1u << q;
-          ++rk;
-        }
-      }
-    }
-  }
-  // assemble words: slot j of lane l covers word 16j + 2*warp + (l >= 16),
-  // nibble 4*(l & 15)
-#pragma unroll
-  for (int j = 0; j < kVecPerThread; ++j) {
-    uint32_t x = ((keep >> (4 * j)) & 0xFu) << (4 * (lane & 7));
+  for (int j = 0; j < kVecPerLane; ++j) {
+    uint32_t x = nib[j] << (4 * (lane & 7));
     x |= __shfl_xor_sync(0xffffffffu, x, 1);
     x |= __shfl_xor_sync(0xffffffffu, x, 2);
     x |= __shfl_xor_sync(0xffffffffu, x, 4);
-    const uint32_t hi32 = __shfl_down_sync(0xffffffffu, x, 8);
-    if ((lane & 15) == 0) sw[16 * j + 2 * warp + (lane >> 4)] = (uint64_t)x | ((uint64_t)hi32 << 32);
+    const uint32_t y = __shfl_sync(0xffffffffu, x, (lane & 3) * 8);
+    if ((lane >> 2) == j) mine = y;
   }
-  __syncthreads();
-  if (tid < kTileWords) {
-    const uint64_t wi = t * kTileWords + tid;
-    const uint64_t nwv = sw[tid];
+  return mine;
+}
+
+__device__ __forceinline__ uint64_t halves_to_word(uint32_t half) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t lo = __shfl_sync(0xffffffffu, half, (2 * lane) & 31);
+  const uint32_t hi = __shfl_sync(0xffffffffu, half, (2 * lane + 1) & 31);
+  return (uint64_t)lo | ((uint64_t)hi << 32);  // meaningful for lanes 0..15
+}
+
+__global__ void __launch_bounds__(kPruneWarps * 32)
+    prune_bitmap_kernel(const float* __restrict__ w, uint64_t len, uint32_t T, uint64_t r,
+                        const uint32_t* __restrict__ tie_prefix, uint64_t* __restrict__ words,
+                        uint64_t nwords, uint32_t* __restrict__ chunk_popc,
+                        uint32_t* __restrict__ ties_out, const uint32_t* __restrict__ ties_prev,
+                        uint64_t* __restrict__ tie_words, BitmapCounts* __restrict__ counts,
+                        uint64_t nchunks) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const bool vec_ok = (((uintptr_t)w) & 15) == 0;
+  uint32_t c_lt = 0, c_eq = 0;
+  int changed = 0, mismatch = 0;
+  const uint64_t nw_total = (uint64_t)gridDim.x * kPruneWarps;
+  for (uint64_t c = (uint64_t)blockIdx.x * kPruneWarps + warp; c < nchunks; c += nw_total) {
+    uint32_t key[kVecPerLane][4], inr[kVecPerLane];
+    load_chunk_keys(w, len, c, vec_ok, key, inr);
+    uint32_t gt[kVecPerLane], eq[kVecPerLane];
+    uint32_t ne = 0;
+#pragma unroll
+    for (int j = 0; j < kVecPerLane; ++j) {
+      gt[j] = eq[j] = 0;
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const uint32_t kq = key[j][b];
+        gt[j] |= (uint32_t)(kq > T) << b;
+        eq[j] |= (uint32_t)(kq == T) << b;
+        c_lt += kq < T && ((inr[j] >> b) & 1);
+      }
+      gt[j] &= inr[j];
+      eq[j] &= inr[j];
+      ne += __popc(eq[j]);
+    }
+    c_eq += ne;
+    const uint32_t E = warp_sum(ne);
+    uint32_t keep[kVecPerLane];
+#pragma unroll
+    for (int j = 0; j < kVecPerLane; ++j) keep[j] = gt[j];
+    if (E) {
+      // in-chunk tie ranks in element order (slot j major, lane, bit)
+      uint32_t run = tie_prefix ? __ldg(tie_prefix + c) : 0u;
+#pragma unroll
+      for (int j = 0; j < kVecPerLane; ++j) {
+        const uint32_t cj = __popc(eq[j]);
+        const uint32_t inc = warp_incl_scan(cj);
+        if (tie_prefix) {
+          uint32_t rk = run + inc - cj;
+#pragma unroll
+          for (int b = 0; b < 4; ++b)
+            if ((eq[j] >> b) & 1) {
+              if ((uint64_t)rk >= r) keep[j] |= 1u << b;
+              ++rk;
+            }
+        }
+        run += __shfl_sync(0xffffffffu, inc, 31);
+      }
+      const uint64_t tw = halves_to_word(gather_halves(eq));
+      if (lane < kChunkWords && c * kChunkWords + lane < nwords) tie_words[c * kChunkWords + lane] = tw;
+    }
+    if (lane == 0) {
+      ties_out[c] = E;
+      if (ties_prev && ties_prev[c] != E) mismatch = 1;
+    }
+    const uint64_t nwv = halves_to_word(gather_halves(keep));
     uint32_t pc = 0;
-    int diff = 0;
-    if (wi < nwords) {
-      diff = words[wi] != nwv;
-      words[wi] = nwv;
-      pc = __popcll(nwv);
+    if (lane < kChunkWords) {
+      const uint64_t wi = c * kChunkWords + lane;
+      if (wi < nwords) {
+        const uint64_t old = words[wi];
+        if (old != nwv) {
+          words[wi] = nwv;
+          changed = 1;
+        }
+        pc = (uint32_t)__popcll(nwv);
+      }
     }
     pc = warp_sum(pc);
-    diff = __any_sync(0xffffffffu, diff);
-    if (lane == 0) {
-      s_pc[warp] = pc;
-      if (diff) atomicOr(changed, 1);
-    }
+    if (lane == 0) chunk_popc[c] = pc;
   }
-  __syncthreads();
-  if (tid == 0) tile_popc[t] = s_pc[0] + s_pc[1];
+  c_lt = warp_sum(c_lt);
+  c_eq = warp_sum(c_eq);
+  changed = __any_sync(0xffffffffu, changed);
+  mismatch = __any_sync(0xffffffffu, mismatch);
+  if (lane == 0) {
+    if (c_lt) atomicAdd(&counts->n_lt, (unsigned long long)c_lt);
+    if (c_eq) atomicAdd(&counts->n_eq, (unsigned long long)c_eq);
+    if (changed) atomicOr(&counts->changed, 1);
+    if (mismatch) atomicOr(&counts->tie_mismatch, 1);
+  }
+}
+
+// ----------------------------------------------------------------- tiefix
+// Rewrite the tie bits of chunks with ties: the first D = clamp(r - prefix,
+// 0, E) ties of the chunk (index order) are dropped, the rest kept.
+__global__ void __launch_bounds__(256)
+    prune_tiefix_kernel(uint64_t* __restrict__ words, uint64_t nwords,
+                        const uint64_t* __restrict__ tie_words, const uint32_t* __restrict__ ties,
+                        const uint32_t* __restrict__ tie_prefix, uint64_t r,
+                        uint32_t* __restrict__ chunk_popc, uint64_t nchunks) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t c = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  if (c >= nchunks) return;
+  const uint32_t E = ties[c];
+  if (E == 0) return;
+  const uint64_t pre = tie_prefix[c];
+  const uint64_t D = r > pre ? (r - pre < E ? r - pre : E) : 0;
+  const uint64_t wi = c * kChunkWords + lane;
+  const bool valid = lane < kChunkWords && wi < nwords;
+  const uint64_t tw = valid ? tie_words[wi] : 0ull;
+  const uint32_t tc = (uint32_t)__popcll(tw);
+  const uint32_t inc = warp_incl_scan(tc);
+  const uint64_t excl = inc - tc;
+  uint64_t d = D > excl ? D - excl : 0;
+  if (d > tc) d = tc;
+  uint64_t drop = 0, x = tw;
+  for (uint64_t n = 0; n < d; ++n) {
+    const uint64_t b = x & (~x + 1);
+    drop |= b;
+    x ^= b;
+  }
+  uint32_t pc = 0;
+  if (valid) {
+    const uint64_t nw = (words[wi] & ~tw) | (tw & ~drop);
+    words[wi] = nw;
+    pc = (uint32_t)__popcll(nw);
+  }
+  pc = warp_sum(pc);
+  if (lane == 0) chunk_popc[c] = pc;
 }
 
 }  // namespace
@@ -335,11 +441,12 @@ void launch_prune_count(const float* w, uint64_t len, const PruneWindow* win_dev
                         PruneCounts* counts_dev, uint32_t* cand, uint64_t cand_cap,
                         cudaStream_t s) {
   cudaMemsetAsync(counts_dev, 0, sizeof(PruneCounts), s);
-  const uint64_t nt = (len + kTile - 1) / kTile;
-  const uint64_t cap = (uint64_t)num_sms() * 6;
-  prune_count_kernel<<<(unsigned)(nt < cap ? nt : cap), kThreads, 0, s>>>(w, len, win_dev,
-                                                                        counts_dev, cand, cand_cap,
-                                                                        nt);
+  const uint64_t nc = (len + kChunk - 1) / kChunk;
+  static unsigned cap = 0;
+  if (!cap) cap = persistent_grid(prune_count_kernel, kPruneWarps * 32, 0, ~0ull >> 8, kPruneWarps);
+  const unsigned grid = (unsigned)((nc + kPruneWarps - 1) / kPruneWarps < cap ? (nc + kPruneWarps - 1) / kPruneWarps : cap);
+  prune_count_kernel<<<grid ? grid : 1, kPruneWarps * 32, 0, s>>>(w, len, win_dev, counts_dev, cand,
+                                                                  cand_cap, nc);
   note_launch();
 }
 
@@ -360,14 +467,29 @@ void launch_prune_hist(const void* src, int from_float, uint64_t n, uint32_t bas
   note_launch();
 }
 
-void launch_prune_bitmap(const float* w, uint64_t len, uint32_t T, uint64_t r, uint64_t* words,
-                         uint32_t* tile_popc, int* changed, uint64_t* ws_state, cudaStream_t s) {
-  const uint64_t nt = (len + kTile - 1) / kTile;
-  cudaMemsetAsync(ws_state, 0, nt * sizeof(uint64_t) + sizeof(unsigned), s);
-  cudaMemsetAsync(changed, 0, sizeof(int), s);
-  prune_bitmap_kernel<<<(unsigned)nt, kThreads, 0, s>>>(
-      w, len, T, r, words, (len + 63) / 64, tile_popc, changed, ws_state,
-      reinterpret_cast<unsigned*>(ws_state + nt));
+void launch_prune_bitmap(const float* w, uint64_t len, uint32_t T, uint64_t r,
+                         const uint32_t* tie_prefix, uint64_t* words, uint32_t* chunk_popc,
+                         uint32_t* ties_out, const uint32_t* ties_prev, uint64_t* tie_words,
+                         BitmapCounts* counts, cudaStream_t s) {
+  const uint64_t nc = (len + kChunk - 1) / kChunk;
+  cudaMemsetAsync(counts, 0, sizeof(BitmapCounts), s);
+  if (!nc) return;
+  static unsigned cap = 0;
+  if (!cap) cap = persistent_grid(prune_bitmap_kernel, kPruneWarps * 32, 0, ~0ull >> 8, kPruneWarps);
+  const uint64_t need = (nc + kPruneWarps - 1) / kPruneWarps;
+  prune_bitmap_kernel<<<(unsigned)(need < cap ? need : cap), kPruneWarps * 32, 0, s>>>(
+      w, len, T, r, tie_prefix, words, (len + 63) / 64, chunk_popc, ties_out, ties_prev, tie_words,
+      counts, nc);
+  note_launch();
+}
+
+void launch_prune_tiefix(uint64_t* words, uint64_t len, const uint64_t* tie_words,
+                         const uint32_t* ties, const uint32_t* tie_prefix, uint64_t r,
+                         uint32_t* chunk_popc, cudaStream_t s) {
+  const uint64_t nc = (len + kChunk - 1) / kChunk;
+  if (!nc) return;
+  prune_tiefix_kernel<<<(unsigned)((nc * 32 + 255) / 256), 256, 0, s>>>(
+      words, (len + 63) / 64, tie_words, ties, tie_prefix, r, chunk_popc, nc);
   note_launch();
 }
 
