@@ -205,6 +205,8 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--ratio", type=float, default=None, help="override the config's prune ratio")
     ap.add_argument("--bucket-mb", type=float, default=None)
+    ap.add_argument("--transport", default="auto", choices=["auto", "nccl", "p2p"],
+                    help="packed exchange for N > 1: NCCL allreduce or the fused NVLink P2P path")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -255,7 +257,8 @@ def main():
     pb.enforce_gradient_sparsity(grad, mask, out=grad)
     out = torch.empty_like(grad)
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
-    policy = pb.SyncPolicy(bucket_bytes=bucket if world > 1 else 0)
+    transport = {"auto": 0, "nccl": 1, "p2p": 2}[args.transport]
+    policy = pb.SyncPolicy(bucket_bytes=bucket if world > 1 else 0, transport=transport)
     w_cur = weights.clone() if reprune else None
 
     def barrier():
@@ -312,6 +315,18 @@ def main():
     alg_unpack = 4 * nnz + n / 8 + 4 * n
     stages = {"pack_us": round(t_pack * 1e6, 2), "unpack_us": round(t_unpack * 1e6, 2),
               "pack_gbs": round(alg_pack / t_pack / 1e9, 1), "unpack_gbs": round(alg_unpack / t_unpack / 1e9, 1)}
+    # per-stage breakdown of the full step (events between the stages; untimed)
+    pol_t = pb.SyncPolicy(bucket_bytes=policy.bucket_bytes, transport=policy.transport, time_stages=True)
+    br = []
+    for i in range(7):
+        flush.zero_()
+        barrier()
+        rr = pb.masked_allreduce(grad, mask, tracker.status(), i, comm, policy=pol_t, out=out)
+        br.append((rr.stats.seconds, rr.stats.t_pack, rr.stats.t_exchange, rr.stats.t_unpack))
+    if br and br[0][1] > 0:
+        med = [statistics.median(x[k] for x in br) * 1e6 for k in range(4)]
+        stages["step_breakdown_us"] = {"total": round(med[0], 1), "pack": round(med[1], 1),
+                                       "exchange": round(med[2], 1), "unpack": round(med[3], 1)}
     if reprune:
         t_prune = statistics.median(timed(lambda i: pb.magnitude_prune(w_cur, ratio, out=mask), 5))
         stages["prune_us"] = round(t_prune * 1e6, 1)
@@ -385,6 +400,7 @@ def main():
                        "len": n, "nnz": nnz, "ratio": ratio, "reprune_per_step": reprune,
                        "l2": "flushed (512 MiB write) before every timed step",
                        "parallelism": f"dp{world}", "bucket_bytes": policy.bucket_bytes,
+                       "transport": ["none", "nccl", "nvlink-p2p"][r.stats.transport],
                        "per_rank_gbs": round(per_rank_gbs, 2)},
             "roofline": roofline, "stages": stages, **({"allreduce": extra} if extra else {}),
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),

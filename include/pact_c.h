@@ -106,6 +106,8 @@ typedef struct pact_sync_stats {
   int buckets;            /* packed buckets issued */
   uint64_t value_count;   /* fp32 values allreduced */
   int fallback_reason;    /* 0 none, 1 unstable, 2 vote disagreed, 3 density */
+  int transport;          /* exchange used: 0 none (single GPU), 1 NCCL, 2 NVLink P2P */
+  double t_pack, t_exchange, t_unpack; /* device seconds per stage (time_stages, single bucket) */
 } pact_sync_stats;
 
 /* Adaptive policy knobs. Zero-initialised = reference policy:
@@ -115,7 +117,15 @@ typedef struct pact_policy {
   uint64_t bucket_bytes;    /* packed bytes per bucket; 0 = single bucket */
   float scale;              /* applied in unpack; 0 => 1.0 (SUM, as the reference returns) */
   int time_stages;          /* record CUDA events around the stages */
+  int transport;            /* packed exchange: 0 auto, 1 NCCL allreduce, 2 NVLink P2P
+                               (peer-memory reduce in the reference fold order, fused
+                               with unpack; bit-identical to the reference ring) */
 } pact_policy;
+
+/* transport values of pact_policy */
+#define PACT_TRANSPORT_AUTO 0
+#define PACT_TRANSPORT_NCCL 1
+#define PACT_TRANSPORT_P2P 2
 
 typedef struct pact_mask_info {
   uint64_t len;

@@ -33,12 +33,14 @@ class Tracker(C.Structure):
 
 class SyncStatsC(C.Structure):
     _fields_ = [("bytes_on_wire", C.c_uint64), ("seconds", C.c_double), ("mode_used", C.c_int),
-                ("buckets", C.c_int), ("value_count", C.c_uint64), ("fallback_reason", C.c_int)]
+                ("buckets", C.c_int), ("value_count", C.c_uint64), ("fallback_reason", C.c_int),
+                ("transport", C.c_int), ("t_pack", C.c_double), ("t_exchange", C.c_double),
+                ("t_unpack", C.c_double)]
 
 
 class PolicyC(C.Structure):
     _fields_ = [("density_threshold", C.c_double), ("bucket_bytes", C.c_uint64),
-                ("scale", C.c_float), ("time_stages", C.c_int)]
+                ("scale", C.c_float), ("time_stages", C.c_int), ("transport", C.c_int)]
 
 
 class MaskInfo(C.Structure):

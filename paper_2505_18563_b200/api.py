@@ -415,6 +415,10 @@ class SyncStats:  # collective.hpp:73-77
     buckets: int = 0
     value_count: int = 0
     fallback_reason: int = 0
+    transport: int = 0               # 0 none (1 GPU), 1 NCCL, 2 NVLink P2P
+    t_pack: float = 0.0              # device seconds per stage (policy.time_stages)
+    t_exchange: float = 0.0
+    t_unpack: float = 0.0
 
 
 @dataclass
@@ -427,18 +431,23 @@ class AggregateResult:  # collective.hpp:130-133
 class SyncPolicy:
     """Adaptive knobs. Defaults == reference policy."""
 
+    AUTO, NCCL, P2P = 0, 1, 2
+
     density_threshold: float = 0.0   # fall back to dense above this agreed density (0: never)
     bucket_bytes: int = 0            # packed bytes per overlapped bucket (0: one bucket)
     scale: float = 1.0               # fused into unpack (1/n gives the mean)
     time_stages: bool = False
+    transport: int = 0               # 0 auto, 1 NCCL allreduce, 2 NVLink P2P (bit-exact fold order)
 
     def c(self) -> _lib.PolicyC:
-        return _lib.PolicyC(self.density_threshold, self.bucket_bytes, self.scale, int(self.time_stages))
+        return _lib.PolicyC(self.density_threshold, self.bucket_bytes, self.scale, int(self.time_stages),
+                            int(self.transport))
 
 
 def _stats(s: _lib.SyncStatsC) -> SyncStats:
     return SyncStats(int(s.bytes_on_wire), float(s.seconds), SyncMode(s.mode_used), int(s.buckets),
-                     int(s.value_count), int(s.fallback_reason))
+                     int(s.value_count), int(s.fallback_reason), int(s.transport), float(s.t_pack),
+                     float(s.t_exchange), float(s.t_unpack))
 
 
 class Comm:

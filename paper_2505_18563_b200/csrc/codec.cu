@@ -433,8 +433,8 @@ void launch_pack(const float* g, uint64_t len, const uint64_t* words, const uint
   if (ce <= cb) return;
   static int cap = 0;
   if (!cap) cap = persistent_grid(pack_kernel, kPuWarps);
-  pack_kernel<<<grid_for(cap, ce - cb, kPuWarps), kPuWarps * 32, 0, s>>>(g, len, words, chunk_off, packed,
-                                                                   cb, ce);
+  pack_kernel<<<grid_for(cap, ce - cb, kPuWarps), kPuWarps * 32, 0, s>>>(g, len, words, chunk_off,
+                                                                         packed, cb, ce);
   note_launch();
 }
 

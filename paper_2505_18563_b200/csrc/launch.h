@@ -7,6 +7,17 @@
 
 namespace pactk {
 
+// ---- NVLink P2P exchange types (p2p.cu, codec.cu) ---------------------------
+constexpr int kP2PMaxRanks = 8;
+constexpr int kP2PPacked = 0, kP2PReduced = 1, kP2PRead = 2;  // flags[kind * 8 + src]
+struct P2PView {  // device-visible pointers into every rank's symmetric buffer
+  const float* packed[kP2PMaxRanks];   // packed gradient of rank r (current parity)
+  const float* reduced[kP2PMaxRanks];  // reduced chunks of rank r, at absolute index
+  uint64_t* flags[kP2PMaxRanks];       // flag array of rank r
+  int rank, n;
+  uint64_t M, C;                       // packed count, ChunkMap chunk = ceil(M/n)
+};
+
 // ---- codec.cu --------------------------------------------------------------
 // chunk range [cb, ce) of 1024-element chunks; all pointers device.
 void launch_pack(const float* g, uint64_t len, const uint64_t* words, const uint32_t* chunk_off,
@@ -28,6 +39,19 @@ void launch_scan_excl(const uint32_t* in, uint64_t n, uint32_t* out, void* scrat
 // count of kernels launched by these launchers (process-wide, for gpu_launches)
 uint64_t launches();
 void note_launch(uint64_t n = 1);
+
+// ---- p2p.cu ----------------------------------------------------------------
+// flags[kind][rank] = value on every rank (system-scope release after a fence)
+void launch_p2p_signal(const P2PView& v, int kind, uint64_t value, cudaStream_t s);
+// wait until flags[kind][s] >= target for all s < n (10 s timeout -> *err)
+void launch_p2p_wait(const uint64_t* flags, int kind, int n, uint64_t target, int* err,
+                     cudaStream_t s);
+// fold packed[*][b, e) in the reference order into out[b, e) (waits PACKED)
+void launch_p2p_fold(const P2PView& v, float* out, uint64_t b, uint64_t e, const uint64_t* flags,
+                     uint64_t target, int* err, cudaStream_t s);
+// out[j] = reduced[owner(j)][j] for all j < M (waits REDUCED)
+void launch_p2p_gather(const P2PView& v, float* out, const uint64_t* flags, uint64_t target, int* err,
+                       cudaStream_t s);
 
 // ---- prune.cu --------------------------------------------------------------
 struct PruneWindow {

@@ -1,0 +1,240 @@
+// p2p.cu -- NVLink peer-memory allreduce of the packed gradient (the B200
+// replacement of ring_allreduce on the packed path; reference:
+// collective.cpp:165-216 and 269-309).
+//
+// Every rank owns one CUDA-IPC-exported "symmetric" buffer: a flag array that
+// peers write into, its packed gradient and a reduced-chunk region (both
+// double-buffered by step parity). With the reference's ChunkMap(M, n)
+// (C = ceil(M/n)) every element of chunk c is folded in the reference's order
+// (((x_c + x_{c+1}) + ...) + x_{c-1}), so the result is BIT-IDENTICAL to the
+// reference ring for every n (NCCL's order is unspecified; the reference ring
+// is order-free only at n = 2).
+//
+//   one-shot (n == 2): every rank folds all M values, pulling the peer's
+//     packed buffer over NVLink (M remote reads per rank, one barrier).
+//   two-shot (n > 2): rank c folds chunk c (reduce-scatter by pulls), then
+//     every rank pulls the other reduced chunks from their owners
+//     (all-gather); 2(n-1)/n * M remote reads per rank, two barriers.
+// Pulls, not pushes: measured on this pool (tools/nvlink_probe.cu) peer
+// float4 loads reach 741 GB/s, aligned float4 stores 696 GB/s, but stores at
+// an arbitrary 4-byte offset (compacted runs) only 413 GB/s. All streams are
+// 16-byte aligned float4 at the same index in source and destination, with
+// several loads in flight per thread; remote reads use ld.global.cg (no stale
+// L1 lines across steps).
+//
+// Ordering: producer kernels complete; a 1-warp signal kernel fences at
+// system scope and stores the step number into every peer's flag slot with
+// st.release.sys; consumers spin on their local flags with ld.acquire.sys,
+// bounded by a 10 s globaltimer timeout that raises a device error flag
+// instead of hanging.
+#include "common.cuh"
+#include "launch.h"
+
+namespace pactk {
+
+namespace {
+
+__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// thread 0 waits until flags[kind][s] >= target for all s < n; block barrier
+__device__ void block_wait_flags(const uint64_t* flags, int kind, int n, uint64_t target, int* err) {
+  if (threadIdx.x == 0) {
+    const uint64_t t0 = globaltimer();
+    for (int s = 0; s < n; ++s) {
+      while (ld_acquire_sys(flags + kind * kP2PMaxRanks + s) < target) {
+        if (globaltimer() - t0 > 10000000000ull) {  // 10 s: a peer died; fail, do not hang
+          atomicExch(err, 1);
+          break;
+        }
+        __nanosleep(64);
+      }
+    }
+  }
+  __syncthreads();
+}
+
+__global__ void p2p_signal_kernel(P2PView v, int kind, uint64_t value) {
+  const int lane = threadIdx.x;
+  __threadfence_system();
+  if (lane < v.n) st_release_sys(v.flags[lane] + kind * kP2PMaxRanks + v.rank, value);
+}
+
+__global__ void p2p_wait_kernel(const uint64_t* flags, int kind, int n, uint64_t target, int* err) {
+  block_wait_flags(flags, kind, n, target, err);
+}
+
+__device__ __forceinline__ float4 ldcg4(const float* p) {
+  return __ldcg(reinterpret_cast<const float4*>(p));
+}
+
+// fold element i of chunk c: ((x_c + x_{c+1}) + ...) + x_{c-1}
+__device__ __forceinline__ float fold1(const P2PView& v, uint32_t c, uint64_t i) {
+  float acc = __ldcg(v.packed[c] + i);
+  for (int s = 1; s < v.n; ++s) {
+    int r = (int)c + s;
+    if (r >= v.n) r -= v.n;
+    acc = __fadd_rn(acc, __ldcg(v.packed[r] + i));
+  }
+  return acc;
+}
+
+// Fold packed[*][b, e) into out[b, e), reference order per element. A float4
+// inside one chunk folds as a vector; chunk-straddling vectors and ragged
+// ends go element by element.
+__device__ void fold_range(const P2PView& v, float* __restrict__ out, uint64_t b, uint64_t e) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t gt = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  const uint64_t vb = (b + 3) & ~3ull, ve = e & ~3ull;
+  if (vb >= ve) {
+    for (uint64_t i = b + gt; i < e; i += stride) out[i] = fold1(v, (uint32_t)(i / v.C), i);
+    return;
+  }
+  for (uint64_t i = b + gt; i < vb; i += stride) out[i] = fold1(v, (uint32_t)(i / v.C), i);
+  for (uint64_t i = ve + gt; i < e; i += stride) out[i] = fold1(v, (uint32_t)(i / v.C), i);
+  constexpr int kU = 2;  // float4 per thread per iteration, x n sources in flight
+  const uint64_t qe = ve / 4;
+  for (uint64_t q = vb / 4 + gt; q < qe; q += stride * kU) {
+    float4 acc[kU];
+    uint32_t c0[kU];
+    bool same[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const uint64_t qq = q + u * stride;
+      same[u] = false;
+      c0[u] = 0;
+      if (qq >= qe) continue;
+      const uint64_t i = 4 * qq;
+      c0[u] = (uint32_t)(i / v.C);
+      same[u] = (uint32_t)((i + 3) / v.C) == c0[u];
+      if (same[u]) acc[u] = ldcg4(v.packed[c0[u]] + i);
+    }
+#pragma unroll
+    for (int s = 1; s < kP2PMaxRanks; ++s) {
+      if (s >= v.n) break;
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        if (!same[u]) continue;
+        int r = (int)c0[u] + s;
+        if (r >= v.n) r -= v.n;
+        const float4 x = ldcg4(v.packed[r] + 4 * (q + u * stride));
+        acc[u].x = __fadd_rn(acc[u].x, x.x);
+        acc[u].y = __fadd_rn(acc[u].y, x.y);
+        acc[u].z = __fadd_rn(acc[u].z, x.z);
+        acc[u].w = __fadd_rn(acc[u].w, x.w);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const uint64_t qq = q + u * stride;
+      if (qq >= qe) continue;
+      const uint64_t i = 4 * qq;
+      if (same[u]) {
+        *reinterpret_cast<float4*>(out + i) = acc[u];
+      } else {
+        for (int k = 0; k < 4; ++k) out[i + k] = fold1(v, (uint32_t)((i + k) / v.C), i + k);
+      }
+    }
+  }
+}
+
+// one-shot (whole vector) or the owner's chunk (two-shot reduce-scatter)
+__global__ void __launch_bounds__(256)
+    p2p_fold_kernel(P2PView v, float* __restrict__ out, uint64_t b, uint64_t e, const uint64_t* flags,
+                    uint64_t target, int* err) {
+  block_wait_flags(flags, kP2PPacked, v.n, target, err);
+  fold_range(v, out, b, e);
+}
+
+// two-shot all-gather: out[j] = reduced[owner(j)][j] (same absolute index)
+__global__ void __launch_bounds__(256)
+    p2p_gather_kernel(P2PView v, float* __restrict__ out, const uint64_t* flags, uint64_t target,
+                      int* err) {
+  block_wait_flags(flags, kP2PReduced, v.n, target, err);
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t gt = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  const uint64_t M = v.M, qe = M / 4;
+  for (uint64_t q = gt; q < qe; q += 2 * stride) {
+    float4 x[2];
+    bool ok[2], same[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const uint64_t qq = q + u * stride;
+      ok[u] = qq < qe;
+      same[u] = false;
+      if (!ok[u]) continue;
+      const uint64_t i = 4 * qq;
+      const uint32_t c = (uint32_t)(i / v.C);
+      same[u] = (uint32_t)((i + 3) / v.C) == c;
+      if (same[u]) x[u] = ldcg4(v.reduced[c] + i);
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      if (!ok[u]) continue;
+      const uint64_t i = 4 * (q + u * stride);
+      if (same[u]) {
+        *reinterpret_cast<float4*>(out + i) = x[u];
+      } else {
+        for (int k = 0; k < 4; ++k) out[i + k] = __ldcg(v.reduced[(i + k) / v.C] + i + k);
+      }
+    }
+  }
+  for (uint64_t i = (M & ~3ull) + gt; i < M; i += stride) out[i] = __ldcg(v.reduced[i / v.C] + i);
+}
+
+int sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+unsigned stream_grid(uint64_t elems) {
+  // consumers spin at entry: keep every CTA resident (<= 8 x 256 per SM)
+  uint64_t blocks = (elems / 4 + 255) / 256;
+  const uint64_t cap = (uint64_t)sms() * 8;
+  if (blocks > cap) blocks = cap;
+  return (unsigned)(blocks ? blocks : 1);
+}
+
+}  // namespace
+
+void launch_p2p_signal(const P2PView& v, int kind, uint64_t value, cudaStream_t s) {
+  p2p_signal_kernel<<<1, 32, 0, s>>>(v, kind, value);
+  note_launch();
+}
+
+void launch_p2p_wait(const uint64_t* flags, int kind, int n, uint64_t target, int* err,
+                     cudaStream_t s) {
+  p2p_wait_kernel<<<1, 32, 0, s>>>(flags, kind, n, target, err);
+  note_launch();
+}
+
+void launch_p2p_fold(const P2PView& v, float* out, uint64_t b, uint64_t e, const uint64_t* flags,
+                     uint64_t target, int* err, cudaStream_t s) {
+  p2p_fold_kernel<<<stream_grid(e > b ? e - b : 0), 256, 0, s>>>(v, out, b, e, flags, target, err);
+  note_launch();
+}
+
+void launch_p2p_gather(const P2PView& v, float* out, const uint64_t* flags, uint64_t target, int* err,
+                       cudaStream_t s) {
+  p2p_gather_kernel<<<stream_grid(v.M), 256, 0, s>>>(v, out, flags, target, err);
+  note_launch();
+}
+
+}  // namespace pactk

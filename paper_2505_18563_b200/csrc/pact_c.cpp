@@ -10,7 +10,13 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <fcntl.h>
+#include <sys/mman.h>
+#include <unistd.h>
+
 #include <algorithm>
+#include <atomic>
+#include <chrono>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -132,6 +138,7 @@ struct pact_ctx {
   cudaStream_t aux[2] = {nullptr, nullptr};  // comm / unpack streams for bucket overlap
   std::vector<cudaEvent_t> ev_pool;
   cudaEvent_t t0 = nullptr, t1 = nullptr;
+  cudaEvent_t stage[3] = {nullptr, nullptr, nullptr};
 };
 
 struct pact_mask {
@@ -156,6 +163,17 @@ struct pact_mask {
   uint32_t spec_T = 0;
 };
 
+namespace {
+struct P2PState {  // CUDA-IPC symmetric buffers of all ranks (p2p.cu)
+  bool tried = false, ok = false;
+  uint64_t cap = 0, creg = 0;  // floats per packed / reduced region (2 regions each)
+  void* sym = nullptr;         // own buffer: [flags 4 KiB][packed x2][reduced x2]
+  char* base[pactk::kP2PMaxRanks] = {};
+  uint64_t k = 0;              // P2P steps completed (flag values)
+  DevBuf err;                  // device timeout flag
+};
+}  // namespace
+
 struct pact_comm {
   pact_ctx* ctx = nullptr;
   ncclComm_t nccl = nullptr;
@@ -163,7 +181,27 @@ struct pact_comm {
   DevBuf vote_dev;  // 32 B own slot + 32*n gathered
   HostBuf vote_pin;
   cudaEvent_t vote_done = nullptr;
+  P2PState p2p;
+  // host vote board in POSIX shared memory (all ranks on one node): the vote
+  // frames are host-known, so the per-step vote never touches the GPU
+  void* shm = nullptr;
+  size_t shm_bytes = 0;
+  uint64_t shm_seq = 0;
+  std::string shm_name;
 };
+
+namespace {
+struct ShmSlot {  // one cache-line pair per rank; frames double-buffered by seq parity
+  std::atomic<uint64_t> seq;
+  uint8_t frame[2][32];
+  uint8_t pad[128 - 8 - 64];
+};
+static_assert(sizeof(ShmSlot) == 128, "slot layout");
+}  // namespace
+
+namespace {
+void p2p_release(pact_comm* c);
+}
 
 namespace {
 
@@ -191,6 +229,7 @@ pact_status ensure_ctx_ws(pact_ctx* ctx) {
     for (auto& s : ctx->aux) CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
     CUDA_TRY(cudaEventCreate(&ctx->t0));
     CUDA_TRY(cudaEventCreate(&ctx->t1));
+    for (auto& e : ctx->stage) CUDA_TRY(cudaEventCreate(&e));
   }
   return PACT_OK;
 }
@@ -246,6 +285,114 @@ uint64_t get_le(const uint8_t* p, int n) {
 }
 
 int imod(int a, int n) { return ((a % n) + n) % n; }
+
+}  // namespace
+
+// ------------------------------------------------ NVLink P2P packed exchange
+
+namespace {
+
+constexpr size_t kFlagBytes = 4096;
+
+// symmetric buffer: [flags 4 KiB][packed x2: cap][reduced chunks x2: cap]
+float* p2p_packed(const P2PState& p, int r, int par) {
+  return reinterpret_cast<float*>(p.base[r] + kFlagBytes) + (size_t)par * p.cap;
+}
+float* p2p_reduced(const P2PState& p, int r, int par) {
+  return reinterpret_cast<float*>(p.base[r] + kFlagBytes + 2 * p.cap * 4) + (size_t)par * p.creg;
+}
+uint64_t* p2p_flags(const P2PState& p, int r) { return reinterpret_cast<uint64_t*>(p.base[r]); }
+
+void p2p_release(pact_comm* c) {
+  P2PState& p = c->p2p;
+  for (int r = 0; r < c->n; ++r)
+    if (r != c->rank && p.base[r]) cudaIpcCloseMemHandle(p.base[r]);
+  if (p.sym) cudaFree(p.sym);
+  for (auto& b : p.base) b = nullptr;
+  p.sym = nullptr;
+  p.ok = false;
+  p.cap = p.creg = 0;
+  p.k = 0;
+}
+
+// Collective: every rank calls it at the same point with the same `need`
+// (the vote-agreed packed count), so the decisions below are unanimous.
+pact_status p2p_setup(pact_comm* c, uint64_t need, cudaStream_t s) {
+  P2PState& p = c->p2p;
+  if (p.ok && p.cap >= need) return PACT_OK;
+  if (p.tried && !p.ok) return PACT_OK;  // unavailable on this node: NCCL path
+  uint8_t one = 1, all[64 * pactk::kP2PMaxRanks];
+  if (p.ok) {  // grow: everyone's GPU work on the old buffers must be done
+    CUDA_TRY(cudaDeviceSynchronize());
+    TRY(pact_allgather_frames(c, &one, 1, all, s));
+    p2p_release(c);
+  }
+  p.tried = true;
+  const uint64_t cap = ((need + need / 4 + (1u << 20)) >> 20) << 20;  // +25%, 1 Mi-float grain
+  const uint64_t creg = cap;  // reduced chunks live at their absolute packed index
+  int ok = c->n <= pactk::kP2PMaxRanks;
+  if (ok && cudaMalloc(&p.sym, kFlagBytes + 2 * cap * 4 + 2 * creg * 4) != cudaSuccess) ok = 0;
+  if (ok && cudaMemset(p.sym, 0, kFlagBytes) != cudaSuccess) ok = 0;
+  if (ok && cudaDeviceSynchronize() != cudaSuccess) ok = 0;
+  cudaIpcMemHandle_t h{};
+  if (ok && cudaIpcGetMemHandle(&h, p.sym) != cudaSuccess) ok = 0;
+  cudaGetLastError();
+  uint8_t frame[1 + sizeof(h)];
+  frame[0] = (uint8_t)ok;
+  std::memcpy(frame + 1, &h, sizeof h);
+  std::vector<uint8_t> frames((size_t)c->n * sizeof frame);
+  TRY(pact_allgather_frames(c, frame, sizeof frame, frames.data(), s));
+  int all_ok = 1;
+  for (int r = 0; r < c->n; ++r) all_ok &= frames[(size_t)r * sizeof frame];
+  int opened = all_ok;
+  if (all_ok) {
+    for (int r = 0; r < c->n; ++r) {
+      if (r == c->rank) {
+        p.base[r] = static_cast<char*>(p.sym);
+        continue;
+      }
+      cudaIpcMemHandle_t hr;
+      std::memcpy(&hr, frames.data() + (size_t)r * sizeof frame + 1, sizeof hr);
+      void* ptr = nullptr;
+      if (cudaIpcOpenMemHandle(&ptr, hr, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+        cudaGetLastError();
+        opened = 0;
+        break;
+      }
+      p.base[r] = static_cast<char*>(ptr);
+    }
+  }
+  uint8_t okb = (uint8_t)opened;
+  TRY(pact_allgather_frames(c, &okb, 1, all, s));
+  int every = 1;
+  for (int r = 0; r < c->n; ++r) every &= all[r];
+  if (!every) {
+    p2p_release(c);
+    return PACT_OK;  // stay on NCCL
+  }
+  TRY(p.err.ensure(sizeof(int)));
+  CUDA_TRY(cudaMemset(p.err.p, 0, sizeof(int)));
+  p.cap = cap;
+  p.creg = creg;
+  p.k = 0;
+  p.ok = true;
+  return PACT_OK;
+}
+
+pactk::P2PView p2p_view(const pact_comm* c, int par, uint64_t M) {
+  const P2PState& p = c->p2p;
+  pactk::P2PView v{};
+  v.C = (M + c->n - 1) / c->n;  // reference ChunkMap (collective.cpp:93-99)
+  for (int r = 0; r < c->n; ++r) {
+    v.packed[r] = p2p_packed(p, r, par);
+    v.reduced[r] = p2p_reduced(p, r, par);
+    v.flags[r] = p2p_flags(p, r);
+  }
+  v.rank = c->rank;
+  v.n = c->n;
+  v.M = M;
+  return v;
+}
 
 }  // namespace
 
@@ -412,6 +559,8 @@ pact_status pact_ctx_destroy(pact_ctx* ctx) {
   for (auto e : ctx->ev_pool) cudaEventDestroy(e);
   if (ctx->t0) cudaEventDestroy(ctx->t0);
   if (ctx->t1) cudaEventDestroy(ctx->t1);
+  for (auto e : ctx->stage)
+    if (e) cudaEventDestroy(e);
   delete ctx;
   return PACT_OK;
 }
@@ -831,6 +980,83 @@ pact_status pact_comm_unique_id(uint8_t out[PACT_UNIQUE_ID_BYTES]) {
   return PACT_OK;
 }
 
+namespace {
+
+uint64_t fnv64(const void* p, size_t n, uint64_t h = 0xcbf29ce484222325ull) {
+  const uint8_t* b = static_cast<const uint8_t*>(p);
+  for (size_t i = 0; i < n; ++i) h = (h ^ b[i]) * 0x100000001b3ull;
+  return h;
+}
+
+// Map the per-comm vote board (/dev/shm) when every rank runs on this host;
+// otherwise the vote stays an NCCL allgather. Collective.
+pact_status shm_vote_setup(pact_comm* c, const uint8_t id[PACT_UNIQUE_ID_BYTES]) {
+  if (getenv("PACT_NO_SHM_VOTE")) return PACT_OK;
+  char host[256] = {0};
+  gethostname(host, sizeof host - 1);
+  uint64_t hh = fnv64(host, strlen(host));
+  std::vector<uint8_t> all((size_t)c->n * 8);
+  TRY(pact_allgather_frames(c, reinterpret_cast<const uint8_t*>(&hh), 8, all.data(), nullptr));
+  bool same = true;
+  for (int r = 0; r < c->n; ++r) same &= std::memcmp(all.data() + 8 * r, &hh, 8) == 0;
+  uint8_t ok = 0;
+  if (same) {
+    char nm[64];
+    snprintf(nm, sizeof nm, "/pact_vote_%016llx", (unsigned long long)fnv64(id, PACT_UNIQUE_ID_BYTES));
+    c->shm_name = nm;
+    c->shm_bytes = sizeof(ShmSlot) * (size_t)c->n;
+    const int fd = shm_open(nm, O_CREAT | O_RDWR, 0600);
+    if (fd >= 0) {
+      if (ftruncate(fd, (off_t)c->shm_bytes) == 0) {
+        void* p = mmap(nullptr, c->shm_bytes, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+        if (p != MAP_FAILED) {
+          c->shm = p;
+          ok = 1;
+        }
+      }
+      close(fd);
+    }
+  }
+  std::vector<uint8_t> oks((size_t)c->n);
+  TRY(pact_allgather_frames(c, &ok, 1, oks.data(), nullptr));  // also: everyone has mapped
+  bool every = true;
+  for (uint8_t o : oks) every &= o != 0;
+  if (!every && c->shm) {
+    munmap(c->shm, c->shm_bytes);
+    c->shm = nullptr;
+  }
+  return PACT_OK;
+}
+
+// host allgather of the 26-byte vote frames through the board: publish into
+// this rank's slot (frame buffer seq&1, then seq with release), spin until
+// every slot reaches seq. A rank cannot reuse a buffer before all ranks have
+// published the next seq, i.e. before everyone finished reading this one.
+pact_status shm_vote(pact_comm* c, const uint8_t frame[PACT_HEADER_BYTES], std::vector<uint8_t>& frames) {
+  ShmSlot* slots = static_cast<ShmSlot*>(c->shm);
+  const uint64_t seq = ++c->shm_seq;
+  ShmSlot& mine = slots[c->rank];
+  std::memcpy(mine.frame[seq & 1], frame, PACT_HEADER_BYTES);
+  mine.seq.store(seq, std::memory_order_release);
+  frames.resize((size_t)c->n * PACT_HEADER_BYTES);
+  const auto t0 = std::chrono::steady_clock::now();
+  for (int r = 0; r < c->n; ++r) {
+    unsigned spins = 0;
+    while (slots[r].seq.load(std::memory_order_acquire) < seq) {
+      if ((++spins & 4095) == 0 &&
+          std::chrono::steady_clock::now() - t0 > std::chrono::seconds(30))
+        return fail(PACT_E_LINK, "vote timed out waiting for rank %d (peer died?)", r);
+#if defined(__x86_64__)
+      __builtin_ia32_pause();
+#endif
+    }
+    std::memcpy(frames.data() + (size_t)r * PACT_HEADER_BYTES, slots[r].frame[seq & 1], PACT_HEADER_BYTES);
+  }
+  return PACT_OK;
+}
+
+}  // namespace
+
 pact_status pact_comm_create(pact_ctx* ctx, const uint8_t id[PACT_UNIQUE_ID_BYTES], int nranks,
                              int rank, pact_comm** out) {
   if (!ctx || !id || !out) return fail(PACT_E_INVALID_ARG, "null args");
@@ -854,6 +1080,7 @@ pact_status pact_comm_create(pact_ctx* ctx, const uint8_t id[PACT_UNIQUE_ID_BYTE
   if (st == PACT_OK) st = c->vote_pin.ensure(32 * (nranks + 1));
   if (st == PACT_OK && cudaEventCreateWithFlags(&c->vote_done, cudaEventDisableTiming) != cudaSuccess)
     st = fail(PACT_E_CUDA, "event create");
+  if (st == PACT_OK) st = shm_vote_setup(c, id);
   if (st != PACT_OK) {
     pact_comm_destroy(c);
     return st;
@@ -865,10 +1092,17 @@ pact_status pact_comm_create(pact_ctx* ctx, const uint8_t id[PACT_UNIQUE_ID_BYTE
 pact_status pact_comm_destroy(pact_comm* c) {
   if (!c) return PACT_OK;
   cudaSetDevice(c->ctx->device);
+  cudaDeviceSynchronize();
+  p2p_release(c);
+  c->p2p.err.release();
   if (c->nccl) ncclCommDestroy(c->nccl);
   c->vote_dev.release();
   c->vote_pin.release();
   if (c->vote_done) cudaEventDestroy(c->vote_done);
+  if (c->shm) {
+    munmap(c->shm, c->shm_bytes);
+    if (c->rank == 0) shm_unlink(c->shm_name.c_str());
+  }
   delete c;
   return PACT_OK;
 }
@@ -975,6 +1209,13 @@ pact_status pact_masked_allreduce(pact_comm* c, pact_ctx* ctx, const float* grad
   const int n = c ? c->n : 1;
   cudaStream_t s = stream;
   if (pol.time_stages) CUDA_TRY(cudaEventRecord(ctx->t0, s));
+  bool marked[3] = {false, false, false};
+  auto mark = [&](int i) {  // stage boundaries: 0 after pack, 1 after exchange, 2 after unpack
+    if (pol.time_stages && !marked[i]) {
+      cudaEventRecord(ctx->stage[i], s);
+      marked[i] = true;
+    }
+  };
 
   // vote frame (collective.cpp:280-283)
   const int stable = pact_decide_sync_mode(PACT_SYNC_PACKED, tracker_stable) == PACT_SYNC_PACKED;
@@ -987,18 +1228,37 @@ pact_status pact_masked_allreduce(pact_comm* c, pact_ctx* ctx, const float* grad
   TRY(ctx->packed.ensure(std::max<uint64_t>(1, m->nnz) * 4));
   float* packed = ctx->packed.as<float>();
 
-  const bool buckets = c && pol.bucket_bytes > 0 && m->nnz * 4 > pol.bucket_bytes;
+  const bool p2p_try = c && m->nnz && n <= pactk::kP2PMaxRanks &&
+                       (pol.transport == PACT_TRANSPORT_P2P || pol.transport == PACT_TRANSPORT_AUTO);
+  const bool p2p_ready = p2p_try && c->p2p.ok && c->p2p.cap >= m->nnz;
+  const bool buckets = c && !p2p_try && pol.bucket_bytes > 0 && m->nnz * 4 > pol.bucket_bytes;
   if (buckets) TRY(mirror_tile_off(m, s));
 
   int agree = 0;
-  bool packed_issued = false;
-  if (c) {
-    TRY(post_vote(c, frame, ctx->aux[0]));
-    // speculative pack overlaps the vote round trip (single-bucket plan only)
+  bool packed_issued = false, packed_in_sym = false;
+  if (c && c->shm) {  // host vote board: microseconds, no GPU work, no stream sync
+    std::vector<uint8_t> frames;
+    TRY(shm_vote(c, frame, frames));
+    TRY(pact_vote_decide(frames.data(), n, &mine, stable, &agree));  // collective.cpp:285-293
+  } else if (c) {
+    // speculative pack overlaps the vote round trip (single-bucket plans);
+    // enqueued first so the GPU starts while the host posts the vote
     if (stable && !buckets && m->nnz) {
-      pactk::launch_pack(grad, len, m->words, m->tile_off, packed, 0, m->ntiles, s);
-      packed_issued = true;
+      if (p2p_ready) {  // straight into this rank's symmetric buffer
+        const uint64_t k1 = c->p2p.k + 1;
+        if (k1 > 2)  // peers finished reading this region (step k1-2)
+          pactk::launch_p2p_wait(p2p_flags(c->p2p, c->rank), pactk::kP2PRead, n, k1 - 2,
+                                 c->p2p.err.as<int>(), s);
+        pactk::launch_pack(grad, len, m->words, m->tile_off, p2p_packed(c->p2p, c->rank, k1 & 1),
+                           0, m->ntiles, s);
+        packed_in_sym = true;
+      } else {
+        pactk::launch_pack(grad, len, m->words, m->tile_off, packed, 0, m->ntiles, s);
+        packed_issued = true;
+      }
+      mark(0);
     }
+    TRY(post_vote(c, frame, ctx->aux[0]));
     std::vector<uint8_t> frames;
     TRY(wait_vote(c, frames));
     TRY(pact_vote_decide(frames.data(), n, &mine, stable, &agree));  // collective.cpp:285-293
@@ -1013,15 +1273,53 @@ pact_status pact_masked_allreduce(pact_comm* c, pact_ctx* ctx, const float* grad
     reason = 3;
   }
 
-  int nbuckets = 0;
-  if (agree) {
+  int nbuckets = 0, transport = c ? PACT_TRANSPORT_NCCL : 0;
+  if (agree && p2p_try) TRY(p2p_setup(c, m->nnz, s));  // collective, no-op once set up
+  if (agree && p2p_try && c->p2p.ok && c->p2p.cap >= m->nnz) {
+    // NVLink pull exchange in the reference fold order (p2p.cu): one-shot at
+    // n = 2, two-shot (reduce-scatter + all-gather by peer loads) above.
+    // Regions alternate by step parity; READ(k-2) guards their reuse.
+    P2PState& p = c->p2p;
+    const uint64_t k1 = p.k + 1;
+    const int par = (int)(k1 & 1);
+    const pactk::P2PView v = p2p_view(c, par, m->nnz);
+    uint64_t* myflags = p2p_flags(p, c->rank);
+    int* err = p.err.as<int>();
+    if (!packed_in_sym) {
+      if (k1 > 2) pactk::launch_p2p_wait(myflags, pactk::kP2PRead, n, k1 - 2, err, s);
+      pactk::launch_pack(grad, len, m->words, m->tile_off, p2p_packed(p, c->rank, par), 0,
+                         m->ntiles, s);
+    }
+    mark(0);
+    pactk::launch_p2p_signal(v, pactk::kP2PPacked, k1, s);
+    if (n == 2) {  // one-shot: fold everything locally from both packed buffers
+      pactk::launch_p2p_fold(v, packed, 0, m->nnz, myflags, k1, err, s);
+    } else {  // two-shot: fold own chunk (reduce-scatter), gather the others
+      const uint64_t b = std::min<uint64_t>(m->nnz, (uint64_t)c->rank * v.C);
+      const uint64_t e = std::min<uint64_t>(m->nnz, b + v.C);
+      pactk::launch_p2p_fold(v, p2p_reduced(p, c->rank, par), b, e, myflags, k1, err, s);
+      pactk::launch_p2p_signal(v, pactk::kP2PReduced, k1, s);
+      pactk::launch_p2p_gather(v, packed, myflags, k1, err, s);
+    }
+    pactk::launch_p2p_signal(v, pactk::kP2PRead, k1, s);  // peers' buffers no longer read
+    mark(1);
+    pactk::launch_unpack(packed, len, m->words, m->tile_off, scale, scale != 1.0f, out, 0,
+                         m->ntiles, s);
+    mark(2);
+    p.k = k1;
+    nbuckets = 1;
+    transport = PACT_TRANSPORT_P2P;
+  } else if (agree) {
     if (!buckets) {
       if (!packed_issued && m->nnz)
         pactk::launch_pack(grad, len, m->words, m->tile_off, packed, 0, m->ntiles, s);
+      mark(0);
       if (c && m->nnz)
         NCCL_TRY(ncclAllReduce(packed, packed, m->nnz, ncclFloat32, ncclSum, c->nccl, s));
+      mark(1);
       pactk::launch_unpack(packed, len, m->words, m->tile_off, scale, scale != 1.0f, out, 0,
                            m->ntiles, s);
+      mark(2);
       nbuckets = 1;
     } else {
       // tile-aligned buckets of ~bucket_bytes packed; pack on s, NCCL on
@@ -1077,12 +1375,22 @@ pact_status pact_masked_allreduce(pact_comm* c, pact_ctx* ctx, const float* grad
     stats->buckets = nbuckets;
     stats->value_count = agree ? m->nnz : len;
     stats->fallback_reason = reason;
+    stats->transport = transport;
     if (pol.time_stages) {
       CUDA_TRY(cudaEventRecord(ctx->t1, s));
       CUDA_TRY(cudaEventSynchronize(ctx->t1));
       float ms = 0;
       cudaEventElapsedTime(&ms, ctx->t0, ctx->t1);
       stats->seconds = ms * 1e-3;
+      if (marked[0] && marked[1] && marked[2]) {
+        float a = 0, b = 0, d = 0;
+        cudaEventElapsedTime(&a, ctx->t0, ctx->stage[0]);
+        cudaEventElapsedTime(&b, ctx->stage[0], ctx->stage[1]);
+        cudaEventElapsedTime(&d, ctx->stage[1], ctx->stage[2]);
+        stats->t_pack = a * 1e-3;
+        stats->t_exchange = b * 1e-3;
+        stats->t_unpack = d * 1e-3;
+      }
     }
   }
   return PACT_OK;

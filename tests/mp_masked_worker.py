@@ -1,0 +1,159 @@
+"""Multi-rank worker for tests/test_multi_gpu.py (launched by torchrun, one
+process per GPU). Every rank generates all ranks' inputs from the shared
+seeds, runs the library's masked_allreduce over NCCL, and checks its own
+result against the CPU oracle (oracle/pact_oracle.c restatement of
+collective.cpp:269-309). Exit code != 0 on any mismatch."""
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import oracle  # noqa: E402
+import paper_2505_18563_b200 as pb  # noqa: E402
+from oracle import words_from_bits  # noqa: E402
+from paper_2505_18563_b200 import synth  # noqa: E402
+
+
+def u32(a):
+    return np.ascontiguousarray(a, dtype=np.float32).view(np.uint32)
+
+
+def main():
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    comm = pb.Comm.from_process_group()
+    port = oracle.port()
+    failures = []
+
+    def check(name, ok):
+        if not ok:
+            failures.append(name)
+            print(f"[rank {rank}] FAIL {name}", flush=True)
+
+    rng = np.random.default_rng(1234)
+    n = 300_007
+    bits = rng.random(n) < 0.2
+    words = words_from_bits(bits)
+    mask = pb.SparsityMask.from_words(torch.from_numpy(words.view(np.int64)).to(dev), n)
+    check("nnz", mask.nnz() == int(bits.sum()))
+
+    for (recipe, tag), transport in [(r_, t_) for r_ in ((synth.G_DYADIC, "dyadic"), (synth.G_FULL, "full"))
+                                     for t_ in (pb.SyncPolicy.NCCL, pb.SyncPolicy.P2P)]:
+        tag = f"{tag}/{'p2p' if transport == pb.SyncPolicy.P2P else 'nccl'}"
+        grads = [port.gse(synth.synth_host(n, synth.grad_seed(r, 1), recipe), words) for r in range(world)]
+        outs, modes, byts = port.masked_allreduce(grads, [words] * world, [1] * world, 3)
+        g = torch.from_numpy(grads[rank]).to(dev)
+        res = pb.masked_allreduce(g, mask, pb.TrackerStatus.Stable, 3, comm,
+                                  policy=pb.SyncPolicy(transport=transport))
+        got = res.tensor.cpu().numpy()
+        check(f"{tag}: packed mode", res.stats.mode_used == pb.SyncMode.PackedAllReduce and modes[rank] == 1)
+        check(f"{tag}: transport", res.stats.transport == transport)
+        check(f"{tag}: bytes_on_wire", res.stats.bytes_on_wire == byts[rank])
+        if recipe == synth.G_DYADIC or world == 2 or transport == pb.SyncPolicy.P2P:
+            # exact partial sums (dyadic), order-free n=2, or the P2P path that
+            # folds in the reference ring order: bit-exact
+            check(f"{tag}: bit-exact", np.array_equal(u32(got), u32(outs[rank])))
+        else:
+            tol = 1e-6 * np.maximum(sum(np.abs(x) for x in grads), 2.0 ** -126)
+            check(f"{tag}: within 1e-6*sum|x|", bool(np.all(np.abs(got - outs[rank]) <= tol)))
+        # repeated P2P steps exercise the double-buffered regions and flags
+        for step in range(3):
+            r2 = pb.masked_allreduce(g, mask, pb.TrackerStatus.Stable, 3 + step, comm,
+                                     policy=pb.SyncPolicy(transport=transport))
+            check(f"{tag}: repeat {step}", torch.equal(r2.tensor, res.tensor))
+        # every rank holds identical bits (collective.hpp:121-122)
+        t = torch.from_numpy(got.view(np.int32).copy()).to(dev)
+        lst = [torch.empty_like(t) for _ in range(world)]
+        dist.all_gather(lst, t)
+        check(f"{tag}: replicas identical", all(torch.equal(lst[0], x) for x in lst))
+
+        # bucketed pipeline == single bucket, bit for bit
+        pol = pb.SyncPolicy(bucket_bytes=64 << 10, transport=transport)
+        if transport == pb.SyncPolicy.P2P:
+            pol.transport = pb.SyncPolicy.NCCL  # buckets are an NCCL-path feature
+        res_b = pb.masked_allreduce(g, mask, pb.TrackerStatus.Stable, 3, comm, policy=pol)
+        check(f"{tag}: buckets>1", res_b.stats.buckets > 1)
+        if recipe == synth.G_DYADIC or world == 2:  # NCCL's order depends on the message size
+            check(f"{tag}: bucketed == single", torch.equal(res_b.tensor, res.tensor))
+        else:
+            tol = 1e-6 * np.maximum(sum(np.abs(x) for x in grads), 2.0 ** -126)
+            check(f"{tag}: bucketed within 1e-6*sum|x|",
+                  bool(np.all(np.abs(res_b.tensor.cpu().numpy() - outs[rank]) <= tol)))
+        # fused mean (to_mean, trainer.cpp:268-273)
+        res_m = pb.masked_allreduce(g, mask, pb.TrackerStatus.Stable, 3, comm,
+                                    policy=pb.SyncPolicy(scale=1.0 / world, transport=transport))
+        check(f"{tag}: fused mean", np.array_equal(u32(res_m.tensor.cpu().numpy()),
+                                                  u32(port.to_mean(got, world))))
+
+    grads = [synth.synth_host(n, synth.grad_seed(r, 2), synth.G_DYADIC) for r in range(world)]
+    g = torch.from_numpy(grads[rank]).to(dev)
+    # one unstable tracker -> every rank falls back to the dense sum
+    stable = [1] * world
+    stable[world - 1] = 0
+    outs, modes, byts = port.masked_allreduce(grads, [words] * world, stable, 4)
+    res = pb.masked_allreduce(g, mask, pb.TrackerStatus.Stable if stable[rank] else pb.TrackerStatus.Unstable, 4, comm)
+    check("unstable: full mode", res.stats.mode_used == pb.SyncMode.FullAllReduce and modes[rank] == 0)
+    check("unstable: bytes", res.stats.bytes_on_wire == byts[rank])
+    check("unstable: exact", np.array_equal(u32(res.tensor.cpu().numpy()), u32(outs[rank])))
+
+    # advertised-digest fault on rank 0 (trainer.cpp:286-290) -> fallback
+    d0 = mask.digest()
+    adv = [d0] * world
+    adv[0] = d0 ^ 0x5A5A5A5A5A5A5A5A
+    outs, modes, byts = port.masked_allreduce(grads, [words] * world, [1] * world, 5, adv)
+    res = pb.masked_allreduce(g, mask, pb.TrackerStatus.Stable, 5, comm, advertised_digest=adv[rank])
+    check("fault: full mode", res.stats.mode_used == pb.SyncMode.FullAllReduce and modes[rank] == 0)
+    check("fault: exact", np.array_equal(u32(res.tensor.cpu().numpy()), u32(outs[rank])))
+
+    # divergent masks on the last rank -> fallback (test_collective.cpp:263-285)
+    bad = bits.copy()
+    bad[6] = not bad[6]
+    wbad = words_from_bits(bad)
+    mine = wbad if rank == world - 1 else words
+    m2 = pb.SparsityMask.from_words(torch.from_numpy(mine.view(np.int64)).to(dev), n)
+    outs, modes, byts = port.masked_allreduce(grads, [words] * (world - 1) + [wbad], [1] * world, 7)
+    res = pb.masked_allreduce(g, m2, pb.TrackerStatus.Stable, 7, comm)
+    check("divergent: full mode", res.stats.mode_used == pb.SyncMode.FullAllReduce)
+    check("divergent: exact", np.array_equal(u32(res.tensor.cpu().numpy()), u32(outs[rank])))
+
+    # density rule: unanimous dense fallback above the threshold
+    res = pb.masked_allreduce(g, mask, pb.TrackerStatus.Stable, 8, comm,
+                              policy=pb.SyncPolicy(density_threshold=0.1))
+    check("density: full mode", res.stats.mode_used == pb.SyncMode.FullAllReduce and res.stats.fallback_reason == 3)
+
+    # full_allreduce == ring semantics; allgather of frames
+    res = pb.full_allreduce(g, comm)  # dyadic inputs: exact in any reduction order
+    check("full_allreduce exact",
+          np.array_equal(u32(res.tensor.cpu().numpy()), u32(port.ring_allreduce(grads)[rank])))
+    check("full bytes", res.stats.bytes_on_wire == port.ring_bytes(world, rank, n))
+    frames = pb.allgather(bytes([rank]) * 26, comm)
+    check("allgather", frames == [bytes([r]) * 26 for r in range(world)])
+
+    # host-buffer entry point
+    gh = torch.from_numpy(grads[rank]).pin_memory()
+    oh = torch.empty(n, dtype=torch.float32).pin_memory()
+    st = pb.masked_allreduce_host(gh, mask, pb.TrackerStatus.Stable, 9, comm, oh)
+    outs, modes, byts = port.masked_allreduce([port.gse(x, words) for x in grads], [words] * world, [1] * world, 9)
+    gse_outs = outs
+    check("host: packed", st.mode_used == pb.SyncMode.PackedAllReduce)
+    check("host: exact", np.array_equal(u32(oh.numpy()), u32(gse_outs[rank])))
+
+    flag = torch.tensor([len(failures)], device=dev)
+    dist.all_reduce(flag)
+    comm.close()
+    dist.destroy_process_group()
+    if rank == 0:
+        print(f"mp_masked_worker world={world} failures={int(flag.item())}", flush=True)
+    sys.exit(1 if int(flag.item()) else 0)
+
+
+if __name__ == "__main__":
+    main()

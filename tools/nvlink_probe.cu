@@ -1,0 +1,88 @@
+// nvlink_probe.cu -- measure GPU0 <-> GPU1 peer-memory access patterns
+// (design evidence for p2p.cu). Single process, peer access enabled.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/nvlink_probe tools/nvlink_probe.cu
+#include <cstdio>
+#include <cuda_runtime.h>
+
+#define CK(x)                                                             \
+  do {                                                                    \
+    cudaError_t e = (x);                                                  \
+    if (e != cudaSuccess) {                                               \
+      printf("%s: %s\n", #x, cudaGetErrorString(e));                     \
+      return 1;                                                           \
+    }                                                                     \
+  } while (0)
+
+__global__ void rd4(const float4* __restrict__ src, float4* __restrict__ dst, size_t n4) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4; i += (size_t)gridDim.x * blockDim.x)
+    dst[i] = __ldcg(src + i);
+}
+__global__ void wr4(const float4* __restrict__ src, float4* __restrict__ dst, size_t n4) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4; i += (size_t)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+__global__ void wr1(const float* __restrict__ src, float* __restrict__ dst, size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+// 4 consecutive floats per thread as scalar stores (strided warp instructions)
+__global__ void wr1x4(const float* __restrict__ src, float* __restrict__ dst, size_t n4) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4; i += (size_t)gridDim.x * blockDim.x) {
+    const float4 v = reinterpret_cast<const float4*>(src)[i];
+    dst[4 * i] = v.x;
+    dst[4 * i + 1] = v.y;
+    dst[4 * i + 2] = v.z;
+    dst[4 * i + 3] = v.w;
+  }
+}
+// contiguous 4-byte stores at a +1 element misalignment (runs of arbitrary offset)
+__global__ void wr1_off(const float* __restrict__ src, float* __restrict__ dst, size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    dst[i + 1] = src[i];
+}
+
+int main() {
+  int ndev = 0;
+  CK(cudaGetDeviceCount(&ndev));
+  if (ndev < 2) {
+    printf("need 2 GPUs\n");
+    return 1;
+  }
+  const size_t bytes = 256ull << 20, n = bytes / 4;
+  float *a0, *b0, *a1;
+  CK(cudaSetDevice(1));
+  CK(cudaMalloc(&a1, bytes + 64));
+  CK(cudaSetDevice(0));
+  CK(cudaDeviceEnablePeerAccess(1, 0));
+  CK(cudaMalloc(&a0, bytes + 64));
+  CK(cudaMalloc(&b0, bytes + 64));
+  CK(cudaMemset(a0, 1, bytes));
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const int grid = 148 * 8, blk = 256;
+  auto run = [&](const char* name, auto launch) {
+    launch();
+    cudaDeviceSynchronize();
+    float best = 1e9;
+    for (int it = 0; it < 5; ++it) {
+      cudaEventRecord(e0);
+      launch();
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      if (ms < best) best = ms;
+    }
+    printf("%-44s %8.1f GB/s  (%.1f us for %zu MB)\n", name, bytes / (best * 1e-3) / 1e9, best * 1e3,
+           bytes >> 20);
+  };
+  run("local copy float4 (HBM r+w, r counted)", [&] { rd4<<<grid, blk>>>((float4*)a0, (float4*)b0, n / 4); });
+  run("remote READ float4 ld.cg  (GPU1 -> GPU0)", [&] { rd4<<<grid, blk>>>((float4*)a1, (float4*)b0, n / 4); });
+  run("remote WRITE float4        (GPU0 -> GPU1)", [&] { wr4<<<grid, blk>>>((float4*)a0, (float4*)a1, n / 4); });
+  run("remote WRITE f32 coalesced (GPU0 -> GPU1)", [&] { wr1<<<grid, blk>>>(a0, a1, n); });
+  run("remote WRITE f32 x4/thread strided", [&] { wr1x4<<<grid, blk>>>(a0, a1, n / 4); });
+  run("remote WRITE f32 coalesced, +4B offset", [&] { wr1_off<<<grid, blk>>>(a0, a1, n); });
+  run("cudaMemcpyPeer GPU0 -> GPU1", [&] { cudaMemcpyPeerAsync(a1, 1, a0, 0, bytes); });
+  return 0;
+}
