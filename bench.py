@@ -334,7 +334,7 @@ def main():
     if t_pack >= t_unpack:
         dom, alg, tdom = "pack_kernel", alg_pack, t_pack
     else:
-        dom, alg, tdom = "unpack_kernel", alg_unpack, t_unpack
+        dom, alg, tdom = "unpack_kernel<0>", alg_unpack, t_unpack
     peak, peak_kind = peaks()
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
