@@ -30,6 +30,7 @@ from .api import (  # noqa: F401
     enforce_gradient_sparsity,
     full_allreduce,
     magnitude_prune,
+    magnitude_prune_per_layer,
     mask_digest,
     masked_allreduce,
     masked_allreduce_host,

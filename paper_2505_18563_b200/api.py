@@ -260,6 +260,18 @@ def magnitude_prune(weights: torch.Tensor, ratio: float, out: Optional[SparsityM
     return m
 
 
+def magnitude_prune_per_layer(weights: torch.Tensor, seg_offsets: Sequence[int], ratio: float,
+                              out: Optional[SparsityMask] = None) -> SparsityMask:
+    """Per-layer mode (north_star): the reference rule applied to
+    every [seg[s], seg[s+1]) slice with k_s = drop_count(ratio, len_s)."""
+    w = _as_grad(weights, "weights")
+    m = out if out is not None else SparsityMask(w.numel())
+    seg = (C.c_uint64 * len(seg_offsets))(*[int(x) for x in seg_offsets])
+    _call(lib.pact_prune_magnitude_segmented, m.ctx.handle, _ptr(w), w.numel(), seg,
+          len(seg_offsets) - 1, C.c_float(ratio), m.handle, _stream())
+    return m
+
+
 def build_prune_mask(weights: torch.Tensor, cfg: PruneConfig) -> SparsityMask:  # sparsity.cpp:121-128
     cfg.validate()
     return magnitude_prune(weights, cfg.ratio)

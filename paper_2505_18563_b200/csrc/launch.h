@@ -89,6 +89,17 @@ void launch_prune_tiefix(uint64_t* words, uint64_t len, const uint64_t* tie_word
                          const uint32_t* ties, const uint32_t* tie_prefix, uint64_t r,
                          uint32_t* chunk_popc, cudaStream_t s);
 
+// per-layer mode: thread per word, element i of segment s kept iff key > T_s;
+// ties recorded (tie_words, word_ties) for the fix-up below
+void launch_prune_seg_bitmap(const float* w, uint64_t len, const uint64_t* seg, uint64_t nseg,
+                             const uint32_t* Tseg, uint64_t* words, uint64_t* tie_words,
+                             uint32_t* word_ties, cudaStream_t s);
+// keep tie j of segment s iff its in-segment rank >= rseg[s]; word_prefix =
+// exclusive scan of word_ties; seg_base scratch (nseg u64)
+void launch_prune_seg_tiefix(uint64_t* words, uint64_t len, const uint64_t* tie_words,
+                             const uint32_t* word_prefix, const uint64_t* seg, uint64_t nseg,
+                             uint64_t* seg_base, const uint64_t* rseg, cudaStream_t s);
+
 // ---- digest.cu -------------------------------------------------------------
 // FNV-1a-64 over the LE bytes of nwords words; scratch sized by
 // digest_scratch_bytes(nwords). Result written to *out_dev.

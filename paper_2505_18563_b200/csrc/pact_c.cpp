@@ -131,6 +131,7 @@ struct pact_ctx {
   DevBuf ws_small;  // PruneWindow | PruneCounts | hist[2048] | digest out | changed flag
   DevBuf cand;      // prune candidates (u32 keys)
   DevBuf state;     // look-back tile states + counter
+  DevBuf seg_ws;    // per-layer prune: segment table, thresholds, tie prefixes
   DevBuf digest_scratch;
   DevBuf packed;    // packed gradient for masked_allreduce
   DevBuf grad_stage, out_stage;  // e2e host path staging
@@ -550,7 +551,7 @@ pact_status pact_ctx_destroy(pact_ctx* ctx) {
   if (!ctx) return PACT_OK;
   cudaSetDevice(ctx->device);
   cudaDeviceSynchronize();
-  for (DevBuf* b : {&ctx->ws_small, &ctx->cand, &ctx->state, &ctx->digest_scratch, &ctx->packed,
+  for (DevBuf* b : {&ctx->ws_small, &ctx->cand, &ctx->state, &ctx->seg_ws, &ctx->digest_scratch, &ctx->packed,
                     &ctx->grad_stage, &ctx->out_stage})
     b->release();
   ctx->pin.release();
@@ -717,6 +718,70 @@ pact_status select_rank(pact_ctx* ctx, const void* src, int from_float, uint64_t
 
 int bit_length(uint32_t v) { return v ? 32 - __builtin_clz(v) : 0; }
 
+// T = k-th smallest key of w[0, len) (1 <= k < len) and c_lt = #(key < T):
+// (1) sampled window, (2) counting pass, (3) exact select among the window
+// interior; a full radix select if the window missed. Synchronises s.
+pact_status find_threshold(pact_ctx* ctx, const float* w, uint64_t len, uint64_t k, cudaStream_t s,
+                           uint32_t* T_out, uint64_t* c_lt_out, pact_prune_stats* st) {
+  Small* sm = ctx->ws_small.as<Small>();
+  const uint64_t cap = std::max<uint64_t>(1u << 20, len / 16);
+  TRY(ctx->cand.ensure(cap * 4));
+  pactk::launch_prune_sample(w, len, k, &sm->win, s);
+  pactk::launch_prune_count(w, len, &sm->win, &sm->counts, ctx->cand.as<uint32_t>(), cap, s);
+  CUDA_TRY(cudaGetLastError());
+  struct {
+    pactk::PruneWindow win;
+    uint32_t pad[2];
+    pactk::PruneCounts c;
+  } h;
+  static_assert(sizeof(h) == offsetof(Small, digest), "layout");
+  CUDA_TRY(cudaMemcpyAsync(ctx->pin.p, sm, sizeof(h), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  std::memcpy(&h, ctx->pin.p, sizeof(h));
+  const uint64_t lo_end = h.c.n_lt + h.c.n_eq_lo;
+  const uint64_t mid_end = lo_end + h.c.n_mid;
+  const uint64_t hi_end = mid_end + h.c.n_eq_hi;
+  uint32_t T = 0;
+  uint64_t c_lt = 0;
+  bool fallback = false;
+  st->candidates = h.c.n_mid;
+  if (k <= h.c.n_lt || k > hi_end) {
+    fallback = true;
+  } else if (k <= lo_end) {
+    T = h.win.lo;
+    c_lt = h.c.n_lt;
+  } else if (k <= mid_end) {
+    if (h.c.n_mid > cap) {
+      fallback = true;
+    } else {
+      const uint32_t base = h.win.lo + 1;
+      const int bits = bit_length(h.win.hi - h.win.lo - 2);
+      uint32_t rel = 0;
+      uint64_t below = 0;
+      if (bits > 0)
+        TRY(select_rank(ctx, ctx->cand.p, 0, h.c.n_mid, base, bits, k - lo_end, s, &rel, &below));
+      T = base + rel;
+      c_lt = lo_end + below;
+    }
+  } else {
+    T = h.win.hi;
+    c_lt = mid_end;
+  }
+  st->path = fallback ? 2 : 1;
+  if (fallback) {  // exact radix select over the whole array
+    uint32_t rel = 0;
+    uint64_t below = 0;
+    TRY(select_rank(ctx, w, 1, len, 0, 31, k, s, &rel, &below));
+    T = rel;
+    c_lt = below;
+  }
+  st->threshold = T;
+  st->c_lt = c_lt;
+  *T_out = T;
+  *c_lt_out = c_lt;
+  return PACT_OK;
+}
+
 }  // namespace
 
 pact_status pact_prune_magnitude(pact_ctx* ctx, const float* w, uint64_t len, float ratio,
@@ -801,60 +866,9 @@ pact_status pact_prune_magnitude(pact_ctx* ctx, const float* w, uint64_t len, fl
   }
 
   if (!done) {
-    const uint64_t cap = std::max<uint64_t>(1u << 20, len / 16);
-    TRY(ctx->cand.ensure(cap * 4));
-    // (1) sampled window, (2) counting pass
-    pactk::launch_prune_sample(w, len, k, &sm->win, s);
-    pactk::launch_prune_count(w, len, &sm->win, &sm->counts, ctx->cand.as<uint32_t>(), cap, s);
-    CUDA_TRY(cudaGetLastError());
-    struct {
-      pactk::PruneWindow win;
-      uint32_t pad[2];
-      pactk::PruneCounts c;
-    } h;
-    static_assert(sizeof(h) == offsetof(Small, digest), "layout");
-    CUDA_TRY(cudaMemcpyAsync(ctx->pin.p, sm, sizeof(h), cudaMemcpyDeviceToHost, s));
-    CUDA_TRY(cudaStreamSynchronize(s));
-    std::memcpy(&h, ctx->pin.p, sizeof(h));
-    const uint64_t lo_end = h.c.n_lt + h.c.n_eq_lo;
-    const uint64_t mid_end = lo_end + h.c.n_mid;
-    const uint64_t hi_end = mid_end + h.c.n_eq_hi;
     uint32_t T = 0;
     uint64_t c_lt = 0;
-    bool fallback = false;
-    st.candidates = h.c.n_mid;
-    if (k <= h.c.n_lt || k > hi_end) {
-      fallback = true;
-    } else if (k <= lo_end) {
-      T = h.win.lo;
-      c_lt = h.c.n_lt;
-    } else if (k <= mid_end) {
-      if (h.c.n_mid > cap) {
-        fallback = true;
-      } else {  // (3) exact select among the window-interior keys
-        const uint32_t base = h.win.lo + 1;
-        const int bits = bit_length(h.win.hi - h.win.lo - 2);
-        uint32_t rel = 0;
-        uint64_t below = 0;
-        if (bits > 0)
-          TRY(select_rank(ctx, ctx->cand.p, 0, h.c.n_mid, base, bits, k - lo_end, s, &rel, &below));
-        T = base + rel;
-        c_lt = lo_end + below;
-      }
-    } else {
-      T = h.win.hi;
-      c_lt = mid_end;
-    }
-    st.path = fallback ? 2 : 1;
-    if (fallback) {  // exact radix select over the whole array
-      uint32_t rel = 0;
-      uint64_t below = 0;
-      TRY(select_rank(ctx, w, 1, len, 0, 31, k, s, &rel, &below));
-      T = rel;
-      c_lt = below;
-    }
-    st.threshold = T;
-    st.c_lt = c_lt;
+    TRY(find_threshold(ctx, w, len, k, s, &T, &c_lt, &st));
     // (4) bitmap, ties provisionally all dropped; exact when r == E
     const uint64_t r = k - c_lt;
     TRY(bitmap(T, r, false, false));
@@ -894,8 +908,69 @@ pact_status pact_prune_magnitude(pact_ctx* ctx, const float* w, uint64_t len, fl
 pact_status pact_prune_magnitude_segmented(pact_ctx* ctx, const float* w, uint64_t len,
                                            const uint64_t* seg, uint64_t nseg, float ratio,
                                            pact_mask* out, pact_stream_t stream) {
-  (void)ctx, (void)w, (void)len, (void)seg, (void)nseg, (void)ratio, (void)out, (void)stream;
-  return fail(PACT_E_INVALID_ARG, "per-layer prune not built yet");
+  if (!ctx || !out || !seg) return fail(PACT_E_INVALID_ARG, "null ctx/mask/segments");
+  uint64_t k0;
+  TRY(pact_drop_count(ratio, 0, &k0));  // InvalidRatio first, as magnitude_prune does
+  if (out->len != len)
+    return fail(PACT_E_SHAPE_MISMATCH, "weights length %llu != mask length %llu",
+                (unsigned long long)len, (unsigned long long)out->len);
+  if (nseg == 0 || seg[0] != 0 || seg[nseg] != len)
+    return fail(PACT_E_INVALID_VIEW, "segments must cover [0, len)");  // tensor.cpp:37-47
+  for (uint64_t s = 0; s < nseg; ++s)
+    if (seg[s + 1] <= seg[s]) return fail(PACT_E_INVALID_VIEW, "segment %llu is empty", (unsigned long long)s);
+  if (len && !w) return fail(PACT_E_INVALID_ARG, "null weights");
+  TRY(set_device(ctx));
+  TRY(ensure_ctx_ws(ctx));
+  cudaStream_t s = stream;
+  // per-segment thresholds: the global rule on each slice
+  std::vector<uint32_t> Ts(nseg);
+  std::vector<uint64_t> rs(nseg);
+  uint64_t kept = 0;
+  for (uint64_t q = 0; q < nseg; ++q) {
+    const uint64_t ls = seg[q + 1] - seg[q];
+    const uint64_t k = drop_count_raw(ratio, ls);  // sparsity.cpp:33-40 per layer
+    if (k == 0) {  // keep all: key > 0, and every key-0 tie has rank >= 0
+      Ts[q] = 0;
+      rs[q] = 0;
+    } else if (k >= ls) {  // drop all: no key exceeds or equals T
+      Ts[q] = 0xffffffffu;
+      rs[q] = 0;
+    } else {
+      uint64_t c_lt = 0;
+      pact_prune_stats st{};
+      TRY(find_threshold(ctx, w + seg[q], ls, k, s, &Ts[q], &c_lt, &st));
+      rs[q] = k - c_lt;
+    }
+    kept += ls - std::min(k, ls);
+  }
+  const uint64_t nw = out->nwords;
+  const size_t off_seg = 0, off_r = off_seg + (nseg + 1) * 8, off_base = off_r + nseg * 8,
+               off_T = off_base + nseg * 8, off_wt = off_T + ((nseg * 4 + 15) & ~size_t(15)),
+               off_wp = off_wt + nw * 4, total = off_wp + (nw + 1) * 4;
+  TRY(ctx->seg_ws.ensure(total));
+  TRY(out->tie_words.ensure(std::max<uint64_t>(1, nw) * 8));
+  char* ws = ctx->seg_ws.as<char>();
+  CUDA_TRY(cudaMemcpyAsync(ws + off_seg, seg, (nseg + 1) * 8, cudaMemcpyHostToDevice, s));
+  CUDA_TRY(cudaMemcpyAsync(ws + off_r, rs.data(), nseg * 8, cudaMemcpyHostToDevice, s));
+  CUDA_TRY(cudaMemcpyAsync(ws + off_T, Ts.data(), nseg * 4, cudaMemcpyHostToDevice, s));
+  const uint64_t* dseg = reinterpret_cast<const uint64_t*>(ws + off_seg);
+  uint32_t* wties = reinterpret_cast<uint32_t*>(ws + off_wt);
+  uint32_t* wpre = reinterpret_cast<uint32_t*>(ws + off_wp);
+  pactk::launch_prune_seg_bitmap(w, len, dseg, nseg, reinterpret_cast<const uint32_t*>(ws + off_T),
+                                 out->words, out->tie_words.as<uint64_t>(), wties, s);
+  TRY(scan(ctx, wties, nw, wpre, s));
+  pactk::launch_prune_seg_tiefix(out->words, len, out->tie_words.as<uint64_t>(), wpre, dseg, nseg,
+                                 reinterpret_cast<uint64_t*>(ws + off_base),
+                                 reinterpret_cast<const uint64_t*>(ws + off_r), s);
+  CUDA_TRY(cudaGetLastError());
+  TRY(refresh_offsets(out, s));
+  out->changed = 1;
+  out->digest_valid = 0;
+  out->spec_valid = 0;
+  if (out->nnz != kept)
+    return fail(PACT_E_RUN_FAILURE, "per-layer prune kept %llu, expected %llu",
+                (unsigned long long)out->nnz, (unsigned long long)kept);
+  return PACT_OK;
 }
 
 // -------------------------------------------------------------- codecs

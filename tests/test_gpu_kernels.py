@@ -328,3 +328,50 @@ def test_full_size_properties(pb, cuda, model, ratio, nnz):
     assert float(p.values.double().sum()) == float(ref_sum)
     u = pb.unpack(p, m)
     assert torch.equal(u, torch.where(keep, g, torch.zeros((), device=g.device)))
+
+
+# ------------------------------------------------- per-layer prune (D1)
+
+
+def test_per_layer_prune_random_segments(pb, port, cuda):
+    rng = np.random.default_rng(21)
+    for t in range(12):
+        n = int(rng.integers(2000, 400_000))
+        nseg = int(rng.integers(1, 40))
+        cuts = np.unique(np.concatenate([[0, n], rng.integers(1, n, nseg - 1)]))
+        if t % 3 == 0:  # tie heavy with signed zeros and 1-element layers
+            x = (rng.integers(-4, 5, n) * 0.5).astype(np.float32)
+            x[rng.random(n) < 0.1] = -0.0
+            cuts = np.unique(np.concatenate([cuts, cuts[1:-1] + 1]))
+            cuts = cuts[cuts <= n]
+        else:
+            x = (rng.standard_normal(n) * np.exp2(rng.integers(-6, 3, n))).astype(np.float32)
+        for ratio in (0.0, 0.5, 0.9, 0.99):
+            m = pb.magnitude_prune_per_layer(dev(x), [int(c) for c in cuts], ratio)
+            ref = port.magnitude_prune_segmented(x, cuts, ratio)
+            assert np.array_equal(m.words_host(), ref), (t, ratio)
+            assert m.nnz() == port.mask_nnz(ref, n)
+
+
+def test_per_layer_prune_model_shapes(pb, port, cuda):
+    from paper_2505_18563_b200 import synth
+
+    shape = synth.model_shape("resnet18")
+    offs = shape.offsets()
+    for recipe in (synth.W_TIES, synth.W_REAL):
+        wd = synth.weights_device(shape, 9, recipe)
+        m = pb.magnitude_prune_per_layer(wd, offs, 0.9)
+        ref = port.magnitude_prune_segmented(wd.cpu().numpy(), np.array(offs, np.uint64), 0.9)
+        assert np.array_equal(m.words_host(), ref)
+        assert m.digest() == port.mask_digest(ref, shape.total)
+
+
+def test_per_layer_prune_errors(pb, cuda):
+    x = dev(np.ones(100, np.float32))
+    for bad in ([0, 50], [0, 50, 50, 100], [1, 100]):
+        with pytest.raises(pb.Error) as e:
+            pb.magnitude_prune_per_layer(x, bad, 0.5)
+        assert e.value.code == pb.Errc.InvalidView
+    with pytest.raises(pb.Error) as e:
+        pb.magnitude_prune_per_layer(x, [0, 100], 1.0)
+    assert e.value.code == pb.Errc.InvalidRatio
