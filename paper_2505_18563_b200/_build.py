@@ -16,6 +16,8 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OUT_DIR = os.path.join(PKG, "_native")
 LIB = os.path.join(OUT_DIR, "libpact_b200.so")
+# A/B experiments: PACT_LIB points the loader at an alternative build
+LIB = os.environ.get("PACT_LIB", LIB)
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

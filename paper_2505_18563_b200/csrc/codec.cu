@@ -140,7 +140,8 @@ __global__ void __launch_bounds__(kPuWarps * 32)
         }
       }
     }
-    run = 0;  // positions recomputed from the (smem) words: fewer live registers
+    run = 0;  // ranks recomputed from the (smem) words: fewer live registers,
+              // measured faster than keeping them (c5 pack 262 vs 276 us)
 #pragma unroll
     for (int j = 0; j < kVecPerLane; ++j) {
       const Slot s = chunk_slot(wc, j, run);
