@@ -280,11 +280,17 @@ def main():
             tracker.observe(mask)
         return pb.masked_allreduce(grad, mask, tracker.status(), e, comm, policy=policy, out=out)
 
+    align = torch.zeros(1, dtype=torch.float32, device=dev)
+
     def timed(fn, k):
-        """k device-timed calls, L2 flushed before each; returns seconds list."""
+        """k device-timed calls, L2 flushed before each; returns seconds list.
+        N > 1: a 1-element allreduce after the flush re-aligns the ranks on
+        the device, so no step is charged for a peer's flush."""
         evs = []
         for i in range(k):
             l2_flush()
+            if world > 1:
+                torch.distributed.all_reduce(align)
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
             fn(i)

@@ -46,12 +46,24 @@ void launch_p2p_signal(const P2PView& v, int kind, uint64_t value, cudaStream_t 
 // wait until flags[kind][s] >= target for all s < n (10 s timeout -> *err)
 void launch_p2p_wait(const uint64_t* flags, int kind, int n, uint64_t target, int* err,
                      cudaStream_t s);
-// fold packed[*][b, e) in the reference order into out[b, e) (waits PACKED)
+// signals fused into the exchange kernels: `entry` published by block 0 at
+// start (the producer ran before on the stream), `exit` by the last CTA to
+// finish; kind < 0 = none. counter: a zeroed u32, self-resetting.
+struct P2PSig {
+  int entry_kind = -1;
+  uint64_t entry_val = 0;
+  int exit_kind = -1;
+  uint64_t exit_val = 0;
+  unsigned* counter = nullptr;
+};
+// fold packed[*][b, e) in the reference order into out[b, e) (waits PACKED);
+// max_ctas > 0 caps the grid (overlap with pack/unpack on other streams)
 void launch_p2p_fold(const P2PView& v, float* out, uint64_t b, uint64_t e, const uint64_t* flags,
-                     uint64_t target, int* err, cudaStream_t s);
-// out[j] = reduced[owner(j)][j] for all j < M (waits REDUCED)
-void launch_p2p_gather(const P2PView& v, float* out, const uint64_t* flags, uint64_t target, int* err,
-                       cudaStream_t s);
+                     uint64_t target, int* err, int max_ctas, const P2PSig& sg, cudaStream_t s);
+// out[j] = reduced[(j - P0) / Cb][j] for j in [b, e) (waits REDUCED)
+void launch_p2p_gather(const P2PView& v, float* out, uint64_t b, uint64_t e, uint64_t P0, uint64_t Cb,
+                       const uint64_t* flags, uint64_t target, int* err, int max_ctas,
+                       const P2PSig& sg, cudaStream_t s);
 
 // ---- prune.cu --------------------------------------------------------------
 struct PruneWindow {

@@ -149,23 +149,68 @@ __device__ void fold_range(const P2PView& v, float* __restrict__ out, uint64_t b
   }
 }
 
+// Fused signalling (saves a launch per signal): the ENTRY flag is published
+// by block 0 before anyone waits -- the producer kernel ran earlier on this
+// stream, so its stores are complete; the EXIT flag is published by the last
+// CTA to finish (thread-fence reduction pattern), after every CTA's stores.
+__device__ void publish(const P2PView& v, int kind, uint64_t value) {
+  __threadfence_system();
+  for (int r = 0; r < v.n; ++r) st_release_sys(v.flags[r] + kind * kP2PMaxRanks + v.rank, value);
+}
+__device__ void entry_signal(const P2PView& v, const P2PSig& sg) {
+  if (sg.entry_kind >= 0 && blockIdx.x == 0 && threadIdx.x == 0) publish(v, sg.entry_kind, sg.entry_val);
+}
+__device__ void exit_signal(const P2PView& v, const P2PSig& sg) {
+  if (sg.exit_kind < 0) return;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(sg.counter, 1u) == gridDim.x - 1) {
+      *sg.counter = 0;  // every other CTA has arrived: reset for the next launch
+      publish(v, sg.exit_kind, sg.exit_val);
+    }
+  }
+}
+
 // one-shot (whole vector) or the owner's chunk (two-shot reduce-scatter)
 __global__ void __launch_bounds__(256)
     p2p_fold_kernel(P2PView v, float* __restrict__ out, uint64_t b, uint64_t e, const uint64_t* flags,
-                    uint64_t target, int* err) {
+                    uint64_t target, int* err, P2PSig sg) {
+  entry_signal(v, sg);
   block_wait_flags(flags, kP2PPacked, v.n, target, err);
   fold_range(v, out, b, e);
+  exit_signal(v, sg);
 }
 
-// two-shot all-gather: out[j] = reduced[owner(j)][j] (same absolute index)
+// two-shot all-gather of [b, e): out[j] = reduced[owner(j)][j] (same
+// absolute index), owner(j) = (j - P0) / Cb (the bucket's ownership split;
+// the fold ORDER always follows the global ChunkMap, so buckets stay exact)
+__device__ void gather_range(const P2PView& v, float* __restrict__ out, uint64_t b, uint64_t e,
+                             uint64_t P0, uint64_t Cb);
+
 __global__ void __launch_bounds__(256)
-    p2p_gather_kernel(P2PView v, float* __restrict__ out, const uint64_t* flags, uint64_t target,
-                      int* err) {
+    p2p_gather_kernel(P2PView v, float* __restrict__ out, uint64_t b, uint64_t e, uint64_t P0,
+                      uint64_t Cb, const uint64_t* flags, uint64_t target, int* err, P2PSig sg) {
+  entry_signal(v, sg);
   block_wait_flags(flags, kP2PReduced, v.n, target, err);
+  gather_range(v, out, b, e, P0, Cb);
+  exit_signal(v, sg);
+}
+
+__device__ void gather_range(const P2PView& v, float* __restrict__ out, uint64_t b, uint64_t e,
+                             uint64_t P0, uint64_t Cb) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   const uint64_t gt = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  const uint64_t M = v.M, qe = M / 4;
-  for (uint64_t q = gt; q < qe; q += 2 * stride) {
+  const uint64_t vb = (b + 3) & ~3ull, ve = e & ~3ull;
+  auto one = [&](uint64_t i) { out[i] = __ldcg(v.reduced[(i - P0) / Cb] + i); };
+  if (vb >= ve) {
+    for (uint64_t i = b + gt; i < e; i += stride) one(i);
+    return;
+  }
+  for (uint64_t i = b + gt; i < vb; i += stride) one(i);
+  for (uint64_t i = ve + gt; i < e; i += stride) one(i);
+  const uint64_t qe = ve / 4;
+  for (uint64_t q = vb / 4 + gt; q < qe; q += 2 * stride) {
     float4 x[2];
     bool ok[2], same[2];
 #pragma unroll
@@ -175,22 +220,20 @@ __global__ void __launch_bounds__(256)
       same[u] = false;
       if (!ok[u]) continue;
       const uint64_t i = 4 * qq;
-      const uint32_t c = (uint32_t)(i / v.C);
-      same[u] = (uint32_t)((i + 3) / v.C) == c;
+      const uint64_t c = (i - P0) / Cb;
+      same[u] = (i + 3 - P0) / Cb == c;
       if (same[u]) x[u] = ldcg4(v.reduced[c] + i);
     }
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
       if (!ok[u]) continue;
       const uint64_t i = 4 * (q + u * stride);
-      if (same[u]) {
+      if (same[u])
         *reinterpret_cast<float4*>(out + i) = x[u];
-      } else {
-        for (int k = 0; k < 4; ++k) out[i + k] = __ldcg(v.reduced[(i + k) / v.C] + i + k);
-      }
+      else
+        for (int k = 0; k < 4; ++k) one(i + k);
     }
   }
-  for (uint64_t i = (M & ~3ull) + gt; i < M; i += stride) out[i] = __ldcg(v.reduced[i / v.C] + i);
 }
 
 int sms() {
@@ -204,10 +247,12 @@ int sms() {
   return n;
 }
 
-unsigned stream_grid(uint64_t elems) {
-  // consumers spin at entry: keep every CTA resident (<= 8 x 256 per SM)
+unsigned stream_grid(uint64_t elems, int max_ctas) {
+  // consumers spin at entry: keep every CTA resident (<= 8 x 256 per SM), and
+  // at most max_ctas when the exchange overlaps pack/unpack on other streams
   uint64_t blocks = (elems / 4 + 255) / 256;
-  const uint64_t cap = (uint64_t)sms() * 8;
+  uint64_t cap = (uint64_t)sms() * 8;
+  if (max_ctas > 0 && (uint64_t)max_ctas < cap) cap = (uint64_t)max_ctas;
   if (blocks > cap) blocks = cap;
   return (unsigned)(blocks ? blocks : 1);
 }
@@ -226,14 +271,17 @@ void launch_p2p_wait(const uint64_t* flags, int kind, int n, uint64_t target, in
 }
 
 void launch_p2p_fold(const P2PView& v, float* out, uint64_t b, uint64_t e, const uint64_t* flags,
-                     uint64_t target, int* err, cudaStream_t s) {
-  p2p_fold_kernel<<<stream_grid(e > b ? e - b : 0), 256, 0, s>>>(v, out, b, e, flags, target, err);
+                     uint64_t target, int* err, int max_ctas, const P2PSig& sg, cudaStream_t s) {
+  p2p_fold_kernel<<<stream_grid(e > b ? e - b : 0, max_ctas), 256, 0, s>>>(v, out, b, e, flags,
+                                                                          target, err, sg);
   note_launch();
 }
 
-void launch_p2p_gather(const P2PView& v, float* out, const uint64_t* flags, uint64_t target, int* err,
-                       cudaStream_t s) {
-  p2p_gather_kernel<<<stream_grid(v.M), 256, 0, s>>>(v, out, flags, target, err);
+void launch_p2p_gather(const P2PView& v, float* out, uint64_t b, uint64_t e, uint64_t P0, uint64_t Cb,
+                       const uint64_t* flags, uint64_t target, int* err, int max_ctas,
+                       const P2PSig& sg, cudaStream_t s) {
+  p2p_gather_kernel<<<stream_grid(e > b ? e - b : 0, max_ctas), 256, 0, s>>>(v, out, b, e, P0, Cb,
+                                                                            flags, target, err, sg);
   note_launch();
 }
 

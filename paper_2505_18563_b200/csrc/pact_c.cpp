@@ -262,6 +262,36 @@ pact_status refresh_offsets(pact_mask* m, cudaStream_t s) {
   return PACT_OK;
 }
 
+int sm_count_host() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+// chunk-aligned bucket boundaries with ~per packed values each:
+// cuts[b]..cuts[b+1] are chunk ranges; at most max_b buckets
+std::vector<uint64_t> bucket_cuts(const std::vector<uint32_t>& off, uint64_t ntiles, uint64_t per,
+                                  int max_b) {
+  const uint64_t total = off[ntiles];
+  per = std::max<uint64_t>({per, 1, (total + max_b - 1) / std::max(1, max_b)});
+  std::vector<uint64_t> cuts{0};
+  uint64_t t = 0;
+  while (t < ntiles) {
+    const uint64_t target = std::min<uint64_t>(off[t] + per, 0xffffffffu);
+    uint64_t u = std::upper_bound(off.begin() + t + 1, off.end(), (uint32_t)target) - off.begin();
+    u = std::max<uint64_t>(u - 1, t + 1);
+    if (u > ntiles) u = ntiles;
+    cuts.push_back(u);
+    t = u;
+  }
+  return cuts;
+}
+
 pact_status mirror_tile_off(pact_mask* m, cudaStream_t s) {
   if (m->host_tile_off_valid) return PACT_OK;
   m->host_tile_off.resize(m->ntiles + 1);
@@ -303,6 +333,10 @@ float* p2p_reduced(const P2PState& p, int r, int par) {
   return reinterpret_cast<float*>(p.base[r] + kFlagBytes + 2 * p.cap * 4) + (size_t)par * p.creg;
 }
 uint64_t* p2p_flags(const P2PState& p, int r) { return reinterpret_cast<uint64_t*>(p.base[r]); }
+// last-CTA counter of the fused exit signals (zeroed flag page, self-resetting)
+unsigned* p2p_counter(const P2PState& p, int r) {
+  return reinterpret_cast<unsigned*>(p.base[r] + kFlagBytes - 64);
+}
 
 void p2p_release(pact_comm* c) {
   P2PState& p = c->p2p;
@@ -1360,30 +1394,123 @@ pact_status pact_masked_allreduce(pact_comm* c, pact_ctx* ctx, const float* grad
     const pactk::P2PView v = p2p_view(c, par, m->nnz);
     uint64_t* myflags = p2p_flags(p, c->rank);
     int* err = p.err.as<int>();
+    float* mine = p2p_packed(p, c->rank, par);
+    // buckets: chunk ranges of ~bucket_bytes packed (auto 4 MiB); pack(b+1)
+    // on s, exchange(b) on aux[0], unpack(b-1) on aux[1], chained by events
+    std::vector<uint64_t> cuts{0, m->ntiles};
     if (!packed_in_sym) {
-      if (k1 > 2) pactk::launch_p2p_wait(myflags, pactk::kP2PRead, n, k1 - 2, err, s);
-      pactk::launch_pack(grad, len, m->words, m->tile_off, p2p_packed(p, c->rank, par), 0,
-                         m->ntiles, s);
+      // auto: 64 MiB packed per bucket -- each bucket costs ~5 launches and
+      // two cross-stream events, so small buckets lose (measured c2, n=2:
+      // 1 MiB buckets 0.99 ms/step vs 0.11 ms unbucketed)
+      // (c4, n=2: 64 MiB buckets 609 us vs 606 us unbucketed -- the exchange
+      // and pack/unpack contend for the same HBM/LSU, so auto = one bucket)
+      const uint64_t bb = pol.bucket_bytes ? pol.bucket_bytes : ~0ull;
+      if (m->nnz * 4 > bb) {
+        TRY(mirror_tile_off(m, s));
+        cuts = bucket_cuts(m->host_tile_off, m->ntiles, bb / 4, 64);
+      }
+    }
+    const int B = (int)cuts.size() - 1;
+    auto poff = [&](uint64_t chunk) -> uint64_t {
+      return B == 1 ? (chunk == 0 ? 0 : m->nnz) : m->host_tile_off[chunk];
+    };
+    auto fval = [&](int b) { return (k1 << 8) | (uint64_t)(b + 1); };  // monotonic across steps
+    const int xctas = B > 1 ? 4 * sm_count_host() : 0;  // leave SMs to pack/unpack
+    const bool two = n > 2;
+    if (!packed_in_sym && k1 > 2) pactk::launch_p2p_wait(myflags, pactk::kP2PRead, n, k1 - 2, err, s);
+    if (B == 1) {  // no pipelining: everything in order on the caller's stream
+      if (!packed_in_sym) pactk::launch_pack(grad, len, m->words, m->tile_off, mine, 0, m->ntiles, s);
+      mark(0);
+      pactk::P2PSig sg;  // PACKED published by the fold's block 0 on entry
+      sg.entry_kind = pactk::kP2PPacked;
+      sg.entry_val = fval(0);
+      sg.counter = p2p_counter(p, c->rank);
+      if (!two) {
+        sg.exit_kind = pactk::kP2PRead;  // peers' buffers no longer read
+        sg.exit_val = k1;
+        pactk::launch_p2p_fold(v, packed, 0, m->nnz, myflags, fval(0), err, 0, sg, s);
+      } else {
+        const uint64_t Cb = std::max<uint64_t>(1, (m->nnz + n - 1) / n);
+        const uint64_t rb = std::min<uint64_t>(m->nnz, (uint64_t)c->rank * Cb);
+        const uint64_t re = std::min<uint64_t>(m->nnz, rb + Cb);
+        sg.exit_kind = pactk::kP2PReduced;
+        sg.exit_val = fval(0);
+        pactk::launch_p2p_fold(v, p2p_reduced(p, c->rank, par), rb, re, myflags, fval(0), err, 0, sg, s);
+        pactk::P2PSig sg2;
+        sg2.exit_kind = pactk::kP2PRead;
+        sg2.exit_val = k1;
+        sg2.counter = sg.counter;
+        pactk::launch_p2p_gather(v, packed, 0, m->nnz, 0, Cb, myflags, fval(0), err, 0, sg2, s);
+      }
+      mark(1);
+      pactk::launch_unpack(packed, len, m->words, m->tile_off, scale, scale != 1.0f, out, 0,
+                           m->ntiles, s);
+      mark(2);
+      p.k = k1;
+      nbuckets = 1;
+      transport = PACT_TRANSPORT_P2P;
+      goto p2p_done;
+    }
+    {
+    cudaEvent_t e_start = pool_event(ctx, 0);
+    CUDA_TRY(cudaEventRecord(e_start, s));
+    CUDA_TRY(cudaStreamWaitEvent(ctx->aux[0], e_start, 0));
+    CUDA_TRY(cudaStreamWaitEvent(ctx->aux[1], e_start, 0));
+    for (int b = 0; b < B; ++b) {
+      if (!packed_in_sym) pactk::launch_pack(grad, len, m->words, m->tile_off, mine, cuts[b], cuts[b + 1], s);
+      CUDA_TRY(cudaEventRecord(pool_event(ctx, 1 + b), s));
     }
     mark(0);
-    pactk::launch_p2p_signal(v, pactk::kP2PPacked, k1, s);
-    if (n == 2) {  // one-shot: fold everything locally from both packed buffers
-      pactk::launch_p2p_fold(v, packed, 0, m->nnz, myflags, k1, err, s);
-    } else {  // two-shot: fold own chunk (reduce-scatter), gather the others
-      const uint64_t b = std::min<uint64_t>(m->nnz, (uint64_t)c->rank * v.C);
-      const uint64_t e = std::min<uint64_t>(m->nnz, b + v.C);
-      pactk::launch_p2p_fold(v, p2p_reduced(p, c->rank, par), b, e, myflags, k1, err, s);
-      pactk::launch_p2p_signal(v, pactk::kP2PReduced, k1, s);
-      pactk::launch_p2p_gather(v, packed, myflags, k1, err, s);
+    for (int b = 0; b < B; ++b) {
+      cudaStream_t x = ctx->aux[0];
+      CUDA_TRY(cudaStreamWaitEvent(x, pool_event(ctx, 1 + b), 0));
+      const uint64_t P0 = poff(cuts[b]), P1 = poff(cuts[b + 1]);
+      pactk::P2PSig sg;  // PACKED(b) published on entry: pack(b) is complete
+      sg.entry_kind = pactk::kP2PPacked;
+      sg.entry_val = fval(b);
+      sg.counter = p2p_counter(p, c->rank);
+      if (!two) {  // one-shot: fold the bucket from both packed buffers
+        if (b == B - 1) {
+          sg.exit_kind = pactk::kP2PRead;  // peers' buffers no longer read
+          sg.exit_val = k1;
+        }
+        pactk::launch_p2p_fold(v, packed, P0, P1, myflags, fval(b), err, xctas, sg, x);
+      } else {  // two-shot: fold this rank's share of the bucket, then gather
+        const uint64_t Cb = std::max<uint64_t>(1, (P1 - P0 + n - 1) / n);
+        const uint64_t rb = std::min<uint64_t>(P1, P0 + (uint64_t)c->rank * Cb);
+        const uint64_t re = std::min<uint64_t>(P1, rb + Cb);
+        sg.exit_kind = pactk::kP2PReduced;
+        sg.exit_val = fval(b);
+        pactk::launch_p2p_fold(v, p2p_reduced(p, c->rank, par), rb, re, myflags, fval(b), err, xctas, sg, x);
+        pactk::P2PSig sg2;
+        sg2.counter = sg.counter;
+        if (b == B - 1) {
+          sg2.exit_kind = pactk::kP2PRead;
+          sg2.exit_val = k1;
+        }
+        pactk::launch_p2p_gather(v, packed, P0, P1, P0, Cb, myflags, fval(b), err, xctas, sg2, x);
+      }
+      CUDA_TRY(cudaEventRecord(pool_event(ctx, 1 + B + b), x));
     }
-    pactk::launch_p2p_signal(v, pactk::kP2PRead, k1, s);  // peers' buffers no longer read
-    mark(1);
-    pactk::launch_unpack(packed, len, m->words, m->tile_off, scale, scale != 1.0f, out, 0,
-                         m->ntiles, s);
-    mark(2);
+    CUDA_TRY(cudaEventRecord(pool_event(ctx, 1 + 2 * B), ctx->aux[0]));
+    for (int b = 0; b < B; ++b) {
+      CUDA_TRY(cudaStreamWaitEvent(ctx->aux[1], pool_event(ctx, 1 + B + b), 0));
+      pactk::launch_unpack(packed, len, m->words, m->tile_off, scale, scale != 1.0f, out, cuts[b],
+                           cuts[b + 1], ctx->aux[1]);
+    }
+    CUDA_TRY(cudaEventRecord(pool_event(ctx, 2 + 2 * B), ctx->aux[1]));
+    CUDA_TRY(cudaStreamWaitEvent(s, pool_event(ctx, 1 + 2 * B), 0));
+    CUDA_TRY(cudaStreamWaitEvent(s, pool_event(ctx, 2 + 2 * B), 0));
+    if (pol.time_stages && marked[0]) {  // exchange / unpack stage ends, on their streams
+      cudaEventRecord(ctx->stage[1], ctx->aux[0]);
+      cudaEventRecord(ctx->stage[2], ctx->aux[1]);
+      marked[1] = marked[2] = true;
+    }
     p.k = k1;
-    nbuckets = 1;
+    nbuckets = B;
     transport = PACT_TRANSPORT_P2P;
+    }
+  p2p_done:;
   } else if (agree) {
     if (!buckets) {
       if (!packed_issued && m->nnz)
@@ -1400,17 +1527,7 @@ pact_status pact_masked_allreduce(pact_comm* c, pact_ctx* ctx, const float* grad
       // tile-aligned buckets of ~bucket_bytes packed; pack on s, NCCL on
       // aux[0], unpack on aux[1], chained by events
       const std::vector<uint32_t>& off = m->host_tile_off;
-      std::vector<uint64_t> cuts{0};
-      const uint64_t per = std::max<uint64_t>(1, pol.bucket_bytes / 4);
-      uint64_t t = 0;
-      while (t < m->ntiles) {
-        const uint64_t target = off[t] + per;
-        uint64_t u = std::upper_bound(off.begin() + t + 1, off.end(), (uint32_t)std::min<uint64_t>(target, 0xffffffffu)) - off.begin();
-        u = std::max<uint64_t>(u - 1, t + 1);
-        if (u > m->ntiles) u = m->ntiles;
-        cuts.push_back(u);
-        t = u;
-      }
+      const std::vector<uint64_t> cuts = bucket_cuts(off, m->ntiles, pol.bucket_bytes / 4, 256);
       nbuckets = (int)cuts.size() - 1;
       cudaEvent_t start = pool_event(ctx, 0);
       CUDA_TRY(cudaEventRecord(start, s));

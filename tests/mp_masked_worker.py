@@ -75,10 +75,14 @@ def main():
         dist.all_gather(lst, t)
         check(f"{tag}: replicas identical", all(torch.equal(lst[0], x) for x in lst))
 
-        # bucketed pipeline == single bucket, bit for bit
+        # bucketed pipeline (pack / exchange / unpack on three streams)
         pol = pb.SyncPolicy(bucket_bytes=64 << 10, transport=transport)
         if transport == pb.SyncPolicy.P2P:
-            pol.transport = pb.SyncPolicy.NCCL  # buckets are an NCCL-path feature
+            for step in range(3):  # the P2P fold order is global: buckets stay bit-exact
+                rp = pb.masked_allreduce(g, mask, pb.TrackerStatus.Stable, 9 + step, comm, policy=pol)
+                check(f"{tag}: p2p buckets>1", rp.stats.buckets > 1 and rp.stats.transport == transport)
+                check(f"{tag}: p2p bucketed bit-exact", np.array_equal(u32(rp.tensor.cpu().numpy()), u32(outs[rank])))
+            pol = pb.SyncPolicy(bucket_bytes=64 << 10, transport=pb.SyncPolicy.NCCL)
         res_b = pb.masked_allreduce(g, mask, pb.TrackerStatus.Stable, 3, comm, policy=pol)
         check(f"{tag}: buckets>1", res_b.stats.buckets > 1)
         if recipe == synth.G_DYADIC or world == 2:  # NCCL's order depends on the message size

@@ -41,6 +41,15 @@ __global__ void wr1_off(const float* __restrict__ src, float* __restrict__ dst, 
     dst[i + 1] = src[i];
 }
 
+// one-shot fold pattern of p2p.cu: out = local + remote (float4)
+__global__ void fold2(const float4* __restrict__ loc, const float4* __restrict__ rem, float4* __restrict__ out,
+                      size_t n4) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4; i += (size_t)gridDim.x * blockDim.x) {
+    const float4 a = __ldcg(loc + i), b = __ldcg(rem + i);
+    out[i] = make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+  }
+}
+
 int main() {
   int ndev = 0;
   CK(cudaGetDeviceCount(&ndev));
@@ -84,5 +93,31 @@ int main() {
   run("remote WRITE f32 x4/thread strided", [&] { wr1x4<<<grid, blk>>>(a0, a1, n / 4); });
   run("remote WRITE f32 coalesced, +4B offset", [&] { wr1_off<<<grid, blk>>>(a0, a1, n); });
   run("cudaMemcpyPeer GPU0 -> GPU1", [&] { cudaMemcpyPeerAsync(a1, 1, a0, 0, bytes); });
+  run("fold local+remote -> local (remote bytes)", [&] { fold2<<<grid, blk>>>((float4*)a0, (float4*)a1, (float4*)b0, n / 4); });
+  for (size_t mb : {4, 20, 64}) {
+    const size_t nn = (mb << 20) / 16;
+    float best = 1e9;
+    for (int it = 0; it < 10; ++it) {
+      cudaEventRecord(e0);
+      fold2<<<grid, blk>>>((float4*)a0, (float4*)a1, (float4*)b0, nn);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      best = ms < best ? ms : best;
+    }
+    float best_r = 1e9;
+    for (int it = 0; it < 10; ++it) {
+      cudaEventRecord(e0);
+      rd4<<<grid, blk>>>((float4*)a1, (float4*)b0, nn);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      best_r = ms < best_r ? ms : best_r;
+    }
+    printf("%3zu MB: fold %7.1f us (%6.1f GB/s remote), remote read %7.1f us (%6.1f GB/s)\n", mb, best * 1e3,
+           (mb << 20) / (best * 1e-3) / 1e9, best_r * 1e3, (mb << 20) / (best_r * 1e-3) / 1e9);
+  }
   return 0;
 }
