@@ -270,29 +270,43 @@ __global__ void __launch_bounds__(256)
 }
 
 // ---------------------------------------------------------------- bitmap
-// Gather the 32-bit halves of the chunk's 16 words into lanes (lane h holds
-// half h) from per-slot 4-bit nibbles (slot j of lane l -> half
-// 4j + (l >> 3), bits 4*(l & 7)).
-__device__ __forceinline__ uint32_t gather_halves(const uint32_t nib[kVecPerLane]) {
+// Lane-major chunk layout: lane l of the warp classifies the 32 consecutive
+// elements [32l, 32l + 32) of its chunk, so its keep / tie bits ARE the
+// 32-bit half 'l' of the chunk's 16 mask words (no cross-lane bit gather)
+// and in-chunk tie ranks are one warp scan. The chunk is streamed into a
+// per-warp cp.async ring with coalesced 16-byte copies; the shared-memory
+// layout is XOR-swizzled so each lane's eight LDS.128 of its own 128 bytes
+// are conflict-free (unit u of the chunk -> owner u/8, column u%8, stored at
+// owner*8 + (column ^ (owner & 7))).
+constexpr int kKeyStages = 2;
+constexpr int kStageFloats = kChunk + 2 * kChunkWords;  // keys, then the 16 old mask words
+constexpr size_t kBitmapSmem = (size_t)kPruneWarps * kKeyStages * kStageFloats * sizeof(float);
+
+__device__ __forceinline__ void chunk_issue(float* st, const float* __restrict__ w,
+                                            const uint64_t* __restrict__ words, uint64_t c) {
   const int lane = threadIdx.x & 31;
-  uint32_t mine = 0;
+  const float* src = w + c * (uint64_t)kChunk + 4 * lane;
 #pragma unroll
   for (int j = 0; j < kVecPerLane; ++j) {
-    uint32_t x = nib[j] << (4 * (lane & 7));
-    x |= __shfl_xor_sync(0xffffffffu, x, 1);
-    x |= __shfl_xor_sync(0xffffffffu, x, 2);
-    x |= __shfl_xor_sync(0xffffffffu, x, 4);
-    const uint32_t y = __shfl_sync(0xffffffffu, x, (lane & 3) * 8);
-    if ((lane >> 2) == j) mine = y;
+    const int u = 32 * j + lane, owner = u >> 3, col = u & 7;
+    const uint32_t sa =
+        (uint32_t)__cvta_generic_to_shared(st + 4 * (owner * 8 + (col ^ (owner & 7))));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(src + 128 * j) : "memory");
   }
-  return mine;
+  if (lane < kChunkWords / 2) {
+    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(st + kChunk + 4 * lane);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa),
+                 "l"(words + c * kChunkWords + 2 * lane)
+                 : "memory");
+  }
 }
 
-__device__ __forceinline__ uint64_t halves_to_word(uint32_t half) {
-  const int lane = threadIdx.x & 31;
-  const uint32_t lo = __shfl_sync(0xffffffffu, half, (2 * lane) & 31);
-  const uint32_t hi = __shfl_sync(0xffffffffu, half, (2 * lane + 1) & 31);
-  return (uint64_t)lo | ((uint64_t)hi << 32);  // meaningful for lanes 0..15
+// (g << 1) | (k > T), (e << 1) | (k >= T) for keys k, T < 2^31: the sign bit
+// of T - k (resp. T - 1 - k, also right for T = 0) funnel-shifted in, two
+// instructions per mask per element.
+__device__ __forceinline__ void classify_push(uint32_t k, uint32_t T, uint32_t& g, uint32_t& e) {
+  g = __funnelshift_l(T - k, g, 1);
+  e = __funnelshift_l(T - 1u - k, e, 1);
 }
 
 __global__ void __launch_bounds__(kPruneWarps * 32)
@@ -302,78 +316,87 @@ __global__ void __launch_bounds__(kPruneWarps * 32)
                         uint32_t* __restrict__ ties_out, const uint32_t* __restrict__ ties_prev,
                         uint64_t* __restrict__ tie_words, BitmapCounts* __restrict__ counts,
                         uint64_t nchunks) {
+  extern __shared__ __align__(16) float ring_all[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  float* ring = ring_all + (size_t)warp * kKeyStages * kStageFloats;
+  uint32_t* words32 = reinterpret_cast<uint32_t*>(words);
+  uint32_t* tie32 = reinterpret_cast<uint32_t*>(tie_words);
+  const uint64_t nhalves = 2 * nwords;
   const bool vec_ok = (((uintptr_t)w) & 15) == 0;
+  // chunks streamed through the ring: whole 1024-element chunks of an
+  // aligned vector (the ragged last chunk is read directly)
+  auto full = [&](uint64_t c) { return vec_ok && (c + 1) * (uint64_t)kChunk <= len; };
   uint32_t c_lt = 0, c_eq = 0;
   int changed = 0, mismatch = 0;
   const uint64_t nw_total = (uint64_t)gridDim.x * kPruneWarps;
-  for (uint64_t c = (uint64_t)blockIdx.x * kPruneWarps + warp; c < nchunks; c += nw_total) {
-    uint32_t key[kVecPerLane][4], inr[kVecPerLane];
-    load_chunk_keys(w, len, c, vec_ok, key, inr);
-    uint32_t gt[kVecPerLane], eq[kVecPerLane];
-    uint32_t ne = 0;
+  const uint64_t c0 = (uint64_t)blockIdx.x * kPruneWarps + warp;
 #pragma unroll
-    for (int j = 0; j < kVecPerLane; ++j) {
-      // keys and T are < 2^31, so the sign bit of T - k is (k > T) and that
-      // of k - T is (k < T): two subtract/shift/merge per element, no
-      // compares or selects (ncu: ISETP+SEL were 40% of this kernel)
-      uint32_t g = 0, l = 0;
-#pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        const uint32_t kq = key[j][b];
-        g |= ((T - kq) >> (31 - b)) & (1u << b);
-        l |= ((kq - T) >> (31 - b)) & (1u << b);
-      }
-      gt[j] = g & inr[j];
-      l &= inr[j];
-      eq[j] = inr[j] & ~(gt[j] | l);
-      c_lt += __popc(l);
-      ne += __popc(eq[j]);
+  for (int s = 0; s < kKeyStages - 1; ++s) {
+    const uint64_t cc = c0 + s * nw_total;
+    if (cc < nchunks && full(cc)) chunk_issue(ring + s * kStageFloats, w, words, cc);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  int slot = 0;
+  for (uint64_t c = c0; c < nchunks; c += nw_total) {
+    {
+      const uint64_t cn = c + (kKeyStages - 1) * nw_total;
+      const int sn = slot == 0 ? kKeyStages - 1 : slot - 1;
+      if (cn < nchunks && full(cn)) chunk_issue(ring + sn * kStageFloats, w, words, cn);
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      asm volatile("cp.async.wait_group %0;" ::"n"(kKeyStages - 1) : "memory");
     }
-    c_eq += ne;
-    const uint32_t E = warp_sum(ne);
-    uint32_t keep[kVecPerLane];
+    const float* st = ring + slot * kStageFloats;
+    slot = slot == kKeyStages - 1 ? 0 : slot + 1;
+    const bool fc = full(c);
+    uint32_t g = 0, e = 0, inr = ~0u;
+    if (fc) {
 #pragma unroll
-    for (int j = 0; j < kVecPerLane; ++j) keep[j] = gt[j];
-    if (E) {
-      // in-chunk tie ranks in element order (slot j major, lane, bit)
-      uint32_t run = tie_prefix ? __ldg(tie_prefix + c) : 0u;
-#pragma unroll
-      for (int j = 0; j < kVecPerLane; ++j) {
-        const uint32_t cj = __popc(eq[j]);
-        const uint32_t inc = warp_incl_scan(cj);
-        if (tie_prefix) {
-          uint32_t rk = run + inc - cj;
-#pragma unroll
-          for (int b = 0; b < 4; ++b)
-            if ((eq[j] >> b) & 1) {
-              if ((uint64_t)rk >= r) keep[j] |= 1u << b;
-              ++rk;
-            }
-        }
-        run += __shfl_sync(0xffffffffu, inc, 31);
+      for (int k = kVecPerLane - 1; k >= 0; --k) {  // elements 32*lane + 4k .. 4k+3
+        const float4 v =
+            *reinterpret_cast<const float4*>(st + 4 * (lane * 8 + (k ^ (lane & 7))));
+        classify_push(mag_key(v.w), T, g, e);
+        classify_push(mag_key(v.z), T, g, e);
+        classify_push(mag_key(v.y), T, g, e);
+        classify_push(mag_key(v.x), T, g, e);
       }
-      const uint64_t tw = halves_to_word(gather_halves(eq));
-      if (lane < kChunkWords && c * kChunkWords + lane < nwords) tie_words[c * kChunkWords + lane] = tw;
+    } else {
+      const uint64_t e0 = c * (uint64_t)kChunk + 32 * lane;
+      inr = e0 >= len ? 0u : (len - e0 >= 32 ? ~0u : (1u << (len - e0)) - 1u);
+      for (int i = 31; i >= 0; --i)
+        classify_push(e0 + i < len ? mag_key(w[e0 + i]) : 0u, T, g, e);
+    }
+    g &= inr;
+    e &= inr;
+    const uint32_t eqm = e & ~g;
+    c_lt += __popc(inr & ~e);
+    const uint32_t ne = __popc(eqm);
+    c_eq += ne;
+    const uint32_t inc = warp_incl_scan(ne);
+    const uint32_t E = __shfl_sync(0xffffffffu, inc, 31);
+    uint32_t keep = g;
+    const uint64_t hi = c * 32 + lane;  // this lane's 32-bit half of the mask
+    if (E) {
+      if (tie_prefix) {
+        // ties of rank < r (index order) are dropped: the first D of this lane
+        const uint64_t rk0 = (uint64_t)__ldg(tie_prefix + c) + inc - ne;
+        uint32_t d = r > rk0 ? (r - rk0 < ne ? (uint32_t)(r - rk0) : ne) : 0u, x = eqm;
+        for (; d; --d) x &= x - 1;
+        keep |= x;
+      }
+      if (hi < nhalves) tie32[hi] = eqm;
     }
     if (lane == 0) {
       ties_out[c] = E;
       if (ties_prev && ties_prev[c] != E) mismatch = 1;
     }
-    const uint64_t nwv = halves_to_word(gather_halves(keep));
-    uint32_t pc = 0;
-    if (lane < kChunkWords) {
-      const uint64_t wi = c * kChunkWords + lane;
-      if (wi < nwords) {
-        const uint64_t old = words[wi];
-        if (old != nwv) {
-          words[wi] = nwv;
-          changed = 1;
-        }
-        pc = (uint32_t)__popcll(nwv);
+    if (hi < nhalves) {
+      const uint32_t old = fc ? reinterpret_cast<const uint32_t*>(st + kChunk)[lane] : words32[hi];
+      if (old != keep) {
+        words32[hi] = keep;
+        changed = 1;
       }
     }
-    pc = warp_sum(pc);
+    const uint32_t pc = warp_sum((uint32_t)__popc(keep));
     if (lane == 0) chunk_popc[c] = pc;
   }
   c_lt = warp_sum(c_lt);
@@ -577,9 +600,14 @@ void launch_prune_bitmap(const float* w, uint64_t len, uint32_t T, uint64_t r,
   cudaMemsetAsync(counts, 0, sizeof(BitmapCounts), s);
   if (!nc) return;
   static unsigned cap = 0;
-  if (!cap) cap = persistent_grid(prune_bitmap_kernel, kPruneWarps * 32, 0, ~0ull >> 8, kPruneWarps);
+  if (!cap) {
+    cudaFuncSetAttribute(prune_bitmap_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kBitmapSmem);
+    cap = persistent_grid(prune_bitmap_kernel, kPruneWarps * 32, kBitmapSmem, ~0ull >> 8,
+                          kPruneWarps);
+  }
   const uint64_t need = (nc + kPruneWarps - 1) / kPruneWarps;
-  prune_bitmap_kernel<<<(unsigned)(need < cap ? need : cap), kPruneWarps * 32, 0, s>>>(
+  prune_bitmap_kernel<<<(unsigned)(need < cap ? need : cap), kPruneWarps * 32, kBitmapSmem, s>>>(
       w, len, T, r, tie_prefix, words, (len + 63) / 64, chunk_popc, ties_out, ties_prev, tie_words,
       counts, nc);
   note_launch();
