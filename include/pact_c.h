@@ -120,6 +120,10 @@ typedef struct pact_policy {
   int transport;            /* packed exchange: 0 auto, 1 NCCL allreduce, 2 NVLink P2P
                                (peer-memory reduce in the reference fold order, fused
                                with unpack; bit-identical to the reference ring) */
+  int gse_dense;            /* the caller's gradient is NOT yet masked: the dense
+                               fallback applies enforce_gradient_sparsity first, as the
+                               trainer does before aggregating (trainer.cpp:369-372);
+                               the packed path needs nothing (unpack writes +0) */
 } pact_policy;
 
 /* transport values of pact_policy */
@@ -204,6 +208,15 @@ pact_status pact_mask_set_words(pact_mask* m, const uint64_t* words_dev, pact_st
  * the GPU (segment-parallel automaton + affine scan); cached until the words
  * change. Synchronises the stream. */
 pact_status pact_mask_digest(pact_mask* m, pact_stream_t stream, uint64_t* digest_out);
+
+/* Sub-mask view for a DDP bucket (BucketView/flatten,
+ * tensor.hpp:54-74, tensor.cpp:49-79): dst bits [o_s, o_s + seg_len[s]) =
+ * src bits [src_begin[s], src_begin[s] + seg_len[s]), o_s = sum of the
+ * earlier seg_len. dst->len must equal the sum of seg_len and every segment
+ * must lie inside src (else PACT_E_SHAPE_MISMATCH). Host tables; tile
+ * offsets, nnz refreshed (synchronises the stream), digest invalidated. */
+pact_status pact_mask_gather(const pact_mask* src, uint64_t nseg, const uint64_t* src_begin,
+                             const uint64_t* seg_len, pact_mask* dst, pact_stream_t stream);
 
 /* ---------------------------------------------------------------- prune */
 

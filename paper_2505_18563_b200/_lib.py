@@ -40,7 +40,8 @@ class SyncStatsC(C.Structure):
 
 class PolicyC(C.Structure):
     _fields_ = [("density_threshold", C.c_double), ("bucket_bytes", C.c_uint64),
-                ("scale", C.c_float), ("time_stages", C.c_int), ("transport", C.c_int)]
+                ("scale", C.c_float), ("time_stages", C.c_int), ("transport", C.c_int),
+                ("gse_dense", C.c_int)]
 
 
 class MaskInfo(C.Structure):
@@ -78,6 +79,7 @@ SIGNATURES = {
     "pact_mask_fill": (C.c_int, [vp, C.c_int, vp]),
     "pact_mask_set_words": (C.c_int, [vp, vp, vp]),
     "pact_mask_digest": (C.c_int, [vp, vp, u64p]),
+    "pact_mask_gather": (C.c_int, [vp, C.c_uint64, u64p, u64p, vp, vp]),
     "pact_prune_magnitude": (C.c_int, [vp, vp, C.c_uint64, C.c_float, vp, vp, C.POINTER(PruneStats)]),
     "pact_prune_magnitude_segmented": (C.c_int, [vp, vp, C.c_uint64, u64p, C.c_uint64, C.c_float, vp, vp]),
     "pact_gse": (C.c_int, [vp, vp, C.c_uint64, vp, vp, vp]),

@@ -20,7 +20,7 @@ from __future__ import annotations
 import ctypes as C
 import enum
 from dataclasses import dataclass, field
-from typing import Optional, Sequence
+from typing import Optional, Sequence, Tuple
 
 import torch
 
@@ -225,6 +225,20 @@ class SparsityMask:
 
 def mask_digest(mask: SparsityMask) -> int:  # tensor.hpp:110
     return mask.digest()
+
+
+def mask_gather(src: SparsityMask, segments: Sequence[Tuple[int, int]],
+                out: Optional[SparsityMask] = None) -> SparsityMask:
+    """Concatenate bit ranges (begin, length) of `src` into one mask: the mask
+    of a DDP bucket whose parameters sit at those offsets of the flattened
+    model (BucketView/flatten, tensor.hpp:54-74)."""
+    total = sum(int(n) for _, n in segments)
+    m = out if out is not None else SparsityMask(total, src.ctx)
+    nseg = len(segments)
+    begins = (C.c_uint64 * max(1, nseg))(*[int(b) for b, _ in segments])
+    lens = (C.c_uint64 * max(1, nseg))(*[int(n) for _, n in segments])
+    _call(lib.pact_mask_gather, src.handle, nseg, begins, lens, m.handle, _stream())
+    return m
 
 
 # ------------------------------------------------------------------ prune
@@ -450,10 +464,11 @@ class SyncPolicy:
     scale: float = 1.0               # fused into unpack (1/n gives the mean)
     time_stages: bool = False
     transport: int = 0               # 0 auto, 1 NCCL allreduce, 2 NVLink P2P (bit-exact fold order)
+    gse_dense: bool = False          # gradient not yet masked: the dense fallback applies GSE first
 
     def c(self) -> _lib.PolicyC:
         return _lib.PolicyC(self.density_threshold, self.bucket_bytes, self.scale, int(self.time_stages),
-                            int(self.transport))
+                            int(self.transport), int(self.gse_dense))
 
 
 def _stats(s: _lib.SyncStatsC) -> SyncStats:

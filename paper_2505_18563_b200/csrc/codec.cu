@@ -424,6 +424,50 @@ __global__ void __launch_bounds__(1024) scan_excl_kernel(const uint32_t* __restr
   }
 }
 
+
+// Bit-gather of mask segments: dst bits [dst_start[s], dst_start[s+1]) =
+// src bits from src_begin[s]. Thread per destination word; the (few)
+// segments overlapping it are found by binary search over dst_start. The
+// words past the last destination bit are written 0 (whole chunk padding).
+__device__ __forceinline__ uint64_t bits_at(const uint64_t* __restrict__ src, uint64_t nsrc_words,
+                                            uint64_t b) {  // 64 bits of src from bit b
+  const uint64_t w = b >> 6;
+  const int sh = (int)(b & 63);
+  const uint64_t lo = w < nsrc_words ? src[w] : 0ull;
+  if (!sh) return lo;
+  const uint64_t hi = w + 1 < nsrc_words ? src[w + 1] : 0ull;
+  return (lo >> sh) | (hi << (64 - sh));
+}
+
+__global__ void mask_gather_kernel(const uint64_t* __restrict__ src, uint64_t nsrc_words,
+                                   const uint64_t* __restrict__ src_begin,
+                                   const uint64_t* __restrict__ dst_start, uint64_t nseg,
+                                   uint64_t* __restrict__ dst, uint64_t dst_len, uint64_t ndst_words) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < ndst_words; w += stride) {
+    const uint64_t d0 = w * 64, dend = d0 + 64 < dst_len ? d0 + 64 : dst_len;
+    uint64_t out = 0;
+    if (d0 < dst_len) {
+      uint64_t lo = 0, hi = nseg;  // last segment with dst_start <= d0
+      while (hi - lo > 1) {
+        const uint64_t mid = (lo + hi) >> 1;
+        if (dst_start[mid] <= d0) lo = mid; else hi = mid;
+      }
+      for (uint64_t sg = lo, d = d0; d < dend && sg < nseg; ++sg) {
+        const uint64_t se = dst_start[sg + 1];
+        if (se <= d) continue;  // empty segment
+        const uint64_t e = se < dend ? se : dend;
+        const int nb = (int)(e - d), at = (int)(d - d0);
+        uint64_t v = bits_at(src, nsrc_words, src_begin[sg] + (d - dst_start[sg]));
+        if (nb < 64) v &= (1ull << nb) - 1ull;
+        out |= v << at;
+        d = e;
+      }
+    }
+    dst[w] = out;
+  }
+}
+
 }  // namespace
 
 uint64_t launches() { return g_launches; }
@@ -498,6 +542,17 @@ void launch_tile_popc(const uint64_t* words, uint64_t len, uint32_t* popc, cudaS
   const uint64_t nc = (len + kChunk - 1) / kChunk;
   if (!nc) return;
   chunk_popc_kernel<<<(unsigned)((nc * 16 + 255) / 256), 256, 0, s>>>(words, (len + 63) / 64, popc, nc);
+  note_launch();
+}
+
+void launch_mask_gather(const uint64_t* src, uint64_t src_len, const uint64_t* src_begin,
+                        const uint64_t* dst_start, uint64_t nseg, uint64_t* dst, uint64_t dst_len,
+                        uint64_t dst_words_padded, cudaStream_t s) {
+  if (!dst_words_padded) return;
+  uint64_t grid = (dst_words_padded + 255) / 256;
+  if (grid > 8192) grid = 8192;
+  mask_gather_kernel<<<(unsigned)grid, 256, 0, s>>>(src, (src_len + 63) / 64, src_begin, dst_start,
+                                                    nseg, dst, dst_len, dst_words_padded);
   note_launch();
 }
 

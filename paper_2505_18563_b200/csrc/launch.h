@@ -33,6 +33,12 @@ void launch_gse(const float* g, uint64_t len, const uint64_t* words, float* out,
 void launch_mask_fill(uint64_t* words, uint64_t len, int keep, uint32_t* chunk_off, cudaStream_t s);
 void launch_clear_tail(uint64_t* words, uint64_t len, cudaStream_t s);
 void launch_tile_popc(const uint64_t* words, uint64_t len, uint32_t* chunk_popc, cudaStream_t s);
+// dst bits [dst_start[s], dst_start[s+1]) <- src bits from src_begin[s]
+// (device tables, nseg entries + 1 for dst_start); all dst_words_padded
+// words are written (zero past dst_len)
+void launch_mask_gather(const uint64_t* src, uint64_t src_len, const uint64_t* src_begin,
+                        const uint64_t* dst_start, uint64_t nseg, uint64_t* dst, uint64_t dst_len,
+                        uint64_t dst_words_padded, cudaStream_t s);
 // exclusive scan of n u32 -> out[0..n], out[n] = total (single pass, look-back)
 size_t scan_scratch_bytes(uint64_t n);
 void launch_scan_excl(const uint32_t* in, uint64_t n, uint32_t* out, void* scratch, cudaStream_t s);

@@ -696,6 +696,47 @@ pact_status pact_mask_set_words(pact_mask* m, const uint64_t* words_dev, pact_st
   return PACT_OK;
 }
 
+pact_status pact_mask_gather(const pact_mask* src, uint64_t nseg, const uint64_t* src_begin,
+                             const uint64_t* seg_len, pact_mask* dst, pact_stream_t stream) {
+  if (!src || !dst || (nseg && (!src_begin || !seg_len)))
+    return fail(PACT_E_INVALID_ARG, "null mask/segment table");
+  if (src->ctx != dst->ctx) return fail(PACT_E_INVALID_ARG, "masks of different contexts");
+  std::vector<uint64_t> tab(2 * nseg + 1);  // [src_begin x nseg][dst_start x nseg+1]
+  uint64_t total = 0;
+  for (uint64_t i = 0; i < nseg; ++i) {
+    if (src_begin[i] > src->len || seg_len[i] > src->len - src_begin[i])
+      return fail(PACT_E_SHAPE_MISMATCH, "segment %llu [%llu, +%llu) outside the source mask (%llu)",
+                  (unsigned long long)i, (unsigned long long)src_begin[i],
+                  (unsigned long long)seg_len[i], (unsigned long long)src->len);
+    tab[i] = src_begin[i];
+    tab[nseg + i] = total;
+    total += seg_len[i];
+  }
+  tab[2 * nseg] = total;
+  if (total != dst->len)
+    return fail(PACT_E_SHAPE_MISMATCH, "segments cover %llu bits, destination mask has %llu",
+                (unsigned long long)total, (unsigned long long)dst->len);
+  pact_ctx* ctx = dst->ctx;
+  TRY(set_device(ctx));
+  cudaStream_t s = (cudaStream_t)stream;
+  TRY(ctx->seg_ws.ensure(tab.size() * 8));
+  uint64_t* dt = ctx->seg_ws.as<uint64_t>();
+  CUDA_TRY(cudaMemcpyAsync(dt, tab.data(), tab.size() * 8, cudaMemcpyHostToDevice, s));
+  pactk::launch_mask_gather(src->words, src->len, dt, dt + nseg, nseg, dst->words, dst->len,
+                            std::max<uint64_t>(1, dst->ntiles) * (PACT_TILE / 64), s);
+  if (dst->ntiles) {
+    TRY(refresh_offsets(dst, s));
+  } else {
+    CUDA_TRY(cudaStreamSynchronize(s));
+    dst->nnz = 0;
+  }
+  CUDA_TRY(cudaGetLastError());
+  dst->changed = 1;
+  dst->digest_valid = 0;
+  dst->spec_valid = 0;
+  return PACT_OK;
+}
+
 pact_status pact_mask_digest(pact_mask* m, pact_stream_t stream, uint64_t* out) {
   if (!m) return fail(PACT_E_INVALID_ARG, "null mask");
   if (!m->digest_valid) {
@@ -1552,11 +1593,16 @@ pact_status pact_masked_allreduce(pact_comm* c, pact_ctx* ctx, const float* grad
       CUDA_TRY(cudaStreamWaitEvent(s, done, 0));
     }
   } else {
+    const float* src = grad;
+    if (pol.gse_dense && len) {  // trainer.cpp:369-372: GSE before the dense sum
+      pactk::launch_gse(grad, len, m->words, out, s);
+      src = out;
+    }
     if (c) {
-      if (len) NCCL_TRY(ncclAllReduce(grad, out, len, ncclFloat32, ncclSum, c->nccl, s));
+      if (len) NCCL_TRY(ncclAllReduce(src, out, len, ncclFloat32, ncclSum, c->nccl, s));
       if (scale != 1.0f) pactk::launch_scale(out, out, len, scale, s);
-    } else if (scale != 1.0f || out != grad) {
-      pactk::launch_scale(grad, out, len, scale, s);
+    } else if (scale != 1.0f || out != src) {
+      pactk::launch_scale(src, out, len, scale, s);
     }
   }
   CUDA_TRY(cudaGetLastError());

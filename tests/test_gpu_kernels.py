@@ -270,6 +270,50 @@ def test_single_gpu_masked_allreduce(pb, port, cuda):
     assert np.array_equal(u32(oh.numpy()), u32(port.gse(g, w)))
 
 
+def test_dense_fallback_gse(pb, port, cuda):
+    """SyncPolicy.gse_dense: an unmasked gradient aggregated on the dense
+    path equals GSE-then-aggregate (trainer.cpp:369-377), like the packed one."""
+    rng = np.random.default_rng(21)
+    n = 777_777
+    g = rng.standard_normal(n).astype(np.float32)
+    bits = rng.random(n) < 0.3
+    w = words_from_bits(bits)
+    m = pb.SparsityMask.from_words(dev(w.view(np.int64)), n)
+    want = u32(port.to_mean(port.gse(g, w), 4))
+    for status in (pb.TrackerStatus.Unstable, pb.TrackerStatus.Stable):
+        pol = pb.SyncPolicy(scale=0.25, gse_dense=True)
+        gd = dev(g)
+        r = pb.masked_allreduce(gd, m, status, 1, None, policy=pol, out=gd)  # in place, like DDP
+        assert np.array_equal(u32(r.tensor.cpu().numpy()), want), status
+
+
+@pytest.mark.parametrize("src_len", [1, 64, 1000, 4096 * 3 + 17, 2_000_003])
+def test_mask_gather(pb, cuda, src_len):
+    """pact_mask_gather == numpy bit slicing/concatenation (DDP bucket masks)."""
+    rng = np.random.default_rng(src_len)
+    bits = rng.random(src_len) < 0.37
+    src = pb.SparsityMask.from_words(dev(words_from_bits(bits).view(np.int64)), src_len)
+    for trial in range(6):
+        nseg = int(rng.integers(1, 40))
+        segs = []
+        for _ in range(nseg):
+            b = int(rng.integers(0, src_len))
+            ln = int(rng.integers(0, src_len - b + 1)) if trial % 2 else int(rng.integers(0, min(200, src_len - b) + 1))
+            segs.append((b, ln))
+        want = np.concatenate([bits[b:b + ln] for b, ln in segs]) if segs else np.zeros(0, bool)
+        m = pb.api.mask_gather(src, segs)
+        assert m.size() == want.size and m.nnz() == int(want.sum())
+        assert np.array_equal(m.words_host(), words_from_bits(want)), (trial, segs[:3])
+        if want.size:
+            assert m.digest() == pb.SparsityMask.from_bits(want).digest()
+    with pytest.raises(pb.Error) as e:
+        pb.api.mask_gather(src, [(src_len - 1, 2)])
+    assert e.value.code == pb.Errc.ShapeMismatch
+    with pytest.raises(pb.Error) as e:
+        pb.api.mask_gather(src, [(0, 1)], out=pb.SparsityMask(2))
+    assert e.value.code == pb.Errc.ShapeMismatch
+
+
 def test_unpack_sgd_matches_trainer(pb, port, cuda):
     rng = np.random.default_rng(13)
     n = 300_001
