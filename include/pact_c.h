@@ -317,6 +317,39 @@ pact_status pact_masked_allreduce_host(pact_comm* c, pact_ctx* ctx, const float*
                                        const pact_policy* policy, float* out_host,
                                        pact_sync_stats* stats, pact_stream_t stream);
 
+/* ------------------------------------------- ternary-on-packed */
+
+/* Device sign buffer size for `count` values: 4 * ceil(count / 16) bytes. The
+ * first ceil(count / 4) bytes are the reference's sign bytes (codec.hpp:73-78:
+ * element i at byte i >> 2, bits 2 (i & 3); 00 = 0, 01 = +1, 10 = -1); the
+ * rest are zero. */
+uint64_t pact_ternary_sign_bytes(uint64_t count);
+
+/* codec.cpp:50-68 ternarize: *scale_dev = max |v_i| (NaN skipped); element i
+ * keeps its sign iff u_i < |v_i| / scale (double), else 0. u_i is the i-th
+ * draw of a counter-based SplitMix64 stream of `seed` (the reference's
+ * sequential mt19937_64 stream is replaced; see ternary.cu), so results are
+ * exact wherever no draw matters (|v_i| in {0, scale}) and unbiased always. */
+pact_status pact_ternarize(pact_ctx* ctx, const float* values, uint64_t count, uint64_t seed,
+                           float* scale_dev, uint8_t* signs_dev, pact_stream_t stream);
+
+/* codec.cpp:70-75 deternarize with decode_ternary's checks (codec.cpp:324-340:
+ * reserved pattern 11, bits past count, negative / non-finite scale, zero
+ * scale with non-zero signs -> PACT_E_CORRUPT_PAYLOAD). Synchronises. */
+pact_status pact_deternarize(pact_ctx* ctx, const float* scale_dev, const uint8_t* signs_dev,
+                             uint64_t count, float* out, pact_stream_t stream);
+
+/* collective.cpp:311-368 ternary_allgather_aggregate: vote (kind Ternary when
+ * the tracker is stable), then pack -> ternarize -> NCCL all-gather of
+ * (signs, scale) -> per-element double mean over ranks in rank order ->
+ * unpack; any disagreement: dense all-reduce then sum / float(n). Returns
+ * the MEAN. bytes_on_wire follows the reference's ring all-gather of the
+ * frames (+ the ring all-reduce on fallback). Blocks until the decision. */
+pact_status pact_ternary_allgather_aggregate(pact_comm* c, pact_ctx* ctx, const float* grad,
+                                             uint64_t len, pact_mask* m, int tracker_stable,
+                                             uint64_t seed, uint32_t epoch, float* out,
+                                             pact_sync_stats* stats, pact_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

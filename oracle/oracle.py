@@ -106,6 +106,9 @@ class Port:
         L.orc_sgd_step.argtypes = [_f32p, _f32p, C.c_size_t, C.c_float, C.c_void_p]
         L.orc_encode_header.argtypes = [C.c_void_p, _u8p]
         L.orc_decode_header.argtypes = [_u8p, C.c_size_t, C.c_void_p]
+        L.orc_ternarize_ctr.argtypes = [_f32p, C.c_size_t, C.c_uint64, C.POINTER(C.c_float), _u8p]
+        L.orc_ternary_check.argtypes = [C.c_float, _u8p, C.c_size_t]
+        L.orc_ternary_mean.argtypes = [C.c_int, _f32p, C.c_void_p, C.c_size_t, _f32p]
 
     # -- scalar / mask helpers
     def splitmix64(self, x: int) -> int:
@@ -220,6 +223,23 @@ class Port:
         self.L.orc_sgd_step(_f(p), _f(g), p.size, lr, None if w is None else C.cast(_u(w), C.c_void_p))
         return p
 
+    # -- ternary
+    def ternarize(self, v, seed):
+        v = np.ascontiguousarray(v, dtype=np.float32)
+        sc = C.c_float()
+        b = np.zeros(max(1, (v.size + 3) // 4), dtype=np.uint8)
+        self.L.orc_ternarize_ctr(_f(v), v.size, seed & 0xFFFFFFFFFFFFFFFF, C.byref(sc),
+                                 b.ctypes.data_as(_u8p))
+        return sc.value, b[: (v.size + 3) // 4].copy()
+
+    def ternary_mean(self, scales, sign_bytes, count):
+        n = len(scales)
+        sc = np.ascontiguousarray(scales, dtype=np.float32)
+        bs = [np.ascontiguousarray(b if len(b) else np.zeros(1, np.uint8), dtype=np.uint8) for b in sign_bytes]
+        out = np.empty(max(1, count), dtype=np.float32)
+        _check(self.L.orc_ternary_mean(n, _f(sc), C.cast(_ptr_array(bs, C.c_uint8), C.c_void_p), count, _f(out)))
+        return out[:count]
+
     def encode_header(self, kind, epoch, digest, count) -> bytes:
         class H(C.Structure):
             _fields_ = [("kind", C.c_uint8), ("epoch", C.c_uint32), ("mask_digest", C.c_uint64),
@@ -251,6 +271,13 @@ class Ref:
         L.ref_masked_allreduce.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.POINTER(C.c_int),
                                            C.c_void_p, C.c_uint32, C.c_size_t, C.c_void_p,
                                            C.POINTER(C.c_int), _u64p]
+        L.ref_ternarize.argtypes = [_f32p, C.c_size_t, C.c_uint64, C.POINTER(C.c_float), _u8p]
+        L.ref_deternarize.argtypes = [C.c_float, _u8p, C.c_size_t, _f32p]
+        L.ref_decode_ternary.argtypes = [_u8p, C.c_size_t, C.POINTER(C.c_float), _u64p, _u64p, _u8p]
+        L.ref_encode_ternary.argtypes = [C.c_float, _u8p, C.c_size_t, C.c_uint32, C.c_uint64, _u8p,
+                                         C.POINTER(C.c_size_t)]
+        L.ref_ternary_aggregate.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.POINTER(C.c_int), _u64p,
+                                            C.c_uint32, C.c_size_t, C.c_void_p, C.POINTER(C.c_int), _u64p]
         L.ref_bench_create.restype = C.c_void_p
         L.ref_bench_create.argtypes = [C.c_int, C.c_void_p, _u64p, C.c_size_t, C.c_int]
         L.ref_bench_destroy.argtypes = [C.c_void_p]
@@ -360,6 +387,51 @@ class Ref:
             n, C.cast(_ptr_array(grads, C.c_float), C.c_void_p),
             C.cast(_ptr_array(masks, C.c_uint64), C.c_void_p), st,
             None if adv is None else C.cast(_u(adv), C.c_void_p), epoch, ln,
+            C.cast(_ptr_array(outs, C.c_float), C.c_void_p), modes, _u(byts)))
+        return outs, list(modes), [int(b) for b in byts]
+
+    # -- ternary: the reference's own mt19937_64 ternarize
+    def ternarize(self, v, seed):
+        v = np.ascontiguousarray(v, dtype=np.float32)
+        sc = C.c_float()
+        b = np.zeros(max(1, (v.size + 3) // 4), dtype=np.uint8)
+        _check(self.L.ref_ternarize(_f(v), v.size, seed & 0xFFFFFFFFFFFFFFFF, C.byref(sc), b.ctypes.data_as(_u8p)))
+        return sc.value, b[: (v.size + 3) // 4].copy()
+
+    def deternarize(self, scale, sign_bytes, n):
+        b = np.ascontiguousarray(sign_bytes if len(sign_bytes) else np.zeros(1, np.uint8), dtype=np.uint8)
+        out = np.empty(max(1, n), dtype=np.float32)
+        _check(self.L.ref_deternarize(scale, b.ctypes.data_as(_u8p), n, _f(out)))
+        return out[:n]
+
+    def encode_ternary(self, scale, sign_bytes, n, epoch, digest) -> bytes:
+        b = np.ascontiguousarray(sign_bytes if len(sign_bytes) else np.zeros(1, np.uint8), dtype=np.uint8)
+        out = (C.c_uint8 * (30 + (n + 3) // 4))()
+        nb = C.c_size_t()
+        _check(self.L.ref_encode_ternary(scale, b.ctypes.data_as(_u8p), n, epoch, digest, out, C.byref(nb)))
+        return bytes(out)[: nb.value]
+
+    def decode_ternary(self, frame: bytes):
+        """-> (scale, len, digest, sign bytes); raises OracleError(8) on a corrupt frame"""
+        buf = (C.c_uint8 * max(1, len(frame))).from_buffer_copy(frame or b"\0")
+        sc, ln, dg = C.c_float(), C.c_uint64(), C.c_uint64()
+        out = (C.c_uint8 * max(1, len(frame)))()
+        _check(self.L.ref_decode_ternary(buf, len(frame), C.byref(sc), C.byref(ln), C.byref(dg), out))
+        return sc.value, ln.value, dg.value, bytes(out)[: (ln.value + 3) // 4]
+
+    def ternary_aggregate(self, grads, masks, stable, seeds, epoch):
+        n = len(grads)
+        ln = grads[0].size
+        grads = [np.ascontiguousarray(x, dtype=np.float32) for x in grads]
+        masks = [np.ascontiguousarray(m, dtype=np.uint64) for m in masks]
+        outs = [np.empty_like(grads[0]) for _ in range(n)]
+        st = (C.c_int * n)(*[int(bool(x)) for x in stable])
+        sd = np.array([x & 0xFFFFFFFFFFFFFFFF for x in seeds], dtype=np.uint64)
+        modes = (C.c_int * n)()
+        byts = np.zeros(n, dtype=np.uint64)
+        _check(self.L.ref_ternary_aggregate(
+            n, C.cast(_ptr_array(grads, C.c_float), C.c_void_p),
+            C.cast(_ptr_array(masks, C.c_uint64), C.c_void_p), st, _u(sd), epoch, ln,
             C.cast(_ptr_array(outs, C.c_float), C.c_void_p), modes, _u(byts)))
         return outs, list(modes), [int(b) for b in byts]
 

@@ -412,3 +412,61 @@ void orc_sgd_step(float* P, const float* g, size_t len, float lr, const uint64_t
       P[i] -= lr * g[i];
   }
 }
+
+/* ---------------------------------------------------- ternary (8f-2) */
+
+void orc_ternarize_ctr(const float* v, size_t n, uint64_t seed, float* scale_out,
+                       uint8_t* sign_bytes) {
+  /* codec.cpp:50-68 */
+  float s = 0.0f;
+  for (size_t i = 0; i < n; ++i) {
+    const float a = fabsf(v[i]);
+    if (s < a) s = a; /* std::max(s, a): a NaN a leaves s */
+  }
+  *scale_out = s;
+  memset(sign_bytes, 0, (n + 3) / 4);
+  if (s == 0.0f) return;
+  for (size_t i = 0; i < n; ++i) {
+    const double keep_p = (double)fabsf(v[i]) / (double)s;
+    /* SplitMix64 stream: state_i = seed + (i + 1) * golden, output = mix(state_i) */
+    const double u = (double)(orc_splitmix64(seed + (uint64_t)i * 0x9e3779b97f4a7c15ULL) >> 11) *
+                     0x1.0p-53;
+    if (u < keep_p) {
+      const uint8_t pair = v[i] > 0.0f ? 0x1 : 0x2;
+      sign_bytes[i >> 2] |= (uint8_t)(pair << (2 * (i & 3)));
+    }
+  }
+}
+
+static int orc_pair(const uint8_t* b, size_t i) { return (b[i >> 2] >> (2 * (i & 3))) & 3; }
+
+int orc_ternary_check(float scale, const uint8_t* b, size_t count) {
+  /* codec.cpp:330-341 */
+  if (!(scale >= 0.0f) || isinf(scale)) return ORC_CORRUPT_PAYLOAD;
+  const size_t words = (count + 3) / 4;
+  for (size_t i = 0; i < count; ++i)
+    if (orc_pair(b, i) == 3) return ORC_CORRUPT_PAYLOAD;
+  for (size_t i = count; i < words * 4; ++i)
+    if (orc_pair(b, i)) return ORC_CORRUPT_PAYLOAD;
+  if (scale == 0.0f)
+    for (size_t i = 0; i < count; ++i)
+      if (orc_pair(b, i)) return ORC_CORRUPT_PAYLOAD;
+  return ORC_OK;
+}
+
+int orc_ternary_mean(int n, const float* scales, const uint8_t* const* b, size_t count, float* mean) {
+  /* collective.cpp:355-360 */
+  for (int r = 0; r < n; ++r) {
+    const int rc = orc_ternary_check(scales[r], b[r], count);
+    if (rc) return rc;
+  }
+  for (size_t j = 0; j < count; ++j) {
+    double acc = 0.0;
+    for (int r = 0; r < n; ++r) {
+      const int p = orc_pair(b[r], j);
+      acc += (double)scales[r] * (double)(p == 1 ? 1 : (p == 2 ? -1 : 0));
+    }
+    mean[j] = (float)(acc / n);
+  }
+  return ORC_OK;
+}

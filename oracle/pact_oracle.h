@@ -134,6 +134,21 @@ void orc_to_mean(const float* sum, size_t len, int n, float* mean);
 void orc_sgd_step(float* params, const float* mean_grad, size_t len, float lr,
                   const uint64_t* words_or_null);
 
+/* ------------------------------------------------- ternary */
+
+/* codec.cpp:50-68 ternarize with the product's counter-based draws: u_i =
+ * (splitmix64(seed + i * 0x9e3779b97f4a7c15) >> 11) * 2^-53 (the i-th output
+ * of a SplitMix64 stream seeded with `seed`) instead of the i-th mt19937_64
+ * draw. sign_bytes: ceil(n/4) bytes, reference layout (codec.hpp:73-78). */
+void orc_ternarize_ctr(const float* v, size_t n, uint64_t seed, float* scale_out,
+                       uint8_t* sign_bytes);
+/* codec.cpp:320-343 decode checks on (scale, sign bytes, count) */
+int orc_ternary_check(float scale, const uint8_t* sign_bytes, size_t count);
+/* collective.cpp:355-360: mean[j] = float(sum_r double(scale_r) * sign_r(j) / n),
+ * ranks in order */
+int orc_ternary_mean(int n, const float* scales, const uint8_t* const* sign_bytes, size_t count,
+                     float* mean);
+
 #ifdef __cplusplus
 }
 #endif

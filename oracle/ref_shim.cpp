@@ -203,6 +203,72 @@ int ref_masked_allreduce(int n, const float* const* grads, const uint64_t* const
   });
 }
 
+// ------------------------------------------------- ternary
+
+int ref_ternarize(const float* v, size_t n, uint64_t seed, float* scale_out, uint8_t* sign_bytes) {
+  return guarded([&] {
+    TernaryGradient t = ternarize(FlatTensor(std::vector<float>(v, v + n)), seed);
+    *scale_out = t.scale;
+    std::memcpy(sign_bytes, t.sign_words.data(), t.sign_words.size());
+  });
+}
+
+int ref_deternarize(float scale, const uint8_t* sign_bytes, size_t n, float* out) {
+  return guarded([&] {
+    TernaryGradient t;
+    t.scale = scale;
+    t.len = n;
+    t.sign_words.assign(sign_bytes, sign_bytes + (n + 3) / 4);
+    FlatTensor d = deternarize(t);
+    std::memcpy(out, d.data(), n * sizeof(float));
+  });
+}
+
+// wire::decode_ternary on a raw frame; scale/len/digest out, sign bytes copied
+int ref_decode_ternary(const uint8_t* frame, size_t bytes, float* scale, uint64_t* len,
+                       uint64_t* digest, uint8_t* sign_bytes) {
+  return guarded([&] {
+    wire::Bytes b(bytes);
+    std::memcpy(b.data(), frame, bytes);
+    uint64_t d = 0;
+    TernaryGradient t = wire::decode_ternary(b, &d);
+    *scale = t.scale;
+    *len = t.len;
+    *digest = d;
+    if (sign_bytes) std::memcpy(sign_bytes, t.sign_words.data(), t.sign_words.size());
+  });
+}
+
+int ref_encode_ternary(float scale, const uint8_t* sign_bytes, size_t n, uint32_t epoch,
+                       uint64_t digest, uint8_t* out, size_t* out_bytes) {
+  return guarded([&] {
+    TernaryGradient t;
+    t.scale = scale;
+    t.len = n;
+    t.sign_words.assign(sign_bytes, sign_bytes + (n + 3) / 4);
+    wire::Bytes b = wire::encode_ternary(t, epoch, digest);
+    std::memcpy(out, b.data(), b.size());
+    *out_bytes = b.size();
+  });
+}
+
+// ternary_allgather_aggregate over SimCluster (collective.cpp:311-368)
+int ref_ternary_aggregate(int n, const float* const* grads, const uint64_t* const* masks,
+                          const int* stable, const uint64_t* seeds, uint32_t epoch, size_t len,
+                          float* const* out, int* mode_out, uint64_t* bytes_out) {
+  return guarded([&] {
+    run_workers(n, [&](int r, Comm& c) {
+      AggregateResult a = ternary_allgather_aggregate(
+          FlatTensor(std::vector<float>(grads[r], grads[r] + len)),
+          SparsityMask::from_bits(bits_of(masks[r], len)),
+          stable[r] ? TrackerStatus::Stable : TrackerStatus::Unstable, seeds[r], epoch, c);
+      std::memcpy(out[r], a.tensor.data(), len * sizeof(float));
+      mode_out[r] = static_cast<int>(a.stats.mode_used);
+      bytes_out[r] = a.stats.bytes_on_wire;
+    });
+  });
+}
+
 // ---------------------------------------------------------------------------
 // CPU baseline arm: prepared inputs so only the reference call is timed.
 // ---------------------------------------------------------------------------

@@ -20,17 +20,22 @@ from .api import (  # noqa: F401
     SyncMode,
     SyncPolicy,
     SyncStats,
+    TernaryGradient,
     TrackerStatus,
     allgather,
     build_prune_mask,
     decide_sync_mode,
     decode_header,
+    decode_ternary,
+    deternarize,
     drop_count,
     encode_header,
+    encode_ternary,
     enforce_gradient_sparsity,
     full_allreduce,
     magnitude_prune,
     magnitude_prune_per_layer,
+    mask_gather,
     mask_digest,
     masked_allreduce,
     masked_allreduce_host,
@@ -39,6 +44,8 @@ from .api import (  # noqa: F401
     ring_allreduce,
     ring_bytes,
     synth_fill,
+    ternarize,
+    ternary_allgather_aggregate,
     tracker_observe,
     unpack,
     unpack_sgd,

@@ -98,6 +98,11 @@ SIGNATURES = {
     "pact_full_allreduce": (C.c_int, [vp, vp, vp, C.c_uint64, C.c_float, C.POINTER(SyncStatsC), vp]),
     "pact_masked_allreduce": (C.c_int, [vp, vp, vp, C.c_uint64, vp, C.c_int, C.c_uint32, u64p,
                                         C.POINTER(PolicyC), vp, C.POINTER(SyncStatsC), vp]),
+    "pact_ternary_sign_bytes": (C.c_uint64, [C.c_uint64]),
+    "pact_ternarize": (C.c_int, [vp, vp, C.c_uint64, C.c_uint64, vp, vp, vp]),
+    "pact_deternarize": (C.c_int, [vp, vp, vp, C.c_uint64, vp, vp]),
+    "pact_ternary_allgather_aggregate": (C.c_int, [vp, vp, vp, C.c_uint64, vp, C.c_int, C.c_uint64,
+                                                   C.c_uint32, vp, C.POINTER(SyncStatsC), vp]),
     "pact_masked_allreduce_host": (C.c_int, [vp, vp, vp, C.c_uint64, vp, C.c_int, C.c_uint32, u64p,
                                              C.POINTER(PolicyC), vp, C.POINTER(SyncStatsC), vp]),
 }

@@ -370,6 +370,52 @@ def unpack_sgd(packed_values: torch.Tensor, mask: SparsityMask, scale: float, lr
           mask.handle, C.c_float(scale), C.c_float(lr), _ptr(grad_out), _ptr(weights), _stream())
 
 
+@dataclass
+class TernaryGradient:  # codec.hpp:32-40
+    """Device ternary payload: ``scale`` (host float, also ``scale_dev``) and
+    ``signs`` (device uint8, pact_ternary_sign_bytes(len) bytes whose first
+    ceil(len/4) are the reference's ``sign_words``)."""
+    scale: float = 0.0
+    len: int = 0
+    signs: Optional[torch.Tensor] = None
+    scale_dev: Optional[torch.Tensor] = None
+
+    def sign_words(self) -> bytes:
+        return bytes(self.signs[: (self.len + 3) // 4].cpu().numpy().tobytes()) if self.len else b""
+
+    def sign_at(self, i: int) -> int:  # codec.cpp:40-48
+        pair = (self.sign_words()[i >> 2] >> (2 * (i & 3))) & 3
+        if pair == 3:
+            raise Error(Errc.CorruptPayload, "reserved ternary sign pattern 11")
+        return (0, 1, -1)[pair]
+
+
+def ternary_sign_bytes(count: int) -> int:
+    return int(lib.pact_ternary_sign_bytes(int(count)))
+
+
+def ternarize(grad: torch.Tensor, seed: int) -> TernaryGradient:  # codec.cpp:50-68
+    """Stochastic ternarization on the GPU; draws from a counter-based
+    SplitMix64 stream of ``seed`` (the reference's mt19937_64 stream is
+    sequential; the distribution and every draw-independent result match)."""
+    g = _as_grad(grad, "grad")
+    signs = torch.empty(max(16, ternary_sign_bytes(g.numel())), dtype=torch.uint8, device=g.device)
+    sc = torch.empty(1, dtype=torch.float32, device=g.device)
+    _call(lib.pact_ternarize, Context.get(g.device.index).handle, _ptr(g), g.numel(),
+          C.c_uint64(int(seed) & 0xFFFFFFFFFFFFFFFF), _ptr(sc), _ptr(signs), _stream())
+    return TernaryGradient(float(sc.item()), g.numel(), signs, sc)
+
+
+def deternarize(t: TernaryGradient, out: Optional[torch.Tensor] = None) -> torch.Tensor:  # codec.cpp:70-75
+    dev = t.signs.device if t.signs is not None else torch.device("cuda", torch.cuda.current_device())
+    o = torch.empty(t.len, dtype=torch.float32, device=dev) if out is None else out
+    sc = t.scale_dev if t.scale_dev is not None else torch.tensor([t.scale], dtype=torch.float32, device=dev)
+    signs = t.signs if t.signs is not None else torch.zeros(16, dtype=torch.uint8, device=dev)
+    _call(lib.pact_deternarize, Context.get(dev.index).handle, _ptr(sc), _ptr(signs), t.len, _ptr(o),
+          _stream())
+    return o
+
+
 class PayloadKind(enum.IntEnum):  # codec.hpp:80-86
     Full = 0
     Packed = 1
@@ -398,6 +444,42 @@ def decode_header(frame: bytes) -> FrameHeader:  # codec.cpp:261-275
     ch = _lib.FrameHeader()
     _call(lib.pact_header_decode, buf, len(frame), C.byref(ch))
     return FrameHeader(PayloadKind(ch.kind), ch.epoch, ch.mask_digest, ch.value_count)
+
+
+def encode_ternary(t: TernaryGradient, epoch: int, mask_digest: int) -> bytes:  # codec.cpp:313-318
+    import struct
+
+    return (encode_header(FrameHeader(PayloadKind.Ternary, epoch, mask_digest, t.len))
+            + struct.pack("<f", t.scale) + t.sign_words())
+
+
+def decode_ternary(frame: bytes) -> Tuple[TernaryGradient, int]:  # codec.cpp:320-343
+    """Host decode with the reference's checks; returns (ternary with HOST
+    sign bytes in ``signs`` as a CPU uint8 tensor, mask digest)."""
+    import math
+    import struct
+
+    h = decode_header(frame)
+    if h.kind != PayloadKind.Ternary:
+        raise Error(Errc.CorruptPayload, "not a ternary frame")
+    words = (h.value_count + 3) // 4
+    if len(frame) < 26 + 4 + words:
+        raise Error(Errc.CorruptPayload, "frame truncated")
+    scale = struct.unpack_from("<f", frame, 26)[0]
+    if not (scale >= 0.0) or not math.isfinite(scale):
+        raise Error(Errc.CorruptPayload, "negative or non-finite ternary scale")
+    sw = bytes(frame[30:30 + words])
+    import numpy as np
+
+    b = np.frombuffer(sw, dtype=np.uint8)
+    pairs = ((b[:, None] >> np.array([0, 2, 4, 6], dtype=np.uint8)) & 3).reshape(-1)
+    if (pairs[: h.value_count] == 3).any():
+        raise Error(Errc.CorruptPayload, "reserved ternary sign pattern 11")
+    if pairs[h.value_count:].any():
+        raise Error(Errc.CorruptPayload, "sign bits past payload length")
+    if scale == 0.0 and pairs.any():
+        raise Error(Errc.CorruptPayload, "zero scale with non-zero signs")
+    return TernaryGradient(scale, int(h.value_count), torch.from_numpy(b.copy())), int(h.mask_digest)
 
 
 # -------------------------------------------------------------- collective
@@ -573,6 +655,21 @@ def masked_allreduce_host(grad_host: torch.Tensor, mask: SparsityMask, tracker: 
           _ptr(grad_host), grad_host.numel(), mask.handle, int(tracker == TrackerStatus.Stable),
           int(epoch), None, C.byref(pol), _ptr(out_host), C.byref(st), _stream())
     return _stats(st)
+
+
+def ternary_allgather_aggregate(grad: torch.Tensor, mask: SparsityMask, tracker: TrackerStatus, seed: int,
+                                epoch: int, comm: Optional[Comm],
+                                out: Optional[torch.Tensor] = None) -> AggregateResult:
+    """collective.cpp:311-368: pack -> ternarize -> all-gather -> mean ->
+    unpack on a unanimous stable vote, else dense all-reduce / n. Returns
+    the MEAN."""
+    g = _as_grad(grad, "grad")
+    o = torch.empty_like(g) if out is None else out
+    st = _lib.SyncStatsC()
+    _call(lib.pact_ternary_allgather_aggregate, comm.handle if comm is not None else None, mask.ctx.handle,
+          _ptr(g), g.numel(), mask.handle, int(tracker == TrackerStatus.Stable),
+          C.c_uint64(int(seed) & 0xFFFFFFFFFFFFFFFF), int(epoch), _ptr(o), C.byref(st), _stream())
+    return AggregateResult(o, _stats(st))
 
 
 def synth_fill(x: torch.Tensor, seed: int, recipe: int, scale: float = 1.0, index_base: int = 0) -> torch.Tensor:

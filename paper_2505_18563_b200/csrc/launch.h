@@ -118,6 +118,21 @@ void launch_prune_seg_tiefix(uint64_t* words, uint64_t len, const uint64_t* tie_
                              const uint32_t* word_prefix, const uint64_t* seg, uint64_t nseg,
                              uint64_t* seg_base, const uint64_t* rseg, cudaStream_t s);
 
+// ---- ternary.cu -------------------------------------------------------------
+// x[i] = x[i] / d (IEEE division; the gather paths' `sum / float(n)`)
+void launch_div(float* x, uint64_t n, float d, cudaStream_t s);
+// *out_bits = bits of max |v_i| over non-NaN v (0 for n = 0)
+void launch_absmax(const float* v, uint64_t n, unsigned* out_bits, cudaStream_t s);
+// signs[ceil(n/16)] u32: element i keeps sign(v_i) iff u_i < |v_i| / max,
+// u_i the i-th SplitMix64 draw of `seed`
+void launch_ternarize(const float* v, uint64_t n, const unsigned* smax_bits, uint64_t seed,
+                      uint32_t* signs, cudaStream_t s);
+// out[i] = float(sum_r double(scales[r*scale_stride]) * sign_r(i) / n), sign
+// words of rank r at signs + r*sign_stride; decode errors OR-ed into *err
+void launch_ternary_mean(const uint32_t* signs, uint64_t sign_stride, const float* scales,
+                         uint64_t scale_stride, int n, uint64_t count, float* out, int* err,
+                         cudaStream_t s);
+
 // ---- digest.cu -------------------------------------------------------------
 // FNV-1a-64 over the LE bytes of nwords words; scratch sized by
 // digest_scratch_bytes(nwords). Result written to *out_dev.

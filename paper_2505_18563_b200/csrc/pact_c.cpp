@@ -135,6 +135,7 @@ struct pact_ctx {
   DevBuf digest_scratch;
   DevBuf packed;    // packed gradient for masked_allreduce
   DevBuf grad_stage, out_stage;  // e2e host path staging
+  DevBuf tern;      // ternary: [smax u32][err i32][pad][own block][n gathered blocks]
   HostBuf pin;      // small pinned readbacks
   cudaStream_t aux[2] = {nullptr, nullptr};  // comm / unpack streams for bucket overlap
   std::vector<cudaEvent_t> ev_pool;
@@ -586,7 +587,7 @@ pact_status pact_ctx_destroy(pact_ctx* ctx) {
   cudaSetDevice(ctx->device);
   cudaDeviceSynchronize();
   for (DevBuf* b : {&ctx->ws_small, &ctx->cand, &ctx->state, &ctx->seg_ws, &ctx->digest_scratch, &ctx->packed,
-                    &ctx->grad_stage, &ctx->out_stage})
+                    &ctx->grad_stage, &ctx->out_stage, &ctx->tern})
     b->release();
   ctx->pin.release();
   for (auto s : ctx->aux)
@@ -1630,6 +1631,166 @@ pact_status pact_masked_allreduce(pact_comm* c, pact_ctx* ctx, const float* grad
         stats->t_unpack = d * 1e-3;
       }
     }
+  }
+  return PACT_OK;
+}
+
+// ------------------------------------------------------------ ternary
+
+uint64_t pact_ternary_sign_bytes(uint64_t count) { return 4 * ((count + 15) / 16); }
+
+namespace {
+// [smax][err][pad x2][own block][gathered blocks]; block = W signs + scale + 3 pad
+struct TernWs {
+  unsigned* smax;
+  int* err;
+  uint32_t* own;
+  uint32_t* all;
+  uint64_t W, blk;
+};
+pact_status tern_ws(pact_ctx* ctx, uint64_t count, int n, TernWs* t) {
+  t->W = (count + 15) / 16;
+  t->blk = t->W + 4;
+  TRY(ctx->tern.ensure((4 + t->blk * (uint64_t)(n + 1)) * 4));
+  uint32_t* b = ctx->tern.as<uint32_t>();
+  t->smax = b;
+  t->err = reinterpret_cast<int*>(b + 1);
+  t->own = b + 4;
+  t->all = t->own + t->blk;
+  return PACT_OK;
+}
+pact_status tern_check(pact_ctx* ctx, int* err_dev, cudaStream_t s) {
+  int* pin = ctx->pin.as<int>();
+  CUDA_TRY(cudaMemcpyAsync(pin, err_dev, 4, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  if (pin[0])
+    return fail(PACT_E_CORRUPT_PAYLOAD, "ternary payload rejected (flags 0x%x: 1 reserved pattern, "
+                "2 bits past length, 4 bad scale, 8 zero scale with signs)", pin[0]);
+  return PACT_OK;
+}
+}  // namespace
+
+pact_status pact_ternarize(pact_ctx* ctx, const float* values, uint64_t count, uint64_t seed,
+                           float* scale_dev, uint8_t* signs_dev, pact_stream_t stream) {
+  if (!ctx || (count && (!values || !signs_dev)) || !scale_dev)
+    return fail(PACT_E_INVALID_ARG, "null args");
+  TRY(set_device(ctx));
+  cudaStream_t s = stream;
+  TernWs t;
+  TRY(tern_ws(ctx, count, 1, &t));
+  pactk::launch_absmax(values, count, t.smax, s);
+  pactk::launch_ternarize(values, count, t.smax, seed, reinterpret_cast<uint32_t*>(signs_dev), s);
+  CUDA_TRY(cudaMemcpyAsync(scale_dev, t.smax, 4, cudaMemcpyDeviceToDevice, s));
+  CUDA_TRY(cudaGetLastError());
+  return PACT_OK;
+}
+
+pact_status pact_deternarize(pact_ctx* ctx, const float* scale_dev, const uint8_t* signs_dev,
+                             uint64_t count, float* out, pact_stream_t stream) {
+  if (!ctx || !scale_dev || (count && (!signs_dev || !out))) return fail(PACT_E_INVALID_ARG, "null args");
+  TRY(set_device(ctx));
+  cudaStream_t s = stream;
+  TernWs t;
+  TRY(tern_ws(ctx, count, 1, &t));
+  CUDA_TRY(cudaMemsetAsync(t.err, 0, 4, s));
+  pactk::launch_ternary_mean(reinterpret_cast<const uint32_t*>(signs_dev), 0, scale_dev, 0, 1, count,
+                             out, t.err, s);
+  CUDA_TRY(cudaGetLastError());
+  return tern_check(ctx, t.err, s);
+}
+
+pact_status pact_ternary_allgather_aggregate(pact_comm* c, pact_ctx* ctx, const float* grad,
+                                             uint64_t len, pact_mask* m, int tracker_stable,
+                                             uint64_t seed, uint32_t epoch, float* out,
+                                             pact_sync_stats* stats, pact_stream_t stream) {
+  if (!ctx || !m) return fail(PACT_E_INVALID_ARG, "null ctx/mask");
+  if (c && c->ctx != ctx) return fail(PACT_E_INVALID_ARG, "comm belongs to another ctx");
+  if (len != m->len)  // collective.cpp:314
+    return fail(PACT_E_SHAPE_MISMATCH, "gradient/mask length mismatch (%llu vs %llu)",
+                (unsigned long long)len, (unsigned long long)m->len);
+  TRY(set_device(ctx));
+  TRY(ensure_ctx_ws(ctx));
+  cudaStream_t s = stream;
+  const int n = c ? c->n : 1;
+  CUDA_TRY(cudaEventRecord(ctx->t0, s));
+  // vote frame (collective.cpp:321-331): Ternary when stable, a bare Full header otherwise
+  const int stable = pact_decide_sync_mode(PACT_SYNC_TERNARY, tracker_stable) == PACT_SYNC_TERNARY;
+  uint64_t digest = 0;
+  TRY(pact_mask_digest(m, s, &digest));
+  pact_frame_header mine{(uint8_t)(stable ? PACT_KIND_TERNARY : PACT_KIND_FULL), epoch, digest, m->nnz};
+  uint8_t frame[PACT_HEADER_BYTES];
+  TRY(pact_header_encode(&mine, frame));
+  std::vector<uint8_t> frames;
+  if (c) {
+    if (c->shm) {
+      TRY(shm_vote(c, frame, frames));
+    } else {
+      TRY(post_vote(c, frame, ctx->aux[0]));
+      TRY(wait_vote(c, frames));
+    }
+  } else {
+    frames.assign(frame, frame + PACT_HEADER_BYTES);
+  }
+  // collective.cpp:334-346: every frame Ternary with this digest and length
+  int agree = stable;
+  uint64_t wire = 0;
+  for (int q = 0; q < n; ++q) {
+    pact_frame_header h;
+    TRY(pact_header_decode(frames.data() + (size_t)q * PACT_HEADER_BYTES, PACT_HEADER_BYTES, &h));
+    if (h.kind != PACT_KIND_TERNARY || h.mask_digest != digest || h.value_count != m->nnz) agree = 0;
+  }
+  if (c)  // ring all-gather of the frames (collective.cpp:222-247): n-1 rounds
+    for (int st = 0; st < n - 1; ++st) {
+      pact_frame_header h;
+      TRY(pact_header_decode(frames.data() + (size_t)imod(c->rank - st, n) * PACT_HEADER_BYTES,
+                             PACT_HEADER_BYTES, &h));
+      wire += PACT_HEADER_BYTES + (h.kind == PACT_KIND_TERNARY ? 4 + (h.value_count + 3) / 4 : 0);
+    }
+  if (agree) {
+    const uint64_t nnz = m->nnz;
+    TRY(ctx->packed.ensure(std::max<uint64_t>(1, nnz) * 4));
+    float* packed = ctx->packed.as<float>();
+    TernWs t;
+    TRY(tern_ws(ctx, nnz, n, &t));
+    CUDA_TRY(cudaMemsetAsync(t.err, 0, 4, s));
+    pactk::launch_pack(grad, len, m->words, m->tile_off, packed, 0, m->ntiles, s);
+    pactk::launch_absmax(packed, nnz, t.smax, s);
+    pactk::launch_ternarize(packed, nnz, t.smax, seed, t.own, s);
+    CUDA_TRY(cudaMemcpyAsync(t.own + t.W, t.smax, 4, cudaMemcpyDeviceToDevice, s));
+    const uint32_t* blocks = t.own;
+    if (c) {
+      NCCL_TRY(ncclAllGather(t.own, t.all, t.blk * 4, ncclUint8, c->nccl, s));
+      blocks = t.all;
+    }
+    // the mean of the packed values, written over them (collective.cpp:355-360)
+    pactk::launch_ternary_mean(blocks, t.blk, reinterpret_cast<const float*>(blocks + t.W), t.blk, n,
+                               nnz, packed, t.err, s);
+    pactk::launch_unpack(packed, len, m->words, m->tile_off, 1.0f, 0, out, 0, m->ntiles, s);
+    CUDA_TRY(cudaGetLastError());
+    TRY(tern_check(ctx, t.err, s));
+  } else {
+    // collective.cpp:348-353: full ring all-reduce, then sum / float(n)
+    if (c) {
+      if (len) NCCL_TRY(ncclAllReduce(grad, out, len, ncclFloat32, ncclSum, c->nccl, s));
+      pactk::launch_div(out, len, (float)n, s);
+      wire += pact_ring_bytes(n, c->rank, len);
+    } else if (out != grad && len) {
+      CUDA_TRY(cudaMemcpyAsync(out, grad, len * 4, cudaMemcpyDeviceToDevice, s));
+    }
+    CUDA_TRY(cudaGetLastError());
+  }
+  if (stats) {
+    CUDA_TRY(cudaEventRecord(ctx->t1, s));
+    CUDA_TRY(cudaEventSynchronize(ctx->t1));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, ctx->t0, ctx->t1);
+    *stats = pact_sync_stats{};
+    stats->bytes_on_wire = wire;
+    stats->seconds = ms * 1e-3;
+    stats->mode_used = agree ? PACT_SYNC_TERNARY : PACT_SYNC_FULL;
+    stats->value_count = agree ? m->nnz : len;
+    stats->fallback_reason = agree ? 0 : (stable ? 2 : 1);
+    stats->transport = c ? PACT_TRANSPORT_NCCL : 0;
   }
   return PACT_OK;
 }

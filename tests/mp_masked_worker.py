@@ -150,6 +150,38 @@ def main():
     check("host: packed", st.mode_used == pb.SyncMode.PackedAllReduce)
     check("host: exact", np.array_equal(u32(oh.numpy()), u32(gse_outs[rank])))
 
+    # ---- ternary-on-packed (collective.cpp:311-368), SURVEY 8f-2
+    nnz = int(bits.sum())
+    seeds = [port.derive_seed(0x7E, r, 11) for r in range(world)]
+    grads = [synth.synth_host(n, synth.grad_seed(r, 12), synth.G_FULL) for r in range(world)]
+    g = torch.from_numpy(grads[rank]).to(dev)
+    rt = pb.ternary_allgather_aggregate(g, mask, pb.TrackerStatus.Stable, seeds[rank], 11, comm)
+    tern = [port.ternarize(port.pack(x, words), sd) for x, sd in zip(grads, seeds)]
+    want = port.unpack(port.ternary_mean([t[0] for t in tern], [t[1] for t in tern], nnz),
+                       port.mask_digest(words, n), words, n)
+    check("ternary: mode", rt.stats.mode_used == pb.SyncMode.TernaryAllGather)
+    check("ternary: bit-exact vs oracle", np.array_equal(u32(rt.tensor.cpu().numpy()), u32(want)))
+    check("ternary: bytes", rt.stats.bytes_on_wire == (world - 1) * (30 + (nnz + 3) // 4))
+    if oracle.ref_available():  # draw-independent inputs: the reference itself
+        R = oracle.ref()
+        sat = [port.gse(np.where(np.arange(n) % 3 == r % 3, 0.0, (r + 1.0) * np.sign(x)).astype(np.float32),
+                        words) for r, x in enumerate(grads)]
+        outs, modes, byts = R.ternary_aggregate(sat, [words] * world, [1] * world, seeds, 11)
+        rs = pb.ternary_allgather_aggregate(torch.from_numpy(sat[rank]).to(dev), mask, pb.TrackerStatus.Stable,
+                                            seeds[rank], 11, comm)
+        check("ternary: saturated == reference",
+              np.array_equal(u32(rs.tensor.cpu().numpy()), u32(outs[rank])) and modes[rank] == 2)
+        check("ternary: bytes == reference", rs.stats.bytes_on_wire == byts[rank])
+        stable = [1] * world
+        stable[0] = 0
+        outs, modes, byts = R.ternary_aggregate(grads, [words] * world, stable, seeds, 12)
+        rf = pb.ternary_allgather_aggregate(g, mask, pb.TrackerStatus.Stable if stable[rank] else
+                                            pb.TrackerStatus.Unstable, seeds[rank], 12, comm)
+        check("ternary fallback: mode", rf.stats.mode_used == pb.SyncMode.FullAllReduce and modes[rank] == 0)
+        check("ternary fallback: bytes == reference", rf.stats.bytes_on_wire == byts[rank])
+        if world == 2:  # NCCL's sum is order-free only for two ranks
+            check("ternary fallback: == reference", np.array_equal(u32(rf.tensor.cpu().numpy()), u32(outs[rank])))
+
     flag = torch.tensor([len(failures)], device=dev)
     dist.all_reduce(flag)
     comm.close()
