@@ -120,6 +120,10 @@ typedef struct pact_policy {
   int transport;            /* packed exchange: 0 auto, 1 NCCL allreduce, 2 NVLink P2P
                                (peer-memory reduce in the reference fold order, fused
                                with unpack; bit-identical to the reference ring) */
+  int wire;                 /* packed exchange payload: PACT_WIRE_F32 (0, the reference's
+                               masked_allreduce) or PACT_WIRE_F16 (binary16 ring with
+                               per-hop re-rounding, F16Wire collective.cpp:133-163, on the
+                               packed values) */
   int gse_dense;            /* the caller's gradient is NOT yet masked: the dense
                                fallback applies enforce_gradient_sparsity first, as the
                                trainer does before aggregating (trainer.cpp:369-372);
@@ -130,6 +134,9 @@ typedef struct pact_policy {
 #define PACT_TRANSPORT_AUTO 0
 #define PACT_TRANSPORT_NCCL 1
 #define PACT_TRANSPORT_P2P 2
+/* wire values of pact_policy */
+#define PACT_WIRE_F32 0
+#define PACT_WIRE_F16 1
 
 typedef struct pact_mask_info {
   uint64_t len;
@@ -316,6 +323,19 @@ pact_status pact_masked_allreduce_host(pact_comm* c, pact_ctx* ctx, const float*
                                        const uint64_t* advertised_digest,
                                        const pact_policy* policy, float* out_host,
                                        pact_sync_stats* stats, pact_stream_t stream);
+
+/* ------------------------------------------------- binary16 wire */
+
+/* codec.cpp:142-146 fp16_roundtrip with the reference's hand-rolled RNE and
+ * clamping (codec.cpp:79-140); out may alias in. */
+pact_status pact_fp16_roundtrip(pact_ctx* ctx, const float* in, float* out, uint64_t len,
+                                pact_stream_t stream);
+
+/* collective.cpp:261-267 fp16_allreduce: the dense ring with binary16 chunks
+ * re-rounded at every hop (F16Wire), bit-identical to ring_allreduce_fp16 on
+ * every rank; SUM. comm NULL: the single owner's rounding. */
+pact_status pact_fp16_allreduce(pact_comm* c, pact_ctx* ctx, const float* grad, float* out,
+                                uint64_t len, pact_sync_stats* stats, pact_stream_t stream);
 
 /* ------------------------------------------- ternary-on-packed */
 

@@ -106,6 +106,9 @@ class Port:
         L.orc_sgd_step.argtypes = [_f32p, _f32p, C.c_size_t, C.c_float, C.c_void_p]
         L.orc_encode_header.argtypes = [C.c_void_p, _u8p]
         L.orc_decode_header.argtypes = [_u8p, C.c_size_t, C.c_void_p]
+        L.orc_float_to_half.argtypes = [_f32p, C.c_size_t, C.POINTER(C.c_uint16)]
+        L.orc_half_to_float.argtypes = [C.POINTER(C.c_uint16), C.c_size_t, _f32p]
+        L.orc_ring_allreduce_fp16.argtypes = [C.c_int, C.c_void_p, C.c_size_t, C.c_void_p]
         L.orc_ternarize_ctr.argtypes = [_f32p, C.c_size_t, C.c_uint64, C.POINTER(C.c_float), _u8p]
         L.orc_ternary_check.argtypes = [C.c_float, _u8p, C.c_size_t]
         L.orc_ternary_mean.argtypes = [C.c_int, _f32p, C.c_void_p, C.c_size_t, _f32p]
@@ -223,6 +226,27 @@ class Port:
         self.L.orc_sgd_step(_f(p), _f(g), p.size, lr, None if w is None else C.cast(_u(w), C.c_void_p))
         return p
 
+    # -- binary16 wire
+    def float_to_half(self, x):
+        x = np.ascontiguousarray(x, dtype=np.float32)
+        out = np.empty(max(1, x.size), dtype=np.uint16)
+        self.L.orc_float_to_half(_f(x), x.size, out.ctypes.data_as(C.POINTER(C.c_uint16)))
+        return out[: x.size]
+
+    def half_to_float(self, h):
+        h = np.ascontiguousarray(h, dtype=np.uint16)
+        out = np.empty(max(1, h.size), dtype=np.float32)
+        self.L.orc_half_to_float(h.ctypes.data_as(C.POINTER(C.c_uint16)), h.size, _f(out))
+        return out[: h.size]
+
+    def ring_allreduce_fp16(self, inputs):
+        inputs = [np.ascontiguousarray(x, dtype=np.float32) for x in inputs]
+        outs = [np.empty_like(inputs[0]) for _ in inputs]
+        self.L.orc_ring_allreduce_fp16(
+            len(inputs), C.cast(_ptr_array(inputs, C.c_float), C.c_void_p), inputs[0].size,
+            C.cast(_ptr_array(outs, C.c_float), C.c_void_p))
+        return outs
+
     # -- ternary
     def ternarize(self, v, seed):
         v = np.ascontiguousarray(v, dtype=np.float32)
@@ -271,6 +295,9 @@ class Ref:
         L.ref_masked_allreduce.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.POINTER(C.c_int),
                                            C.c_void_p, C.c_uint32, C.c_size_t, C.c_void_p,
                                            C.POINTER(C.c_int), _u64p]
+        L.ref_float_to_half.argtypes = [_f32p, C.c_size_t, C.POINTER(C.c_uint16)]
+        L.ref_half_to_float.argtypes = [C.POINTER(C.c_uint16), C.c_size_t, _f32p]
+        L.ref_fp16_allreduce.argtypes = [C.c_int, C.c_void_p, C.c_size_t, C.c_void_p, _u64p]
         L.ref_ternarize.argtypes = [_f32p, C.c_size_t, C.c_uint64, C.POINTER(C.c_float), _u8p]
         L.ref_deternarize.argtypes = [C.c_float, _u8p, C.c_size_t, _f32p]
         L.ref_decode_ternary.argtypes = [_u8p, C.c_size_t, C.POINTER(C.c_float), _u64p, _u64p, _u8p]
@@ -389,6 +416,22 @@ class Ref:
             None if adv is None else C.cast(_u(adv), C.c_void_p), epoch, ln,
             C.cast(_ptr_array(outs, C.c_float), C.c_void_p), modes, _u(byts)))
         return outs, list(modes), [int(b) for b in byts]
+
+    # -- binary16
+    def float_to_half(self, x):
+        x = np.ascontiguousarray(x, dtype=np.float32)
+        out = np.empty(max(1, x.size), dtype=np.uint16)
+        self.L.ref_float_to_half(_f(x), x.size, out.ctypes.data_as(C.POINTER(C.c_uint16)))
+        return out[: x.size]
+
+    def half_to_float(self, h):
+        h = np.ascontiguousarray(h, dtype=np.uint16)
+        out = np.empty(max(1, h.size), dtype=np.float32)
+        self.L.ref_half_to_float(h.ctypes.data_as(C.POINTER(C.c_uint16)), h.size, _f(out))
+        return out[: h.size]
+
+    def fp16_allreduce(self, inputs):
+        return self._coll(self.L.ref_fp16_allreduce, inputs)
 
     # -- ternary: the reference's own mt19937_64 ternarize
     def ternarize(self, v, seed):

@@ -470,3 +470,84 @@ int orc_ternary_mean(int n, const float* scales, const uint8_t* const* b, size_t
   }
   return ORC_OK;
 }
+
+/* ------------------------------------------------ binary16 wire (8f-3) */
+
+static uint16_t f2h(float v) { /* codec.cpp:79-111 */
+  uint32_t bits;
+  memcpy(&bits, &v, 4);
+  const uint16_t sign = (uint16_t)((bits >> 16) & 0x8000u);
+  const int32_t exp = (int32_t)((bits >> 23) & 0xff) - 127;
+  uint32_t mant = bits & 0x7fffffu;
+  if (exp == 128) return (uint16_t)(sign | (mant != 0 ? 0x7e00u : 0x7bffu));
+  if (exp > 15) return (uint16_t)(sign | 0x7bffu);
+  if (exp >= -14) {
+    uint32_t m = mant >> 13;
+    const uint32_t rest = mant & 0x1fffu;
+    if (rest > 0x1000u || (rest == 0x1000u && (m & 1u))) ++m;
+    const uint32_t h = ((uint32_t)(exp + 15) << 10) + m;
+    if (h >= 0x7c00u) return (uint16_t)(sign | 0x7bffu);
+    return (uint16_t)(sign | h);
+  }
+  if (exp >= -25) {
+    mant |= 0x800000u;
+    const int shift = -exp - 14 + 13;
+    uint32_t m = mant >> shift;
+    const uint32_t cut = mant & ((1u << shift) - 1u);
+    const uint32_t half_ulp = 1u << (shift - 1);
+    if (cut > half_ulp || (cut == half_ulp && (m & 1u))) ++m;
+    return (uint16_t)(sign | m);
+  }
+  return sign;
+}
+
+static float h2f(uint16_t h) { /* codec.cpp:113-140 */
+  const uint32_t sign = (uint32_t)(h & 0x8000u) << 16;
+  const uint32_t exp = (h >> 10) & 0x1f;
+  const uint32_t mant = h & 0x3ffu;
+  uint32_t bits;
+  if (exp == 0) {
+    if (mant == 0) {
+      bits = sign;
+    } else {
+      int e = 1;
+      uint32_t m = mant;
+      while ((m & 0x400u) == 0) {
+        m <<= 1;
+        --e;
+      }
+      bits = sign | ((uint32_t)(e + 112) << 23) | ((m & 0x3ffu) << 13);
+    }
+  } else if (exp == 31) {
+    bits = sign | 0x7f800000u | (mant << 13);
+  } else {
+    bits = sign | ((exp + 112) << 23) | (mant << 13);
+  }
+  float f;
+  memcpy(&f, &bits, 4);
+  return f;
+}
+
+void orc_float_to_half(const float* in, size_t n, uint16_t* out) {
+  for (size_t i = 0; i < n; ++i) out[i] = f2h(in[i]);
+}
+void orc_half_to_float(const uint16_t* in, size_t n, float* out) {
+  for (size_t i = 0; i < n; ++i) out[i] = h2f(in[i]);
+}
+
+void orc_ring_allreduce_fp16(int n, const float* const* in, size_t len, float* const* out) {
+  /* collective.cpp:165-216 with F16Wire: chunk c starts at position c, every
+   * hop sends encode(partial), the receiver adds decode() to its own value,
+   * the owner (position c - 1) rounds once more; the all-gather copies. */
+  const size_t chunk = (len + (size_t)n - 1) / (size_t)n;
+  for (int c = 0; c < n; ++c) {
+    const size_t b = (size_t)c * chunk < len ? (size_t)c * chunk : len;
+    const size_t e = ((size_t)c + 1) * chunk < len ? ((size_t)c + 1) * chunk : len;
+    for (size_t i = b; i < e; ++i) {
+      float p = in[c][i];
+      for (int k = 1; k < n; ++k) p = in[(c + k) % n][i] + h2f(f2h(p));
+      const float fin = h2f(f2h(p));
+      for (int r = 0; r < n; ++r) out[r][i] = fin;
+    }
+  }
+}

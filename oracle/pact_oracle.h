@@ -134,6 +134,15 @@ void orc_to_mean(const float* sum, size_t len, int n, float* mean);
 void orc_sgd_step(float* params, const float* mean_grad, size_t len, float lr,
                   const uint64_t* words_or_null);
 
+/* ------------------------------------------------- binary16 wire (8f-3) */
+
+/* codec.cpp:79-111 / 113-140, element-wise over arrays */
+void orc_float_to_half(const float* in, size_t n, uint16_t* out);
+void orc_half_to_float(const uint16_t* in, size_t n, float* out);
+/* collective.cpp:165-216 with F16Wire (133-163): outputs[r] = the binary16
+ * ring's SUM as rank r sees it (identical bits on every rank) */
+void orc_ring_allreduce_fp16(int n, const float* const* inputs, size_t len, float* const* outputs);
+
 /* ------------------------------------------------- ternary */
 
 /* codec.cpp:50-68 ternarize with the product's counter-based draws: u_i =

@@ -203,6 +203,26 @@ int ref_masked_allreduce(int n, const float* const* grads, const uint64_t* const
   });
 }
 
+// -------------------------------------------------- binary16
+
+void ref_float_to_half(const float* in, size_t n, uint16_t* out) {
+  for (size_t i = 0; i < n; ++i) out[i] = float_to_half(in[i]);
+}
+void ref_half_to_float(const uint16_t* in, size_t n, float* out) {
+  for (size_t i = 0; i < n; ++i) out[i] = half_to_float(in[i]);
+}
+
+int ref_fp16_allreduce(int n, const float* const* in, size_t len, float* const* out,
+                       uint64_t* bytes_out) {
+  return guarded([&] {
+    run_workers(n, [&](int r, Comm& c) {
+      AggregateResult a = fp16_allreduce(FlatTensor(std::vector<float>(in[r], in[r] + len)), c);
+      std::memcpy(out[r], a.tensor.data(), len * sizeof(float));
+      bytes_out[r] = a.stats.bytes_on_wire;
+    });
+  });
+}
+
 // ------------------------------------------------- ternary
 
 int ref_ternarize(const float* v, size_t n, uint64_t seed, float* scale_out, uint8_t* sign_bytes) {

@@ -32,6 +32,8 @@ from .api import (  # noqa: F401
     encode_header,
     encode_ternary,
     enforce_gradient_sparsity,
+    fp16_allreduce,
+    fp16_roundtrip,
     full_allreduce,
     magnitude_prune,
     magnitude_prune_per_layer,

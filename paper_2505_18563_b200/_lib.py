@@ -41,7 +41,7 @@ class SyncStatsC(C.Structure):
 class PolicyC(C.Structure):
     _fields_ = [("density_threshold", C.c_double), ("bucket_bytes", C.c_uint64),
                 ("scale", C.c_float), ("time_stages", C.c_int), ("transport", C.c_int),
-                ("gse_dense", C.c_int)]
+                ("wire", C.c_int), ("gse_dense", C.c_int)]
 
 
 class MaskInfo(C.Structure):
@@ -98,6 +98,8 @@ SIGNATURES = {
     "pact_full_allreduce": (C.c_int, [vp, vp, vp, C.c_uint64, C.c_float, C.POINTER(SyncStatsC), vp]),
     "pact_masked_allreduce": (C.c_int, [vp, vp, vp, C.c_uint64, vp, C.c_int, C.c_uint32, u64p,
                                         C.POINTER(PolicyC), vp, C.POINTER(SyncStatsC), vp]),
+    "pact_fp16_roundtrip": (C.c_int, [vp, vp, vp, C.c_uint64, vp]),
+    "pact_fp16_allreduce": (C.c_int, [vp, vp, vp, vp, C.c_uint64, C.POINTER(SyncStatsC), vp]),
     "pact_ternary_sign_bytes": (C.c_uint64, [C.c_uint64]),
     "pact_ternarize": (C.c_int, [vp, vp, C.c_uint64, C.c_uint64, vp, vp, vp]),
     "pact_deternarize": (C.c_int, [vp, vp, vp, C.c_uint64, vp, vp]),

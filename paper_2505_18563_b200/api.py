@@ -546,11 +546,14 @@ class SyncPolicy:
     scale: float = 1.0               # fused into unpack (1/n gives the mean)
     time_stages: bool = False
     transport: int = 0               # 0 auto, 1 NCCL allreduce, 2 NVLink P2P (bit-exact fold order)
+    wire: int = 0                    # packed payload: 0 fp32 (reference), 1 binary16 ring (F16Wire)
     gse_dense: bool = False          # gradient not yet masked: the dense fallback applies GSE first
+
+    F32, F16 = 0, 1
 
     def c(self) -> _lib.PolicyC:
         return _lib.PolicyC(self.density_threshold, self.bucket_bytes, self.scale, int(self.time_stages),
-                            int(self.transport), int(self.gse_dense))
+                            int(self.transport), int(self.wire), int(self.gse_dense))
 
 
 def _stats(s: _lib.SyncStatsC) -> SyncStats:
@@ -655,6 +658,26 @@ def masked_allreduce_host(grad_host: torch.Tensor, mask: SparsityMask, tracker: 
           _ptr(grad_host), grad_host.numel(), mask.handle, int(tracker == TrackerStatus.Stable),
           int(epoch), None, C.byref(pol), _ptr(out_host), C.byref(st), _stream())
     return _stats(st)
+
+
+def fp16_roundtrip(grad: torch.Tensor, out: Optional[torch.Tensor] = None) -> torch.Tensor:  # codec.cpp:142-146
+    g = _as_grad(grad, "grad")
+    o = torch.empty_like(g) if out is None else out
+    _call(lib.pact_fp16_roundtrip, Context.get(g.device.index).handle, _ptr(g), _ptr(o), g.numel(), _stream())
+    return o
+
+
+def fp16_allreduce(grad: torch.Tensor, comm: Optional[Comm],
+                   out: Optional[torch.Tensor] = None) -> AggregateResult:  # collective.cpp:261-267
+    """Dense ring all-reduce with binary16 chunks re-rounded at every hop
+    (F16Wire, collective.cpp:133-163), bit-identical to the reference ring."""
+    g = _as_grad(grad, "grad")
+    o = torch.empty_like(g) if out is None else out
+    st = _lib.SyncStatsC()
+    ctx = comm.ctx if comm is not None else Context.get(g.device.index)
+    _call(lib.pact_fp16_allreduce, comm.handle if comm is not None else None, ctx.handle, _ptr(g), _ptr(o),
+          g.numel(), C.byref(st), _stream())
+    return AggregateResult(o, _stats(st))
 
 
 def ternary_allgather_aggregate(grad: torch.Tensor, mask: SparsityMask, tracker: TrackerStatus, seed: int,

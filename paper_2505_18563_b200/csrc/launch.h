@@ -133,6 +133,15 @@ void launch_ternary_mean(const uint32_t* signs, uint64_t sign_stride, const floa
                          uint64_t scale_stride, int n, uint64_t count, float* out, int* err,
                          cudaStream_t s);
 
+// ---- f16wire.cu (reference binary16 conversions, codec.cpp:77-146) --------
+void launch_f16_encode(const float* x, uint64_t n, uint16_t* out, cudaStream_t s);
+// out[i] = encode(x[i] + decode(recv[i]))
+void launch_f16_step(const float* x, const uint16_t* recv, uint64_t n, uint16_t* out, cudaStream_t s);
+// out[j] = decode(gathered[((j / C) + n - 1) % n][j % C]) for j < count
+void launch_f16_gather(const uint16_t* gathered, uint64_t count, int n, uint64_t C, float* out,
+                       cudaStream_t s);
+void launch_f16_roundtrip(const float* x, uint64_t n, float* out, cudaStream_t s);
+
 // ---- digest.cu -------------------------------------------------------------
 // FNV-1a-64 over the LE bytes of nwords words; scratch sized by
 // digest_scratch_bytes(nwords). Result written to *out_dev.

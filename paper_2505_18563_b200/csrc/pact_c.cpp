@@ -136,6 +136,7 @@ struct pact_ctx {
   DevBuf packed;    // packed gradient for masked_allreduce
   DevBuf grad_stage, out_stage;  // e2e host path staging
   DevBuf tern;      // ternary: [smax u32][err i32][pad][own block][n gathered blocks]
+  DevBuf f16;       // binary16 ring: send x2, recv, n gathered chunks
   HostBuf pin;      // small pinned readbacks
   cudaStream_t aux[2] = {nullptr, nullptr};  // comm / unpack streams for bucket overlap
   std::vector<cudaEvent_t> ev_pool;
@@ -587,7 +588,7 @@ pact_status pact_ctx_destroy(pact_ctx* ctx) {
   cudaSetDevice(ctx->device);
   cudaDeviceSynchronize();
   for (DevBuf* b : {&ctx->ws_small, &ctx->cand, &ctx->state, &ctx->seg_ws, &ctx->digest_scratch, &ctx->packed,
-                    &ctx->grad_stage, &ctx->out_stage, &ctx->tern})
+                    &ctx->grad_stage, &ctx->out_stage, &ctx->tern, &ctx->f16})
     b->release();
   ctx->pin.release();
   for (auto s : ctx->aux)
@@ -1343,6 +1344,79 @@ pact_status pact_full_allreduce(pact_comm* c, const float* grad, float* out, uin
   return PACT_OK;
 }
 
+// ------------------------------------------------------- binary16 ring
+namespace {
+// ring_allreduce_impl<F16Wire> (collective.cpp:165-216 with 133-163): n-1
+// reduce-scatter hops as grouped NCCL send/recv of binary16 chunks, each
+// followed by the add-and-re-round kernel; the owners' rounded chunks are
+// then all-gathered (a copy, so every rank ends with the same bits). x and
+// out may alias. n = 1 (no comm): the owner's rounding only.
+pact_status f16_ring(pact_comm* c, pact_ctx* ctx, const float* x, uint64_t count, float* out,
+                     cudaStream_t s) {
+  const int n = c ? c->n : 1;
+  if (!count) return PACT_OK;
+  if (n == 1) {
+    pactk::launch_f16_roundtrip(x, count, out, s);
+    return PACT_OK;
+  }
+  const int r = c->rank;
+  const uint64_t C = (count + n - 1) / n;
+  auto begin = [&](int ch) { return std::min<uint64_t>(count, (uint64_t)ch * C); };
+  auto elems = [&](int ch) { return std::min<uint64_t>(count, ((uint64_t)ch + 1) * C) - begin(ch); };
+  TRY(ctx->f16.ensure((3 + (uint64_t)n) * C * 2));
+  uint16_t* send[2] = {ctx->f16.as<uint16_t>(), ctx->f16.as<uint16_t>() + C};
+  uint16_t* recv = send[1] + C;
+  uint16_t* gathered = recv + C;
+  pactk::launch_f16_encode(x + begin(r), elems(r), send[0], s);
+  for (int st = 0; st < n - 1; ++st) {
+    const int send_c = imod(r - st, n), recv_c = imod(r - st - 1, n);
+    NCCL_TRY(ncclGroupStart());
+    NCCL_TRY(ncclSend(send[st & 1], elems(send_c) * 2, ncclUint8, (r + 1) % n, c->nccl, s));
+    NCCL_TRY(ncclRecv(recv, elems(recv_c) * 2, ncclUint8, (r + n - 1) % n, c->nccl, s));
+    NCCL_TRY(ncclGroupEnd());
+    // last hop: the owner's prepare_owned rounding lands in its all-gather slot
+    uint16_t* dst = st < n - 2 ? send[(st + 1) & 1] : gathered + (uint64_t)r * C;
+    pactk::launch_f16_step(x + begin(recv_c), recv, elems(recv_c), dst, s);
+  }
+  NCCL_TRY(ncclAllGather(gathered + (uint64_t)r * C, gathered, C * 2, ncclUint8, c->nccl, s));
+  pactk::launch_f16_gather(gathered, count, n, C, out, s);
+  return PACT_OK;
+}
+}  // namespace
+
+pact_status pact_fp16_roundtrip(pact_ctx* ctx, const float* in, float* out, uint64_t len,
+                                pact_stream_t stream) {
+  if (!ctx || (len && (!in || !out))) return fail(PACT_E_INVALID_ARG, "null args");
+  TRY(set_device(ctx));
+  pactk::launch_f16_roundtrip(in, len, out, stream);
+  CUDA_TRY(cudaGetLastError());
+  return PACT_OK;
+}
+
+pact_status pact_fp16_allreduce(pact_comm* c, pact_ctx* ctx, const float* grad, float* out,
+                                uint64_t len, pact_sync_stats* stats, pact_stream_t stream) {
+  if (!ctx) return fail(PACT_E_INVALID_ARG, "null ctx");
+  if (c && c->ctx != ctx) return fail(PACT_E_INVALID_ARG, "comm belongs to another ctx");
+  TRY(set_device(ctx));
+  cudaStream_t s = stream;
+  CUDA_TRY(cudaEventRecord(ctx->t0, s));
+  TRY(f16_ring(c, ctx, grad, len, out, s));
+  CUDA_TRY(cudaGetLastError());
+  if (stats) {
+    CUDA_TRY(cudaEventRecord(ctx->t1, s));
+    CUDA_TRY(cudaEventSynchronize(ctx->t1));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, ctx->t0, ctx->t1);
+    *stats = pact_sync_stats{};
+    stats->bytes_on_wire = c ? pact_ring_bytes(c->n, c->rank, len) / 2 : 0;  // collective.cpp:261-267
+    stats->seconds = ms * 1e-3;
+    stats->mode_used = PACT_SYNC_FP16;
+    stats->value_count = len;
+    stats->transport = c ? PACT_TRANSPORT_NCCL : 0;
+  }
+  return PACT_OK;
+}
+
 pact_status pact_masked_allreduce(pact_comm* c, pact_ctx* ctx, const float* grad, uint64_t len,
                                   pact_mask* m, int tracker_stable, uint32_t epoch,
                                   const uint64_t* advertised, const pact_policy* policy,
@@ -1379,10 +1453,11 @@ pact_status pact_masked_allreduce(pact_comm* c, pact_ctx* ctx, const float* grad
   TRY(ctx->packed.ensure(std::max<uint64_t>(1, m->nnz) * 4));
   float* packed = ctx->packed.as<float>();
 
-  const bool p2p_try = c && m->nnz && n <= pactk::kP2PMaxRanks &&
+  const bool f16 = pol.wire == PACT_WIRE_F16;  // binary16 ring on the packed values (8f-3)
+  const bool p2p_try = c && m->nnz && n <= pactk::kP2PMaxRanks && !f16 &&
                        (pol.transport == PACT_TRANSPORT_P2P || pol.transport == PACT_TRANSPORT_AUTO);
   const bool p2p_ready = p2p_try && c->p2p.ok && c->p2p.cap >= m->nnz;
-  const bool buckets = c && !p2p_try && pol.bucket_bytes > 0 && m->nnz * 4 > pol.bucket_bytes;
+  const bool buckets = c && !p2p_try && !f16 && pol.bucket_bytes > 0 && m->nnz * 4 > pol.bucket_bytes;
   if (buckets) TRY(mirror_tile_off(m, s));
 
   int agree = 0;
@@ -1558,7 +1633,9 @@ pact_status pact_masked_allreduce(pact_comm* c, pact_ctx* ctx, const float* grad
       if (!packed_issued && m->nnz)
         pactk::launch_pack(grad, len, m->words, m->tile_off, packed, 0, m->ntiles, s);
       mark(0);
-      if (c && m->nnz)
+      if (f16)  // ring_allreduce_fp16 of the packed values (collective.cpp:133-163)
+        TRY(f16_ring(c, ctx, packed, m->nnz, packed, s));
+      else if (c && m->nnz)
         NCCL_TRY(ncclAllReduce(packed, packed, m->nnz, ncclFloat32, ncclSum, c->nccl, s));
       mark(1);
       pactk::launch_unpack(packed, len, m->words, m->tile_off, scale, scale != 1.0f, out, 0,
@@ -1610,6 +1687,8 @@ pact_status pact_masked_allreduce(pact_comm* c, pact_ctx* ctx, const float* grad
   if (stats) {
     *stats = pact_sync_stats{};
     stats->bytes_on_wire = c ? pact_masked_bytes(n, c->rank, agree ? m->nnz : len) : 0;
+    if (c && agree && f16)  // 2-byte ring payloads
+      stats->bytes_on_wire -= pact_ring_bytes(n, c->rank, m->nnz) / 2;
     stats->mode_used = agree ? PACT_SYNC_PACKED : PACT_SYNC_FULL;
     stats->buckets = nbuckets;
     stats->value_count = agree ? m->nnz : len;

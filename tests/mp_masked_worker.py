@@ -182,6 +182,22 @@ def main():
         if world == 2:  # NCCL's sum is order-free only for two ranks
             check("ternary fallback: == reference", np.array_equal(u32(rf.tensor.cpu().numpy()), u32(outs[rank])))
 
+    # ---- binary16 wire (collective.cpp:133-216, 261-267), SURVEY 8f-3
+    grads = [(synth.synth_host(n, synth.grad_seed(r, 13), synth.G_FULL) * (1000.0 if r % 2 else 0.001)
+              ).astype(np.float32) for r in range(world)]
+    g = torch.from_numpy(grads[rank]).to(dev)
+    rh = pb.fp16_allreduce(g, comm)
+    want = port.ring_allreduce_fp16(grads)[rank]
+    check("fp16: bit-exact vs ring", np.array_equal(u32(rh.tensor.cpu().numpy()), u32(want)))
+    check("fp16: bytes", rh.stats.bytes_on_wire == port.ring_bytes(world, rank, n) // 2)
+    check("fp16: mode", rh.stats.mode_used == pb.SyncMode.Fp16AllReduce)
+    rp = pb.masked_allreduce(g, mask, pb.TrackerStatus.Stable, 14, comm, policy=pb.SyncPolicy(wire=pb.SyncPolicy.F16))
+    pk = port.ring_allreduce_fp16([port.pack(x, words) for x in grads])[rank]
+    want = port.unpack(pk, port.mask_digest(words, n), words, n)
+    check("fp16 packed: bit-exact", np.array_equal(u32(rp.tensor.cpu().numpy()), u32(want)))
+    check("fp16 packed: bytes",
+          rp.stats.bytes_on_wire == 26 * (world - 1) + port.ring_bytes(world, rank, int(bits.sum())) // 2)
+
     flag = torch.tensor([len(failures)], device=dev)
     dist.all_reduce(flag)
     comm.close()
