@@ -324,6 +324,33 @@ pact_status pact_masked_allreduce_host(pact_comm* c, pact_ctx* ctx, const float*
                                        const pact_policy* policy, float* out_host,
                                        pact_sync_stats* stats, pact_stream_t stream);
 
+/* ------------------------------------------------------------ TopK */
+
+/* codec.cpp:148-155: k = max(1, floor(rate*len + len*1e-7)) capped at len;
+ * PACT_E_INVALID_RATE unless 0 < rate <= 1. */
+pact_status pact_topk_count(uint64_t len, float rate, uint64_t* k_out);
+
+/* codec.cpp:147-172 topk_select: the k largest |g_i| (ties select the lower
+ * index), indices strictly increasing, values bit-copied. Selection by the
+ * prune kernels (radix-selected threshold, bitmap, tie fix-up). Outputs hold
+ * pact_topk_count(len, rate) entries. Synchronises the stream. Inputs are
+ * finite (the reference's comparator has no order for NaN). */
+pact_status pact_topk_select(pact_ctx* ctx, const float* grad, uint64_t len, float rate,
+                             uint32_t* indices, float* values, uint64_t* k_out, pact_stream_t stream);
+
+/* codec.cpp:174-182 topk_densify: zeros, then out[indices[j]] = values[j];
+ * PACT_E_CORRUPT_PAYLOAD on an index >= len. Synchronises. */
+pact_status pact_topk_densify(pact_ctx* ctx, const uint32_t* indices, const float* values, uint64_t k,
+                              uint64_t len, float* out, pact_stream_t stream);
+
+/* collective.cpp:370-390 topk_allgather_aggregate: select, NCCL all-gather
+ * of (indices, values), per-element double sum over ranks in rank order,
+ * float(acc / n). Returns the MEAN. bytes_on_wire: ring all-gather of the
+ * n frames (26 + 8k bytes each). */
+pact_status pact_topk_allgather_aggregate(pact_comm* c, pact_ctx* ctx, const float* grad, uint64_t len,
+                                          float rate, uint32_t epoch, float* out, pact_sync_stats* stats,
+                                          pact_stream_t stream);
+
 /* ------------------------------------------------- binary16 wire */
 
 /* codec.cpp:142-146 fp16_roundtrip with the reference's hand-rolled RNE and

@@ -106,6 +106,8 @@ class Port:
         L.orc_sgd_step.argtypes = [_f32p, _f32p, C.c_size_t, C.c_float, C.c_void_p]
         L.orc_encode_header.argtypes = [C.c_void_p, _u8p]
         L.orc_decode_header.argtypes = [_u8p, C.c_size_t, C.c_void_p]
+        L.orc_topk_select.argtypes = [_f32p, C.c_size_t, C.c_float, C.POINTER(C.c_uint32), _f32p, _u64p]
+        L.orc_topk_mean.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_size_t, C.c_size_t, _f32p]
         L.orc_float_to_half.argtypes = [_f32p, C.c_size_t, C.POINTER(C.c_uint16)]
         L.orc_half_to_float.argtypes = [C.POINTER(C.c_uint16), C.c_size_t, _f32p]
         L.orc_ring_allreduce_fp16.argtypes = [C.c_int, C.c_void_p, C.c_size_t, C.c_void_p]
@@ -226,6 +228,26 @@ class Port:
         self.L.orc_sgd_step(_f(p), _f(g), p.size, lr, None if w is None else C.cast(_u(w), C.c_void_p))
         return p
 
+    # -- TopK
+    def topk_select(self, g, rate):
+        g = np.ascontiguousarray(g, dtype=np.float32)
+        idx = np.empty(max(1, g.size), dtype=np.uint32)
+        val = np.empty(max(1, g.size), dtype=np.float32)
+        k = C.c_uint64()
+        _check(self.L.orc_topk_select(_f(g), g.size, rate, idx.ctypes.data_as(C.POINTER(C.c_uint32)), _f(val),
+                                      C.byref(k)))
+        return idx[: k.value].copy(), val[: k.value].copy()
+
+    def topk_mean(self, idxs, vals, length):
+        n = len(idxs)
+        idxs = [np.ascontiguousarray(i if i.size else np.zeros(1, np.uint32), dtype=np.uint32) for i in idxs]
+        vals = [np.ascontiguousarray(v if v.size else np.zeros(1, np.float32), dtype=np.float32) for v in vals]
+        k = min(i.size for i in idxs)
+        out = np.empty(max(1, length), dtype=np.float32)
+        _check(self.L.orc_topk_mean(n, C.cast(_ptr_array(idxs, C.c_uint32), C.c_void_p),
+                                    C.cast(_ptr_array(vals, C.c_float), C.c_void_p), k, length, _f(out)))
+        return out[:length]
+
     # -- binary16 wire
     def float_to_half(self, x):
         x = np.ascontiguousarray(x, dtype=np.float32)
@@ -295,6 +317,11 @@ class Ref:
         L.ref_masked_allreduce.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.POINTER(C.c_int),
                                            C.c_void_p, C.c_uint32, C.c_size_t, C.c_void_p,
                                            C.POINTER(C.c_int), _u64p]
+        L.ref_topk_select.argtypes = [_f32p, C.c_size_t, C.c_float, C.POINTER(C.c_uint32), _f32p, _u64p]
+        L.ref_topk_densify.argtypes = [C.POINTER(C.c_uint32), _f32p, C.c_size_t, C.c_size_t, _f32p]
+        L.ref_topk_decode_check.argtypes = [_u8p, C.c_size_t, C.c_size_t, _u64p]
+        L.ref_topk_aggregate.argtypes = [C.c_int, C.c_void_p, C.c_size_t, C.c_float, C.c_uint32, C.c_void_p,
+                                         _u64p]
         L.ref_float_to_half.argtypes = [_f32p, C.c_size_t, C.POINTER(C.c_uint16)]
         L.ref_half_to_float.argtypes = [C.POINTER(C.c_uint16), C.c_size_t, _f32p]
         L.ref_fp16_allreduce.argtypes = [C.c_int, C.c_void_p, C.c_size_t, C.c_void_p, _u64p]
@@ -416,6 +443,38 @@ class Ref:
             None if adv is None else C.cast(_u(adv), C.c_void_p), epoch, ln,
             C.cast(_ptr_array(outs, C.c_float), C.c_void_p), modes, _u(byts)))
         return outs, list(modes), [int(b) for b in byts]
+
+    # -- TopK
+    def topk_select(self, g, rate):
+        g = np.ascontiguousarray(g, dtype=np.float32)
+        idx = np.empty(max(1, g.size), dtype=np.uint32)
+        val = np.empty(max(1, g.size), dtype=np.float32)
+        k = C.c_uint64()
+        _check(self.L.ref_topk_select(_f(g), g.size, rate, idx.ctypes.data_as(C.POINTER(C.c_uint32)), _f(val),
+                                      C.byref(k)))
+        return idx[: k.value].copy(), val[: k.value].copy()
+
+    def topk_densify(self, idx, val, length):
+        idx = np.ascontiguousarray(idx if len(idx) else np.zeros(1, np.uint32), dtype=np.uint32)
+        val = np.ascontiguousarray(val if len(val) else np.zeros(1, np.float32), dtype=np.float32)
+        out = np.empty(max(1, length), dtype=np.float32)
+        _check(self.L.ref_topk_densify(idx.ctypes.data_as(C.POINTER(C.c_uint32)), _f(val), len(idx), length,
+                                       _f(out)))
+        return out[:length]
+
+    def topk_decode_ok(self, frame: bytes, original_len: int) -> bool:
+        buf = (C.c_uint8 * max(1, len(frame))).from_buffer_copy(frame or b"\0")
+        k = C.c_uint64()
+        return self.L.ref_topk_decode_check(buf, len(frame), original_len, C.byref(k)) == 0
+
+    def topk_aggregate(self, grads, rate, epoch=0):
+        grads = [np.ascontiguousarray(x, dtype=np.float32) for x in grads]
+        outs = [np.empty_like(grads[0]) for _ in grads]
+        byts = np.zeros(len(grads), dtype=np.uint64)
+        _check(self.L.ref_topk_aggregate(len(grads), C.cast(_ptr_array(grads, C.c_float), C.c_void_p),
+                                         grads[0].size, rate, epoch, C.cast(_ptr_array(outs, C.c_float), C.c_void_p),
+                                         _u(byts)))
+        return outs, [int(b) for b in byts]
 
     # -- binary16
     def float_to_half(self, x):

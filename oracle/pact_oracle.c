@@ -551,3 +551,61 @@ void orc_ring_allreduce_fp16(int n, const float* const* in, size_t len, float* c
     }
   }
 }
+
+/* ------------------------------------------------------------ TopK (8f-4) */
+
+typedef struct {
+  uint32_t key, idx;
+} orc_kv;
+
+static int orc_kv_desc(const void* a, const void* b) {
+  /* stable_sort by descending |g| == sort by (key desc, index asc) */
+  const orc_kv* x = (const orc_kv*)a;
+  const orc_kv* y = (const orc_kv*)b;
+  if (x->key != y->key) return x->key > y->key ? -1 : 1;
+  return x->idx < y->idx ? -1 : (x->idx > y->idx);
+}
+
+static int orc_u32_asc(const void* a, const void* b) {
+  const uint32_t x = *(const uint32_t*)a, y = *(const uint32_t*)b;
+  return x < y ? -1 : (x > y);
+}
+
+int orc_topk_select(const float* g, size_t len, float rate, uint32_t* idx, float* val, uint64_t* k_out) {
+  if (!(rate > 0.0f && rate <= 1.0f)) return ORC_INVALID_RATE; /* codec.cpp:148-149 */
+  double kd = floor((double)rate * (double)len + (double)len * 1e-7);
+  uint64_t k = kd < 1.0 ? 1 : (uint64_t)kd;
+  if (k > len) k = len;
+  orc_kv* kv = (orc_kv*)malloc((len ? len : 1) * sizeof(orc_kv));
+  if (!kv) return ORC_NUMERICAL_FAILURE;
+  for (size_t i = 0; i < len; ++i) {
+    uint32_t b;
+    memcpy(&b, &g[i], 4);
+    kv[i].key = b & 0x7fffffffu; /* fabs order for finite values */
+    kv[i].idx = (uint32_t)i;
+  }
+  qsort(kv, len, sizeof(orc_kv), orc_kv_desc);
+  for (uint64_t j = 0; j < k; ++j) idx[j] = kv[j].idx;
+  qsort(idx, k, sizeof(uint32_t), orc_u32_asc);
+  for (uint64_t j = 0; j < k; ++j) val[j] = g[idx[j]];
+  free(kv);
+  *k_out = k;
+  return ORC_OK;
+}
+
+int orc_topk_mean(int n, const uint32_t* const* idx, const float* const* val, size_t k, size_t len,
+                  float* mean) {
+  double* acc = (double*)calloc(len ? len : 1, sizeof(double));
+  if (!acc) return ORC_NUMERICAL_FAILURE;
+  for (int r = 0; r < n; ++r)
+    for (size_t j = 0; j < k; ++j) {
+      if (idx[r][j] >= len) {
+        free(acc);
+        return ORC_CORRUPT_PAYLOAD;
+      }
+      acc[idx[r][j]] += val[r][j];
+    }
+  for (size_t i = 0; i < len; ++i) mean[i] = (float)(acc[i] / n);
+  free(acc);
+  return ORC_OK;
+}

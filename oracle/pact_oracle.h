@@ -134,6 +134,16 @@ void orc_to_mean(const float* sum, size_t len, int n, float* mean);
 void orc_sgd_step(float* params, const float* mean_grad, size_t len, float lr,
                   const uint64_t* words_or_null);
 
+/* ------------------------------------------------------ TopK (8f-4) */
+
+/* codec.cpp:147-172: k = max(1, floor(rate*len + len*1e-7)) (capped at len);
+ * the k largest |g| with ties to the lower index, indices ascending. idx/val
+ * hold len entries; *k_out = k. ORC_INVALID_RATE unless 0 < rate <= 1. */
+int orc_topk_select(const float* g, size_t len, float rate, uint32_t* idx, float* val, uint64_t* k_out);
+/* collective.cpp:383-388: acc over ranks in order (double), mean = float(acc/n) */
+int orc_topk_mean(int n, const uint32_t* const* idx, const float* const* val, size_t k, size_t len,
+                  float* mean);
+
 /* ------------------------------------------------- binary16 wire (8f-3) */
 
 /* codec.cpp:79-111 / 113-140, element-wise over arrays */

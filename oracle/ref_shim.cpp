@@ -203,6 +203,49 @@ int ref_masked_allreduce(int n, const float* const* grads, const uint64_t* const
   });
 }
 
+// ------------------------------------------------------ TopK
+
+int ref_topk_select(const float* g, size_t len, float rate, uint32_t* idx, float* val, uint64_t* k_out) {
+  return guarded([&] {
+    TopKPayload p = topk_select(FlatTensor(std::vector<float>(g, g + len)), rate);
+    std::memcpy(idx, p.indices.data(), p.indices.size() * 4);
+    std::memcpy(val, p.values.data(), p.values.size() * 4);
+    *k_out = p.indices.size();
+  });
+}
+
+int ref_topk_densify(const uint32_t* idx, const float* val, size_t k, size_t len, float* out) {
+  return guarded([&] {
+    TopKPayload p;
+    p.indices.assign(idx, idx + k);
+    p.values.assign(val, val + k);
+    p.original_len = len;
+    FlatTensor d = topk_densify(p);
+    std::memcpy(out, d.data(), len * sizeof(float));
+  });
+}
+
+int ref_topk_decode_check(const uint8_t* frame, size_t bytes, size_t original_len, uint64_t* k_out) {
+  return guarded([&] {
+    wire::Bytes b(bytes);
+    std::memcpy(b.data(), frame, bytes);
+    TopKPayload p = wire::decode_topk(b, original_len);
+    *k_out = p.indices.size();
+  });
+}
+
+int ref_topk_aggregate(int n, const float* const* grads, size_t len, float rate, uint32_t epoch,
+                       float* const* out, uint64_t* bytes_out) {
+  return guarded([&] {
+    run_workers(n, [&](int r, Comm& c) {
+      AggregateResult a =
+          topk_allgather_aggregate(FlatTensor(std::vector<float>(grads[r], grads[r] + len)), rate, epoch, c);
+      std::memcpy(out[r], a.tensor.data(), len * sizeof(float));
+      bytes_out[r] = a.stats.bytes_on_wire;
+    });
+  });
+}
+
 // -------------------------------------------------- binary16
 
 void ref_float_to_half(const float* in, size_t n, uint16_t* out) {

@@ -416,6 +416,39 @@ def deternarize(t: TernaryGradient, out: Optional[torch.Tensor] = None) -> torch
     return o
 
 
+@dataclass
+class TopKPayload:  # codec.hpp:60-66 (device tensors)
+    indices: Optional[torch.Tensor] = None  # int32 view of the u32 indices, strictly increasing
+    values: Optional[torch.Tensor] = None
+    original_len: int = 0
+
+
+def topk_count(length: int, rate: float) -> int:  # codec.cpp:148-155
+    k = C.c_uint64()
+    _call(lib.pact_topk_count, int(length), C.c_float(rate), C.byref(k))
+    return int(k.value)
+
+
+def topk_select(grad: torch.Tensor, rate: float) -> TopKPayload:  # codec.cpp:147-172
+    g = _as_grad(grad, "grad")
+    k = topk_count(g.numel(), rate)
+    idx = torch.empty(max(1, k), dtype=torch.int32, device=g.device)
+    val = torch.empty(max(1, k), dtype=torch.float32, device=g.device)
+    kk = C.c_uint64()
+    _call(lib.pact_topk_select, Context.get(g.device.index).handle, _ptr(g), g.numel(), C.c_float(rate),
+          _ptr(idx), _ptr(val), C.byref(kk), _stream())
+    return TopKPayload(idx[:k], val[:k], g.numel())
+
+
+def topk_densify(p: TopKPayload, out: Optional[torch.Tensor] = None) -> torch.Tensor:  # codec.cpp:174-182
+    dev = p.values.device if p.values is not None else torch.device("cuda", torch.cuda.current_device())
+    o = torch.empty(p.original_len, dtype=torch.float32, device=dev) if out is None else out
+    k = p.indices.numel() if p.indices is not None else 0
+    _call(lib.pact_topk_densify, Context.get(dev.index).handle, _ptr(p.indices), _ptr(p.values), k,
+          p.original_len, _ptr(o), _stream())
+    return o
+
+
 class PayloadKind(enum.IntEnum):  # codec.hpp:80-86
     Full = 0
     Packed = 1
@@ -480,6 +513,31 @@ def decode_ternary(frame: bytes) -> Tuple[TernaryGradient, int]:  # codec.cpp:32
     if scale == 0.0 and pairs.any():
         raise Error(Errc.CorruptPayload, "zero scale with non-zero signs")
     return TernaryGradient(scale, int(h.value_count), torch.from_numpy(b.copy())), int(h.mask_digest)
+
+
+def encode_topk(p: TopKPayload, epoch: int) -> bytes:  # codec.cpp:345-350
+    idx = p.indices.cpu().numpy().astype("<u4").tobytes()
+    val = p.values.cpu().numpy().astype("<f4").tobytes()
+    return encode_header(FrameHeader(PayloadKind.TopK, epoch, 0, p.indices.numel())) + idx + val
+
+
+def decode_topk(frame: bytes, original_len: int) -> TopKPayload:  # codec.cpp:352-369
+    """Host decode with the reference's checks (range, strictly increasing)."""
+    import numpy as np
+
+    h = decode_header(frame)
+    if h.kind != PayloadKind.TopK:
+        raise Error(Errc.CorruptPayload, "not a topk frame")
+    k = int(h.value_count)
+    if len(frame) < 26 + 8 * k:
+        raise Error(Errc.CorruptPayload, "frame truncated")
+    idx = np.frombuffer(frame, dtype="<u4", count=k, offset=26).copy()
+    val = np.frombuffer(frame, dtype="<f4", count=k, offset=26 + 4 * k).copy()
+    if k and (idx >= original_len).any():
+        raise Error(Errc.CorruptPayload, "topk index out of range")
+    if k > 1 and not (np.diff(idx.astype(np.int64)) > 0).all():
+        raise Error(Errc.CorruptPayload, "topk indices not strictly increasing")
+    return TopKPayload(torch.from_numpy(idx.view(np.int32)), torch.from_numpy(val), int(original_len))
 
 
 # -------------------------------------------------------------- collective
@@ -658,6 +716,19 @@ def masked_allreduce_host(grad_host: torch.Tensor, mask: SparsityMask, tracker: 
           _ptr(grad_host), grad_host.numel(), mask.handle, int(tracker == TrackerStatus.Stable),
           int(epoch), None, C.byref(pol), _ptr(out_host), C.byref(st), _stream())
     return _stats(st)
+
+
+def topk_allgather_aggregate(grad: torch.Tensor, rate: float, epoch: int, comm: Optional[Comm],
+                             out: Optional[torch.Tensor] = None) -> AggregateResult:  # collective.cpp:370-390
+    """All-gather of every rank's TopK payload, double-accumulated densify,
+    float(acc / n). Returns the MEAN."""
+    g = _as_grad(grad, "grad")
+    o = torch.empty_like(g) if out is None else out
+    st = _lib.SyncStatsC()
+    ctx = comm.ctx if comm is not None else Context.get(g.device.index)
+    _call(lib.pact_topk_allgather_aggregate, comm.handle if comm is not None else None, ctx.handle, _ptr(g),
+          g.numel(), C.c_float(rate), int(epoch), _ptr(o), C.byref(st), _stream())
+    return AggregateResult(o, _stats(st))
 
 
 def fp16_roundtrip(grad: torch.Tensor, out: Optional[torch.Tensor] = None) -> torch.Tensor:  # codec.cpp:142-146

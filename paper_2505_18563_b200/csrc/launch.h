@@ -102,10 +102,22 @@ void launch_prune_bitmap(const float* w, uint64_t len, uint32_t T, uint64_t r,
                          const uint32_t* tie_prefix, uint64_t* words, uint32_t* chunk_popc,
                          uint32_t* ties_out, const uint32_t* ties_prev, uint64_t* tie_words,
                          BitmapCounts* counts, cudaStream_t s);
-// exact tie bits from the exact tie prefix; updates chunk_popc of tie chunks
+// exact tie bits from the exact tie prefix; updates chunk_popc of tie chunks.
+// Ties of global rank < r dropped (prune) or, keep_low, kept (TopK)
 void launch_prune_tiefix(uint64_t* words, uint64_t len, const uint64_t* tie_words,
                          const uint32_t* ties, const uint32_t* tie_prefix, uint64_t r,
-                         uint32_t* chunk_popc, cudaStream_t s);
+                         uint32_t* chunk_popc, cudaStream_t s, int keep_low = 0);
+// TopK payload: the ascending indices of the set bits (u32), chunk offsets given
+void launch_pack_index(uint64_t len, const uint64_t* words, const uint32_t* chunk_off,
+                       uint32_t* idx, cudaStream_t s);
+// acc[idx[j]] += double(val[j]) (unique idx per call); err |= 1 on idx >= len
+void launch_scatter_add_f64(const uint32_t* idx, const float* val, uint64_t k, uint64_t len,
+                            double* acc, int* err, cudaStream_t s);
+// out[i] = float(acc[i] / n)
+void launch_f64_mean(const double* acc, uint64_t len, int n, float* out, cudaStream_t s);
+// out[idx[j]] = val[j] over a zero-filled out; err |= 1 on idx >= len
+void launch_scatter_f32(const uint32_t* idx, const float* val, uint64_t k, uint64_t len, float* out,
+                        int* err, cudaStream_t s);
 
 // per-layer mode: thread per word, element i of segment s kept iff key > T_s;
 // ties recorded (tie_words, word_ties) for the fix-up below

@@ -137,6 +137,8 @@ struct pact_ctx {
   DevBuf grad_stage, out_stage;  // e2e host path staging
   DevBuf tern;      // ternary: [smax u32][err i32][pad][own block][n gathered blocks]
   DevBuf f16;       // binary16 ring: send x2, recv, n gathered chunks
+  DevBuf topk;      // TopK: [own idx k][own val k][n gathered blocks] + f64 accumulator
+  pact_mask* topk_sel = nullptr;  // TopK selection bitmap (prune machinery)
   HostBuf pin;      // small pinned readbacks
   cudaStream_t aux[2] = {nullptr, nullptr};  // comm / unpack streams for bucket overlap
   std::vector<cudaEvent_t> ev_pool;
@@ -588,8 +590,9 @@ pact_status pact_ctx_destroy(pact_ctx* ctx) {
   cudaSetDevice(ctx->device);
   cudaDeviceSynchronize();
   for (DevBuf* b : {&ctx->ws_small, &ctx->cand, &ctx->state, &ctx->seg_ws, &ctx->digest_scratch, &ctx->packed,
-                    &ctx->grad_stage, &ctx->out_stage, &ctx->tern, &ctx->f16})
+                    &ctx->grad_stage, &ctx->out_stage, &ctx->tern, &ctx->f16, &ctx->topk})
     b->release();
+  if (ctx->topk_sel) pact_mask_destroy(ctx->topk_sel);
   ctx->pin.release();
   for (auto s : ctx->aux)
     if (s) cudaStreamDestroy(s);
@@ -1340,6 +1343,172 @@ pact_status pact_full_allreduce(pact_comm* c, const float* grad, float* out, uin
     stats->seconds = ms * 1e-3;
     stats->mode_used = PACT_SYNC_FULL;
     stats->value_count = len;
+  }
+  return PACT_OK;
+}
+
+// ------------------------------------------------------------- TopK
+
+pact_status pact_topk_count(uint64_t len, float rate, uint64_t* k_out) {
+  if (!k_out) return fail(PACT_E_INVALID_ARG, "null out");
+  if (!(rate > 0.0f && rate <= 1.0f))  // codec.cpp:148-149
+    return fail(PACT_E_INVALID_RATE, "rate %g outside (0, 1]", (double)rate);
+  // codec.cpp:153-155: k = max(1, floor(rate*len + len*1e-7)), capped at len
+  const uint64_t k = std::max<uint64_t>(
+      1, (uint64_t)std::floor((double)rate * (double)len + (double)len * 1e-7));
+  *k_out = std::min<uint64_t>(k, len);
+  return PACT_OK;
+}
+
+namespace {
+// selection bitmap of the k largest |g| (ties -> lower index): the prune
+// machinery with k_drop = len - k, whose tie fix-up keeps the LOW ranks
+pact_status topk_mask(pact_ctx* ctx, const float* g, uint64_t len, uint64_t k, cudaStream_t s,
+                      pact_mask** out) {
+  if (!ctx->topk_sel || ctx->topk_sel->len != len) {
+    if (ctx->topk_sel) pact_mask_destroy(ctx->topk_sel);
+    ctx->topk_sel = nullptr;
+    TRY(pact_mask_create(ctx, len, &ctx->topk_sel));
+  }
+  pact_mask* m = ctx->topk_sel;
+  *out = m;
+  m->changed = 1;
+  m->digest_valid = 0;
+  m->spec_valid = 0;
+  const uint64_t kd = len - k;
+  if (kd == 0 || len == 0) return pact_mask_fill(m, 1, s);
+  const uint64_t nc = m->ntiles;
+  TRY(m->tie_words.ensure(m->nwords * 8));
+  TRY(m->ties[0].ensure(nc * 4));
+  TRY(m->tie_prefix.ensure((nc + 1) * 4));
+  pact_prune_stats st{};
+  uint32_t T = 0;
+  uint64_t c_lt = 0;
+  TRY(find_threshold(ctx, g, len, kd, s, &T, &c_lt, &st));
+  Small* sm = ctx->ws_small.as<Small>();
+  const uint64_t r = kd - c_lt;  // ties dropped (the highest-index ones)
+  pactk::launch_prune_bitmap(g, len, T, r, nullptr, m->words, m->tile_popc, m->ties[0].as<uint32_t>(),
+                             nullptr, m->tie_words.as<uint64_t>(), &sm->bcounts, s);
+  CUDA_TRY(cudaGetLastError());
+  pactk::BitmapCounts hb{};
+  CUDA_TRY(cudaMemcpyAsync(ctx->pin.p, &sm->bcounts, sizeof hb, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  std::memcpy(&hb, ctx->pin.p, sizeof hb);
+  if (hb.n_lt != c_lt || !(c_lt < kd && kd <= hb.n_lt + hb.n_eq))
+    return fail(PACT_E_RUN_FAILURE, "topk threshold inconsistent (T=%u)", T);
+  const uint64_t r_keep = hb.n_eq - r;  // ties kept: the lowest-index ones
+  if (r_keep) {
+    TRY(scan(ctx, m->ties[0].as<uint32_t>(), nc, m->tie_prefix.as<uint32_t>(), s));
+    pactk::launch_prune_tiefix(m->words, len, m->tie_words.as<uint64_t>(), m->ties[0].as<uint32_t>(),
+                               m->tie_prefix.as<uint32_t>(), r_keep, m->tile_popc, s, 1);
+  }
+  m->ties_cur = 0;
+  TRY(scan(ctx, m->tile_popc, nc, m->tile_off, s));
+  uint32_t* pin32 = ctx->pin.as<uint32_t>();
+  CUDA_TRY(cudaMemcpyAsync(pin32, m->tile_off + nc, 4, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  m->nnz = pin32[0];
+  m->host_tile_off_valid = 0;
+  if (m->nnz != k)
+    return fail(PACT_E_RUN_FAILURE, "topk selected %llu, expected %llu", (unsigned long long)m->nnz,
+                (unsigned long long)k);
+  return PACT_OK;
+}
+}  // namespace
+
+pact_status pact_topk_select(pact_ctx* ctx, const float* grad, uint64_t len, float rate,
+                             uint32_t* indices, float* values, uint64_t* k_out, pact_stream_t stream) {
+  if (!ctx || (len && !grad)) return fail(PACT_E_INVALID_ARG, "null args");
+  uint64_t k = 0;
+  TRY(pact_topk_count(len, rate, &k));
+  if (len > PACT_MAX_LEN) return fail(PACT_E_SHAPE_MISMATCH, "len > PACT_MAX_LEN");
+  if (k && (!indices || !values)) return fail(PACT_E_INVALID_ARG, "null outputs");
+  TRY(set_device(ctx));
+  TRY(ensure_ctx_ws(ctx));
+  cudaStream_t s = stream;
+  if (len) {
+    pact_mask* m = nullptr;
+    TRY(topk_mask(ctx, grad, len, k, s, &m));
+    pactk::launch_pack(grad, len, m->words, m->tile_off, values, 0, m->ntiles, s);
+    pactk::launch_pack_index(len, m->words, m->tile_off, indices, s);
+    CUDA_TRY(cudaGetLastError());
+  }
+  if (k_out) *k_out = k;
+  return PACT_OK;
+}
+
+pact_status pact_topk_densify(pact_ctx* ctx, const uint32_t* indices, const float* values, uint64_t k,
+                              uint64_t len, float* out, pact_stream_t stream) {
+  if (!ctx || (k && (!indices || !values)) || (len && !out)) return fail(PACT_E_INVALID_ARG, "null args");
+  TRY(set_device(ctx));
+  TRY(ensure_ctx_ws(ctx));
+  cudaStream_t s = stream;
+  int* err = reinterpret_cast<int*>(&ctx->ws_small.as<Small>()->changed);
+  CUDA_TRY(cudaMemsetAsync(err, 0, 4, s));
+  if (len) CUDA_TRY(cudaMemsetAsync(out, 0, len * 4, s));  // codec.cpp:175 (+0.0f)
+  pactk::launch_scatter_f32(indices, values, k, len, out, err, s);
+  CUDA_TRY(cudaGetLastError());
+  int* pin = ctx->pin.as<int>();
+  CUDA_TRY(cudaMemcpyAsync(pin, err, 4, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  if (pin[0]) return fail(PACT_E_CORRUPT_PAYLOAD, "topk index out of range");  // codec.cpp:177-178
+  return PACT_OK;
+}
+
+pact_status pact_topk_allgather_aggregate(pact_comm* c, pact_ctx* ctx, const float* grad, uint64_t len,
+                                          float rate, uint32_t epoch, float* out, pact_sync_stats* stats,
+                                          pact_stream_t stream) {
+  (void)epoch;  // carried by the reference's frame header only
+  if (!ctx || (len && (!grad || !out))) return fail(PACT_E_INVALID_ARG, "null args");
+  if (c && c->ctx != ctx) return fail(PACT_E_INVALID_ARG, "comm belongs to another ctx");
+  uint64_t k = 0;
+  TRY(pact_topk_count(len, rate, &k));
+  TRY(set_device(ctx));
+  TRY(ensure_ctx_ws(ctx));
+  cudaStream_t s = stream;
+  const int n = c ? c->n : 1;
+  CUDA_TRY(cudaEventRecord(ctx->t0, s));
+  // [own idx k | own val k] [n blocks of 2k words] [f64 acc len], 16-byte aligned
+  const uint64_t blk = (2 * k + 3) & ~3ull;
+  const uint64_t words32 = blk * (uint64_t)(n + 1);
+  TRY(ctx->topk.ensure(words32 * 4 + len * 8 + 16));
+  uint32_t* own = ctx->topk.as<uint32_t>();
+  uint32_t* all = own + blk;
+  double* acc = reinterpret_cast<double*>(ctx->topk.as<char>() + ((words32 * 4 + 15) & ~15ull));
+  int* err = reinterpret_cast<int*>(&ctx->ws_small.as<Small>()->changed);
+  CUDA_TRY(cudaMemsetAsync(err, 0, 4, s));
+  if (len) {
+    TRY(pact_topk_select(ctx, grad, len, rate, own, reinterpret_cast<float*>(own + k), nullptr, s));
+    const uint32_t* blocks = own;
+    if (c) {
+      NCCL_TRY(ncclAllGather(own, all, blk * 4, ncclUint8, c->nccl, s));
+      blocks = all;
+    }
+    // collective.cpp:383-388: acc[i] += values, ranks in order; mean = float(acc / n)
+    CUDA_TRY(cudaMemsetAsync(acc, 0, len * 8, s));
+    for (int q = 0; q < n; ++q) {
+      const uint32_t* b = blocks + (uint64_t)q * blk;
+      pactk::launch_scatter_add_f64(b, reinterpret_cast<const float*>(b + k), k, len, acc, err, s);
+    }
+    pactk::launch_f64_mean(acc, len, n, out, s);
+    CUDA_TRY(cudaGetLastError());
+    int* pin = ctx->pin.as<int>();
+    CUDA_TRY(cudaMemcpyAsync(pin, err, 4, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    if (pin[0]) return fail(PACT_E_CORRUPT_PAYLOAD, "topk index out of range");
+  }
+  if (stats) {
+    CUDA_TRY(cudaEventRecord(ctx->t1, s));
+    CUDA_TRY(cudaEventSynchronize(ctx->t1));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, ctx->t0, ctx->t1);
+    *stats = pact_sync_stats{};
+    // ring all-gather of n equal frames: 26-byte header + 4k indices + 4k values
+    stats->bytes_on_wire = c ? (uint64_t)(n - 1) * (PACT_HEADER_BYTES + 8 * k) : 0;
+    stats->seconds = ms * 1e-3;
+    stats->mode_used = PACT_SYNC_TOPK;
+    stats->value_count = k;
+    stats->transport = c ? PACT_TRANSPORT_NCCL : 0;
   }
   return PACT_OK;
 }

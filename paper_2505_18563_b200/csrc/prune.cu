@@ -413,11 +413,13 @@ __global__ void __launch_bounds__(kPruneWarps * 32)
 
 // ----------------------------------------------------------------- tiefix
 // Rewrite the tie bits of chunks with ties: the first D = clamp(r - prefix,
-// 0, E) ties of the chunk (index order) are dropped, the rest kept.
+// 0, E) ties of the chunk (index order) are dropped, the rest kept -- or,
+// keep_low (TopK, codec.cpp:147-172: ties select the lower index), the
+// first D kept and the rest dropped.
 __global__ void __launch_bounds__(256)
     prune_tiefix_kernel(uint64_t* __restrict__ words, uint64_t nwords,
                         const uint64_t* __restrict__ tie_words, const uint32_t* __restrict__ ties,
-                        const uint32_t* __restrict__ tie_prefix, uint64_t r,
+                        const uint32_t* __restrict__ tie_prefix, uint64_t r, int keep_low,
                         uint32_t* __restrict__ chunk_popc, uint64_t nchunks) {
   const int lane = threadIdx.x & 31;
   const uint64_t c = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
@@ -434,15 +436,16 @@ __global__ void __launch_bounds__(256)
   const uint64_t excl = inc - tc;
   uint64_t d = D > excl ? D - excl : 0;
   if (d > tc) d = tc;
-  uint64_t drop = 0, x = tw;
+  uint64_t first = 0, x = tw;  // the chunk's first d ties of this word
   for (uint64_t n = 0; n < d; ++n) {
     const uint64_t b = x & (~x + 1);
-    drop |= b;
+    first |= b;
     x ^= b;
   }
   uint32_t pc = 0;
   if (valid) {
-    const uint64_t nw = (words[wi] & ~tw) | (tw & ~drop);
+    // prune: the first ties (lowest indices) are dropped; TopK keeps them
+    const uint64_t nw = (words[wi] & ~tw) | (keep_low ? first : (tw & ~first));
     words[wi] = nw;
     pc = (uint32_t)__popcll(nw);
   }
@@ -615,11 +618,11 @@ void launch_prune_bitmap(const float* w, uint64_t len, uint32_t T, uint64_t r,
 
 void launch_prune_tiefix(uint64_t* words, uint64_t len, const uint64_t* tie_words,
                          const uint32_t* ties, const uint32_t* tie_prefix, uint64_t r,
-                         uint32_t* chunk_popc, cudaStream_t s) {
+                         uint32_t* chunk_popc, cudaStream_t s, int keep_low) {
   const uint64_t nc = (len + kChunk - 1) / kChunk;
   if (!nc) return;
   prune_tiefix_kernel<<<(unsigned)((nc * 32 + 255) / 256), 256, 0, s>>>(
-      words, (len + 63) / 64, tie_words, ties, tie_prefix, r, chunk_popc, nc);
+      words, (len + 63) / 64, tie_words, ties, tie_prefix, r, keep_low, chunk_popc, nc);
   note_launch();
 }
 

@@ -1,0 +1,113 @@
+// topk.cu -- TopK payload kernels.
+//
+// Reference: topk_select / topk_densify (codec.cpp:147-182) and the mean in
+// topk_allgather_aggregate (collective.cpp:370-390). The selection itself
+// reuses the prune machinery (radix select of the threshold + bitmap +
+// tie fix-up with the lower-index-first tie rule, prune.cu); here are the
+// payload kernels around it:
+//  * pack_index: ascending indices of the selected bits (the values come
+//    from pack_kernel over the same mask);
+//  * scatter_add_f64 / f64_mean: the per-element double accumulator over
+//    ranks in rank order, then float(acc / n);
+//  * scatter_f32: topk_densify (zeros elsewhere, out-of-range -> error).
+#include "common.cuh"
+#include "launch.h"
+
+namespace pactk {
+
+namespace {
+
+// warp per 1024-element chunk; lane l owns the 32-bit half l of the chunk's
+// 16 words, so its indices are consecutive from chunk_off[c] + (excl scan).
+__global__ void __launch_bounds__(256)
+    pack_index_kernel(uint64_t len, const uint32_t* __restrict__ words32,
+                      const uint32_t* __restrict__ chunk_off, uint32_t* __restrict__ idx,
+                      uint64_t nchunks) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t nhalves = 2 * ((len + 63) / 64);
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t c = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; c < nchunks; c += nw) {
+    const uint64_t h = c * 32 + lane;
+    uint32_t bits = h < nhalves ? words32[h] : 0u;
+    const uint32_t cnt = __popc(bits);
+    uint32_t pos = chunk_off[c] + warp_incl_scan(cnt) - cnt;
+    const uint32_t base = (uint32_t)(h * 32);
+    while (bits) {
+      const int b = __ffs(bits) - 1;
+      idx[pos++] = base + (uint32_t)b;
+      bits &= bits - 1;
+    }
+  }
+}
+
+__global__ void scatter_add_f64_kernel(const uint32_t* __restrict__ idx, const float* __restrict__ val,
+                                       uint64_t k, uint64_t len, double* __restrict__ acc,
+                                       int* __restrict__ err) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < k; j += stride) {
+    const uint32_t i = idx[j];
+    if (i >= len) {
+      atomicOr(err, 1);
+      continue;
+    }
+    acc[i] += (double)val[j];
+  }
+}
+
+__global__ void f64_mean_kernel(const double* __restrict__ acc, uint64_t len, int n, float* __restrict__ out) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < len; i += stride)
+    out[i] = (float)(acc[i] / (double)n);
+}
+
+__global__ void scatter_f32_kernel(const uint32_t* __restrict__ idx, const float* __restrict__ val,
+                                   uint64_t k, uint64_t len, float* __restrict__ out, int* __restrict__ err) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < k; j += stride) {
+    const uint32_t i = idx[j];
+    if (i >= len)
+      atomicOr(err, 1);
+    else
+      out[i] = val[j];
+  }
+}
+
+unsigned grid_of(uint64_t n) {
+  uint64_t g = (n + 255) / 256;
+  return (unsigned)(g > 4736 ? 4736 : (g ? g : 1));
+}
+
+}  // namespace
+
+void launch_pack_index(uint64_t len, const uint64_t* words, const uint32_t* chunk_off, uint32_t* idx,
+                       cudaStream_t s) {
+  const uint64_t nc = (len + kChunk - 1) / kChunk;
+  if (!nc) return;
+  uint64_t grid = (nc * 32 + 255) / 256;
+  if (grid > 148 * 16) grid = 148 * 16;
+  pack_index_kernel<<<(unsigned)grid, 256, 0, s>>>(len, reinterpret_cast<const uint32_t*>(words),
+                                                   chunk_off, idx, nc);
+  note_launch();
+}
+
+void launch_scatter_add_f64(const uint32_t* idx, const float* val, uint64_t k, uint64_t len, double* acc,
+                            int* err, cudaStream_t s) {
+  if (!k) return;
+  scatter_add_f64_kernel<<<grid_of(k), 256, 0, s>>>(idx, val, k, len, acc, err);
+  note_launch();
+}
+
+void launch_f64_mean(const double* acc, uint64_t len, int n, float* out, cudaStream_t s) {
+  if (!len) return;
+  f64_mean_kernel<<<grid_of(len), 256, 0, s>>>(acc, len, n, out);
+  note_launch();
+}
+
+void launch_scatter_f32(const uint32_t* idx, const float* val, uint64_t k, uint64_t len, float* out,
+                        int* err, cudaStream_t s) {
+  if (!k) return;
+  scatter_f32_kernel<<<grid_of(k), 256, 0, s>>>(idx, val, k, len, out, err);
+  note_launch();
+}
+
+}  // namespace pactk

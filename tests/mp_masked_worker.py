@@ -198,6 +198,17 @@ def main():
     check("fp16 packed: bytes",
           rp.stats.bytes_on_wire == 26 * (world - 1) + port.ring_bytes(world, rank, int(bits.sum())) // 2)
 
+    # ---- TopK all-gather baseline (collective.cpp:370-390), SURVEY 8f-4
+    grads = [(np.round(synth.synth_host(n, synth.grad_seed(r, 15), synth.G_FULL) * 8) / 8).astype(np.float32)
+             for r in range(world)]  # coarse grid: heavy ties across ranks
+    g = torch.from_numpy(grads[rank]).to(dev)
+    rk = pb.topk_allgather_aggregate(g, 0.02, 0, comm)
+    sel = [port.topk_select(x, 0.02) for x in grads]
+    want = port.topk_mean([q[0] for q in sel], [q[1] for q in sel], n)
+    check("topk: bit-exact vs oracle", np.array_equal(u32(rk.tensor.cpu().numpy()), u32(want)))
+    check("topk: bytes", rk.stats.bytes_on_wire == (world - 1) * (26 + 8 * sel[0][0].size))
+    check("topk: mode", rk.stats.mode_used == pb.SyncMode.TopKAllGather)
+
     flag = torch.tensor([len(failures)], device=dev)
     dist.all_reduce(flag)
     comm.close()
