@@ -207,6 +207,11 @@ def main():
     ap.add_argument("--bucket-mb", type=float, default=None)
     ap.add_argument("--transport", default="auto", choices=["auto", "nccl", "p2p"],
                     help="packed exchange for N > 1: NCCL allreduce or the fused NVLink P2P path")
+    ap.add_argument("--path", default="masked", choices=["masked", "ternary", "fp16", "fp16-packed", "topk"],
+                    help="masked: the headline (masked_allreduce); the others time the SURVEY 8f rows "
+                         "on the same workload (ternary_allgather_aggregate, fp16_allreduce, "
+                         "masked_allreduce on the binary16 wire, topk_allgather_aggregate)")
+    ap.add_argument("--topk-rate", type=float, default=0.01)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -298,6 +303,10 @@ def main():
             evs.append((a, b))
         torch.cuda.synchronize()
         return [a.elapsed_time(b) * 1e-3 for a, b in evs]
+
+    if args.path != "masked":
+        return run_path(args, pb, torch, comm, rank, world, local, dev, cfg, model, ratio, shape, n, nnz, mask,
+                        tracker, grad, out, timed, barrier)
 
     # ---- headline: device-resident step
     for i in range(args.warmup):
@@ -420,6 +429,88 @@ def main():
             "roofline": roofline, "stages": stages, **({"allreduce": extra} if extra else {}),
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if comm is not None:
+        torch.distributed.barrier()
+        comm.close()
+        torch.distributed.destroy_process_group()
+
+
+def run_path(args, pb, torch, comm, rank, world, local, dev, cfg, model, ratio, shape, n, nnz, mask, tracker,
+             grad, out, timed, barrier):
+    """The SURVEY 8f rows on the headline workload: one step = one call of the
+    path's aggregate over the model-sized gradient (inputs HBM resident, L2
+    flushed, CUDA events, max over ranks). `roofline` is the whole step's
+    algorithmic HBM bytes (per kernel) over its time."""
+    from paper_2505_18563_b200 import synth
+
+    k = pb.topk_count(n, args.topk_rate)
+    seed = synth.grad_seed(rank, 7)
+    if args.path == "ternary":
+        def step(e):
+            return pb.ternary_allgather_aggregate(grad, mask, pb.TrackerStatus.Stable, seed + e, e, comm, out=out)
+        mode = pb.SyncMode.TernaryAllGather
+        # pack, absmax, ternarize, mean over n blocks, unpack
+        alg = (4 * n + n / 8 + 4 * nnz) + 4 * nnz + (4 * nnz + nnz / 4) + (world * nnz / 4 + 4 * nnz) + \
+              (4 * nnz + n / 8 + 4 * n)
+    elif args.path == "fp16":
+        def step(e):
+            return pb.fp16_allreduce(grad, comm, out=out)
+        mode = pb.SyncMode.Fp16AllReduce
+        c = n / world  # encode + (n-1) steps + gather (decode into the full output)
+        alg = (4 * c + 2 * c) + (world - 1) * (4 * c + 2 * c + 2 * c) + (2 * n + 4 * n) if world > 1 else 8 * n
+    elif args.path == "fp16-packed":
+        pol = pb.SyncPolicy(wire=pb.SyncPolicy.F16)
+
+        def step(e):
+            return pb.masked_allreduce(grad, mask, pb.TrackerStatus.Stable, e, comm, policy=pol, out=out)
+        mode = pb.SyncMode.PackedAllReduce
+        c = nnz / world
+        ring = ((4 * c + 2 * c) + (world - 1) * (4 * c + 2 * c + 2 * c) + (2 * nnz + 4 * nnz)) if world > 1 \
+            else 8 * nnz
+        alg = (4 * n + n / 8 + 4 * nnz) + ring + (4 * nnz + n / 8 + 4 * n)
+    else:  # topk
+        def step(e):
+            return pb.topk_allgather_aggregate(grad, args.topk_rate, e, comm, out=out)
+        mode = pb.SyncMode.TopKAllGather
+        # threshold (sample + count reads), bitmap, pack values + indices,
+        # f64 zero + n scatter-adds + mean
+        alg = 4 * n + (4 * n + n / 8) + (4 * n + n / 8 + 4 * k) + (n / 8 + 4 * k) + 8 * n + \
+              world * (8 * k + 16 * k) + (8 * n + 4 * n)
+    for i in range(args.warmup):
+        r = step(i)
+    assert r.stats.mode_used == mode, r.stats
+    barrier()
+    ctx = pb.Context.get(local)
+    l0 = ctx.kernel_launches()
+    with ClockSampler(local) as clk:
+        barrier()
+        ts = timed(step, args.steps)
+        barrier()
+    launches = ctx.kernel_launches() - l0
+    t_step = sum(ts) / len(ts)
+    if world > 1:
+        tt = torch.tensor([t_step], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        t_step = float(tt.item())
+    peak, peak_kind = peaks()
+    achieved = alg / t_step / 1e9
+    if rank == 0:
+        line = {
+            "metric": METRIC.replace("prune+pack+allreduce+unpack", args.path + " aggregate"),
+            "value": round(4.0 * n / t_step / 1e9 * world, 2), "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t_step * 1e3, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "path": args.path,
+            "config": {"workload": f"{cfg}:{model} fp32 grads, {int(round(ratio * 100))}% magnitude-pruned mask",
+                       "len": n, "nnz": nnz, "topk_k": k if args.path == "topk" else None,
+                       "l2": "flushed before every timed step", "parallelism": f"dp{world}",
+                       "bytes_on_wire": r.stats.bytes_on_wire},
+            "roofline": {"bound": "hbm", "kernel": "whole step", "achieved": round(achieved, 1), "peak": peak,
+                         "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
+                         "peak_kind": peak_kind, "algorithmic_bytes": int(alg)},
+            "gpu_launches": int(launches), "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
     if comm is not None:
