@@ -25,6 +25,7 @@
 // formulation minimises instructions per element.
 #include "common.cuh"
 #include "launch.h"
+#include "p2p_sync.cuh"
 
 namespace pactk {
 
@@ -179,28 +180,101 @@ __device__ __forceinline__ void offs_words_issue(uint64_t* dst, const uint64_t* 
                  : "memory");
   }
 }
+// Copy a packed run of cnt floats into shared memory. When dst and src agree
+// mod 16 bytes the interior moves as 16-byte cp.async.cg (a quarter of the
+// copy instructions, and full-sector requests over NVLink), the ragged head
+// and tail as 4-byte copies. Callers place dst at the source's 16-byte phase
+// (run_phase) so the fast path always applies.
+__device__ __forceinline__ uint32_t run_phase(const float* src) { return ((uintptr_t)src >> 2) & 3u; }
 __device__ __forceinline__ void run_issue(float* dst, const float* __restrict__ src, uint32_t cnt) {
   const int lane = threadIdx.x & 31;
-  for (uint32_t i = lane; i < cnt; i += 32) {
+  auto cp4 = [&](uint32_t i) {
     const uint32_t sa = (uint32_t)__cvta_generic_to_shared(dst + i);
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(src + i) : "memory");
+  };
+  if ((((uintptr_t)dst ^ (uintptr_t)src) & 15) != 0) {
+    for (uint32_t i = lane; i < cnt; i += 32) cp4(i);
+    return;
   }
+  uint32_t head = (4u - run_phase(src)) & 3u;
+  if (head > cnt) head = cnt;
+  const uint32_t nvec = (cnt - head) >> 2, tail0 = head + 4 * nvec;
+  if ((uint32_t)lane < head) cp4(lane);
+  for (uint32_t q = lane; q < nvec; q += 32) {
+    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(dst + head + 4 * q);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(src + head + 4 * q) : "memory");
+  }
+  if ((uint32_t)lane < cnt - tail0) cp4(tail0 + lane);
 }
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 
-template <bool kSgd>
+// Where a chunk's packed run comes from (the exchange fused into unpack):
+//   kSrcLocal  this rank's packed (or already reduced) vector;
+//   kSrcPair   NVLink one-shot, n = 2: the local run and the peer's run
+//              (peer memory), summed at expansion -- the reference fold of
+//              two terms, x_c + x_{c+1}, is the same in either order;
+//   kSrcOwner  NVLink two-shot all-gather: the run read straight from the
+//              owner's reduced chunk (owner = j / C, at most one owner
+//              boundary per run since C >= 1024).
+constexpr int kSrcLocal = 0, kSrcPair = 1, kSrcOwner = 2;
+
+constexpr int kRunCap = kChunk + 4;  // a run plus its 16-byte phase
+
+// source(s) of run [b, b + cnt); stage slot layout: run at phase offset
+// run_phase(src), the pair variant's peer run kRunCap floats further
+template <int kSrc>
+__device__ __forceinline__ const float* run_src(const float* __restrict__ packed, const P2PView& v, uint32_t b,
+                                                int which) {
+  if constexpr (kSrc == kSrcLocal) return packed + b;
+  else if constexpr (kSrc == kSrcPair) return (which ? v.packed[v.rank ^ 1] : packed) + b;
+  else return v.reduced[b / v.C] + b;
+}
+
+template <int kSrc>
+__device__ __forceinline__ void issue_run(float* dst, const float* __restrict__ packed, const P2PView& v,
+                                          uint32_t b, uint32_t cnt) {
+  if constexpr (kSrc == kSrcLocal) {
+    const float* src = packed + b;
+    run_issue(dst + run_phase(src), src, cnt);
+  } else if constexpr (kSrc == kSrcPair) {
+    const float* a = packed + b;
+    const float* r = v.packed[v.rank ^ 1] + b;
+    run_issue(dst + run_phase(a), a, cnt);
+    run_issue(dst + kRunCap + run_phase(r), r, cnt);
+  } else {  // owners' reduced chunks live at the absolute packed index
+    const uint64_t o = b / v.C, nb = (o + 1) * v.C;
+    const uint32_t n1 = nb - b < cnt ? (uint32_t)(nb - b) : cnt;
+    const float* a = v.reduced[o] + b;
+    const uint32_t ph = run_phase(a);
+    run_issue(dst + ph, a, n1);
+    if (n1 < cnt) run_issue(dst + ph + n1, v.reduced[o + 1] + b + n1, cnt - n1);
+  }
+}
+
+template <bool kSgd, int kSrc>
 __global__ void __launch_bounds__(kPuWarps * 32)
     unpack_kernel(const float* __restrict__ packed, uint64_t len, const uint64_t* __restrict__ words,
                   const uint32_t* __restrict__ chunk_off, float scale, int do_scale,
                   float* __restrict__ out, float lr, float* __restrict__ weights, uint64_t cb,
-                  uint64_t ce) {
-  __shared__ __align__(16) float psm[kPuWarps][2][kChunk];
+                  uint64_t ce, P2PView v, const uint64_t* __restrict__ flags, uint64_t target,
+                  int* __restrict__ err, P2PSig sg) {
+  // packed-run stages: static, except the pair variant's two runs per stage
+  // (64 KiB per CTA, dynamic shared memory)
+  constexpr int kRun = kSrc == kSrcPair ? 2 * kRunCap : kRunCap;
+  __shared__ __align__(16) float st_psm[kSrc == kSrcPair ? 4 : kPuWarps * 2 * kRun];
+  extern __shared__ __align__(16) float dyn_psm[];
+  float* const psm_base = kSrc == kSrcPair ? dyn_psm : st_psm;
+  auto psm = [&](int w, int st) { return psm_base + (w * 2 + st) * kRun; };
   __shared__ __align__(16) uint64_t wsm[kPuWarps][3][kWbuf];
+  if constexpr (kSrc != kSrcLocal) {  // peers' PACKED (one-shot) / REDUCED (two-shot) flags
+    p2psync::entry_signal(v, sg);
+    p2psync::block_wait_flags(flags, kSrc == kSrcPair ? kP2PPacked : kP2PReduced, v.n, target, err);
+  }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const bool vec_ok = ((((uintptr_t)out) | (kSgd ? (uintptr_t)weights : 0)) & 15) == 0;
   const uint64_t nwt = (uint64_t)gridDim.x * kPuWarps;
   uint64_t c = cb + (uint64_t)blockIdx.x * kPuWarps + warp;
-  if (c >= ce) return;
+  if (c < ce) {
   auto offs = [&](int slot, uint32_t& b, uint32_t& n) {
     const uint32_t* o = reinterpret_cast<const uint32_t*>(wsm[warp][slot] + kChunkWords);
     b = o[0];
@@ -216,7 +290,7 @@ __global__ void __launch_bounds__(kPuWarps * 32)
   {
     uint32_t b, n;
     offs(0, b, n);
-    run_issue(psm[warp][0], packed + b, n);
+    issue_run<kSrc>(psm(warp, 0), packed, v, b, n);
   }
   cp_commit();
   int wi = 0, pi = 0;
@@ -229,11 +303,12 @@ __global__ void __launch_bounds__(kPuWarps * 32)
     if (c + nwt < ce) {
       uint32_t b, n;
       offs(w1, b, n);
-      run_issue(psm[warp][pi ^ 1], packed + b, n);
+      issue_run<kSrc>(psm(warp, pi ^ 1), packed, v, b, n);
     }
     cp_commit();
     const uint64_t* wc = wsm[warp][wi];
-    const float* stage = psm[warp][pi];
+    const uint32_t rb = reinterpret_cast<const uint32_t*>(wsm[warp][wi] + kChunkWords)[0];
+    const float* stage = psm(warp, pi) + run_phase(run_src<kSrc>(packed, v, rb, 0));
     const uint64_t e0 = c * (uint64_t)kChunk + 4 * lane;
     uint32_t run = 0;
 #pragma unroll
@@ -248,6 +323,13 @@ __global__ void __launch_bounds__(kPuWarps * 32)
       o[1] = b1 ? stage[s.pos + b0] : 0.0f;
       o[2] = b2 ? stage[s.pos + b0 + b1] : 0.0f;
       o[3] = (nib & 8) ? stage[s.pos + b0 + b1 + b2] : 0.0f;
+      if constexpr (kSrc == kSrcPair) {  // + the peer's value (one-shot fold, n = 2)
+        const float* peer = psm(warp, pi) + kRunCap + run_phase(run_src<kSrc>(packed, v, rb, 1));
+        if (b0) o[0] = __fadd_rn(o[0], peer[s.pos]);
+        if (b1) o[1] = __fadd_rn(o[1], peer[s.pos + b0]);
+        if (b2) o[2] = __fadd_rn(o[2], peer[s.pos + b0 + b1]);
+        if (nib & 8) o[3] = __fadd_rn(o[3], peer[s.pos + b0 + b1 + b2]);
+      }
       if (do_scale) {
 #pragma unroll
         for (int b = 0; b < 4; ++b)
@@ -282,6 +364,8 @@ __global__ void __launch_bounds__(kPuWarps * 32)
     pi ^= 1;
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
+  }
+  if constexpr (kSrc != kSrcLocal) p2psync::exit_signal(v, sg);  // READ: peers may reuse their buffers
 }
 
 // ------------------------------------------------------------------- GSE
@@ -488,9 +572,40 @@ void launch_unpack(const float* packed, uint64_t len, const uint64_t* words,
                    uint64_t ce, cudaStream_t s) {
   if (ce <= cb) return;
   static int cap = 0;
-  if (!cap) cap = persistent_grid(unpack_kernel<false>, kPuWarps);
-  unpack_kernel<false><<<grid_for(cap, ce - cb, kPuWarps), kPuWarps * 32, 0, s>>>(
-      packed, len, words, chunk_off, scale, do_scale, out, 0.f, nullptr, cb, ce);
+  if (!cap) cap = persistent_grid(unpack_kernel<false, kSrcLocal>, kPuWarps);
+  unpack_kernel<false, kSrcLocal><<<grid_for(cap, ce - cb, kPuWarps), kPuWarps * 32, 0, s>>>(
+      packed, len, words, chunk_off, scale, do_scale, out, 0.f, nullptr, cb, ce, P2PView{}, nullptr, 0,
+      nullptr, P2PSig{});
+  note_launch();
+}
+
+void launch_unpack_p2p(const float* packed_local, uint64_t len, const uint64_t* words,
+                       const uint32_t* chunk_off, float scale, int do_scale, float* out, const P2PView& v,
+                       int two_shot, const uint64_t* flags, uint64_t target, int* err, const P2PSig& sg,
+                       cudaStream_t s) {
+  const uint64_t nc = (len + kChunk - 1) / kChunk;
+  if (!nc) return;
+  // every CTA runs the flag wait and the exit count, so each gets >= 1 chunk
+  // per warp 0 (grid <= ceil(nc / kPuWarps))
+  if (!two_shot) {
+    constexpr int kDyn = kPuWarps * 2 * 2 * kRunCap * sizeof(float);
+    static int cap = 0;
+    if (!cap) {
+      cudaFuncSetAttribute(unpack_kernel<false, kSrcPair>, cudaFuncAttributeMaxDynamicSharedMemorySize, kDyn);
+      int per_sm = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, unpack_kernel<false, kSrcPair>, kPuWarps * 32, kDyn);
+      cap = sm_count() * (per_sm > 0 ? per_sm : 1);
+    }
+    unpack_kernel<false, kSrcPair><<<grid_for(cap, nc, kPuWarps), kPuWarps * 32, kDyn, s>>>(
+        packed_local, len, words, chunk_off, scale, do_scale, out, 0.f, nullptr, 0, nc, v, flags, target,
+        err, sg);
+  } else {
+    static int cap = 0;
+    if (!cap) cap = persistent_grid(unpack_kernel<false, kSrcOwner>, kPuWarps);
+    unpack_kernel<false, kSrcOwner><<<grid_for(cap, nc, kPuWarps), kPuWarps * 32, 0, s>>>(
+        packed_local, len, words, chunk_off, scale, do_scale, out, 0.f, nullptr, 0, nc, v, flags, target,
+        err, sg);
+  }
   note_launch();
 }
 
@@ -500,9 +615,10 @@ void launch_unpack_sgd(const float* packed, uint64_t len, const uint64_t* words,
   const uint64_t nc = (len + kChunk - 1) / kChunk;
   if (!nc) return;
   static int cap = 0;
-  if (!cap) cap = persistent_grid(unpack_kernel<true>, kPuWarps);
-  unpack_kernel<true><<<grid_for(cap, nc, kPuWarps), kPuWarps * 32, 0, s>>>(
-      packed, len, words, chunk_off, scale, do_scale, grad_out, lr, weights, 0, nc);
+  if (!cap) cap = persistent_grid(unpack_kernel<true, kSrcLocal>, kPuWarps);
+  unpack_kernel<true, kSrcLocal><<<grid_for(cap, nc, kPuWarps), kPuWarps * 32, 0, s>>>(
+      packed, len, words, chunk_off, scale, do_scale, grad_out, lr, weights, 0, nc, P2PView{}, nullptr, 0,
+      nullptr, P2PSig{});
   note_launch();
 }
 

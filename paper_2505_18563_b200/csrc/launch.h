@@ -17,6 +17,16 @@ struct P2PView {  // device-visible pointers into every rank's symmetric buffer
   int rank, n;
   uint64_t M, C;                       // packed count, ChunkMap chunk = ceil(M/n)
 };
+// signals fused into the exchange kernels: `entry` published by block 0 at
+// start (the producer ran before on the stream), `exit` by the last CTA to
+// finish; kind < 0 = none. counter: a zeroed u32, self-resetting.
+struct P2PSig {
+  int entry_kind = -1;
+  uint64_t entry_val = 0;
+  int exit_kind = -1;
+  uint64_t exit_val = 0;
+  unsigned* counter = nullptr;
+};
 
 // ---- codec.cu --------------------------------------------------------------
 // chunk range [cb, ce) of 1024-element chunks; all pointers device.
@@ -25,6 +35,14 @@ void launch_pack(const float* g, uint64_t len, const uint64_t* words, const uint
 void launch_unpack(const float* packed, uint64_t len, const uint64_t* words,
                    const uint32_t* chunk_off, float scale, int do_scale, float* out, uint64_t cb,
                    uint64_t ce, cudaStream_t s);
+// unpack with the exchange fused in (NVLink P2P, B == 1): one-shot (n == 2)
+// sums the local and the peer's packed runs (waits PACKED); two-shot reads
+// each run from its owner's reduced chunk (waits REDUCED; needs C >= 1024).
+// Publishes sg's exit flag (READ) when every CTA is done.
+void launch_unpack_p2p(const float* packed_local, uint64_t len, const uint64_t* words,
+                       const uint32_t* chunk_off, float scale, int do_scale, float* out, const P2PView& v,
+                       int two_shot, const uint64_t* flags, uint64_t target, int* err, const P2PSig& sg,
+                       cudaStream_t s);
 void launch_unpack_sgd(const float* packed, uint64_t len, const uint64_t* words,
                        const uint32_t* chunk_off, float scale, int do_scale, float lr,
                        float* grad_out, float* weights, cudaStream_t s);
@@ -52,16 +70,6 @@ void launch_p2p_signal(const P2PView& v, int kind, uint64_t value, cudaStream_t 
 // wait until flags[kind][s] >= target for all s < n (10 s timeout -> *err)
 void launch_p2p_wait(const uint64_t* flags, int kind, int n, uint64_t target, int* err,
                      cudaStream_t s);
-// signals fused into the exchange kernels: `entry` published by block 0 at
-// start (the producer ran before on the stream), `exit` by the last CTA to
-// finish; kind < 0 = none. counter: a zeroed u32, self-resetting.
-struct P2PSig {
-  int entry_kind = -1;
-  uint64_t entry_val = 0;
-  int exit_kind = -1;
-  uint64_t exit_val = 0;
-  unsigned* counter = nullptr;
-};
 // fold packed[*][b, e) in the reference order into out[b, e) (waits PACKED);
 // max_ctas > 0 caps the grid (overlap with pack/unpack on other streams)
 void launch_p2p_fold(const P2PView& v, float* out, uint64_t b, uint64_t e, const uint64_t* flags,

@@ -29,41 +29,13 @@
 // instead of hanging.
 #include "common.cuh"
 #include "launch.h"
+#include "p2p_sync.cuh"
 
 namespace pactk {
 
 namespace {
 
-__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
-  uint64_t v;
-  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
-  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ uint64_t globaltimer() {
-  uint64_t t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-
-// thread 0 waits until flags[kind][s] >= target for all s < n; block barrier
-__device__ void block_wait_flags(const uint64_t* flags, int kind, int n, uint64_t target, int* err) {
-  if (threadIdx.x == 0) {
-    const uint64_t t0 = globaltimer();
-    for (int s = 0; s < n; ++s) {
-      while (ld_acquire_sys(flags + kind * kP2PMaxRanks + s) < target) {
-        if (globaltimer() - t0 > 10000000000ull) {  // 10 s: a peer died; fail, do not hang
-          atomicExch(err, 1);
-          break;
-        }
-        __nanosleep(64);
-      }
-    }
-  }
-  __syncthreads();
-}
+using namespace p2psync;
 
 __global__ void p2p_signal_kernel(P2PView v, int kind, uint64_t value) {
   const int lane = threadIdx.x;
@@ -145,29 +117,6 @@ __device__ void fold_range(const P2PView& v, float* __restrict__ out, uint64_t b
       } else {
         for (int k = 0; k < 4; ++k) out[i + k] = fold1(v, (uint32_t)((i + k) / v.C), i + k);
       }
-    }
-  }
-}
-
-// Fused signalling (saves a launch per signal): the ENTRY flag is published
-// by block 0 before anyone waits -- the producer kernel ran earlier on this
-// stream, so its stores are complete; the EXIT flag is published by the last
-// CTA to finish (thread-fence reduction pattern), after every CTA's stores.
-__device__ void publish(const P2PView& v, int kind, uint64_t value) {
-  __threadfence_system();
-  for (int r = 0; r < v.n; ++r) st_release_sys(v.flags[r] + kind * kP2PMaxRanks + v.rank, value);
-}
-__device__ void entry_signal(const P2PView& v, const P2PSig& sg) {
-  if (sg.entry_kind >= 0 && blockIdx.x == 0 && threadIdx.x == 0) publish(v, sg.entry_kind, sg.entry_val);
-}
-__device__ void exit_signal(const P2PView& v, const P2PSig& sg) {
-  if (sg.exit_kind < 0) return;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    if (atomicAdd(sg.counter, 1u) == gridDim.x - 1) {
-      *sg.counter = 0;  // every other CTA has arrived: reset for the next launch
-      publish(v, sg.exit_kind, sg.exit_val);
     }
   }
 }

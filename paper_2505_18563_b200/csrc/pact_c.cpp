@@ -1631,14 +1631,11 @@ pact_status pact_masked_allreduce(pact_comm* c, pact_ctx* ctx, const float* grad
 
   int agree = 0;
   bool packed_issued = false, packed_in_sym = false;
-  if (c && c->shm) {  // host vote board: microseconds, no GPU work, no stream sync
-    std::vector<uint8_t> frames;
-    TRY(shm_vote(c, frame, frames));
-    TRY(pact_vote_decide(frames.data(), n, &mine, stable, &agree));  // collective.cpp:285-293
-  } else if (c) {
-    // speculative pack overlaps the vote round trip (single-bucket plans);
-    // enqueued first so the GPU starts while the host posts the vote
-    if (stable && !buckets && m->nnz) {
+  if (c) {
+    // speculative pack overlaps the vote (single-bucket plans): enqueued
+    // first so the GPU starts while the host votes; unused on a fallback
+    const bool p2p_buckets = p2p_try && pol.bucket_bytes > 0 && m->nnz * 4 > pol.bucket_bytes;
+    if (stable && !buckets && !p2p_buckets && !f16 && m->nnz) {
       if (p2p_ready) {  // straight into this rank's symmetric buffer
         const uint64_t k1 = c->p2p.k + 1;
         if (k1 > 2)  // peers finished reading this region (step k1-2)
@@ -1653,9 +1650,13 @@ pact_status pact_masked_allreduce(pact_comm* c, pact_ctx* ctx, const float* grad
       }
       mark(0);
     }
-    TRY(post_vote(c, frame, ctx->aux[0]));
     std::vector<uint8_t> frames;
-    TRY(wait_vote(c, frames));
+    if (c->shm) {  // host vote board: microseconds, no GPU work, no stream sync
+      TRY(shm_vote(c, frame, frames));
+    } else {
+      TRY(post_vote(c, frame, ctx->aux[0]));
+      TRY(wait_vote(c, frames));
+    }
     TRY(pact_vote_decide(frames.data(), n, &mine, stable, &agree));  // collective.cpp:285-293
   } else {
     agree = stable;  // the one-rank vote: only this rank's frame
@@ -1711,12 +1712,27 @@ pact_status pact_masked_allreduce(pact_comm* c, pact_ctx* ctx, const float* grad
       sg.entry_kind = pactk::kP2PPacked;
       sg.entry_val = fval(0);
       sg.counter = p2p_counter(p, c->rank);
+      // opt-in (PACT_P2P_FUSED=1): the exchange's consumer side fused into
+      // unpack (peer loads straight into the unpack's staging; one-shot sums
+      // local + peer runs, two-shot reads runs from the owners' reduced
+      // chunks, needs C >= 1024). Bit-identical, but measured slower on c2:
+      // n=2 127 vs 110 us, n=4 190 vs 154 us -- the unpack's per-warp run
+      // pipeline cannot keep enough NVLink reads in flight, while the separate
+      // fold streams float4 pulls at ~530 GB/s.
+      static const bool fuse_env = getenv("PACT_P2P_FUSED") != nullptr;
+      const uint64_t Cb = std::max<uint64_t>(1, (m->nnz + n - 1) / n);
+      const bool fuse = fuse_env && (!two || Cb >= PACT_TILE);
       if (!two) {
         sg.exit_kind = pactk::kP2PRead;  // peers' buffers no longer read
         sg.exit_val = k1;
-        pactk::launch_p2p_fold(v, packed, 0, m->nnz, myflags, fval(0), err, 0, sg, s);
+        if (fuse) {
+          mark(1);
+          pactk::launch_unpack_p2p(mine, len, m->words, m->tile_off, scale, scale != 1.0f, out, v, 0, myflags,
+                                   fval(0), err, sg, s);
+        } else {
+          pactk::launch_p2p_fold(v, packed, 0, m->nnz, myflags, fval(0), err, 0, sg, s);
+        }
       } else {
-        const uint64_t Cb = std::max<uint64_t>(1, (m->nnz + n - 1) / n);
         const uint64_t rb = std::min<uint64_t>(m->nnz, (uint64_t)c->rank * Cb);
         const uint64_t re = std::min<uint64_t>(m->nnz, rb + Cb);
         sg.exit_kind = pactk::kP2PReduced;
@@ -1726,11 +1742,19 @@ pact_status pact_masked_allreduce(pact_comm* c, pact_ctx* ctx, const float* grad
         sg2.exit_kind = pactk::kP2PRead;
         sg2.exit_val = k1;
         sg2.counter = sg.counter;
-        pactk::launch_p2p_gather(v, packed, 0, m->nnz, 0, Cb, myflags, fval(0), err, 0, sg2, s);
+        if (fuse) {
+          mark(1);
+          pactk::launch_unpack_p2p(mine, len, m->words, m->tile_off, scale, scale != 1.0f, out, v, 1, myflags,
+                                   fval(0), err, sg2, s);
+        } else {
+          pactk::launch_p2p_gather(v, packed, 0, m->nnz, 0, Cb, myflags, fval(0), err, 0, sg2, s);
+        }
       }
-      mark(1);
-      pactk::launch_unpack(packed, len, m->words, m->tile_off, scale, scale != 1.0f, out, 0,
-                           m->ntiles, s);
+      if (!fuse) {
+        mark(1);
+        pactk::launch_unpack(packed, len, m->words, m->tile_off, scale, scale != 1.0f, out, 0,
+                             m->ntiles, s);
+      }
       mark(2);
       p.k = k1;
       nbuckets = 1;

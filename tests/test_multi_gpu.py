@@ -99,6 +99,10 @@ def test_nccl_masked_allreduce_multi_gpu(pb):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr=127.0.0.1", f"--master-port={_free_port()}",
            os.path.join(ROOT, "tests", "mp_masked_worker.py")]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
-    print(r.stdout[-4000:], r.stderr[-4000:])
-    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    # default exchange, then the opt-in unpack-fused P2P consumer (PACT_P2P_FUSED)
+    for extra in ({}, {"PACT_P2P_FUSED": "1"}):
+        env = dict(os.environ, **extra)
+        cmd[6] = f"--master-port={_free_port()}"
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
+        print(r.stdout[-4000:], r.stderr[-4000:])
+        assert r.returncode == 0, str(extra) + r.stdout[-2000:] + r.stderr[-2000:]

@@ -119,5 +119,52 @@ int main() {
     printf("%3zu MB: fold %7.1f us (%6.1f GB/s remote), remote read %7.1f us (%6.1f GB/s)\n", mb, best * 1e3,
            (mb << 20) / (best * 1e-3) / 1e9, best_r * 1e3, (mb << 20) / (best_r * 1e-3) / 1e9);
   }
+  // both GPUs fold at once (each reads the other: the one-shot exchange)
+  {
+    float *b1, *o1;
+    CK(cudaSetDevice(1));
+    CK(cudaDeviceEnablePeerAccess(0, 0));
+    CK(cudaMalloc(&b1, bytes + 64));
+    CK(cudaMalloc(&o1, bytes + 64));
+    cudaStream_t s0, s1;
+    cudaEvent_t f0, f1, g0, g1;
+    cudaStreamCreate(&s1);
+    cudaEventCreate(&f1);
+    cudaEventCreate(&g1);
+    CK(cudaSetDevice(0));
+    cudaStreamCreate(&s0);
+    cudaEventCreate(&f0);
+    cudaEventCreate(&g0);
+    for (size_t mb : {4, 20, 64}) {
+      const size_t nn = (mb << 20) / 16;
+      float best0 = 1e9, best1 = 1e9;
+      for (int it = 0; it < 10; ++it) {
+        CK(cudaSetDevice(0));
+        cudaDeviceSynchronize();
+        CK(cudaSetDevice(1));
+        cudaDeviceSynchronize();
+        CK(cudaSetDevice(0));
+        cudaEventRecord(f0, s0);
+        fold2<<<grid, blk, 0, s0>>>((float4*)a0, (float4*)b1, (float4*)b0, nn);
+        cudaEventRecord(g0, s0);
+        CK(cudaSetDevice(1));
+        cudaEventRecord(f1, s1);
+        fold2<<<grid, blk, 0, s1>>>((float4*)b1, (float4*)a0, (float4*)o1, nn);
+        cudaEventRecord(g1, s1);
+        cudaEventSynchronize(g1);
+        CK(cudaSetDevice(0));
+        cudaEventSynchronize(g0);
+        float m0, m1;
+        cudaEventElapsedTime(&m0, f0, g0);
+        CK(cudaSetDevice(1));
+        cudaEventElapsedTime(&m1, f1, g1);
+        CK(cudaSetDevice(0));
+        best0 = m0 < best0 ? m0 : best0;
+        best1 = m1 < best1 ? m1 : best1;
+      }
+      printf("%3zu MB: bidirectional fold GPU0 %7.1f us, GPU1 %7.1f us (%6.1f GB/s remote each)\n", mb,
+             best0 * 1e3, best1 * 1e3, (mb << 20) / (best0 * 1e-3) / 1e9);
+    }
+  }
   return 0;
 }
