@@ -357,12 +357,12 @@ def main():
     if t_pack >= t_unpack:
         dom, alg, tdom = "pack_kernel", alg_pack, t_pack
     else:
-        dom, alg, tdom = "unpack_kernel<0>", alg_unpack, t_unpack
+        dom, alg, tdom = "unpack_kernel<0, 0>", alg_unpack, t_unpack
     peak, peak_kind = peaks()
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
-        try:
+        try:  # ncu's per-launch DRAM bytes of this kernel on this workload (tools/ncu_summary.py)
             traffic = json.load(open(tp)).get(f"{cfg}:{dom}")
         except Exception:
             traffic = None

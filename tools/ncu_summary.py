@@ -24,7 +24,7 @@ def short(name: str) -> str:
     n = name.split("(")[0]
     for junk in ("pactk::", "<unnamed>::", "unnamed>::", "(anonymous namespace)::"):
         n = n.replace(junk, "")
-    n = n.replace("void ", "")
+    n = n.replace("void ", "").replace("(bool)", "").replace("(int)", "")
     return n.strip()
 
 
