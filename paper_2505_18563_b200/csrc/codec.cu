@@ -309,27 +309,59 @@ __global__ void __launch_bounds__(kPuWarps * 32)
     const uint64_t* wc = wsm[warp][wi];
     const uint32_t rb = reinterpret_cast<const uint32_t*>(wsm[warp][wi] + kChunkWords)[0];
     const float* stage = psm(warp, pi) + run_phase(run_src<kSrc>(packed, v, rb, 0));
+    // (1) lane-major expansion: lane l owns the 32 elements of mask half-word
+    // l, whose kept values are consecutive in the staged run from its warp
+    // rank -- one scan per chunk instead of a rank per float4 slot
+    const uint32_t h = reinterpret_cast<const uint32_t*>(wc)[lane];
+    const uint32_t hc = __popc(h);
+    const uint32_t pos0 = warp_incl_scan(hc) - hc;
+    // 32-bit shared addresses walked by predicated increments: per element a
+    // bit test, a predicated LDS and a predicated add
+    float x[32];
+#pragma unroll
+    for (int e = 0; e < 32; ++e) x[e] = 0.0f;
+    if constexpr (kSrc != kSrcPair) {
+      uint32_t sa = (uint32_t)__cvta_generic_to_shared(stage + pos0);
+#pragma unroll
+      for (int e = 0; e < 32; ++e)
+        asm volatile(
+            "{\n .reg .pred p;\n setp.ne.u32 p, %2, 0;\n @p ld.shared.f32 %0, [%1];\n"
+            " @p add.u32 %1, %1, 4;\n}"
+            : "+f"(x[e]), "+r"(sa)
+            : "r"(h & (1u << e)));
+    } else {  // + the peer's value (one-shot fold, n = 2)
+      const float* sa = stage + pos0;
+      const float* sp = psm(warp, pi) + kRunCap + run_phase(run_src<kSrc>(packed, v, rb, 1)) + pos0;
+#pragma unroll
+      for (int e = 0; e < 32; ++e)
+        if (h & (1u << e)) x[e] = __fadd_rn(*sa++, *sp++);
+    }
+    // (2) transpose through the consumed run buffer (XOR-swizzled 16-byte
+    // cells: conflict-free both ways) into the coalesced layout: store j of
+    // lane l covers elements 128 j + 4 l .. + 3
+    __syncwarp();
+    float4* T = reinterpret_cast<float4*>(psm(warp, pi));
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      T[lane * 8 + (k ^ (lane & 7))] = make_float4(x[4 * k], x[4 * k + 1], x[4 * k + 2], x[4 * k + 3]);
+    __syncwarp();
     const uint64_t e0 = c * (uint64_t)kChunk + 4 * lane;
-    uint32_t run = 0;
+    // cell of store j: row 4j + l/8, column (l & 7) ^ (row & 7) -- the XOR
+    // term depends on j's parity only, so two per-lane bases + immediates
+    const int tb0 = (lane >> 3) * 8 + ((lane & 7) ^ (lane >> 3));
+    const int tb1 = (lane >> 3) * 8 + ((lane & 7) ^ ((lane >> 3) + 4));
+    if (!kSgd && !do_scale && vec_ok && (c + 1) * (uint64_t)kChunk <= len) {  // whole chunk: 8 x (LDS.128, STG.128)
+#pragma unroll
+      for (int j = 0; j < kVecPerLane; ++j)
+        st_stream_f4(reinterpret_cast<float4*>(out + e0 + 128 * j), T[32 * j + ((j & 1) ? tb1 : tb0)]);
+    } else
 #pragma unroll
     for (int j = 0; j < kVecPerLane; ++j) {
-      const Slot s = chunk_slot(wc, j, run);
       const uint64_t ge = e0 + 128 * j;
       if (ge >= len) continue;
-      const uint32_t nib = s.nib;
-      const uint32_t b0 = nib & 1, b1 = (nib >> 1) & 1, b2 = (nib >> 2) & 1;
-      float o[4];
-      o[0] = b0 ? stage[s.pos] : 0.0f;
-      o[1] = b1 ? stage[s.pos + b0] : 0.0f;
-      o[2] = b2 ? stage[s.pos + b0 + b1] : 0.0f;
-      o[3] = (nib & 8) ? stage[s.pos + b0 + b1 + b2] : 0.0f;
-      if constexpr (kSrc == kSrcPair) {  // + the peer's value (one-shot fold, n = 2)
-        const float* peer = psm(warp, pi) + kRunCap + run_phase(run_src<kSrc>(packed, v, rb, 1));
-        if (b0) o[0] = __fadd_rn(o[0], peer[s.pos]);
-        if (b1) o[1] = __fadd_rn(o[1], peer[s.pos + b0]);
-        if (b2) o[2] = __fadd_rn(o[2], peer[s.pos + b0 + b1]);
-        if (nib & 8) o[3] = __fadd_rn(o[3], peer[s.pos + b0 + b1 + b2]);
-      }
+      const float4 t = T[32 * j + ((j & 1) ? tb1 : tb0)];
+      float o[4] = {t.x, t.y, t.z, t.w};
+      const uint32_t nib = (uint32_t)(wc[2 * j + (lane >> 4)] >> (4 * (lane & 15))) & 0xFu;
       if (do_scale) {
 #pragma unroll
         for (int b = 0; b < 4; ++b)
