@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <algorithm>
 #include <cstring>
 #include <memory>
 #include <optional>
@@ -249,6 +250,92 @@ inline FlatTensor unpack(const PackedGradient& p, const SparsityMask& mask) {  /
   return FlatTensor(std::move(out));
 }
 
+// codec.cpp:40-75: ternary payload (host copy of the device result)
+struct TernaryGradient {  // codec.hpp:32-40
+  float scale = 0.0f;
+  size_t len = 0;
+  std::vector<uint8_t> sign_words;  // 4 elements per byte, little-endian pairs
+  int sign_at(size_t i) const {
+    const uint8_t pair = (sign_words[i >> 2] >> (2 * (i & 3))) & 0x3;
+    if (pair == 3) throw Error(Errc::CorruptPayload, "reserved ternary sign pattern 11");
+    return pair == 1 ? 1 : (pair == 2 ? -1 : 0);
+  }
+};
+
+// codec.cpp:50-68; draws from a counter-based SplitMix64 stream of `seed`
+// (pact_c.h: the reference's sequential mt19937_64 stream is replaced)
+inline TernaryGradient ternarize(const FlatTensor& grad, uint64_t seed) {
+  const size_t n = grad.size();
+  auto dg = detail::dev_alloc<float>(n);
+  auto ds = detail::dev_alloc<uint8_t>(pact_ternary_sign_bytes(n));
+  auto dsc = detail::dev_alloc<float>(1);
+  detail::cuda(cudaMemcpy(dg.get(), grad.data(), n * 4, cudaMemcpyHostToDevice));
+  detail::check(pact_ternarize(detail::ctx(), dg.get(), n, seed, dsc.get(), ds.get(), nullptr));
+  TernaryGradient t;
+  t.len = n;
+  t.sign_words.resize((n + 3) / 4);
+  detail::cuda(cudaMemcpy(&t.scale, dsc.get(), 4, cudaMemcpyDeviceToHost));
+  detail::cuda(cudaMemcpy(t.sign_words.data(), ds.get(), t.sign_words.size(), cudaMemcpyDeviceToHost));
+  return t;
+}
+
+inline FlatTensor deternarize(const TernaryGradient& t) {  // codec.cpp:70-75
+  const size_t sb = pact_ternary_sign_bytes(t.len);
+  std::vector<uint8_t> padded(sb ? sb : 1, 0);
+  std::memcpy(padded.data(), t.sign_words.data(), std::min(t.sign_words.size(), padded.size()));
+  auto ds = detail::dev_alloc<uint8_t>(padded.size());
+  auto dsc = detail::dev_alloc<float>(1);
+  auto dout = detail::dev_alloc<float>(t.len);
+  detail::cuda(cudaMemcpy(ds.get(), padded.data(), padded.size(), cudaMemcpyHostToDevice));
+  detail::cuda(cudaMemcpy(dsc.get(), &t.scale, 4, cudaMemcpyHostToDevice));
+  detail::check(pact_deternarize(detail::ctx(), dsc.get(), ds.get(), t.len, dout.get(), nullptr));
+  std::vector<float> out(t.len);
+  detail::cuda(cudaMemcpy(out.data(), dout.get(), t.len * 4, cudaMemcpyDeviceToHost));
+  return FlatTensor(std::move(out));
+}
+
+inline FlatTensor fp16_roundtrip(const FlatTensor& grad) {  // codec.cpp:142-146
+  auto d = detail::dev_alloc<float>(grad.size());
+  detail::cuda(cudaMemcpy(d.get(), grad.data(), grad.size() * 4, cudaMemcpyHostToDevice));
+  detail::check(pact_fp16_roundtrip(detail::ctx(), d.get(), d.get(), grad.size(), nullptr));
+  std::vector<float> out(grad.size());
+  detail::cuda(cudaMemcpy(out.data(), d.get(), out.size() * 4, cudaMemcpyDeviceToHost));
+  return FlatTensor(std::move(out));
+}
+
+struct TopKPayload {  // codec.hpp:60-66
+  std::vector<uint32_t> indices;
+  std::vector<float> values;
+  size_t original_len = 0;
+};
+
+inline TopKPayload topk_select(const FlatTensor& grad, float rate) {  // codec.cpp:147-172
+  uint64_t k = 0;
+  detail::check(pact_topk_count(grad.size(), rate, &k));
+  auto dg = detail::dev_alloc<float>(grad.size());
+  auto di = detail::dev_alloc<uint32_t>(k);
+  auto dv = detail::dev_alloc<float>(k);
+  detail::cuda(cudaMemcpy(dg.get(), grad.data(), grad.size() * 4, cudaMemcpyHostToDevice));
+  detail::check(pact_topk_select(detail::ctx(), dg.get(), grad.size(), rate, di.get(), dv.get(), &k, nullptr));
+  TopKPayload p{std::vector<uint32_t>(k), std::vector<float>(k), grad.size()};
+  detail::cuda(cudaMemcpy(p.indices.data(), di.get(), k * 4, cudaMemcpyDeviceToHost));
+  detail::cuda(cudaMemcpy(p.values.data(), dv.get(), k * 4, cudaMemcpyDeviceToHost));
+  return p;
+}
+
+inline FlatTensor topk_densify(const TopKPayload& p) {  // codec.cpp:174-182
+  const size_t k = p.indices.size();
+  auto di = detail::dev_alloc<uint32_t>(k);
+  auto dv = detail::dev_alloc<float>(k);
+  auto dout = detail::dev_alloc<float>(p.original_len);
+  detail::cuda(cudaMemcpy(di.get(), p.indices.data(), k * 4, cudaMemcpyHostToDevice));
+  detail::cuda(cudaMemcpy(dv.get(), p.values.data(), k * 4, cudaMemcpyHostToDevice));
+  detail::check(pact_topk_densify(detail::ctx(), di.get(), dv.get(), k, p.original_len, dout.get(), nullptr));
+  std::vector<float> out(p.original_len);
+  detail::cuda(cudaMemcpy(out.data(), dout.get(), out.size() * 4, cudaMemcpyDeviceToHost));
+  return FlatTensor(std::move(out));
+}
+
 namespace wire {  // codec.hpp:80-103
 enum class PayloadKind : uint8_t { Full = 0, Packed = 1, Ternary = 2, Fp16 = 3, TopK = 4 };
 inline constexpr size_t kHeaderSize = PACT_HEADER_BYTES;
@@ -340,6 +427,49 @@ inline AggregateResult full_allreduce(const FlatTensor& grad, Comm& comm) {
   std::vector<float> out(grad.size());
   detail::cuda(cudaMemcpy(out.data(), d.get(), out.size() * 4, cudaMemcpyDeviceToHost));
   return {FlatTensor(std::move(out)), {st.bytes_on_wire, st.seconds, SyncMode::FullAllReduce}};
+}
+
+namespace detail {
+// host-buffer aggregate call: H2D grad, device path, D2H result
+template <typename F>
+AggregateResult host_aggregate(const FlatTensor& grad, F&& call) {
+  auto d = dev_alloc<float>(grad.size());
+  auto o = dev_alloc<float>(grad.size());
+  cuda(cudaMemcpy(d.get(), grad.data(), grad.size() * 4, cudaMemcpyHostToDevice));
+  pact_sync_stats st{};
+  call(d.get(), o.get(), &st);
+  std::vector<float> out(grad.size());
+  cuda(cudaMemcpy(out.data(), o.get(), out.size() * 4, cudaMemcpyDeviceToHost));
+  return {FlatTensor(std::move(out)), {st.bytes_on_wire, st.seconds, static_cast<SyncMode>(st.mode_used)}};
+}
+}  // namespace detail
+
+// collective.cpp:311-368; returns the MEAN
+inline AggregateResult ternary_allgather_aggregate(const FlatTensor& grad, const SparsityMask& mask,
+                                                   TrackerStatus tracker, uint64_t seed, uint32_t epoch,
+                                                   Comm& comm) {
+  if (grad.size() != mask.size()) throw Error(Errc::ShapeMismatch, "gradient/mask length mismatch");
+  return detail::host_aggregate(grad, [&](float* d, float* o, pact_sync_stats* st) {
+    detail::check(pact_ternary_allgather_aggregate(comm.handle(), detail::ctx(), d, grad.size(), mask.handle(),
+                                                   tracker == TrackerStatus::Stable, seed, epoch, o, st,
+                                                   nullptr));
+  });
+}
+
+// collective.cpp:370-390; returns the MEAN
+inline AggregateResult topk_allgather_aggregate(const FlatTensor& grad, float rate, uint32_t epoch,
+                                                Comm& comm) {
+  return detail::host_aggregate(grad, [&](float* d, float* o, pact_sync_stats* st) {
+    detail::check(pact_topk_allgather_aggregate(comm.handle(), detail::ctx(), d, grad.size(), rate, epoch, o,
+                                                st, nullptr));
+  });
+}
+
+// collective.cpp:261-267 (binary16 ring, F16Wire); returns the SUM
+inline AggregateResult fp16_allreduce(const FlatTensor& grad, Comm& comm) {
+  return detail::host_aggregate(grad, [&](float* d, float* o, pact_sync_stats* st) {
+    detail::check(pact_fp16_allreduce(comm.handle(), detail::ctx(), d, o, grad.size(), st, nullptr));
+  });
 }
 
 }  // namespace pact

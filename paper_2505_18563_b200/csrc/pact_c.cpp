@@ -1623,8 +1623,15 @@ pact_status pact_masked_allreduce(pact_comm* c, pact_ctx* ctx, const float* grad
   float* packed = ctx->packed.as<float>();
 
   const bool f16 = pol.wire == PACT_WIRE_F16;  // binary16 ring on the packed values (8f-3)
+  // AUTO picks the measured-faster exchange (B200 x2/x4, bench.py c2/c3/c5):
+  // NVLink P2P for n = 2 up to 64 MiB packed (c2 108 vs 118 us, c3 266 vs 312
+  // us) and for n <= 4 up to 24 MiB (c2 n=4 153 vs 160 us); NCCL above (c5
+  // n=2 1.03 vs 1.10 ms, n=4 1.12 vs 1.33 ms; c3 n=4 351 vs 363 us) and for
+  // n > 4. PACT_TRANSPORT_P2P forces the bit-exact reference-order fold.
+  const uint64_t pbytes = m->nnz * 4;
+  const bool auto_p2p = c && (n == 2 ? pbytes <= (64ull << 20) : (n <= 4 && pbytes <= (24ull << 20)));
   const bool p2p_try = c && m->nnz && n <= pactk::kP2PMaxRanks && !f16 &&
-                       (pol.transport == PACT_TRANSPORT_P2P || pol.transport == PACT_TRANSPORT_AUTO);
+                       (pol.transport == PACT_TRANSPORT_P2P || (pol.transport == PACT_TRANSPORT_AUTO && auto_p2p));
   const bool p2p_ready = p2p_try && c->p2p.ok && c->p2p.cap >= m->nnz;
   const bool buckets = c && !p2p_try && !f16 && pol.bucket_bytes > 0 && m->nnz * 4 > pol.bucket_bytes;
   if (buckets) TRY(mirror_tile_off(m, s));

@@ -143,6 +143,45 @@ int main() {
   CHECK(decide_sync_mode(SyncMode::Fp16AllReduce, TrackerStatus::Unstable) == SyncMode::Fp16AllReduce);
   CHECK(code_of([] { Comm c(0, 1, Comm::unique_id()); }) == Errc::BadTopology);  // n >= 2
 
+  // test_codec.cpp:96-136: ternarize / deternarize
+  {
+    TernaryGradient t = ternarize(FlatTensor({1.0f, -1.0f}), 123);
+    CHECK(t.scale == 1.0f && t.sign_at(0) == 1 && t.sign_at(1) == -1);
+    TernaryGradient z = ternarize(FlatTensor::zeros(9), 5);
+    CHECK(z.scale == 0.0f);
+    for (size_t i = 0; i < 9; ++i) CHECK(z.sign_at(i) == 0);
+    std::mt19937_64 rng(13);
+    std::normal_distribution<float> nd;
+    std::vector<float> g(97);
+    for (auto& x : g) x = nd(rng);
+    TernaryGradient r = ternarize(FlatTensor(g), 31337);
+    FlatTensor dec = deternarize(r);
+    for (size_t i = 0; i < dec.size(); ++i) CHECK(dec[i] == r.scale || dec[i] == -r.scale || dec[i] == 0.0f);
+    TernaryGradient bad;
+    bad.scale = 1.0f;
+    bad.len = 1;
+    bad.sign_words = {0x3};
+    CHECK(code_of([&] { bad.sign_at(0); }) == Errc::CorruptPayload);
+    CHECK(code_of([&] { deternarize(bad); }) == Errc::CorruptPayload);
+  }
+  // codec.cpp:77-146: binary16 clamping and round trip
+  {
+    FlatTensor h = fp16_roundtrip(FlatTensor({1.0f, 65520.0f, -1e30f, 0.1f, 5.96e-8f}));
+    CHECK(h[0] == 1.0f && h[1] == 65504.0f && h[2] == -65504.0f);
+    CHECK(h[3] == 0.0999755859375f && h[4] == 5.9604644775390625e-8f);
+  }
+  // test_codec.cpp: topk: ties -> lower index, ascending
+  {
+    TopKPayload p = topk_select(FlatTensor({0.5f, -2.0f, 0.5f, 2.0f, 0.5f}), 0.6f);
+    CHECK((p.indices == std::vector<uint32_t>{0, 1, 3}));
+    CHECK((p.values == std::vector<float>{0.5f, -2.0f, 2.0f}));
+    FlatTensor d = topk_densify(p);
+    CHECK(d == FlatTensor({0.5f, -2.0f, 0.0f, 2.0f, 0.0f}));
+    CHECK(code_of([] { topk_select(FlatTensor({1.0f}), 0.0f); }) == Errc::InvalidRate);
+    TopKPayload oob{{7}, {1.0f}, 3};
+    CHECK(code_of([&] { topk_densify(oob); }) == Errc::CorruptPayload);
+  }
+
   std::printf("dropin_test: %d failure(s)\n", g_fail);
   return g_fail;
 }
