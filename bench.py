@@ -36,12 +36,12 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 CONFIGS = {
-    # name: (model shape, prune ratio, re-prune per step, bucket bytes)
+    # name: (model shape, prune ratio, re-prune per step, bucket bytes; 0 = the library's auto)
     "c1": ("resnet18", 0.9, False, 0),
     "c2": ("resnet50", 0.8, False, 0),
-    "c3": ("vgg19", 0.95, False, 16 << 20),
+    "c3": ("vgg19", 0.95, False, 0),
     "c4": ("bert-base", 0.5, False, 0),
-    "c5": ("gpt2-medium", 0.9, True, 32 << 20),
+    "c5": ("gpt2-medium", 0.9, True, 0),
 }
 L2_FLUSH_BYTES = 512 << 20
 

@@ -114,14 +114,15 @@ typedef struct pact_sync_stats {
  * never fall back on density, one bucket. */
 typedef struct pact_policy {
   double density_threshold; /* fall back to dense when agreed nnz/len > this; <=0 or >=1: never */
-  uint64_t bucket_bytes;    /* packed bytes per bucket; 0 = single bucket */
+  uint64_t bucket_bytes;    /* packed bytes per bucket; 0 = auto (NCCL: one bucket up to
+                               64 MiB packed, 32 MiB buckets above; P2P: one bucket) */
   float scale;              /* applied in unpack; 0 => 1.0 (SUM, as the reference returns) */
   int time_stages;          /* record CUDA events around the stages */
   int transport;            /* packed exchange: 0 auto (the measured-faster one: P2P for
-                               n = 2 up to 64 MiB packed and n <= 4 up to 24 MiB, else
-                               NCCL), 1 NCCL allreduce, 2 NVLink P2P (peer-memory reduce
-                               in the reference fold order; bit-identical to the
-                               reference ring) */
+                               n = 2 up to 64 MiB packed, else NCCL), 1 NCCL allreduce
+                               (single bucket on an NCCL symmetric-memory window),
+                               2 NVLink P2P (peer-memory reduce in the reference fold
+                               order; bit-identical to the reference ring) */
   int wire;                 /* packed exchange payload: PACT_WIRE_F32 (0, the reference's
                                masked_allreduce) or PACT_WIRE_F16 (binary16 ring with
                                per-hop re-rounding, F16Wire collective.cpp:133-163, on the

@@ -600,7 +600,7 @@ class SyncPolicy:
     AUTO, NCCL, P2P = 0, 1, 2
 
     density_threshold: float = 0.0   # fall back to dense above this agreed density (0: never)
-    bucket_bytes: int = 0            # packed bytes per overlapped bucket (0: one bucket)
+    bucket_bytes: int = 0            # packed bytes per overlapped bucket (0: auto, see pact_c.h)
     scale: float = 1.0               # fused into unpack (1/n gives the mean)
     time_stages: bool = False
     transport: int = 0               # 0 auto, 1 NCCL allreduce, 2 NVLink P2P (bit-exact fold order)

@@ -193,6 +193,13 @@ struct pact_comm {
   size_t shm_bytes = 0;
   uint64_t shm_seq = 0;
   std::string shm_name;
+  // NCCL symmetric-memory window for the packed buffer of the NCCL exchange
+  // (ncclMemAlloc + ncclCommWindowRegister(NCCL_WIN_COLL_SYMMETRIC): NCCL's
+  // low-latency symmetric allreduce kernels over NVLink)
+  void* sym = nullptr;
+  size_t sym_bytes = 0;
+  ncclWindow_t win = nullptr;
+  bool sym_failed = false;
 };
 
 namespace {
@@ -1250,6 +1257,8 @@ pact_status pact_comm_destroy(pact_comm* c) {
   cudaDeviceSynchronize();
   p2p_release(c);
   c->p2p.err.release();
+  if (c->win) ncclCommWindowDeregister(c->nccl, c->win);
+  if (c->sym) ncclMemFree(c->sym);
   if (c->nccl) ncclCommDestroy(c->nccl);
   c->vote_dev.release();
   c->vote_pin.release();
@@ -1513,6 +1522,36 @@ pact_status pact_topk_allgather_aggregate(pact_comm* c, pact_ctx* ctx, const flo
   return PACT_OK;
 }
 
+namespace {
+// Collective (every rank, same bytes: the vote agreed on nnz). Returns the
+// symmetric packed buffer or nullptr (disabled / unsupported -> ctx->packed).
+pact_status nccl_sym_packed(pact_comm* c, uint64_t bytes, cudaStream_t s, float** out) {
+  static const bool enabled = !getenv("PACT_NO_NCCL_SYMMETRIC");
+  *out = nullptr;
+  if (!enabled || c->sym_failed || !bytes) return PACT_OK;
+  if (c->sym_bytes < bytes) {
+    CUDA_TRY(cudaStreamSynchronize(s));
+    if (c->win) ncclCommWindowDeregister(c->nccl, c->win);
+    if (c->sym) ncclMemFree(c->sym);
+    c->win = nullptr;
+    c->sym = nullptr;
+    c->sym_bytes = 0;
+    const size_t want = ((bytes + bytes / 4 + (4u << 20)) >> 20) << 20;
+    if (ncclMemAlloc(&c->sym, want) != ncclSuccess ||
+        ncclCommWindowRegister(c->nccl, c->sym, want, &c->win, NCCL_WIN_COLL_SYMMETRIC) != ncclSuccess) {
+      if (c->sym) ncclMemFree(c->sym);
+      c->sym = nullptr;
+      c->win = nullptr;
+      c->sym_failed = true;  // NCCL reports the failure on every rank alike
+      return PACT_OK;
+    }
+    c->sym_bytes = want;
+  }
+  *out = static_cast<float*>(c->sym);
+  return PACT_OK;
+}
+}  // namespace
+
 // ------------------------------------------------------- binary16 ring
 namespace {
 // ring_allreduce_impl<F16Wire> (collective.cpp:165-216 with 133-163): n-1
@@ -1625,15 +1664,19 @@ pact_status pact_masked_allreduce(pact_comm* c, pact_ctx* ctx, const float* grad
   const bool f16 = pol.wire == PACT_WIRE_F16;  // binary16 ring on the packed values (8f-3)
   // AUTO picks the measured-faster exchange (B200 x2/x4, bench.py c2/c3/c5):
   // NVLink P2P for n = 2 up to 64 MiB packed (c2 108 vs 118 us, c3 266 vs 312
-  // us) and for n <= 4 up to 24 MiB (c2 n=4 153 vs 160 us); NCCL above (c5
-  // n=2 1.03 vs 1.10 ms, n=4 1.12 vs 1.33 ms; c3 n=4 351 vs 363 us) and for
-  // n > 4. PACT_TRANSPORT_P2P forces the bit-exact reference-order fold.
+  // us); NCCL otherwise -- on a symmetric window for one bucket (c2 n=4 115
+  // vs P2P 148 us), bucketed above (c5 n=2 1.03 vs 1.10 ms, n=4 1.12 vs
+  // 1.33 ms). PACT_TRANSPORT_P2P forces the bit-exact reference-order fold.
   const uint64_t pbytes = m->nnz * 4;
-  const bool auto_p2p = c && (n == 2 ? pbytes <= (64ull << 20) : (n <= 4 && pbytes <= (24ull << 20)));
+  const bool auto_p2p = c && n == 2 && pbytes <= (64ull << 20);
   const bool p2p_try = c && m->nnz && n <= pactk::kP2PMaxRanks && !f16 &&
                        (pol.transport == PACT_TRANSPORT_P2P || (pol.transport == PACT_TRANSPORT_AUTO && auto_p2p));
   const bool p2p_ready = p2p_try && c->p2p.ok && c->p2p.cap >= m->nnz;
-  const bool buckets = c && !p2p_try && !f16 && pol.bucket_bytes > 0 && m->nnz * 4 > pol.bucket_bytes;
+  // NCCL buckets: bucket_bytes, or auto (0): one bucket on the symmetric
+  // window up to 64 MiB packed (c3 n=4 277 vs 351 us bucketed), 32 MiB
+  // buckets above (c5 n=4 1.12 vs 1.22 ms single)
+  const uint64_t nccl_bb = pol.bucket_bytes ? pol.bucket_bytes : (pbytes > (64ull << 20) ? (32ull << 20) : 0);
+  const bool buckets = c && !p2p_try && !f16 && nccl_bb > 0 && m->nnz * 4 > nccl_bb;
   if (buckets) TRY(mirror_tile_off(m, s));
 
   int agree = 0;
@@ -1652,6 +1695,8 @@ pact_status pact_masked_allreduce(pact_comm* c, pact_ctx* ctx, const float* grad
                            0, m->ntiles, s);
         packed_in_sym = true;
       } else {
+        // the NCCL symmetric window once registered (an earlier agreed step)
+        if (!p2p_try && !buckets && c->sym && c->sym_bytes >= m->nnz * 4) packed = static_cast<float*>(c->sym);
         pactk::launch_pack(grad, len, m->words, m->tile_off, packed, 0, m->ntiles, s);
         packed_issued = true;
       }
@@ -1829,6 +1874,18 @@ pact_status pact_masked_allreduce(pact_comm* c, pact_ctx* ctx, const float* grad
     }
   p2p_done:;
   } else if (agree) {
+    // NCCL exchange, single bucket: pack into the symmetric window (collective
+    // setup). Measured (bench.py, NCCL transport): c2 n=4 115 vs 158 us, n=2
+    // 118 vs 117 us; the bucketed pipeline is faster on plain buffers (c5 n=4
+    // 1.12 vs 1.30 ms), so buckets keep ctx->packed.
+    if (c && !f16 && !buckets) {
+      float* symp = nullptr;
+      TRY(nccl_sym_packed(c, m->nnz * 4, s, &symp));
+      if (symp && symp != packed) {
+        packed = symp;
+        packed_issued = false;  // the speculative pack went to the plain buffer (first step)
+      }
+    }
     if (!buckets) {
       if (!packed_issued && m->nnz)
         pactk::launch_pack(grad, len, m->words, m->tile_off, packed, 0, m->ntiles, s);
@@ -1846,7 +1903,7 @@ pact_status pact_masked_allreduce(pact_comm* c, pact_ctx* ctx, const float* grad
       // tile-aligned buckets of ~bucket_bytes packed; pack on s, NCCL on
       // aux[0], unpack on aux[1], chained by events
       const std::vector<uint32_t>& off = m->host_tile_off;
-      const std::vector<uint64_t> cuts = bucket_cuts(off, m->ntiles, pol.bucket_bytes / 4, 256);
+      const std::vector<uint64_t> cuts = bucket_cuts(off, m->ntiles, nccl_bb / 4, 256);
       nbuckets = (int)cuts.size() - 1;
       cudaEvent_t start = pool_event(ctx, 0);
       CUDA_TRY(cudaEventRecord(start, s));
