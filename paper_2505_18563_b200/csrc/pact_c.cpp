@@ -2131,23 +2131,124 @@ pact_status pact_ternary_allgather_aggregate(pact_comm* c, pact_ctx* ctx, const 
   return PACT_OK;
 }
 
+// Host-buffer entry point, pipelined over gradient segments: H2D of segment
+// b+1 (caller's stream), pack -> NCCL allreduce of the segment's packed slice
+// -> unpack of segment b (aux[0]), and D2H of segment b-1 (aux[1]) overlap,
+// so the step costs about max(H2D, D2H) over PCIe instead of their sum. Same
+// vote, fallback rules and bytes_on_wire accounting as pact_masked_allreduce.
 pact_status pact_masked_allreduce_host(pact_comm* c, pact_ctx* ctx, const float* grad_host,
                                        uint64_t len, pact_mask* m, int tracker_stable,
                                        uint32_t epoch, const uint64_t* advertised,
                                        const pact_policy* policy, float* out_host,
                                        pact_sync_stats* stats, pact_stream_t stream) {
   if (!ctx || !m) return fail(PACT_E_INVALID_ARG, "null ctx/mask");
+  if (c && c->ctx != ctx) return fail(PACT_E_INVALID_ARG, "comm belongs to another ctx");
   if (len != m->len)
     return fail(PACT_E_SHAPE_MISMATCH, "gradient/mask length mismatch (%llu vs %llu)",
                 (unsigned long long)len, (unsigned long long)m->len);
+  if (len && (!grad_host || !out_host)) return fail(PACT_E_INVALID_ARG, "null host buffers");
   TRY(set_device(ctx));
+  TRY(ensure_ctx_ws(ctx));
+  pact_policy pol{};
+  if (policy) pol = *policy;
+  const float scale = pol.scale == 0.0f ? 1.0f : pol.scale;
+  const int n = c ? c->n : 1;
+  cudaStream_t s = stream;
+  CUDA_TRY(cudaEventRecord(ctx->t0, s));
+
+  // vote (collective.cpp:280-293) + density rule, as the device path
+  const int stable = pact_decide_sync_mode(PACT_SYNC_PACKED, tracker_stable) == PACT_SYNC_PACKED;
+  uint64_t digest = 0;
+  if (!advertised || stable) TRY(pact_mask_digest(m, s, &digest));
+  pact_frame_header mine{(uint8_t)(stable ? PACT_KIND_PACKED : PACT_KIND_FULL), epoch,
+                         advertised ? *advertised : digest, m->nnz};
+  int agree = stable;
+  if (c) {
+    uint8_t frame[PACT_HEADER_BYTES];
+    TRY(pact_header_encode(&mine, frame));
+    std::vector<uint8_t> frames;
+    if (c->shm) {
+      TRY(shm_vote(c, frame, frames));
+    } else {
+      TRY(post_vote(c, frame, ctx->aux[0]));
+      TRY(wait_vote(c, frames));
+    }
+    TRY(pact_vote_decide(frames.data(), n, &mine, stable, &agree));
+  }
+  int reason = agree ? 0 : (stable ? 2 : 1);
+  if (agree && pol.density_threshold > 0.0 && pol.density_threshold < 1.0 && len &&
+      (double)m->nnz / (double)len > pol.density_threshold) {
+    agree = 0;
+    reason = 3;
+  }
+
   TRY(ctx->grad_stage.ensure(std::max<uint64_t>(1, len) * 4));
+  TRY(ctx->out_stage.ensure(std::max<uint64_t>(1, len) * 4));
+  TRY(ctx->packed.ensure(std::max<uint64_t>(1, m->nnz) * 4));
   float* dg = ctx->grad_stage.as<float>();
-  if (len) CUDA_TRY(cudaMemcpyAsync(dg, grad_host, len * 4, cudaMemcpyHostToDevice, stream));
-  TRY(pact_masked_allreduce(c, ctx, dg, len, m, tracker_stable, epoch, advertised, policy, dg,
-                            stats, stream));
-  if (len) CUDA_TRY(cudaMemcpyAsync(out_host, dg, len * 4, cudaMemcpyDeviceToHost, stream));
-  CUDA_TRY(cudaStreamSynchronize(stream));
+  float* dout = ctx->out_stage.as<float>();
+  float* packed = ctx->packed.as<float>();
+  if (agree) TRY(mirror_tile_off(m, s));
+  // segments: whole chunks, ~8 MiB of gradient each, at most 64
+  const uint64_t nt = std::max<uint64_t>(1, m->ntiles);
+  const uint64_t per = std::max<uint64_t>((nt + 63) / 64, (8ull << 20) / 4 / PACT_TILE);
+  const int B = (int)((nt + per - 1) / per);
+  cudaStream_t xs = ctx->aux[0], ds = ctx->aux[1];
+  cudaEvent_t e0 = pool_event(ctx, 0);
+  CUDA_TRY(cudaEventRecord(e0, s));
+  CUDA_TRY(cudaStreamWaitEvent(xs, e0, 0));
+  CUDA_TRY(cudaStreamWaitEvent(ds, e0, 0));
+  for (int b = 0; b < B && len; ++b) {
+    const uint64_t tb = (uint64_t)b * per, te = std::min<uint64_t>(nt, tb + per);
+    const uint64_t eb = tb * PACT_TILE, ee = std::min<uint64_t>(len, te * PACT_TILE);
+    if (eb >= ee) continue;
+    cudaEvent_t eh = pool_event(ctx, 1 + 2 * b), eu = pool_event(ctx, 2 + 2 * b);
+    CUDA_TRY(cudaMemcpyAsync(dg + eb, grad_host + eb, (ee - eb) * 4, cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaEventRecord(eh, s));
+    CUDA_TRY(cudaStreamWaitEvent(xs, eh, 0));
+    if (agree) {
+      const uint64_t o0 = m->host_tile_off[tb], cnt = m->host_tile_off[te] - o0;
+      pactk::launch_pack(dg, len, m->words, m->tile_off, packed, tb, te, xs);
+      if (c && cnt) NCCL_TRY(ncclAllReduce(packed + o0, packed + o0, cnt, ncclFloat32, ncclSum, c->nccl, xs));
+      pactk::launch_unpack(packed, len, m->words, m->tile_off, scale, scale != 1.0f, dout, tb, te, xs);
+    } else {  // dense: (GSE) -> sum -> scale, segment by segment
+      float* d = dout + eb;
+      const uint64_t cnt = ee - eb;
+      const float* src = dg + eb;
+      if (pol.gse_dense) {  // eb is chunk aligned: the segment's words start at eb / 64
+        pactk::launch_gse(src, cnt, m->words + eb / 64, d, xs);
+        src = d;
+      }
+      if (c) {
+        NCCL_TRY(ncclAllReduce(src, d, cnt, ncclFloat32, ncclSum, c->nccl, xs));
+        src = d;
+      }
+      if (scale != 1.0f || src != d) pactk::launch_scale(src, d, cnt, scale, xs);
+    }
+    CUDA_TRY(cudaEventRecord(eu, xs));
+    CUDA_TRY(cudaStreamWaitEvent(ds, eu, 0));
+    CUDA_TRY(cudaMemcpyAsync(out_host + eb, dout + eb, (ee - eb) * 4, cudaMemcpyDeviceToHost, ds));
+  }
+  cudaEvent_t ex = pool_event(ctx, 1 + 2 * B), ed = pool_event(ctx, 2 + 2 * B);
+  CUDA_TRY(cudaEventRecord(ex, xs));
+  CUDA_TRY(cudaEventRecord(ed, ds));
+  CUDA_TRY(cudaStreamWaitEvent(s, ex, 0));
+  CUDA_TRY(cudaStreamWaitEvent(s, ed, 0));
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaEventRecord(ctx->t1, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  if (stats) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, ctx->t0, ctx->t1);
+    *stats = pact_sync_stats{};
+    stats->bytes_on_wire = c ? pact_masked_bytes(n, c->rank, agree ? m->nnz : len) : 0;
+    stats->seconds = ms * 1e-3;
+    stats->mode_used = agree ? PACT_SYNC_PACKED : PACT_SYNC_FULL;
+    stats->buckets = B;
+    stats->value_count = agree ? m->nnz : len;
+    stats->fallback_reason = reason;
+    stats->transport = c ? PACT_TRANSPORT_NCCL : 0;
+  }
   return PACT_OK;
 }
 

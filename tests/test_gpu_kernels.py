@@ -268,6 +268,20 @@ def test_single_gpu_masked_allreduce(pb, port, cuda):
     st = pb.masked_allreduce_host(gh, m, pb.TrackerStatus.Stable, 5, None, oh)
     assert st.mode_used == pb.SyncMode.PackedAllReduce
     assert np.array_equal(u32(oh.numpy()), u32(port.gse(g, w)))
+    # pipelined segments (len > 8 MiB) on every mode of the host entry point
+    n2 = 5_000_011
+    g2 = rng.standard_normal(n2).astype(np.float32)
+    w2 = words_from_bits(rng.random(n2) < 0.3)
+    m2 = pb.SparsityMask.from_words(dev(w2.view(np.int64)), n2)
+    gh2 = torch.from_numpy(g2).pin_memory()
+    oh2 = torch.empty(n2, dtype=torch.float32).pin_memory()
+    for status, pol, want in (
+            (pb.TrackerStatus.Stable, pb.SyncPolicy(scale=0.5), port.to_mean(port.gse(g2, w2), 2)),
+            (pb.TrackerStatus.Unstable, None, g2),
+            (pb.TrackerStatus.Unstable, pb.SyncPolicy(scale=0.25, gse_dense=True), port.to_mean(port.gse(g2, w2), 4))):
+        st = pb.masked_allreduce_host(gh2, m2, status, 6, None, oh2, policy=pol)
+        assert st.buckets > 1
+        assert np.array_equal(u32(oh2.numpy()), u32(want)), (status, pol)
 
 
 def test_dense_fallback_gse(pb, port, cuda):
