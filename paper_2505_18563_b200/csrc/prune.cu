@@ -90,18 +90,32 @@ __device__ __forceinline__ void load_chunk_keys(const float* __restrict__ w, uin
 }
 
 // ---------------------------------------------------------------- sample
-// 16384 keys, 16 per thread in registers; bitonic network: in-register for
-// strides < 16, warp shuffles for strides < 512, shared memory above.
-__device__ __forceinline__ void cswap(uint32_t& a, uint32_t& b, bool asc) {
-  const uint32_t lo = min(a, b), hi = max(a, b);
-  a = asc ? lo : hi;
-  b = asc ? hi : lo;
+// 16384 strided keys, 16 per thread in registers; the window ends are two
+// order statistics of the sample, found by an in-CTA radix select (11/11/9
+// bits: shared-memory histogram, block scan, pick the bucket holding the
+// rank) -- no sort. (The first version bitonic-sorted the sample in one CTA:
+// 130 us, the largest term of a first-time prune at C2.)
+__device__ __forceinline__ uint32_t block1024_excl_scan(uint32_t v, uint32_t* scratch) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t inc = warp_incl_scan(v);
+  if (lane == 31) scratch[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    const uint32_t x = scratch[lane];
+    scratch[lane] = warp_incl_scan(x) - x;
+  }
+  __syncthreads();
+  const uint32_t r = scratch[warp] + inc - v;
+  __syncthreads();
+  return r;
 }
 
 __global__ void __launch_bounds__(1024, 1)
     prune_sample_kernel(const float* __restrict__ w, uint64_t len, uint64_t k,
                         PruneWindow* __restrict__ win) {
-  extern __shared__ uint32_t s[];
+  __shared__ uint32_t hist[2048];
+  __shared__ uint32_t scratch[32];
+  __shared__ uint32_t sh_prefix, sh_rank;
   const int t = threadIdx.x;
   uint32_t r[16];
 #pragma unroll
@@ -109,70 +123,45 @@ __global__ void __launch_bounds__(1024, 1)
     const uint64_t i = (uint64_t)t * 16 + q;
     r[q] = mag_key(w[(i * len + len / 2) / kSample]);
   }
-  // stages with k <= 16: entirely in registers
+  const double p = (double)k / (double)len;
+  const double center = ((double)k - 0.5) / (double)len * kSample;
+  const double margin = 6.0 * sqrt(kSample * p * (1.0 - p)) + 8.0;
+  const long lo_i = (long)floor(center - margin);
+  const long hi_i = (long)ceil(center + margin);
+  uint32_t res[2] = {0u, 0x7fffffffu};
+  for (int which = 0; which < 2; ++which) {
+    const long target = which ? hi_i : lo_i;
+    if (which == 0 ? target <= 0 : target >= kSample - 1) continue;  // window open on that side
+    uint32_t prefix = 0, pmask = 0, rank = (uint32_t)target;          // rank in the sorted sample
+#pragma unroll 1
+    for (int pass = 0; pass < 3; ++pass) {
+      const int sh = pass == 0 ? 20 : (pass == 1 ? 9 : 0);
+      const uint32_t nb = pass == 2 ? 512u : 2048u;
+      hist[t] = 0;
+      hist[t + 1024] = 0;
+      __syncthreads();
 #pragma unroll
-  for (int kk = 2; kk <= 16; kk <<= 1) {
-#pragma unroll
-    for (int j = kk >> 1; j > 0; j >>= 1) {
-#pragma unroll
-      for (int q = 0; q < 16; ++q) {
-        if ((q & j) == 0) {
-          const uint32_t i = (uint32_t)t * 16 + q;
-          cswap(r[q], r[q | j], (i & kk) == 0);
-        }
+      for (int q = 0; q < 16; ++q)
+        if ((r[q] & pmask) == prefix) atomicAdd(&hist[(r[q] >> sh) & (nb - 1)], 1u);
+      __syncthreads();
+      const uint32_t a = hist[2 * t], b2 = hist[2 * t + 1];
+      const uint32_t excl = block1024_excl_scan(a + b2, scratch);
+      if (rank >= excl && rank < excl + a) {
+        sh_prefix = prefix | ((uint32_t)(2 * t) << sh);
+        sh_rank = rank - excl;
+      } else if (rank >= excl + a && rank < excl + a + b2) {
+        sh_prefix = prefix | ((uint32_t)(2 * t + 1) << sh);
+        sh_rank = rank - excl - a;
       }
+      __syncthreads();
+      prefix = sh_prefix;
+      rank = sh_rank;
+      pmask |= (nb - 1) << sh;
+      __syncthreads();
     }
+    res[which] = prefix;
   }
-  for (int kk = 32; kk <= kSample; kk <<= 1) {
-    for (int j = kk >> 1; j >= 16; j >>= 1) {
-      if (j >= 512) {
-#pragma unroll
-        for (int q = 0; q < 16; ++q) s[t * 16 + q] = r[q];
-        __syncthreads();
-#pragma unroll
-        for (int q = 0; q < 16; ++q) {
-          const uint32_t i = (uint32_t)t * 16 + q;
-          const uint32_t o = s[i ^ j];
-          const bool asc = (i & kk) == 0, lower = (i & j) == 0;
-          r[q] = (lower == asc) ? min(r[q], o) : max(r[q], o);
-        }
-        __syncthreads();
-      } else {
-        const int lanemask = j >> 4;
-#pragma unroll
-        for (int q = 0; q < 16; ++q) {
-          const uint32_t i = (uint32_t)t * 16 + q;
-          const uint32_t o = __shfl_xor_sync(0xffffffffu, r[q], lanemask);
-          const bool asc = (i & kk) == 0, lower = (i & j) == 0;
-          r[q] = (lower == asc) ? min(r[q], o) : max(r[q], o);
-        }
-      }
-    }
-#pragma unroll
-    for (int j = 8; j > 0; j >>= 1) {
-#pragma unroll
-      for (int q = 0; q < 16; ++q) {
-        if ((q & j) == 0) {
-          const uint32_t i = (uint32_t)t * 16 + q;
-          cswap(r[q], r[q | j], (i & kk) == 0);
-        }
-      }
-    }
-  }
-#pragma unroll
-  for (int q = 0; q < 16; ++q) s[t * 16 + q] = r[q];
-  __syncthreads();
-  if (t == 0) {
-    const double p = (double)k / (double)len;
-    const double center = ((double)k - 0.5) / (double)len * kSample;
-    const double margin = 6.0 * sqrt(kSample * p * (1.0 - p)) + 8.0;
-    const long lo_i = (long)floor(center - margin);
-    const long hi_i = (long)ceil(center + margin);
-    PruneWindow out;
-    out.lo = lo_i <= 0 ? 0u : s[lo_i];
-    out.hi = hi_i >= kSample - 1 ? 0x7fffffffu : s[hi_i];
-    *win = out;
-  }
+  if (t == 0) *win = PruneWindow{res[0], res[1]};
 }
 
 // ----------------------------------------------------------------- count
@@ -555,13 +544,7 @@ void launch_prune_seg_tiefix(uint64_t* words, uint64_t len, const uint64_t* tie_
 
 void launch_prune_sample(const float* w, uint64_t len, uint64_t k, PruneWindow* win_dev,
                          cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(prune_sample_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         kSample * 4);
-    attr = true;
-  }
-  prune_sample_kernel<<<1, 1024, kSample * 4, s>>>(w, len, k, win_dev);
+  prune_sample_kernel<<<1, 1024, 0, s>>>(w, len, k, win_dev);
   note_launch();
 }
 
