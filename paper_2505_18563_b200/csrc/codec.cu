@@ -99,22 +99,41 @@ __device__ __forceinline__ Slot chunk_slot(const uint64_t* wc, int j, uint32_t& 
 }
 
 // ------------------------------------------------------------------ pack
-// One warp per chunk; kept values are staged in a 4 KiB per-warp buffer and
-// leave as one coalesced run (full-line writes of the packed buffer).
+// One warp per chunk; kept values are staged in a per-warp buffer (at the
+// destination's 16-byte phase) and leave as one coalesced run. kPush (NVLink
+// one-shot, n = 2): the run is also stored into the peer's incoming region
+// as aligned float4 (scalar head / tail), and the last CTA publishes PACKED. (Tried: the body as a TMA bulk copy smem -> global,
+// cp.async.bulk: c5 pack 264 -> 297 us, push step unchanged; reverted.)
 constexpr int kPuWarps = 4;  // 128-thread CTAs
 
+// dst and st are 16-byte aligned; values occupy [ph, ph + run)
+__device__ __forceinline__ void write_run(float* __restrict__ dst, const float* st, uint32_t ph, uint32_t run) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t tot = ph + run;
+  const uint32_t q0 = ph ? 1u : 0u, qe = tot >> 2;
+  if (ph) {  // head: [ph, min(4, tot))
+    const uint32_t i = ph + lane;
+    if (i < 4 && i < tot) dst[i] = st[i];
+  }
+  for (uint32_t q = q0 + lane; q < qe; q += 32)
+    reinterpret_cast<float4*>(dst)[q] = reinterpret_cast<const float4*>(st)[q];
+  const uint32_t t0 = 4 * (qe > q0 ? qe : q0);
+  if (t0 + lane < tot) dst[t0 + lane] = st[t0 + lane];
+}
+
+template <bool kPush>
 __global__ void __launch_bounds__(kPuWarps * 32)
     pack_kernel(const float* __restrict__ g, uint64_t len, const uint64_t* __restrict__ words,
                 const uint32_t* __restrict__ chunk_off, float* __restrict__ packed, uint64_t cb,
-                uint64_t ce) {
-  __shared__ float stage_all[kPuWarps][kChunk];
+                uint64_t ce, float* __restrict__ remote, P2PView v, P2PSig sg) {
+  __shared__ __align__(16) float stage_all[kPuWarps][kChunk + 4];
   __shared__ __align__(16) uint64_t wsm[kPuWarps][2][kWbuf];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   float* stage = stage_all[warp];
   const bool vec_ok = (((uintptr_t)g) & 15) == 0;
   const uint64_t nwt = (uint64_t)gridDim.x * kPuWarps;
   uint64_t c = cb + (uint64_t)blockIdx.x * kPuWarps + warp;
-  if (c >= ce) return;
+  if (c < ce) {
   words_issue(wsm[warp][0], words, chunk_off, c);
   for (int cur = 0; c < ce; c += nwt, cur ^= 1) {
     if (c + nwt < ce) words_issue(wsm[warp][cur ^ 1], words, chunk_off, c + nwt);
@@ -122,22 +141,23 @@ __global__ void __launch_bounds__(kPuWarps * 32)
     words_wait_prev();
     const uint64_t* wc = wsm[warp][cur];
     const uint32_t base = (uint32_t)wc[kChunkWords];
+    const uint32_t ph = (uint32_t)(((uintptr_t)(packed + base) >> 2) & 3u);
     const uint64_t e0 = c * (uint64_t)kChunk + 4 * lane;
     uint32_t run = 0;
-    float4 v[kVecPerLane];
+    float4 x[kVecPerLane];
 #pragma unroll
     for (int j = 0; j < kVecPerLane; ++j) {
       const Slot s = chunk_slot(wc, j, run);
       const uint64_t ge = e0 + 128 * j;
-      v[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+      x[j] = make_float4(0.f, 0.f, 0.f, 0.f);
       if (s.nib) {
         if (vec_ok && ge + 4 <= len) {
-          v[j] = ld_stream_f4(reinterpret_cast<const float4*>(g + ge));
+          x[j] = ld_stream_f4(reinterpret_cast<const float4*>(g + ge));
         } else {  // unaligned base or ragged tail: only kept (hence in-range) lanes
-          if (s.nib & 1) v[j].x = g[ge];
-          if (s.nib & 2) v[j].y = g[ge + 1];
-          if (s.nib & 4) v[j].z = g[ge + 2];
-          if (s.nib & 8) v[j].w = g[ge + 3];
+          if (s.nib & 1) x[j].x = g[ge];
+          if (s.nib & 2) x[j].y = g[ge + 1];
+          if (s.nib & 4) x[j].z = g[ge + 2];
+          if (s.nib & 8) x[j].w = g[ge + 3];
         }
       }
     }
@@ -146,19 +166,23 @@ __global__ void __launch_bounds__(kPuWarps * 32)
 #pragma unroll
     for (int j = 0; j < kVecPerLane; ++j) {
       const Slot s = chunk_slot(wc, j, run);
-      const uint32_t nib = s.nib, p = s.pos;
+      const uint32_t nib = s.nib, p = ph + s.pos;
       const uint32_t b0 = nib & 1, b1 = (nib >> 1) & 1, b2 = (nib >> 2) & 1;
-      if (b0) stage[p] = v[j].x;
-      if (b1) stage[p + b0] = v[j].y;
-      if (b2) stage[p + b0 + b1] = v[j].z;
-      if (nib & 8) stage[p + b0 + b1 + b2] = v[j].w;
+      if (b0) stage[p] = x[j].x;
+      if (b1) stage[p + b0] = x[j].y;
+      if (b2) stage[p + b0 + b1] = x[j].z;
+      if (nib & 8) stage[p + b0 + b1 + b2] = x[j].w;
     }
     __syncwarp();
-    float* dst = packed + base;
+    float* dst = packed + base;  // local: coalesced scalar run (measured faster than float4 here)
 #pragma unroll 4
-    for (uint32_t i = lane; i < run; i += 32) dst[i] = stage[i];
+    for (uint32_t i = lane; i < run; i += 32) dst[i] = stage[ph + i];
+    // remote: aligned float4 (misaligned 4-byte NVLink stores run at ~60%)
+    if constexpr (kPush) write_run(remote + base - ph, stage, ph, run);
     __syncwarp();  // stage and buffer `cur` are reused
   }
+  }
+  if constexpr (kPush) p2psync::exit_signal(v, sg);  // PACKED: every CTA's remote stores are done
 }
 
 // ---------------------------------------------------------------- unpack
@@ -593,9 +617,20 @@ void launch_pack(const float* g, uint64_t len, const uint64_t* words, const uint
                  float* packed, uint64_t cb, uint64_t ce, cudaStream_t s) {
   if (ce <= cb) return;
   static int cap = 0;
-  if (!cap) cap = persistent_grid(pack_kernel, kPuWarps);
-  pack_kernel<<<grid_for(cap, ce - cb, kPuWarps), kPuWarps * 32, 0, s>>>(g, len, words, chunk_off,
-                                                                         packed, cb, ce);
+  if (!cap) cap = persistent_grid(pack_kernel<false>, kPuWarps);
+  pack_kernel<false><<<grid_for(cap, ce - cb, kPuWarps), kPuWarps * 32, 0, s>>>(
+      g, len, words, chunk_off, packed, cb, ce, nullptr, P2PView{}, P2PSig{});
+  note_launch();
+}
+
+void launch_pack_push(const float* g, uint64_t len, const uint64_t* words, const uint32_t* chunk_off,
+                      float* packed, float* remote, const P2PView& v, const P2PSig& sg, cudaStream_t s) {
+  const uint64_t nc = (len + kChunk - 1) / kChunk;
+  if (!nc) return;
+  static int cap = 0;
+  if (!cap) cap = persistent_grid(pack_kernel<true>, kPuWarps);
+  pack_kernel<true><<<grid_for(cap, nc, kPuWarps), kPuWarps * 32, 0, s>>>(g, len, words, chunk_off, packed,
+                                                                          0, nc, remote, v, sg);
   note_launch();
 }
 

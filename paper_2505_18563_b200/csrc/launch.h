@@ -32,6 +32,10 @@ struct P2PSig {
 // chunk range [cb, ce) of 1024-element chunks; all pointers device.
 void launch_pack(const float* g, uint64_t len, const uint64_t* words, const uint32_t* chunk_off,
                  float* packed, uint64_t cb, uint64_t ce, cudaStream_t s);
+// pack into `packed` and, with the same offsets, into `remote` (the peer's
+// incoming region, NVLink stores); the last CTA publishes sg's exit flag
+void launch_pack_push(const float* g, uint64_t len, const uint64_t* words, const uint32_t* chunk_off,
+                      float* packed, float* remote, const P2PView& v, const P2PSig& sg, cudaStream_t s);
 void launch_unpack(const float* packed, uint64_t len, const uint64_t* words,
                    const uint32_t* chunk_off, float scale, int do_scale, float* out, uint64_t cb,
                    uint64_t ce, cudaStream_t s);

@@ -1672,6 +1672,12 @@ pact_status pact_masked_allreduce(pact_comm* c, pact_ctx* ctx, const float* grad
   const bool p2p_try = c && m->nnz && n <= pactk::kP2PMaxRanks && !f16 &&
                        (pol.transport == PACT_TRANSPORT_P2P || (pol.transport == PACT_TRANSPORT_AUTO && auto_p2p));
   const bool p2p_ready = p2p_try && c->p2p.ok && c->p2p.cap >= m->nnz;
+  const bool p2p_buckets = p2p_try && pol.bucket_bytes > 0 && m->nnz * 4 > pol.bucket_bytes;
+  // n = 2, one bucket: push exchange (pack stores its run into the peer's
+  // incoming region as well; unpack folds two LOCAL runs). No speculative
+  // pack in this mode: PACKED is published by the pack itself.
+  static const bool push_env = !getenv("PACT_P2P_PULL");
+  const bool p2p_push = push_env && p2p_try && n == 2 && !p2p_buckets;
   // NCCL buckets: bucket_bytes, or auto (0): one bucket on the symmetric
   // window up to 64 MiB packed (c3 n=4 277 vs 351 us bucketed), 32 MiB
   // buckets above (c5 n=4 1.12 vs 1.22 ms single)
@@ -1684,8 +1690,7 @@ pact_status pact_masked_allreduce(pact_comm* c, pact_ctx* ctx, const float* grad
   if (c) {
     // speculative pack overlaps the vote (single-bucket plans): enqueued
     // first so the GPU starts while the host votes; unused on a fallback
-    const bool p2p_buckets = p2p_try && pol.bucket_bytes > 0 && m->nnz * 4 > pol.bucket_bytes;
-    if (stable && !buckets && !p2p_buckets && !f16 && m->nnz) {
+    if (stable && !buckets && !p2p_buckets && !p2p_push && !f16 && m->nnz) {
       if (p2p_ready) {  // straight into this rank's symmetric buffer
         const uint64_t k1 = c->p2p.k + 1;
         if (k1 > 2)  // peers finished reading this region (step k1-2)
@@ -1757,6 +1762,32 @@ pact_status pact_masked_allreduce(pact_comm* c, pact_ctx* ctx, const float* grad
     const int xctas = B > 1 ? 4 * sm_count_host() : 0;  // leave SMs to pack/unpack
     const bool two = n > 2;
     if (!packed_in_sym && k1 > 2) pactk::launch_p2p_wait(myflags, pactk::kP2PRead, n, k1 - 2, err, s);
+    if (B == 1 && p2p_push) {
+      // push one-shot (n = 2): pack -> {own packed, peer's incoming} and
+      // PACKED on exit; unpack waits for the peer's PACKED and folds the
+      // local run with the incoming one (x_c + x_{c+1}: order-free for two)
+      const int peer = c->rank ^ 1;
+      pactk::P2PSig sgp;
+      sgp.exit_kind = pactk::kP2PPacked;
+      sgp.exit_val = fval(0);
+      sgp.counter = p2p_counter(p, c->rank);
+      pactk::launch_pack_push(grad, len, m->words, m->tile_off, mine, p2p_reduced(p, peer, par), v, sgp, s);
+      mark(0);
+      mark(1);
+      pactk::P2PView vin = v;
+      vin.packed[peer] = p2p_reduced(p, c->rank, par);  // this rank's incoming region
+      pactk::P2PSig sgu;
+      sgu.exit_kind = pactk::kP2PRead;
+      sgu.exit_val = k1;
+      sgu.counter = sgp.counter;
+      pactk::launch_unpack_p2p(mine, len, m->words, m->tile_off, scale, scale != 1.0f, out, vin, 0, myflags,
+                               fval(0), err, sgu, s);
+      mark(2);
+      p.k = k1;
+      nbuckets = 1;
+      transport = PACT_TRANSPORT_P2P;
+      goto p2p_done;
+    }
     if (B == 1) {  // no pipelining: everything in order on the caller's stream
       if (!packed_in_sym) pactk::launch_pack(grad, len, m->words, m->tile_off, mine, 0, m->ntiles, s);
       mark(0);
