@@ -355,7 +355,7 @@ def main():
         stages["prune_us"] = round(t_prune * 1e6, 1)
         stages["prune_gbs"] = round((4 * n + n / 8) / t_prune / 1e9, 1)
     if t_pack >= t_unpack:
-        dom, alg, tdom = "pack_kernel", alg_pack, t_pack
+        dom, alg, tdom = "pack_lm_kernel<0>", alg_pack, t_pack
     else:
         dom, alg, tdom = "unpack_kernel<0, 0>", alg_unpack, t_unpack
     peak, peak_kind = peaks()

@@ -275,6 +275,123 @@ __device__ __forceinline__ void issue_run(float* dst, const float* __restrict__ 
   }
 }
 
+// ------------------------------------------------------- pack, lane-major
+// The register-resident pack above spends ~570 warp-instructions per chunk
+// recomputing per-slot ranks (ncu c2: issue-bound, 65% issue slots busy at
+// 33% of DRAM peak). This variant moves the chunk through shared memory so
+// that the compaction is lane-major like the unpack: lane l owns mask
+// half-word l (32 consecutive elements), its kept values land at one warp
+// scan's offset, no per-slot ranks. Three-stage cp.async pipeline per warp
+// (words + offsets of chunk i+2; the gradient slots of chunk i+1, issued only
+// where the slot's 4-bit nibble is non-zero, so only sectors holding kept
+// values are read; compaction of chunk i). The stage is XOR-swizzled (16-byte
+// cell q of a 128-byte row at column (q ^ row) & 7) so both the slot-major
+// cp.async writes and the lane-major LDS.128 reads are conflict-free; the
+// compacted run is written back in place (after every lane has read its
+// cells) at the destination's 16-byte phase and leaves as one coalesced run.
+constexpr int kPkStage = kChunk + 4;  // a chunk, or a run plus its 16-byte phase
+__device__ __forceinline__ int swz_cell(int q) { return (q & ~7) | ((q ^ (q >> 3)) & 7); }
+
+__device__ __forceinline__ void pack_data_issue(float* st, const float* __restrict__ g, uint64_t len, bool vec_ok,
+                                                const uint64_t* wc, uint64_t c) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t e0 = c * (uint64_t)kChunk;
+#pragma unroll
+  for (int j = 0; j < kVecPerLane; ++j) {
+    const uint32_t nib = (uint32_t)(wc[2 * j + (lane >> 4)] >> (4 * (lane & 15))) & 0xFu;
+    const int q = 32 * j + lane;
+    const uint64_t ge = e0 + 4 * (uint64_t)q;
+    float* d = st + 4 * swz_cell(q);
+    if (nib) {
+      if (vec_ok && ge + 4 <= len) {
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(d)),
+                     "l"(g + ge)
+                     : "memory");
+      } else {  // unaligned base or ragged tail: kept (hence in-range) elements only
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+          if ((nib >> b) & 1)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
+                             (uint32_t)__cvta_generic_to_shared(d + b)),
+                         "l"(g + ge + b)
+                         : "memory");
+      }
+    }
+  }
+}
+
+template <bool kPush>
+__global__ void __launch_bounds__(kPuWarps * 32)
+    pack_lm_kernel(const float* __restrict__ g, uint64_t len, const uint64_t* __restrict__ words,
+                   const uint32_t* __restrict__ chunk_off, float* __restrict__ packed, uint64_t cb,
+                   uint64_t ce, float* __restrict__ remote, P2PView v, P2PSig sg) {
+  __shared__ __align__(16) float dsm[kPuWarps][2][kPkStage];
+  __shared__ __align__(16) uint64_t wsm[kPuWarps][3][kWbuf];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const bool vec_ok = (((uintptr_t)g) & 15) == 0;
+  const uint64_t nwt = (uint64_t)gridDim.x * kPuWarps;
+  uint64_t c = cb + (uint64_t)blockIdx.x * kPuWarps + warp;
+  if (c < ce) {
+    // prologue: words(c0), words(c1), data(c0)
+    offs_words_issue(wsm[warp][0], words, chunk_off, c);
+    cp_commit();
+    if (c + nwt < ce) offs_words_issue(wsm[warp][1], words, chunk_off, c + nwt);
+    cp_commit();
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
+    __syncwarp();
+    pack_data_issue(dsm[warp][0], g, len, vec_ok, wsm[warp][0], c);
+    cp_commit();
+    int wi = 0, pi = 0;
+    for (; c < ce; c += nwt) {
+      const int w1 = wi == 2 ? 0 : wi + 1, w2 = w1 == 2 ? 0 : w1 + 1;
+      if (c + 2 * nwt < ce) offs_words_issue(wsm[warp][w2], words, chunk_off, c + 2 * nwt);
+      cp_commit();
+      asm volatile("cp.async.wait_group 1;" ::: "memory");  // words(c+nwt), data(c) landed
+      __syncwarp();
+      if (c + nwt < ce) pack_data_issue(dsm[warp][pi ^ 1], g, len, vec_ok, wsm[warp][w1], c + nwt);
+      cp_commit();
+      const uint64_t* wc = wsm[warp][wi];
+      const uint32_t base = reinterpret_cast<const uint32_t*>(wc + kChunkWords)[0];
+      float* st = dsm[warp][pi];
+      const uint32_t h = reinterpret_cast<const uint32_t*>(wc)[lane];
+      const uint32_t hc = __popc(h);
+      const uint32_t incl = warp_incl_scan(hc);
+      const uint32_t run = __shfl_sync(0xffffffffu, incl, 31);
+      const uint32_t ph = (uint32_t)(((uintptr_t)(packed + base) >> 2) & 3u);
+      // lane-major read of the lane's 32 elements (cells 8 l .. 8 l + 7)
+      float x[32];
+      const float4* S = reinterpret_cast<const float4*>(st);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const float4 t = S[8 * lane + ((k ^ lane) & 7)];
+        x[4 * k] = t.x, x[4 * k + 1] = t.y, x[4 * k + 2] = t.z, x[4 * k + 3] = t.w;
+      }
+      __syncwarp();
+      // in-place compaction: per element a bit test, a predicated STS and a
+      // predicated address increment
+      uint32_t sa = (uint32_t)__cvta_generic_to_shared(st + ph + incl - hc);
+#pragma unroll
+      for (int e = 0; e < 32; ++e)
+        asm volatile(
+            "{\n .reg .pred p;\n setp.ne.u32 p, %2, 0;\n @p st.shared.f32 [%0], %1;\n"
+            " @p add.u32 %0, %0, 4;\n}"
+            : "+r"(sa)
+            : "f"(x[e]), "r"(h & (1u << e))
+            : "memory");
+      __syncwarp();
+      float* dst = packed + base;
+#pragma unroll 4
+      for (uint32_t i = lane; i < run; i += 32) dst[i] = st[ph + i];
+      if constexpr (kPush) write_run(remote + base - ph, st, ph, run);
+      __syncwarp();  // stage pi and word buffer wi are refilled next
+      wi = w1;
+      pi ^= 1;
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+  }
+  if constexpr (kPush) p2psync::exit_signal(v, sg);  // PACKED: every CTA's remote stores are done
+}
+
 template <bool kSgd, int kSrc>
 __global__ void __launch_bounds__(kPuWarps * 32)
     unpack_kernel(const float* __restrict__ packed, uint64_t len, const uint64_t* __restrict__ words,
@@ -616,10 +733,15 @@ void note_launch(uint64_t n) { g_launches += n; }
 void launch_pack(const float* g, uint64_t len, const uint64_t* words, const uint32_t* chunk_off,
                  float* packed, uint64_t cb, uint64_t ce, cudaStream_t s) {
   if (ce <= cb) return;
+  static const bool v1 = getenv("PACT_PACK_V1") != nullptr;
   static int cap = 0;
-  if (!cap) cap = persistent_grid(pack_kernel<false>, kPuWarps);
-  pack_kernel<false><<<grid_for(cap, ce - cb, kPuWarps), kPuWarps * 32, 0, s>>>(
-      g, len, words, chunk_off, packed, cb, ce, nullptr, P2PView{}, P2PSig{});
+  if (!cap) cap = v1 ? persistent_grid(pack_kernel<false>, kPuWarps) : persistent_grid(pack_lm_kernel<false>, kPuWarps);
+  if (v1)
+    pack_kernel<false><<<grid_for(cap, ce - cb, kPuWarps), kPuWarps * 32, 0, s>>>(
+        g, len, words, chunk_off, packed, cb, ce, nullptr, P2PView{}, P2PSig{});
+  else
+    pack_lm_kernel<false><<<grid_for(cap, ce - cb, kPuWarps), kPuWarps * 32, 0, s>>>(
+        g, len, words, chunk_off, packed, cb, ce, nullptr, P2PView{}, P2PSig{});
   note_launch();
 }
 
@@ -627,10 +749,15 @@ void launch_pack_push(const float* g, uint64_t len, const uint64_t* words, const
                       float* packed, float* remote, const P2PView& v, const P2PSig& sg, cudaStream_t s) {
   const uint64_t nc = (len + kChunk - 1) / kChunk;
   if (!nc) return;
+  static const bool v1 = getenv("PACT_PACK_V1") != nullptr;
   static int cap = 0;
-  if (!cap) cap = persistent_grid(pack_kernel<true>, kPuWarps);
-  pack_kernel<true><<<grid_for(cap, nc, kPuWarps), kPuWarps * 32, 0, s>>>(g, len, words, chunk_off, packed,
-                                                                          0, nc, remote, v, sg);
+  if (!cap) cap = v1 ? persistent_grid(pack_kernel<true>, kPuWarps) : persistent_grid(pack_lm_kernel<true>, kPuWarps);
+  if (v1)
+    pack_kernel<true><<<grid_for(cap, nc, kPuWarps), kPuWarps * 32, 0, s>>>(g, len, words, chunk_off, packed, 0,
+                                                                            nc, remote, v, sg);
+  else
+    pack_lm_kernel<true><<<grid_for(cap, nc, kPuWarps), kPuWarps * 32, 0, s>>>(g, len, words, chunk_off, packed,
+                                                                               0, nc, remote, v, sg);
   note_launch();
 }
 

@@ -20,6 +20,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -2220,9 +2221,14 @@ pact_status pact_masked_allreduce_host(pact_comm* c, pact_ctx* ctx, const float*
   float* dout = ctx->out_stage.as<float>();
   float* packed = ctx->packed.as<float>();
   if (agree) TRY(mirror_tile_off(m, s));
-  // segments: whole chunks, ~8 MiB of gradient each, at most 64
+  // segments: whole chunks, ~8 MiB of gradient each (PACT_HOST_SEG_MB), at most 64
+  static const uint64_t seg_bytes = [] {
+    const char* e = getenv("PACT_HOST_SEG_MB");
+    const double mb = e ? atof(e) : 8.0;
+    return (uint64_t)((mb > 0.0 ? mb : 8.0) * (1 << 20));
+  }();
   const uint64_t nt = std::max<uint64_t>(1, m->ntiles);
-  const uint64_t per = std::max<uint64_t>((nt + 63) / 64, (8ull << 20) / 4 / PACT_TILE);
+  const uint64_t per = std::max<uint64_t>({(nt + 63) / 64, seg_bytes / 4 / PACT_TILE, 1});
   const int B = (int)((nt + per - 1) / per);
   cudaStream_t xs = ctx->aux[0], ds = ctx->aux[1];
   cudaEvent_t e0 = pool_event(ctx, 0);
