@@ -171,6 +171,34 @@ METRIC = "dense-equiv. gradient sync GB/s (prune+pack+allreduce+unpack)"
 # ------------------------------------------------------------------ ours
 
 
+def pcie_roofline(torch, gh, oh, dg, dout, stream, t_e2e):
+    """The host-buffer path moves 4*len bytes each way over PCIe: its floor is
+    one H2D and one D2H of the step's buffers running concurrently. Measured
+    live on the same pinned buffers (two streams, median of 5)."""
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    ts = []
+    for _ in range(6):
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        s1.wait_stream(stream)
+        s2.wait_stream(stream)
+        with torch.cuda.stream(s1):
+            dg.copy_(gh, non_blocking=True)
+        with torch.cuda.stream(s2):
+            oh.copy_(dout, non_blocking=True)
+        stream.wait_stream(s1)
+        stream.wait_stream(s2)
+        b.record(stream)
+        b.synchronize()
+        ts.append(a.elapsed_time(b) * 1e-3)
+    t_floor = statistics.median(ts[1:])
+    return {"bound": "pcie", "floor_ms": round(t_floor * 1e3, 3),
+            "peak_gbs_per_direction": round(dg.numel() * 4 / t_floor / 1e9, 2),
+            "frac": round(t_floor / t_e2e, 4),
+            "note": "floor = concurrent H2D + D2H of the step's pinned buffers, measured in this run"}
+
+
 def cpu_baseline_sample(shape, ratio, words_np, n):
     """Reference CPU path on this host, bounded sample (rank 0, N=1 only)."""
     try:
@@ -197,6 +225,10 @@ def cpu_baseline_sample(shape, ratio, words_np, n):
 
 
 def main():
+    # the image sets NCCL_DEBUG=VERSION, which makes NCCL print its version to
+    # rank 0's stdout at communicator init; the contract is ONE JSON line
+    if os.environ.get("NCCL_DEBUG", "").upper() == "VERSION":
+        os.environ["NCCL_DEBUG"] = "WARN"
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
@@ -377,10 +409,17 @@ def main():
         t_dense = statistics.median(timed(lambda i: pb.full_allreduce(grad, comm, out=out), 10))
         t_packed_ar = statistics.median(timed(lambda i: pb.ring_allreduce(packed, comm, out=packed), 10))
         f = 2 * (world - 1) / world
+        # the exchange as the step pays for it: step time minus pack and
+        # unpack timed alone (the P2P exchange is fused into them, so there
+        # is no separate exchange kernel to time)
+        t_x = max(t_step - t_pack - t_unpack, 1e-9)
         extra = {"dense_allreduce_us": round(t_dense * 1e6, 1),
                  "dense_busbw_gbs": round(4 * n * f / t_dense / 1e9, 1),
                  "packed_allreduce_us": round(t_packed_ar * 1e6, 1),
                  "packed_busbw_gbs": round(4 * nnz * f / t_packed_ar / 1e9, 1),
+                 "step_exchange_us": round(t_x * 1e6, 1),
+                 "step_exchange_busbw_gbs": round(4 * nnz * f / t_x / 1e9, 1),
+                 "step_exchange_vs_dense_busbw": round((4 * nnz * f / t_x) / (4 * n * f / t_dense), 3),
                  "dense_sync_equiv_gbs_per_rank": round(4 * n / t_dense / 1e9, 1)}
 
     # ---- e2e through the host-buffer C-ABI entry point
@@ -407,7 +446,8 @@ def main():
             torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
             t_e2e = float(tt.item())
         e2e = {"value": round(4.0 * n / t_e2e / 1e9 * world, 3), "unit": "GB/s",
-               "h2d_bytes_per_step": 4 * n, "d2h_bytes_per_step": 4 * n, "ms_per_step": round(t_e2e * 1e3, 3)}
+               "h2d_bytes_per_step": 4 * n, "d2h_bytes_per_step": 4 * n, "ms_per_step": round(t_e2e * 1e3, 3),
+               "roofline": pcie_roofline(torch, gh, oh, grad, out, stream, t_e2e)}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

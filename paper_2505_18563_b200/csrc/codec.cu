@@ -9,20 +9,22 @@
 // Layout: the gradient is cut into 1024-element chunks (16 mask words; the
 // word array is padded to whole chunks). A mask carries chunk_off[c] = kept
 // elements before chunk c, so one WARP owns one chunk end to end with no
-// inter-warp communication and no shared memory. Lane l's eight float4 slots
-// cover elements 128*j + 4*l (coalesced 512-byte warp accesses); slot j's two
-// mask words arrive as one broadcast 16-byte load (L1 resident: the next
-// chunk's 128-byte word line is prefetched into L1 one iteration ahead), and
-// the lane's rank inside the chunk is a popcount of the bits below it, so no
-// shuffles or scans are needed. Pack skips a slot's gradient load when its
-// 4-bit nibble is zero (only sectors holding kept values are read) and
-// stores kept values straight to their packed positions; unpack gathers them
-// with predicated loads and writes full float4s. All loads of a chunk are
-// issued before any use. Persistent grids; warps stride over chunks.
+// inter-warp communication. Pack and unpack are LANE-MAJOR: lane l owns mask
+// half-word l (32 consecutive elements), so a lane's kept values are
+// consecutive in the packed run from one warp scan of the half-word
+// popcounts -- no per-slot ranks. The dense side moves through a per-warp,
+// XOR-swizzled shared-memory stage (cp.async in, coalesced float4 out), so
+// global accesses stay coalesced while the compaction / expansion works on
+// the lane-major view. Persistent grids; warps stride over chunks; every
+// kernel keeps a three-stage cp.async pipeline per warp (words of chunk
+// i+2, data of chunk i+1, work on chunk i).
 //
-// The kernels are issue-bound, not bandwidth-bound, at the sizes of interest
-// (ncu: ~480 warp-instructions per chunk in the smem-staged version), so the
-// formulation minimises instructions per element.
+// The kernels are issue- and shared-memory-bound, not DRAM-bound, at the
+// sizes of interest, so the formulation minimises instructions per element
+// (ncu c2: the earlier register-resident pack issued ~570 warp-instructions
+// per chunk at 65% issue utilisation and 33% of DRAM peak).
+#include <cstdlib>
+
 #include "common.cuh"
 #include "launch.h"
 #include "p2p_sync.cuh"
@@ -58,27 +60,8 @@ unsigned grid_for(int cap, uint64_t chunks, int warps = kCodecWarps) {
   return (unsigned)(need < (uint64_t)cap ? need : (uint64_t)cap);
 }
 
-// Per-warp double buffer of the next chunk's 16 mask words + its offset,
-// filled with cp.async one iteration ahead (no registers held in flight).
-constexpr int kWbuf = kChunkWords + 2;  // 16 words, chunk_off in [16]
-__device__ __forceinline__ void words_issue(uint64_t* dst, const uint64_t* __restrict__ words,
-                                            const uint32_t* __restrict__ chunk_off, uint64_t c) {
-  const int lane = threadIdx.x & 31;
-  if (lane < 8) {
-    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(dst + 2 * lane);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa),
-                 "l"(words + c * kChunkWords + 2 * lane)
-                 : "memory");
-  } else if (lane == 8 && chunk_off) {
-    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(dst + kChunkWords);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(chunk_off + c) : "memory");
-  }
-  asm volatile("cp.async.commit_group;" ::: "memory");
-}
-__device__ __forceinline__ void words_wait_prev() {
-  asm volatile("cp.async.wait_group 1;" ::: "memory");
-  __syncwarp();
-}
+// per-warp stage of a chunk's 16 mask words + chunk_off[c], chunk_off[c+1]
+constexpr int kWbuf = kChunkWords + 2;
 
 // Slot j of the current chunk: nibble and in-chunk rank of lane's first
 // element. `run` accumulates the kept count of the slots before (uniform).
@@ -99,11 +82,10 @@ __device__ __forceinline__ Slot chunk_slot(const uint64_t* wc, int j, uint32_t& 
 }
 
 // ------------------------------------------------------------------ pack
-// One warp per chunk; kept values are staged in a per-warp buffer (at the
-// destination's 16-byte phase) and leave as one coalesced run. kPush (NVLink
-// one-shot, n = 2): the run is also stored into the peer's incoming region
-// as aligned float4 (scalar head / tail), and the last CTA publishes PACKED. (Tried: the body as a TMA bulk copy smem -> global,
-// cp.async.bulk: c5 pack 264 -> 297 us, push step unchanged; reverted.)
+// kPush (NVLink one-shot, n = 2): the run is also written into the peer's
+// incoming region (aligned float4 cells; scalar head / tail), and the last
+// CTA publishes PACKED. (Tried: the LOCAL run as a TMA bulk copy smem ->
+// global: c5 pack 264 -> 297 us; the remote run as a bulk copy is kept.)
 constexpr int kPuWarps = 4;  // 128-thread CTAs
 
 // dst and st are 16-byte aligned; values occupy [ph, ph + run)
@@ -119,70 +101,6 @@ __device__ __forceinline__ void write_run(float* __restrict__ dst, const float* 
     reinterpret_cast<float4*>(dst)[q] = reinterpret_cast<const float4*>(st)[q];
   const uint32_t t0 = 4 * (qe > q0 ? qe : q0);
   if (t0 + lane < tot) dst[t0 + lane] = st[t0 + lane];
-}
-
-template <bool kPush>
-__global__ void __launch_bounds__(kPuWarps * 32)
-    pack_kernel(const float* __restrict__ g, uint64_t len, const uint64_t* __restrict__ words,
-                const uint32_t* __restrict__ chunk_off, float* __restrict__ packed, uint64_t cb,
-                uint64_t ce, float* __restrict__ remote, P2PView v, P2PSig sg) {
-  __shared__ __align__(16) float stage_all[kPuWarps][kChunk + 4];
-  __shared__ __align__(16) uint64_t wsm[kPuWarps][2][kWbuf];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  float* stage = stage_all[warp];
-  const bool vec_ok = (((uintptr_t)g) & 15) == 0;
-  const uint64_t nwt = (uint64_t)gridDim.x * kPuWarps;
-  uint64_t c = cb + (uint64_t)blockIdx.x * kPuWarps + warp;
-  if (c < ce) {
-  words_issue(wsm[warp][0], words, chunk_off, c);
-  for (int cur = 0; c < ce; c += nwt, cur ^= 1) {
-    if (c + nwt < ce) words_issue(wsm[warp][cur ^ 1], words, chunk_off, c + nwt);
-    else asm volatile("cp.async.commit_group;" ::: "memory");
-    words_wait_prev();
-    const uint64_t* wc = wsm[warp][cur];
-    const uint32_t base = (uint32_t)wc[kChunkWords];
-    const uint32_t ph = (uint32_t)(((uintptr_t)(packed + base) >> 2) & 3u);
-    const uint64_t e0 = c * (uint64_t)kChunk + 4 * lane;
-    uint32_t run = 0;
-    float4 x[kVecPerLane];
-#pragma unroll
-    for (int j = 0; j < kVecPerLane; ++j) {
-      const Slot s = chunk_slot(wc, j, run);
-      const uint64_t ge = e0 + 128 * j;
-      x[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (s.nib) {
-        if (vec_ok && ge + 4 <= len) {
-          x[j] = ld_stream_f4(reinterpret_cast<const float4*>(g + ge));
-        } else {  // unaligned base or ragged tail: only kept (hence in-range) lanes
-          if (s.nib & 1) x[j].x = g[ge];
-          if (s.nib & 2) x[j].y = g[ge + 1];
-          if (s.nib & 4) x[j].z = g[ge + 2];
-          if (s.nib & 8) x[j].w = g[ge + 3];
-        }
-      }
-    }
-    run = 0;  // ranks recomputed from the (smem) words: fewer live registers,
-              // measured faster than keeping them (c5 pack 262 vs 276 us)
-#pragma unroll
-    for (int j = 0; j < kVecPerLane; ++j) {
-      const Slot s = chunk_slot(wc, j, run);
-      const uint32_t nib = s.nib, p = ph + s.pos;
-      const uint32_t b0 = nib & 1, b1 = (nib >> 1) & 1, b2 = (nib >> 2) & 1;
-      if (b0) stage[p] = x[j].x;
-      if (b1) stage[p + b0] = x[j].y;
-      if (b2) stage[p + b0 + b1] = x[j].z;
-      if (nib & 8) stage[p + b0 + b1 + b2] = x[j].w;
-    }
-    __syncwarp();
-    float* dst = packed + base;  // local: coalesced scalar run (measured faster than float4 here)
-#pragma unroll 4
-    for (uint32_t i = lane; i < run; i += 32) dst[i] = stage[ph + i];
-    // remote: aligned float4 (misaligned 4-byte NVLink stores run at ~60%)
-    if constexpr (kPush) write_run(remote + base - ph, stage, ph, run);
-    __syncwarp();  // stage and buffer `cur` are reused
-  }
-  }
-  if constexpr (kPush) p2psync::exit_signal(v, sg);  // PACKED: every CTA's remote stores are done
 }
 
 // ---------------------------------------------------------------- unpack
@@ -289,6 +207,36 @@ __device__ __forceinline__ void issue_run(float* dst, const float* __restrict__ 
 // cp.async writes and the lane-major LDS.128 reads are conflict-free; the
 // compacted run is written back in place (after every lane has read its
 // cells) at the destination's 16-byte phase and leaves as one coalesced run.
+constexpr int kPushNone = 0, kPushStores = 1, kPushTma = 2;
+
+// NVLink push of a staged run as one bulk async copy (TMA engine, smem ->
+// peer global) for the whole 16-byte cells, scalar stores for the partial
+// head / tail cells (they are shared with the neighbouring chunks' runs).
+// The warp does not wait for the remote stores: the stage is recycled after
+// cp.async.bulk.wait_group.read, the kernel exit waits for completion.
+__device__ __forceinline__ void push_run_bulk(float* __restrict__ dst, const float* st, uint32_t ph, uint32_t run) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t tot = ph + run;
+  const uint32_t q0 = ph ? 1u : 0u, qe = tot >> 2;
+  if (ph) {
+    const uint32_t i = ph + lane;
+    if (i < 4 && i < tot) dst[i] = st[i];
+  }
+  const uint32_t t0 = 4 * (qe > q0 ? qe : q0);
+  if (t0 + lane < tot) dst[t0 + lane] = st[t0 + lane];
+  if (qe > q0) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the compaction's STS -> async proxy
+    __syncwarp();
+    if (lane == 0) {
+      asm volatile(
+          "cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n"
+          " cp.async.bulk.commit_group;" ::"l"(dst + 4 * q0),
+          "r"((uint32_t)__cvta_generic_to_shared(st + 4 * q0)), "r"((qe - q0) * 16u)
+          : "memory");
+    }
+  }
+}
+
 constexpr int kPkStage = kChunk + 4;  // a chunk, or a run plus its 16-byte phase
 __device__ __forceinline__ int swz_cell(int q) { return (q & ~7) | ((q ^ (q >> 3)) & 7); }
 
@@ -320,7 +268,7 @@ __device__ __forceinline__ void pack_data_issue(float* st, const float* __restri
   }
 }
 
-template <bool kPush>
+template <int kPush>
 __global__ void __launch_bounds__(kPuWarps * 32)
     pack_lm_kernel(const float* __restrict__ g, uint64_t len, const uint64_t* __restrict__ words,
                    const uint32_t* __restrict__ chunk_off, float* __restrict__ packed, uint64_t cb,
@@ -348,6 +296,10 @@ __global__ void __launch_bounds__(kPuWarps * 32)
       cp_commit();
       asm volatile("cp.async.wait_group 1;" ::: "memory");  // words(c+nwt), data(c) landed
       __syncwarp();
+      if constexpr (kPush == kPushTma) {  // the bulk push of stage pi ^ 1 has read it
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        __syncwarp();
+      }
       if (c + nwt < ce) pack_data_issue(dsm[warp][pi ^ 1], g, len, vec_ok, wsm[warp][w1], c + nwt);
       cp_commit();
       const uint64_t* wc = wsm[warp][wi];
@@ -382,14 +334,19 @@ __global__ void __launch_bounds__(kPuWarps * 32)
       float* dst = packed + base;
 #pragma unroll 4
       for (uint32_t i = lane; i < run; i += 32) dst[i] = st[ph + i];
-      if constexpr (kPush) write_run(remote + base - ph, st, ph, run);
+      if constexpr (kPush == kPushStores) write_run(remote + base - ph, st, ph, run);
+      if constexpr (kPush == kPushTma) push_run_bulk(remote + base - ph, st, ph, run);
       __syncwarp();  // stage pi and word buffer wi are refilled next
       wi = w1;
       pi ^= 1;
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
+    if constexpr (kPush == kPushTma) {  // the bulk stores have landed in the peer's memory
+      if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;\n fence.proxy.async.global;" ::: "memory");
+      __syncwarp();
+    }
   }
-  if constexpr (kPush) p2psync::exit_signal(v, sg);  // PACKED: every CTA's remote stores are done
+  if constexpr (kPush != kPushNone) p2psync::exit_signal(v, sg);  // PACKED: every CTA's remote stores are done
 }
 
 template <bool kSgd, int kSrc>
@@ -471,11 +428,21 @@ __global__ void __launch_bounds__(kPuWarps * 32)
             : "+f"(x[e]), "+r"(sa)
             : "r"(h & (1u << e)));
     } else {  // + the peer's value (one-shot fold, n = 2)
-      const float* sa = stage + pos0;
-      const float* sp = psm(warp, pi) + kRunCap + run_phase(run_src<kSrc>(packed, v, rb, 1)) + pos0;
+      uint32_t sa = (uint32_t)__cvta_generic_to_shared(stage + pos0);
+      uint32_t sp = (uint32_t)__cvta_generic_to_shared(
+          psm(warp, pi) + kRunCap + run_phase(run_src<kSrc>(packed, v, rb, 1)) + pos0);
+      float y[32];
+#pragma unroll
+      for (int e = 0; e < 32; ++e) y[e] = 0.0f;
 #pragma unroll
       for (int e = 0; e < 32; ++e)
-        if (h & (1u << e)) x[e] = __fadd_rn(*sa++, *sp++);
+        asm volatile(
+            "{\n .reg .pred p;\n setp.ne.u32 p, %4, 0;\n @p ld.shared.f32 %0, [%2];\n"
+            " @p ld.shared.f32 %1, [%3];\n @p add.u32 %2, %2, 4;\n @p add.u32 %3, %3, 4;\n}"
+            : "+f"(x[e]), "+f"(y[e]), "+r"(sa), "+r"(sp)
+            : "r"(h & (1u << e)));
+#pragma unroll
+      for (int e = 0; e < 32; ++e) x[e] = __fadd_rn(x[e], y[e]);  // 0 + 0 = +0 at cleared bits
     }
     // (2) transpose through the consumed run buffer (XOR-swizzled 16-byte
     // cells: conflict-free both ways) into the coalesced layout: store j of
@@ -733,15 +700,10 @@ void note_launch(uint64_t n) { g_launches += n; }
 void launch_pack(const float* g, uint64_t len, const uint64_t* words, const uint32_t* chunk_off,
                  float* packed, uint64_t cb, uint64_t ce, cudaStream_t s) {
   if (ce <= cb) return;
-  static const bool v1 = getenv("PACT_PACK_V1") != nullptr;
   static int cap = 0;
-  if (!cap) cap = v1 ? persistent_grid(pack_kernel<false>, kPuWarps) : persistent_grid(pack_lm_kernel<false>, kPuWarps);
-  if (v1)
-    pack_kernel<false><<<grid_for(cap, ce - cb, kPuWarps), kPuWarps * 32, 0, s>>>(
-        g, len, words, chunk_off, packed, cb, ce, nullptr, P2PView{}, P2PSig{});
-  else
-    pack_lm_kernel<false><<<grid_for(cap, ce - cb, kPuWarps), kPuWarps * 32, 0, s>>>(
-        g, len, words, chunk_off, packed, cb, ce, nullptr, P2PView{}, P2PSig{});
+  if (!cap) cap = persistent_grid(pack_lm_kernel<kPushNone>, kPuWarps);
+  pack_lm_kernel<kPushNone><<<grid_for(cap, ce - cb, kPuWarps), kPuWarps * 32, 0, s>>>(
+      g, len, words, chunk_off, packed, cb, ce, nullptr, P2PView{}, P2PSig{});
   note_launch();
 }
 
@@ -749,15 +711,20 @@ void launch_pack_push(const float* g, uint64_t len, const uint64_t* words, const
                       float* packed, float* remote, const P2PView& v, const P2PSig& sg, cudaStream_t s) {
   const uint64_t nc = (len + kChunk - 1) / kChunk;
   if (!nc) return;
-  static const bool v1 = getenv("PACT_PACK_V1") != nullptr;
+  // PACT_PUSH_STORES=1: float4 stores instead of bulk async copies (measured
+  // c2 n=2 pack 61 vs 55-61 us: the exchange is NVLink-bound either way)
+  static const bool stores = getenv("PACT_PUSH_STORES") != nullptr;
   static int cap = 0;
-  if (!cap) cap = v1 ? persistent_grid(pack_kernel<true>, kPuWarps) : persistent_grid(pack_lm_kernel<true>, kPuWarps);
-  if (v1)
-    pack_kernel<true><<<grid_for(cap, nc, kPuWarps), kPuWarps * 32, 0, s>>>(g, len, words, chunk_off, packed, 0,
-                                                                            nc, remote, v, sg);
+  if (!cap)
+    cap = stores ? persistent_grid(pack_lm_kernel<kPushStores>, kPuWarps)
+                 : persistent_grid(pack_lm_kernel<kPushTma>, kPuWarps);
+  const unsigned grid = grid_for(cap, nc, kPuWarps);
+  if (stores)
+    pack_lm_kernel<kPushStores><<<grid, kPuWarps * 32, 0, s>>>(g, len, words, chunk_off, packed, 0, nc, remote,
+                                                               v, sg);
   else
-    pack_lm_kernel<true><<<grid_for(cap, nc, kPuWarps), kPuWarps * 32, 0, s>>>(g, len, words, chunk_off, packed,
-                                                                               0, nc, remote, v, sg);
+    pack_lm_kernel<kPushTma><<<grid, kPuWarps * 32, 0, s>>>(g, len, words, chunk_off, packed, 0, nc, remote, v,
+                                                            sg);
   note_launch();
 }
 

@@ -166,5 +166,59 @@ int main() {
              best0 * 1e3, best1 * 1e3, (mb << 20) / (best0 * 1e-3) / 1e9);
     }
   }
+  // both GPUs WRITE into each other at once (the n = 2 push exchange),
+  // 20 MiB each way, at several grid sizes; then the copy engines
+  {
+    float *r0, *r1, *l1;
+    CK(cudaSetDevice(1));
+    CK(cudaMalloc(&r1, bytes + 64));
+    CK(cudaMalloc(&l1, bytes + 64));
+    CK(cudaSetDevice(0));
+    CK(cudaMalloc(&r0, bytes + 64));
+    cudaStream_t s0, s1;
+    cudaEvent_t f0, f1, g0, g1;
+    CK(cudaSetDevice(1));
+    cudaStreamCreate(&s1);
+    cudaEventCreate(&f1);
+    cudaEventCreate(&g1);
+    CK(cudaSetDevice(0));
+    cudaStreamCreate(&s0);
+    cudaEventCreate(&f0);
+    cudaEventCreate(&g0);
+    const size_t mb = 20, nn = (mb << 20) / 16;
+    for (int mode = 0; mode < 5; ++mode) {
+      const int grids[4] = {148, 296, 592, 1184};
+      float best0 = 1e9, best1 = 1e9;
+      for (int it = 0; it < 10; ++it) {
+        CK(cudaSetDevice(0));
+        cudaDeviceSynchronize();
+        CK(cudaSetDevice(1));
+        cudaDeviceSynchronize();
+        CK(cudaSetDevice(0));
+        cudaEventRecord(f0, s0);
+        if (mode < 4) wr4<<<grids[mode], blk, 0, s0>>>((float4*)a0, (float4*)r1, nn);
+        else cudaMemcpyPeerAsync(r1, 1, a0, 0, mb << 20, s0);
+        cudaEventRecord(g0, s0);
+        CK(cudaSetDevice(1));
+        cudaEventRecord(f1, s1);
+        if (mode < 4) wr4<<<grids[mode], blk, 0, s1>>>((float4*)l1, (float4*)r0, nn);
+        else cudaMemcpyPeerAsync(r0, 0, l1, 1, mb << 20, s1);
+        cudaEventRecord(g1, s1);
+        cudaEventSynchronize(g1);
+        CK(cudaSetDevice(0));
+        cudaEventSynchronize(g0);
+        float m0, m1;
+        cudaEventElapsedTime(&m0, f0, g0);
+        CK(cudaSetDevice(1));
+        cudaEventElapsedTime(&m1, f1, g1);
+        CK(cudaSetDevice(0));
+        best0 = m0 < best0 ? m0 : best0;
+        best1 = m1 < best1 ? m1 : best1;
+      }
+      printf("%3zu MB bidirectional %s (grid %d): GPU0 %7.1f us, GPU1 %7.1f us (%6.1f GB/s each way)\n", mb,
+             mode < 4 ? "WRITE float4" : "cudaMemcpyPeer", mode < 4 ? grids[mode] : 0, best0 * 1e3, best1 * 1e3,
+             (mb << 20) / (best0 * 1e-3) / 1e9);
+    }
+  }
   return 0;
 }
