@@ -289,6 +289,9 @@ __global__ void __launch_bounds__(kPuWarps * 32)
     __syncwarp();
     pack_data_issue(dsm[warp][0], g, len, vec_ok, wsm[warp][0], c);
     cp_commit();
+    // lane-major rank of chunk i+1 computed during chunk i (as in unpack)
+    uint32_t h = reinterpret_cast<const uint32_t*>(wsm[warp][0])[lane];
+    uint32_t hc = __popc(h), incl = warp_incl_scan(hc);
     int wi = 0, pi = 0;
     for (; c < ce; c += nwt) {
       const int w1 = wi == 2 ? 0 : wi + 1, w2 = w1 == 2 ? 0 : w1 + 1;
@@ -305,9 +308,8 @@ __global__ void __launch_bounds__(kPuWarps * 32)
       const uint64_t* wc = wsm[warp][wi];
       const uint32_t base = reinterpret_cast<const uint32_t*>(wc + kChunkWords)[0];
       float* st = dsm[warp][pi];
-      const uint32_t h = reinterpret_cast<const uint32_t*>(wc)[lane];
-      const uint32_t hc = __popc(h);
-      const uint32_t incl = warp_incl_scan(hc);
+      const uint32_t h_n = reinterpret_cast<const uint32_t*>(wsm[warp][w1])[lane];  // chunk c + nwt
+      const uint32_t hc_n = __popc(h_n), incl_n = warp_incl_scan(hc_n);
       const uint32_t run = __shfl_sync(0xffffffffu, incl, 31);
       const uint32_t ph = (uint32_t)(((uintptr_t)(packed + base) >> 2) & 3u);
       // lane-major read of the lane's 32 elements (cells 8 l .. 8 l + 7)
@@ -339,6 +341,9 @@ __global__ void __launch_bounds__(kPuWarps * 32)
       __syncwarp();  // stage pi and word buffer wi are refilled next
       wi = w1;
       pi ^= 1;
+      h = h_n;
+      hc = hc_n;
+      incl = incl_n;
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
     if constexpr (kPush == kPushTma) {  // the bulk stores have landed in the peer's memory
@@ -391,6 +396,12 @@ __global__ void __launch_bounds__(kPuWarps * 32)
     issue_run<kSrc>(psm(warp, 0), packed, v, b, n);
   }
   cp_commit();
+  // (1') the chunk's lane-major rank, one chunk ahead: lane l owns the 32
+  // elements of mask half-word l, whose kept values are consecutive in the
+  // staged run from its warp rank. The scan of chunk i+1 is issued before
+  // chunk i's expansion so its shuffle latency overlaps that work.
+  uint32_t h = reinterpret_cast<const uint32_t*>(wsm[warp][0])[lane];
+  uint32_t pos0 = warp_incl_scan((uint32_t)__popc(h)) - (uint32_t)__popc(h);
   int wi = 0, pi = 0;
   for (; c < ce; c += nwt) {
     const int w1 = wi == 2 ? 0 : wi + 1, w2 = w1 == 2 ? 0 : w1 + 1;
@@ -407,14 +418,13 @@ __global__ void __launch_bounds__(kPuWarps * 32)
     const uint64_t* wc = wsm[warp][wi];
     const uint32_t rb = reinterpret_cast<const uint32_t*>(wsm[warp][wi] + kChunkWords)[0];
     const float* stage = psm(warp, pi) + run_phase(run_src<kSrc>(packed, v, rb, 0));
-    // (1) lane-major expansion: lane l owns the 32 elements of mask half-word
-    // l, whose kept values are consecutive in the staged run from its warp
-    // rank -- one scan per chunk instead of a rank per float4 slot
-    const uint32_t h = reinterpret_cast<const uint32_t*>(wc)[lane];
-    const uint32_t hc = __popc(h);
-    const uint32_t pos0 = warp_incl_scan(hc) - hc;
-    // 32-bit shared addresses walked by predicated increments: per element a
-    // bit test, a predicated LDS and a predicated add
+    const uint32_t h_n = reinterpret_cast<const uint32_t*>(wsm[warp][w1])[lane];  // chunk c + nwt
+    const uint32_t pos0_n = warp_incl_scan((uint32_t)__popc(h_n)) - (uint32_t)__popc(h_n);
+    // (1) lane-major expansion of chunk c: per element a bit test, a
+    // predicated LDS at the lane's walking 32-bit shared address and a
+    // predicated address increment. (Tried: unconditional loads at the
+    // walking address + a bit mask, which frees the loads from the
+    // predicate chain but puts all 32 lanes on the banks: c2 24.6 -> 28.6 us.)
     float x[32];
 #pragma unroll
     for (int e = 0; e < 32; ++e) x[e] = 0.0f;
@@ -428,21 +438,11 @@ __global__ void __launch_bounds__(kPuWarps * 32)
             : "+f"(x[e]), "+r"(sa)
             : "r"(h & (1u << e)));
     } else {  // + the peer's value (one-shot fold, n = 2)
-      uint32_t sa = (uint32_t)__cvta_generic_to_shared(stage + pos0);
-      uint32_t sp = (uint32_t)__cvta_generic_to_shared(
-          psm(warp, pi) + kRunCap + run_phase(run_src<kSrc>(packed, v, rb, 1)) + pos0);
-      float y[32];
-#pragma unroll
-      for (int e = 0; e < 32; ++e) y[e] = 0.0f;
+      const float* sa = stage + pos0;
+      const float* sp = psm(warp, pi) + kRunCap + run_phase(run_src<kSrc>(packed, v, rb, 1)) + pos0;
 #pragma unroll
       for (int e = 0; e < 32; ++e)
-        asm volatile(
-            "{\n .reg .pred p;\n setp.ne.u32 p, %4, 0;\n @p ld.shared.f32 %0, [%2];\n"
-            " @p ld.shared.f32 %1, [%3];\n @p add.u32 %2, %2, 4;\n @p add.u32 %3, %3, 4;\n}"
-            : "+f"(x[e]), "+f"(y[e]), "+r"(sa), "+r"(sp)
-            : "r"(h & (1u << e)));
-#pragma unroll
-      for (int e = 0; e < 32; ++e) x[e] = __fadd_rn(x[e], y[e]);  // 0 + 0 = +0 at cleared bits
+        if (h & (1u << e)) x[e] = __fadd_rn(*sa++, *sp++);
     }
     // (2) transpose through the consumed run buffer (XOR-swizzled 16-byte
     // cells: conflict-free both ways) into the coalesced layout: store j of
@@ -502,6 +502,8 @@ __global__ void __launch_bounds__(kPuWarps * 32)
     __syncwarp();  // run buffer `pi` and word buffer `wi` are refilled next
     wi = w1;
     pi ^= 1;
+    h = h_n;
+    pos0 = pos0_n;
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
   }
