@@ -225,10 +225,10 @@ def cpu_baseline_sample(shape, ratio, words_np, n):
 
 
 def main():
-    # the image sets NCCL_DEBUG=VERSION, which makes NCCL print its version to
-    # rank 0's stdout at communicator init; the contract is ONE JSON line
-    if os.environ.get("NCCL_DEBUG", "").upper() == "VERSION":
-        os.environ["NCCL_DEBUG"] = "WARN"
+    # the image sets NCCL_DEBUG=VERSION: NCCL prints its version (and any
+    # warnings) to stdout at communicator init; the contract is ONE JSON line
+    # on stdout, so NCCL's log goes to stderr instead
+    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
@@ -239,7 +239,7 @@ def main():
     ap.add_argument("--bucket-mb", type=float, default=None)
     ap.add_argument("--transport", default="auto", choices=["auto", "nccl", "p2p"],
                     help="packed exchange for N > 1: NCCL allreduce or the fused NVLink P2P path")
-    ap.add_argument("--path", default="masked", choices=["masked", "ternary", "fp16", "fp16-packed", "topk"],
+    ap.add_argument("--path", default="masked", choices=["masked", "ternary", "fp16", "fp16-packed", "topk", "sweep"],
                     help="masked: the headline (masked_allreduce); the others time the SURVEY 8f rows "
                          "on the same workload (ternary_allgather_aggregate, fp16_allreduce, "
                          "masked_allreduce on the binary16 wire, topk_allgather_aggregate)")
@@ -336,6 +336,8 @@ def main():
         torch.cuda.synchronize()
         return [a.elapsed_time(b) * 1e-3 for a, b in evs]
 
+    if args.path == "sweep":
+        return run_sweep(args, pb, torch, comm, rank, world, local, dev, cfg, model, n, weights, grad, out, timed)
     if args.path != "masked":
         return run_path(args, pb, torch, comm, rank, world, local, dev, cfg, model, ratio, shape, n, nnz, mask,
                         tracker, grad, out, timed, barrier)
@@ -469,6 +471,65 @@ def main():
             "roofline": roofline, "stages": stages, **({"allreduce": extra} if extra else {}),
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if comm is not None:
+        torch.distributed.barrier()
+        comm.close()
+        torch.distributed.destroy_process_group()
+
+
+SWEEP_RATIOS = (0.5, 0.6, 0.7, 0.8, 0.9, 0.95, 0.99)
+
+
+def run_sweep(args, pb, torch, comm, rank, world, local, dev, cfg, model, n, weights, grad, out, timed):
+    """BASELINE config 4: the sparsity sweep exercising the adaptive
+    dense/sparse switch. The threshold is MEASURED (pact_calibrate_density on
+    this communicator and length, synthetic inputs), then at each ratio the
+    packed path, the dense path and the auto policy are timed on the
+    workload's own mask (L2 flushed, CUDA events, max over ranks)."""
+    cal = pb.calibrate_density(n, comm)
+    auto = pb.SyncPolicy(density_threshold=cal.threshold)
+    packed_pol, dense_pol = pb.SyncPolicy(), pb.SyncPolicy(density_threshold=1e-300)
+    k = max(3, min(args.steps, 10))
+
+    def tmax(x):
+        if world > 1:
+            tt = torch.tensor([x], dtype=torch.float64, device=dev)
+            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+            x = float(tt.item())
+        return x
+
+    rows, gbs = [], []
+    for ratio in SWEEP_RATIOS:
+        m = pb.magnitude_prune(weights, ratio)
+        res = {}
+        for name, pol in (("packed", packed_pol), ("dense", dense_pol), ("auto", auto)):
+            def st(i, pol=pol):
+                return pb.masked_allreduce(grad, m, pb.TrackerStatus.Stable, i, comm, policy=pol, out=out)
+            for i in range(2):
+                r = st(i)
+            res[name] = (tmax(statistics.median(timed(st, k))), r.stats.mode_used)
+        best = min(res["packed"][0], res["dense"][0])
+        gbs.append(4.0 * n * world / res["auto"][0] / 1e9)
+        rows.append({"ratio": ratio, "density": round(m.nnz() / n, 6),
+                     "packed_us": round(res["packed"][0] * 1e6, 1), "dense_us": round(res["dense"][0] * 1e6, 1),
+                     "auto_us": round(res["auto"][0] * 1e6, 1),
+                     "auto_mode": "packed" if res["auto"][1] == pb.SyncMode.PackedAllReduce else "dense",
+                     "auto_vs_best": round(res["auto"][0] / best, 3)})
+    if rank == 0:
+        geo = math.exp(sum(math.log(x) for x in gbs) / len(gbs))
+        line = {
+            "metric": METRIC.replace("prune+pack+allreduce+unpack", "adaptive policy sweep, geomean"),
+            "value": round(geo, 2), "unit": "GB/s", "n_gpus": world, "steps": k, "warmup": 2,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic", "path": "sweep",
+            "config": {"workload": f"{cfg}:{model} fp32 grads, magnitude masks at ratios {list(SWEEP_RATIOS)}",
+                       "len": n, "l2": "flushed before every timed step", "parallelism": f"dp{world}"},
+            "calibration": {"threshold_density": round(cal.threshold, 4), "probe_densities": cal.densities,
+                            "t_packed_us": [round(t * 1e6, 1) for t in cal.t_packed],
+                            "t_dense_us": round(cal.t_dense * 1e6, 1)},
+            "sweep": rows,
         }
         print(json.dumps(line), flush=True)
     if comm is not None:

@@ -319,6 +319,20 @@ pact_status pact_masked_allreduce(pact_comm* c, pact_ctx* ctx, const float* grad
                                   const uint64_t* advertised_digest, const pact_policy* policy,
                                   float* out, pact_sync_stats* stats, pact_stream_t stream);
 
+/* Adaptive dense/sparse policy, measured (north_star (4)): times
+ * pact_masked_allreduce's packed path at each probe density (a magnitude
+ * mask of synthetic weights at ratio 1 - d) against its dense path, for this
+ * communicator and length, max over ranks, and returns the crossover density
+ * (linear interpolation between the last winning and first losing probe; 1.0
+ * when packing always wins). Feed it to policy->density_threshold. densities
+ * may be NULL (a default grid 0.01 .. 0.95); t_packed_out (ndens entries) and
+ * t_dense_out may be NULL. Collective (same arguments on every rank);
+ * allocates 12 * len bytes of scratch for its duration. c may be NULL (the
+ * single-GPU path, where nothing is exchanged). */
+pact_status pact_calibrate_density(pact_comm* c, pact_ctx* ctx, uint64_t len, const pact_policy* policy,
+                                   const double* densities, int ndens, double* t_packed_out,
+                                   double* t_dense_out, double* threshold_out, pact_stream_t stream);
+
 /* Same as pact_masked_allreduce on HOST fp32 buffers: H2D of grad, device
  * sync path, D2H of the result (pinned staging owned by ctx). Synchronous. */
 pact_status pact_masked_allreduce_host(pact_comm* c, pact_ctx* ctx, const float* grad_host,

@@ -98,6 +98,8 @@ SIGNATURES = {
     "pact_full_allreduce": (C.c_int, [vp, vp, vp, C.c_uint64, C.c_float, C.POINTER(SyncStatsC), vp]),
     "pact_masked_allreduce": (C.c_int, [vp, vp, vp, C.c_uint64, vp, C.c_int, C.c_uint32, u64p,
                                         C.POINTER(PolicyC), vp, C.POINTER(SyncStatsC), vp]),
+    "pact_calibrate_density": (C.c_int, [vp, vp, C.c_uint64, C.POINTER(PolicyC), C.POINTER(C.c_double), C.c_int,
+                                         C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_double), vp]),
     "pact_topk_count": (C.c_int, [C.c_uint64, C.c_float, u64p]),
     "pact_topk_select": (C.c_int, [vp, vp, C.c_uint64, C.c_float, vp, vp, u64p, vp]),
     "pact_topk_densify": (C.c_int, [vp, vp, vp, C.c_uint64, C.c_uint64, vp, vp]),

@@ -20,7 +20,7 @@ from __future__ import annotations
 import ctypes as C
 import enum
 from dataclasses import dataclass, field
-from typing import Optional, Sequence, Tuple
+from typing import List, Optional, Sequence, Tuple
 
 import torch
 
@@ -704,6 +704,33 @@ def masked_allreduce(grad: torch.Tensor, mask: SparsityMask, tracker: TrackerSta
           _ptr(g), g.numel(), mask.handle, int(tracker == TrackerStatus.Stable), int(epoch),
           C.byref(adv) if adv is not None else None, C.byref(pol), _ptr(o), C.byref(st), _stream())
     return AggregateResult(o, _stats(st))
+
+
+@dataclass
+class DensityCalibration:
+    """pact_calibrate_density: the measured dense/sparse crossover."""
+    threshold: float              # feed to SyncPolicy.density_threshold (1.0: packing always wins)
+    densities: List[float]
+    t_packed: List[float]         # seconds per masked_allreduce at each probe density (max over ranks)
+    t_dense: float                # seconds per dense masked_allreduce (max over ranks)
+
+
+def calibrate_density(length: int, comm: Optional[Comm], policy: Optional[SyncPolicy] = None,
+                      densities: Optional[Sequence[float]] = None,
+                      ctx: Optional["Context"] = None) -> DensityCalibration:
+    """The adaptive policy's crossover density, measured on this communicator
+    for gradients of `length` elements (north_star (4)). Collective:
+    call on every rank with the same arguments."""
+    ctx = ctx or (comm.ctx if comm is not None else Context.get())
+    ds = list(densities) if densities is not None else [0.01, 0.02, 0.05, 0.1, 0.2, 0.3, 0.4, 0.5, 0.6, 0.7,
+                                                         0.8, 0.9, 0.95]
+    dv = (C.c_double * len(ds))(*ds)
+    tp = (C.c_double * len(ds))()
+    td, thr = C.c_double(), C.c_double()
+    pol = (policy or SyncPolicy()).c()
+    _call(lib.pact_calibrate_density, comm.handle if comm is not None else None, ctx.handle, int(length),
+          C.byref(pol), dv, len(ds), tp, C.byref(td), C.byref(thr), _stream())
+    return DensityCalibration(thr.value, ds, list(tp), td.value)
 
 
 def masked_allreduce_host(grad_host: torch.Tensor, mask: SparsityMask, tracker: TrackerStatus,

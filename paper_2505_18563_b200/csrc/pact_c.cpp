@@ -2003,6 +2003,117 @@ pact_status pact_masked_allreduce(pact_comm* c, pact_ctx* ctx, const float* grad
   return PACT_OK;
 }
 
+// ------------------------------------------------ density calibration (D2)
+
+// The adaptive policy's threshold, measured (north_star (4): "falls back to a
+// dense allreduce when the measured density makes packing unprofitable").
+// Times the packed path (prune -> pack -> exchange -> unpack, the same
+// masked_allreduce the caller runs) at each probe density against the dense
+// path, on synthetic inputs of the caller's length, takes the max over ranks
+// and interpolates the crossover. Collective: every rank calls it with the
+// same arguments (all votes stay in step).
+pact_status pact_calibrate_density(pact_comm* c, pact_ctx* ctx, uint64_t len, const pact_policy* policy,
+                                   const double* densities, int ndens, double* t_packed_out,
+                                   double* t_dense_out, double* threshold_out, pact_stream_t stream) {
+  static const double kGrid[] = {0.01, 0.02, 0.05, 0.1, 0.2, 0.3, 0.4, 0.5, 0.6, 0.7, 0.8, 0.9, 0.95};
+  if (!ctx || !threshold_out) return fail(PACT_E_INVALID_ARG, "null ctx/threshold");
+  if (c && c->ctx != ctx) return fail(PACT_E_INVALID_ARG, "comm belongs to another ctx");
+  if (len < 1024) return fail(PACT_E_INVALID_ARG, "calibration needs len >= 1024");
+  if (!densities) {
+    densities = kGrid;
+    ndens = (int)(sizeof(kGrid) / sizeof(kGrid[0]));
+  }
+  if (ndens <= 0 || ndens > 64) return fail(PACT_E_INVALID_ARG, "1..64 probe densities");
+  for (int i = 0; i < ndens; ++i)
+    if (!(densities[i] > 0.0 && densities[i] < 1.0) || (i && densities[i] <= densities[i - 1]))
+      return fail(PACT_E_INVALID_ARG, "densities must increase strictly inside (0, 1)");
+  TRY(set_device(ctx));
+  cudaStream_t s = stream;
+  DevBuf w, g, out, tv;
+  TRY(w.ensure(len * 4));
+  TRY(g.ensure(len * 4));
+  TRY(out.ensure(len * 4));
+  TRY(tv.ensure((ndens + 1) * 4));
+  pact_mask* m = nullptr;
+  pact_status st = PACT_OK;
+  std::vector<float> t(ndens + 1, 0.0f);
+  cudaEvent_t a = nullptr, b = nullptr;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  pact_policy pol{};
+  if (policy) pol = *policy;
+  pol.time_stages = 0;
+  auto timed = [&](pact_policy* p, float* best) -> pact_status {
+    *best = 1e30f;
+    for (int r = 0; r < 4; ++r) {  // one warm-up, min of three
+      if (c) TRY(pact_allreduce_sum(c, tv.as<float>(), tv.as<float>(), 1, s));  // device-side rank alignment
+      CUDA_TRY(cudaEventRecord(a, s));
+      TRY(pact_masked_allreduce(c, ctx, g.as<float>(), len, m, 1, (uint32_t)r, nullptr, p, out.as<float>(),
+                                nullptr, s));
+      CUDA_TRY(cudaEventRecord(b, s));
+      CUDA_TRY(cudaEventSynchronize(b));
+      float ms = 0;
+      cudaEventElapsedTime(&ms, a, b);
+      if (r && ms < *best) *best = ms;
+    }
+    return PACT_OK;
+  };
+  do {
+    if ((st = pact_synth_fill(ctx, w.as<float>(), len, 0x43414c49ull, 0, 1, 1.0f, s)) != PACT_OK) break;
+    if ((st = pact_synth_fill(ctx, g.as<float>(), len, 0x47524144ull + (c ? c->rank : 0), 0, 3, 1.0f, s)) !=
+        PACT_OK)
+      break;
+    if ((st = pact_mask_create(ctx, len, &m)) != PACT_OK) break;
+    for (int i = 0; i <= ndens && st == PACT_OK; ++i) {
+      const double d = i < ndens ? densities[i] : densities[ndens - 1];
+      if (i < ndens) {
+        if ((st = pact_prune_magnitude(ctx, w.as<float>(), len, (float)(1.0 - d), m, s, nullptr)) != PACT_OK)
+          break;
+        pol.density_threshold = 0.0;  // packed
+      } else {
+        pol.density_threshold = 1e-300;  // any density is above it: the dense path
+      }
+      st = timed(&pol, &t[i]);
+    }
+  } while (false);
+  if (st == PACT_OK) {  // max over ranks: every rank takes the same decision
+    cudaMemcpyAsync(tv.as<float>(), t.data(), (ndens + 1) * 4, cudaMemcpyHostToDevice, s);
+    if (c && ncclAllReduce(tv.as<float>(), tv.as<float>(), ndens + 1, ncclFloat32, ncclMax, c->nccl, s) !=
+                 ncclSuccess)
+      st = fail(PACT_E_NCCL, "calibration max-reduce");
+    cudaMemcpyAsync(t.data(), tv.as<float>(), (ndens + 1) * 4, cudaMemcpyDeviceToHost, s);
+    if (cudaStreamSynchronize(s) != cudaSuccess && st == PACT_OK) st = fail(PACT_E_CUDA, "calibration readback");
+  }
+  if (m) pact_mask_destroy(m);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  w.release();
+  g.release();
+  out.release();
+  tv.release();
+  if (st != PACT_OK) return st;
+  const double td = t[ndens];
+  // crossover: the first probe where packing loses, interpolated against the
+  // previous (winning) probe; packing wins everywhere -> 1 (never fall back)
+  double thr = 1.0;
+  for (int i = 0; i < ndens; ++i) {
+    if (t[i] >= td) {
+      if (i == 0) {
+        thr = densities[0] * 0.5;  // dense wins even at the sparsest probe
+      } else {
+        const double d0 = densities[i - 1], d1 = densities[i], t0 = t[i - 1], t1 = t[i];
+        thr = t1 > t0 ? d0 + (d1 - d0) * (td - t0) / (t1 - t0) : d0;
+      }
+      break;
+    }
+  }
+  for (int i = 0; i < ndens; ++i)
+    if (t_packed_out) t_packed_out[i] = t[i] * 1e-3;
+  if (t_dense_out) *t_dense_out = td * 1e-3;
+  *threshold_out = thr;
+  return PACT_OK;
+}
+
 // ------------------------------------------------------------ ternary
 
 uint64_t pact_ternary_sign_bytes(uint64_t count) { return 4 * ((count + 15) / 16); }

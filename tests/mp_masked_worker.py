@@ -209,6 +209,22 @@ def main():
     check("topk: bytes", rk.stats.bytes_on_wire == (world - 1) * (26 + 8 * sel[0][0].size))
     check("topk: mode", rk.stats.mode_used == pb.SyncMode.TopKAllGather)
 
+    # ---- measured dense/sparse crossover: unanimous threshold,
+    # and the policy it feeds picks packed below / dense above it
+    cal = pb.calibrate_density(1 << 22, comm, densities=[0.05, 0.3, 0.6, 0.9])
+    th = torch.tensor([cal.threshold], dtype=torch.float64, device=dev)
+    ths = [torch.empty_like(th) for _ in range(world)]
+    dist.all_gather(ths, th)
+    check("calibrate: same threshold on every rank", all(float(x) == cal.threshold for x in ths))
+    check("calibrate: timings", len(cal.t_packed) == 4 and all(t > 0 for t in cal.t_packed) and cal.t_dense > 0)
+    check("calibrate: threshold in (0, 1]", 0.0 < cal.threshold <= 1.0)
+    pol = pb.SyncPolicy(density_threshold=min(cal.threshold, 0.999))
+    g = torch.from_numpy(grads[rank][:n].copy()).to(dev)
+    r = pb.masked_allreduce(g, mask, pb.TrackerStatus.Stable, 1, comm, policy=pol)
+    dens = mask.nnz() / n
+    want_mode = pb.SyncMode.PackedAllReduce if dens <= pol.density_threshold else pb.SyncMode.FullAllReduce
+    check("calibrate: policy decision follows the threshold", r.stats.mode_used == want_mode)
+
     flag = torch.tensor([len(failures)], device=dev)
     dist.all_reduce(flag)
     comm.close()

@@ -301,6 +301,19 @@ def test_dense_fallback_gse(pb, port, cuda):
         assert np.array_equal(u32(r.tensor.cpu().numpy()), want), status
 
 
+def test_calibrate_density_single_gpu(pb, cuda):
+    """pact_calibrate_density on one GPU: well-formed timings; with nothing
+    to exchange the dense path (a copy) beats pack + unpack at every density,
+    so the measured crossover sits below the sparsest probe."""
+    cal = pb.calibrate_density(1 << 21, None, densities=[0.1, 0.5, 0.9])
+    assert len(cal.t_packed) == 3 and all(t > 0 for t in cal.t_packed) and cal.t_dense > 0
+    assert 0.0 < cal.threshold <= 1.0
+    if cal.t_packed[0] >= cal.t_dense:
+        assert cal.threshold == pytest.approx(0.05)
+    with pytest.raises(pb.Error):
+        pb.calibrate_density(1 << 20, None, densities=[0.5, 0.2])
+
+
 @pytest.mark.parametrize("src_len", [1, 64, 1000, 4096 * 3 + 17, 2_000_003])
 def test_mask_gather(pb, cuda, src_len):
     """pact_mask_gather == numpy bit slicing/concatenation (DDP bucket masks)."""
