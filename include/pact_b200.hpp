@@ -401,14 +401,16 @@ class Comm {  // collective.hpp:89-116, NCCL-backed
   std::unique_ptr<pact_comm, Del> c_;
 };
 
-// collective.cpp:269-309; returns the SUM
+// collective.cpp:269-309; returns the SUM. `policy` (extension):
+// the adaptive knobs, e.g. density_threshold from calibrate_density.
 inline AggregateResult masked_allreduce(const FlatTensor& grad, const SparsityMask& mask,
                                         TrackerStatus tracker, uint32_t epoch, Comm& comm,
-                                        std::optional<uint64_t> advertised_digest = {}) {
+                                        std::optional<uint64_t> advertised_digest = {},
+                                        const pact_policy& policy = pact_policy{}) {
   if (grad.size() != mask.size()) throw Error(Errc::ShapeMismatch, "gradient/mask length mismatch");
   std::vector<float> out(grad.size());
   pact_sync_stats st{};
-  pact_policy pol{};
+  pact_policy pol = policy;
   uint64_t adv = advertised_digest.value_or(0);
   detail::check(pact_masked_allreduce_host(comm.handle(), detail::ctx(), grad.data(), grad.size(),
                                            mask.handle(), tracker == TrackerStatus::Stable, epoch,
@@ -416,6 +418,16 @@ inline AggregateResult masked_allreduce(const FlatTensor& grad, const SparsityMa
                                            nullptr));
   return {FlatTensor(std::move(out)),
           {st.bytes_on_wire, st.seconds, static_cast<SyncMode>(st.mode_used)}};
+}
+
+// Extension (north_star (4)): the measured crossover density above which
+// the dense allreduce is faster than pack -> packed allreduce -> unpack on
+// this communicator for gradients of `len` elements. Collective.
+inline double calibrate_density(Comm& comm, size_t len) {
+  double thr = 1.0;
+  detail::check(pact_calibrate_density(comm.handle(), detail::ctx(), len, nullptr, nullptr, 0, nullptr, nullptr,
+                                       &thr, nullptr));
+  return thr;
 }
 
 // collective.cpp:253-259; returns the SUM

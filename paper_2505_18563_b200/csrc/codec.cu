@@ -55,6 +55,16 @@ int persistent_grid(K kernel, int warps = kCodecWarps) {
   return sm_count() * per_sm;
 }
 
+// persistent grid of a kernel with `dyn` bytes of dynamic shared memory (opted in above 48 KiB)
+template <typename K>
+int persistent_grid_dyn(K kernel, int warps, int dyn) {
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, warps * 32, dyn);
+  if (per_sm <= 0) per_sm = 1;
+  return sm_count() * per_sm;
+}
+
 unsigned grid_for(int cap, uint64_t chunks, int warps = kCodecWarps) {
   const uint64_t need = (chunks + warps - 1) / warps;
   return (unsigned)(need < (uint64_t)cap ? need : (uint64_t)cap);
@@ -354,21 +364,29 @@ __global__ void __launch_bounds__(kPuWarps * 32)
   if constexpr (kPush != kPushNone) p2psync::exit_signal(v, sg);  // PACKED: every CTA's remote stores are done
 }
 
-template <bool kSgd, int kSrc>
+// kA = packed runs in flight ahead of the expansion. 2 halves the exposed
+// run latency but costs a third more shared memory (16 instead of 24 warps
+// per SM): it wins once each warp has many chunks (c3 unpack 111 -> 104 us,
+// c5 290 -> 262 us) and loses on short grids (c2 24.6 -> 26.6 us), so the
+// launcher picks by chunks per warp. The pair variant keeps 1 (two runs
+// per stage).
+template <int kSrc, int kA>
+__host__ __device__ constexpr int unpack_smem_bytes() {
+  return kPuWarps * (kA + 1) * (kSrc == kSrcPair ? 2 : 1) * kRunCap * (int)sizeof(float);
+}
+
+template <bool kSgd, int kSrc, int kA>
 __global__ void __launch_bounds__(kPuWarps * 32)
     unpack_kernel(const float* __restrict__ packed, uint64_t len, const uint64_t* __restrict__ words,
                   const uint32_t* __restrict__ chunk_off, float scale, int do_scale,
                   float* __restrict__ out, float lr, float* __restrict__ weights, uint64_t cb,
                   uint64_t ce, P2PView v, const uint64_t* __restrict__ flags, uint64_t target,
                   int* __restrict__ err, P2PSig sg) {
-  // packed-run stages: static, except the pair variant's two runs per stage
-  // (64 KiB per CTA, dynamic shared memory)
+  constexpr int kRS = kA + 1, kWS = kA + 2;  // run / word stages
   constexpr int kRun = kSrc == kSrcPair ? 2 * kRunCap : kRunCap;
-  __shared__ __align__(16) float st_psm[kSrc == kSrcPair ? 4 : kPuWarps * 2 * kRun];
-  extern __shared__ __align__(16) float dyn_psm[];
-  float* const psm_base = kSrc == kSrcPair ? dyn_psm : st_psm;
-  auto psm = [&](int w, int st) { return psm_base + (w * 2 + st) * kRun; };
-  __shared__ __align__(16) uint64_t wsm[kPuWarps][3][kWbuf];
+  extern __shared__ __align__(16) float psm_base[];  // unpack_smem_bytes<kSrc, kA>()
+  auto psm = [&](int w, int st) { return psm_base + (w * kRS + st) * kRun; };
+  __shared__ __align__(16) uint64_t wsm[kPuWarps][kWS][kWbuf];
   if constexpr (kSrc != kSrcLocal) {  // peers' PACKED (one-shot) / REDUCED (two-shot) flags
     p2psync::entry_signal(v, sg);
     p2psync::block_wait_flags(flags, kSrc == kSrcPair ? kP2PPacked : kP2PReduced, v.n, target, err);
@@ -383,19 +401,23 @@ __global__ void __launch_bounds__(kPuWarps * 32)
     b = o[0];
     n = o[2] - o[0];
   };
-  // prologue: words(c0), words(c1), run(c0)
-  offs_words_issue(wsm[warp][0], words, chunk_off, c);
-  cp_commit();
-  if (c + nwt < ce) offs_words_issue(wsm[warp][1], words, chunk_off, c + nwt);
-  cp_commit();
-  asm volatile("cp.async.wait_group 1;" ::: "memory");
-  __syncwarp();
-  {
-    uint32_t b, n;
-    offs(0, b, n);
-    issue_run<kSrc>(psm(warp, 0), packed, v, b, n);
+  // cp.async groups, in commit order: words w0..w_kA, runs r0..r_{kA-1};
+  // then per chunk i: w_{i+kA+1}, r_{i+kA}. At chunk i, waiting for all but
+  // the newest kA groups leaves exactly r_i and w_{i+kA} landed.
+  for (int j = 0; j <= kA; ++j) {
+    if (c + j * nwt < ce) offs_words_issue(wsm[warp][j], words, chunk_off, c + j * nwt);
+    cp_commit();
   }
-  cp_commit();
+  asm volatile("cp.async.wait_group 1;" ::: "memory");  // w0 .. w_{kA-1}
+  __syncwarp();
+  for (int j = 0; j < kA; ++j) {
+    if (c + j * nwt < ce) {
+      uint32_t b, n;
+      offs(j, b, n);
+      issue_run<kSrc>(psm(warp, j), packed, v, b, n);
+    }
+    cp_commit();
+  }
   // (1') the chunk's lane-major rank, one chunk ahead: lane l owns the 32
   // elements of mask half-word l, whose kept values are consecutive in the
   // staged run from its warp rank. The scan of chunk i+1 is issued before
@@ -404,15 +426,15 @@ __global__ void __launch_bounds__(kPuWarps * 32)
   uint32_t pos0 = warp_incl_scan((uint32_t)__popc(h)) - (uint32_t)__popc(h);
   int wi = 0, pi = 0;
   for (; c < ce; c += nwt) {
-    const int w1 = wi == 2 ? 0 : wi + 1, w2 = w1 == 2 ? 0 : w1 + 1;
-    if (c + 2 * nwt < ce) offs_words_issue(wsm[warp][w2], words, chunk_off, c + 2 * nwt);
+    const int w1 = (wi + 1) % kWS, wa = (wi + kA) % kWS, wa1 = (wi + kA + 1) % kWS, pa = (pi + kA) % kRS;
+    if (c + (kA + 1) * nwt < ce) offs_words_issue(wsm[warp][wa1], words, chunk_off, c + (kA + 1) * nwt);
     cp_commit();
-    asm volatile("cp.async.wait_group 1;" ::: "memory");  // words(c+nwt), run(c) landed
+    asm volatile("cp.async.wait_group %0;" ::"n"(kA) : "memory");  // run(c), words(c + kA nwt) landed
     __syncwarp();
-    if (c + nwt < ce) {
+    if (c + kA * nwt < ce) {
       uint32_t b, n;
-      offs(w1, b, n);
-      issue_run<kSrc>(psm(warp, pi ^ 1), packed, v, b, n);
+      offs(wa, b, n);
+      issue_run<kSrc>(psm(warp, pa), packed, v, b, n);
     }
     cp_commit();
     const uint64_t* wc = wsm[warp][wi];
@@ -501,7 +523,7 @@ __global__ void __launch_bounds__(kPuWarps * 32)
     }
     __syncwarp();  // run buffer `pi` and word buffer `wi` are refilled next
     wi = w1;
-    pi ^= 1;
+    pi = pi + 1 == kRS ? 0 : pi + 1;
     h = h_n;
     pos0 = pos0_n;
   }
@@ -730,15 +752,34 @@ void launch_pack_push(const float* g, uint64_t len, const uint64_t* words, const
   note_launch();
 }
 
+namespace {
+// chunks per warp of the one-run-ahead grid above which two runs ahead win
+constexpr uint64_t kDeepUnpackChunksPerWarp = 16;
+template <bool kSgd>
+void unpack_local(const float* packed, uint64_t len, const uint64_t* words, const uint32_t* chunk_off, float scale,
+                  int do_scale, float* out, float lr, float* weights, uint64_t cb, uint64_t ce, cudaStream_t s) {
+  constexpr int kDyn1 = unpack_smem_bytes<kSrcLocal, 1>(), kDyn2 = unpack_smem_bytes<kSrcLocal, 2>();
+  static int cap1 = 0, cap2 = 0;
+  if (!cap1) {
+    cap1 = persistent_grid_dyn(unpack_kernel<kSgd, kSrcLocal, 1>, kPuWarps, kDyn1);
+    cap2 = persistent_grid_dyn(unpack_kernel<kSgd, kSrcLocal, 2>, kPuWarps, kDyn2);
+  }
+  if ((ce - cb) >= kDeepUnpackChunksPerWarp * (uint64_t)cap1 * kPuWarps)
+    unpack_kernel<kSgd, kSrcLocal, 2><<<grid_for(cap2, ce - cb, kPuWarps), kPuWarps * 32, kDyn2, s>>>(
+        packed, len, words, chunk_off, scale, do_scale, out, lr, weights, cb, ce, P2PView{}, nullptr, 0, nullptr,
+        P2PSig{});
+  else
+    unpack_kernel<kSgd, kSrcLocal, 1><<<grid_for(cap1, ce - cb, kPuWarps), kPuWarps * 32, kDyn1, s>>>(
+        packed, len, words, chunk_off, scale, do_scale, out, lr, weights, cb, ce, P2PView{}, nullptr, 0, nullptr,
+        P2PSig{});
+}
+}  // namespace
+
 void launch_unpack(const float* packed, uint64_t len, const uint64_t* words,
                    const uint32_t* chunk_off, float scale, int do_scale, float* out, uint64_t cb,
                    uint64_t ce, cudaStream_t s) {
   if (ce <= cb) return;
-  static int cap = 0;
-  if (!cap) cap = persistent_grid(unpack_kernel<false, kSrcLocal>, kPuWarps);
-  unpack_kernel<false, kSrcLocal><<<grid_for(cap, ce - cb, kPuWarps), kPuWarps * 32, 0, s>>>(
-      packed, len, words, chunk_off, scale, do_scale, out, 0.f, nullptr, cb, ce, P2PView{}, nullptr, 0,
-      nullptr, P2PSig{});
+  unpack_local<false>(packed, len, words, chunk_off, scale, do_scale, out, 0.f, nullptr, cb, ce, s);
   note_launch();
 }
 
@@ -751,21 +792,17 @@ void launch_unpack_p2p(const float* packed_local, uint64_t len, const uint64_t* 
   // every CTA runs the flag wait and the exit count, so each gets >= 1 chunk
   // per warp 0 (grid <= ceil(nc / kPuWarps))
   if (!two_shot) {
-    constexpr int kDyn = kPuWarps * 2 * 2 * kRunCap * sizeof(float);
+    constexpr int kDyn = unpack_smem_bytes<kSrcPair, 1>();
     static int cap = 0;
-    if (!cap) {
-      cudaFuncSetAttribute(unpack_kernel<false, kSrcPair>, cudaFuncAttributeMaxDynamicSharedMemorySize, kDyn);
-      int per_sm = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, unpack_kernel<false, kSrcPair>, kPuWarps * 32, kDyn);
-      cap = sm_count() * (per_sm > 0 ? per_sm : 1);
-    }
-    unpack_kernel<false, kSrcPair><<<grid_for(cap, nc, kPuWarps), kPuWarps * 32, kDyn, s>>>(
+    if (!cap) cap = persistent_grid_dyn(unpack_kernel<false, kSrcPair, 1>, kPuWarps, kDyn);
+    unpack_kernel<false, kSrcPair, 1><<<grid_for(cap, nc, kPuWarps), kPuWarps * 32, kDyn, s>>>(
         packed_local, len, words, chunk_off, scale, do_scale, out, 0.f, nullptr, 0, nc, v, flags, target,
         err, sg);
   } else {
     static int cap = 0;
-    if (!cap) cap = persistent_grid(unpack_kernel<false, kSrcOwner>, kPuWarps);
-    unpack_kernel<false, kSrcOwner><<<grid_for(cap, nc, kPuWarps), kPuWarps * 32, 0, s>>>(
+    constexpr int kDyn = unpack_smem_bytes<kSrcOwner, 1>();
+    if (!cap) cap = persistent_grid_dyn(unpack_kernel<false, kSrcOwner, 1>, kPuWarps, kDyn);
+    unpack_kernel<false, kSrcOwner, 1><<<grid_for(cap, nc, kPuWarps), kPuWarps * 32, kDyn, s>>>(
         packed_local, len, words, chunk_off, scale, do_scale, out, 0.f, nullptr, 0, nc, v, flags, target,
         err, sg);
   }
@@ -777,11 +814,7 @@ void launch_unpack_sgd(const float* packed, uint64_t len, const uint64_t* words,
                        float* grad_out, float* weights, cudaStream_t s) {
   const uint64_t nc = (len + kChunk - 1) / kChunk;
   if (!nc) return;
-  static int cap = 0;
-  if (!cap) cap = persistent_grid(unpack_kernel<true, kSrcLocal>, kPuWarps);
-  unpack_kernel<true, kSrcLocal><<<grid_for(cap, nc, kPuWarps), kPuWarps * 32, 0, s>>>(
-      packed, len, words, chunk_off, scale, do_scale, grad_out, lr, weights, 0, nc, P2PView{}, nullptr, 0,
-      nullptr, P2PSig{});
+  unpack_local<true>(packed, len, words, chunk_off, scale, do_scale, grad_out, lr, weights, 0, nc, s);
   note_launch();
 }
 
