@@ -114,8 +114,8 @@ typedef struct pact_sync_stats {
  * never fall back on density, one bucket. */
 typedef struct pact_policy {
   double density_threshold; /* fall back to dense when agreed nnz/len > this; <=0 or >=1: never */
-  uint64_t bucket_bytes;    /* packed bytes per bucket; 0 = auto (NCCL: one bucket up to
-                               64 MiB packed, 32 MiB buckets above; P2P: one bucket) */
+  uint64_t bucket_bytes;    /* packed bytes per bucket; 0 = auto = one bucket (measured
+                               faster than pipelined buckets on B200) */
   float scale;              /* applied in unpack; 0 => 1.0 (SUM, as the reference returns) */
   int time_stages;          /* record CUDA events around the stages */
   int transport;            /* packed exchange: 0 auto (the measured-faster one: P2P for

@@ -1679,11 +1679,18 @@ pact_status pact_masked_allreduce(pact_comm* c, pact_ctx* ctx, const float* grad
   // pack in this mode: PACKED is published by the pack itself.
   static const bool push_env = !getenv("PACT_P2P_PULL");
   const bool p2p_push = push_env && p2p_try && n == 2 && !p2p_buckets;
-  // NCCL buckets: bucket_bytes, or auto (0): one bucket on the symmetric
-  // window up to 64 MiB packed (c3 n=4 277 vs 351 us bucketed), 32 MiB
-  // buckets above (c5 n=4 1.12 vs 1.22 ms single)
-  const uint64_t nccl_bb = pol.bucket_bytes ? pol.bucket_bytes : (pbytes > (64ull << 20) ? (32ull << 20) : 0);
+  // NCCL buckets: bucket_bytes, or auto (0): ONE bucket. Bucketed pipelines
+  // lose on B200: the persistent pack/unpack grids hold every SM, so the
+  // NCCL kernels of bucket b wait behind pack(b+1) / unpack(b-1) instead of
+  // overlapping them (B200 x2/x4, bench.py, step ms, 32 MiB buckets vs one
+  // bucket: c4 n=2 0.886 vs 0.668, n=4 1.081 vs 0.754; c5 n=2 1.047 vs 1.097,
+  // n=4 1.245 vs 1.125). The single bucket sits on the NCCL symmetric window
+  // (its low-latency kernels: c2 n=4 111 -> 70 us exchange), except at n = 2
+  // above 64 MiB packed, where the ring on a plain buffer is faster (c4
+  // 0.668 vs 0.796 ms, c5 1.097 vs 1.166 ms).
+  const uint64_t nccl_bb = pol.bucket_bytes;
   const bool buckets = c && !p2p_try && !f16 && nccl_bb > 0 && m->nnz * 4 > nccl_bb;
+  const bool nccl_sym_ok = c && !(n == 2 && pbytes > (64ull << 20));
   if (buckets) TRY(mirror_tile_off(m, s));
 
   int agree = 0;
@@ -1702,7 +1709,8 @@ pact_status pact_masked_allreduce(pact_comm* c, pact_ctx* ctx, const float* grad
         packed_in_sym = true;
       } else {
         // the NCCL symmetric window once registered (an earlier agreed step)
-        if (!p2p_try && !buckets && c->sym && c->sym_bytes >= m->nnz * 4) packed = static_cast<float*>(c->sym);
+        if (!p2p_try && !buckets && nccl_sym_ok && c->sym && c->sym_bytes >= m->nnz * 4)
+          packed = static_cast<float*>(c->sym);
         pactk::launch_pack(grad, len, m->words, m->tile_off, packed, 0, m->ntiles, s);
         packed_issued = true;
       }
@@ -1910,7 +1918,7 @@ pact_status pact_masked_allreduce(pact_comm* c, pact_ctx* ctx, const float* grad
     // setup). Measured (bench.py, NCCL transport): c2 n=4 115 vs 158 us, n=2
     // 118 vs 117 us; the bucketed pipeline is faster on plain buffers (c5 n=4
     // 1.12 vs 1.30 ms), so buckets keep ctx->packed.
-    if (c && !f16 && !buckets) {
+    if (c && !f16 && !buckets && nccl_sym_ok) {
       float* symp = nullptr;
       TRY(nccl_sym_packed(c, m->nnz * 4, s, &symp));
       if (symp && symp != packed) {
