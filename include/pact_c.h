@@ -119,7 +119,7 @@ typedef struct pact_policy {
   float scale;              /* applied in unpack; 0 => 1.0 (SUM, as the reference returns) */
   int time_stages;          /* record CUDA events around the stages */
   int transport;            /* packed exchange: 0 auto (the measured-faster one: P2P for
-                               n = 2 up to 64 MiB packed, else NCCL), 1 NCCL allreduce
+                               n = 2 up to 1 GiB packed, else NCCL), 1 NCCL allreduce
                                (single bucket on an NCCL symmetric-memory window),
                                2 NVLink P2P (peer-memory reduce in the reference fold
                                order; bit-identical to the reference ring) */

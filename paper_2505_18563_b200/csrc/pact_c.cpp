@@ -1663,13 +1663,14 @@ pact_status pact_masked_allreduce(pact_comm* c, pact_ctx* ctx, const float* grad
   float* packed = ctx->packed.as<float>();
 
   const bool f16 = pol.wire == PACT_WIRE_F16;  // binary16 ring on the packed values (8f-3)
-  // AUTO picks the measured-faster exchange (B200 x2/x4, bench.py c2/c3/c5):
-  // NVLink P2P for n = 2 up to 64 MiB packed (c2 108 vs 118 us, c3 266 vs 312
-  // us); NCCL otherwise -- on a symmetric window for one bucket (c2 n=4 115
-  // vs P2P 148 us), bucketed above (c5 n=2 1.03 vs 1.10 ms, n=4 1.12 vs
-  // 1.33 ms). PACT_TRANSPORT_P2P forces the bit-exact reference-order fold.
+  // AUTO picks the measured-faster exchange (B200 x2/x4, bench.py, step ms
+  // P2P vs NCCL): NVLink P2P push at n = 2 (c1 0.052 vs 0.056, c2 0.097 vs
+  // 0.116, c3 0.256 vs 0.262, c5 1.004 vs 1.090), up to 1 GiB packed (its
+  // IPC buffers hold 4x the packed vector); NCCL otherwise (c2 n=4 115 vs
+  // P2P two-shot 148 us). PACT_TRANSPORT_P2P forces the bit-exact
+  // reference-order fold at any n.
   const uint64_t pbytes = m->nnz * 4;
-  const bool auto_p2p = c && n == 2 && pbytes <= (64ull << 20);
+  const bool auto_p2p = c && n == 2 && pbytes <= (1ull << 30);
   const bool p2p_try = c && m->nnz && n <= pactk::kP2PMaxRanks && !f16 &&
                        (pol.transport == PACT_TRANSPORT_P2P || (pol.transport == PACT_TRANSPORT_AUTO && auto_p2p));
   const bool p2p_ready = p2p_try && c->p2p.ok && c->p2p.cap >= m->nnz;
