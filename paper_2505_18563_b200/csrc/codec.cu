@@ -289,6 +289,9 @@ __global__ void __launch_bounds__(kPuWarps * 32)
   const bool vec_ok = (((uintptr_t)g) & 15) == 0;
   const uint64_t nwt = (uint64_t)gridDim.x * kPuWarps;
   uint64_t c = cb + (uint64_t)blockIdx.x * kPuWarps + warp;
+  // a programmatic dependent (the unpack) may be scheduled as soon as SMs
+  // free up; it waits for this grid's completion before reading `packed`
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (c < ce) {
     // prologue: words(c0), words(c1), data(c0)
     offs_words_issue(wsm[warp][0], words, chunk_off, c);
@@ -410,6 +413,9 @@ __global__ void __launch_bounds__(kPuWarps * 32)
   }
   asm volatile("cp.async.wait_group 1;" ::: "memory");  // w0 .. w_{kA-1}
   __syncwarp();
+  // launched as a programmatic dependent of the pack: the packed vector is
+  // complete and visible only past this point (no-op otherwise)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   for (int j = 0; j < kA; ++j) {
     if (c + j * nwt < ce) {
       uint32_t b, n;
@@ -757,29 +763,43 @@ namespace {
 constexpr uint64_t kDeepUnpackChunksPerWarp = 16;
 template <bool kSgd>
 void unpack_local(const float* packed, uint64_t len, const uint64_t* words, const uint32_t* chunk_off, float scale,
-                  int do_scale, float* out, float lr, float* weights, uint64_t cb, uint64_t ce, cudaStream_t s) {
+                  int do_scale, float* out, float lr, float* weights, uint64_t cb, uint64_t ce, cudaStream_t s,
+                  bool pdl = false) {
   constexpr int kDyn1 = unpack_smem_bytes<kSrcLocal, 1>(), kDyn2 = unpack_smem_bytes<kSrcLocal, 2>();
   static int cap1 = 0, cap2 = 0;
   if (!cap1) {
     cap1 = persistent_grid_dyn(unpack_kernel<kSgd, kSrcLocal, 1>, kPuWarps, kDyn1);
     cap2 = persistent_grid_dyn(unpack_kernel<kSgd, kSrcLocal, 2>, kPuWarps, kDyn2);
   }
-  if ((ce - cb) >= kDeepUnpackChunksPerWarp * (uint64_t)cap1 * kPuWarps)
-    unpack_kernel<kSgd, kSrcLocal, 2><<<grid_for(cap2, ce - cb, kPuWarps), kPuWarps * 32, kDyn2, s>>>(
-        packed, len, words, chunk_off, scale, do_scale, out, lr, weights, cb, ce, P2PView{}, nullptr, 0, nullptr,
-        P2PSig{});
+  const bool deep = (ce - cb) >= kDeepUnpackChunksPerWarp * (uint64_t)cap1 * kPuWarps;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid_for(deep ? cap2 : cap1, ce - cb, kPuWarps));
+  cfg.blockDim = dim3(kPuWarps * 32);
+  cfg.dynamicSmemBytes = deep ? kDyn2 : kDyn1;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  const P2PView v{};
+  const P2PSig sg{};
+  const uint64_t* nf = nullptr;
+  int* ne = nullptr;
+  if (deep)
+    cudaLaunchKernelEx(&cfg, unpack_kernel<kSgd, kSrcLocal, 2>, packed, len, words, chunk_off, scale, do_scale, out,
+                       lr, weights, cb, ce, v, nf, (uint64_t)0, ne, sg);
   else
-    unpack_kernel<kSgd, kSrcLocal, 1><<<grid_for(cap1, ce - cb, kPuWarps), kPuWarps * 32, kDyn1, s>>>(
-        packed, len, words, chunk_off, scale, do_scale, out, lr, weights, cb, ce, P2PView{}, nullptr, 0, nullptr,
-        P2PSig{});
+    cudaLaunchKernelEx(&cfg, unpack_kernel<kSgd, kSrcLocal, 1>, packed, len, words, chunk_off, scale, do_scale, out,
+                       lr, weights, cb, ce, v, nf, (uint64_t)0, ne, sg);
 }
 }  // namespace
 
 void launch_unpack(const float* packed, uint64_t len, const uint64_t* words,
                    const uint32_t* chunk_off, float scale, int do_scale, float* out, uint64_t cb,
-                   uint64_t ce, cudaStream_t s) {
+                   uint64_t ce, cudaStream_t s, bool pdl) {
   if (ce <= cb) return;
-  unpack_local<false>(packed, len, words, chunk_off, scale, do_scale, out, 0.f, nullptr, cb, ce, s);
+  unpack_local<false>(packed, len, words, chunk_off, scale, do_scale, out, 0.f, nullptr, cb, ce, s, pdl);
   note_launch();
 }
 

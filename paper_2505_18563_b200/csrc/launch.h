@@ -36,9 +36,13 @@ void launch_pack(const float* g, uint64_t len, const uint64_t* words, const uint
 // incoming region, NVLink stores); the last CTA publishes sg's exit flag
 void launch_pack_push(const float* g, uint64_t len, const uint64_t* words, const uint32_t* chunk_off,
                       float* packed, float* remote, const P2PView& v, const P2PSig& sg, cudaStream_t s);
+// pdl: launched as a programmatic dependent of the kernel before it on the
+// stream (which must not write words / chunk_off): its CTAs start while the
+// predecessor drains and load their first mask words, then wait
+// (griddepcontrol.wait) before touching the packed runs
 void launch_unpack(const float* packed, uint64_t len, const uint64_t* words,
                    const uint32_t* chunk_off, float scale, int do_scale, float* out, uint64_t cb,
-                   uint64_t ce, cudaStream_t s);
+                   uint64_t ce, cudaStream_t s, bool pdl = false);
 // unpack with the exchange fused in (NVLink P2P, B == 1): one-shot (n == 2)
 // sums the local and the peer's packed runs (waits PACKED); two-shot reads
 // each run from its owner's reduced chunk (waits REDUCED; needs C >= 1024).

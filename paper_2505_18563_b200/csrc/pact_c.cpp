@@ -1936,8 +1936,10 @@ pact_status pact_masked_allreduce(pact_comm* c, pact_ctx* ctx, const float* grad
       else if (c && m->nnz)
         NCCL_TRY(ncclAllReduce(packed, packed, m->nnz, ncclFloat32, ncclSum, c->nccl, s));
       mark(1);
+      // single GPU: the unpack follows the pack directly -> programmatic
+      // dependent launch (its prologue overlaps the pack's tail)
       pactk::launch_unpack(packed, len, m->words, m->tile_off, scale, scale != 1.0f, out, 0,
-                           m->ntiles, s);
+                           m->ntiles, s, /*pdl=*/!c && !pol.time_stages);
       mark(2);
       nbuckets = 1;
     } else {

@@ -75,7 +75,8 @@ class PactHookState:
     """State of :func:`pact_hook` (one per DDP model and rank)."""
 
     def __init__(self, module: torch.nn.Module, process_group=None, stability_threshold: int = 3,
-                 policy: Optional[SyncPolicy] = None, comm: Optional[Comm] = None):
+                 policy: Optional[SyncPolicy] = None, comm: Optional[Comm] = None,
+                 auto_density: bool = False):
         self.params = [p for p in module.parameters() if p.requires_grad]
         self.layout, self.length = flat_layout(self.params)
         self.group = process_group
@@ -92,6 +93,19 @@ class PactHookState:
         self._bucket_masks: Dict[int, Tuple[int, Tuple[Tuple[int, int], ...], SparsityMask]] = {}
         self.last_stats: Dict[int, SyncStats] = {}
         self.mode_counts: Counter = Counter()
+        # adaptive policy (north_star (4)): the dense/sparse crossover measured
+        # once per bucket length on this communicator (collective: DDP calls
+        # the hook for the same buckets in the same order on every rank)
+        self.auto_density = auto_density
+        self.density_thresholds: Dict[int, float] = {}
+
+    def density_threshold(self, length: int) -> float:
+        if not self.auto_density or self.comm() is None:
+            return self.policy.density_threshold
+        if length not in self.density_thresholds:
+            from .api import calibrate_density
+            self.density_thresholds[length] = calibrate_density(length, self.comm(), policy=self.policy).threshold
+        return self.density_thresholds[length]
 
     # -- communicator (created on first use: needs the GPU and the group)
     def comm(self) -> Optional[Comm]:
@@ -178,7 +192,8 @@ def pact_hook(state: PactHookState, bucket: dist.GradBucket) -> torch.futures.Fu
         else:
             stats = SyncStats(0, 0.0, SyncMode.FullAllReduce)
     else:
-        pol = dataclasses.replace(state.policy, scale=inv_n, gse_dense=True)
+        pol = dataclasses.replace(state.policy, scale=inv_n, gse_dense=True,
+                                  density_threshold=state.density_threshold(buf.numel()))
         r = masked_allreduce(buf, state.bucket_mask(bucket), status, state.epoch, comm, policy=pol, out=buf)
         stats = r.stats
     state.last_stats[bucket.index()] = stats

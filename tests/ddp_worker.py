@@ -38,13 +38,17 @@ def main():
             failures.append(name)
             print(f"[rank {rank}] FAIL {name}", flush=True)
 
-    for transport in (pb.SyncPolicy.NCCL, pb.SyncPolicy.P2P):
+    for transport in (pb.SyncPolicy.NCCL, pb.SyncPolicy.P2P, "auto-density"):
+        auto = transport == "auto-density"
+        if auto:
+            transport = pb.SyncPolicy.AUTO
         torch.manual_seed(0)
         model = torch.nn.Sequential(torch.nn.Linear(64, 512), torch.nn.ReLU(), torch.nn.Linear(512, 384),
                                     torch.nn.ReLU(), torch.nn.Linear(384, 10)).to(dev)
         ref = copy.deepcopy(model)
         ddpm = torch.nn.parallel.DistributedDataParallel(model, device_ids=[local], bucket_cap_mb=0.25)
-        state = PactHookState(model, stability_threshold=3, policy=pb.SyncPolicy(transport=transport))
+        state = PactHookState(model, stability_threshold=3, policy=pb.SyncPolicy(transport=transport),
+                              auto_density=auto)
         ddpm.register_comm_hook(state, pact_hook)
         opt = torch.optim.SGD(model.parameters(), lr=0.05)
         modes = []
@@ -83,8 +87,15 @@ def main():
         # dense warm-up (steps 0-1); the mask is observed from step 2 and the
         # tracker turns Stable on the 4th equal digest (sparsity.cpp:17-25,
         # K = 3): Full through step 4, Packed from step 5
-        check(f"transport {transport}: modes {modes}",
-              all(m == [0] for m in modes[:5]) and all(m == [1] for m in modes[5:]))
+        if not auto:
+            check(f"transport {transport}: modes {modes}",
+                  all(m == [0] for m in modes[:5]) and all(m == [1] for m in modes[5:]))
+        else:  # packed or a density fallback (reason 3) per the measured crossover of each bucket length
+            thr = state.density_thresholds
+            check(f"auto density: thresholds {thr}", len(thr) >= 1 and all(0 < t <= 1 for t in thr.values()))
+            check(f"auto density: modes {modes}", all(m == [0] for m in modes[:5]) and
+                  all(st.mode_used == pb.SyncMode.PackedAllReduce or st.fallback_reason == 3
+                      for st in state.last_stats.values()))
         w = state.flat_weights()
         ws = [torch.empty_like(w) for _ in range(world)]
         dist.all_gather(ws, w)
