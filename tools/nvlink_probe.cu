@@ -1,7 +1,10 @@
 // nvlink_probe.cu -- measure GPU0 <-> GPU1 peer-memory access patterns
 // (design evidence for p2p.cu). Single process, peer access enabled.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/nvlink_probe tools/nvlink_probe.cu
+#include <cstdint>
 #include <cstdio>
+#include <cstdlib>
+#include <vector>
 #include <cuda_runtime.h>
 
 #define CK(x)                                                             \
@@ -48,6 +51,33 @@ __global__ void fold2(const float4* __restrict__ loc, const float4* __restrict__
     const float4 a = __ldcg(loc + i), b = __ldcg(rem + i);
     out[i] = make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
   }
+}
+
+// smem-staged bulk copy / bulk reduce-add to a (peer) global buffer: 4 KiB
+// per warp-iteration, issued by lane 0 (the n = 2 reduce-push candidate)
+template <bool kReduce>
+__global__ void bulk_push(const float* __restrict__ src, float* __restrict__ dst, size_t n) {
+  __shared__ __align__(128) float st[8][1024];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float* b = st[warp];
+  for (size_t c = (size_t)blockIdx.x * 8 + warp; c * 1024 < n; c += (size_t)gridDim.x * 8) {
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    __syncwarp();
+    for (int i = lane; i < 256; i += 32)
+      reinterpret_cast<float4*>(b)[i] = reinterpret_cast<const float4*>(src + c * 1024)[i];
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    if (lane == 0) {
+      const uint32_t sa = (uint32_t)__cvta_generic_to_shared(b);
+      if (kReduce)
+        asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], 4096;\n"
+                     " cp.async.bulk.commit_group;" ::"l"(dst + c * 1024), "r"(sa) : "memory");
+      else
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], 4096;\n"
+                     " cp.async.bulk.commit_group;" ::"l"(dst + c * 1024), "r"(sa) : "memory");
+    }
+  }
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 int main() {
@@ -218,6 +248,49 @@ int main() {
       printf("%3zu MB bidirectional %s (grid %d): GPU0 %7.1f us, GPU1 %7.1f us (%6.1f GB/s each way)\n", mb,
              mode < 4 ? "WRITE float4" : "cudaMemcpyPeer", mode < 4 ? grids[mode] : 0, best0 * 1e3, best1 * 1e3,
              (mb << 20) / (best0 * 1e-3) / 1e9);
+    }
+    // bulk copy / bulk reduce-add, both directions at once; then check the sums
+    for (int red = 0; red < 2; ++red) {
+      float best0 = 1e9;
+      for (int it = 0; it < 10; ++it) {
+        CK(cudaSetDevice(0));
+        cudaDeviceSynchronize();
+        CK(cudaSetDevice(1));
+        cudaDeviceSynchronize();
+        CK(cudaSetDevice(0));
+        cudaEventRecord(f0, s0);
+        if (red) bulk_push<true><<<148 * 2, 256, 0, s0>>>(a0, r1, nn * 4);
+        else bulk_push<false><<<148 * 2, 256, 0, s0>>>(a0, r1, nn * 4);
+        cudaEventRecord(g0, s0);
+        CK(cudaSetDevice(1));
+        if (red) bulk_push<true><<<148 * 2, 256, 0, s1>>>(l1, r0, nn * 4);
+        else bulk_push<false><<<148 * 2, 256, 0, s1>>>(l1, r0, nn * 4);
+        cudaStreamSynchronize(s1);
+        CK(cudaSetDevice(0));
+        cudaEventSynchronize(g0);
+        float m0;
+        cudaEventElapsedTime(&m0, f0, g0);
+        best0 = m0 < best0 ? m0 : best0;
+      }
+      CK(cudaGetLastError());
+      printf("%3zu MB bidirectional bulk %s: %7.1f us (%6.1f GB/s each way)\n", mb, red ? "REDUCE-ADD" : "copy",
+             best0 * 1e3, (mb << 20) / (best0 * 1e-3) / 1e9);
+    }
+    {  // correctness of the remote reduce-add: r1 = 1.0 + sum of pushes
+      CK(cudaSetDevice(0));
+      float* h = (float*)malloc(16 * 4);
+      std::vector<float> ones(nn * 4, 1.0f), twos(nn * 4, 2.0f);
+      CK(cudaMemcpy(a0, twos.data(), nn * 16, cudaMemcpyHostToDevice));
+      CK(cudaSetDevice(1));
+      CK(cudaMemcpy(r1, ones.data(), nn * 16, cudaMemcpyHostToDevice));
+      CK(cudaSetDevice(0));
+      bulk_push<true><<<148 * 2, 256, 0, s0>>>(a0, r1, nn * 4);
+      CK(cudaStreamSynchronize(s0));
+      CK(cudaSetDevice(1));
+      CK(cudaMemcpy(h, r1 + 12345, 16 * 4, cudaMemcpyDeviceToHost));
+      printf("remote reduce-add check: %s (r1[12345] = %.1f, want 3.0)\n", h[0] == 3.0f ? "OK" : "WRONG", h[0]);
+      CK(cudaSetDevice(0));
+      free(h);
     }
   }
   return 0;
