@@ -185,6 +185,54 @@ def test_unaligned_and_inplace(pb, port, cuda):
     assert np.array_equal(u32(x.cpu().numpy()), u32(port.gse(g_h, w)))
 
 
+@pytest.mark.parametrize("n", [1, 31, 1000, 1025, 65_537, 300_007])
+def test_no_writes_outside_outputs(pb, port, cuda, n):
+    """Bounds check without a sanitizer: pack / unpack / GSE / unpack_sgd /
+    masked_allreduce write into buffers flanked by 64-float canaries (at
+    16-byte-aligned and unaligned offsets); the canaries must survive and
+    the payload must match the oracle."""
+    import ctypes as C
+
+    rng = np.random.default_rng(n)
+    g_h = rng.standard_normal(n).astype(np.float32)
+    bits = rng.random(n) < 0.37
+    w = words_from_bits(bits)
+    m = pb.SparsityMask.from_words(dev(w.view(np.int64)), n)
+    nnz = int(bits.sum())
+    canary = -12345.5
+    for lead in (64, 65):  # aligned / unaligned payload start
+        def framed(k):
+            buf = torch.full((lead + k + 64,), canary, device=cuda)
+            return buf, buf[lead:lead + k]
+
+        def intact(buf, k):
+            b = buf.cpu().numpy()
+            return bool(np.all(b[:lead] == canary) and np.all(b[lead + k:] == canary))
+
+        gd = dev(g_h)
+        pbuf, packed = framed(max(nnz, 1))
+        ctx = pb.Context.get()
+        pb.api._call(pb.api.lib.pact_pack, ctx.handle, pb.api._ptr(gd), n, m.handle, pb.api._ptr(packed), 0,
+                     C.c_uint64(2 ** 64 - 1), pb.api._stream())
+        assert intact(pbuf, nnz), "pack wrote outside the packed vector"
+        assert np.array_equal(u32(packed[:nnz].cpu().numpy()), u32(port.pack(g_h, w)))
+        obuf, out = framed(n)
+        pb.unpack(pb.PackedGradient(m.digest(), 0, packed[:nnz]), m, out=out)
+        assert intact(obuf, n), "unpack wrote outside the output"
+        assert np.array_equal(u32(out.cpu().numpy()), u32(port.gse(g_h, w)))
+        ebuf, eout = framed(n)
+        pb.enforce_gradient_sparsity(gd, m, out=eout)
+        assert intact(ebuf, n), "GSE wrote outside the output"
+        wbuf, wts = framed(n)
+        wts.copy_(gd)
+        pb.unpack_sgd(packed[:nnz], m, 0.5, 0.25, wts)
+        assert intact(wbuf, n), "unpack_sgd wrote outside the weights"
+        rbuf, rout = framed(n)
+        pb.masked_allreduce(gd, m, pb.TrackerStatus.Stable, 0, None, out=rout)
+        assert intact(rbuf, n), "masked_allreduce wrote outside the output"
+        assert np.array_equal(u32(rout.cpu().numpy()), u32(port.gse(g_h, w)))
+
+
 def test_codec_errors(pb, cuda):
     m = pb.SparsityMask.all_ones(2)
     p = pb.pack(dev(np.array([1.0, 2.0], np.float32)), m, 0)
