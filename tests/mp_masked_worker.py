@@ -209,6 +209,23 @@ def main():
     check("topk: bytes", rk.stats.bytes_on_wire == (world - 1) * (26 + 8 * sel[0][0].size))
     check("topk: mode", rk.stats.mode_used == pb.SyncMode.TopKAllGather)
 
+    # ---- n = 2 push exchange, compact pair unpack with a few dense chunks
+    # (runs > 512 values read the peer's run from global memory)
+    if world == 2:
+        nb = 200_003
+        bits2 = rng.random(nb) < 0.1
+        bits2[:10 * 1024 + 77] = True
+        words2 = words_from_bits(bits2)
+        mask2 = pb.SparsityMask.from_words(torch.from_numpy(words2.view(np.int64)).to(dev), nb)
+        grads2 = [port.gse(synth.synth_host(nb, synth.grad_seed(r, 21), synth.G_FULL), words2) for r in range(world)]
+        outs2, _, _ = port.masked_allreduce(grads2, [words2] * world, [1] * world, 5)
+        g2 = torch.from_numpy(grads2[rank]).to(dev)
+        for step in range(3):
+            r2 = pb.masked_allreduce(g2, mask2, pb.TrackerStatus.Stable, 5 + step, comm,
+                                     policy=pb.SyncPolicy(transport=pb.SyncPolicy.P2P))
+            check(f"compact pair with dense chunks: bit-exact (step {step})",
+                  np.array_equal(u32(r2.tensor.cpu().numpy()), u32(outs2[rank])))
+
     # ---- measured dense/sparse crossover: unanimous threshold,
     # and the policy it feeds picks packed below / dense above it
     cal = pb.calibrate_density(1 << 22, comm, densities=[0.05, 0.3, 0.6, 0.9])
