@@ -1,0 +1,207 @@
+// cluster_test.cpp -- the reference's collective unit assertions
+// (/root/reference/proj/tests/test_collective.cpp:46-285), rerun on real GPUs
+// through the C++ drop-in header include/pact_b200.hpp. The reference runs
+// its workers as threads of one process (SimCluster, test_collective.cpp:
+// 23-35); here every worker is a PROCESS on its own GPU (the B200 topology:
+// one process per GPU, NCCL + CUDA IPC), started by tests/test_cpp_dropin.py
+// as `cluster_test <rank> <world> <id-file>`; rank 0 publishes the NCCL
+// unique id through the file. Every rank rebuilds all ranks' inputs from the
+// seeds, so each checks its own result against the whole-cluster oracle.
+// Exit code = failed checks.
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cstdlib>
+#include <cmath>
+#include <cstdio>
+#include <random>
+#include <thread>
+#include <vector>
+
+#include "pact_b200.hpp"
+
+using namespace pact;
+
+static std::atomic<int> g_fail{0};
+#define CHECK(cond)                                                   \
+  do {                                                                \
+    if (!(cond)) {                                                    \
+      std::printf("FAIL %s:%d: %s\n", __FILE__, __LINE__, #cond);   \
+      ++g_fail;                                                       \
+    }                                                                 \
+  } while (0)
+
+static FlatTensor random_tensor(std::mt19937_64& g, size_t len) {  // test_collective.cpp:17-21
+  std::normal_distribution<float> d(0.0f, 1.0f);
+  std::vector<float> v(len);
+  for (float& x : v) x = d(g);
+  return FlatTensor(std::move(v));
+}
+
+static std::vector<double> sequential_sum(const std::vector<FlatTensor>& in) {  // :37-42
+  std::vector<double> out(in[0].size(), 0.0);
+  for (const auto& t : in)
+    for (size_t i = 0; i < t.size(); ++i) out[i] += t[i];
+  return out;
+}
+
+static int g_rank = 0, g_world = 0;
+static const char* g_idfile = nullptr;
+static int g_round = 0;
+
+// fn(rank, comm) on the first n ranks (the others idle this round); one
+// communicator per round, its unique id passed through <id-file>.<round>
+template <typename Fn>
+static void run_workers(int n, Fn fn) {
+  const int round = g_round++;
+  char path[512];
+  std::snprintf(path, sizeof path, "%s.%d", g_idfile, round);
+  if (g_rank >= n) return;
+  std::vector<uint8_t> id(PACT_UNIQUE_ID_BYTES);
+  if (g_rank == 0) {
+    id = Comm::unique_id();
+    char tmp[520];
+    std::snprintf(tmp, sizeof tmp, "%s.tmp", path);
+    FILE* f = std::fopen(tmp, "wb");
+    std::fwrite(id.data(), 1, id.size(), f);
+    std::fclose(f);
+    std::rename(tmp, path);
+  } else {
+    for (int t = 0; t < 60000; ++t) {  // <= 60 s
+      FILE* f = std::fopen(path, "rb");
+      if (f) {
+        const size_t got = std::fread(id.data(), 1, id.size(), f);
+        std::fclose(f);
+        if (got == id.size()) break;
+      }
+      std::this_thread::sleep_for(std::chrono::milliseconds(1));
+    }
+  }
+  try {
+    Comm comm(g_rank, n, id);
+    fn(g_rank, comm);
+  } catch (const std::exception& e) {
+    std::printf("FAIL rank %d round %d: %s\n", g_rank, round, e.what());
+    ++g_fail;
+  }
+}
+
+static std::vector<bool> bits_of(size_t len, size_t off_bit, bool drop_extra, size_t extra) {
+  std::vector<bool> b(len, true);
+  b[off_bit] = false;
+  if (drop_extra) b[extra] = false;
+  return b;
+}
+
+int main(int argc, char** argv) {
+  if (argc < 4) {
+    std::printf("usage: cluster_test <rank> <world> <id-file>\n");
+    return 2;
+  }
+  g_rank = std::atoi(argv[1]);
+  g_world = std::atoi(argv[2]);
+  g_idfile = argv[3];
+  detail::cuda(cudaSetDevice(g_rank));
+  const int ngpu = g_world;
+  const int nmax = std::min(g_world, 4);
+  const int r0 = g_rank;  // checks below look at this rank's own result
+
+  // test_collective.cpp:46-54: two workers sum [1,2] and [3,4]
+  {
+    std::vector<FlatTensor> in{FlatTensor({1.0f, 2.0f}), FlatTensor({3.0f, 4.0f})};
+    std::vector<FlatTensor> out(2);
+    run_workers(2, [&](int r, Comm& c) { out[r] = full_allreduce(in[r], c).tensor; });
+    if (r0 < 2) CHECK(out[r0].size() == 2 && out[r0][0] == 4.0f && out[r0][1] == 6.0f);
+  }
+  // :56-62 zeros stay zeros
+  {
+    std::vector<FlatTensor> out(nmax);
+    run_workers(nmax, [&](int r, Comm& c) { out[r] = full_allreduce(FlatTensor::zeros(37), c).tensor; });
+    if (r0 < nmax)
+      for (size_t i = 0; i < out[r0].size(); ++i) CHECK(out[r0][i] == 0.0f);
+  }
+  // :210-244 masked allreduce on a stable mask halves the bytes
+  {
+    const int n = nmax;
+    const size_t len = 100000;
+    std::vector<bool> bits(len);
+    for (size_t i = 0; i < len; ++i) bits[i] = (i % 2) == 0;
+    std::mt19937_64 g(123);
+    std::vector<FlatTensor> raw;
+    for (int r = 0; r < n; ++r) raw.push_back(random_tensor(g, len));
+    std::vector<SyncStats> ps(n), fs(n);
+    std::vector<FlatTensor> po(n), fo(n);
+    run_workers(n, [&](int r, Comm& c) {
+      const SparsityMask mask = SparsityMask::from_bits(bits);  // device resident: one per GPU
+      const FlatTensor grad = enforce_gradient_sparsity(raw[r], mask);
+      auto a = masked_allreduce(grad, mask, TrackerStatus::Stable, 1, c);
+      po[r] = std::move(a.tensor);
+      ps[r] = a.stats;
+      auto b = masked_allreduce(grad, mask, TrackerStatus::Unstable, 1, c);
+      fo[r] = std::move(b.tensor);
+      fs[r] = b.stats;
+    });
+    if (r0 < n) {
+      CHECK(ps[r0].mode_used == SyncMode::PackedAllReduce);
+      CHECK(fs[r0].mode_used == SyncMode::FullAllReduce);
+      const double ratio = (double)ps[r0].bytes_on_wire / (double)fs[r0].bytes_on_wire;
+      CHECK(ratio <= 0.51 && ratio >= 0.49);
+      for (size_t i = 0; i < len; i += 97)
+        CHECK(std::fabs(po[r0][i] - fo[r0][i]) <= 1e-5 * std::max(1.0f, std::fabs(fo[r0][i])));
+    }
+  }
+  // :246-260 the unstable masked path equals the full path bit-for-bit
+  {
+    const int n = std::min(nmax, 3);
+    std::mt19937_64 g(9);
+    std::vector<FlatTensor> raw;
+    for (int r = 0; r < n; ++r) raw.push_back(random_tensor(g, 257));
+    std::vector<FlatTensor> a(n), b(n);
+    run_workers(n, [&](int r, Comm& c) {
+      const SparsityMask mask = SparsityMask::all_ones(257).with_bit(13, false);
+      const FlatTensor grad = enforce_gradient_sparsity(raw[r], mask);
+      a[r] = masked_allreduce(grad, mask, TrackerStatus::Unstable, 0, c).tensor;
+      b[r] = full_allreduce(grad, c).tensor;
+    });
+    if (r0 < n) CHECK(a[r0] == b[r0]);
+  }
+  // :262-285 divergent masks trigger the fallback and still match the oracle
+  {
+    const int n = nmax;
+    const size_t len = 300;
+    std::mt19937_64 g(44);
+    std::vector<FlatTensor> grads;
+    for (int r = 0; r < n; ++r) grads.push_back(random_tensor(g, len));
+    const auto expect = sequential_sum(grads);
+    std::vector<SyncStats> st(n);
+    std::vector<FlatTensor> out(n);
+    run_workers(n, [&](int r, Comm& c) {
+      const SparsityMask mine = SparsityMask::from_bits(bits_of(len, 5, r == n / 2, 6));  // one worker disagrees
+      auto res = masked_allreduce(grads[r], mine, TrackerStatus::Stable, 7, c);
+      out[r] = std::move(res.tensor);
+      st[r] = res.stats;
+    });
+    if (r0 < n) {
+      CHECK(st[r0].mode_used == SyncMode::FullAllReduce);
+      for (size_t i = 0; i < len; ++i)
+        CHECK(std::fabs(out[r0][i] - expect[i]) <= 1e-5 * std::max(1.0, std::fabs(expect[i])));
+    }
+  }
+  // extension: the measured dense/sparse crossover is unanimous
+  {
+    const int n = 2;
+    std::vector<double> thr(n, -1.0);
+    run_workers(n, [&](int r, Comm& c) { thr[r] = calibrate_density(c, size_t{1} << 20); });
+    if (r0 < n) {
+      CHECK(thr[r0] > 0.0 && thr[r0] <= 1.0);
+      // unanimous: the threshold summed over the ranks is n times this one
+      std::vector<FlatTensor> tot(n);
+      run_workers(n, [&](int r, Comm& c) { tot[r] = full_allreduce(FlatTensor({(float)thr[r]}), c).tensor; });
+      CHECK(tot[r0][0] == (float)(n * (float)thr[r0]));
+    } else {
+      run_workers(n, [](int, Comm&) {});
+    }
+  }
+  std::printf("cluster_test rank %d/%d: %d failed check(s)\n", g_rank, ngpu, g_fail.load());
+  return g_fail.load();
+}
