@@ -140,6 +140,7 @@ struct pact_ctx {
   DevBuf f16;       // binary16 ring: send x2, recv, n gathered chunks
   DevBuf topk;      // TopK: [own idx k][own val k][n gathered blocks] + f64 accumulator
   pact_mask* topk_sel = nullptr;  // TopK selection bitmap (prune machinery)
+  pact_mask* topk_union = nullptr;  // TopK aggregate: union of the ranks' selections
   HostBuf pin;      // small pinned readbacks
   cudaStream_t aux[2] = {nullptr, nullptr};  // comm / unpack streams for bucket overlap
   std::vector<cudaEvent_t> ev_pool;
@@ -601,6 +602,7 @@ pact_status pact_ctx_destroy(pact_ctx* ctx) {
                     &ctx->grad_stage, &ctx->out_stage, &ctx->tern, &ctx->f16, &ctx->topk})
     b->release();
   if (ctx->topk_sel) pact_mask_destroy(ctx->topk_sel);
+  if (ctx->topk_union) pact_mask_destroy(ctx->topk_union);
   ctx->pin.release();
   for (auto s : ctx->aux)
     if (s) cudaStreamDestroy(s);
@@ -1478,13 +1480,21 @@ pact_status pact_topk_allgather_aggregate(pact_comm* c, pact_ctx* ctx, const flo
   cudaStream_t s = stream;
   const int n = c ? c->n : 1;
   CUDA_TRY(cudaEventRecord(ctx->t0, s));
-  // [own idx k | own val k] [n blocks of 2k words] [f64 acc len], 16-byte aligned
+  // [own idx k | own val k] [n blocks of 2k words] [f64 acc n*k] [f32 slot means n*k], 16-byte aligned
   const uint64_t blk = (2 * k + 3) & ~3ull;
   const uint64_t words32 = blk * (uint64_t)(n + 1);
-  TRY(ctx->topk.ensure(words32 * 4 + len * 8 + 16));
+  const uint64_t slots = std::max<uint64_t>(1, std::min<uint64_t>(len, k * (uint64_t)n));
+  const uint64_t acc_off = (words32 * 4 + 15) & ~15ull;
+  TRY(ctx->topk.ensure(acc_off + slots * 12 + 16));
   uint32_t* own = ctx->topk.as<uint32_t>();
   uint32_t* all = own + blk;
-  double* acc = reinterpret_cast<double*>(ctx->topk.as<char>() + ((words32 * 4 + 15) & ~15ull));
+  double* acc = reinterpret_cast<double*>(ctx->topk.as<char>() + acc_off);
+  float* means = reinterpret_cast<float*>(acc + slots);
+  if (len && (!ctx->topk_union || ctx->topk_union->len != len)) {
+    if (ctx->topk_union) pact_mask_destroy(ctx->topk_union);
+    ctx->topk_union = nullptr;
+    TRY(pact_mask_create(ctx, len, &ctx->topk_union));
+  }
   int* err = reinterpret_cast<int*>(&ctx->ws_small.as<Small>()->changed);
   CUDA_TRY(cudaMemsetAsync(err, 0, 4, s));
   if (len) {
@@ -1494,13 +1504,27 @@ pact_status pact_topk_allgather_aggregate(pact_comm* c, pact_ctx* ctx, const flo
       NCCL_TRY(ncclAllGather(own, all, blk * 4, ncclUint8, c->nccl, s));
       blocks = all;
     }
-    // collective.cpp:383-388: acc[i] += values, ranks in order; mean = float(acc / n)
-    CUDA_TRY(cudaMemsetAsync(acc, 0, len * 8, s));
+    // collective.cpp:383-388: acc[i] += values, ranks in order; mean =
+    // float(acc / n). Sparse: the accumulator holds only the union U of the
+    // ranks' indices (at most n*k slots, addressed by U's bitmap rank), the
+    // means are expanded by the unpack kernel over U (+0.0 elsewhere, as
+    // float(0.0 / n)) -- no len-sized double array to clear and stream.
+    pact_mask* u = ctx->topk_union;
+    CUDA_TRY(cudaMemsetAsync(u->words, 0, ((u->nwords + 15) & ~15ull) * 8, s));
+    for (int q = 0; q < n; ++q) pactk::launch_union_bits(blocks + (uint64_t)q * blk, k, len, u->words, err, s);
+    pactk::launch_tile_popc(u->words, u->len, u->tile_popc, s);
+    TRY(scan(ctx, u->tile_popc, u->ntiles, u->tile_off, s));
+    CUDA_TRY(cudaMemsetAsync(acc, 0, slots * 8, s));
     for (int q = 0; q < n; ++q) {
       const uint32_t* b = blocks + (uint64_t)q * blk;
-      pactk::launch_scatter_add_f64(b, reinterpret_cast<const float*>(b + k), k, len, acc, err, s);
+      pactk::launch_scatter_add_slot(b, reinterpret_cast<const float*>(b + k), k, len, u->words, u->tile_off, acc,
+                                     s);
     }
-    pactk::launch_f64_mean(acc, len, n, out, s);
+    pactk::launch_slot_mean(acc, u->tile_off + u->ntiles, slots, n, means, s);
+    pactk::launch_unpack(means, len, u->words, u->tile_off, 1.0f, 0, out, 0, u->ntiles, s);
+    u->changed = 1;
+    u->digest_valid = 0;
+    u->host_tile_off_valid = 0;
     CUDA_TRY(cudaGetLastError());
     int* pin = ctx->pin.as<int>();
     CUDA_TRY(cudaMemcpyAsync(pin, err, 4, cudaMemcpyDeviceToHost, s));

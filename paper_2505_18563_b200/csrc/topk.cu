@@ -72,6 +72,51 @@ __global__ void scatter_f32_kernel(const uint32_t* __restrict__ idx, const float
   }
 }
 
+// ---- sparse accumulator over the union of the ranks' selections
+// U = OR of every rank's index set (bit i of words[i >> 6]); validates ranges
+__global__ void union_bits_kernel(const uint32_t* __restrict__ idx, uint64_t k, uint64_t len,
+                                  unsigned long long* __restrict__ words, int* __restrict__ err) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < k; j += stride) {
+    const uint32_t i = idx[j];
+    if (i >= len) {
+      atomicOr(err, 1);
+      continue;
+    }
+    atomicOr(words + (i >> 6), 1ull << (i & 63));
+  }
+}
+
+// slot of index i in U: kept elements of U before i (chunk offset + the
+// popcounts of the chunk's earlier words and of word i>>6 below bit i)
+__device__ __forceinline__ uint32_t union_slot(const uint64_t* __restrict__ words, const uint32_t* __restrict__ off,
+                                               uint32_t i) {
+  const uint32_t c = i >> 10, w = i >> 6;
+  uint32_t s = off[c];
+  for (uint32_t q = c << 4; q < w; ++q) s += __popcll(words[q]);
+  return s + __popcll(words[w] & ((1ull << (i & 63)) - 1ull));
+}
+
+// acc[slot(i)] += (double)val -- one rank's list (indices unique), ranks in
+// order on the stream: the reference's per-index double accumulation order
+__global__ void scatter_add_slot_kernel(const uint32_t* __restrict__ idx, const float* __restrict__ val, uint64_t k,
+                                        uint64_t len, const uint64_t* __restrict__ words,
+                                        const uint32_t* __restrict__ off, double* __restrict__ acc) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < k; j += stride) {
+    const uint32_t i = idx[j];
+    if (i < len) acc[union_slot(words, off, i)] += (double)val[j];
+  }
+}
+
+// packed[s] = float(acc[s] / n) for s < |U| (= off[nchunks])
+__global__ void slot_mean_kernel(const double* __restrict__ acc, const uint32_t* __restrict__ total, int n,
+                                 float* __restrict__ packed) {
+  const uint64_t m = *total, stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < m; s += stride)
+    packed[s] = (float)(acc[s] / (double)n);
+}
+
 unsigned grid_of(uint64_t n) {
   uint64_t g = (n + 255) / 256;
   return (unsigned)(g > 4736 ? 4736 : (g ? g : 1));
@@ -94,6 +139,26 @@ void launch_scatter_add_f64(const uint32_t* idx, const float* val, uint64_t k, u
                             int* err, cudaStream_t s) {
   if (!k) return;
   scatter_add_f64_kernel<<<grid_of(k), 256, 0, s>>>(idx, val, k, len, acc, err);
+  note_launch();
+}
+
+void launch_union_bits(const uint32_t* idx, uint64_t k, uint64_t len, uint64_t* words, int* err, cudaStream_t s) {
+  if (!k) return;
+  union_bits_kernel<<<grid_of(k), 256, 0, s>>>(idx, k, len, reinterpret_cast<unsigned long long*>(words), err);
+  note_launch();
+}
+
+void launch_scatter_add_slot(const uint32_t* idx, const float* val, uint64_t k, uint64_t len, const uint64_t* words,
+                             const uint32_t* off, double* acc, cudaStream_t s) {
+  if (!k) return;
+  scatter_add_slot_kernel<<<grid_of(k), 256, 0, s>>>(idx, val, k, len, words, off, acc);
+  note_launch();
+}
+
+void launch_slot_mean(const double* acc, const uint32_t* total, uint64_t max_slots, int n, float* packed,
+                      cudaStream_t s) {
+  if (!max_slots) return;
+  slot_mean_kernel<<<grid_of(max_slots), 256, 0, s>>>(acc, total, n, packed);
   note_launch();
 }
 
