@@ -1596,6 +1596,41 @@ pact_status f16_ring(pact_comm* c, pact_ctx* ctx, const float* x, uint64_t count
   const uint64_t C = (count + n - 1) / n;
   auto begin = [&](int ch) { return std::min<uint64_t>(count, (uint64_t)ch * C); };
   auto elems = [&](int ch) { return std::min<uint64_t>(count, ((uint64_t)ch + 1) * C) - begin(ch); };
+  // n = 2 over NVLink peer memory: the ring's single hop reads the peer's
+  // encoded chunk in place, the all-gather is one copy into the peer's slot
+  // (same arithmetic and slot layout as the NCCL ring below: bit-identical)
+  static const bool nccl_only = getenv("PACT_F16_NCCL") != nullptr;
+  if (n == 2 && !nccl_only) {
+    TRY(p2p_setup(c, (count + 1) / 2 + 1, s));
+    if (c->p2p.ok && c->p2p.cap * 2 >= count + 2) {
+      P2PState& p = c->p2p;
+      const uint64_t k1 = p.k + 1;
+      const int par = (int)(k1 & 1), peer = r ^ 1;
+      const pactk::P2PView v = p2p_view(c, par, count);
+      uint64_t* myflags = p2p_flags(p, r);
+      int* err = p.err.as<int>();
+      const uint64_t fv = (k1 << 8) | 1;
+      if (k1 > 2) pactk::launch_p2p_wait(myflags, pactk::kP2PRead, n, k1 - 2, err, s);
+      auto* send_mine = reinterpret_cast<uint16_t*>(p2p_packed(p, r, par));
+      const auto* send_peer = reinterpret_cast<const uint16_t*>(p2p_packed(p, peer, par));
+      auto* gath_mine = reinterpret_cast<uint16_t*>(p2p_reduced(p, r, par));
+      auto* gath_peer = reinterpret_cast<uint16_t*>(p2p_reduced(p, peer, par));
+      pactk::launch_f16_encode(x + begin(r), elems(r), send_mine, s);  // hop 0: my chunk r
+      pactk::launch_p2p_signal(v, pactk::kP2PPacked, fv, s);
+      pactk::launch_p2p_wait(myflags, pactk::kP2PPacked, n, fv, err, s);
+      // owner's rounding of chunk 1 - r (the peer's encoded chunk, read over NVLink) -> my slot r
+      pactk::launch_f16_step(x + begin(peer), send_peer, elems(peer), gath_mine + (uint64_t)r * C, s);
+      if (elems(peer))
+        CUDA_TRY(cudaMemcpyAsync(gath_peer + (uint64_t)r * C, gath_mine + (uint64_t)r * C, elems(peer) * 2,
+                                 cudaMemcpyDeviceToDevice, s));
+      pactk::launch_p2p_signal(v, pactk::kP2PReduced, fv, s);
+      pactk::launch_p2p_wait(myflags, pactk::kP2PReduced, n, fv, err, s);
+      pactk::launch_f16_gather(gath_mine, count, n, C, out, s);
+      pactk::launch_p2p_signal(v, pactk::kP2PRead, k1, s);
+      p.k = k1;
+      return PACT_OK;
+    }
+  }
   TRY(ctx->f16.ensure((3 + (uint64_t)n) * C * 2));
   uint16_t* send[2] = {ctx->f16.as<uint16_t>(), ctx->f16.as<uint16_t>() + C};
   uint16_t* recv = send[1] + C;
