@@ -282,16 +282,18 @@ template <int kPush>
 __global__ void __launch_bounds__(kPuWarps * 32)
     pack_lm_kernel(const float* __restrict__ g, uint64_t len, const uint64_t* __restrict__ words,
                    const uint32_t* __restrict__ chunk_off, float* __restrict__ packed, uint64_t cb,
-                   uint64_t ce, float* __restrict__ remote, P2PView v, P2PSig sg) {
+                   uint64_t ce, float* __restrict__ remote, P2PView v, P2PSig sg, int pdl_trigger) {
   __shared__ __align__(16) float dsm[kPuWarps][2][kPkStage];
   __shared__ __align__(16) uint64_t wsm[kPuWarps][3][kWbuf];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const bool vec_ok = (((uintptr_t)g) & 15) == 0;
   const uint64_t nwt = (uint64_t)gridDim.x * kPuWarps;
   uint64_t c = cb + (uint64_t)blockIdx.x * kPuWarps + warp;
-  // a programmatic dependent (the unpack) may be scheduled as soon as SMs
-  // free up; it waits for this grid's completion before reading `packed`
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  // a programmatic dependent (the single-GPU unpack) may be scheduled as soon
+  // as SMs free up; it waits for this grid's completion before reading
+  // `packed`. Only when the caller launches one: a PDL-capable successor of
+  // another kind (e.g. a collective kernel) must not be let in early.
+  if (pdl_trigger) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (c < ce) {
     // prologue: words(c0), words(c1), data(c0)
     offs_words_issue(wsm[warp][0], words, chunk_off, c);
@@ -728,12 +730,12 @@ uint64_t launches() { return g_launches; }
 void note_launch(uint64_t n) { g_launches += n; }
 
 void launch_pack(const float* g, uint64_t len, const uint64_t* words, const uint32_t* chunk_off,
-                 float* packed, uint64_t cb, uint64_t ce, cudaStream_t s) {
+                 float* packed, uint64_t cb, uint64_t ce, cudaStream_t s, bool pdl_trigger) {
   if (ce <= cb) return;
   static int cap = 0;
   if (!cap) cap = persistent_grid(pack_lm_kernel<kPushNone>, kPuWarps);
   pack_lm_kernel<kPushNone><<<grid_for(cap, ce - cb, kPuWarps), kPuWarps * 32, 0, s>>>(
-      g, len, words, chunk_off, packed, cb, ce, nullptr, P2PView{}, P2PSig{});
+      g, len, words, chunk_off, packed, cb, ce, nullptr, P2PView{}, P2PSig{}, pdl_trigger ? 1 : 0);
   note_launch();
 }
 
@@ -751,10 +753,10 @@ void launch_pack_push(const float* g, uint64_t len, const uint64_t* words, const
   const unsigned grid = grid_for(cap, nc, kPuWarps);
   if (stores)
     pack_lm_kernel<kPushStores><<<grid, kPuWarps * 32, 0, s>>>(g, len, words, chunk_off, packed, 0, nc, remote,
-                                                               v, sg);
+                                                               v, sg, 0);
   else
     pack_lm_kernel<kPushTma><<<grid, kPuWarps * 32, 0, s>>>(g, len, words, chunk_off, packed, 0, nc, remote, v,
-                                                            sg);
+                                                            sg, 0);
   note_launch();
 }
 

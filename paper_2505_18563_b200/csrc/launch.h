@@ -30,8 +30,9 @@ struct P2PSig {
 
 // ---- codec.cu --------------------------------------------------------------
 // chunk range [cb, ce) of 1024-element chunks; all pointers device.
+// pdl_trigger: let a programmatic dependent (launch_unpack(..., pdl)) start early
 void launch_pack(const float* g, uint64_t len, const uint64_t* words, const uint32_t* chunk_off,
-                 float* packed, uint64_t cb, uint64_t ce, cudaStream_t s);
+                 float* packed, uint64_t cb, uint64_t ce, cudaStream_t s, bool pdl_trigger = false);
 // pack into `packed` and, with the same offsets, into `remote` (the peer's
 // incoming region, NVLink stores); the last CTA publishes sg's exit flag
 void launch_pack_push(const float* g, uint64_t len, const uint64_t* words, const uint32_t* chunk_off,

@@ -1987,8 +1987,8 @@ pact_status pact_masked_allreduce(pact_comm* c, pact_ctx* ctx, const float* grad
       }
     }
     if (!buckets) {
-      if (!packed_issued && m->nnz)
-        pactk::launch_pack(grad, len, m->words, m->tile_off, packed, 0, m->ntiles, s);
+      if (!packed_issued && m->nnz)  // single GPU: the unpack follows as a programmatic dependent
+        pactk::launch_pack(grad, len, m->words, m->tile_off, packed, 0, m->ntiles, s, !c && !pol.time_stages);
       mark(0);
       if (f16)  // ring_allreduce_fp16 of the packed values (collective.cpp:133-163)
         TRY(f16_ring(c, ctx, packed, m->nnz, packed, s));
