@@ -128,8 +128,7 @@ void launch_prune_tiefix(uint64_t* words, uint64_t len, const uint64_t* tie_word
 void launch_pack_index(uint64_t len, const uint64_t* words, const uint32_t* chunk_off,
                        uint32_t* idx, cudaStream_t s);
 // acc[idx[j]] += double(val[j]) (unique idx per call); err |= 1 on idx >= len
-void launch_scatter_add_f64(const uint32_t* idx, const float* val, uint64_t k, uint64_t len,
-                            double* acc, int* err, cudaStream_t s);
+
 // out[i] = float(acc[i] / n)
 // sparse TopK accumulator: union bitmap of all ranks' indices, per-slot
 // double sums (rank order = launch order), slot means -> packed for unpack
@@ -138,7 +137,7 @@ void launch_scatter_add_slot(const uint32_t* idx, const float* val, uint64_t k, 
                              const uint32_t* off, double* acc, cudaStream_t s);
 void launch_slot_mean(const double* acc, const uint32_t* total, uint64_t max_slots, int n, float* packed,
                       cudaStream_t s);
-void launch_f64_mean(const double* acc, uint64_t len, int n, float* out, cudaStream_t s);
+
 // out[idx[j]] = val[j] over a zero-filled out; err |= 1 on idx >= len
 void launch_scatter_f32(const uint32_t* idx, const float* val, uint64_t k, uint64_t len, float* out,
                         int* err, cudaStream_t s);

@@ -6,9 +6,10 @@
 // tie fix-up with the lower-index-first tie rule, prune.cu); here are the
 // payload kernels around it:
 //  * pack_index: ascending indices of the selected bits (the values come
-//    from pack_kernel over the same mask);
-//  * scatter_add_f64 / f64_mean: the per-element double accumulator over
-//    ranks in rank order, then float(acc / n);
+//    from pack_lm_kernel over the same mask);
+//  * union_bits / scatter_add_slot / slot_mean: the per-index double
+//    accumulator over ranks in rank order, then float(acc / n), kept only
+//    for the union of the ranks' indices (the unpack kernel expands it);
 //  * scatter_f32: topk_densify (zeros elsewhere, out-of-range -> error).
 #include "common.cuh"
 #include "launch.h"
@@ -38,26 +39,6 @@ __global__ void __launch_bounds__(256)
       bits &= bits - 1;
     }
   }
-}
-
-__global__ void scatter_add_f64_kernel(const uint32_t* __restrict__ idx, const float* __restrict__ val,
-                                       uint64_t k, uint64_t len, double* __restrict__ acc,
-                                       int* __restrict__ err) {
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < k; j += stride) {
-    const uint32_t i = idx[j];
-    if (i >= len) {
-      atomicOr(err, 1);
-      continue;
-    }
-    acc[i] += (double)val[j];
-  }
-}
-
-__global__ void f64_mean_kernel(const double* __restrict__ acc, uint64_t len, int n, float* __restrict__ out) {
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < len; i += stride)
-    out[i] = (float)(acc[i] / (double)n);
 }
 
 __global__ void scatter_f32_kernel(const uint32_t* __restrict__ idx, const float* __restrict__ val,
@@ -135,13 +116,6 @@ void launch_pack_index(uint64_t len, const uint64_t* words, const uint32_t* chun
   note_launch();
 }
 
-void launch_scatter_add_f64(const uint32_t* idx, const float* val, uint64_t k, uint64_t len, double* acc,
-                            int* err, cudaStream_t s) {
-  if (!k) return;
-  scatter_add_f64_kernel<<<grid_of(k), 256, 0, s>>>(idx, val, k, len, acc, err);
-  note_launch();
-}
-
 void launch_union_bits(const uint32_t* idx, uint64_t k, uint64_t len, uint64_t* words, int* err, cudaStream_t s) {
   if (!k) return;
   union_bits_kernel<<<grid_of(k), 256, 0, s>>>(idx, k, len, reinterpret_cast<unsigned long long*>(words), err);
@@ -159,12 +133,6 @@ void launch_slot_mean(const double* acc, const uint32_t* total, uint64_t max_slo
                       cudaStream_t s) {
   if (!max_slots) return;
   slot_mean_kernel<<<grid_of(max_slots), 256, 0, s>>>(acc, total, n, packed);
-  note_launch();
-}
-
-void launch_f64_mean(const double* acc, uint64_t len, int n, float* out, cudaStream_t s) {
-  if (!len) return;
-  f64_mean_kernel<<<grid_of(len), 256, 0, s>>>(acc, len, n, out);
   note_launch();
 }
 
