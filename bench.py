@@ -433,6 +433,10 @@ def main():
                  "step_exchange_us": round(t_x * 1e6, 1),
                  "step_exchange_busbw_gbs": round(4 * nnz * f / t_x / 1e9, 1),
                  "step_exchange_vs_dense_busbw": round((4 * nnz * f / t_x) / (4 * n * f / t_dense), 3),
+                 # NVLink 5: 900 GB/s per direction per GPU nominal (north_star); the
+                 # measured bidirectional SM-store rate is ~540 GB/s (tools/nvlink_probe.cu)
+                 "nvlink_peak_gbs": 900.0,
+                 "step_exchange_busbw_frac_of_nvlink": round(4 * nnz * f / t_x / 1e9 / 900.0, 3),
                  "dense_sync_equiv_gbs_per_rank": round(4 * n / t_dense / 1e9, 1)}
 
     # ---- e2e through the host-buffer C-ABI entry point
