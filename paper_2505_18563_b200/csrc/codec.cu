@@ -34,6 +34,16 @@ namespace pactk {
 namespace {
 
 constexpr int kCodecWarps = 8;  // 256-thread CTAs
+
+// PACT_P2P_TRACE diagnostics of the n = 2 push exchange (%globaltimer ns):
+// [0] pack entry (min) [1] pack exit (max) [2] unpack entry (min)
+// [3] unpack past the PACKED wait (max) [4] unpack exit (max)
+__device__ unsigned long long g_pair_trace[5];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 unsigned long long g_launches = 0;
 
 int sm_count() {
@@ -294,6 +304,8 @@ __global__ void __launch_bounds__(kPuWarps * 32)
   // `packed`. Only when the caller launches one: a PDL-capable successor of
   // another kind (e.g. a collective kernel) must not be let in early.
   if (pdl_trigger) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if constexpr (kPush != kPushNone)
+    if (threadIdx.x == 0) atomicMin(&g_pair_trace[0], gtimer());
   if (c < ce) {
     // prologue: words(c0), words(c1), data(c0)
     offs_words_issue(wsm[warp][0], words, chunk_off, c);
@@ -366,7 +378,10 @@ __global__ void __launch_bounds__(kPuWarps * 32)
       __syncwarp();
     }
   }
-  if constexpr (kPush != kPushNone) p2psync::exit_signal(v, sg);  // PACKED: every CTA's remote stores are done
+  if constexpr (kPush != kPushNone) {
+    p2psync::exit_signal(v, sg);  // PACKED: every CTA's remote stores are done
+    if (threadIdx.x == 0) atomicMax(&g_pair_trace[1], gtimer());
+  }
 }
 
 // kA = packed runs in flight ahead of the expansion. 2 halves the exposed
@@ -394,7 +409,9 @@ __global__ void __launch_bounds__(kPuWarps * 32)
   __shared__ __align__(16) uint64_t wsm[kPuWarps][kWS][kWbuf];
   if constexpr (kSrc != kSrcLocal) {  // peers' PACKED (one-shot) / REDUCED (two-shot) flags
     p2psync::entry_signal(v, sg);
+    if (threadIdx.x == 0) atomicMin(&g_pair_trace[2], gtimer());
     p2psync::block_wait_flags(flags, kSrc == kSrcPair ? kP2PPacked : kP2PReduced, v.n, target, err);
+    if (threadIdx.x == 0) atomicMax(&g_pair_trace[3], gtimer());
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const bool vec_ok = ((((uintptr_t)out) | (kSgd ? (uintptr_t)weights : 0)) & 15) == 0;
@@ -416,8 +433,10 @@ __global__ void __launch_bounds__(kPuWarps * 32)
   asm volatile("cp.async.wait_group 1;" ::: "memory");  // w0 .. w_{kA-1}
   __syncwarp();
   // launched as a programmatic dependent of the pack: the packed vector is
-  // complete and visible only past this point (no-op otherwise)
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+  // complete and visible only past this point (no-op otherwise). The NVLink
+  // variants need no grid dependency: the PACKED / REDUCED flags they waited
+  // for are published by the producers' last CTAs after all their stores.
+  if constexpr (kSrc == kSrcLocal) asm volatile("griddepcontrol.wait;" ::: "memory");
   for (int j = 0; j < kA; ++j) {
     if (c + j * nwt < ce) {
       uint32_t b, n;
@@ -537,7 +556,10 @@ __global__ void __launch_bounds__(kPuWarps * 32)
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
   }
-  if constexpr (kSrc != kSrcLocal) p2psync::exit_signal(v, sg);  // READ: peers may reuse their buffers
+  if constexpr (kSrc != kSrcLocal) {
+    p2psync::exit_signal(v, sg);  // READ: peers may reuse their buffers
+    if (threadIdx.x == 0) atomicMax(&g_pair_trace[4], gtimer());
+  }
 }
 
 // ------------------------------------------------------------------- GSE
@@ -727,6 +749,15 @@ __global__ void mask_gather_kernel(const uint64_t* __restrict__ src, uint64_t ns
 }  // namespace
 
 uint64_t launches() { return g_launches; }
+
+void pair_trace_reset(cudaStream_t s) {
+  unsigned long long init[5] = {~0ull, 0, ~0ull, 0, 0};
+  cudaMemcpyToSymbolAsync(g_pair_trace, init, sizeof init, 0, cudaMemcpyHostToDevice, s);
+}
+void pair_trace_read(unsigned long long out[5], cudaStream_t s) {
+  cudaMemcpyFromSymbolAsync(out, g_pair_trace, 5 * sizeof(unsigned long long), 0, cudaMemcpyDeviceToHost, s);
+  cudaStreamSynchronize(s);
+}
 void note_launch(uint64_t n) { g_launches += n; }
 
 void launch_pack(const float* g, uint64_t len, const uint64_t* words, const uint32_t* chunk_off,
@@ -819,6 +850,9 @@ void launch_unpack_p2p(const float* packed_local, uint64_t len, const uint64_t* 
     constexpr int kDyn = unpack_smem_bytes<kSrcPair, 1>();
     static int cap = 0;
     if (!cap) cap = persistent_grid_dyn(unpack_kernel<false, kSrcPair, 1>, kPuWarps, kDyn);
+    // (Tried: a programmatic dependent launch after the push pack, waiting on
+    // PACKED instead of the grid: the ~10 us gap after the push pack stays
+    // and long grids slow down -- c3 0.26 -> 0.36 ms, c5 1.00 -> 1.21 ms.)
     unpack_kernel<false, kSrcPair, 1><<<grid_for(cap, nc, kPuWarps), kPuWarps * 32, kDyn, s>>>(
         packed_local, len, words, chunk_off, scale, do_scale, out, 0.f, nullptr, 0, nc, v, flags, target,
         err, sg);

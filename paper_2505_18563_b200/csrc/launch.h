@@ -29,6 +29,9 @@ struct P2PSig {
 };
 
 // ---- codec.cu --------------------------------------------------------------
+// PACT_P2P_TRACE diagnostics of the n = 2 push exchange (codec.cu)
+void pair_trace_reset(cudaStream_t s);
+void pair_trace_read(unsigned long long out[5], cudaStream_t s);
 // chunk range [cb, ce) of 1024-element chunks; all pointers device.
 // pdl_trigger: let a programmatic dependent (launch_unpack(..., pdl)) start early
 void launch_pack(const float* g, uint64_t len, const uint64_t* words, const uint32_t* chunk_off,

@@ -1840,6 +1840,8 @@ pact_status pact_masked_allreduce(pact_comm* c, pact_ctx* ctx, const float* grad
       sgp.exit_kind = pactk::kP2PPacked;
       sgp.exit_val = fval(0);
       sgp.counter = p2p_counter(p, c->rank);
+      static const bool trace = getenv("PACT_P2P_TRACE") != nullptr;
+      if (trace) pactk::pair_trace_reset(s);
       pactk::launch_pack_push(grad, len, m->words, m->tile_off, mine, p2p_reduced(p, peer, par), v, sgp, s);
       mark(0);
       mark(1);
@@ -1851,6 +1853,15 @@ pact_status pact_masked_allreduce(pact_comm* c, pact_ctx* ctx, const float* grad
       sgu.counter = sgp.counter;
       pactk::launch_unpack_p2p(mine, len, m->words, m->tile_off, scale, scale != 1.0f, out, vin, 0, myflags,
                                fval(0), err, sgu, s);
+      if (trace) {
+        unsigned long long t[5];
+        pactk::pair_trace_read(t, s);
+        fprintf(stderr,
+                "[pact p2p trace rank %d] pack %.1f us | gap %.1f | PACKED wait %.1f | unpack body %.1f | "
+                "pack exit %llu unpack pass %llu\n",
+                c->rank, (t[1] - t[0]) * 1e-3, ((double)t[2] - (double)t[1]) * 1e-3, ((double)t[3] - (double)t[2]) * 1e-3,
+                ((double)t[4] - (double)t[3]) * 1e-3, t[1], t[3]);
+      }
       mark(2);
       p.k = k1;
       nbuckets = 1;
