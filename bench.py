@@ -361,10 +361,13 @@ def main():
         barrier()
     launches = ctx.kernel_launches() - l0
     t_step = sum(ts) / len(ts)
+    qs = sorted(ts)
+    pct = [qs[int(q * (len(qs) - 1))] for q in (0.1, 0.5, 0.9)]
     if world > 1:
-        tt = torch.tensor([t_step], dtype=torch.float64, device=dev)
+        tt = torch.tensor([t_step] + pct, dtype=torch.float64, device=dev)
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-        t_step = float(tt.item())
+        t_step, pct = float(tt[0].item()), [float(x) for x in tt[1:].tolist()]
+    step_dist = {"p10_us": round(pct[0] * 1e6, 1), "p50_us": round(pct[1] * 1e6, 1), "p90_us": round(pct[2] * 1e6, 1)}
     per_rank_gbs = 4.0 * n / t_step / 1e9
     value = per_rank_gbs * world
 
@@ -485,6 +488,7 @@ def main():
                        "parallelism": f"dp{world}", "bucket_bytes": policy.bucket_bytes,
                        "transport": ["none", "nccl", "nvlink-p2p"][r.stats.transport],
                        "per_rank_gbs": round(per_rank_gbs, 2)},
+            "step_distribution": step_dist,
             "roofline": roofline, "stages": stages, **({"allreduce": extra} if extra else {}),
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clk.summary(),

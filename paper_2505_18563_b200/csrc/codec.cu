@@ -305,7 +305,7 @@ __global__ void __launch_bounds__(kPuWarps * 32)
   // another kind (e.g. a collective kernel) must not be let in early.
   if (pdl_trigger) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if constexpr (kPush != kPushNone)
-    if (threadIdx.x == 0) atomicMin(&g_pair_trace[0], gtimer());
+    if (sg.trace && threadIdx.x == 0) atomicMin(&g_pair_trace[0], gtimer());
   if (c < ce) {
     // prologue: words(c0), words(c1), data(c0)
     offs_words_issue(wsm[warp][0], words, chunk_off, c);
@@ -380,7 +380,7 @@ __global__ void __launch_bounds__(kPuWarps * 32)
   }
   if constexpr (kPush != kPushNone) {
     p2psync::exit_signal(v, sg);  // PACKED: every CTA's remote stores are done
-    if (threadIdx.x == 0) atomicMax(&g_pair_trace[1], gtimer());
+    if (sg.trace && threadIdx.x == 0) atomicMax(&g_pair_trace[1], gtimer());
   }
 }
 
@@ -409,9 +409,9 @@ __global__ void __launch_bounds__(kPuWarps * 32)
   __shared__ __align__(16) uint64_t wsm[kPuWarps][kWS][kWbuf];
   if constexpr (kSrc != kSrcLocal) {  // peers' PACKED (one-shot) / REDUCED (two-shot) flags
     p2psync::entry_signal(v, sg);
-    if (threadIdx.x == 0) atomicMin(&g_pair_trace[2], gtimer());
+    if (sg.trace && threadIdx.x == 0) atomicMin(&g_pair_trace[2], gtimer());
     p2psync::block_wait_flags(flags, kSrc == kSrcPair ? kP2PPacked : kP2PReduced, v.n, target, err);
-    if (threadIdx.x == 0) atomicMax(&g_pair_trace[3], gtimer());
+    if (sg.trace && threadIdx.x == 0) atomicMax(&g_pair_trace[3], gtimer());
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const bool vec_ok = ((((uintptr_t)out) | (kSgd ? (uintptr_t)weights : 0)) & 15) == 0;
@@ -558,7 +558,7 @@ __global__ void __launch_bounds__(kPuWarps * 32)
   }
   if constexpr (kSrc != kSrcLocal) {
     p2psync::exit_signal(v, sg);  // READ: peers may reuse their buffers
-    if (threadIdx.x == 0) atomicMax(&g_pair_trace[4], gtimer());
+    if (sg.trace && threadIdx.x == 0) atomicMax(&g_pair_trace[4], gtimer());
   }
 }
 

@@ -26,6 +26,7 @@ struct P2PSig {
   int exit_kind = -1;
   uint64_t exit_val = 0;
   unsigned* counter = nullptr;
+  int trace = 0;  // PACT_P2P_TRACE: stamp the push exchange's phases (codec.cu)
 };
 
 // ---- codec.cu --------------------------------------------------------------

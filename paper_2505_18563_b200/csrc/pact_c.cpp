@@ -1841,6 +1841,7 @@ pact_status pact_masked_allreduce(pact_comm* c, pact_ctx* ctx, const float* grad
       sgp.exit_val = fval(0);
       sgp.counter = p2p_counter(p, c->rank);
       static const bool trace = getenv("PACT_P2P_TRACE") != nullptr;
+      sgp.trace = trace;
       if (trace) pactk::pair_trace_reset(s);
       pactk::launch_pack_push(grad, len, m->words, m->tile_off, mine, p2p_reduced(p, peer, par), v, sgp, s);
       mark(0);
@@ -1851,6 +1852,7 @@ pact_status pact_masked_allreduce(pact_comm* c, pact_ctx* ctx, const float* grad
       sgu.exit_kind = pactk::kP2PRead;
       sgu.exit_val = k1;
       sgu.counter = sgp.counter;
+      sgu.trace = trace;
       pactk::launch_unpack_p2p(mine, len, m->words, m->tile_off, scale, scale != 1.0f, out, vin, 0, myflags,
                                fval(0), err, sgu, s);
       if (trace) {
