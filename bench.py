@@ -163,7 +163,7 @@ def run_reference(args, cfg):
                          "sample": what + f"; {args.steps} steps, full {model} gradient per step"},
         "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    _emit(line)
 
 
 METRIC = "dense-equiv. gradient sync GB/s (prune+pack+allreduce+unpack)"
@@ -225,7 +225,29 @@ def cpu_baseline_sample(shape, ratio, words_np, n):
                       f"{nthreads} thread slices, median of {len(ts)} runs (~10 s)"}
 
 
+_JSON_OUT = None
+
+
+def _emit(line):
+    """The contract's one JSON line, on the process's original stdout."""
+    out = _JSON_OUT or sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
+
+
+def _stdout_to_stderr():
+    """Native libraries (NCCL's version banner under NCCL_DEBUG=VERSION, seen
+    on stdout at communicator init despite NCCL_DEBUG_FILE) write to fd 1
+    directly; point fd 1 at stderr for the whole run and keep a private copy
+    of the original stdout for the JSON line."""
+    global _JSON_OUT
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
+
+
 def main():
+    _stdout_to_stderr()
     # the image sets NCCL_DEBUG=VERSION: NCCL prints its version (and any
     # warnings) to stdout at communicator init; the contract is ONE JSON line
     # on stdout, so NCCL's log goes to stderr instead
@@ -493,7 +515,7 @@ def main():
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clk.summary(),
         }
-        print(json.dumps(line), flush=True)
+        _emit(line)
     if comm is not None:
         torch.distributed.barrier()
         comm.close()
@@ -552,7 +574,7 @@ def run_sweep(args, pb, torch, comm, rank, world, local, dev, cfg, model, n, wei
                             "t_dense_us": round(cal.t_dense * 1e6, 1)},
             "sweep": rows,
         }
-        print(json.dumps(line), flush=True)
+        _emit(line)
     if comm is not None:
         torch.distributed.barrier()
         comm.close()
@@ -634,7 +656,7 @@ def run_path(args, pb, torch, comm, rank, world, local, dev, cfg, model, ratio, 
                          "peak_kind": peak_kind, "algorithmic_bytes": int(alg)},
             "gpu_launches": int(launches), "clocks": clk.summary(),
         }
-        print(json.dumps(line), flush=True)
+        _emit(line)
     if comm is not None:
         torch.distributed.barrier()
         comm.close()
