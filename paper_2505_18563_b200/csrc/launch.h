@@ -115,6 +115,20 @@ void launch_prune_count(const float* w, uint64_t len, const PruneWindow* win_dev
 // u32 keys. hist (1<<nbits u32) is zeroed by the launcher.
 void launch_prune_hist(const void* src, int from_float, uint64_t n, uint32_t base, int shift,
                        int nbits, uint32_t prefix, uint32_t* hist, cudaStream_t s);
+// Device-resident radix select: the digit prefix is read from sel->prefix
+// (0 on the first pass), and a 1-CTA pick kernel consumes the histogram:
+// d = first digit whose inclusive count reaches rem (the host loop of
+// select_rank, run on the device), then rem -= counts below d, below += the
+// same, prefix = prefix << nbits | d; err = 1 if the histogram holds < rem.
+struct SelState {
+  uint32_t prefix;
+  int err;
+  unsigned long long rem, below;
+};
+void launch_prune_hist_sel(const void* src, int from_float, uint64_t n, uint32_t base, int shift,
+                           int nbits, int first, const SelState* sel, uint32_t* hist, cudaStream_t s);
+void launch_prune_pick(const uint32_t* hist, int nbits, int first, uint64_t rank, SelState* sel,
+                       cudaStream_t s);
 // full read: words (written only where they change) + per-chunk kept counts;
 // ties resolved against tie_prefix (per chunk) or all dropped if it is null;
 // per-chunk tie counts -> ties_out (compared with ties_prev when given), tie

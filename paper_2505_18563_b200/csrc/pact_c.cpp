@@ -229,6 +229,7 @@ struct Small {
   int pad1[3];
   uint32_t hist[2048];
   pactk::BitmapCounts bcounts;
+  pactk::SelState sel;
 };
 
 pact_status set_device(pact_ctx* ctx) {
@@ -780,29 +781,31 @@ namespace {
 pact_status select_rank(pact_ctx* ctx, const void* src, int from_float, uint64_t n, uint32_t base,
                         int bits, uint64_t rank, cudaStream_t s, uint32_t* value,
                         uint64_t* below) {
+  // the digit walk stays on the device (hist -> pick per 11-bit digit); one
+  // readback of the final state instead of one per digit
   Small* sm = ctx->ws_small.as<Small>();
-  uint32_t* pin = ctx->pin.as<uint32_t>();
-  uint32_t prefix = 0;
-  uint64_t rem = rank, blw = 0;
-  int hi = bits;
+  int hi = bits, first = 1;
   while (hi > 0) {
     const int nb = std::min(11, hi);
     const int shift = hi - nb;
-    pactk::launch_prune_hist(src, from_float, n, base, shift, nb, prefix, sm->hist, s);
-    CUDA_TRY(cudaMemcpyAsync(pin, sm->hist, sizeof(uint32_t) << nb, cudaMemcpyDeviceToHost, s));
-    CUDA_TRY(cudaStreamSynchronize(s));
-    uint32_t d = 0;
-    while (d < (1u << nb) && pin[d] < rem) {
-      rem -= pin[d];
-      blw += pin[d];
-      ++d;
-    }
-    if (d >= (1u << nb)) return fail(PACT_E_RUN_FAILURE, "radix select lost its rank");
-    prefix = (prefix << nb) | d;
+    pactk::launch_prune_hist_sel(src, from_float, n, base, shift, nb, first, &sm->sel, sm->hist, s);
+    pactk::launch_prune_pick(sm->hist, nb, first, rank, &sm->sel, s);
+    first = 0;
     hi = shift;
   }
-  *value = prefix;
-  *below = blw;
+  if (first) {  // bits == 0: nothing to select
+    *value = 0;
+    *below = 0;
+    return PACT_OK;
+  }
+  CUDA_TRY(cudaGetLastError());
+  pactk::SelState st{};
+  CUDA_TRY(cudaMemcpyAsync(ctx->pin.p, &sm->sel, sizeof st, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  std::memcpy(&st, ctx->pin.p, sizeof st);
+  if (st.err) return fail(PACT_E_RUN_FAILURE, "radix select lost its rank");
+  *value = st.prefix;
+  *below = st.below;
   return PACT_OK;
 }
 
@@ -1375,8 +1378,11 @@ pact_status pact_topk_count(uint64_t len, float rate, uint64_t* k_out) {
 namespace {
 // selection bitmap of the k largest |g| (ties -> lower index): the prune
 // machinery with k_drop = len - k, whose tie fix-up keeps the LOW ranks
+// nnz_pin: null -> the selected count is read back and checked here; else
+// its copy is only enqueued into *nnz_pin and the caller checks it after its
+// own synchronisation (one host round trip fewer on the aggregate path).
 pact_status topk_mask(pact_ctx* ctx, const float* g, uint64_t len, uint64_t k, cudaStream_t s,
-                      pact_mask** out) {
+                      pact_mask** out, uint32_t* nnz_pin = nullptr) {
   if (!ctx->topk_sel || ctx->topk_sel->len != len) {
     if (ctx->topk_sel) pact_mask_destroy(ctx->topk_sel);
     ctx->topk_sel = nullptr;
@@ -1388,7 +1394,10 @@ pact_status topk_mask(pact_ctx* ctx, const float* g, uint64_t len, uint64_t k, c
   m->digest_valid = 0;
   m->spec_valid = 0;
   const uint64_t kd = len - k;
-  if (kd == 0 || len == 0) return pact_mask_fill(m, 1, s);
+  if (kd == 0 || len == 0) {
+    if (nnz_pin) *nnz_pin = (uint32_t)k;
+    return pact_mask_fill(m, 1, s);
+  }
   const uint64_t nc = m->ntiles;
   TRY(m->tie_words.ensure(m->nwords * 8));
   TRY(m->ties[0].ensure(nc * 4));
@@ -1416,6 +1425,12 @@ pact_status topk_mask(pact_ctx* ctx, const float* g, uint64_t len, uint64_t k, c
   }
   m->ties_cur = 0;
   TRY(scan(ctx, m->tile_popc, nc, m->tile_off, s));
+  m->host_tile_off_valid = 0;
+  if (nnz_pin) {
+    CUDA_TRY(cudaMemcpyAsync(nnz_pin, m->tile_off + nc, 4, cudaMemcpyDeviceToHost, s));
+    m->nnz = k;  // verified by the caller
+    return PACT_OK;
+  }
   uint32_t* pin32 = ctx->pin.as<uint32_t>();
   CUDA_TRY(cudaMemcpyAsync(pin32, m->tile_off + nc, 4, cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaStreamSynchronize(s));
@@ -1428,8 +1443,10 @@ pact_status topk_mask(pact_ctx* ctx, const float* g, uint64_t len, uint64_t k, c
 }
 }  // namespace
 
-pact_status pact_topk_select(pact_ctx* ctx, const float* grad, uint64_t len, float rate,
-                             uint32_t* indices, float* values, uint64_t* k_out, pact_stream_t stream) {
+namespace {
+pact_status topk_select_impl(pact_ctx* ctx, const float* grad, uint64_t len, float rate,
+                             uint32_t* indices, float* values, uint64_t* k_out, pact_stream_t stream,
+                             uint32_t* nnz_pin) {
   if (!ctx || (len && !grad)) return fail(PACT_E_INVALID_ARG, "null args");
   uint64_t k = 0;
   TRY(pact_topk_count(len, rate, &k));
@@ -1440,13 +1457,19 @@ pact_status pact_topk_select(pact_ctx* ctx, const float* grad, uint64_t len, flo
   cudaStream_t s = stream;
   if (len) {
     pact_mask* m = nullptr;
-    TRY(topk_mask(ctx, grad, len, k, s, &m));
+    TRY(topk_mask(ctx, grad, len, k, s, &m, nnz_pin));
     pactk::launch_pack(grad, len, m->words, m->tile_off, values, 0, m->ntiles, s);
     pactk::launch_pack_index(len, m->words, m->tile_off, indices, s);
     CUDA_TRY(cudaGetLastError());
   }
   if (k_out) *k_out = k;
   return PACT_OK;
+}
+}  // namespace
+
+pact_status pact_topk_select(pact_ctx* ctx, const float* grad, uint64_t len, float rate,
+                             uint32_t* indices, float* values, uint64_t* k_out, pact_stream_t stream) {
+  return topk_select_impl(ctx, grad, len, rate, indices, values, k_out, stream, nullptr);
 }
 
 pact_status pact_topk_densify(pact_ctx* ctx, const uint32_t* indices, const float* values, uint64_t k,
@@ -1498,7 +1521,8 @@ pact_status pact_topk_allgather_aggregate(pact_comm* c, pact_ctx* ctx, const flo
   int* err = reinterpret_cast<int*>(&ctx->ws_small.as<Small>()->changed);
   CUDA_TRY(cudaMemsetAsync(err, 0, 4, s));
   if (len) {
-    TRY(pact_topk_select(ctx, grad, len, rate, own, reinterpret_cast<float*>(own + k), nullptr, s));
+    uint32_t* nnz_pin = ctx->pin.as<uint32_t>() + 16;  // checked after the final synchronisation
+    TRY(topk_select_impl(ctx, grad, len, rate, own, reinterpret_cast<float*>(own + k), nullptr, s, nnz_pin));
     const uint32_t* blocks = own;
     if (c) {
       NCCL_TRY(ncclAllGather(own, all, blk * 4, ncclUint8, c->nccl, s));
@@ -1529,6 +1553,9 @@ pact_status pact_topk_allgather_aggregate(pact_comm* c, pact_ctx* ctx, const flo
     int* pin = ctx->pin.as<int>();
     CUDA_TRY(cudaMemcpyAsync(pin, err, 4, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));
+    if (nnz_pin[0] != k)
+      return fail(PACT_E_RUN_FAILURE, "topk selected %llu, expected %llu", (unsigned long long)nnz_pin[0],
+                  (unsigned long long)k);
     if (pin[0]) return fail(PACT_E_CORRUPT_PAYLOAD, "topk index out of range");
   }
   if (stats) {

@@ -235,8 +235,9 @@ __global__ void __launch_bounds__(kPruneWarps * 32)
 template <bool kFloat>
 __global__ void __launch_bounds__(256)
     prune_hist_kernel(const void* __restrict__ src, uint64_t n, uint32_t base, int shift, int nbits,
-                      uint32_t prefix, uint32_t* __restrict__ ghist) {
+                      uint32_t prefix, uint32_t* __restrict__ ghist, const SelState* __restrict__ sel) {
   extern __shared__ uint32_t sh[];
+  if (sel) prefix = sel->prefix;
   const int nb = 1 << nbits;
   for (int b = threadIdx.x; b < nb; b += blockDim.x) sh[b] = 0;
   __syncthreads();
@@ -256,6 +257,60 @@ __global__ void __launch_bounds__(256)
   __syncthreads();
   for (int b = threadIdx.x; b < nb; b += blockDim.x)
     if (sh[b]) atomicAdd(&ghist[b], sh[b]);
+}
+
+// 1 CTA of 1024 threads, bins 2t and 2t + 1 per thread (nbits <= 11): block
+// exclusive scan of the counts, the one thread whose bins straddle rem
+// updates the state. Same digit as select_rank's host loop (first bin whose
+// inclusive count >= rem; bin 0 when rem == 0).
+__global__ void __launch_bounds__(1024)
+    prune_pick_kernel(const uint32_t* __restrict__ hist, int nbits, int first, uint64_t rank,
+                      SelState* __restrict__ sel) {
+  __shared__ unsigned long long wsum[32], s_total;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int nb = 1 << nbits;
+  const uint64_t a = 2 * t < nb ? hist[2 * t] : 0u, b = 2 * t + 1 < nb ? hist[2 * t + 1] : 0u;
+  const uint64_t rem = first ? rank : sel->rem;
+  const uint32_t prefix = first ? 0u : sel->prefix;
+  const uint64_t below = first ? 0ull : sel->below;
+  uint64_t inc = a + b;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint64_t y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  if (lane == 31) wsum[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    uint64_t x = wsum[lane], xi = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint64_t y = __shfl_up_sync(0xffffffffu, xi, o);
+      if (lane >= o) xi += y;
+    }
+    wsum[lane] = xi - x;
+    if (lane == 31) s_total = xi;
+  }
+  __syncthreads();
+  const uint64_t e0 = wsum[warp] + inc - (a + b), total = s_total;
+  int d = -1;
+  uint64_t eb = 0;
+  if (rem == 0) {
+    if (t == 0) d = 0;
+  } else if (e0 < rem && rem <= e0 + a) {
+    d = 2 * t;
+    eb = e0;
+  } else if (e0 + a < rem && rem <= e0 + a + b) {
+    d = 2 * t + 1;
+    eb = e0 + a;
+  }
+  if (d >= 0) {
+    sel->prefix = (prefix << nbits) | (uint32_t)d;
+    sel->rem = rem - eb;
+    sel->below = below + eb;
+    if (first) sel->err = 0;
+  }
+  if (t == 0 && total < rem) sel->err = 1;
 }
 
 // ---------------------------------------------------------------- bitmap
@@ -571,10 +626,32 @@ void launch_prune_hist(const void* src, int from_float, uint64_t n, uint32_t bas
   const size_t smem = sizeof(uint32_t) << nbits;
   if (from_float)
     prune_hist_kernel<true><<<(unsigned)blocks, 256, smem, s>>>(src, n, base, shift, nbits, prefix,
-                                                               hist);
+                                                               hist, nullptr);
   else
     prune_hist_kernel<false><<<(unsigned)blocks, 256, smem, s>>>(src, n, base, shift, nbits,
-                                                                prefix, hist);
+                                                                prefix, hist, nullptr);
+  note_launch();
+}
+
+void launch_prune_hist_sel(const void* src, int from_float, uint64_t n, uint32_t base, int shift,
+                           int nbits, int first, const SelState* sel, uint32_t* hist, cudaStream_t s) {
+  cudaMemsetAsync(hist, 0, sizeof(uint32_t) << nbits, s);
+  uint64_t blocks = (n + 255) / 256;
+  const uint64_t cap = (uint64_t)num_sms() * 8;
+  if (blocks > cap) blocks = cap;
+  if (blocks == 0) blocks = 1;
+  const size_t smem = sizeof(uint32_t) << nbits;
+  const SelState* sp = first ? nullptr : sel;  // first pass: prefix 0
+  if (from_float)
+    prune_hist_kernel<true><<<(unsigned)blocks, 256, smem, s>>>(src, n, base, shift, nbits, 0u, hist, sp);
+  else
+    prune_hist_kernel<false><<<(unsigned)blocks, 256, smem, s>>>(src, n, base, shift, nbits, 0u, hist, sp);
+  note_launch();
+}
+
+void launch_prune_pick(const uint32_t* hist, int nbits, int first, uint64_t rank, SelState* sel,
+                       cudaStream_t s) {
+  prune_pick_kernel<<<1, 1024, 0, s>>>(hist, nbits, first, rank, sel);
   note_launch();
 }
 
