@@ -6,6 +6,19 @@
 
 namespace pactk {
 
+// Host-side launcher caches (occupancy grids, dynamic-smem opt-ins) are per
+// DEVICE: one process may drive several GPUs (thread per GPU), and
+// cudaFuncSetAttribute applies to the current device's context only.
+template <typename T>
+struct DeviceCache {
+  T v[64] = {};
+  T& get() {
+    int d = 0;
+    cudaGetDevice(&d);
+    return v[d & 63];
+  }
+};
+
 // Offset granularity of a mask: one warp work unit of pack/unpack.
 constexpr int kChunk = 1024;             // elements (= PACT_TILE)
 constexpr int kChunkWords = kChunk / 64; // 16 words

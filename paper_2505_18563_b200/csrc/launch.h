@@ -101,7 +101,19 @@ struct PruneCounts {  // device-side accumulators (zeroed by the launcher)
 };
 struct BitmapCounts {  // zeroed by launch_prune_bitmap
   unsigned long long n_lt, n_eq;
-  int changed, tie_mismatch;
+  int changed, tie_mismatch;     // changed: a word bit outside the candidates
+  unsigned long long n_cand_below;  // candidates with key < T (#(key < lo) = n_lt - this)
+  unsigned long long n_cand;     // window candidates seen (may exceed cand.cap)
+  int changed_cand, fix_changed;  // a candidate bit changed (bitmap pass / after a fix-up)
+};
+// Window candidates of the bitmap pass (temporal reuse, prune.cu): elements
+// with lo <= key <= hi and key != T are compacted as key[j], idx[j] | (the
+// element's PREVIOUS mask bit << 31). lo > hi disables the window.
+struct PruneCandBuf {
+  uint32_t lo = 1, hi = 0;
+  uint32_t* key = nullptr;
+  uint32_t* idx = nullptr;
+  uint64_t cap = 0;
 };
 // 1 CTA: strided sample of keys, sorted; writes the [lo, hi] window.
 void launch_prune_sample(const float* w, uint64_t len, uint64_t k, PruneWindow* win_dev,
@@ -124,6 +136,7 @@ struct SelState {
   uint32_t prefix;
   int err;
   unsigned long long rem, below;
+  unsigned long long eq;  // elements in the picked bin (after the last digit: #(key == result))
 };
 void launch_prune_hist_sel(const void* src, int from_float, uint64_t n, uint32_t base, int shift,
                            int nbits, int first, const SelState* sel, uint32_t* hist, cudaStream_t s);
@@ -136,7 +149,22 @@ void launch_prune_pick(const uint32_t* hist, int nbits, int first, uint64_t rank
 void launch_prune_bitmap(const float* w, uint64_t len, uint32_t T, uint64_t r,
                          const uint32_t* tie_prefix, uint64_t* words, uint32_t* chunk_popc,
                          uint32_t* ties_out, const uint32_t* ties_prev, uint64_t* tie_words,
-                         BitmapCounts* counts, cudaStream_t s);
+                         BitmapCounts* counts, cudaStream_t s, const PruneCandBuf& cand = PruneCandBuf{});
+// Window fix-up once the true threshold T' of a moved mask is known (it lies
+// in the window, T' != the pass's T): every candidate gets key > T' (ties at
+// T' provisionally dropped; with `straddle` their bits go to tie_words and
+// per-chunk counts to ties for the tie fix-up); words by 64-bit atomics,
+// chunk_popc adjusted by the flips. tie_clear first zeroes the tie words of
+// every chunk holding a T'-tie.
+void launch_prune_cand_fix(const uint32_t* key, const uint32_t* idx, uint64_t n, uint32_t T, int straddle,
+                           uint64_t* words, uint32_t* chunk_popc, uint64_t* tie_words, uint32_t* ties,
+                           int* changed, cudaStream_t s);
+void launch_prune_cand_tieclear(const uint32_t* key, const uint32_t* idx, uint64_t n, uint32_t T,
+                                uint64_t* tie_words, cudaStream_t s);
+// *flag = 1 if a tie candidate's (key == T) final bit differs from its
+// recorded previous bit (the fix-up checks the others into the same flag)
+void launch_prune_cand_changed(const uint32_t* key, const uint32_t* idx, uint64_t n, uint32_t T,
+                               const uint64_t* words, int* flag, cudaStream_t s);
 // exact tie bits from the exact tie prefix; updates chunk_popc of tie chunks.
 // Ties of global rank < r dropped (prune) or, keep_low, kept (TopK)
 void launch_prune_tiefix(uint64_t* words, uint64_t len, const uint64_t* tie_words,

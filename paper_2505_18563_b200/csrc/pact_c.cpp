@@ -166,8 +166,15 @@ struct pact_mask {
   DevBuf tie_prefix;  // nchunks + 1 exclusive prefix of ties[cur]
   int ties_cur = 0;
   int spec_valid = 0;
+  int spec_prefix_valid = 0;  // tie_prefix / ties[ties_cur] describe the ties at spec_T
   uint64_t spec_k = 0, spec_c_lt = 0;
   uint32_t spec_T = 0;
+  // key window [win_lo, win_hi] around spec_T (about +-len/1024 ranks): the
+  // bitmap pass compacts its elements, so a MOVED threshold is resolved from
+  // them instead of another full read of the weights
+  int win_valid = 0;
+  uint32_t win_lo = 1, win_hi = 0;
+  DevBuf cand_key, cand_idx;
 };
 
 namespace {
@@ -660,6 +667,8 @@ pact_status pact_mask_destroy(pact_mask* m) {
   m->ties[0].release();
   m->ties[1].release();
   m->tie_prefix.release();
+  m->cand_key.release();
+  m->cand_idx.release();
   delete m;
   return PACT_OK;
 }
@@ -907,6 +916,13 @@ pact_status pact_prune_magnitude(pact_ctx* ctx, const float* w, uint64_t len, fl
   TRY(out->ties[0].ensure(nc * 4));
   TRY(out->ties[1].ensure(nc * 4));
   TRY(out->tie_prefix.ensure((nc + 1) * 4));
+  // window half-width (ranks) and candidate capacity
+  const uint64_t mwin = std::max<uint64_t>(4096, len >> 10);
+  const uint64_t ccap = 4 * mwin + 65536;
+  TRY(out->cand_key.ensure(ccap * 4));
+  TRY(out->cand_idx.ensure(ccap * 4));
+  uint32_t* ckey = out->cand_key.as<uint32_t>();
+  uint32_t* cidx = out->cand_idx.as<uint32_t>();
   Small* sm = ctx->ws_small.as<Small>();
   pactk::BitmapCounts* bc = &sm->bcounts;
   pactk::BitmapCounts hb{};
@@ -915,19 +931,27 @@ pact_status pact_prune_magnitude(pact_ctx* ctx, const float* w, uint64_t len, fl
   bool done = false;
 
   // one bitmap pass at (T, r); tie prefix from the previous call (spec) or
-  // "all ties dropped" (prefix null); returns the pass's own counts
-  auto bitmap = [&](uint32_t T, uint64_t r, bool use_prefix, bool compare_prev) -> pact_status {
+  // "all ties dropped" (prefix null); window candidates when win; returns
+  // the pass's own counts
+  auto bitmap = [&](uint32_t T, uint64_t r, bool use_prefix, bool compare_prev, bool win) -> pact_status {
     const int nxt = out->ties_cur ^ 1;
+    pactk::PruneCandBuf cb;
+    if (win && out->win_valid) {
+      cb.lo = out->win_lo;
+      cb.hi = out->win_hi;
+      cb.key = ckey;
+      cb.idx = cidx;
+      cb.cap = ccap;
+    }
     pactk::launch_prune_bitmap(w, len, T, r, use_prefix ? out->tie_prefix.as<uint32_t>() : nullptr,
                                out->words, out->tile_popc, out->ties[nxt].as<uint32_t>(),
                                compare_prev ? out->ties[out->ties_cur].as<uint32_t>() : nullptr,
-                               out->tie_words.as<uint64_t>(), bc, s);
+                               out->tie_words.as<uint64_t>(), bc, s, cb);
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cudaMemcpyAsync(ctx->pin.p, bc, sizeof hb, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));
     std::memcpy(&hb, ctx->pin.p, sizeof hb);
     out->ties_cur = nxt;
-    changed |= hb.changed;
     return PACT_OK;
   };
   // exact tie bits once the true (T, r) and per-chunk tie counts are known
@@ -937,34 +961,144 @@ pact_status pact_prune_magnitude(pact_ctx* ctx, const float* w, uint64_t len, fl
     pactk::launch_prune_tiefix(out->words, len, out->tie_words.as<uint64_t>(), ties,
                                out->tie_prefix.as<uint32_t>(), r, out->tile_popc, s);
     CUDA_TRY(cudaGetLastError());
+    out->spec_prefix_valid = 1;
     changed = 1;  // conservative: the digest is recomputed on demand
     return PACT_OK;
   };
+  // the window for the next call: keys at candidate ranks q0, q1 (1-based,
+  // clamped) of the n candidate keys at src (key' = key - base < 2^bits)
+  auto set_window = [&](const uint32_t* src, uint64_t n, uint32_t base, uint32_t top, int64_t q0, int64_t q1,
+                        uint32_t T) -> pact_status {
+    out->win_valid = 0;
+    if (n == 0) return PACT_OK;
+    const int bits = bit_length(top - base);
+    uint32_t v0 = 0, v1 = 0;
+    uint64_t below = 0;
+    q0 = std::max<int64_t>(1, std::min<int64_t>(q0, (int64_t)n));
+    q1 = std::max<int64_t>(1, std::min<int64_t>(q1, (int64_t)n));
+    if (bits > 0) {
+      TRY(select_rank(ctx, src, 0, n, base, bits, (uint64_t)q0, s, &v0, &below));
+      TRY(select_rank(ctx, src, 0, n, base, bits, (uint64_t)q1, s, &v1, &below));
+    }
+    out->win_lo = std::min(base + v0, T);
+    out->win_hi = std::max(base + v1, T);
+    out->win_valid = 1;
+    return PACT_OK;
+  };
 
-  // (0) temporal reuse: previous threshold, verified by the pass itself
+  // (0) temporal reuse: the previous threshold, verified by the pass itself
   if (out->spec_valid && out->spec_k == k) {
+    const uint32_t T0 = out->spec_T;
     const uint64_t r0 = k - out->spec_c_lt;
-    TRY(bitmap(out->spec_T, r0, true, true));
+    const bool pv = out->spec_prefix_valid;
+    if (out->win_valid && !(out->win_lo <= T0 && T0 <= out->win_hi)) out->win_valid = 0;
+    TRY(bitmap(T0, r0, pv, pv, true));
     if (hb.n_lt < k && k <= hb.n_lt + hb.n_eq) {  // threshold still the k-th key
+      changed |= hb.changed | hb.changed_cand;
       const uint64_t r = k - hb.n_lt;
-      if (r != r0 || hb.tie_mismatch) TRY(fix_ties(r));
+      if (pv ? (r != r0 || hb.tie_mismatch) : r < hb.n_eq) TRY(fix_ties(r));
       st.path = 3;
-      st.threshold = out->spec_T;
+      st.threshold = T0;
       st.c_lt = hb.n_lt;
+      st.candidates = hb.n_cand;
       out->spec_c_lt = hb.n_lt;
       done = true;
-    } else {
-      changed = 1;
+    } else if (out->win_valid && hb.n_cand <= ccap) {
+      // (0') the threshold moved: the k-th key lies in the window when
+      // n_below < k <= n_below + (candidates) + (ties at T0, not compacted)
+      const uint64_t E0 = hb.n_eq, ncand = hb.n_cand;
+      const uint64_t n_below = hb.n_lt - hb.n_cand_below;  // #(key < win_lo)
+      if (n_below < k && k <= n_below + ncand + E0) {
+        const bool up = k > hb.n_lt + hb.n_eq;  // T' > T0 (else T' < T0)
+        const uint64_t rho = k - n_below - (up ? E0 : 0);  // rank among the candidates
+        uint32_t rel = 0;
+        uint64_t below = 0;
+        const uint32_t base = out->win_lo;
+        const int bits = bit_length(out->win_hi - base);
+        TRY(select_rank(ctx, ckey, 0, ncand, base, bits, rho, s, &rel, &below));
+        pactk::SelState sel{};
+        std::memcpy(&sel, ctx->pin.p, sizeof sel);  // select_rank left its state in pin
+        const uint32_t T1 = base + rel;
+        const uint64_t eq1 = bits > 0 ? sel.eq : ncand;
+        const uint64_t c_lt1 = n_below + below + (up ? E0 : 0);
+        const uint64_t r1 = k - c_lt1;
+        changed = hb.changed;  // outside the window the bits are final; candidates: fix_changed
+        if (T1 == T0 || r1 == 0 || r1 > eq1)
+          return fail(PACT_E_RUN_FAILURE, "prune window select inconsistent (T0=%u T1=%u r1=%llu eq=%llu)", T0, T1,
+                      (unsigned long long)r1, (unsigned long long)eq1);
+        // ties at T0 are all dropped (T' > T0) or all kept (T' < T0)
+        if (E0) {
+          const uint32_t* ties0 = out->ties[out->ties_cur].as<uint32_t>();
+          pactk::launch_prune_tiefix(out->words, len, out->tie_words.as<uint64_t>(), ties0,
+                                     out->tie_prefix.as<uint32_t>(), up ? ~0ull : 0ull, out->tile_popc, s);
+          changed = 1;  // the pass compared these bits against T0's tie ranks, not the old mask
+        }
+        const bool straddle = r1 < eq1;
+        const int tn = out->ties_cur ^ 1;
+        uint32_t* ties1 = out->ties[tn].as<uint32_t>();
+        if (straddle) {
+          pactk::launch_prune_cand_tieclear(ckey, cidx, ncand, T1, out->tie_words.as<uint64_t>(), s);
+          CUDA_TRY(cudaMemsetAsync(ties1, 0, nc * 4, s));
+        }
+        pactk::launch_prune_cand_fix(ckey, cidx, ncand, T1, straddle, out->words, out->tile_popc,
+                                     out->tie_words.as<uint64_t>(), ties1, &bc->fix_changed, s);
+        if (straddle) {
+          TRY(scan(ctx, ties1, nc, out->tie_prefix.as<uint32_t>(), s));
+          pactk::launch_prune_tiefix(out->words, len, out->tie_words.as<uint64_t>(), ties1,
+                                     out->tie_prefix.as<uint32_t>(), r1, out->tile_popc, s);
+          out->ties_cur = tn;
+        }
+        out->spec_prefix_valid = straddle;
+        if (straddle) pactk::launch_prune_cand_changed(ckey, cidx, ncand, T1, out->words, &bc->fix_changed, s);
+        CUDA_TRY(cudaGetLastError());
+        // re-centre the window when T' sits near one of its ends
+        const uint64_t pos = below + 1;  // T's rank among the candidates
+        if (pos < mwin / 2 || ncand - std::min(ncand, pos) < mwin / 2)
+          TRY(set_window(ckey, ncand, base, out->win_hi, (int64_t)pos - (int64_t)mwin, (int64_t)pos + (int64_t)mwin,
+                         T1));
+        // the fix-up's own change flag (read back with the offsets below)
+        st.path = 4;
+        st.threshold = T1;
+        st.c_lt = c_lt1;
+        st.candidates = ncand;
+        out->spec_T = T1;
+        out->spec_c_lt = c_lt1;
+        done = true;
+        changed |= 2;  // resolved from fix_changed below
+      }
     }
+    if (!done) changed = 1;
   }
 
   if (!done) {
     uint32_t T = 0;
     uint64_t c_lt = 0;
     TRY(find_threshold(ctx, w, len, k, s, &T, &c_lt, &st));
+    // window for the next call: about +-mwin ranks around the k-th key, from
+    // the counting pass's candidates (keys strictly inside the sampled window)
+    {
+      Small h{};
+      CUDA_TRY(cudaMemcpyAsync(ctx->pin.p, sm, offsetof(Small, digest), cudaMemcpyDeviceToHost, s));
+      CUDA_TRY(cudaStreamSynchronize(s));
+      std::memcpy(&h, ctx->pin.p, offsetof(Small, digest));
+      const uint64_t lo_end = h.counts.n_lt + h.counts.n_eq_lo;
+      out->win_valid = 0;
+      if (st.path == 1 && h.counts.n_mid && h.counts.n_mid <= std::max<uint64_t>(1u << 20, len / 16) &&
+          h.win.hi > h.win.lo + 1) {
+        TRY(set_window(ctx->cand.as<uint32_t>(), h.counts.n_mid, h.win.lo + 1, h.win.hi - 1,
+                       (int64_t)k - (int64_t)mwin - (int64_t)lo_end, (int64_t)k + (int64_t)mwin - (int64_t)lo_end,
+                       T));
+      }
+      if (!out->win_valid) {  // the sampled window ends themselves
+        out->win_lo = std::min(h.win.lo, T);
+        out->win_hi = std::max(h.win.hi, T);
+        out->win_valid = st.path == 1;
+      }
+    }
     // (4) bitmap, ties provisionally all dropped; exact when r == E
     const uint64_t r = k - c_lt;
-    TRY(bitmap(T, r, false, false));
+    TRY(bitmap(T, r, false, false, false));
+    changed |= hb.changed;
     if (hb.n_lt != c_lt || !(c_lt < k && k <= hb.n_lt + hb.n_eq))
       return fail(PACT_E_RUN_FAILURE, "prune threshold inconsistent (T=%u c_lt=%llu n_lt=%llu n_eq=%llu k=%llu)",
                   T, (unsigned long long)c_lt, (unsigned long long)hb.n_lt,
@@ -973,6 +1107,7 @@ pact_status pact_prune_magnitude(pact_ctx* ctx, const float* w, uint64_t len, fl
       TRY(fix_ties(r));  // ties straddle r
     } else {
       TRY(scan(ctx, out->ties[out->ties_cur].as<uint32_t>(), nc, out->tie_prefix.as<uint32_t>(), s));
+      out->spec_prefix_valid = 1;
     }
     out->spec_valid = 1;
     out->spec_k = k;
@@ -981,15 +1116,17 @@ pact_status pact_prune_magnitude(pact_ctx* ctx, const float* w, uint64_t len, fl
   }
 
   // (5) chunk offsets (unchanged words keep their offsets)
-  out->changed = changed;
   if (changed || out->nnz != len - k) {
     TRY(scan(ctx, out->tile_popc, nc, out->tile_off, s));
     uint32_t* pin32 = ctx->pin.as<uint32_t>();
     CUDA_TRY(cudaMemcpyAsync(pin32, out->tile_off + nc, 4, cudaMemcpyDeviceToHost, s));
+    if (changed & 2) CUDA_TRY(cudaMemcpyAsync(pin32 + 1, &bc->fix_changed, 4, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));
     out->nnz = pin32[0];
+    if (changed & 2) changed = (changed & 1) | (pin32[1] != 0);
     out->host_tile_off_valid = 0;
   }
+  out->changed = changed != 0;
   out->digest_valid = had_digest && !changed;
   if (out->nnz != len - k)
     return fail(PACT_E_RUN_FAILURE, "prune kept %llu, expected %llu", (unsigned long long)out->nnz,
@@ -2143,7 +2280,7 @@ pact_status pact_calibrate_density(pact_comm* c, pact_ctx* ctx, uint64_t len, co
   TRY(w.ensure(len * 4));
   TRY(g.ensure(len * 4));
   TRY(out.ensure(len * 4));
-  TRY(tv.ensure((ndens + 1) * 4));
+  TRY(tv.ensure((ndens + 2) * 4));
   pact_mask* m = nullptr;
   pact_status st = PACT_OK;
   std::vector<float> t(ndens + 1, 0.0f);
@@ -2168,31 +2305,51 @@ pact_status pact_calibrate_density(pact_comm* c, pact_ctx* ctx, uint64_t len, co
     }
     return PACT_OK;
   };
-  do {
-    if ((st = pact_synth_fill(ctx, w.as<float>(), len, 0x43414c49ull, 0, 1, 1.0f, s)) != PACT_OK) break;
-    if ((st = pact_synth_fill(ctx, g.as<float>(), len, 0x47524144ull + (c ? c->rank : 0), 0, 3, 1.0f, s)) !=
-        PACT_OK)
-      break;
-    if ((st = pact_mask_create(ctx, len, &m)) != PACT_OK) break;
-    for (int i = 0; i <= ndens && st == PACT_OK; ++i) {
-      const double d = i < ndens ? densities[i] : densities[ndens - 1];
-      if (i < ndens) {
-        if ((st = pact_prune_magnitude(ctx, w.as<float>(), len, (float)(1.0 - d), m, s, nullptr)) != PACT_OK)
-          break;
-        pol.density_threshold = 0.0;  // packed
-      } else {
-        pol.density_threshold = 1e-300;  // any density is above it: the dense path
-      }
-      st = timed(&pol, &t[i]);
+  // every rank reaches every collective below: a local failure is agreed on
+  // (max of an error slot) before the next timed probe, and the final
+  // max-reduce always runs, carrying the error slot
+  float* errslot = tv.as<float>() + ndens + 1;
+  auto agree_ok = [&](pact_status mine) -> bool {
+    if (!c) return mine == PACT_OK;
+    const float e = mine == PACT_OK ? 0.0f : 1.0f;
+    float h = 0.0f;
+    if (cudaMemcpyAsync(errslot, &e, 4, cudaMemcpyHostToDevice, s) != cudaSuccess ||
+        ncclAllReduce(errslot, errslot, 1, ncclFloat32, ncclMax, c->nccl, s) != ncclSuccess ||
+        cudaMemcpyAsync(&h, errslot, 4, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess)
+      return false;
+    return h == 0.0f;
+  };
+  pact_status prep = pact_synth_fill(ctx, w.as<float>(), len, 0x43414c49ull, 0, 1, 1.0f, s);
+  if (prep == PACT_OK)
+    prep = pact_synth_fill(ctx, g.as<float>(), len, 0x47524144ull + (c ? c->rank : 0), 0, 3, 1.0f, s);
+  if (prep == PACT_OK) prep = pact_mask_create(ctx, len, &m);
+  if (!agree_ok(prep)) st = prep != PACT_OK ? prep : fail(PACT_E_RUN_FAILURE, "calibration: a peer failed to prepare");
+  for (int i = 0; i <= ndens && st == PACT_OK; ++i) {
+    pact_status ps = PACT_OK;
+    if (i < ndens) {
+      ps = pact_prune_magnitude(ctx, w.as<float>(), len, (float)(1.0 - densities[i]), m, s, nullptr);
+      pol.density_threshold = 0.0;  // packed
+    } else {
+      pol.density_threshold = 1e-300;  // any density is above it: the dense path
     }
-  } while (false);
-  if (st == PACT_OK) {  // max over ranks: every rank takes the same decision
-    cudaMemcpyAsync(tv.as<float>(), t.data(), (ndens + 1) * 4, cudaMemcpyHostToDevice, s);
-    if (c && ncclAllReduce(tv.as<float>(), tv.as<float>(), ndens + 1, ncclFloat32, ncclMax, c->nccl, s) !=
-                 ncclSuccess)
+    if (!agree_ok(ps)) {
+      st = ps != PACT_OK ? ps : fail(PACT_E_RUN_FAILURE, "calibration: a peer failed to prune");
+      break;
+    }
+    st = timed(&pol, &t[i]);
+  }
+  {  // max over ranks: every rank takes the same decision
+    std::vector<float> tt(t);
+    tt.push_back(st == PACT_OK ? 0.0f : 1.0f);
+    cudaMemcpyAsync(tv.as<float>(), tt.data(), (ndens + 2) * 4, cudaMemcpyHostToDevice, s);
+    if (c && ncclAllReduce(tv.as<float>(), tv.as<float>(), ndens + 2, ncclFloat32, ncclMax, c->nccl, s) !=
+                 ncclSuccess && st == PACT_OK)
       st = fail(PACT_E_NCCL, "calibration max-reduce");
-    cudaMemcpyAsync(t.data(), tv.as<float>(), (ndens + 1) * 4, cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(tt.data(), tv.as<float>(), (ndens + 2) * 4, cudaMemcpyDeviceToHost, s);
     if (cudaStreamSynchronize(s) != cudaSuccess && st == PACT_OK) st = fail(PACT_E_CUDA, "calibration readback");
+    if (st == PACT_OK && tt[ndens + 1] != 0.0f) st = fail(PACT_E_RUN_FAILURE, "calibration failed on a peer");
+    std::copy(tt.begin(), tt.begin() + ndens + 1, t.begin());
   }
   if (m) pact_mask_destroy(m);
   cudaEventDestroy(a);

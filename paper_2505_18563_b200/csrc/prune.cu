@@ -308,6 +308,7 @@ __global__ void __launch_bounds__(1024)
     sel->prefix = (prefix << nbits) | (uint32_t)d;
     sel->rem = rem - eb;
     sel->below = below + eb;
+    sel->eq = d == 2 * t ? a : b;
     if (first) sel->err = 0;
   }
   if (t == 0 && total < rem) sel->err = 1;
@@ -324,7 +325,9 @@ __global__ void __launch_bounds__(1024)
 // owner*8 + (column ^ (owner & 7))).
 constexpr int kKeyStages = 2;
 constexpr int kStageFloats = kChunk + 2 * kChunkWords;  // keys, then the 16 old mask words
-constexpr size_t kBitmapSmem = (size_t)kPruneWarps * kKeyStages * kStageFloats * sizeof(float);
+constexpr int kCandBuf = 64;                            // per-warp window-candidate staging
+constexpr size_t kBitmapSmem =
+    (size_t)kPruneWarps * (kKeyStages * kStageFloats * sizeof(float) + 2 * kCandBuf * sizeof(uint32_t));
 
 __device__ __forceinline__ void chunk_issue(float* st, const float* __restrict__ w,
                                             const uint64_t* __restrict__ words, uint64_t c) {
@@ -353,25 +356,44 @@ __device__ __forceinline__ void classify_push(uint32_t k, uint32_t T, uint32_t& 
   e = __funnelshift_l(T - 1u - k, e, 1);
 }
 
+// staged window candidates of one warp -> the global list (one atomic per flush)
+__device__ __forceinline__ void flush_pairs(const uint32_t* bk, const uint32_t* bi, uint32_t fill,
+                                            unsigned long long* n_cand, const PruneCandBuf& cb) {
+  const int lane = threadIdx.x & 31;
+  unsigned long long base = 0;
+  if (lane == 0) base = atomicAdd(n_cand, (unsigned long long)fill);
+  base = __shfl_sync(0xffffffffu, base, 0);
+  for (uint32_t i = lane; i < fill; i += 32)
+    if (base + i < cb.cap) {
+      cb.key[base + i] = bk[i];
+      cb.idx[base + i] = bi[i];
+    }
+  __syncwarp();
+}
+
 __global__ void __launch_bounds__(kPruneWarps * 32)
     prune_bitmap_kernel(const float* __restrict__ w, uint64_t len, uint32_t T, uint64_t r,
                         const uint32_t* __restrict__ tie_prefix, uint64_t* __restrict__ words,
                         uint64_t nwords, uint32_t* __restrict__ chunk_popc,
                         uint32_t* __restrict__ ties_out, const uint32_t* __restrict__ ties_prev,
                         uint64_t* __restrict__ tie_words, BitmapCounts* __restrict__ counts,
-                        uint64_t nchunks) {
+                        uint64_t nchunks, PruneCandBuf cb) {
   extern __shared__ __align__(16) float ring_all[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   float* ring = ring_all + (size_t)warp * kKeyStages * kStageFloats;
+  uint32_t* cbk = reinterpret_cast<uint32_t*>(ring_all + (size_t)kPruneWarps * kKeyStages * kStageFloats) +
+                  warp * 2 * kCandBuf;
+  uint32_t* cbi = cbk + kCandBuf;
   uint32_t* words32 = reinterpret_cast<uint32_t*>(words);
   uint32_t* tie32 = reinterpret_cast<uint32_t*>(tie_words);
   const uint64_t nhalves = 2 * nwords;
   const bool vec_ok = (((uintptr_t)w) & 15) == 0;
+  const bool use_win = cb.lo <= cb.hi;
   // chunks streamed through the ring: whole 1024-element chunks of an
   // aligned vector (the ragged last chunk is read directly)
   auto full = [&](uint64_t c) { return vec_ok && (c + 1) * (uint64_t)kChunk <= len; };
-  uint32_t c_lt = 0, c_eq = 0;
-  int changed = 0, mismatch = 0;
+  uint32_t c_lt = 0, c_eq = 0, c_below = 0, fill = 0;
+  int changed = 0, changed_cand = 0, mismatch = 0;
   const uint64_t nw_total = (uint64_t)gridDim.x * kPruneWarps;
   const uint64_t c0 = (uint64_t)blockIdx.x * kPruneWarps + warp;
 #pragma unroll
@@ -385,14 +407,21 @@ __global__ void __launch_bounds__(kPruneWarps * 32)
     {
       const uint64_t cn = c + (kKeyStages - 1) * nw_total;
       const int sn = slot == 0 ? kKeyStages - 1 : slot - 1;
+      __syncwarp();  // every lane is done reading stage sn (the previous chunk)
       if (cn < nchunks && full(cn)) chunk_issue(ring + sn * kStageFloats, w, words, cn);
       asm volatile("cp.async.commit_group;" ::: "memory");
       asm volatile("cp.async.wait_group %0;" ::"n"(kKeyStages - 1) : "memory");
+      __syncwarp();  // lanes read stage cells other lanes' cp.async filled
     }
     const float* st = ring + slot * kStageFloats;
     slot = slot == kKeyStages - 1 ? 0 : slot + 1;
     const bool fc = full(c);
-    uint32_t g = 0, e = 0, inr = ~0u;
+    const uint64_t e0 = c * (uint64_t)kChunk + 32 * lane;
+    // window test: (key - lo) <= W as unsigned (keys, lo < 2^31, so key < lo
+    // wraps above W); the running minimum tells whether ANY of the lane's 32
+    // keys is inside, the exact mask is rebuilt only then (a few % of lanes)
+    const uint32_t W = cb.hi - cb.lo;
+    uint32_t g = 0, e = 0, mn = ~0u, inr = ~0u;
     if (fc) {
 #pragma unroll
       for (int k = kVecPerLane - 1; k >= 0; --k) {  // elements 32*lane + 4k .. 4k+3
@@ -402,12 +431,18 @@ __global__ void __launch_bounds__(kPruneWarps * 32)
         classify_push(mag_key(v.z), T, g, e);
         classify_push(mag_key(v.y), T, g, e);
         classify_push(mag_key(v.x), T, g, e);
+        if (use_win) {
+          mn = min(mn, min(min(mag_key(v.w) - cb.lo, mag_key(v.z) - cb.lo),
+                           min(mag_key(v.y) - cb.lo, mag_key(v.x) - cb.lo)));
+        }
       }
     } else {
-      const uint64_t e0 = c * (uint64_t)kChunk + 32 * lane;
       inr = e0 >= len ? 0u : (len - e0 >= 32 ? ~0u : (1u << (len - e0)) - 1u);
-      for (int i = 31; i >= 0; --i)
-        classify_push(e0 + i < len ? mag_key(w[e0 + i]) : 0u, T, g, e);
+      for (int i = 31; i >= 0; --i) {
+        const uint32_t kq = e0 + i < len ? mag_key(w[e0 + i]) : 0u;
+        classify_push(kq, T, g, e);
+        if (use_win && e0 + i < len) mn = min(mn, kq - cb.lo);
+      }
     }
     g &= inr;
     e &= inr;
@@ -433,26 +468,120 @@ __global__ void __launch_bounds__(kPruneWarps * 32)
       ties_out[c] = E;
       if (ties_prev && ties_prev[c] != E) mismatch = 1;
     }
-    if (hi < nhalves) {
-      const uint32_t old = fc ? reinterpret_cast<const uint32_t*>(st + kChunk)[lane] : words32[hi];
-      if (old != keep) {
-        words32[hi] = keep;
-        changed = 1;
+    const uint32_t old = hi < nhalves ? (fc ? reinterpret_cast<const uint32_t*>(st + kChunk)[lane] : words32[hi]) : 0u;
+    uint32_t cand = 0;
+    if (use_win) {
+      // lanes whose 32 keys touch the window are resolved one at a time by
+      // the whole warp: lane j tests element j of lane l, a ballot is lane
+      // l's candidate mask (bit j = element j), and the warp stages the
+      // candidates with their previous mask bits
+      uint32_t todo = __ballot_sync(0xffffffffu, mn <= W);
+      while (todo) {
+        const int l = __ffs(todo) - 1;
+        todo &= todo - 1;
+        const uint64_t el0 = c * (uint64_t)kChunk + 32 * l;
+        bool ok = true;
+        uint32_t kq;
+        if (fc) {
+          kq = mag_key(st[4 * (l * 8 + ((lane >> 2) ^ (l & 7))) + (lane & 3)]);
+        } else {
+          ok = el0 + lane < len;
+          kq = ok ? mag_key(w[el0 + lane]) : 0u;
+        }
+        const uint32_t eql = __shfl_sync(0xffffffffu, eqm, l);
+        const bool in = ok && (kq - cb.lo <= W) && !((eql >> lane) & 1u);
+        const uint32_t m = __ballot_sync(0xffffffffu, in);
+        if (lane == l) cand = m;
+        if (!m) continue;
+        const uint32_t oldl = __shfl_sync(0xffffffffu, old, l);
+        const uint32_t el = __shfl_sync(0xffffffffu, e, l);
+        if (lane == 0) c_below += __popc(m & ~el);  // #(key < lo) = #(key < T) - these
+        const uint32_t nm = __popc(m);
+        if (fill + nm > (uint32_t)kCandBuf) {
+          flush_pairs(cbk, cbi, fill, &counts->n_cand, cb);
+          fill = 0;
+        }
+        if (in) {
+          const uint32_t pos = fill + __popc(m & ((1u << lane) - 1u));
+          cbk[pos] = kq;
+          cbi[pos] = (uint32_t)(el0 + lane) | (((oldl >> lane) & 1u) << 31);
+        }
+        __syncwarp();
+        fill += nm;
       }
+    }
+    if (hi < nhalves && old != keep) {
+      words32[hi] = keep;
+      if ((old ^ keep) & ~cand) changed = 1;
+      if ((old ^ keep) & cand) changed_cand = 1;
     }
     const uint32_t pc = warp_sum((uint32_t)__popc(keep));
     if (lane == 0) chunk_popc[c] = pc;
   }
+  if (fill) flush_pairs(cbk, cbi, fill, &counts->n_cand, cb);
   c_lt = warp_sum(c_lt);
   c_eq = warp_sum(c_eq);
+  c_below = warp_sum(c_below);
   changed = __any_sync(0xffffffffu, changed);
+  changed_cand = __any_sync(0xffffffffu, changed_cand);
   mismatch = __any_sync(0xffffffffu, mismatch);
   if (lane == 0) {
     if (c_lt) atomicAdd(&counts->n_lt, (unsigned long long)c_lt);
     if (c_eq) atomicAdd(&counts->n_eq, (unsigned long long)c_eq);
+    if (c_below) atomicAdd(&counts->n_cand_below, (unsigned long long)c_below);  // candidates below T
     if (changed) atomicOr(&counts->changed, 1);
+    if (changed_cand) atomicOr(&counts->changed_cand, 1);
     if (mismatch) atomicOr(&counts->tie_mismatch, 1);
   }
+}
+
+// ------------------------------------------------------- window fix-up
+// The pass's threshold T was stale, the true T' lies in the window: every
+// candidate's bit is rewritten for T' (ties provisionally dropped, recorded
+// for the tie fix-up when they straddle the rank r').
+__global__ void __launch_bounds__(256)
+    prune_cand_tieclear_kernel(const uint32_t* __restrict__ key, const uint32_t* __restrict__ idx, uint64_t n,
+                               uint32_t T, uint64_t* __restrict__ tie_words) {
+  const uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (j >= n || key[j] != T) return;
+  const uint64_t c = (idx[j] & 0x7fffffffu) >> 10;
+#pragma unroll
+  for (int q = 0; q < kChunkWords; ++q) tie_words[c * kChunkWords + q] = 0ull;
+}
+
+__global__ void __launch_bounds__(256)
+    prune_cand_fix_kernel(const uint32_t* __restrict__ key, const uint32_t* __restrict__ idx, uint64_t n,
+                          uint32_t T, int straddle, unsigned long long* __restrict__ words,
+                          uint32_t* __restrict__ chunk_popc, unsigned long long* __restrict__ tie_words,
+                          uint32_t* __restrict__ ties, int* __restrict__ changed) {
+  const uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  bool ch = false;
+  if (j < n) {
+    const uint32_t kq = key[j], v = idx[j], ix = v & 0x7fffffffu;
+    const bool keep = kq > T;
+    const unsigned long long bit = 1ull << (ix & 63);
+    const bool tie = kq == T && straddle;  // final bit decided by the tie fix-up
+    if (tie) {
+      atomicOr(&tie_words[ix >> 6], bit);
+      atomicAdd(&ties[ix >> 10], 1u);
+    }
+    const unsigned long long old = keep ? atomicOr(&words[ix >> 6], bit) : atomicAnd(&words[ix >> 6], ~bit);
+    if (((old & bit) != 0) != keep) atomicAdd(&chunk_popc[ix >> 10], keep ? 1u : 0xffffffffu);
+    ch = !tie && keep != (bool)(v >> 31);
+  }
+  if (__any_sync(0xffffffffu, ch) && (threadIdx.x & 31) == 0) *changed = 1;
+}
+
+__global__ void __launch_bounds__(256)
+    prune_cand_changed_kernel(const uint32_t* __restrict__ key, const uint32_t* __restrict__ idx, uint64_t n,
+                              uint32_t T, const uint64_t* __restrict__ words, int* __restrict__ flag) {
+  const uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  bool ch = false;
+  if (j < n && key[j] == T) {  // the tie candidates (the others were checked by the fix-up)
+    const uint32_t v = idx[j], ix = v & 0x7fffffffu;
+    ch = ((words[ix >> 6] >> (ix & 63)) & 1u) != (v >> 31);
+  }
+  if (__any_sync(0xffffffffu, ch) && (threadIdx.x & 31) == 0) *flag = 1;
 }
 
 // ----------------------------------------------------------------- tiefix
@@ -465,36 +594,46 @@ __global__ void __launch_bounds__(256)
                         const uint64_t* __restrict__ tie_words, const uint32_t* __restrict__ ties,
                         const uint32_t* __restrict__ tie_prefix, uint64_t r, int keep_low,
                         uint32_t* __restrict__ chunk_popc, uint64_t nchunks) {
+  // a warp scans the tie counts of 32 chunks at a time (one coalesced load)
+  // and fixes only the chunks that hold ties: ties are rare except at key 0
   const int lane = threadIdx.x & 31;
-  const uint64_t c = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
-  if (c >= nchunks) return;
-  const uint32_t E = ties[c];
-  if (E == 0) return;
-  const uint64_t pre = tie_prefix[c];
-  const uint64_t D = r > pre ? (r - pre < E ? r - pre : E) : 0;
-  const uint64_t wi = c * kChunkWords + lane;
-  const bool valid = lane < kChunkWords && wi < nwords;
-  const uint64_t tw = valid ? tie_words[wi] : 0ull;
-  const uint32_t tc = (uint32_t)__popcll(tw);
-  const uint32_t inc = warp_incl_scan(tc);
-  const uint64_t excl = inc - tc;
-  uint64_t d = D > excl ? D - excl : 0;
-  if (d > tc) d = tc;
-  uint64_t first = 0, x = tw;  // the chunk's first d ties of this word
-  for (uint64_t n = 0; n < d; ++n) {
-    const uint64_t b = x & (~x + 1);
-    first |= b;
-    x ^= b;
+  const uint64_t wg = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t g0 = wg * 32; g0 < nchunks; g0 += nwarps * 32) {
+    const uint32_t El = g0 + lane < nchunks ? ties[g0 + lane] : 0u;
+    uint32_t todo = __ballot_sync(0xffffffffu, El != 0);
+    while (todo) {
+      const int bsel = __ffs(todo) - 1;
+      todo &= todo - 1;
+      const uint64_t c = g0 + bsel;
+      const uint32_t E = __shfl_sync(0xffffffffu, El, bsel);
+      const uint64_t pre = tie_prefix[c];
+      const uint64_t D = r > pre ? (r - pre < E ? r - pre : E) : 0;
+      const uint64_t wi = c * kChunkWords + lane;
+      const bool valid = lane < kChunkWords && wi < nwords;
+      const uint64_t tw = valid ? tie_words[wi] : 0ull;
+      const uint32_t tc = (uint32_t)__popcll(tw);
+      const uint32_t inc = warp_incl_scan(tc);
+      const uint64_t excl = inc - tc;
+      uint64_t d = D > excl ? D - excl : 0;
+      if (d > tc) d = tc;
+      uint64_t first = 0, x = tw;  // the chunk's first d ties of this word
+      for (uint64_t q = 0; q < d; ++q) {
+        const uint64_t bb = x & (~x + 1);
+        first |= bb;
+        x ^= bb;
+      }
+      uint32_t pc = 0;
+      if (valid) {
+        // prune: the first ties (lowest indices) are dropped; TopK keeps them
+        const uint64_t nw = (words[wi] & ~tw) | (keep_low ? first : (tw & ~first));
+        words[wi] = nw;
+        pc = (uint32_t)__popcll(nw);
+      }
+      pc = warp_sum(pc);
+      if (lane == 0) chunk_popc[c] = pc;
+    }
   }
-  uint32_t pc = 0;
-  if (valid) {
-    // prune: the first ties (lowest indices) are dropped; TopK keeps them
-    const uint64_t nw = (words[wi] & ~tw) | (keep_low ? first : (tw & ~first));
-    words[wi] = nw;
-    pc = (uint32_t)__popcll(nw);
-  }
-  pc = warp_sum(pc);
-  if (lane == 0) chunk_popc[c] = pc;
 }
 
 // ------------------------------------------------------ per-layer (segmented)
@@ -636,7 +775,9 @@ void launch_prune_hist(const void* src, int from_float, uint64_t n, uint32_t bas
 void launch_prune_hist_sel(const void* src, int from_float, uint64_t n, uint32_t base, int shift,
                            int nbits, int first, const SelState* sel, uint32_t* hist, cudaStream_t s) {
   cudaMemsetAsync(hist, 0, sizeof(uint32_t) << nbits, s);
-  uint64_t blocks = (n + 255) / 256;
+  // candidate lists are small and L2 resident: few CTAs, so the per-CTA
+  // histogram flushes (up to 2^nbits global atomics each) stay cheap
+  uint64_t blocks = from_float ? (n + 255) / 256 : (n + 4095) / 4096;
   const uint64_t cap = (uint64_t)num_sms() * 8;
   if (blocks > cap) blocks = cap;
   if (blocks == 0) blocks = 1;
@@ -658,21 +799,45 @@ void launch_prune_pick(const uint32_t* hist, int nbits, int first, uint64_t rank
 void launch_prune_bitmap(const float* w, uint64_t len, uint32_t T, uint64_t r,
                          const uint32_t* tie_prefix, uint64_t* words, uint32_t* chunk_popc,
                          uint32_t* ties_out, const uint32_t* ties_prev, uint64_t* tie_words,
-                         BitmapCounts* counts, cudaStream_t s) {
+                         BitmapCounts* counts, cudaStream_t s, const PruneCandBuf& cand) {
   const uint64_t nc = (len + kChunk - 1) / kChunk;
   cudaMemsetAsync(counts, 0, sizeof(BitmapCounts), s);
   if (!nc) return;
-  static unsigned cap = 0;
-  if (!cap) {
+  static DeviceCache<unsigned> cap;
+  unsigned& cp = cap.get();
+  if (!cp) {
     cudaFuncSetAttribute(prune_bitmap_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)kBitmapSmem);
-    cap = persistent_grid(prune_bitmap_kernel, kPruneWarps * 32, kBitmapSmem, ~0ull >> 8,
-                          kPruneWarps);
+    cp = persistent_grid(prune_bitmap_kernel, kPruneWarps * 32, kBitmapSmem, ~0ull >> 8, kPruneWarps);
   }
   const uint64_t need = (nc + kPruneWarps - 1) / kPruneWarps;
-  prune_bitmap_kernel<<<(unsigned)(need < cap ? need : cap), kPruneWarps * 32, kBitmapSmem, s>>>(
+  prune_bitmap_kernel<<<(unsigned)(need < cp ? need : cp), kPruneWarps * 32, kBitmapSmem, s>>>(
       w, len, T, r, tie_prefix, words, (len + 63) / 64, chunk_popc, ties_out, ties_prev, tie_words,
-      counts, nc);
+      counts, nc, cand);
+  note_launch();
+}
+
+void launch_prune_cand_tieclear(const uint32_t* key, const uint32_t* idx, uint64_t n, uint32_t T,
+                                uint64_t* tie_words, cudaStream_t s) {
+  if (!n) return;
+  prune_cand_tieclear_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(key, idx, n, T, tie_words);
+  note_launch();
+}
+
+void launch_prune_cand_fix(const uint32_t* key, const uint32_t* idx, uint64_t n, uint32_t T, int straddle,
+                           uint64_t* words, uint32_t* chunk_popc, uint64_t* tie_words, uint32_t* ties,
+                           int* changed, cudaStream_t s) {
+  if (!n) return;
+  prune_cand_fix_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(
+      key, idx, n, T, straddle, reinterpret_cast<unsigned long long*>(words), chunk_popc,
+      reinterpret_cast<unsigned long long*>(tie_words), ties, changed);
+  note_launch();
+}
+
+void launch_prune_cand_changed(const uint32_t* key, const uint32_t* idx, uint64_t n, uint32_t T,
+                               const uint64_t* words, int* flag, cudaStream_t s) {
+  if (!n) return;
+  prune_cand_changed_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(key, idx, n, T, words, flag);
   note_launch();
 }
 
@@ -681,8 +846,11 @@ void launch_prune_tiefix(uint64_t* words, uint64_t len, const uint64_t* tie_word
                          uint32_t* chunk_popc, cudaStream_t s, int keep_low) {
   const uint64_t nc = (len + kChunk - 1) / kChunk;
   if (!nc) return;
-  prune_tiefix_kernel<<<(unsigned)((nc * 32 + 255) / 256), 256, 0, s>>>(
-      words, (len + 63) / 64, tie_words, ties, tie_prefix, r, keep_low, chunk_popc, nc);
+  uint64_t blocks = (nc + 255) / 256;  // 8 warps x 32 chunks per CTA and pass
+  const uint64_t cap = (uint64_t)num_sms() * 8;
+  if (blocks > cap) blocks = cap;
+  prune_tiefix_kernel<<<(unsigned)blocks, 256, 0, s>>>(words, (len + 63) / 64, tie_words, ties, tie_prefix, r,
+                                                       keep_low, chunk_popc, nc);
   note_launch();
 }
 

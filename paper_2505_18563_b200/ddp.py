@@ -100,7 +100,9 @@ class PactHookState:
         self.density_thresholds: Dict[int, float] = {}
 
     def density_threshold(self, length: int) -> float:
-        if not self.auto_density or self.comm() is None:
+        # pact_calibrate_density needs len >= 1024: tiny buckets keep the
+        # policy's static threshold (identical on every rank: no collective)
+        if not self.auto_density or self.comm() is None or length < 1024:
             return self.policy.density_threshold
         if length not in self.density_thresholds:
             from .api import calibrate_density

@@ -423,10 +423,142 @@ def test_prune_resnet50_full_size_bitexact(pb, port, cuda):
         assert m.digest() == port.mask_digest(ref, shape.total)
 
 
+# Exact kept counts of SURVEY 8 (drop_count, sparsity.cpp:33-40)
+FULL_NNZ = {("resnet18", 0.9): 1_168_951, ("resnet50", 0.8): 5_111_404, ("vgg19", 0.95): 7_183_350,
+            ("bert-base", 0.5): 54_741_110, ("bert-base", 0.8): 21_896_436, ("bert-base", 0.9): 10_948_216,
+            ("bert-base", 0.95): 5_474_103, ("bert-base", 0.99): 1_094_811, ("gpt2-medium", 0.9): 35_482_290}
+C4_SWEEP = (0.5, 0.6, 0.7, 0.8, 0.9, 0.95, 0.99)
+
+
+def _check_full(pb, port, wd, ratio, n, tag):
+    m = pb.magnitude_prune(wd, ratio)
+    ref = port.magnitude_prune(wd.cpu().numpy(), ratio)
+    assert m.nnz() == n - port.drop_count(ratio, n), tag
+    assert np.array_equal(m.words_host(), ref), tag
+    assert m.digest() == port.mask_digest(ref, n), tag
+    return m, ref
+
+
+@pytest.mark.parametrize("model,ratios", [("resnet18", (0.9,)), ("vgg19", (0.95,)), ("bert-base", C4_SWEEP),
+                                          ("gpt2-medium", (0.9,))])
+def test_prune_full_size_bitexact(pb, port, cuda, model, ratios):
+    """C1 (global), C3, C4 at every sweep ratio, C5: words, nnz and digest
+    bit-exact against the oracle's restatement of sparsity.cpp:44-59 at the
+    exact BASELINE sizes, both weight recipes (W_TIES: ~40 exact repeats per
+    magnitude at 355M, so the tie ranks decide bits)."""
+    from paper_2505_18563_b200 import synth
+
+    shape = synth.model_shape(model)
+    n = shape.total
+    for recipe in (synth.W_REAL, synth.W_TIES):
+        wd = synth.weights_device(shape, 41 + recipe, recipe)
+        for ratio in ratios:
+            m, _ = _check_full(pb, port, wd, ratio, n, (model, recipe, ratio))
+            if (model, ratio) in FULL_NNZ:
+                assert m.nnz() == FULL_NNZ[(model, ratio)]
+            del m
+        del wd
+        torch.cuda.empty_cache()
+
+
+def _perturb(kind, w, keep, rng, synth, step):
+    """Re-prune schedules (SURVEY A.9 and moves of the threshold both ways)."""
+    n = w.size
+    if kind == "same":
+        return w
+    if kind == "up":  # 40 dropped elements just below T become large: T moves up
+        drop = np.nonzero(~keep)[0]
+        j = drop[np.argsort(np.abs(w[drop]), kind="stable")[-40:]]
+        w = w.copy()
+        w[j] = np.float32(4.0) * np.sign(w[j] + np.float32(1e-30))
+        return w
+    if kind in ("down", "down3k"):  # kept elements just above T become tiny: T moves down
+        kept = np.nonzero(keep)[0]
+        j = kept[np.argsort(np.abs(w[kept]), kind="stable")[:40 if kind == "down" else 3000]]
+        w = w.copy()
+        w[j] = np.float32(2.0 ** -40)
+        return w
+    if kind == "a9":  # w <- GSE(w) + delta: kept entries drift, pruned ones get fresh tiny noise
+        jit = synth.synth_host(n, 1000 + step, synth.W_REAL, 2.0 ** -16)
+        drift = synth.synth_host(n, 2000 + step, synth.W_REAL, 2.0 ** -12)
+        return np.where(keep, w + drift, np.float32(0.0)).astype(np.float32) + jit
+    if kind == "a9ties":  # the same with the noise on 2^10 levels: ties at the threshold
+        jit = synth.synth_host(n, 3000 + step, synth.W_REAL, 2.0 ** -16)
+        jit = (np.round(jit.astype(np.float64) * 2.0 ** 26) * 2.0 ** -26).astype(np.float32)
+        return np.where(keep, w, np.float32(0.0)).astype(np.float32) + jit
+    if kind == "new":  # unrelated weights: the window misses
+        return synth.synth_host(n, 4000 + step, synth.W_REAL, 0.25)
+    raise ValueError(kind)
+
+
+SCHEDULE = ["same", "up", "down", "same", "a9", "a9", "a9", "same", "up", "a9ties", "a9ties", "down3k",
+            "a9ties", "down", "new", "same"]
+
+
+@pytest.mark.parametrize("n", [3_000_017, 200_003])
+def test_reprune_sequence_paths(pb, port, cuda, n):
+    """Per-step re-pruning (C5's mask regeneration) through every prune path:
+    temporal reuse (3), a moved threshold resolved from the bitmap pass's
+    window candidates (4, both directions, ties straddling r), the sampled
+    path (1). Words and digest bit-exact at every step; `changed` never
+    misses a change."""
+    from paper_2505_18563_b200 import synth
+
+    for recipe in (synth.W_REAL, synth.W_TIES):
+        rng = np.random.default_rng(n + recipe)
+        w = synth.synth_host(n, 77 + recipe, recipe, 0.25)
+        m = pb.SparsityMask(n)
+        prev, paths = None, []
+        for t, kind in enumerate(["same"] + SCHEDULE):
+            if prev is not None:
+                w = _perturb(kind, w, bits_from_words(prev, n), rng, synth, t)
+            st = {}
+            pb.magnitude_prune(dev(w), 0.9, out=m, stats=st)
+            ref = port.magnitude_prune(w, 0.9)
+            got = m.words_host()
+            assert np.array_equal(got, ref), (recipe, t, kind, st, np.nonzero(got != ref)[0][:5])
+            assert m.nnz() == n - port.drop_count(0.9, n)
+            if prev is not None and not m.changed:
+                assert np.array_equal(ref, prev), (recipe, t, kind, "change missed")
+            assert m.digest() == port.mask_digest(ref, n), (recipe, t, kind)
+            paths.append((kind, st["path"]))
+            prev = ref
+        got_paths = [p for _, p in paths]
+        assert got_paths.count(3) >= 3, paths
+        assert got_paths.count(4) >= 4, paths
+
+
+def test_c5_reprune_a9_full_size(pb, port, cuda):
+    """C5 (GPT-2-medium, 354,823,168) per-step re-pruning at 0.9 with the A.9
+    recipe (w <- GSE(w) + delta), plus threshold moves both ways: words
+    bit-exact against the oracle at every step."""
+    from paper_2505_18563_b200 import synth
+
+    shape = synth.model_shape("gpt2-medium")
+    n = shape.total
+    w = synth.weights_host(shape, 51, synth.W_TIES)
+    m = pb.SparsityMask(n)
+    prev = None
+    rng = np.random.default_rng(5)
+    paths = []
+    for t, kind in enumerate(["same", "same", "a9", "a9", "up", "down"]):
+        if prev is not None:
+            w = _perturb(kind, w, bits_from_words(prev, n), rng, synth, t)
+        st = {}
+        pb.magnitude_prune(dev(w), 0.9, out=m, stats=st)
+        ref = port.magnitude_prune(w, 0.9)
+        assert np.array_equal(m.words_host(), ref), (t, kind, st)
+        assert m.nnz() == 35_482_290
+        assert m.digest() == port.mask_digest(ref, n)
+        paths.append(st["path"])
+        prev = ref
+    assert 3 in paths and 4 in paths, paths
+
+
 @pytest.mark.parametrize("model,ratio,nnz", [("vgg19", 0.95, 7_183_350), ("gpt2-medium", 0.9, 35_482_290)])
-def test_full_size_properties(pb, cuda, model, ratio, nnz):
-    """C3/C5 sizes: exact kept count, threshold property, pack->unpack == GSE,
-    checksum of the packed values == checksum of the GSE'd gradient."""
+def test_full_size_pack_properties(pb, cuda, model, ratio, nnz):
+    """C3/C5 sizes: pack -> unpack == GSE and the packed checksum == the
+    checksum of the GSE'd gradient (size-independent properties)."""
     from paper_2505_18563_b200 import synth
 
     shape = synth.model_shape(model)
