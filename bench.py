@@ -1,25 +1,29 @@
 """Benchmark of the PacTrain gradient-sync hot path on B200.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5] [--impl ours|reference]
 
 Metric (BASELINE.json): dense-equivalent gradient-sync GB/s
-    = 4 * len bytes of fp32 gradient per rank / t_step,
+    = 4 * len bytes of fp32 gradient / t_step      (per rank)
 where a step is one pass of the hot path over one synthetic gradient:
-vote -> pack -> NCCL allreduce -> unpack (N > 1), pack -> unpack (N = 1,
-no exchange), plus the magnitude re-prune for config c5. `value` is
-the whole-job aggregate: N ranks x 4*len / t_step (weak scaling: every rank
-syncs a full model-sized gradient). Inputs are HBM resident; the L2 is
-flushed (a 512 MiB write) before every timed step; timing is CUDA events on
-the launching stream, max over ranks. `e2e` is the same metric through the
-host-buffer C-ABI call (pinned H2D of the gradient, D2H of the result inside
-the timed region).
+magnitude re-prune of the current weights (config c5, the default: GPT-2-
+medium shape, 354,823,168 elements, 90%) -> vote -> pack -> exchange ->
+unpack (N > 1), or prune -> pack -> unpack (N = 1, no exchange).
+Between timed steps (untimed) the weights evolve per SURVEY A.9: w <- GSE(w)
++ delta on the kept entries, fresh regrowth noise on the pruned ones, so every
+step re-derives the mask from new weights. `value` is per rank (every rank
+syncs a full model-sized gradient; weak scaling), `value_job` = N x value.
+Inputs are HBM resident; the L2 is flushed before every timed step; timing
+is CUDA events on the launching stream, max over ranks. `e2e` is the same
+step through the host-buffer C-ABI call (pinned H2D of the gradient, D2H of
+the result inside the timed region).
 
 Multi-GPU: launched by the driver under torch.distributed.run, one process per
 GPU; torch.distributed (nccl) carries the barrier / max-over-ranks plumbing and
 the NCCL unique id; the collective itself is the library's own NCCL comm.
 
 --impl reference times the reference's own CPU implementation (oracle/_ref,
-compiled from /root/reference by oracle/Makefile) on the host cores, on rank 0.
+compiled from /root/reference by oracle/Makefile) on the host cores, on rank 0;
+that process never maps the product library (asserted).
 """
 from __future__ import annotations
 
@@ -45,6 +49,32 @@ CONFIGS = {
 }
 L2_FLUSH_BYTES = 512 << 20
 HOST_GATE_CYCLES = 2_000_000  # ~1 ms at 1.965 GHz
+
+
+def _synth_module():
+    """synth.py loaded by file path: importing the package would map the
+    product library, which the reference arm must not do."""
+    import importlib.util
+
+    spec = importlib.util.spec_from_file_location("_pact_synth_bench",
+                                                  os.path.join(ROOT, "paper_2505_18563_b200", "synth.py"))
+    m = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(m)
+    return m
+
+
+def _assert_no_product_lib():
+    try:
+        with open("/proc/self/maps") as f:
+            maps = f.read()
+    except OSError:
+        return
+    assert "libpact_b200" not in maps, "the reference arm mapped the product library"
+
+
+def workload_name(cfg, model, ratio, reprune):
+    return (f"{cfg}:{model} fp32 grads, {int(round(ratio * 100))}% magnitude-pruned mask"
+            + (", re-pruned every step" if reprune else ""))
 
 
 def dist_env():
@@ -119,48 +149,75 @@ class ClockSampler:
 
 
 def run_reference(args, cfg):
-    """The reference's own CPU path (oracle/_ref) on this host's cores."""
+    """The reference's own CPU path (oracle/_ref) on this host's cores, on the
+    same workload: N = 1 -> per step the mask re-derivation (c5) plus the
+    reference pack -> unpack over the full gradient on all host threads; N > 1
+    -> the reference masked_allreduce over SimCluster with N worker threads."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
     import numpy as np
 
     import oracle
-    from paper_2505_18563_b200 import synth
 
-    model, ratio, _, _ = CONFIGS[cfg]
+    synth = _synth_module()
+    model, ratio, reprune, _ = CONFIGS[cfg]
     shape = synth.model_shape(model)
     n = shape.total
     R = oracle.ref()
+    P = oracle.port()
     w = synth.weights_host(shape, 1234, synth.W_REAL)
-    words, nnz, _ = R.magnitude_prune(w, ratio)
+    words = P.magnitude_prune(w, ratio)
+    nnz = P.mask_nnz(words, n)
     nthreads = os.cpu_count() or 1
     nworkers = max(2, args.gpus)
     grads = [R.gse(synth.synth_host(n, synth.grad_seed(r, 0), synth.G_FULL), words) for r in range(max(1, args.gpus))]
     if args.gpus == 1:
         h = R.bench_create(grads[:1], words, slices=nthreads)
         fn = lambda: R.bench_pack_unpack(h)  # noqa: E731
-        what = f"reference pack->unpack on {nthreads} thread slices of the full gradient"
+        what = f"reference pack->unpack (codec.cpp:14-38) on {nthreads} thread slices of the full gradient"
         cores = nthreads
     else:
         h = R.bench_create(grads, words, slices=0)
         fn = lambda: R.bench_masked(h)  # noqa: E731
-        what = f"reference masked_allreduce (tracker Stable) over SimCluster, {nworkers} worker threads"
+        what = f"reference masked_allreduce (collective.cpp:269-309, tracker Stable) over SimCluster, {nworkers} worker threads"
         cores = nworkers
+    prune_note = ""
+    if reprune:
+        # the reference's magnitude_prune is a std::stable_sort of the whole
+        # index array (sparsity.cpp:44-59): ~2 minutes per call at 355M on one
+        # core, so each step re-derives the mask with the oracle's O(n)
+        # restatement of the same rule (bit-identical words, single thread);
+        # the reference's own sort is timed once on a 4 Mi-element slice
+        def step():
+            t0 = time.perf_counter()
+            wd = P.magnitude_prune(w, ratio)
+            t1 = time.perf_counter()
+            assert wd.size == words.size
+            return (t1 - t0) + fn()
+        t_ref_sort = R.bench_prune(w[:1 << 22], ratio)
+        prune_note = (f"; mask re-derived every step by the oracle port's O(n) magnitude_prune over all {n} "
+                      f"weights (1 thread; the reference's stable_sort: {t_ref_sort:.2f} s per 4,194,304 weights)")
+    else:
+        step = fn
+    _assert_no_product_lib()
     for _ in range(args.warmup):
-        fn()
-    ts = [fn() for _ in range(args.steps)]
+        step()
+    ts = [step() for _ in range(args.steps)]
     R.bench_destroy(h)
+    _assert_no_product_lib()
     t = sum(ts) / len(ts)
-    per_rank = 4.0 * n / t / 1e9
-    value = per_rank * args.gpus
+    value = 4.0 * n / t / 1e9
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GB/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t * 1e3, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic", "config": {"workload": f"{cfg}:{model}", "len": n, "nnz": nnz, "ratio": ratio},
+        "data": "synthetic",
+        "config": {"workload": workload_name(cfg, model, ratio, reprune), "len": n, "nnz": nnz, "ratio": ratio,
+                   "reprune_per_step": reprune, "parallelism": f"dp{args.gpus}"},
+        "value_job": round(value * args.gpus, 4),
         "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": cores, "kind": "reference",
-                         "sample": what + f"; {args.steps} steps, full {model} gradient per step"},
+                         "sample": what + prune_note + f"; {args.steps} steps, full {model} gradient per step"},
         "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     _emit(line)
@@ -200,13 +257,18 @@ def pcie_roofline(torch, gh, oh, dg, dout, stream, t_e2e):
             "note": "floor = concurrent H2D + D2H of the step's pinned buffers, measured in this run"}
 
 
-def cpu_baseline_sample(shape, ratio, words_np, n):
-    """Reference CPU path on this host, bounded sample (rank 0, N=1 only)."""
+def cpu_baseline_sample(shape, ratio, words_np, n, w_host=None):
+    """Reference CPU path on this host, bounded sample (rank 0, N=1 only):
+    the reference pack -> unpack over the full gradient on all host threads,
+    plus (re-pruning configs) the mask re-derivation by the oracle port's O(n)
+    magnitude_prune on one thread (the reference's stable_sort takes minutes
+    at this size)."""
     try:
         import oracle
         from paper_2505_18563_b200 import synth
 
         R = oracle.ref()
+        P = oracle.port()
         kind = "reference"
     except Exception as e:  # pragma: no cover
         return {"value": None, "unit": "GB/s", "cores": 0, "kind": "unavailable", "sample": str(e)}
@@ -220,9 +282,20 @@ def cpu_baseline_sample(shape, ratio, words_np, n):
         ts.append(R.bench_pack_unpack(h))
     R.bench_destroy(h)
     t = statistics.median(ts)
+    what = (f"reference pack->unpack (codec.cpp:14-38) over the full {shape.name} gradient, "
+            f"{nthreads} thread slices, median of {len(ts)} runs (~10 s)")
+    if w_host is not None:
+        tp = []
+        t0 = time.time()
+        while time.time() - t0 < 15.0 and len(tp) < 3:
+            a = time.perf_counter()
+            P.magnitude_prune(w_host, ratio)
+            tp.append(time.perf_counter() - a)
+        t += statistics.median(tp)
+        what += (f" + the mask re-derivation: oracle-port magnitude_prune (sparsity.cpp:44-59 restated, O(n), "
+                 f"1 thread) over all {n} weights, median of {len(tp)}")
     return {"value": round(4.0 * n / t / 1e9, 4), "unit": "GB/s", "cores": nthreads, "kind": kind,
-            "sample": f"reference pack->unpack (codec.cpp:14-38) over the full {shape.name} gradient, "
-                      f"{nthreads} thread slices, median of {len(ts)} runs (~10 s)"}
+            "sample": what}
 
 
 _JSON_OUT = None
@@ -257,7 +330,7 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="c5", choices=sorted(CONFIGS))
     ap.add_argument("--ratio", type=float, default=None, help="override the config's prune ratio")
     ap.add_argument("--bucket-mb", type=float, default=None)
     ap.add_argument("--transport", default="auto", choices=["auto", "nccl", "p2p"],
@@ -328,6 +401,42 @@ def main():
     transport = {"auto": 0, "nccl": 1, "p2p": 2}[args.transport]
     policy = pb.SyncPolicy(bucket_bytes=bucket if world > 1 else 0, transport=transport)
     w_cur = weights.clone() if reprune else None
+    pert = {}
+
+    def expand_keep(m, out_u8):
+        """mask words -> one byte per element (untimed bench plumbing)"""
+        b = m.words().view(torch.uint8)
+        sh = torch.arange(8, device=dev, dtype=torch.uint8)
+        torch.bitwise_and(torch.bitwise_right_shift(b.view(-1, 1), sh), 1, out=out_u8.view(-1, 8))
+
+    def perturb(t, kind="a9"):
+        """SURVEY A.9 between timed steps (untimed, identical on every rank):
+        kept weights drift (w + delta, |delta| <= 2^-14), pruned ones are
+        replaced by fresh regrowth noise (|eps| <= 2^-20, far below any kept
+        magnitude), so the mask is re-derived from new weights every step and
+        normally reproduces. kind="drift": a dense update of every weight
+        (|delta| <= 2^-17), which moves the threshold and flips elements near
+        it. kind="regrow": 4096 pruned weights become large (a real change)."""
+        if not pert:
+            nb = ((n + 63) // 64) * 64
+            pert["keep"] = torch.empty(nb, dtype=torch.uint8, device=dev)
+            pert["a"] = torch.empty(n, dtype=torch.float32, device=dev)
+            pert["b"] = torch.empty(n, dtype=torch.float32, device=dev)
+        keep, ta, tb = pert["keep"], pert["a"], pert["b"]
+        if kind == "drift":
+            pb.synth_fill(ta, synth.derive_seed(0xD81F7, t), synth.W_REAL, 2.0 ** -17)
+            w_cur.add_(ta)
+            return
+        expand_keep(mask, keep)
+        kb = keep[:n].bool()
+        if kind == "regrow":
+            idx = torch.nonzero(~kb)[(t * 4096) % max(1, n - nnz - 4096):][:4096, 0]
+            w_cur[idx] = 0.5
+            return
+        pb.synth_fill(ta, synth.derive_seed(0xA9D, t), synth.W_REAL, 2.0 ** -14)
+        pb.synth_fill(tb, synth.derive_seed(0xA9E, t), synth.W_REAL, 2.0 ** -20)
+        torch.add(w_cur, ta, out=ta)
+        torch.where(kb, ta, tb, out=w_cur)
 
     def barrier():
         if world > 1:
@@ -342,12 +451,15 @@ def main():
 
     align = torch.zeros(1, dtype=torch.float32, device=dev)
 
-    def timed(fn, k):
+    def timed(fn, k, pre=None):
         """k device-timed calls, L2 flushed before each; returns seconds list.
-        N > 1: a 1-element allreduce after the flush re-aligns the ranks on
-        the device, so no step is charged for a peer's flush."""
+        pre(i) runs (untimed) before call i. N > 1: a 1-element allreduce after
+        the flush re-aligns the ranks on the device, so no step is
+        charged for a peer's flush."""
         evs = []
         for i in range(k):
+            if pre is not None:
+                pre(i)
             l2_flush()
             if world > 1:
                 torch.distributed.all_reduce(align)
@@ -372,16 +484,31 @@ def main():
                         tracker, grad, out, timed, barrier)
 
     # ---- headline: device-resident step
+    paths = {}
+
+    def step_h(e):
+        if reprune:
+            st = {}
+            pb.magnitude_prune(w_cur, ratio, out=mask, stats=st)
+            paths[st["path"]] = paths.get(st["path"], 0) + 1
+            tracker.observe(mask)
+        return pb.masked_allreduce(grad, mask, tracker.status(), e, comm, policy=policy, out=out)
+
+    pre = perturb if reprune else None
     for i in range(args.warmup):
-        r = step(i)
+        if pre:
+            pre(10_000 + i)
+        r = step_h(i)
     assert r.stats.mode_used == pb.SyncMode.PackedAllReduce, r.stats
+    paths.clear()
     barrier()
     l0 = ctx.kernel_launches()
     with ClockSampler(local) as clk:
         barrier()
-        ts = timed(step, args.steps)
+        ts = timed(step_h, args.steps, pre=pre)
         barrier()
     launches = ctx.kernel_launches() - l0
+    assert r.stats.mode_used == pb.SyncMode.PackedAllReduce, r.stats
     t_step = sum(ts) / len(ts)
     qs = sorted(ts)
     pct = [qs[int(q * (len(qs) - 1))] for q in (0.1, 0.5, 0.9)]
@@ -391,7 +518,7 @@ def main():
         t_step, pct = float(tt[0].item()), [float(x) for x in tt[1:].tolist()]
     step_dist = {"p10_us": round(pct[0] * 1e6, 1), "p50_us": round(pct[1] * 1e6, 1), "p90_us": round(pct[2] * 1e6, 1)}
     per_rank_gbs = 4.0 * n / t_step / 1e9
-    value = per_rank_gbs * world
+    value = per_rank_gbs
 
     # ---- dominant kernel roofline: pack and unpack timed alone (flushed)
     packed = torch.empty(max(1, nnz), dtype=torch.float32, device=dev)
@@ -417,9 +544,75 @@ def main():
         stages["step_breakdown_us"] = {"total": round(med[0], 1), "pack": round(med[1], 1),
                                        "exchange": round(med[2], 1), "unpack": round(med[3], 1)}
     if reprune:
-        t_prune = statistics.median(timed(lambda i: pb.magnitude_prune(w_cur, ratio, out=mask), 5))
-        stages["prune_us"] = round(t_prune * 1e6, 1)
-        stages["prune_gbs"] = round((4 * n + n / 8) / t_prune / 1e9, 1)
+        # the prune paths on their own (prune.cu; DESIGN 3a): threshold reuse,
+        # A.9 (the headline's), a dense drift that moves the threshold and
+        # flips elements (+ the digest the tracker then needs), a regrowth
+        # that changes the mask, and the first-time sampled path
+        alg_prune = 4 * n + n / 8
+        pr = {}
+
+        def prune_only(i):
+            st = {}
+            pb.magnitude_prune(w_cur, ratio, out=mask, stats=st)
+            pr.setdefault("paths", []).append(st["path"])
+
+        def prune_digest(i):
+            prune_only(i)
+            mask.digest()
+        t_hit = statistics.median(timed(prune_only, 5))
+        pr["paths"] = []
+        t_a9 = statistics.median(timed(prune_only, 5, pre=lambda i: perturb(20_000 + i)))
+        p_a9 = pr.pop("paths")
+        # dense drift from the dense (never GSE'd) weights, on its own mask
+        w_keep, mask_keep = w_cur, mask
+        w_cur = weights.clone()
+        mask = pb.magnitude_prune(w_cur, ratio)
+        pb.magnitude_prune(w_cur, ratio, out=mask)
+        t_drift = statistics.median(timed(prune_digest, 5, pre=lambda i: perturb(30_000 + i, "drift")))
+        p_drift = pr.pop("paths")
+        w_cur, mask = w_keep, mask_keep
+        t_regrow = statistics.median(timed(prune_digest, 5, pre=lambda i: perturb(40_000 + i, "regrow")))
+        p_regrow = pr.pop("paths")
+        scratch = pb.SparsityMask(n)
+
+        def prune_full(i):
+            st = {}
+            pb.magnitude_prune(w_cur, ratio, out=scratch, stats=st)
+            pr.setdefault("paths", []).append(st["path"])
+        prune_full(0)
+        t_full = statistics.median(timed(prune_full, 3, pre=lambda i: pb.api._call(
+            pb.api.lib.pact_mask_fill, scratch.handle, 0, pb.api._stream())))
+        p_full = pr.pop("paths")
+        del scratch
+        # a whole step whose mask changed (regrowth), on the packed path
+        # (the tracker would fall back to dense for K steps; this is the cost
+        # of the mask regeneration itself) vs the headline's steady state
+        def step_stable(e):
+            pb.magnitude_prune(w_cur, ratio, out=mask)
+            mask.digest()
+            return pb.masked_allreduce(grad, mask, pb.TrackerStatus.Stable, e, comm, policy=policy, out=out)
+        t_step_change = statistics.median(timed(step_stable, 5, pre=lambda i: perturb(50_000 + i, "regrow")))
+        t_step_hit = statistics.median(timed(step_stable, 5))
+        if world > 1:
+            tt = torch.tensor([t_hit, t_a9, t_drift, t_regrow, t_full, t_step_change, t_step_hit],
+                              dtype=torch.float64, device=dev)
+            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+            t_hit, t_a9, t_drift, t_regrow, t_full, t_step_change, t_step_hit = tt.tolist()
+        stages["prune"] = {
+            "reuse_hit_us": round(t_hit * 1e6, 1), "reuse_hit_gbs": round(alg_prune / t_hit / 1e9, 1),
+            "a9_us": round(t_a9 * 1e6, 1), "a9_paths": p_a9,
+            "dense_drift_plus_digest_us": round(t_drift * 1e6, 1), "dense_drift_paths": p_drift,
+            "regrowth_change_plus_digest_us": round(t_regrow * 1e6, 1), "regrowth_paths": p_regrow,
+            "first_time_sampled_us": round(t_full * 1e6, 1), "first_time_paths": p_full,
+            "paths_legend": "1 sampled window, 2 full radix, 3 threshold reuse, 4 moved threshold from window candidates",
+        }
+        stages["mask_change_step_us"] = round(t_step_change * 1e6, 1)
+        stages["mask_reuse_step_us"] = round(t_step_hit * 1e6, 1)
+        stages["mask_change_vs_reuse_step"] = round(t_step_change / t_step_hit, 3)
+        # back to a stable tracker for the e2e leg
+        for _ in range(4):
+            pb.magnitude_prune(w_cur, ratio, out=mask)
+            tracker.observe(mask)
     if t_pack >= t_unpack:
         dom, alg, tdom = "pack_lm_kernel<0>", alg_pack, t_pack
     else:
@@ -450,7 +643,7 @@ def main():
         # the exchange as the step pays for it: step time minus pack and
         # unpack timed alone (the P2P exchange is fused into them, so there
         # is no separate exchange kernel to time)
-        t_x = max(t_step - t_pack - t_unpack - (t_prune if reprune else 0.0), 1e-9)
+        t_x = max(t_step - t_pack - t_unpack - (t_a9 if reprune else 0.0), 1e-9)
         extra = {"dense_allreduce_us": round(t_dense * 1e6, 1),
                  "dense_busbw_gbs": round(4 * n * f / t_dense / 1e9, 1),
                  "packed_allreduce_us": round(t_packed_ar * 1e6, 1),
@@ -463,22 +656,35 @@ def main():
                  "nvlink_peak_gbs": 900.0,
                  "step_exchange_busbw_frac_of_nvlink": round(4 * nnz * f / t_x / 1e9 / 900.0, 3),
                  "dense_sync_equiv_gbs_per_rank": round(4 * n / t_dense / 1e9, 1)}
+        bx = stages.get("step_breakdown_us", {}).get("exchange", 0.0) * 1e-6
+        if bx > 0:  # NCCL transport: the exchange timed directly inside the step (events around it)
+            extra["exchange_in_step_us"] = round(bx * 1e6, 1)
+            extra["exchange_in_step_busbw_gbs"] = round(4 * nnz * f / bx / 1e9, 1)
+            extra["exchange_in_step_vs_dense_busbw"] = round((4 * nnz * f / bx) / (4 * n * f / t_dense), 3)
 
     # ---- e2e through the host-buffer C-ABI entry point
     e2e = None
     if not args.no_e2e:
         gh = grad.cpu().pin_memory()
         oh = torch.empty(n, dtype=torch.float32).pin_memory()
+
+        def step_e2e(i):
+            if reprune:  # the weights are model state on the device; the gradient comes from the host
+                pb.magnitude_prune(w_cur, ratio, out=mask)
+                tracker.observe(mask)
+            return pb.masked_allreduce_host(gh, mask, tracker.status(), i, comm, oh, policy=policy)
         for i in range(2):
-            pb.masked_allreduce_host(gh, mask, tracker.status(), i, comm, oh, policy=policy)
+            step_e2e(i)
         barrier()
         te = []
         for i in range(max(5, min(args.steps, 20))):
+            if reprune:
+                perturb(60_000 + i)
             l2_flush()
             torch.cuda.synchronize()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
-            pb.masked_allreduce_host(gh, mask, tracker.status(), i, comm, oh, policy=policy)
+            st_e = step_e2e(i)
             b.record(stream)
             b.synchronize()
             te.append(a.elapsed_time(b) * 1e-3)
@@ -487,13 +693,17 @@ def main():
             tt = torch.tensor([t_e2e], dtype=torch.float64, device=dev)
             torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
             t_e2e = float(tt.item())
-        e2e = {"value": round(4.0 * n / t_e2e / 1e9 * world, 3), "unit": "GB/s",
+        e2e = {"value": round(4.0 * n / t_e2e / 1e9, 3), "unit": "GB/s",
                "h2d_bytes_per_step": 4 * n, "d2h_bytes_per_step": 4 * n, "ms_per_step": round(t_e2e * 1e3, 3),
+               "mode": "packed" if st_e.mode_used == pb.SyncMode.PackedAllReduce else "dense",
+               "includes": "prune of the device weights + pact_masked_allreduce_host (pinned H2D of the "
+                           "gradient, D2H of the result)" if reprune else "pact_masked_allreduce_host",
                "roofline": pcie_roofline(torch, gh, oh, grad, out, stream, t_e2e)}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline_sample(shape, ratio, mask.words_host(), n)
+        cpu = cpu_baseline_sample(shape, ratio, mask.words_host(), n,
+                                  w_cur.cpu().numpy() if reprune else None)
 
     if rank == 0:
         line = {
@@ -501,15 +711,21 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t_step * 1e3, 4),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
-            "config": {"workload": f"{cfg}:{model} fp32 grads, {int(round(ratio * 100))}% magnitude-pruned mask",
+            "value_job": round(value * world, 2),
+            "config": {"workload": workload_name(cfg, model, ratio, reprune),
                        "len": n, "nnz": nnz, "ratio": ratio, "reprune_per_step": reprune,
+                       "weights": "W-real (SURVEY A.9), identical on every rank",
+                       "perturbation": ("A.9 between timed steps: kept w += delta (|delta| <= 2^-14), pruned "
+                                        "w = fresh noise (|eps| <= 2^-20); prune paths taken: "
+                                        + json.dumps({str(k): v for k, v in sorted(paths.items())}))
+                       if reprune else None,
                        "l2": "flushed before every timed step (512 MiB write, then a 512 MiB read "
                              "so the flush's dirty lines are written back outside the timed region)",
                        "host_gate": "1 ms device spin before each timed step's start event (launches "
                                     "enqueued ahead; e2e keeps the host cost)",
                        "parallelism": f"dp{world}", "bucket_bytes": policy.bucket_bytes,
                        "transport": ["none", "nccl", "nvlink-p2p"][r.stats.transport],
-                       "per_rank_gbs": round(per_rank_gbs, 2)},
+                       "value_is": "per rank: 4*len / t_step (SURVEY 8(d)); value_job = n_gpus x value"},
             "step_distribution": step_dist,
             "roofline": roofline, "stages": stages, **({"allreduce": extra} if extra else {}),
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
@@ -554,7 +770,7 @@ def run_sweep(args, pb, torch, comm, rank, world, local, dev, cfg, model, n, wei
                 r = st(i)
             res[name] = (tmax(statistics.median(timed(st, k))), r.stats.mode_used)
         best = min(res["packed"][0], res["dense"][0])
-        gbs.append(4.0 * n * world / res["auto"][0] / 1e9)
+        gbs.append(4.0 * n / res["auto"][0] / 1e9)
         rows.append({"ratio": ratio, "density": round(m.nnz() / n, 6),
                      "packed_us": round(res["packed"][0] * 1e6, 1), "dense_us": round(res["dense"][0] * 1e6, 1),
                      "auto_us": round(res["auto"][0] * 1e6, 1),
@@ -643,7 +859,7 @@ def run_path(args, pb, torch, comm, rank, world, local, dev, cfg, model, ratio, 
     if rank == 0:
         line = {
             "metric": METRIC.replace("prune+pack+allreduce+unpack", args.path + " aggregate"),
-            "value": round(4.0 * n / t_step / 1e9 * world, 2), "unit": "GB/s", "n_gpus": world,
+            "value": round(4.0 * n / t_step / 1e9, 2), "unit": "GB/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t_step * 1e3, 4),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "path": args.path,

@@ -18,6 +18,7 @@
 #include <cstdint>
 #include <algorithm>
 #include <cstring>
+#include <functional>
 #include <memory>
 #include <optional>
 #include <stdexcept>
@@ -208,6 +209,32 @@ inline SparsityMask magnitude_prune(const FlatTensor& weights, float ratio) {
   return magnitude_prune(d.get(), weights.size(), ratio);
 }
 
+// sparsity.hpp:15-31, sparsity.cpp:11-15. GraSP (PruneMethod::Grasp) is off
+// the gradient-sync path (out of scope): build_prune_mask rejects it.
+enum class PruneMethod { Magnitude, Grasp };
+enum class GraspKeep { MostNegative, MostPositive };
+struct PruneConfig {
+  float ratio = 0.0f;  // fraction of elements to drop, in [0, 1)
+  PruneMethod method = PruneMethod::Magnitude;
+  float grasp_epsilon = 1e-2f;
+  GraspKeep grasp_keep = GraspKeep::MostNegative;
+  void validate() const {
+    if (!(ratio >= 0.0f && ratio < 1.0f))
+      throw Error(Errc::InvalidRatio, "prune ratio " + std::to_string(ratio) + " outside [0, 1)");
+    if (!(grasp_epsilon > 0.0f)) throw Error(Errc::InvalidRatio, "grasp_epsilon must be positive");
+  }
+};
+using GradientFn = std::function<FlatTensor(const FlatTensor&)>;  // sparsity.hpp:69
+
+// sparsity.cpp:121-128
+inline SparsityMask build_prune_mask(const FlatTensor& weights, const PruneConfig& cfg,
+                                     const GradientFn& grad_of = nullptr) {
+  cfg.validate();
+  if (cfg.method == PruneMethod::Magnitude) return magnitude_prune(weights, cfg.ratio);
+  if (!grad_of) throw Error(Errc::NumericalFailure, "gradient-flow pruning needs a gradient function");
+  throw Error(Errc::RunFailure, "GraSP pruning is not part of the B200 gradient-sync path");
+}
+
 // sparsity.cpp:112-119
 inline FlatTensor enforce_gradient_sparsity(const FlatTensor& grad, const SparsityMask& mask) {
   if (grad.size() != mask.size()) throw Error(Errc::ShapeMismatch, "gradient/mask length mismatch");
@@ -357,6 +384,58 @@ inline FrameHeader decode_header(const Bytes& f) {
   detail::check(pact_header_decode(reinterpret_cast<const uint8_t*>(f.data()), f.size(), &c));
   return {static_cast<PayloadKind>(c.kind), c.epoch, c.mask_digest, c.value_count};
 }
+namespace detail {
+inline void put_f32s(Bytes& b, const float* v, size_t n) {  // little-endian binary32 (codec.cpp:214-218)
+  const size_t o = b.size();
+  b.resize(o + 4 * n);
+  for (size_t i = 0; i < n; ++i) {
+    uint32_t u;
+    std::memcpy(&u, v + i, 4);
+    for (int k = 0; k < 4; ++k) b[o + 4 * i + k] = static_cast<std::byte>((u >> (8 * k)) & 0xffu);
+  }
+}
+inline void get_f32s(const Bytes& b, size_t off, float* v, size_t n) {  // codec.cpp:220-237
+  for (size_t i = 0; i < n; ++i) {
+    uint32_t u = 0;
+    for (int k = 0; k < 4; ++k) u |= static_cast<uint32_t>(std::to_integer<uint8_t>(b[off + 4 * i + k])) << (8 * k);
+    std::memcpy(v + i, &u, 4);
+  }
+}
+inline void need(const Bytes& b, size_t n) {  // codec.cpp:239-241
+  if (b.size() < n) throw Error(Errc::CorruptPayload, "frame truncated");
+}
+}  // namespace detail
+// codec.cpp:277-291
+inline Bytes encode_full(const FlatTensor& grad, uint32_t epoch) {
+  Bytes b = encode_header({PayloadKind::Full, epoch, 0, grad.size()});
+  detail::put_f32s(b, grad.data(), grad.size());
+  return b;
+}
+inline FlatTensor decode_full(const Bytes& frame) {
+  const FrameHeader h = decode_header(frame);
+  if (h.kind != PayloadKind::Full) throw Error(Errc::CorruptPayload, "not a full frame");
+  detail::need(frame, kHeaderSize + h.value_count * 4);
+  std::vector<float> v(h.value_count);
+  detail::get_f32s(frame, kHeaderSize, v.data(), v.size());
+  return FlatTensor(std::move(v));
+}
+// codec.cpp:293-311
+inline Bytes encode_packed(const PackedGradient& packed) {
+  Bytes b = encode_header({PayloadKind::Packed, packed.epoch, packed.mask_digest, packed.values.size()});
+  detail::put_f32s(b, packed.values.data(), packed.values.size());
+  return b;
+}
+inline PackedGradient decode_packed(const Bytes& frame) {
+  const FrameHeader h = decode_header(frame);
+  if (h.kind != PayloadKind::Packed) throw Error(Errc::CorruptPayload, "not a packed frame");
+  detail::need(frame, kHeaderSize + h.value_count * 4);
+  PackedGradient p;
+  p.mask_digest = h.mask_digest;
+  p.epoch = h.epoch;
+  p.values.resize(h.value_count);
+  detail::get_f32s(frame, kHeaderSize, p.values.data(), p.values.size());
+  return p;
+}
 }  // namespace wire
 
 // ------------------------------------------------------------ collective
@@ -428,6 +507,38 @@ inline double calibrate_density(Comm& comm, size_t len) {
   detail::check(pact_calibrate_density(comm.handle(), detail::ctx(), len, nullptr, nullptr, 0, nullptr, nullptr,
                                        &thr, nullptr));
   return thr;
+}
+
+// collective.cpp:165-216: the SUM with the reference ring's own fold order,
+// bit-identical on every rank (NVLink peer memory; ShapeMismatch when the
+// ranks' lengths differ)
+inline FlatTensor ring_allreduce(const FlatTensor& local, Comm& comm) {
+  auto d = detail::dev_alloc<float>(local.size());
+  detail::cuda(cudaMemcpy(d.get(), local.data(), local.size() * 4, cudaMemcpyHostToDevice));
+  detail::check(pact_ring_allreduce(comm.handle(), d.get(), d.get(), local.size(), nullptr));
+  std::vector<float> out(local.size());
+  detail::cuda(cudaMemcpy(out.data(), d.get(), out.size() * 4, cudaMemcpyDeviceToHost));
+  return FlatTensor(std::move(out));
+}
+
+// collective.cpp:222-247: every rank ends with all n payloads, indexed by
+// rank (payload sizes may differ: the sizes go first, then padded frames)
+inline std::vector<std::vector<std::byte>> allgather(const std::vector<std::byte>& payload, Comm& comm) {
+  const int n = comm.world_size();
+  const uint64_t mine = payload.size();
+  std::vector<uint64_t> sizes(n);
+  detail::check(pact_allgather_frames(comm.handle(), reinterpret_cast<const uint8_t*>(&mine), 8,
+                                      reinterpret_cast<uint8_t*>(sizes.data()), nullptr));
+  const uint64_t mx = std::max<uint64_t>(1, *std::max_element(sizes.begin(), sizes.end()));
+  std::vector<uint8_t> frame(mx, 0), all((size_t)n * mx);
+  std::memcpy(frame.data(), payload.data(), payload.size());
+  detail::check(pact_allgather_frames(comm.handle(), frame.data(), mx, all.data(), nullptr));
+  std::vector<std::vector<std::byte>> out(n);
+  for (int r = 0; r < n; ++r) {
+    out[r].resize(sizes[r]);
+    std::memcpy(out[r].data(), all.data() + (size_t)r * mx, sizes[r]);
+  }
+  return out;
 }
 
 // collective.cpp:253-259; returns the SUM

@@ -289,12 +289,31 @@ pact_status pact_comm_unique_id(uint8_t out[PACT_UNIQUE_ID_BYTES]);
 pact_status pact_comm_create(pact_ctx* ctx, const uint8_t id[PACT_UNIQUE_ID_BYTES], int nranks,
                              int rank, pact_comm** out);
 pact_status pact_comm_destroy(pact_comm* c);
+/* Fail-fast (reference SimCluster::poison + LinkError, collective.cpp:430-458):
+ * waits for `stream` with a deadline (timeout_ms <= 0: PACT_LINK_TIMEOUT_MS,
+ * default 30 s). A peer that stopped publishing (NVLink flags, the vote
+ * board) or an NCCL asynchronous error returns PACT_E_LINK; on the deadline
+ * the NCCL communicator is aborted (its kernels exit) and PACT_E_LINK is
+ * returned. After a PACT_E_LINK every collective on the comm returns
+ * PACT_E_LINK immediately. */
+pact_status pact_comm_check(pact_comm* c, pact_stream_t stream, int timeout_ms);
+int pact_comm_failed(const pact_comm* c);
 int pact_comm_rank(const pact_comm* c);
 int pact_comm_size(const pact_comm* c);
 
 /* collective.cpp:165-216 ring_allreduce (SUM, fp32). in may equal out. */
 pact_status pact_allreduce_sum(pact_comm* c, const float* in, float* out, uint64_t count,
                                pact_stream_t stream);
+
+/* collective.cpp:93-131, 165-216 ring_allreduce in the reference's exact
+ * arithmetic: every element of ChunkMap(count, n) chunk c is folded as
+ * ((x_c + x_{c+1}) + ...) + x_{c-1}, so every rank receives bits identical to
+ * the reference ring (NCCL's order is unspecified). Runs over NVLink peer
+ * memory (one node); the counts are agreed first, PACT_E_SHAPE_MISMATCH on
+ * every rank if they differ (the reference's size check);
+ * PACT_E_BAD_TOPOLOGY if the ranks cannot map each other's memory. */
+pact_status pact_ring_allreduce(pact_comm* c, const float* in, float* out, uint64_t count,
+                                pact_stream_t stream);
 
 /* collective.cpp:222-247 allgather of one fixed-size frame per rank (host
  * buffers; frames_out holds n*frame_bytes, indexed by rank). Synchronous. */

@@ -94,6 +94,9 @@ SIGNATURES = {
     "pact_comm_rank": (C.c_int, [vp]),
     "pact_comm_size": (C.c_int, [vp]),
     "pact_allreduce_sum": (C.c_int, [vp, vp, vp, C.c_uint64, vp]),
+    "pact_ring_allreduce": (C.c_int, [vp, vp, vp, C.c_uint64, vp]),
+    "pact_comm_check": (C.c_int, [vp, vp, C.c_int]),
+    "pact_comm_failed": (C.c_int, [vp]),
     "pact_allgather_frames": (C.c_int, [vp, u8p, C.c_size_t, u8p, vp]),
     "pact_full_allreduce": (C.c_int, [vp, vp, vp, C.c_uint64, C.c_float, C.POINTER(SyncStatsC), vp]),
     "pact_masked_allreduce": (C.c_int, [vp, vp, vp, C.c_uint64, vp, C.c_int, C.c_uint32, u64p,

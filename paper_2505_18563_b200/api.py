@@ -652,17 +652,35 @@ class Comm:
     def world_size(self) -> int:
         return int(lib.pact_comm_size(self.handle))
 
+    def check(self, timeout_ms: int = 0) -> None:
+        """Wait for this rank's collectives on the current stream with a
+        deadline; raises Error(LinkError) when a peer is lost (reference
+        SimCluster::poison, collective.cpp:430-458). timeout_ms <= 0:
+        PACT_LINK_TIMEOUT_MS (default 30 s)."""
+        _call(lib.pact_comm_check, self.handle, _stream(), int(timeout_ms))
+
+    @property
+    def failed(self) -> bool:
+        return bool(lib.pact_comm_failed(self.handle))
+
     def close(self) -> None:
         if getattr(self, "handle", None) is not None and self.handle.value:
             lib.pact_comm_destroy(self.handle)
             self.handle = None
 
 
-def ring_allreduce(local: torch.Tensor, comm: Comm, out: Optional[torch.Tensor] = None) -> torch.Tensor:
-    """collective.cpp:165-216 semantics (SUM); NCCL chooses the reduction order."""
+def ring_allreduce(local: torch.Tensor, comm: Comm, out: Optional[torch.Tensor] = None,
+                   exact: bool = False) -> torch.Tensor:
+    """collective.cpp:165-216 (SUM). exact=False: NCCL chooses the reduction
+    order; exact=True: the reference's own fold order over NVLink peer memory
+    (pact_ring_allreduce), bit-identical to the reference ring on every rank,
+    with the reference's length agreement (ShapeMismatch)."""
     g = _as_grad(local, "local")
     o = torch.empty_like(g) if out is None else out
-    _call(lib.pact_allreduce_sum, comm.handle, _ptr(g), _ptr(o), g.numel(), _stream())
+    if exact:
+        _call(lib.pact_ring_allreduce, comm.handle, _ptr(g), _ptr(o), g.numel(), _stream())
+    else:
+        _call(lib.pact_allreduce_sum, comm.handle, _ptr(g), _ptr(o), g.numel(), _stream())
     return o
 
 

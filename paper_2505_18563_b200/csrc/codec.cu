@@ -25,6 +25,8 @@
 // per chunk at 65% issue utilisation and 33% of DRAM peak).
 #include <cstdlib>
 
+#include <atomic>
+
 #include "common.cuh"
 #include "launch.h"
 #include "p2p_sync.cuh"
@@ -44,7 +46,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
-unsigned long long g_launches = 0;
+std::atomic<unsigned long long> g_launches{0};
 
 int sm_count() {
   static int sms = 0;
@@ -401,7 +403,7 @@ __global__ void __launch_bounds__(kPuWarps * 32)
                   const uint32_t* __restrict__ chunk_off, float scale, int do_scale,
                   float* __restrict__ out, float lr, float* __restrict__ weights, uint64_t cb,
                   uint64_t ce, P2PView v, const uint64_t* __restrict__ flags, uint64_t target,
-                  int* __restrict__ err, P2PSig sg) {
+                  P2PErr* __restrict__ err, P2PSig sg) {
   constexpr int kRS = kA + 1, kWS = kA + 2;  // run / word stages
   constexpr int kRun = kSrc == kSrcPair ? 2 * kRunCap : kRunCap;
   extern __shared__ __align__(16) float psm_base[];  // unpack_smem_bytes<kSrc, kA>()
@@ -410,7 +412,8 @@ __global__ void __launch_bounds__(kPuWarps * 32)
   if constexpr (kSrc != kSrcLocal) {  // peers' PACKED (one-shot) / REDUCED (two-shot) flags
     p2psync::entry_signal(v, sg);
     if (sg.trace && threadIdx.x == 0) atomicMin(&g_pair_trace[2], gtimer());
-    p2psync::block_wait_flags(flags, kSrc == kSrcPair ? kP2PPacked : kP2PReduced, v.n, target, err);
+    if (!p2psync::block_wait_flags(flags, kSrc == kSrcPair ? kP2PPacked : kP2PReduced, v.n, target, err))
+      return;  // the exchange failed: no peer reads, no READ signal (LinkError on the host)
     if (sg.trace && threadIdx.x == 0) atomicMax(&g_pair_trace[3], gtimer());
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -638,7 +641,8 @@ __global__ void chunk_popc_kernel(const uint64_t* __restrict__ words, uint64_t n
 // Single-pass exclusive scan (decoupled look-back): 8192 values per CTA,
 // tiles ordered by a ticket so every CTA's predecessors are running or done.
 constexpr uint64_t kStAgg = 1ull << 62, kStIncl = 2ull << 62, kStMask = 3ull << 62;
-constexpr int kScanItems = 8192;
+constexpr int kScanPerThread = 8;  // 2 x uint4 per thread
+constexpr int kScanItems = 1024 * kScanPerThread;
 
 __global__ void __launch_bounds__(1024) scan_excl_kernel(const uint32_t* __restrict__ in, uint64_t n,
                                                          uint32_t* __restrict__ out,
@@ -652,14 +656,25 @@ __global__ void __launch_bounds__(1024) scan_excl_kernel(const uint32_t* __restr
   __syncthreads();
   const uint64_t t = s_tile;
   const uint64_t base = t * kScanItems;
-  uint32_t v[8];
+  uint32_t v[kScanPerThread];
   uint32_t s = 0;
+  const uint64_t b0 = base + (uint64_t)tid * kScanPerThread;
+  const bool vec = b0 + kScanPerThread <= n && ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15) == 0;
+  if (vec) {
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const uint64_t idx = base + (uint64_t)tid * 8 + i;
-    v[i] = idx < n ? in[idx] : 0u;
-    s += v[i];
+    for (int i = 0; i < kScanPerThread / 4; ++i) {
+      const uint4 q = __ldg(reinterpret_cast<const uint4*>(in + b0) + i);
+      v[4 * i] = q.x;
+      v[4 * i + 1] = q.y;
+      v[4 * i + 2] = q.z;
+      v[4 * i + 3] = q.w;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < kScanPerThread; ++i) v[i] = b0 + i < n ? in[b0 + i] : 0u;
   }
+#pragma unroll
+  for (int i = 0; i < kScanPerThread; ++i) s += v[i];
   const uint32_t inc = warp_incl_scan(s);
   if (lane == 31) warp_tot[warp] = inc;
   __syncthreads();
@@ -695,10 +710,19 @@ __global__ void __launch_bounds__(1024) scan_excl_kernel(const uint32_t* __restr
   __syncthreads();
   uint32_t run = (uint32_t)s_prefix + warp_tot[warp] + inc - s;
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const uint64_t idx = base + (uint64_t)tid * 8 + i;
-    if (idx < n) out[idx] = run;
-    run += v[i];
+  for (int i = 0; i < kScanPerThread; ++i) {
+    const uint32_t x = v[i];
+    v[i] = run;
+    run += x;
+  }
+  if (vec) {
+#pragma unroll
+    for (int i = 0; i < kScanPerThread / 4; ++i)
+      reinterpret_cast<uint4*>(out + b0)[i] = make_uint4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+  } else {
+#pragma unroll
+    for (int i = 0; i < kScanPerThread; ++i)
+      if (b0 + i < n) out[b0 + i] = v[i];
   }
 }
 
@@ -799,7 +823,9 @@ void unpack_local(const float* packed, uint64_t len, const uint64_t* words, cons
                   int do_scale, float* out, float lr, float* weights, uint64_t cb, uint64_t ce, cudaStream_t s,
                   bool pdl = false) {
   constexpr int kDyn1 = unpack_smem_bytes<kSrcLocal, 1>(), kDyn2 = unpack_smem_bytes<kSrcLocal, 2>();
-  static int cap1 = 0, cap2 = 0;
+  static DeviceCache<int> c1c, c2c;  // dyn-smem opt-ins are per device
+  int& cap1 = c1c.get();
+  int& cap2 = c2c.get();
   if (!cap1) {
     cap1 = persistent_grid_dyn(unpack_kernel<kSgd, kSrcLocal, 1>, kPuWarps, kDyn1);
     cap2 = persistent_grid_dyn(unpack_kernel<kSgd, kSrcLocal, 2>, kPuWarps, kDyn2);
@@ -820,7 +846,7 @@ void unpack_local(const float* packed, uint64_t len, const uint64_t* words, cons
   const P2PView v{};
   const P2PSig sg{};
   const uint64_t* nf = nullptr;
-  int* ne = nullptr;
+  P2PErr* ne = nullptr;
   if (deep)
     cudaLaunchKernelEx(&cfg, unpack_kernel<kSgd, kSrcLocal, 2>, packed, len, words, chunk_off, scale, do_scale, out,
                        lr, weights, cb, ce, v, nf, (uint64_t)0, ne, sg);
@@ -840,7 +866,7 @@ void launch_unpack(const float* packed, uint64_t len, const uint64_t* words,
 
 void launch_unpack_p2p(const float* packed_local, uint64_t len, const uint64_t* words,
                        const uint32_t* chunk_off, float scale, int do_scale, float* out, const P2PView& v,
-                       int two_shot, const uint64_t* flags, uint64_t target, int* err, const P2PSig& sg,
+                       int two_shot, const uint64_t* flags, uint64_t target, P2PErr* err, const P2PSig& sg,
                        cudaStream_t s) {
   const uint64_t nc = (len + kChunk - 1) / kChunk;
   if (!nc) return;
@@ -848,7 +874,8 @@ void launch_unpack_p2p(const float* packed_local, uint64_t len, const uint64_t* 
   // per warp 0 (grid <= ceil(nc / kPuWarps))
   if (!two_shot) {
     constexpr int kDyn = unpack_smem_bytes<kSrcPair, 1>();
-    static int cap = 0;
+    static DeviceCache<int> cc;
+    int& cap = cc.get();
     if (!cap) cap = persistent_grid_dyn(unpack_kernel<false, kSrcPair, 1>, kPuWarps, kDyn);
     // (Tried: a programmatic dependent launch after the push pack, waiting on
     // PACKED instead of the grid: the ~10 us gap after the push pack stays
@@ -857,7 +884,8 @@ void launch_unpack_p2p(const float* packed_local, uint64_t len, const uint64_t* 
         packed_local, len, words, chunk_off, scale, do_scale, out, 0.f, nullptr, 0, nc, v, flags, target,
         err, sg);
   } else {
-    static int cap = 0;
+    static DeviceCache<int> cc;
+    int& cap = cc.get();
     constexpr int kDyn = unpack_smem_bytes<kSrcOwner, 1>();
     if (!cap) cap = persistent_grid_dyn(unpack_kernel<false, kSrcOwner, 1>, kPuWarps, kDyn);
     unpack_kernel<false, kSrcOwner, 1><<<grid_for(cap, nc, kPuWarps), kPuWarps * 32, kDyn, s>>>(

@@ -16,7 +16,7 @@
 //  (3) With the low-byte trajectory fixed, h ^ b == h + d(s, b), so a segment
 //      is the affine map h -> P^L * h + (g_L - s0 * P^L), g_L = the FNV chain
 //      of the segment started from the value s0; affine maps compose.
-// Each thread owns a 256-byte segment, a CTA a tile of 256 segments. Three
+// Each thread owns a 128-byte segment, a CTA a tile of 256 segments. Three
 // kernels, one per fact; each composes its per-thread maps into a tile map
 // (warp shuffles + 8 warp totals) and the last CTA to finish scans the tile
 // maps (the classic last-block pattern), so a digest is 3 kernels and a
@@ -33,7 +33,7 @@ namespace {
 constexpr uint64_t kFnvBasis = 0xcbf29ce484222325ull;
 constexpr uint64_t kFnvPrime = 0x100000001b3ull;
 constexpr int kDThreads = 256;             // segments per tile
-constexpr int kSegWords = 32;              // 256 bytes per segment (thread)
+constexpr int kSegWords = 16;              // 128 bytes per segment (thread)
 constexpr int kTileWordsD = kDThreads * kSegWords;
 
 __host__ __device__ inline uint64_t pow_p(uint64_t e) {
@@ -158,6 +158,27 @@ __device__ void scan_tiles(const uint4* tile_map, uint32_t* tile_in, uint32_t nt
   }
 }
 
+// the thread's whole segment in registers before the serial chain: 8
+// independent 16-byte loads in flight instead of one 8-byte load per step
+struct SegRegs {
+  uint2 w[kSegWords];
+};
+__device__ __forceinline__ void load_seg(const uint64_t* __restrict__ words, uint64_t seg, int nw, SegRegs& r) {
+  const uint64_t* src = words + seg * kSegWords;
+  if (nw == kSegWords) {
+#pragma unroll
+    for (int i = 0; i < kSegWords / 2; ++i) {
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>(src) + i);
+      r.w[2 * i] = make_uint2(v.x, v.y);
+      r.w[2 * i + 1] = make_uint2(v.z, v.w);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < kSegWords; ++i)
+      r.w[i] = i < nw ? __ldg(reinterpret_cast<const uint2*>(src) + i) : make_uint2(0u, 0u);
+  }
+}
+
 __device__ __forceinline__ int seg_words(uint64_t nwords, uint64_t seg) {
   const uint64_t w0 = seg * kSegWords;
   return w0 >= nwords ? 0 : (int)min((uint64_t)kSegWords, nwords - w0);
@@ -170,10 +191,13 @@ __global__ void __launch_bounds__(kDThreads)
   __shared__ MapScratch sh;
   const uint64_t seg = (uint64_t)blockIdx.x * kDThreads + threadIdx.x;
   const int nw = seg_words(nwords, seg);
-  const uint2* src = reinterpret_cast<const uint2*>(words + seg * kSegWords);
+  SegRegs sr;
+  load_seg(words, seg, nw, sr);
   uint4 x = map_identity();
-  for (int i = 0; i < nw; ++i) {
-    const uint2 wv = __ldg(src + i);
+#pragma unroll
+  for (int i = 0; i < kSegWords; ++i) {
+    if (i >= nw) break;
+    const uint2 wv = sr.w[i];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const uint32_t w32 = h ? wv.y : wv.x;
@@ -208,11 +232,14 @@ __global__ void __launch_bounds__(kDThreads)
   const int nw = seg_words(nwords, seg);
   const uint32_t tin = tile_scan_map(seg_low[seg], tile_tin[blockIdx.x], sh);
   seg_tin[seg] = (uint8_t)tin;
-  const uint2* src = reinterpret_cast<const uint2*>(words + seg * kSegWords);
+  SegRegs sr;
+  load_seg(words, seg, nw, sr);
   uint4 x = map_identity();
   uint32_t t = tin;
-  for (int i = 0; i < nw; ++i) {
-    const uint2 wv = __ldg(src + i);
+#pragma unroll
+  for (int i = 0; i < kSegWords; ++i) {
+    if (i >= nw) break;
+    const uint2 wv = sr.w[i];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const uint32_t w32 = h ? wv.y : wv.x;
@@ -253,10 +280,13 @@ __global__ void __launch_bounds__(kDThreads)
   const int nw = seg_words(nwords, seg);
   const uint32_t hin = tile_scan_map(seg_high[seg], tile_hin[blockIdx.x], sh);
   const uint64_t s0 = (uint64_t)((hin << 4) | seg_tin[seg]);
-  const uint2* src = reinterpret_cast<const uint2*>(words + seg * kSegWords);
+  SegRegs sr;
+  load_seg(words, seg, nw, sr);
   uint64_t h = s0;
-  for (int i = 0; i < nw; ++i) {
-    const uint2 wv = __ldg(src + i);
+#pragma unroll
+  for (int i = 0; i < kSegWords; ++i) {
+    if (i >= nw) break;
+    const uint2 wv = sr.w[i];
 #pragma unroll
     for (int b = 0; b < 8; ++b) {
       h ^= ((b < 4 ? wv.x : wv.y) >> (8 * (b & 3))) & 0xffu;

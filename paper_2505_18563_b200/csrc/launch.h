@@ -17,6 +17,17 @@ struct P2PView {  // device-visible pointers into every rank's symmetric buffer
   int rank, n;
   uint64_t M, C;                       // packed count, ChunkMap chunk = ceil(M/n)
 };
+// Failure state of the NVLink exchange (device memory). A consumer that
+// waits longer than timeout_ns for a peer's flag sets `flag` and the
+// host-mapped `*host` (the library reads it before the next call: LinkError),
+// and every later consumer skips its peer reads and its own signals, so a
+// dead peer fails the step instead of hanging it or folding stale memory.
+struct P2PErr {
+  int flag;
+  int pad;
+  volatile int* host;
+  unsigned long long timeout_ns;
+};
 // signals fused into the exchange kernels: `entry` published by block 0 at
 // start (the producer ran before on the stream), `exit` by the last CTA to
 // finish; kind < 0 = none. counter: a zeroed u32, self-resetting.
@@ -54,7 +65,7 @@ void launch_unpack(const float* packed, uint64_t len, const uint64_t* words,
 // Publishes sg's exit flag (READ) when every CTA is done.
 void launch_unpack_p2p(const float* packed_local, uint64_t len, const uint64_t* words,
                        const uint32_t* chunk_off, float scale, int do_scale, float* out, const P2PView& v,
-                       int two_shot, const uint64_t* flags, uint64_t target, int* err, const P2PSig& sg,
+                       int two_shot, const uint64_t* flags, uint64_t target, P2PErr* err, const P2PSig& sg,
                        cudaStream_t s);
 void launch_unpack_sgd(const float* packed, uint64_t len, const uint64_t* words,
                        const uint32_t* chunk_off, float scale, int do_scale, float lr,
@@ -80,16 +91,16 @@ void note_launch(uint64_t n = 1);
 // ---- p2p.cu ----------------------------------------------------------------
 // flags[kind][rank] = value on every rank (system-scope release after a fence)
 void launch_p2p_signal(const P2PView& v, int kind, uint64_t value, cudaStream_t s);
-// wait until flags[kind][s] >= target for all s < n (10 s timeout -> *err)
-void launch_p2p_wait(const uint64_t* flags, int kind, int n, uint64_t target, int* err,
+// wait until flags[kind][s] >= target for all s < n (timeout -> *err)
+void launch_p2p_wait(const uint64_t* flags, int kind, int n, uint64_t target, P2PErr* err,
                      cudaStream_t s);
 // fold packed[*][b, e) in the reference order into out[b, e) (waits PACKED);
 // max_ctas > 0 caps the grid (overlap with pack/unpack on other streams)
 void launch_p2p_fold(const P2PView& v, float* out, uint64_t b, uint64_t e, const uint64_t* flags,
-                     uint64_t target, int* err, int max_ctas, const P2PSig& sg, cudaStream_t s);
+                     uint64_t target, P2PErr* err, int max_ctas, const P2PSig& sg, cudaStream_t s);
 // out[j] = reduced[(j - P0) / Cb][j] for j in [b, e) (waits REDUCED)
 void launch_p2p_gather(const P2PView& v, float* out, uint64_t b, uint64_t e, uint64_t P0, uint64_t Cb,
-                       const uint64_t* flags, uint64_t target, int* err, int max_ctas,
+                       const uint64_t* flags, uint64_t target, P2PErr* err, int max_ctas,
                        const P2PSig& sg, cudaStream_t s);
 
 // ---- prune.cu --------------------------------------------------------------
@@ -105,6 +116,7 @@ struct BitmapCounts {  // zeroed by launch_prune_bitmap
   unsigned long long n_cand_below;  // candidates with key < T (#(key < lo) = n_lt - this)
   unsigned long long n_cand;     // window candidates seen (may exceed cand.cap)
   int changed_cand, fix_changed;  // a candidate bit changed (bitmap pass / after a fix-up)
+  int changed_tie, pad;           // a tie bit changed (before any tie fix-up)
 };
 // Window candidates of the bitmap pass (temporal reuse, prune.cu): elements
 // with lo <= key <= hi and key != T are compacted as key[j], idx[j] | (the
@@ -114,6 +126,11 @@ struct PruneCandBuf {
   uint32_t* key = nullptr;
   uint32_t* idx = nullptr;
   uint64_t cap = 0;
+  // histogram of the candidates' top digit (key - lo) >> hshift (<= 256
+  // bins, zeroed by the launcher): the first radix digit of the moved
+  // threshold's select comes for free with the pass
+  uint32_t* hist = nullptr;
+  int hshift = 0;
 };
 // 1 CTA: strided sample of keys, sorted; writes the [lo, hi] window.
 void launch_prune_sample(const float* w, uint64_t len, uint64_t k, PruneWindow* win_dev,
@@ -149,27 +166,53 @@ void launch_prune_pick(const uint32_t* hist, int nbits, int first, uint64_t rank
 void launch_prune_bitmap(const float* w, uint64_t len, uint32_t T, uint64_t r,
                          const uint32_t* tie_prefix, uint64_t* words, uint32_t* chunk_popc,
                          uint32_t* ties_out, const uint32_t* ties_prev, uint64_t* tie_words,
-                         BitmapCounts* counts, cudaStream_t s, const PruneCandBuf& cand = PruneCandBuf{});
+                         BitmapCounts* counts, cudaStream_t s, const PruneCandBuf& cand = PruneCandBuf{},
+                         uint64_t* tie_old = nullptr);
+// The moved threshold T' of the window path, resolved on the device from
+// the select over the candidates (no host round trip before the fix-ups):
+// T' = base + the select's value, c_lt' = c_base + #(candidates < T'),
+// r' = k - c_lt', straddle = ties at T' split by r'.
+struct WinSel {
+  uint32_t T1;
+  int straddle, err, pad;
+  unsigned long long c_lt1, r1, eq1, below;
+};
+void launch_prune_win_final(const SelState* sel, uint32_t base, int bits, uint64_t ncand, uint64_t c_base,
+                            uint64_t k, WinSel* ws, cudaStream_t s);
+// one readback for the window path: {ws, *digest, *nnz, *fix_changed} -> out
+struct WinReport {
+  WinSel w;
+  unsigned long long digest;
+  uint32_t nnz;
+  int fix_changed;
+};
+void launch_prune_win_report(const WinSel* ws, const uint64_t* digest, const uint32_t* nnz,
+                             const int* fix_changed, WinReport* out, cudaStream_t s);
 // Window fix-up once the true threshold T' of a moved mask is known (it lies
 // in the window, T' != the pass's T): every candidate gets key > T' (ties at
 // T' provisionally dropped; with `straddle` their bits go to tie_words and
 // per-chunk counts to ties for the tie fix-up); words by 64-bit atomics,
 // chunk_popc adjusted by the flips. tie_clear first zeroes the tie words of
 // every chunk holding a T'-tie.
-void launch_prune_cand_fix(const uint32_t* key, const uint32_t* idx, uint64_t n, uint32_t T, int straddle,
+void launch_prune_cand_fix(const uint32_t* key, const uint32_t* idx, uint64_t n, const WinSel* ws,
                            uint64_t* words, uint32_t* chunk_popc, uint64_t* tie_words, uint32_t* ties,
                            int* changed, cudaStream_t s);
-void launch_prune_cand_tieclear(const uint32_t* key, const uint32_t* idx, uint64_t n, uint32_t T,
+void launch_prune_cand_tieclear(const uint32_t* key, const uint32_t* idx, uint64_t n, const WinSel* ws,
                                 uint64_t* tie_words, cudaStream_t s);
-// *flag = 1 if a tie candidate's (key == T) final bit differs from its
+// *flag = 1 if a tie candidate's (key == T') final bit differs from its
 // recorded previous bit (the fix-up checks the others into the same flag)
-void launch_prune_cand_changed(const uint32_t* key, const uint32_t* idx, uint64_t n, uint32_t T,
+void launch_prune_cand_changed(const uint32_t* key, const uint32_t* idx, uint64_t n, const WinSel* ws,
                                const uint64_t* words, int* flag, cudaStream_t s);
 // exact tie bits from the exact tie prefix; updates chunk_popc of tie chunks.
 // Ties of global rank < r dropped (prune) or, keep_low, kept (TopK)
+// tie_old (optional, the bitmap pass's previous tie bits): *changed = 1 if a
+// tie bit ends different from it
+// ws (optional): r = ws->r1, and nothing to do unless ws->straddle
 void launch_prune_tiefix(uint64_t* words, uint64_t len, const uint64_t* tie_words,
                          const uint32_t* ties, const uint32_t* tie_prefix, uint64_t r,
-                         uint32_t* chunk_popc, cudaStream_t s, int keep_low = 0);
+                         uint32_t* chunk_popc, cudaStream_t s, int keep_low = 0,
+                         const uint64_t* tie_old = nullptr, int* changed = nullptr,
+                         const WinSel* ws = nullptr);
 // TopK payload: the ascending indices of the set bits (u32), chunk offsets given
 void launch_pack_index(uint64_t len, const uint64_t* words, const uint32_t* chunk_off,
                        uint32_t* idx, cudaStream_t s);

@@ -43,7 +43,7 @@ __global__ void p2p_signal_kernel(P2PView v, int kind, uint64_t value) {
   if (lane < v.n) st_release_sys(v.flags[lane] + kind * kP2PMaxRanks + v.rank, value);
 }
 
-__global__ void p2p_wait_kernel(const uint64_t* flags, int kind, int n, uint64_t target, int* err) {
+__global__ void p2p_wait_kernel(const uint64_t* flags, int kind, int n, uint64_t target, P2PErr* err) {
   block_wait_flags(flags, kind, n, target, err);
 }
 
@@ -124,9 +124,9 @@ __device__ void fold_range(const P2PView& v, float* __restrict__ out, uint64_t b
 // one-shot (whole vector) or the owner's chunk (two-shot reduce-scatter)
 __global__ void __launch_bounds__(256)
     p2p_fold_kernel(P2PView v, float* __restrict__ out, uint64_t b, uint64_t e, const uint64_t* flags,
-                    uint64_t target, int* err, P2PSig sg) {
-  entry_signal(v, sg);
-  block_wait_flags(flags, kP2PPacked, v.n, target, err);
+                    uint64_t target, P2PErr* err, P2PSig sg) {
+  entry_signal(v, sg);  // this rank's packed buffer is complete (the producer ran before)
+  if (!block_wait_flags(flags, kP2PPacked, v.n, target, err)) return;
   fold_range(v, out, b, e);
   exit_signal(v, sg);
 }
@@ -139,9 +139,9 @@ __device__ void gather_range(const P2PView& v, float* __restrict__ out, uint64_t
 
 __global__ void __launch_bounds__(256)
     p2p_gather_kernel(P2PView v, float* __restrict__ out, uint64_t b, uint64_t e, uint64_t P0,
-                      uint64_t Cb, const uint64_t* flags, uint64_t target, int* err, P2PSig sg) {
+                      uint64_t Cb, const uint64_t* flags, uint64_t target, P2PErr* err, P2PSig sg) {
   entry_signal(v, sg);
-  block_wait_flags(flags, kP2PReduced, v.n, target, err);
+  if (!block_wait_flags(flags, kP2PReduced, v.n, target, err)) return;
   gather_range(v, out, b, e, P0, Cb);
   exit_signal(v, sg);
 }
@@ -213,21 +213,21 @@ void launch_p2p_signal(const P2PView& v, int kind, uint64_t value, cudaStream_t 
   note_launch();
 }
 
-void launch_p2p_wait(const uint64_t* flags, int kind, int n, uint64_t target, int* err,
+void launch_p2p_wait(const uint64_t* flags, int kind, int n, uint64_t target, P2PErr* err,
                      cudaStream_t s) {
   p2p_wait_kernel<<<1, 32, 0, s>>>(flags, kind, n, target, err);
   note_launch();
 }
 
 void launch_p2p_fold(const P2PView& v, float* out, uint64_t b, uint64_t e, const uint64_t* flags,
-                     uint64_t target, int* err, int max_ctas, const P2PSig& sg, cudaStream_t s) {
+                     uint64_t target, P2PErr* err, int max_ctas, const P2PSig& sg, cudaStream_t s) {
   p2p_fold_kernel<<<stream_grid(e > b ? e - b : 0, max_ctas), 256, 0, s>>>(v, out, b, e, flags,
                                                                           target, err, sg);
   note_launch();
 }
 
 void launch_p2p_gather(const P2PView& v, float* out, uint64_t b, uint64_t e, uint64_t P0, uint64_t Cb,
-                       const uint64_t* flags, uint64_t target, int* err, int max_ctas,
+                       const uint64_t* flags, uint64_t target, P2PErr* err, int max_ctas,
                        const P2PSig& sg, cudaStream_t s) {
   p2p_gather_kernel<<<stream_grid(e > b ? e - b : 0, max_ctas), 256, 0, s>>>(v, out, b, e, P0, Cb,
                                                                             flags, target, err, sg);

@@ -23,21 +23,33 @@ __device__ __forceinline__ uint64_t globaltimer() {
   return t;
 }
 
-// thread 0 waits until flags[kind][s] >= target for all s < n; block barrier
-__device__ __forceinline__ void block_wait_flags(const uint64_t* flags, int kind, int n, uint64_t target, int* err) {
+// thread 0 waits until flags[kind][s] >= target for all s < n; block
+// barrier. Returns false (in every thread) when the exchange has failed:
+// already flagged, or a peer did not publish within the timeout (then the
+// failure is raised, device and host side). Callers skip their peer reads
+// and their exit signals on false.
+__device__ __forceinline__ bool block_wait_flags(const uint64_t* flags, int kind, int n, uint64_t target,
+                                                 P2PErr* err) {
+  __shared__ int s_ok;
   if (threadIdx.x == 0) {
+    int ok = *reinterpret_cast<volatile int*>(&err->flag) == 0;
     const uint64_t t0 = globaltimer();
-    for (int s = 0; s < n; ++s) {
+    for (int s = 0; ok && s < n; ++s) {
       while (ld_acquire_sys(flags + kind * kP2PMaxRanks + s) < target) {
-        if (globaltimer() - t0 > 10000000000ull) {  // 10 s: a peer died; fail, do not hang
-          atomicExch(err, 1);
+        if (globaltimer() - t0 > err->timeout_ns) {  // a peer died or stalled: fail, do not hang
+          atomicExch(&err->flag, 1);
+          if (err->host) *err->host = 1;
+          __threadfence_system();
+          ok = 0;
           break;
         }
         __nanosleep(64);
       }
     }
+    s_ok = ok;
   }
   __syncthreads();
+  return s_ok != 0;
 }
 
 // Fused signalling (saves a launch per signal): the ENTRY flag is published

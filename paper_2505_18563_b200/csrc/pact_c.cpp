@@ -175,6 +175,7 @@ struct pact_mask {
   int win_valid = 0;
   uint32_t win_lo = 1, win_hi = 0;
   DevBuf cand_key, cand_idx;
+  DevBuf tie_old;  // nwords u64: previous bits of the tie positions (exact change test)
 };
 
 namespace {
@@ -184,7 +185,8 @@ struct P2PState {  // CUDA-IPC symmetric buffers of all ranks (p2p.cu)
   void* sym = nullptr;         // own buffer: [flags 4 KiB][packed x2][reduced x2]
   char* base[pactk::kP2PMaxRanks] = {};
   uint64_t k = 0;              // P2P steps completed (flag values)
-  DevBuf err;                  // device timeout flag
+  DevBuf err;                  // pactk::P2PErr (device): a consumer timed out
+  int* err_host = nullptr;     // its host-mapped twin, read before every call
 };
 }  // namespace
 
@@ -209,6 +211,10 @@ struct pact_comm {
   size_t sym_bytes = 0;
   ncclWindow_t win = nullptr;
   bool sym_failed = false;
+  // fail-fast (reference SimCluster::poison, collective.cpp:430-458): once a
+  // peer is lost every later call returns PACT_E_LINK at once
+  bool failed = false;
+  std::string fail_msg;
 };
 
 namespace {
@@ -237,6 +243,9 @@ struct Small {
   uint32_t hist[2048];
   pactk::BitmapCounts bcounts;
   pactk::SelState sel;
+  pactk::WinSel win_sel;
+  uint32_t cand_hist[2048];
+  pactk::WinReport report;
 };
 
 pact_status set_device(pact_ctx* ctx) {
@@ -321,6 +330,17 @@ pact_status mirror_tile_off(pact_mask* m, cudaStream_t s) {
   CUDA_TRY(cudaStreamSynchronize(s));
   m->host_tile_off_valid = 1;
   return PACT_OK;
+}
+
+// how long a rank waits for a peer (vote board, NVLink flags) before the
+// link is declared dead: PACT_LINK_TIMEOUT_MS, default 30 s
+uint64_t link_timeout_ms() {
+  static const uint64_t ms = [] {
+    const char* e = getenv("PACT_LINK_TIMEOUT_MS");
+    const long long v = e ? atoll(e) : 0;
+    return v > 0 ? (uint64_t)v : (uint64_t)30000;
+  }();
+  return ms;
 }
 
 uint64_t drop_count_raw(float ratio, uint64_t len) {  // sparsity.cpp:38-39
@@ -426,8 +446,19 @@ pact_status p2p_setup(pact_comm* c, uint64_t need, cudaStream_t s) {
     p2p_release(c);
     return PACT_OK;  // stay on NCCL
   }
-  TRY(p.err.ensure(sizeof(int)));
-  CUDA_TRY(cudaMemset(p.err.p, 0, sizeof(int)));
+  TRY(p.err.ensure(sizeof(pactk::P2PErr)));
+  if (!p.err_host) {
+    CUDA_TRY(cudaHostAlloc(&p.err_host, sizeof(int), cudaHostAllocMapped));
+  }
+  *p.err_host = 0;
+  {
+    pactk::P2PErr e{};
+    int* dev_host = nullptr;
+    CUDA_TRY(cudaHostGetDevicePointer(&dev_host, p.err_host, 0));
+    e.host = dev_host;
+    e.timeout_ns = link_timeout_ms() * 1000000ull;
+    CUDA_TRY(cudaMemcpy(p.err.p, &e, sizeof e, cudaMemcpyHostToDevice));
+  }
   p.cap = cap;
   p.creg = creg;
   p.k = 0;
@@ -450,6 +481,43 @@ pactk::P2PView p2p_view(const pact_comm* c, int par, uint64_t M) {
   return v;
 }
 
+}  // namespace
+
+namespace {
+// A lost peer poisons the communicator (reference SimCluster::poison,
+// collective.cpp:430-443, and the trainer's rethrow, trainer.cpp:416-437):
+// NCCL work in flight is aborted (ncclCommAbort unblocks its kernels), and
+// this and every later call on the comm returns PACT_E_LINK at once.
+pact_status poison(pact_comm* c, const char* why) {
+  if (!c->failed) {
+    c->failed = true;
+    c->fail_msg = why;
+    if (c->nccl) {
+      ncclCommAbort(c->nccl);
+      c->nccl = nullptr;
+      c->win = nullptr;
+    }
+  }
+  return fail(PACT_E_LINK, "%s", c->fail_msg.c_str());
+}
+
+// before every collective: a failure seen earlier (an NVLink consumer that
+// timed out, an NCCL asynchronous error) surfaces here as PACT_E_LINK
+pact_status link_check(pact_comm* c) {
+  if (!c) return PACT_OK;
+  if (c->failed) return fail(PACT_E_LINK, "%s", c->fail_msg.c_str());
+  if (c->p2p.err_host && *reinterpret_cast<volatile int*>(c->p2p.err_host))
+    return poison(c, "a peer did not publish its NVLink exchange flags within PACT_LINK_TIMEOUT_MS (peer lost)");
+  if (c->nccl) {
+    ncclResult_t r = ncclSuccess;
+    if (ncclCommGetAsyncError(c->nccl, &r) == ncclSuccess && r != ncclSuccess && r != ncclInProgress) {
+      char msg[160];
+      snprintf(msg, sizeof msg, "NCCL asynchronous error: %s", ncclGetErrorString(r));
+      return poison(c, msg);
+    }
+  }
+  return PACT_OK;
+}
 }  // namespace
 
 // =================================================================== ABI
@@ -669,6 +737,7 @@ pact_status pact_mask_destroy(pact_mask* m) {
   m->tie_prefix.release();
   m->cand_key.release();
   m->cand_idx.release();
+  m->tie_old.release();
   delete m;
   return PACT_OK;
 }
@@ -787,13 +856,17 @@ namespace {
 
 // radix select of the `rank`-th smallest (1-based) key' = key - base over
 // elements with key' < 2^bits; returns key' and #(key' smaller).
-pact_status select_rank(pact_ctx* ctx, const void* src, int from_float, uint64_t n, uint32_t base,
-                        int bits, uint64_t rank, cudaStream_t s, uint32_t* value,
-                        uint64_t* below) {
-  // the digit walk stays on the device (hist -> pick per 11-bit digit); one
-  // readback of the final state instead of one per digit
+// the select's kernels only (device-resident state in Small::sel); with
+// first_hist, the top digit's histogram (bits [lo_bits, bits)) is given
+void select_enqueue(pact_ctx* ctx, const void* src, int from_float, uint64_t n, uint32_t base, int bits,
+                    uint64_t rank, cudaStream_t s, const uint32_t* first_hist = nullptr, int lo_bits = 0) {
   Small* sm = ctx->ws_small.as<Small>();
   int hi = bits, first = 1;
+  if (first_hist && bits > 0) {
+    pactk::launch_prune_pick(first_hist, bits - lo_bits, 1, rank, &sm->sel, s);
+    first = 0;
+    hi = lo_bits;
+  }
   while (hi > 0) {
     const int nb = std::min(11, hi);
     const int shift = hi - nb;
@@ -802,7 +875,16 @@ pact_status select_rank(pact_ctx* ctx, const void* src, int from_float, uint64_t
     first = 0;
     hi = shift;
   }
-  if (first) {  // bits == 0: nothing to select
+}
+
+pact_status select_rank(pact_ctx* ctx, const void* src, int from_float, uint64_t n, uint32_t base,
+                        int bits, uint64_t rank, cudaStream_t s, uint32_t* value,
+                        uint64_t* below) {
+  // the digit walk stays on the device (hist -> pick per 11-bit digit); one
+  // readback of the final state instead of one per digit
+  Small* sm = ctx->ws_small.as<Small>();
+  select_enqueue(ctx, src, from_float, n, base, bits, rank, s);
+  if (bits <= 0) {  // bits == 0: nothing to select
     *value = 0;
     *below = 0;
     return PACT_OK;
@@ -913,11 +995,12 @@ pact_status pact_prune_magnitude(pact_ctx* ctx, const float* w, uint64_t len, fl
   }
   const uint64_t nc = out->ntiles;
   TRY(out->tie_words.ensure(out->nwords * 8));
+  TRY(out->tie_old.ensure(out->nwords * 8));
   TRY(out->ties[0].ensure(nc * 4));
   TRY(out->ties[1].ensure(nc * 4));
   TRY(out->tie_prefix.ensure((nc + 1) * 4));
   // window half-width (ranks) and candidate capacity
-  const uint64_t mwin = std::max<uint64_t>(4096, len >> 10);
+  const uint64_t mwin = std::max<uint64_t>(4096, len >> 11);
   const uint64_t ccap = 4 * mwin + 65536;
   TRY(out->cand_key.ensure(ccap * 4));
   TRY(out->cand_idx.ensure(ccap * 4));
@@ -942,11 +1025,13 @@ pact_status pact_prune_magnitude(pact_ctx* ctx, const float* w, uint64_t len, fl
       cb.key = ckey;
       cb.idx = cidx;
       cb.cap = ccap;
+      cb.hist = sm->cand_hist;
+      cb.hshift = std::max(0, bit_length(out->win_hi - out->win_lo) - 8);
     }
     pactk::launch_prune_bitmap(w, len, T, r, use_prefix ? out->tie_prefix.as<uint32_t>() : nullptr,
                                out->words, out->tile_popc, out->ties[nxt].as<uint32_t>(),
                                compare_prev ? out->ties[out->ties_cur].as<uint32_t>() : nullptr,
-                               out->tie_words.as<uint64_t>(), bc, s, cb);
+                               out->tie_words.as<uint64_t>(), bc, s, cb, out->tie_old.as<uint64_t>());
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cudaMemcpyAsync(ctx->pin.p, bc, sizeof hb, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));
@@ -954,15 +1039,18 @@ pact_status pact_prune_magnitude(pact_ctx* ctx, const float* w, uint64_t len, fl
     out->ties_cur = nxt;
     return PACT_OK;
   };
-  // exact tie bits once the true (T, r) and per-chunk tie counts are known
+  // exact tie bits once the true (T, r) and per-chunk tie counts are known;
+  // whether a tie bit ended different from the previous mask lands in
+  // fix_changed (read back with the offsets: changed bit 2)
   auto fix_ties = [&](uint64_t r) -> pact_status {
     const uint32_t* ties = out->ties[out->ties_cur].as<uint32_t>();
     TRY(scan(ctx, ties, nc, out->tie_prefix.as<uint32_t>(), s));
     pactk::launch_prune_tiefix(out->words, len, out->tie_words.as<uint64_t>(), ties,
-                               out->tie_prefix.as<uint32_t>(), r, out->tile_popc, s);
+                               out->tie_prefix.as<uint32_t>(), r, out->tile_popc, s, 0,
+                               out->tie_old.as<uint64_t>(), &bc->fix_changed);
     CUDA_TRY(cudaGetLastError());
     out->spec_prefix_valid = 1;
-    changed = 1;  // conservative: the digest is recomputed on demand
+    changed |= 2;
     return PACT_OK;
   };
   // the window for the next call: keys at candidate ranks q0, q1 (1-based,
@@ -996,7 +1084,10 @@ pact_status pact_prune_magnitude(pact_ctx* ctx, const float* w, uint64_t len, fl
     if (hb.n_lt < k && k <= hb.n_lt + hb.n_eq) {  // threshold still the k-th key
       changed |= hb.changed | hb.changed_cand;
       const uint64_t r = k - hb.n_lt;
-      if (pv ? (r != r0 || hb.tie_mismatch) : r < hb.n_eq) TRY(fix_ties(r));
+      if (pv ? (r != r0 || hb.tie_mismatch) : r < hb.n_eq)
+        TRY(fix_ties(r));
+      else
+        changed |= hb.changed_tie;
       st.path = 3;
       st.threshold = T0;
       st.c_lt = hb.n_lt;
@@ -1011,60 +1102,67 @@ pact_status pact_prune_magnitude(pact_ctx* ctx, const float* w, uint64_t len, fl
       if (n_below < k && k <= n_below + ncand + E0) {
         const bool up = k > hb.n_lt + hb.n_eq;  // T' > T0 (else T' < T0)
         const uint64_t rho = k - n_below - (up ? E0 : 0);  // rank among the candidates
-        uint32_t rel = 0;
-        uint64_t below = 0;
         const uint32_t base = out->win_lo;
         const int bits = bit_length(out->win_hi - base);
-        TRY(select_rank(ctx, ckey, 0, ncand, base, bits, rho, s, &rel, &below));
-        pactk::SelState sel{};
-        std::memcpy(&sel, ctx->pin.p, sizeof sel);  // select_rank left its state in pin
-        const uint32_t T1 = base + rel;
-        const uint64_t eq1 = bits > 0 ? sel.eq : ncand;
-        const uint64_t c_lt1 = n_below + below + (up ? E0 : 0);
-        const uint64_t r1 = k - c_lt1;
-        changed = hb.changed;  // outside the window the bits are final; candidates: fix_changed
-        if (T1 == T0 || r1 == 0 || r1 > eq1)
-          return fail(PACT_E_RUN_FAILURE, "prune window select inconsistent (T0=%u T1=%u r1=%llu eq=%llu)", T0, T1,
-                      (unsigned long long)r1, (unsigned long long)eq1);
+        changed = hb.changed | 2;  // outside the window the bits are final; candidates, ties: fix_changed
+        // everything below stays on the device until one readback: the select
+        // over the candidates, T' / r' / straddle (WinSel), the fix-ups, the
+        // offsets and (the mask normally moved) its digest
+        select_enqueue(ctx, ckey, 0, ncand, base, bits, rho, s, sm->cand_hist, std::max(0, bits - 8));
+        pactk::WinSel* ws = &sm->win_sel;
+        pactk::launch_prune_win_final(&sm->sel, base, bits, ncand, n_below + (up ? E0 : 0), k, ws, s);
         // ties at T0 are all dropped (T' > T0) or all kept (T' < T0)
         if (E0) {
           const uint32_t* ties0 = out->ties[out->ties_cur].as<uint32_t>();
           pactk::launch_prune_tiefix(out->words, len, out->tie_words.as<uint64_t>(), ties0,
-                                     out->tie_prefix.as<uint32_t>(), up ? ~0ull : 0ull, out->tile_popc, s);
-          changed = 1;  // the pass compared these bits against T0's tie ranks, not the old mask
+                                     out->tie_prefix.as<uint32_t>(), up ? ~0ull : 0ull, out->tile_popc, s, 0,
+                                     out->tie_old.as<uint64_t>(), &bc->fix_changed);
         }
-        const bool straddle = r1 < eq1;
         const int tn = out->ties_cur ^ 1;
         uint32_t* ties1 = out->ties[tn].as<uint32_t>();
-        if (straddle) {
-          pactk::launch_prune_cand_tieclear(ckey, cidx, ncand, T1, out->tie_words.as<uint64_t>(), s);
-          CUDA_TRY(cudaMemsetAsync(ties1, 0, nc * 4, s));
-        }
-        pactk::launch_prune_cand_fix(ckey, cidx, ncand, T1, straddle, out->words, out->tile_popc,
+        CUDA_TRY(cudaMemsetAsync(ties1, 0, nc * 4, s));
+        pactk::launch_prune_cand_tieclear(ckey, cidx, ncand, ws, out->tie_words.as<uint64_t>(), s);
+        pactk::launch_prune_cand_fix(ckey, cidx, ncand, ws, out->words, out->tile_popc,
                                      out->tie_words.as<uint64_t>(), ties1, &bc->fix_changed, s);
-        if (straddle) {
-          TRY(scan(ctx, ties1, nc, out->tie_prefix.as<uint32_t>(), s));
-          pactk::launch_prune_tiefix(out->words, len, out->tie_words.as<uint64_t>(), ties1,
-                                     out->tie_prefix.as<uint32_t>(), r1, out->tile_popc, s);
-          out->ties_cur = tn;
-        }
-        out->spec_prefix_valid = straddle;
-        if (straddle) pactk::launch_prune_cand_changed(ckey, cidx, ncand, T1, out->words, &bc->fix_changed, s);
+        TRY(scan(ctx, ties1, nc, out->tie_prefix.as<uint32_t>(), s));
+        pactk::launch_prune_tiefix(out->words, len, out->tie_words.as<uint64_t>(), ties1,
+                                   out->tie_prefix.as<uint32_t>(), 0, out->tile_popc, s, 0, nullptr, nullptr, ws);
+        out->ties_cur = tn;  // T' tie counts (all zero unless they straddle r')
+        pactk::launch_prune_cand_changed(ckey, cidx, ncand, ws, out->words, &bc->fix_changed, s);
+        TRY(scan(ctx, out->tile_popc, nc, out->tile_off, s));
+        TRY(ctx->digest_scratch.ensure(pactk::digest_scratch_bytes(out->nwords)));
+        pactk::launch_digest(out->words, out->nwords, ctx->digest_scratch.p, &sm->digest, s);
         CUDA_TRY(cudaGetLastError());
+        pactk::launch_prune_win_report(ws, &sm->digest, out->tile_off + nc, &bc->fix_changed, &sm->report, s);
+        pactk::WinReport h{};
+        CUDA_TRY(cudaMemcpyAsync(ctx->pin.p, &sm->report, sizeof h, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+        std::memcpy(&h, ctx->pin.p, sizeof h);
+        if (h.w.err || h.w.T1 == T0)
+          return fail(PACT_E_RUN_FAILURE, "prune window select inconsistent (T0=%u T1=%u r1=%llu eq=%llu)", T0,
+                      h.w.T1, (unsigned long long)h.w.r1, (unsigned long long)h.w.eq1);
+        out->spec_prefix_valid = h.w.straddle;
+        out->nnz = h.nnz;
+        out->host_tile_off_valid = 0;
+        out->digest = h.digest;  // exact for the final words whether or not they moved
+        out->changed = (changed & 1) || h.fix_changed;
+        out->digest_valid = 1;
+        out->spec_T = h.w.T1;
+        out->spec_c_lt = h.w.c_lt1;
+        st.path = 4;
+        st.threshold = h.w.T1;
+        st.c_lt = h.w.c_lt1;
+        st.candidates = ncand;
         // re-centre the window when T' sits near one of its ends
-        const uint64_t pos = below + 1;  // T's rank among the candidates
+        const uint64_t pos = h.w.below + 1;  // T's rank among the candidates
         if (pos < mwin / 2 || ncand - std::min(ncand, pos) < mwin / 2)
           TRY(set_window(ckey, ncand, base, out->win_hi, (int64_t)pos - (int64_t)mwin, (int64_t)pos + (int64_t)mwin,
-                         T1));
-        // the fix-up's own change flag (read back with the offsets below)
-        st.path = 4;
-        st.threshold = T1;
-        st.c_lt = c_lt1;
-        st.candidates = ncand;
-        out->spec_T = T1;
-        out->spec_c_lt = c_lt1;
-        done = true;
-        changed |= 2;  // resolved from fix_changed below
+                         h.w.T1));
+        if (out->nnz != len - k)
+          return fail(PACT_E_RUN_FAILURE, "prune kept %llu, expected %llu", (unsigned long long)out->nnz,
+                      (unsigned long long)(len - k));
+        if (stats) *stats = st;
+        return PACT_OK;
       }
     }
     if (!done) changed = 1;
@@ -1098,7 +1196,7 @@ pact_status pact_prune_magnitude(pact_ctx* ctx, const float* w, uint64_t len, fl
     // (4) bitmap, ties provisionally all dropped; exact when r == E
     const uint64_t r = k - c_lt;
     TRY(bitmap(T, r, false, false, false));
-    changed |= hb.changed;
+    changed |= hb.changed | hb.changed_cand | hb.changed_tie;
     if (hb.n_lt != c_lt || !(c_lt < k && k <= hb.n_lt + hb.n_eq))
       return fail(PACT_E_RUN_FAILURE, "prune threshold inconsistent (T=%u c_lt=%llu n_lt=%llu n_eq=%llu k=%llu)",
                   T, (unsigned long long)c_lt, (unsigned long long)hb.n_lt,
@@ -1349,8 +1447,11 @@ pact_status shm_vote(pact_comm* c, const uint8_t frame[PACT_HEADER_BYTES], std::
     unsigned spins = 0;
     while (slots[r].seq.load(std::memory_order_acquire) < seq) {
       if ((++spins & 4095) == 0 &&
-          std::chrono::steady_clock::now() - t0 > std::chrono::seconds(30))
-        return fail(PACT_E_LINK, "vote timed out waiting for rank %d (peer died?)", r);
+          std::chrono::steady_clock::now() - t0 > std::chrono::milliseconds(link_timeout_ms())) {
+        char msg[128];
+        snprintf(msg, sizeof msg, "vote timed out waiting for rank %d (peer lost)", r);
+        return poison(c, msg);
+      }
 #if defined(__x86_64__)
       __builtin_ia32_pause();
 #endif
@@ -1400,7 +1501,9 @@ pact_status pact_comm_destroy(pact_comm* c) {
   cudaDeviceSynchronize();
   p2p_release(c);
   c->p2p.err.release();
-  if (c->win) ncclCommWindowDeregister(c->nccl, c->win);
+  if (c->p2p.err_host) cudaFreeHost(c->p2p.err_host);
+  c->p2p.err_host = nullptr;
+  if (c->win && c->nccl) ncclCommWindowDeregister(c->nccl, c->win);
   if (c->sym) ncclMemFree(c->sym);
   if (c->nccl) ncclCommDestroy(c->nccl);
   c->vote_dev.release();
@@ -1414,12 +1517,31 @@ pact_status pact_comm_destroy(pact_comm* c) {
   return PACT_OK;
 }
 
+pact_status pact_comm_check(pact_comm* c, pact_stream_t stream, int timeout_ms) {
+  if (!c) return fail(PACT_E_INVALID_ARG, "null comm");
+  TRY(set_device(c->ctx));
+  const auto t0 = std::chrono::steady_clock::now();
+  const uint64_t lim = timeout_ms > 0 ? (uint64_t)timeout_ms : link_timeout_ms();
+  while (true) {
+    TRY(link_check(c));
+    const cudaError_t q = cudaStreamQuery((cudaStream_t)stream);
+    if (q == cudaSuccess) return link_check(c);  // a consumer may have failed just before the end
+    if (q != cudaErrorNotReady) return fail(PACT_E_CUDA, "stream: %s", cudaGetErrorString(q));
+    if (std::chrono::steady_clock::now() - t0 > std::chrono::milliseconds(lim))
+      return poison(c, "a collective did not complete within the timeout (peer lost)");
+    usleep(50);
+  }
+}
+
+int pact_comm_failed(const pact_comm* c) { return c && c->failed ? 1 : 0; }
+
 int pact_comm_rank(const pact_comm* c) { return c ? c->rank : 0; }
 int pact_comm_size(const pact_comm* c) { return c ? c->n : 1; }
 
 pact_status pact_allreduce_sum(pact_comm* c, const float* in, float* out, uint64_t count,
                                pact_stream_t stream) {
   if (!c) return fail(PACT_E_INVALID_ARG, "null comm");
+  TRY(link_check(c));
   TRY(set_device(c->ctx));
   if (count) NCCL_TRY(ncclAllReduce(in, out, count, ncclFloat32, ncclSum, c->nccl, stream));
   return PACT_OK;
@@ -1451,9 +1573,62 @@ pact_status wait_vote(pact_comm* c, std::vector<uint8_t>& frames) {
 
 }  // namespace
 
+pact_status pact_ring_allreduce(pact_comm* c, const float* in, float* out, uint64_t count,
+                                pact_stream_t stream) {
+  if (!c || (count && (!in || !out))) return fail(PACT_E_INVALID_ARG, "null args");
+  TRY(link_check(c));
+  TRY(set_device(c->ctx));
+  cudaStream_t s = stream;
+  const int n = c->n;
+  {  // the reference ring checks the sizes it receives: agree on count first
+    std::vector<uint8_t> all((size_t)n * 8);
+    TRY(pact_allgather_frames(c, reinterpret_cast<const uint8_t*>(&count), 8, all.data(), s));
+    for (int r = 0; r < n; ++r)
+      if (std::memcmp(all.data() + 8 * r, &count, 8) != 0)
+        return fail(PACT_E_SHAPE_MISMATCH, "ring_allreduce: rank %d has a different length", r);
+  }
+  if (!count) return PACT_OK;
+  TRY(p2p_setup(c, count, s));  // collective
+  if (!c->p2p.ok || c->p2p.cap < count)
+    return fail(PACT_E_BAD_TOPOLOGY, "ring_allreduce needs NVLink peer mappings between the ranks");
+  P2PState& p = c->p2p;
+  const uint64_t k1 = p.k + 1;
+  const int par = (int)(k1 & 1);
+  const pactk::P2PView v = p2p_view(c, par, count);
+  uint64_t* myflags = p2p_flags(p, c->rank);
+  pactk::P2PErr* err = p.err.as<pactk::P2PErr>();
+  if (k1 > 2) pactk::launch_p2p_wait(myflags, pactk::kP2PRead, n, k1 - 2, err, s);
+  CUDA_TRY(cudaMemcpyAsync(p2p_packed(p, c->rank, par), in, count * 4, cudaMemcpyDeviceToDevice, s));
+  const uint64_t fv = (k1 << 8) | 1;
+  pactk::P2PSig sg;  // PACKED published by the fold's block 0: the copy before it is complete
+  sg.entry_kind = pactk::kP2PPacked;
+  sg.entry_val = fv;
+  sg.counter = p2p_counter(p, c->rank);
+  if (n == 2) {  // one-shot: both ranks fold every element
+    sg.exit_kind = pactk::kP2PRead;
+    sg.exit_val = k1;
+    pactk::launch_p2p_fold(v, out, 0, count, myflags, fv, err, 0, sg, s);
+  } else {  // reduce-scatter by pulls into the owner's chunk, then all-gather by pulls
+    const uint64_t Cb = (count + n - 1) / n;
+    const uint64_t rb = std::min<uint64_t>(count, (uint64_t)c->rank * Cb), re = std::min<uint64_t>(count, rb + Cb);
+    sg.exit_kind = pactk::kP2PReduced;
+    sg.exit_val = fv;
+    pactk::launch_p2p_fold(v, p2p_reduced(p, c->rank, par), rb, re, myflags, fv, err, 0, sg, s);
+    pactk::P2PSig sg2;
+    sg2.exit_kind = pactk::kP2PRead;
+    sg2.exit_val = k1;
+    sg2.counter = sg.counter;
+    pactk::launch_p2p_gather(v, out, 0, count, 0, Cb, myflags, fv, err, 0, sg2, s);
+  }
+  CUDA_TRY(cudaGetLastError());
+  p.k = k1;
+  return PACT_OK;
+}
+
 pact_status pact_allgather_frames(pact_comm* c, const uint8_t* frame, size_t frame_bytes,
                                   uint8_t* frames_out, pact_stream_t stream) {
   if (!c || !frame || !frames_out) return fail(PACT_E_INVALID_ARG, "null args");
+  TRY(link_check(c));
   TRY(set_device(c->ctx));
   DevBuf tmp;
   TRY(tmp.ensure(frame_bytes * (c->n + 1)));
@@ -1480,6 +1655,7 @@ pact_status pact_allgather_frames(pact_comm* c, const uint8_t* frame, size_t fra
 pact_status pact_full_allreduce(pact_comm* c, const float* grad, float* out, uint64_t len,
                                 float scale, pact_sync_stats* stats, pact_stream_t stream) {
   if (!c) return fail(PACT_E_INVALID_ARG, "null comm");
+  TRY(link_check(c));
   TRY(set_device(c->ctx));
   pact_ctx* ctx = c->ctx;
   CUDA_TRY(cudaEventRecord(ctx->t0, stream));
@@ -1635,6 +1811,7 @@ pact_status pact_topk_allgather_aggregate(pact_comm* c, pact_ctx* ctx, const flo
   if (c && c->ctx != ctx) return fail(PACT_E_INVALID_ARG, "comm belongs to another ctx");
   uint64_t k = 0;
   TRY(pact_topk_count(len, rate, &k));
+  TRY(link_check(c));
   TRY(set_device(ctx));
   TRY(ensure_ctx_ws(ctx));
   cudaStream_t s = stream;
@@ -1772,7 +1949,7 @@ pact_status f16_ring(pact_comm* c, pact_ctx* ctx, const float* x, uint64_t count
       const int par = (int)(k1 & 1), peer = r ^ 1;
       const pactk::P2PView v = p2p_view(c, par, count);
       uint64_t* myflags = p2p_flags(p, r);
-      int* err = p.err.as<int>();
+      pactk::P2PErr* err = p.err.as<pactk::P2PErr>();
       const uint64_t fv = (k1 << 8) | 1;
       if (k1 > 2) pactk::launch_p2p_wait(myflags, pactk::kP2PRead, n, k1 - 2, err, s);
       auto* send_mine = reinterpret_cast<uint16_t*>(p2p_packed(p, r, par));
@@ -1829,6 +2006,7 @@ pact_status pact_fp16_allreduce(pact_comm* c, pact_ctx* ctx, const float* grad, 
                                 uint64_t len, pact_sync_stats* stats, pact_stream_t stream) {
   if (!ctx) return fail(PACT_E_INVALID_ARG, "null ctx");
   if (c && c->ctx != ctx) return fail(PACT_E_INVALID_ARG, "comm belongs to another ctx");
+  TRY(link_check(c));
   TRY(set_device(ctx));
   cudaStream_t s = stream;
   CUDA_TRY(cudaEventRecord(ctx->t0, s));
@@ -1858,6 +2036,7 @@ pact_status pact_masked_allreduce(pact_comm* c, pact_ctx* ctx, const float* grad
   if (len != m->len)  // collective.cpp:272
     return fail(PACT_E_SHAPE_MISMATCH, "gradient/mask length mismatch (%llu vs %llu)",
                 (unsigned long long)len, (unsigned long long)m->len);
+  TRY(link_check(c));
   TRY(set_device(ctx));
   TRY(ensure_ctx_ws(ctx));
   pact_policy pol{};
@@ -1927,7 +2106,7 @@ pact_status pact_masked_allreduce(pact_comm* c, pact_ctx* ctx, const float* grad
         const uint64_t k1 = c->p2p.k + 1;
         if (k1 > 2)  // peers finished reading this region (step k1-2)
           pactk::launch_p2p_wait(p2p_flags(c->p2p, c->rank), pactk::kP2PRead, n, k1 - 2,
-                                 c->p2p.err.as<int>(), s);
+                                 c->p2p.err.as<pactk::P2PErr>(), s);
         pactk::launch_pack(grad, len, m->words, m->tile_off, p2p_packed(c->p2p, c->rank, k1 & 1),
                            0, m->ntiles, s);
         packed_in_sym = true;
@@ -1970,7 +2149,7 @@ pact_status pact_masked_allreduce(pact_comm* c, pact_ctx* ctx, const float* grad
     const int par = (int)(k1 & 1);
     const pactk::P2PView v = p2p_view(c, par, m->nnz);
     uint64_t* myflags = p2p_flags(p, c->rank);
-    int* err = p.err.as<int>();
+    pactk::P2PErr* err = p.err.as<pactk::P2PErr>();
     float* mine = p2p_packed(p, c->rank, par);
     // buckets: chunk ranges of ~bucket_bytes packed (auto 4 MiB); pack(b+1)
     // on s, exchange(b) on aux[0], unpack(b-1) on aux[1], chained by events
@@ -2274,6 +2453,7 @@ pact_status pact_calibrate_density(pact_comm* c, pact_ctx* ctx, uint64_t len, co
   for (int i = 0; i < ndens; ++i)
     if (!(densities[i] > 0.0 && densities[i] < 1.0) || (i && densities[i] <= densities[i - 1]))
       return fail(PACT_E_INVALID_ARG, "densities must increase strictly inside (0, 1)");
+  TRY(link_check(c));
   TRY(set_device(ctx));
   cudaStream_t s = stream;
   DevBuf w, g, out, tv;
@@ -2454,6 +2634,7 @@ pact_status pact_ternary_allgather_aggregate(pact_comm* c, pact_ctx* ctx, const 
   if (len != m->len)  // collective.cpp:314
     return fail(PACT_E_SHAPE_MISMATCH, "gradient/mask length mismatch (%llu vs %llu)",
                 (unsigned long long)len, (unsigned long long)m->len);
+  TRY(link_check(c));
   TRY(set_device(ctx));
   TRY(ensure_ctx_ws(ctx));
   cudaStream_t s = stream;
@@ -2557,6 +2738,7 @@ pact_status pact_masked_allreduce_host(pact_comm* c, pact_ctx* ctx, const float*
     return fail(PACT_E_SHAPE_MISMATCH, "gradient/mask length mismatch (%llu vs %llu)",
                 (unsigned long long)len, (unsigned long long)m->len);
   if (len && (!grad_host || !out_host)) return fail(PACT_E_INVALID_ARG, "null host buffers");
+  TRY(link_check(c));
   TRY(set_device(ctx));
   TRY(ensure_ctx_ws(ctx));
   pact_policy pol{};

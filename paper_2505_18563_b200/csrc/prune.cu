@@ -326,8 +326,10 @@ __global__ void __launch_bounds__(1024)
 constexpr int kKeyStages = 2;
 constexpr int kStageFloats = kChunk + 2 * kChunkWords;  // keys, then the 16 old mask words
 constexpr int kCandBuf = 64;                            // per-warp window-candidate staging
+constexpr int kCandHistBits = 8;                        // first select digit, counted by the pass
 constexpr size_t kBitmapSmem =
-    (size_t)kPruneWarps * (kKeyStages * kStageFloats * sizeof(float) + 2 * kCandBuf * sizeof(uint32_t));
+    (size_t)kPruneWarps * (kKeyStages * kStageFloats * sizeof(float) + 2 * kCandBuf * sizeof(uint32_t)) +
+    (sizeof(uint32_t) << kCandHistBits);
 
 __device__ __forceinline__ void chunk_issue(float* st, const float* __restrict__ w,
                                             const uint64_t* __restrict__ words, uint64_t c) {
@@ -346,14 +348,6 @@ __device__ __forceinline__ void chunk_issue(float* st, const float* __restrict__
                  "l"(words + c * kChunkWords + 2 * lane)
                  : "memory");
   }
-}
-
-// (g << 1) | (k > T), (e << 1) | (k >= T) for keys k, T < 2^31: the sign bit
-// of T - k (resp. T - 1 - k, also right for T = 0) funnel-shifted in, two
-// instructions per mask per element.
-__device__ __forceinline__ void classify_push(uint32_t k, uint32_t T, uint32_t& g, uint32_t& e) {
-  g = __funnelshift_l(T - k, g, 1);
-  e = __funnelshift_l(T - 1u - k, e, 1);
 }
 
 // staged window candidates of one warp -> the global list (one atomic per flush)
@@ -376,24 +370,38 @@ __global__ void __launch_bounds__(kPruneWarps * 32)
                         const uint32_t* __restrict__ tie_prefix, uint64_t* __restrict__ words,
                         uint64_t nwords, uint32_t* __restrict__ chunk_popc,
                         uint32_t* __restrict__ ties_out, const uint32_t* __restrict__ ties_prev,
-                        uint64_t* __restrict__ tie_words, BitmapCounts* __restrict__ counts,
-                        uint64_t nchunks, PruneCandBuf cb) {
+                        uint64_t* __restrict__ tie_words, uint64_t* __restrict__ tie_old,
+                        BitmapCounts* __restrict__ counts, uint64_t nchunks, PruneCandBuf cb) {
   extern __shared__ __align__(16) float ring_all[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   float* ring = ring_all + (size_t)warp * kKeyStages * kStageFloats;
   uint32_t* cbk = reinterpret_cast<uint32_t*>(ring_all + (size_t)kPruneWarps * kKeyStages * kStageFloats) +
                   warp * 2 * kCandBuf;
   uint32_t* cbi = cbk + kCandBuf;
+  // CTA histogram of the candidates' top digit (warp-aggregated smem
+  // atomics; a window whose lower end is crowded sends most to one bin),
+  // added to the global one once at the end
+  uint32_t* chist = reinterpret_cast<uint32_t*>(ring_all + (size_t)kPruneWarps * kKeyStages * kStageFloats) +
+                    kPruneWarps * 2 * kCandBuf;
+  if (cb.hist) {
+    for (int b = threadIdx.x; b < (1 << kCandHistBits); b += blockDim.x) chist[b] = 0;
+    __syncthreads();
+  }
   uint32_t* words32 = reinterpret_cast<uint32_t*>(words);
   uint32_t* tie32 = reinterpret_cast<uint32_t*>(tie_words);
+  uint32_t* tie_old32 = reinterpret_cast<uint32_t*>(tie_old);
   const uint64_t nhalves = 2 * nwords;
   const bool vec_ok = (((uintptr_t)w) & 15) == 0;
-  const bool use_win = cb.lo <= cb.hi;
+  // the window always contains T (a disabled window is [T, T]): a lane
+  // with no key inside it has no tie either, so its ">= T" mask is its
+  // "> T" mask; only lanes touching the window rebuild both exactly
+  const bool use_win = cb.lo <= cb.hi && cb.key != nullptr;
+  const uint32_t wlo = use_win ? cb.lo : T, W = use_win ? cb.hi - cb.lo : 0u;
   // chunks streamed through the ring: whole 1024-element chunks of an
   // aligned vector (the ragged last chunk is read directly)
   auto full = [&](uint64_t c) { return vec_ok && (c + 1) * (uint64_t)kChunk <= len; };
   uint32_t c_lt = 0, c_eq = 0, c_below = 0, fill = 0;
-  int changed = 0, changed_cand = 0, mismatch = 0;
+  int changed = 0, changed_cand = 0, changed_tie = 0, mismatch = 0;
   const uint64_t nw_total = (uint64_t)gridDim.x * kPruneWarps;
   const uint64_t c0 = (uint64_t)blockIdx.x * kPruneWarps + warp;
 #pragma unroll
@@ -417,64 +425,36 @@ __global__ void __launch_bounds__(kPruneWarps * 32)
     slot = slot == kKeyStages - 1 ? 0 : slot + 1;
     const bool fc = full(c);
     const uint64_t e0 = c * (uint64_t)kChunk + 32 * lane;
-    // window test: (key - lo) <= W as unsigned (keys, lo < 2^31, so key < lo
-    // wraps above W); the running minimum tells whether ANY of the lane's 32
-    // keys is inside, the exact mask is rebuilt only then (a few % of lanes)
-    const uint32_t W = cb.hi - cb.lo;
-    uint32_t g = 0, e = 0, mn = ~0u, inr = ~0u;
+    // per element: one compare against T (funnel-shifted sign) and the
+    // running minimum of key - lo (unsigned: keys below lo wrap above W)
+    uint32_t g = 0, mn = ~0u, inr = ~0u;
     if (fc) {
 #pragma unroll
       for (int k = kVecPerLane - 1; k >= 0; --k) {  // elements 32*lane + 4k .. 4k+3
         const float4 v =
             *reinterpret_cast<const float4*>(st + 4 * (lane * 8 + (k ^ (lane & 7))));
-        classify_push(mag_key(v.w), T, g, e);
-        classify_push(mag_key(v.z), T, g, e);
-        classify_push(mag_key(v.y), T, g, e);
-        classify_push(mag_key(v.x), T, g, e);
-        if (use_win) {
-          mn = min(mn, min(min(mag_key(v.w) - cb.lo, mag_key(v.z) - cb.lo),
-                           min(mag_key(v.y) - cb.lo, mag_key(v.x) - cb.lo)));
-        }
+        const uint32_t k3 = mag_key(v.w), k2 = mag_key(v.z), k1 = mag_key(v.y), k0 = mag_key(v.x);
+        g = __funnelshift_l(T - k3, g, 1);
+        g = __funnelshift_l(T - k2, g, 1);
+        g = __funnelshift_l(T - k1, g, 1);
+        g = __funnelshift_l(T - k0, g, 1);
+        mn = min(mn, min(min(k3 - wlo, k2 - wlo), min(k1 - wlo, k0 - wlo)));
       }
     } else {
       inr = e0 >= len ? 0u : (len - e0 >= 32 ? ~0u : (1u << (len - e0)) - 1u);
       for (int i = 31; i >= 0; --i) {
         const uint32_t kq = e0 + i < len ? mag_key(w[e0 + i]) : 0u;
-        classify_push(kq, T, g, e);
-        if (use_win && e0 + i < len) mn = min(mn, kq - cb.lo);
+        g = __funnelshift_l(T - kq, g, 1);
+        if (e0 + i < len) mn = min(mn, kq - wlo);
       }
     }
     g &= inr;
-    e &= inr;
-    const uint32_t eqm = e & ~g;
-    c_lt += __popc(inr & ~e);
-    const uint32_t ne = __popc(eqm);
-    c_eq += ne;
-    const uint32_t inc = warp_incl_scan(ne);
-    const uint32_t E = __shfl_sync(0xffffffffu, inc, 31);
-    uint32_t keep = g;
+    uint32_t e = g, cand = 0;
     const uint64_t hi = c * 32 + lane;  // this lane's 32-bit half of the mask
-    if (E) {
-      if (tie_prefix) {
-        // ties of rank < r (index order) are dropped: the first D of this lane
-        const uint64_t rk0 = (uint64_t)__ldg(tie_prefix + c) + inc - ne;
-        uint32_t d = r > rk0 ? (r - rk0 < ne ? (uint32_t)(r - rk0) : ne) : 0u, x = eqm;
-        for (; d; --d) x &= x - 1;
-        keep |= x;
-      }
-      if (hi < nhalves) tie32[hi] = eqm;
-    }
-    if (lane == 0) {
-      ties_out[c] = E;
-      if (ties_prev && ties_prev[c] != E) mismatch = 1;
-    }
     const uint32_t old = hi < nhalves ? (fc ? reinterpret_cast<const uint32_t*>(st + kChunk)[lane] : words32[hi]) : 0u;
-    uint32_t cand = 0;
-    if (use_win) {
-      // lanes whose 32 keys touch the window are resolved one at a time by
-      // the whole warp: lane j tests element j of lane l, a ballot is lane
-      // l's candidate mask (bit j = element j), and the warp stages the
-      // candidates with their previous mask bits
+    {
+      // lanes whose keys touch the window, one at a time, by the whole warp:
+      // lane j tests element j of lane l, ballots are lane l's exact masks
       uint32_t todo = __ballot_sync(0xffffffffu, mn <= W);
       while (todo) {
         const int l = __ffs(todo) - 1;
@@ -488,42 +468,79 @@ __global__ void __launch_bounds__(kPruneWarps * 32)
           ok = el0 + lane < len;
           kq = ok ? mag_key(w[el0 + lane]) : 0u;
         }
-        const uint32_t eql = __shfl_sync(0xffffffffu, eqm, l);
-        const bool in = ok && (kq - cb.lo <= W) && !((eql >> lane) & 1u);
-        const uint32_t m = __ballot_sync(0xffffffffu, in);
-        if (lane == l) cand = m;
-        if (!m) continue;
+        const uint32_t me = __ballot_sync(0xffffffffu, ok && kq >= T);
+        const uint32_t mw = __ballot_sync(0xffffffffu, ok && kq != T && kq - wlo <= W);
+        if (lane == l) {
+          e = me;
+          cand = use_win ? mw : 0u;
+        }
+        if (!use_win || !mw) continue;
         const uint32_t oldl = __shfl_sync(0xffffffffu, old, l);
-        const uint32_t el = __shfl_sync(0xffffffffu, e, l);
-        if (lane == 0) c_below += __popc(m & ~el);  // #(key < lo) = #(key < T) - these
-        const uint32_t nm = __popc(m);
+        if (lane == 0) c_below += __popc(mw & ~me);  // #(key < lo) = #(key < T) - these
+        const uint32_t nm = __popc(mw);
         if (fill + nm > (uint32_t)kCandBuf) {
           flush_pairs(cbk, cbi, fill, &counts->n_cand, cb);
           fill = 0;
         }
-        if (in) {
-          const uint32_t pos = fill + __popc(m & ((1u << lane) - 1u));
+        if ((mw >> lane) & 1u) {
+          const uint32_t pos = fill + __popc(mw & ((1u << lane) - 1u));
           cbk[pos] = kq;
           cbi[pos] = (uint32_t)(el0 + lane) | (((oldl >> lane) & 1u) << 31);
+        }
+        if (cb.hist && ((mw >> lane) & 1u)) {
+          const uint32_t bin = (kq - wlo) >> cb.hshift;
+          const unsigned peers = __match_any_sync(mw, bin);
+          if (lane == __ffs(peers) - 1) atomicAdd(&chist[bin], (uint32_t)__popc(peers));
         }
         __syncwarp();
         fill += nm;
       }
     }
+    const uint32_t eqm = e & ~g;
+    c_lt += __popc(inr & ~e);
+    const uint32_t ne = __popc(eqm);
+    c_eq += ne;
+    const uint32_t inc = warp_incl_scan(ne);
+    const uint32_t E = __shfl_sync(0xffffffffu, inc, 31);
+    uint32_t keep = g;
+    if (E) {
+      if (tie_prefix) {
+        // ties of rank < r (index order) are dropped: the first D of this lane
+        const uint64_t rk0 = (uint64_t)__ldg(tie_prefix + c) + inc - ne;
+        uint32_t d = r > rk0 ? (r - rk0 < ne ? (uint32_t)(r - rk0) : ne) : 0u, x = eqm;
+        for (; d; --d) x &= x - 1;
+        keep |= x;
+      }
+      if (hi < nhalves) {
+        tie32[hi] = eqm;
+        if (tie_old32) tie_old32[hi] = old & eqm;  // previous bits of the ties: the fix-up's change test
+      }
+    }
+    if (lane == 0) {
+      ties_out[c] = E;
+      if (ties_prev && ties_prev[c] != E) mismatch = 1;
+    }
     if (hi < nhalves && old != keep) {
       words32[hi] = keep;
-      if ((old ^ keep) & ~cand) changed = 1;
+      if ((old ^ keep) & ~cand & ~eqm) changed = 1;
       if ((old ^ keep) & cand) changed_cand = 1;
+      if ((old ^ keep) & eqm) changed_tie = 1;
     }
     const uint32_t pc = warp_sum((uint32_t)__popc(keep));
     if (lane == 0) chunk_popc[c] = pc;
   }
   if (fill) flush_pairs(cbk, cbi, fill, &counts->n_cand, cb);
+  if (cb.hist) {
+    __syncthreads();
+    for (int b = threadIdx.x; b < (1 << kCandHistBits); b += blockDim.x)
+      if (chist[b]) atomicAdd(&cb.hist[b], chist[b]);
+  }
   c_lt = warp_sum(c_lt);
   c_eq = warp_sum(c_eq);
   c_below = warp_sum(c_below);
   changed = __any_sync(0xffffffffu, changed);
   changed_cand = __any_sync(0xffffffffu, changed_cand);
+  changed_tie = __any_sync(0xffffffffu, changed_tie);
   mismatch = __any_sync(0xffffffffu, mismatch);
   if (lane == 0) {
     if (c_lt) atomicAdd(&counts->n_lt, (unsigned long long)c_lt);
@@ -531,6 +548,7 @@ __global__ void __launch_bounds__(kPruneWarps * 32)
     if (c_below) atomicAdd(&counts->n_cand_below, (unsigned long long)c_below);  // candidates below T
     if (changed) atomicOr(&counts->changed, 1);
     if (changed_cand) atomicOr(&counts->changed_cand, 1);
+    if (changed_tie) atomicOr(&counts->changed_tie, 1);
     if (mismatch) atomicOr(&counts->tie_mismatch, 1);
   }
 }
@@ -539,11 +557,32 @@ __global__ void __launch_bounds__(kPruneWarps * 32)
 // The pass's threshold T was stale, the true T' lies in the window: every
 // candidate's bit is rewritten for T' (ties provisionally dropped, recorded
 // for the tie fix-up when they straddle the rank r').
+__global__ void prune_win_final_kernel(const SelState* __restrict__ sel, uint32_t base, int bits, uint64_t ncand,
+                                       uint64_t c_base, uint64_t k, WinSel* __restrict__ ws) {
+  WinSel o{};
+  uint64_t below = 0, eq = ncand;
+  uint32_t v = 0;
+  if (bits > 0) {
+    v = sel->prefix;
+    below = sel->below;
+    eq = sel->eq;
+    o.err = sel->err;
+  }
+  o.T1 = base + v;
+  o.below = below;
+  o.eq1 = eq;
+  o.c_lt1 = c_base + below;
+  o.r1 = k - o.c_lt1;
+  if (o.c_lt1 >= k || o.r1 > eq) o.err = 1;
+  o.straddle = !o.err && o.r1 < eq;
+  *ws = o;
+}
+
 __global__ void __launch_bounds__(256)
     prune_cand_tieclear_kernel(const uint32_t* __restrict__ key, const uint32_t* __restrict__ idx, uint64_t n,
-                               uint32_t T, uint64_t* __restrict__ tie_words) {
+                               const WinSel* __restrict__ ws, uint64_t* __restrict__ tie_words) {
   const uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  if (j >= n || key[j] != T) return;
+  if (!ws->straddle || j >= n || key[j] != ws->T1) return;
   const uint64_t c = (idx[j] & 0x7fffffffu) >> 10;
 #pragma unroll
   for (int q = 0; q < kChunkWords; ++q) tie_words[c * kChunkWords + q] = 0ull;
@@ -551,10 +590,12 @@ __global__ void __launch_bounds__(256)
 
 __global__ void __launch_bounds__(256)
     prune_cand_fix_kernel(const uint32_t* __restrict__ key, const uint32_t* __restrict__ idx, uint64_t n,
-                          uint32_t T, int straddle, unsigned long long* __restrict__ words,
+                          const WinSel* __restrict__ ws, unsigned long long* __restrict__ words,
                           uint32_t* __restrict__ chunk_popc, unsigned long long* __restrict__ tie_words,
                           uint32_t* __restrict__ ties, int* __restrict__ changed) {
   const uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  const uint32_t T = ws->T1;
+  const int straddle = ws->straddle;
   bool ch = false;
   if (j < n) {
     const uint32_t kq = key[j], v = idx[j], ix = v & 0x7fffffffu;
@@ -565,8 +606,12 @@ __global__ void __launch_bounds__(256)
       atomicOr(&tie_words[ix >> 6], bit);
       atomicAdd(&ties[ix >> 10], 1u);
     }
-    const unsigned long long old = keep ? atomicOr(&words[ix >> 6], bit) : atomicAnd(&words[ix >> 6], ~bit);
-    if (((old & bit) != 0) != keep) atomicAdd(&chunk_popc[ix >> 10], keep ? 1u : 0xffffffffu);
+    // only the bits between the pass's threshold and T' flip: test first,
+    // atomics for the flips alone (other candidates of the word may flip too)
+    if ((((words[ix >> 6] & bit) != 0) != keep) || tie) {
+      const unsigned long long old = keep ? atomicOr(&words[ix >> 6], bit) : atomicAnd(&words[ix >> 6], ~bit);
+      if (((old & bit) != 0) != keep) atomicAdd(&chunk_popc[ix >> 10], keep ? 1u : 0xffffffffu);
+    }
     ch = !tie && keep != (bool)(v >> 31);
   }
   if (__any_sync(0xffffffffu, ch) && (threadIdx.x & 31) == 0) *changed = 1;
@@ -574,10 +619,12 @@ __global__ void __launch_bounds__(256)
 
 __global__ void __launch_bounds__(256)
     prune_cand_changed_kernel(const uint32_t* __restrict__ key, const uint32_t* __restrict__ idx, uint64_t n,
-                              uint32_t T, const uint64_t* __restrict__ words, int* __restrict__ flag) {
+                              const WinSel* __restrict__ ws, const uint64_t* __restrict__ words,
+                              int* __restrict__ flag) {
   const uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (!ws->straddle) return;
   bool ch = false;
-  if (j < n && key[j] == T) {  // the tie candidates (the others were checked by the fix-up)
+  if (j < n && key[j] == ws->T1) {  // the tie candidates (the others were checked by the fix-up)
     const uint32_t v = idx[j], ix = v & 0x7fffffffu;
     ch = ((words[ix >> 6] >> (ix & 63)) & 1u) != (v >> 31);
   }
@@ -593,7 +640,13 @@ __global__ void __launch_bounds__(256)
     prune_tiefix_kernel(uint64_t* __restrict__ words, uint64_t nwords,
                         const uint64_t* __restrict__ tie_words, const uint32_t* __restrict__ ties,
                         const uint32_t* __restrict__ tie_prefix, uint64_t r, int keep_low,
-                        uint32_t* __restrict__ chunk_popc, uint64_t nchunks) {
+                        uint32_t* __restrict__ chunk_popc, uint64_t nchunks,
+                        const uint64_t* __restrict__ tie_old, int* __restrict__ changed,
+                        const WinSel* __restrict__ ws) {
+  if (ws) {
+    if (!ws->straddle) return;
+    r = ws->r1;
+  }
   // a warp scans the tie counts of 32 chunks at a time (one coalesced load)
   // and fixes only the chunks that hold ties: ties are rare except at key 0
   const int lane = threadIdx.x & 31;
@@ -624,12 +677,15 @@ __global__ void __launch_bounds__(256)
         x ^= bb;
       }
       uint32_t pc = 0;
+      bool ch = false;
       if (valid) {
         // prune: the first ties (lowest indices) are dropped; TopK keeps them
         const uint64_t nw = (words[wi] & ~tw) | (keep_low ? first : (tw & ~first));
         words[wi] = nw;
         pc = (uint32_t)__popcll(nw);
+        if (tie_old) ch = (nw & tw) != tie_old[wi];
       }
+      if (tie_old && __any_sync(0xffffffffu, ch) && lane == 0) *changed = 1;
       pc = warp_sum(pc);
       if (lane == 0) chunk_popc[c] = pc;
     }
@@ -799,9 +855,11 @@ void launch_prune_pick(const uint32_t* hist, int nbits, int first, uint64_t rank
 void launch_prune_bitmap(const float* w, uint64_t len, uint32_t T, uint64_t r,
                          const uint32_t* tie_prefix, uint64_t* words, uint32_t* chunk_popc,
                          uint32_t* ties_out, const uint32_t* ties_prev, uint64_t* tie_words,
-                         BitmapCounts* counts, cudaStream_t s, const PruneCandBuf& cand) {
+                         BitmapCounts* counts, cudaStream_t s, const PruneCandBuf& cand,
+                         uint64_t* tie_old) {
   const uint64_t nc = (len + kChunk - 1) / kChunk;
   cudaMemsetAsync(counts, 0, sizeof(BitmapCounts), s);
+  if (cand.hist) cudaMemsetAsync(cand.hist, 0, sizeof(uint32_t) << kCandHistBits, s);
   if (!nc) return;
   static DeviceCache<unsigned> cap;
   unsigned& cp = cap.get();
@@ -812,45 +870,68 @@ void launch_prune_bitmap(const float* w, uint64_t len, uint32_t T, uint64_t r,
   }
   const uint64_t need = (nc + kPruneWarps - 1) / kPruneWarps;
   prune_bitmap_kernel<<<(unsigned)(need < cp ? need : cp), kPruneWarps * 32, kBitmapSmem, s>>>(
-      w, len, T, r, tie_prefix, words, (len + 63) / 64, chunk_popc, ties_out, ties_prev, tie_words,
+      w, len, T, r, tie_prefix, words, (len + 63) / 64, chunk_popc, ties_out, ties_prev, tie_words, tie_old,
       counts, nc, cand);
   note_launch();
 }
 
-void launch_prune_cand_tieclear(const uint32_t* key, const uint32_t* idx, uint64_t n, uint32_t T,
-                                uint64_t* tie_words, cudaStream_t s) {
-  if (!n) return;
-  prune_cand_tieclear_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(key, idx, n, T, tie_words);
+__global__ void prune_win_report_kernel(const WinSel* ws, const uint64_t* digest, const uint32_t* nnz,
+                                        const int* fix_changed, WinReport* out) {
+  WinReport r;
+  r.w = *ws;
+  r.digest = *digest;
+  r.nnz = *nnz;
+  r.fix_changed = *fix_changed;
+  *out = r;
+}
+
+void launch_prune_win_report(const WinSel* ws, const uint64_t* digest, const uint32_t* nnz,
+                             const int* fix_changed, WinReport* out, cudaStream_t s) {
+  prune_win_report_kernel<<<1, 1, 0, s>>>(ws, digest, nnz, fix_changed, out);
   note_launch();
 }
 
-void launch_prune_cand_fix(const uint32_t* key, const uint32_t* idx, uint64_t n, uint32_t T, int straddle,
+void launch_prune_win_final(const SelState* sel, uint32_t base, int bits, uint64_t ncand, uint64_t c_base,
+                            uint64_t k, WinSel* ws, cudaStream_t s) {
+  prune_win_final_kernel<<<1, 1, 0, s>>>(sel, base, bits, ncand, c_base, k, ws);
+  note_launch();
+}
+
+void launch_prune_cand_tieclear(const uint32_t* key, const uint32_t* idx, uint64_t n, const WinSel* ws,
+                                uint64_t* tie_words, cudaStream_t s) {
+  if (!n) return;
+  prune_cand_tieclear_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(key, idx, n, ws, tie_words);
+  note_launch();
+}
+
+void launch_prune_cand_fix(const uint32_t* key, const uint32_t* idx, uint64_t n, const WinSel* ws,
                            uint64_t* words, uint32_t* chunk_popc, uint64_t* tie_words, uint32_t* ties,
                            int* changed, cudaStream_t s) {
   if (!n) return;
   prune_cand_fix_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(
-      key, idx, n, T, straddle, reinterpret_cast<unsigned long long*>(words), chunk_popc,
+      key, idx, n, ws, reinterpret_cast<unsigned long long*>(words), chunk_popc,
       reinterpret_cast<unsigned long long*>(tie_words), ties, changed);
   note_launch();
 }
 
-void launch_prune_cand_changed(const uint32_t* key, const uint32_t* idx, uint64_t n, uint32_t T,
+void launch_prune_cand_changed(const uint32_t* key, const uint32_t* idx, uint64_t n, const WinSel* ws,
                                const uint64_t* words, int* flag, cudaStream_t s) {
   if (!n) return;
-  prune_cand_changed_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(key, idx, n, T, words, flag);
+  prune_cand_changed_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(key, idx, n, ws, words, flag);
   note_launch();
 }
 
 void launch_prune_tiefix(uint64_t* words, uint64_t len, const uint64_t* tie_words,
                          const uint32_t* ties, const uint32_t* tie_prefix, uint64_t r,
-                         uint32_t* chunk_popc, cudaStream_t s, int keep_low) {
+                         uint32_t* chunk_popc, cudaStream_t s, int keep_low, const uint64_t* tie_old,
+                         int* changed, const WinSel* ws) {
   const uint64_t nc = (len + kChunk - 1) / kChunk;
   if (!nc) return;
   uint64_t blocks = (nc + 255) / 256;  // 8 warps x 32 chunks per CTA and pass
   const uint64_t cap = (uint64_t)num_sms() * 8;
   if (blocks > cap) blocks = cap;
   prune_tiefix_kernel<<<(unsigned)blocks, 256, 0, s>>>(words, (len + 63) / 64, tie_words, ties, tie_prefix, r,
-                                                       keep_low, chunk_popc, nc);
+                                                       keep_low, chunk_popc, nc, tie_old, changed, ws);
   note_launch();
 }
 

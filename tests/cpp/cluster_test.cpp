@@ -187,6 +187,66 @@ int main(int argc, char** argv) {
         CHECK(std::fabs(out[r0][i] - expect[i]) <= 1e-5 * std::max(1.0, std::fabs(expect[i])));
     }
   }
+  // collective.cpp:165-216 ring_allreduce in the reference's own fold order:
+  // bit-identical to ((x_c + x_{c+1}) + ...) + x_{c-1} per ChunkMap chunk c
+  {
+    const int n = nmax;
+    {
+      std::vector<FlatTensor> in;
+      for (int r = 0; r < n; ++r) in.push_back(FlatTensor(std::vector<float>(n, r == 0 ? 1e8f : r == 1 ? -1e8f : 1.0f)));
+      std::vector<FlatTensor> out(n);
+      run_workers(n, [&](int r, Comm& c) { out[r] = ring_allreduce(in[r], c); });
+      if (r0 < n) {
+        const size_t len = in[0].size(), C = (len + n - 1) / n;
+        for (size_t i = 0; i < len; ++i) {
+          const int c = (int)(i / C);
+          float acc = in[c][i];
+          for (int s = 1; s < n; ++s) acc += in[(c + s) % n][i];
+          CHECK(out[r0][i] == acc);  // n = 3: [1, 0, 0] (SURVEY A.6 probe)
+        }
+      }
+    }
+    std::mt19937_64 g(77);
+    std::vector<FlatTensor> raw;
+    for (int r = 0; r < n; ++r) raw.push_back(random_tensor(g, 100003));
+    std::vector<FlatTensor> out(n);
+    run_workers(n, [&](int r, Comm& c) { out[r] = ring_allreduce(raw[r], c); });
+    if (r0 < n) {
+      const size_t len = raw[0].size(), C = (len + n - 1) / n;
+      for (size_t i = 0; i < len; ++i) {
+        const int c = (int)(i / C);
+        float acc = raw[c][i];
+        for (int s = 1; s < n; ++s) acc += raw[(c + s) % n][i];
+        CHECK(out[r0][i] == acc);
+      }
+    }
+    // lengths that disagree: ShapeMismatch on every rank
+    std::vector<int> code(n, -1);
+    run_workers(n, [&](int r, Comm& c) {
+      try {
+        ring_allreduce(FlatTensor::zeros(r == 0 ? 11 : 10), c);
+        code[r] = 0;
+      } catch (const Error& e) {
+        code[r] = (int)e.code();
+      }
+    });
+    if (r0 < n) CHECK(code[r0] == (int)Errc::ShapeMismatch);
+  }
+  // collective.cpp:222-247 allgather: payloads of different sizes, by rank
+  {
+    const int n = nmax;
+    std::vector<std::vector<std::vector<std::byte>>> got(n);
+    run_workers(n, [&](int r, Comm& c) {
+      got[r] = allgather(std::vector<std::byte>((size_t)r + 1, static_cast<std::byte>(r + 1)), c);
+    });
+    if (r0 < n) {
+      CHECK((int)got[r0].size() == n);
+      for (int q = 0; q < n && q < (int)got[r0].size(); ++q) {
+        CHECK(got[r0][q].size() == (size_t)q + 1);
+        for (auto b : got[r0][q]) CHECK(std::to_integer<int>(b) == q + 1);
+      }
+    }
+  }
   // extension: the measured dense/sparse crossover is unanimous
   {
     const int n = 2;

@@ -182,6 +182,52 @@ int main() {
     CHECK(code_of([&] { topk_densify(oob); }) == Errc::CorruptPayload);
   }
 
+  // test_codec.cpp:276-287: packed frame payload size is 4*nnz + header
+  {
+    std::mt19937_64 rng(71);
+    std::normal_distribution<float> nd;
+    std::uniform_real_distribution<double> u(0, 1);
+    std::vector<float> v(200);
+    std::vector<bool> bits(200);
+    for (size_t i = 0; i < 200; ++i) {
+      v[i] = nd(rng);
+      bits[i] = u(rng) < 0.4;
+    }
+    SparsityMask m = SparsityMask::from_bits(bits);
+    PackedGradient p = pack(FlatTensor(v), m, 2);
+    wire::Bytes b = wire::encode_packed(p);
+    CHECK(b.size() == wire::kHeaderSize + 4 * m.nnz());
+    PackedGradient back = wire::decode_packed(b);
+    CHECK(back.values == p.values);
+    CHECK(back.mask_digest == p.mask_digest);
+    CHECK(back.epoch == p.epoch);
+    b.pop_back();
+    CHECK(code_of([&] { wire::decode_packed(b); }) == Errc::CorruptPayload);  // truncated
+    CHECK(code_of([&] { wire::decode_packed(wire::encode_full(FlatTensor(v), 0)); }) == Errc::CorruptPayload);
+    CHECK(wire::decode_full(wire::encode_full(FlatTensor(v), 3)) == FlatTensor(v));
+  }
+  // sparsity.cpp:11-15, 121-128: build_prune_mask(Magnitude) == magnitude_prune
+  {
+    std::mt19937_64 rng(5);
+    std::normal_distribution<float> nd;
+    std::vector<float> w(5000);
+    for (auto& x : w) x = nd(rng);
+    PruneConfig cfg;
+    cfg.ratio = 0.7f;
+    SparsityMask a = build_prune_mask(FlatTensor(w), cfg), b = magnitude_prune(FlatTensor(w), 0.7f);
+    CHECK(a.words() == b.words() && a.nnz() == 1500);
+    PruneConfig bad;
+    bad.ratio = 1.0f;
+    CHECK(code_of([&] { build_prune_mask(FlatTensor(w), bad); }) == Errc::InvalidRatio);
+    PruneConfig eps;
+    eps.grasp_epsilon = 0.0f;
+    CHECK(code_of([&] { eps.validate(); }) == Errc::InvalidRatio);
+    PruneConfig grasp;
+    grasp.method = PruneMethod::Grasp;
+    grasp.ratio = 0.5f;
+    CHECK(code_of([&] { build_prune_mask(FlatTensor(w), grasp); }) == Errc::NumericalFailure);
+  }
+
   std::printf("dropin_test: %d failure(s)\n", g_fail);
   return g_fail;
 }
