@@ -340,6 +340,9 @@ def main():
                          "on the same workload (ternary_allgather_aggregate, fp16_allreduce, "
                          "masked_allreduce on the binary16 wire, topk_allgather_aggregate)")
     ap.add_argument("--topk-rate", type=float, default=0.01)
+    ap.add_argument("--prune", default="global", choices=["global", "per-layer"],
+                    help="re-prune rule of the timed step: one global threshold (the reference's "
+                         "magnitude_prune) or one threshold per layer (north_star (1), SURVEY D1)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -486,11 +489,17 @@ def main():
     # ---- headline: device-resident step
     paths = {}
 
+    layer_offs = shape.offsets()
+
     def step_h(e):
         if reprune:
-            st = {}
-            pb.magnitude_prune(w_cur, ratio, out=mask, stats=st)
-            paths[st["path"]] = paths.get(st["path"], 0) + 1
+            if args.prune == "per-layer":
+                pb.magnitude_prune_per_layer(w_cur, layer_offs, ratio, out=mask)
+                paths["per-layer"] = paths.get("per-layer", 0) + 1
+            else:
+                st = {}
+                pb.magnitude_prune(w_cur, ratio, out=mask, stats=st)
+                paths[st["path"]] = paths.get(st["path"], 0) + 1
             tracker.observe(mask)
         return pb.masked_allreduce(grad, mask, tracker.status(), e, comm, policy=policy, out=out)
 
@@ -583,6 +592,10 @@ def main():
         t_full = statistics.median(timed(prune_full, 3, pre=lambda i: pb.api._call(
             pb.api.lib.pact_mask_fill, scratch.handle, 0, pb.api._stream())))
         p_full = pr.pop("paths")
+        # per-layer thresholds: every layer's own k-th key, all
+        # layers at once (prune_seg.cu), against the global first-time prune
+        t_layer = statistics.median(timed(lambda i: pb.magnitude_prune_per_layer(w_cur, layer_offs, ratio,
+                                                                                 out=scratch), 3))
         del scratch
         # a whole step whose mask changed (regrowth), on the packed path
         # (the tracker would fall back to dense for K steps; this is the cost
@@ -594,16 +607,18 @@ def main():
         t_step_change = statistics.median(timed(step_stable, 5, pre=lambda i: perturb(50_000 + i, "regrow")))
         t_step_hit = statistics.median(timed(step_stable, 5))
         if world > 1:
-            tt = torch.tensor([t_hit, t_a9, t_drift, t_regrow, t_full, t_step_change, t_step_hit],
+            tt = torch.tensor([t_hit, t_a9, t_drift, t_regrow, t_full, t_step_change, t_step_hit, t_layer],
                               dtype=torch.float64, device=dev)
             torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-            t_hit, t_a9, t_drift, t_regrow, t_full, t_step_change, t_step_hit = tt.tolist()
+            t_hit, t_a9, t_drift, t_regrow, t_full, t_step_change, t_step_hit, t_layer = tt.tolist()
         stages["prune"] = {
             "reuse_hit_us": round(t_hit * 1e6, 1), "reuse_hit_gbs": round(alg_prune / t_hit / 1e9, 1),
             "a9_us": round(t_a9 * 1e6, 1), "a9_paths": p_a9,
             "dense_drift_plus_digest_us": round(t_drift * 1e6, 1), "dense_drift_paths": p_drift,
             "regrowth_change_plus_digest_us": round(t_regrow * 1e6, 1), "regrowth_paths": p_regrow,
             "first_time_sampled_us": round(t_full * 1e6, 1), "first_time_paths": p_full,
+            "per_layer_us": round(t_layer * 1e6, 1), "per_layer_layers": len(layer_offs) - 1,
+            "per_layer_vs_global_first_time": round(t_layer / t_full, 3),
             "paths_legend": "1 sampled window, 2 full radix, 3 threshold reuse, 4 moved threshold from window candidates",
         }
         stages["mask_change_step_us"] = round(t_step_change * 1e6, 1)
@@ -712,7 +727,8 @@ def main():
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
             "value_job": round(value * world, 2),
-            "config": {"workload": workload_name(cfg, model, ratio, reprune),
+            "config": {"workload": workload_name(cfg, model, ratio, reprune)
+                       + (", per-layer thresholds" if reprune and args.prune == "per-layer" else ""),
                        "len": n, "nnz": nnz, "ratio": ratio, "reprune_per_step": reprune,
                        "weights": "W-real (SURVEY A.9), identical on every rank",
                        "perturbation": ("A.9 between timed steps: kept w += delta (|delta| <= 2^-14), pruned "

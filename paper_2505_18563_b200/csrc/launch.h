@@ -231,16 +231,40 @@ void launch_slot_mean(const double* acc, const uint32_t* total, uint64_t max_slo
 void launch_scatter_f32(const uint32_t* idx, const float* val, uint64_t k, uint64_t len, float* out,
                         int* err, cudaStream_t s);
 
-// per-layer mode: thread per word, element i of segment s kept iff key > T_s;
-// ties recorded (tie_words, word_ties) for the fix-up below
-void launch_prune_seg_bitmap(const float* w, uint64_t len, const uint64_t* seg, uint64_t nseg,
-                             const uint32_t* Tseg, uint64_t* words, uint64_t* tie_words,
-                             uint32_t* word_ties, cudaStream_t s);
-// keep tie j of segment s iff its in-segment rank >= rseg[s]; word_prefix =
-// exclusive scan of word_ties; seg_base scratch (nseg u64)
-void launch_prune_seg_tiefix(uint64_t* words, uint64_t len, const uint64_t* tie_words,
-                             const uint32_t* word_prefix, const uint64_t* seg, uint64_t nseg,
-                             uint64_t* seg_base, const uint64_t* rseg, cudaStream_t s);
+// ---- prune_seg.cu (per-layer mode, every layer at once) ---------------------
+struct SegInfo {  // host-filled, one per layer [begin, end)
+  unsigned long long begin, end, k;       // element range, drop count
+  unsigned long long cand_off, cand_cap;  // the layer's window-candidate region
+  int trivial;                            // 0 select, 1 keep all, 2 drop all
+  int pad;
+};
+struct SegState {  // device-filled (the host seeds trivial layers)
+  uint32_t lo, hi;  // sampled window of the k-th key
+  uint32_t T;       // the layer's threshold key
+  int mode;         // 0 resolved, 1 window missed (the host selects exactly)
+  unsigned long long n_lt, n_eq_lo, n_eq_hi;  // counting pass
+  unsigned long long c_lt, r;                 // #(key < T), ties dropped
+  unsigned long long tie_base;                // ties before the layer's first element
+  unsigned long long b_lt, b_eq;              // bitmap pass: #(key < T), #(key == T)
+};
+struct SegTile {  // a <= 64 Ki-element range inside one layer
+  uint32_t seg, pad;
+  unsigned long long begin, end;
+};
+void launch_seg_sample(const float* w, const SegInfo* info, SegState* st, uint32_t nseg, cudaStream_t s);
+void launch_seg_count(const float* w, const SegInfo* info, SegState* st, const SegTile* tiles, uint32_t ntiles,
+                      uint32_t* cand, unsigned long long* fill, cudaStream_t s);
+void launch_seg_select(const SegInfo* info, SegState* st, uint32_t nseg, const uint32_t* cand,
+                       const unsigned long long* fill, cudaStream_t s);
+// words (ties provisionally dropped), tie words of chunks with ties,
+// per-chunk tie counts and kept counts, per-layer b_lt / b_eq
+void launch_seg_bitmap(const float* w, uint64_t len, const SegInfo* info, SegState* st, const uint32_t* chunk_seg,
+                       uint64_t* words, uint64_t* tie_words, uint32_t* ties, uint32_t* chunk_popc, cudaStream_t s);
+void launch_seg_tiebase(const SegInfo* info, SegState* st, uint32_t nseg, const uint64_t* tie_words,
+                        const uint32_t* ties, const uint32_t* tie_prefix, cudaStream_t s);
+void launch_seg_tiefix(uint64_t len, const SegInfo* info, const SegState* st, const uint32_t* chunk_seg,
+                       uint64_t* words, const uint64_t* tie_words, const uint32_t* ties, const uint32_t* tie_prefix,
+                       uint32_t* chunk_popc, cudaStream_t s);
 
 // ---- ternary.cu -------------------------------------------------------------
 // x[i] = x[i] / d (IEEE division; the gather paths' `sum / float(n)`)

@@ -184,6 +184,7 @@ struct P2PState {  // CUDA-IPC symmetric buffers of all ranks (p2p.cu)
   uint64_t cap = 0, creg = 0;  // floats per packed / reduced region (2 regions each)
   void* sym = nullptr;         // own buffer: [flags 4 KiB][packed x2][reduced x2]
   char* base[pactk::kP2PMaxRanks] = {};
+  bool ipc[pactk::kP2PMaxRanks] = {};  // base[r] opened through CUDA IPC (else same process)
   uint64_t k = 0;              // P2P steps completed (flag values)
   DevBuf err;                  // pactk::P2PErr (device): a consumer timed out
   int* err_host = nullptr;     // its host-mapped twin, read before every call
@@ -382,7 +383,8 @@ unsigned* p2p_counter(const P2PState& p, int r) {
 void p2p_release(pact_comm* c) {
   P2PState& p = c->p2p;
   for (int r = 0; r < c->n; ++r)
-    if (r != c->rank && p.base[r]) cudaIpcCloseMemHandle(p.base[r]);
+    if (r != c->rank && p.base[r] && p.ipc[r]) cudaIpcCloseMemHandle(p.base[r]);
+  for (auto& f : p.ipc) f = false;
   if (p.sym) cudaFree(p.sym);
   for (auto& b : p.base) b = nullptr;
   p.sym = nullptr;
@@ -413,9 +415,17 @@ pact_status p2p_setup(pact_comm* c, uint64_t need, cudaStream_t s) {
   cudaIpcMemHandle_t h{};
   if (ok && cudaIpcGetMemHandle(&h, p.sym) != cudaSuccess) ok = 0;
   cudaGetLastError();
-  uint8_t frame[1 + sizeof(h)];
+  // frame: ok | IPC handle | pid | device | raw pointer. Ranks that are
+  // threads of this process (the reference's SimCluster topology) map each
+  // other by peer access instead: a process cannot open its own IPC handles.
+  const int32_t pid = (int32_t)getpid(), mydev = c->ctx->device;
+  const uint64_t raw = (uint64_t)(uintptr_t)p.sym;
+  uint8_t frame[1 + sizeof(h) + 4 + 4 + 8];
   frame[0] = (uint8_t)ok;
   std::memcpy(frame + 1, &h, sizeof h);
+  std::memcpy(frame + 1 + sizeof h, &pid, 4);
+  std::memcpy(frame + 5 + sizeof h, &mydev, 4);
+  std::memcpy(frame + 9 + sizeof h, &raw, 8);
   std::vector<uint8_t> frames((size_t)c->n * sizeof frame);
   TRY(pact_allgather_frames(c, frame, sizeof frame, frames.data(), s));
   int all_ok = 1;
@@ -427,8 +437,28 @@ pact_status p2p_setup(pact_comm* c, uint64_t need, cudaStream_t s) {
         p.base[r] = static_cast<char*>(p.sym);
         continue;
       }
+      const uint8_t* fr = frames.data() + (size_t)r * sizeof frame;
+      int32_t rpid = 0, rdev = 0;
+      uint64_t rraw = 0;
+      std::memcpy(&rpid, fr + 1 + sizeof h, 4);
+      std::memcpy(&rdev, fr + 5 + sizeof h, 4);
+      std::memcpy(&rraw, fr + 9 + sizeof h, 8);
+      if (rpid == pid) {  // a thread of this process on another GPU
+        int can = 0;
+        cudaDeviceCanAccessPeer(&can, mydev, rdev);
+        const cudaError_t pe = can ? cudaDeviceEnablePeerAccess(rdev, 0) : cudaErrorPeerAccessUnsupported;
+        if (pe != cudaSuccess && pe != cudaErrorPeerAccessAlreadyEnabled) {
+          cudaGetLastError();
+          opened = 0;
+          break;
+        }
+        cudaGetLastError();
+        p.base[r] = reinterpret_cast<char*>((uintptr_t)rraw);
+        p.ipc[r] = false;
+        continue;
+      }
       cudaIpcMemHandle_t hr;
-      std::memcpy(&hr, frames.data() + (size_t)r * sizeof frame + 1, sizeof hr);
+      std::memcpy(&hr, fr + 1, sizeof hr);
       void* ptr = nullptr;
       if (cudaIpcOpenMemHandle(&ptr, hr, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
         cudaGetLastError();
@@ -436,6 +466,7 @@ pact_status p2p_setup(pact_comm* c, uint64_t need, cudaStream_t s) {
         break;
       }
       p.base[r] = static_cast<char*>(ptr);
+      p.ipc[r] = true;
     }
   }
   uint8_t okb = (uint8_t)opened;
@@ -1247,54 +1278,127 @@ pact_status pact_prune_magnitude_segmented(pact_ctx* ctx, const float* w, uint64
   for (uint64_t s = 0; s < nseg; ++s)
     if (seg[s + 1] <= seg[s]) return fail(PACT_E_INVALID_VIEW, "segment %llu is empty", (unsigned long long)s);
   if (len && !w) return fail(PACT_E_INVALID_ARG, "null weights");
+  if (nseg > 0xffffffffull) return fail(PACT_E_INVALID_ARG, "too many segments");
   TRY(set_device(ctx));
   TRY(ensure_ctx_ws(ctx));
   cudaStream_t s = stream;
-  // per-segment thresholds: the global rule on each slice
-  std::vector<uint32_t> Ts(nseg);
-  std::vector<uint64_t> rs(nseg);
-  uint64_t kept = 0;
+  const uint64_t nc = out->ntiles, nw = out->nwords;
+  // host tables: per-layer drop counts and candidate regions, (layer, range)
+  // tiles of <= 64 Ki elements for the counting pass, and the layer holding
+  // each chunk's first element for the bitmap pass
+  std::vector<pactk::SegInfo> info(nseg);
+  std::vector<pactk::SegState> st0(nseg);
+  std::vector<pactk::SegTile> tiles;
+  std::vector<uint32_t> chunk_seg(std::max<uint64_t>(1, nc));
+  uint64_t kept = 0, cand_total = 0;
+  constexpr uint64_t kTileElems = 65536;
   for (uint64_t q = 0; q < nseg; ++q) {
     const uint64_t ls = seg[q + 1] - seg[q];
     const uint64_t k = drop_count_raw(ratio, ls);  // sparsity.cpp:33-40 per layer
-    if (k == 0) {  // keep all: key > 0, and every key-0 tie has rank >= 0
-      Ts[q] = 0;
-      rs[q] = 0;
-    } else if (k >= ls) {  // drop all: no key exceeds or equals T
-      Ts[q] = 0xffffffffu;
-      rs[q] = 0;
-    } else {
-      uint64_t c_lt = 0;
-      pact_prune_stats st{};
-      TRY(find_threshold(ctx, w + seg[q], ls, k, s, &Ts[q], &c_lt, &st));
-      rs[q] = k - c_lt;
-    }
+    pactk::SegInfo& I = info[q];
+    I.begin = seg[q];
+    I.end = seg[q + 1];
+    I.k = std::min(k, ls);
     kept += ls - std::min(k, ls);
+    if (k == 0) {  // keep all: key > 0, and every key-0 tie has rank >= 0
+      I.trivial = 1;
+      st0[q].T = 0;
+      st0[q].r = 0;
+    } else if (k >= ls) {  // drop all: no key exceeds T, every tie has rank < r
+      I.trivial = 2;
+      st0[q].T = 0x7fffffffu;
+      st0[q].r = ls;
+    } else {
+      // candidates: the +-6 sigma window of a 65536-key sample (~1.4% of the
+      // layer) with room to spare; an overflow falls back to an exact select
+      const uint64_t cap = ls > 65536 ? ls / 32 + 8192 : 0;
+      I.cand_off = cand_total;
+      I.cand_cap = cap;
+      cand_total += cap;
+      for (uint64_t b = seg[q]; b < seg[q + 1]; b += kTileElems)
+        tiles.push_back({(uint32_t)q, 0, b, std::min(seg[q + 1], b + kTileElems)});
+    }
   }
-  const uint64_t nw = out->nwords;
-  const size_t off_seg = 0, off_r = off_seg + (nseg + 1) * 8, off_base = off_r + nseg * 8,
-               off_T = off_base + nseg * 8, off_wt = off_T + ((nseg * 4 + 15) & ~size_t(15)),
-               off_wp = off_wt + nw * 4, total = off_wp + (nw + 1) * 4;
+  for (uint64_t c = 0, q = 0; c < nc; ++c) {
+    while (c * PACT_TILE >= seg[q + 1]) ++q;
+    chunk_seg[c] = (uint32_t)q;
+  }
+  // device workspace: [info][state][fill][chunk_seg][tiles][candidates]
+  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+  const size_t o_info = 0, o_st = o_info + al(nseg * sizeof(pactk::SegInfo)),
+               o_fill = o_st + al(nseg * sizeof(pactk::SegState)), o_cs = o_fill + al(nseg * 8),
+               o_tiles = o_cs + al(chunk_seg.size() * 4), o_cand = o_tiles + al(std::max<size_t>(1, tiles.size()) *
+                                                                                   sizeof(pactk::SegTile)),
+               total = o_cand + al(std::max<uint64_t>(1, cand_total) * 4);
   TRY(ctx->seg_ws.ensure(total));
   TRY(out->tie_words.ensure(std::max<uint64_t>(1, nw) * 8));
+  TRY(out->ties[0].ensure(std::max<uint64_t>(1, nc) * 4));
+  TRY(out->tie_prefix.ensure((nc + 1) * 4));
   char* ws = ctx->seg_ws.as<char>();
-  CUDA_TRY(cudaMemcpyAsync(ws + off_seg, seg, (nseg + 1) * 8, cudaMemcpyHostToDevice, s));
-  CUDA_TRY(cudaMemcpyAsync(ws + off_r, rs.data(), nseg * 8, cudaMemcpyHostToDevice, s));
-  CUDA_TRY(cudaMemcpyAsync(ws + off_T, Ts.data(), nseg * 4, cudaMemcpyHostToDevice, s));
-  const uint64_t* dseg = reinterpret_cast<const uint64_t*>(ws + off_seg);
-  uint32_t* wties = reinterpret_cast<uint32_t*>(ws + off_wt);
-  uint32_t* wpre = reinterpret_cast<uint32_t*>(ws + off_wp);
-  pactk::launch_prune_seg_bitmap(w, len, dseg, nseg, reinterpret_cast<const uint32_t*>(ws + off_T),
-                                 out->words, out->tie_words.as<uint64_t>(), wties, s);
-  TRY(scan(ctx, wties, nw, wpre, s));
-  pactk::launch_prune_seg_tiefix(out->words, len, out->tie_words.as<uint64_t>(), wpre, dseg, nseg,
-                                 reinterpret_cast<uint64_t*>(ws + off_base),
-                                 reinterpret_cast<const uint64_t*>(ws + off_r), s);
+  auto* d_info = reinterpret_cast<pactk::SegInfo*>(ws + o_info);
+  auto* d_st = reinterpret_cast<pactk::SegState*>(ws + o_st);
+  auto* d_fill = reinterpret_cast<unsigned long long*>(ws + o_fill);
+  auto* d_cs = reinterpret_cast<uint32_t*>(ws + o_cs);
+  auto* d_tiles = reinterpret_cast<pactk::SegTile*>(ws + o_tiles);
+  auto* d_cand = reinterpret_cast<uint32_t*>(ws + o_cand);
+  CUDA_TRY(cudaMemcpyAsync(d_info, info.data(), nseg * sizeof(pactk::SegInfo), cudaMemcpyHostToDevice, s));
+  CUDA_TRY(cudaMemcpyAsync(d_st, st0.data(), nseg * sizeof(pactk::SegState), cudaMemcpyHostToDevice, s));
+  CUDA_TRY(cudaMemsetAsync(d_fill, 0, nseg * 8, s));
+  CUDA_TRY(cudaMemcpyAsync(d_cs, chunk_seg.data(), chunk_seg.size() * 4, cudaMemcpyHostToDevice, s));
+  if (!tiles.empty())
+    CUDA_TRY(cudaMemcpyAsync(d_tiles, tiles.data(), tiles.size() * sizeof(pactk::SegTile), cudaMemcpyHostToDevice,
+                             s));
+  // (1) sampled windows, (2) one counting pass, (3) per-layer selects
+  pactk::launch_seg_sample(w, d_info, d_st, (uint32_t)nseg, s);
+  pactk::launch_seg_count(w, d_info, d_st, d_tiles, (uint32_t)tiles.size(), d_cand, d_fill, s);
+  pactk::launch_seg_select(d_info, d_st, (uint32_t)nseg, d_cand, d_fill, s);
   CUDA_TRY(cudaGetLastError());
-  TRY(refresh_offsets(out, s));
+  std::vector<pactk::SegState> hst(nseg);
+  CUDA_TRY(cudaMemcpyAsync(hst.data(), d_st, nseg * sizeof(pactk::SegState), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  // layers whose sampled window missed: the exact global select on the slice
+  bool patched = false;
+  for (uint64_t q = 0; q < nseg; ++q) {
+    if (info[q].trivial || hst[q].mode == 0) continue;
+    const uint64_t ls = info[q].end - info[q].begin;
+    uint32_t T = 0;
+    uint64_t c_lt = 0;
+    pact_prune_stats pst{};
+    TRY(find_threshold(ctx, w + info[q].begin, ls, info[q].k, s, &T, &c_lt, &pst));
+    hst[q].T = T;
+    hst[q].c_lt = c_lt;
+    hst[q].r = info[q].k - c_lt;
+    hst[q].mode = 0;
+    patched = true;
+  }
+  if (patched)
+    CUDA_TRY(cudaMemcpyAsync(d_st, hst.data(), nseg * sizeof(pactk::SegState), cudaMemcpyHostToDevice, s));
+  // (4) bitmap with ties dropped, (5) per-layer tie ranks, (6) offsets
+  uint32_t* ties = out->ties[0].as<uint32_t>();
+  pactk::launch_seg_bitmap(w, len, d_info, d_st, d_cs, out->words, out->tie_words.as<uint64_t>(), ties,
+                           out->tile_popc, s);
+  TRY(scan(ctx, ties, nc, out->tie_prefix.as<uint32_t>(), s));
+  pactk::launch_seg_tiebase(d_info, d_st, (uint32_t)nseg, out->tie_words.as<uint64_t>(), ties,
+                            out->tie_prefix.as<uint32_t>(), s);
+  pactk::launch_seg_tiefix(len, d_info, d_st, d_cs, out->words, out->tie_words.as<uint64_t>(), ties,
+                           out->tie_prefix.as<uint32_t>(), out->tile_popc, s);
+  TRY(scan(ctx, out->tile_popc, nc, out->tile_off, s));
+  uint32_t* pin32 = ctx->pin.as<uint32_t>();
+  CUDA_TRY(cudaMemcpyAsync(pin32, out->tile_off + nc, 4, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaMemcpyAsync(hst.data(), d_st, nseg * sizeof(pactk::SegState), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaStreamSynchronize(s));
+  out->nnz = pin32[0];
+  out->host_tile_off_valid = 0;
   out->changed = 1;
   out->digest_valid = 0;
   out->spec_valid = 0;
+  // every layer's threshold verified by the bitmap pass's own counts
+  for (uint64_t q = 0; q < nseg; ++q) {
+    if (info[q].trivial) continue;
+    if (hst[q].b_lt != hst[q].c_lt || !(hst[q].c_lt < info[q].k && info[q].k <= hst[q].b_lt + hst[q].b_eq))
+      return fail(PACT_E_RUN_FAILURE, "per-layer threshold inconsistent at layer %llu", (unsigned long long)q);
+  }
   if (out->nnz != kept)
     return fail(PACT_E_RUN_FAILURE, "per-layer prune kept %llu, expected %llu",
                 (unsigned long long)out->nnz, (unsigned long long)kept);

@@ -692,105 +692,7 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-// ------------------------------------------------------ per-layer (segmented)
-// Thread per mask word (64 consecutive elements): the reference rule applied
-// with each element's own segment threshold; ties provisionally dropped and
-// recorded (tie bits + per-word tie counts) for the segmented fix-up.
-__device__ __forceinline__ uint64_t seg_of(const uint64_t* seg, uint64_t nseg, uint64_t i) {
-  uint64_t lo = 0, hi = nseg;  // largest s with seg[s] <= i
-  while (hi - lo > 1) {
-    const uint64_t mid = (lo + hi) >> 1;
-    if (seg[mid] <= i) lo = mid; else hi = mid;
-  }
-  return lo;
-}
-
-__global__ void __launch_bounds__(256)
-    prune_seg_bitmap_kernel(const float* __restrict__ w, uint64_t len, const uint64_t* __restrict__ seg,
-                            uint64_t nseg, const uint32_t* __restrict__ Tseg, uint64_t* __restrict__ words,
-                            uint64_t* __restrict__ tie_words, uint32_t* __restrict__ word_ties,
-                            uint64_t nwords) {
-  const uint64_t wi = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  if (wi >= nwords) return;
-  const uint64_t e0 = wi * 64;
-  const uint64_t e1 = e0 + 64 < len ? e0 + 64 : len;
-  uint64_t s = seg_of(seg, nseg, e0);
-  uint64_t next = seg[s + 1];
-  uint32_t T = Tseg[s];
-  uint64_t keep = 0, tie = 0;
-  for (uint64_t i = e0; i < e1; ++i) {
-    while (i >= next) {
-      ++s;
-      next = seg[s + 1];
-      T = Tseg[s];
-    }
-    const uint32_t kq = mag_key(w[i]);
-    keep |= (uint64_t)(kq > T) << (i - e0);
-    tie |= (uint64_t)(kq == T) << (i - e0);
-  }
-  words[wi] = keep;
-  tie_words[wi] = tie;
-  word_ties[wi] = (uint32_t)__popcll(tie);
-}
-
-// tie rank base of each segment: ties before its first element
-__global__ void prune_seg_tiebase_kernel(const uint64_t* __restrict__ seg, uint64_t nseg,
-                                         const uint64_t* __restrict__ tie_words,
-                                         const uint32_t* __restrict__ word_prefix,
-                                         uint64_t* __restrict__ base) {
-  const uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  if (s >= nseg) return;
-  const uint64_t i = seg[s], wi = i >> 6, b = i & 63;
-  base[s] = word_prefix[wi] + (b ? (uint64_t)__popcll(tie_words[wi] & ((1ull << b) - 1ull)) : 0ull);
-}
-
-// keep tie j of segment s iff its in-segment rank >= r_s
-__global__ void __launch_bounds__(256)
-    prune_seg_tiefix_kernel(uint64_t* __restrict__ words, const uint64_t* __restrict__ tie_words,
-                            const uint32_t* __restrict__ word_prefix, const uint64_t* __restrict__ seg,
-                            uint64_t nseg, const uint64_t* __restrict__ seg_base,
-                            const uint64_t* __restrict__ rseg, uint64_t nwords) {
-  const uint64_t wi = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  if (wi >= nwords) return;
-  uint64_t tw = tie_words[wi];
-  if (!tw) return;
-  const uint64_t pre = word_prefix[wi];
-  uint64_t s = seg_of(seg, nseg, wi * 64);
-  uint64_t keep = 0, seen = 0;
-  while (tw) {
-    const int b = __ffsll((long long)tw) - 1;
-    tw &= tw - 1;
-    const uint64_t i = wi * 64 + b;
-    while (i >= seg[s + 1]) ++s;
-    if (pre + seen - seg_base[s] >= rseg[s]) keep |= 1ull << b;
-    ++seen;
-  }
-  words[wi] |= keep;
-}
-
 }  // namespace
-
-void launch_prune_seg_bitmap(const float* w, uint64_t len, const uint64_t* seg, uint64_t nseg,
-                             const uint32_t* Tseg, uint64_t* words, uint64_t* tie_words,
-                             uint32_t* word_ties, cudaStream_t s) {
-  const uint64_t nw = (len + 63) / 64;
-  if (!nw) return;
-  prune_seg_bitmap_kernel<<<(unsigned)((nw + 255) / 256), 256, 0, s>>>(w, len, seg, nseg, Tseg, words,
-                                                                       tie_words, word_ties, nw);
-  note_launch();
-}
-
-void launch_prune_seg_tiefix(uint64_t* words, uint64_t len, const uint64_t* tie_words,
-                             const uint32_t* word_prefix, const uint64_t* seg, uint64_t nseg,
-                             uint64_t* seg_base, const uint64_t* rseg, cudaStream_t s) {
-  const uint64_t nw = (len + 63) / 64;
-  if (!nw) return;
-  prune_seg_tiebase_kernel<<<(unsigned)((nseg + 255) / 256), 256, 0, s>>>(seg, nseg, tie_words,
-                                                                          word_prefix, seg_base);
-  prune_seg_tiefix_kernel<<<(unsigned)((nw + 255) / 256), 256, 0, s>>>(words, tie_words, word_prefix,
-                                                                       seg, nseg, seg_base, rseg, nw);
-  note_launch(2);
-}
 
 void launch_prune_sample(const float* w, uint64_t len, uint64_t k, PruneWindow* win_dev,
                          cudaStream_t s) {

@@ -15,6 +15,7 @@
 #include <cmath>
 #include <cstdio>
 #include <random>
+#include <string>
 #include <thread>
 #include <vector>
 
@@ -45,9 +46,13 @@ static std::vector<double> sequential_sum(const std::vector<FlatTensor>& in) {  
   return out;
 }
 
-static int g_rank = 0, g_world = 0;
+// per worker: a process (one rank each) or a thread of one process (all
+// ranks, `cluster_test threads <world> <id-file>`: the reference's own
+// SimCluster topology, every thread driving its own GPU)
+static thread_local int g_rank = 0;
+static int g_world = 0;
 static const char* g_idfile = nullptr;
-static int g_round = 0;
+static thread_local int g_round = 0;
 
 // fn(rank, comm) on the first n ranks (the others idle this round); one
 // communicator per round, its unique id passed through <id-file>.<round>
@@ -93,15 +98,35 @@ static std::vector<bool> bits_of(size_t len, size_t off_bit, bool drop_extra, si
   return b;
 }
 
+static void body();
+
 int main(int argc, char** argv) {
   if (argc < 4) {
-    std::printf("usage: cluster_test <rank> <world> <id-file>\n");
+    std::printf("usage: cluster_test <rank>|threads <world> <id-file>\n");
     return 2;
   }
-  g_rank = std::atoi(argv[1]);
   g_world = std::atoi(argv[2]);
   g_idfile = argv[3];
+  if (std::string(argv[1]) == "threads") {
+    std::vector<std::thread> th;
+    for (int r = 0; r < g_world; ++r)
+      th.emplace_back([r] {
+        g_rank = r;
+        detail::cuda(cudaSetDevice(r));
+        body();
+      });
+    for (auto& t : th) t.join();
+    std::printf("cluster_test threads x%d: %d failed check(s)\n", g_world, g_fail.load());
+    return g_fail.load();
+  }
+  g_rank = std::atoi(argv[1]);
   detail::cuda(cudaSetDevice(g_rank));
+  body();
+  std::printf("cluster_test rank %d/%d: %d failed check(s)\n", g_rank, g_world, g_fail.load());
+  return g_fail.load();
+}
+
+static void body() {
   const int ngpu = g_world;
   const int nmax = std::min(g_world, 4);
   const int r0 = g_rank;  // checks below look at this rank's own result
@@ -262,6 +287,5 @@ int main(int argc, char** argv) {
       run_workers(n, [](int, Comm&) {});
     }
   }
-  std::printf("cluster_test rank %d/%d: %d failed check(s)\n", g_rank, ngpu, g_fail.load());
-  return g_fail.load();
+  (void)ngpu;
 }

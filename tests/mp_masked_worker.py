@@ -32,11 +32,14 @@ def main():
     comm = pb.Comm.from_process_group()
     port = oracle.port()
     failures = []
+    passed = []
 
     def check(name, ok):
         if not ok:
             failures.append(name)
             print(f"[rank {rank}] FAIL {name}", flush=True)
+        else:
+            passed.append(name)
 
     rng = np.random.default_rng(1234)
     n = 300_007
@@ -242,8 +245,49 @@ def main():
     want_mode = pb.SyncMode.PackedAllReduce if dens <= pol.density_threshold else pb.SyncMode.FullAllReduce
     check("calibrate: policy decision follows the threshold", r.stats.mode_used == want_mode)
 
+    # ---- ring_allreduce in the reference's fold order (collective.cpp:165-216)
+    grads = [synth.synth_host(n, synth.grad_seed(r, 31), synth.G_FULL) for r in range(world)]
+    g = torch.from_numpy(grads[rank]).to(dev)
+    ro = pb.ring_allreduce(g, comm, exact=True)
+    check("ring_allreduce exact: == reference ring order",
+          np.array_equal(u32(ro.cpu().numpy()), u32(port.ring_allreduce(grads)[rank])))
+    try:
+        pb.ring_allreduce(g[: n - (rank == 0)], comm, exact=True)
+        check("ring_allreduce: length mismatch raises", False)
+    except pb.Error as e:
+        check("ring_allreduce: length mismatch raises", e.code == pb.Errc.ShapeMismatch)
+
+    # ---- BASELINE size: C2 (ResNet-50 shape, 25,557,032, 80%) on the
+    # device-pruned global mask, full-mantissa gradients, both transports
+    shape = synth.model_shape("resnet50")
+    nb = shape.total
+    wd = synth.weights_device(shape, 1234, synth.W_REAL, device=dev)
+    mb = pb.magnitude_prune(wd, 0.8)
+    wb = mb.words_host()
+    check("C2: nnz", mb.nnz() == 5_111_404)
+    check("C2: mask == oracle prune", np.array_equal(wb, port.magnitude_prune(wd.cpu().numpy(), 0.8)))
+    gradsb = [port.gse(synth.synth_host(nb, synth.grad_seed(r, 41), synth.G_FULL), wb) for r in range(world)]
+    outsb, modesb, bytsb = port.masked_allreduce(gradsb, [wb] * world, [1] * world, 2)
+    gb = torch.from_numpy(gradsb[rank]).to(dev)
+    sumabs = sum(np.abs(x) for x in gradsb)
+    for transport, tname in ((pb.SyncPolicy.NCCL, "nccl"), (pb.SyncPolicy.P2P, "p2p"), (pb.SyncPolicy.AUTO, "auto")):
+        rb = pb.masked_allreduce(gb, mb, pb.TrackerStatus.Stable, 2, comm, policy=pb.SyncPolicy(transport=transport))
+        got = rb.tensor.cpu().numpy()
+        check(f"C2/{tname}: packed", rb.stats.mode_used == pb.SyncMode.PackedAllReduce and modesb[rank] == 1)
+        check(f"C2/{tname}: bytes_on_wire", rb.stats.bytes_on_wire == bytsb[rank])
+        if world == 2 or rb.stats.transport == pb.SyncPolicy.P2P:
+            check(f"C2/{tname}: bit-exact", np.array_equal(u32(got), u32(outsb[rank])))
+        else:
+            tol = 1e-6 * np.maximum(sumabs, 2.0 ** -126)
+            check(f"C2/{tname}: within 1e-6*sum|x|", bool(np.all(np.abs(got - outsb[rank]) <= tol)))
+    del wd, gb
+
     flag = torch.tensor([len(failures)], device=dev)
     dist.all_reduce(flag)
+    if rank == 0:
+        print(f"mp_masked_worker world={world} checks passed on rank 0: {len(passed)}", flush=True)
+        for nm in passed:
+            print(f"  ok {nm}", flush=True)
     comm.close()
     dist.destroy_process_group()
     if rank == 0:

@@ -65,6 +65,27 @@ def test_reference_collective_assertions_multi_gpu(pb, cuda):
 
 
 @pytest.mark.gpu
+def test_reference_collective_assertions_threaded_multi_gpu(pb, cuda):
+    """The same assertions with every worker a THREAD of one process driving
+    its own GPU -- the reference's own SimCluster topology (SURVEY 8(b)
+    "Threading"): NCCL communicators per thread, NVLink peer access instead
+    of CUDA IPC between the threads."""
+    import tempfile
+
+    import torch
+
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs >= 2 GPUs (run with gpurun --gpus 2)")
+    exe = _build(pb, CLUSTER_SRC, CLUSTER_OUT)
+    world = min(torch.cuda.device_count(), 4)
+    with tempfile.TemporaryDirectory() as d:
+        r = subprocess.run([exe, "threads", str(world), os.path.join(d, "ncclid")], capture_output=True,
+                           text=True, timeout=600)
+    print(r.stdout[-3000:], r.stderr[-2000:])
+    assert r.returncode == 0, r.stdout[-3000:]
+
+
+@pytest.mark.gpu
 def test_reference_unit_assertions_on_gpu(pb, cuda):
     exe = _build(pb)
     r = subprocess.run([exe], capture_output=True, text=True, timeout=300)

@@ -617,6 +617,25 @@ def test_per_layer_prune_model_shapes(pb, port, cuda):
         assert m.digest() == port.mask_digest(ref, shape.total)
 
 
+@pytest.mark.parametrize("model", ["gpt2-medium", "bert-base"])
+def test_per_layer_prune_full_size(pb, port, cuda, model):
+    """Per-layer mode (north_star (1)) at C5 / C4 size: every
+    layer's own k-th threshold, words bit-exact against the oracle applied to
+    each layer slice, both weight recipes."""
+    from paper_2505_18563_b200 import synth
+
+    shape = synth.model_shape(model)
+    offs = shape.offsets()
+    for recipe in (synth.W_REAL, synth.W_TIES):
+        wd = synth.weights_device(shape, 61 + recipe, recipe)
+        m = pb.magnitude_prune_per_layer(wd, offs, 0.9)
+        ref = port.magnitude_prune_segmented(wd.cpu().numpy(), np.array(offs, np.uint64), 0.9)
+        assert np.array_equal(m.words_host(), ref), (model, recipe)
+        assert m.nnz() == port.mask_nnz(ref, shape.total)
+        del wd, m
+        torch.cuda.empty_cache()
+
+
 def test_per_layer_prune_errors(pb, cuda):
     x = dev(np.ones(100, np.float32))
     for bad in ([0, 50], [0, 50, 50, 100], [1, 100]):

@@ -106,3 +106,34 @@ def test_nccl_masked_allreduce_multi_gpu(pb):
         r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
         print(r.stdout[-4000:], r.stderr[-4000:])
         assert r.returncode == 0, str(extra) + r.stdout[-2000:] + r.stderr[-2000:]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("transport", ["nccl", "p2p"])
+def test_fail_fast_link_error_multi_gpu(pb, transport):
+    """A rank killed mid-step: the survivor gets LinkError within the link
+    timeout and the comm stays poisoned (reference SimCluster::poison,
+    collective.cpp:430-458; trainer.cpp:416-437)."""
+    import tempfile
+
+    import torch
+
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs >= 2 GPUs (run with gpurun --gpus 2)")
+    env = dict(os.environ, PACT_LINK_TIMEOUT_MS="4000")
+    with tempfile.TemporaryDirectory() as d:
+        idf = os.path.join(d, "id")
+        procs = [subprocess.Popen([sys.executable, os.path.join(ROOT, "tests", "mp_failfast_worker.py"), str(r), "2",
+                                   idf, transport], stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True,
+                                  env=env, cwd=ROOT) for r in range(2)]
+        try:
+            out0, _ = procs[0].communicate(timeout=240)
+            procs[1].wait(timeout=60)
+        finally:
+            for p in procs:
+                if p.poll() is None:
+                    p.kill()
+        print(out0)
+        assert procs[0].returncode == 0, out0
+        assert "fail-fast ok" in out0
+        assert procs[1].returncode == -9  # the killed rank
