@@ -25,6 +25,7 @@
 // per chunk at 65% issue utilisation and 33% of DRAM peak).
 #include <cstdlib>
 
+#include <algorithm>
 #include <atomic>
 
 #include "common.cuh"
@@ -785,11 +786,12 @@ void pair_trace_read(unsigned long long out[5], cudaStream_t s) {
 void note_launch(uint64_t n) { g_launches += n; }
 
 void launch_pack(const float* g, uint64_t len, const uint64_t* words, const uint32_t* chunk_off,
-                 float* packed, uint64_t cb, uint64_t ce, cudaStream_t s, bool pdl_trigger) {
+                 float* packed, uint64_t cb, uint64_t ce, cudaStream_t s, bool pdl_trigger, float grid_frac) {
   if (ce <= cb) return;
   static int cap = 0;
   if (!cap) cap = persistent_grid(pack_lm_kernel<kPushNone>, kPuWarps);
-  pack_lm_kernel<kPushNone><<<grid_for(cap, ce - cb, kPuWarps), kPuWarps * 32, 0, s>>>(
+  const int c = grid_frac > 0.f ? std::max(1, (int)(cap * grid_frac)) : cap;
+  pack_lm_kernel<kPushNone><<<grid_for(c, ce - cb, kPuWarps), kPuWarps * 32, 0, s>>>(
       g, len, words, chunk_off, packed, cb, ce, nullptr, P2PView{}, P2PSig{}, pdl_trigger ? 1 : 0);
   note_launch();
 }
@@ -821,7 +823,7 @@ constexpr uint64_t kDeepUnpackChunksPerWarp = 16;
 template <bool kSgd>
 void unpack_local(const float* packed, uint64_t len, const uint64_t* words, const uint32_t* chunk_off, float scale,
                   int do_scale, float* out, float lr, float* weights, uint64_t cb, uint64_t ce, cudaStream_t s,
-                  bool pdl = false) {
+                  bool pdl = false, float grid_frac = 0.f) {
   constexpr int kDyn1 = unpack_smem_bytes<kSrcLocal, 1>(), kDyn2 = unpack_smem_bytes<kSrcLocal, 2>();
   static DeviceCache<int> c1c, c2c;  // dyn-smem opt-ins are per device
   int& cap1 = c1c.get();
@@ -831,8 +833,10 @@ void unpack_local(const float* packed, uint64_t len, const uint64_t* words, cons
     cap2 = persistent_grid_dyn(unpack_kernel<kSgd, kSrcLocal, 2>, kPuWarps, kDyn2);
   }
   const bool deep = (ce - cb) >= kDeepUnpackChunksPerWarp * (uint64_t)cap1 * kPuWarps;
+  const int cb_ = deep ? cap2 : cap1;
+  const int c = grid_frac > 0.f ? std::max(1, (int)(cb_ * grid_frac)) : cb_;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid_for(deep ? cap2 : cap1, ce - cb, kPuWarps));
+  cfg.gridDim = dim3(grid_for(c, ce - cb, kPuWarps));
   cfg.blockDim = dim3(kPuWarps * 32);
   cfg.dynamicSmemBytes = deep ? kDyn2 : kDyn1;
   cfg.stream = s;
@@ -858,9 +862,9 @@ void unpack_local(const float* packed, uint64_t len, const uint64_t* words, cons
 
 void launch_unpack(const float* packed, uint64_t len, const uint64_t* words,
                    const uint32_t* chunk_off, float scale, int do_scale, float* out, uint64_t cb,
-                   uint64_t ce, cudaStream_t s, bool pdl) {
+                   uint64_t ce, cudaStream_t s, bool pdl, float grid_frac) {
   if (ce <= cb) return;
-  unpack_local<false>(packed, len, words, chunk_off, scale, do_scale, out, 0.f, nullptr, cb, ce, s, pdl);
+  unpack_local<false>(packed, len, words, chunk_off, scale, do_scale, out, 0.f, nullptr, cb, ce, s, pdl, grid_frac);
   note_launch();
 }
 

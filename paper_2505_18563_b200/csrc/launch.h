@@ -46,8 +46,11 @@ void pair_trace_reset(cudaStream_t s);
 void pair_trace_read(unsigned long long out[5], cudaStream_t s);
 // chunk range [cb, ce) of 1024-element chunks; all pointers device.
 // pdl_trigger: let a programmatic dependent (launch_unpack(..., pdl)) start early
+// grid_frac > 0: at most that fraction of the persistent grid (bucket
+// pipelines leave SMs to the exchange on the other streams)
 void launch_pack(const float* g, uint64_t len, const uint64_t* words, const uint32_t* chunk_off,
-                 float* packed, uint64_t cb, uint64_t ce, cudaStream_t s, bool pdl_trigger = false);
+                 float* packed, uint64_t cb, uint64_t ce, cudaStream_t s, bool pdl_trigger = false,
+                 float grid_frac = 0.f);
 // pack into `packed` and, with the same offsets, into `remote` (the peer's
 // incoming region, NVLink stores); the last CTA publishes sg's exit flag
 void launch_pack_push(const float* g, uint64_t len, const uint64_t* words, const uint32_t* chunk_off,
@@ -58,7 +61,7 @@ void launch_pack_push(const float* g, uint64_t len, const uint64_t* words, const
 // (griddepcontrol.wait) before touching the packed runs
 void launch_unpack(const float* packed, uint64_t len, const uint64_t* words,
                    const uint32_t* chunk_off, float scale, int do_scale, float* out, uint64_t cb,
-                   uint64_t ce, cudaStream_t s, bool pdl = false);
+                   uint64_t ce, cudaStream_t s, bool pdl = false, float grid_frac = 0.f);
 // unpack with the exchange fused in (NVLink P2P, B == 1): one-shot (n == 2)
 // sums the local and the peer's packed runs (waits PACKED); two-shot reads
 // each run from its owner's reduced chunk (waits REDUCED; needs C >= 1024).

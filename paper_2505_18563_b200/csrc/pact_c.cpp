@@ -344,6 +344,15 @@ uint64_t link_timeout_ms() {
   return ms;
 }
 
+// bucketed pipelines: fraction of the persistent pack/unpack grids they
+// may take, so pack(b+1), the exchange of b and unpack(b-1) run at once
+// (PACT_BUCKET_GRID_FRAC, read per call for sweeps)
+float bucket_grid_frac() {
+  const char* e = getenv("PACT_BUCKET_GRID_FRAC");
+  const float f = e ? (float)atof(e) : 0.75f;
+  return f > 0.f && f <= 1.f ? f : 0.75f;
+}
+
 uint64_t drop_count_raw(float ratio, uint64_t len) {  // sparsity.cpp:38-39
   return (uint64_t)std::floor((double)ratio * (double)len + (double)len * 1e-7);
 }
@@ -2176,7 +2185,21 @@ pact_status pact_masked_allreduce(pact_comm* c, pact_ctx* ctx, const float* grad
   // P2P two-shot 148 us). PACT_TRANSPORT_P2P forces the bit-exact
   // reference-order fold at any n.
   const uint64_t pbytes = m->nnz * 4;
-  const bool auto_p2p = c && n == 2 && pbytes <= (1ull << 30);
+  // AUTO bucketing (B200 x2 / x4, tools/bucket_sweep.py, step us single vs
+  // bucketed NCCL with 0.75 codec grids): medium and large packed vectors
+  // pipeline pack(b+1) / allreduce(b) / unpack(b-1) in EQUAL-CHUNK buckets
+  // -- c3 (28.7 MB) 3 buckets: n=4 257 -> 233, n=2 263 (P2P) -> 237;
+  // c5 (142 MB) 2 buckets: n=4 841 -> 682, n=2 742 (P2P) -> 681; c4 (219 MB)
+  // 3 buckets: n=4 752 -> 675 -- except n = 2 above 160 MB, where the P2P
+  // push (c4 535 us) wins; under 24 MB one bucket (c2: every split loses)
+  constexpr uint64_t kMiB = 1ull << 20;
+  uint64_t auto_bb = 0;
+  if (c && !f16 && pol.transport == PACT_TRANSPORT_AUTO && pol.bucket_bytes == 0 && pbytes >= 24 * kMiB &&
+      !(n == 2 && pbytes > 160 * kMiB)) {
+    const uint64_t B = pbytes < 96 * kMiB ? 3 : std::max<uint64_t>(2, (pbytes + 36 * kMiB) / (72 * kMiB));
+    auto_bb = (pbytes + B - 1) / B;
+  }
+  const bool auto_p2p = c && n == 2 && pbytes <= (1ull << 30) && auto_bb == 0;
   const bool p2p_try = c && m->nnz && n <= pactk::kP2PMaxRanks && !f16 &&
                        (pol.transport == PACT_TRANSPORT_P2P || (pol.transport == PACT_TRANSPORT_AUTO && auto_p2p));
   const bool p2p_ready = p2p_try && c->p2p.ok && c->p2p.cap >= m->nnz;
@@ -2186,16 +2209,17 @@ pact_status pact_masked_allreduce(pact_comm* c, pact_ctx* ctx, const float* grad
   // pack in this mode: PACKED is published by the pack itself.
   static const bool push_env = !getenv("PACT_P2P_PULL");
   const bool p2p_push = push_env && p2p_try && n == 2 && !p2p_buckets;
-  // NCCL buckets: bucket_bytes, or auto (0): ONE bucket. Bucketed pipelines
-  // lose on B200: the persistent pack/unpack grids hold every SM, so the
-  // NCCL kernels of bucket b wait behind pack(b+1) / unpack(b-1) instead of
-  // overlapping them (B200 x2/x4, bench.py, step ms, 32 MiB buckets vs one
-  // bucket: c4 n=2 0.886 vs 0.668, n=4 1.081 vs 0.754; c5 n=2 1.047 vs 1.097,
-  // n=4 1.245 vs 1.125). The single bucket sits on the NCCL symmetric window
-  // (its low-latency kernels: c2 n=4 111 -> 70 us exchange), except at n = 2
-  // above 64 MiB packed, where the ring on a plain buffer is faster (c4
-  // 0.668 vs 0.796 ms, c5 1.097 vs 1.166 ms).
-  const uint64_t nccl_bb = pol.bucket_bytes;
+  // NCCL buckets: bucket_bytes, or the AUTO choice above. Round 1 measured
+  // bucketing losing (32 MiB buckets cut by packed bytes on full codec
+  // grids: c4 n=2 0.886 vs 0.668 ms): the persistent pack/unpack grids held
+  // every SM, so the allreduce of bucket b queued behind pack(b+1) /
+  // unpack(b-1), the byte cuts put VGG-19's dense classifier in one bucket,
+  // and the buckets ran NCCL's LL ring on a plain buffer. Now the codec
+  // grids take 3/4 of the SMs, cuts are equal chunk ranges and every bucket
+  // allreduces a slice of the NCCL symmetric window (its NVLS kernels),
+  // except at n = 2 above 64 MiB packed, where the ring on a plain buffer is
+  // faster (c4 0.668 vs 0.796 ms, c5 1.097 vs 1.166 ms).
+  const uint64_t nccl_bb = pol.bucket_bytes ? pol.bucket_bytes : auto_bb;
   const bool buckets = c && !p2p_try && !f16 && nccl_bb > 0 && m->nnz * 4 > nccl_bb;
   const bool nccl_sym_ok = c && !(n == 2 && pbytes > (64ull << 20));
   if (buckets) TRY(mirror_tile_off(m, s));
@@ -2378,8 +2402,10 @@ pact_status pact_masked_allreduce(pact_comm* c, pact_ctx* ctx, const float* grad
     CUDA_TRY(cudaEventRecord(e_start, s));
     CUDA_TRY(cudaStreamWaitEvent(ctx->aux[0], e_start, 0));
     CUDA_TRY(cudaStreamWaitEvent(ctx->aux[1], e_start, 0));
+    const float gfrac = bucket_grid_frac();
     for (int b = 0; b < B; ++b) {
-      if (!packed_in_sym) pactk::launch_pack(grad, len, m->words, m->tile_off, mine, cuts[b], cuts[b + 1], s);
+      if (!packed_in_sym)
+        pactk::launch_pack(grad, len, m->words, m->tile_off, mine, cuts[b], cuts[b + 1], s, false, gfrac);
       CUDA_TRY(cudaEventRecord(pool_event(ctx, 1 + b), s));
     }
     mark(0);
@@ -2418,7 +2444,7 @@ pact_status pact_masked_allreduce(pact_comm* c, pact_ctx* ctx, const float* grad
     for (int b = 0; b < B; ++b) {
       CUDA_TRY(cudaStreamWaitEvent(ctx->aux[1], pool_event(ctx, 1 + B + b), 0));
       pactk::launch_unpack(packed, len, m->words, m->tile_off, scale, scale != 1.0f, out, cuts[b],
-                           cuts[b + 1], ctx->aux[1]);
+                           cuts[b + 1], ctx->aux[1], false, gfrac);
     }
     CUDA_TRY(cudaEventRecord(pool_event(ctx, 2 + 2 * B), ctx->aux[1]));
     CUDA_TRY(cudaStreamWaitEvent(s, pool_event(ctx, 1 + 2 * B), 0));
@@ -2438,7 +2464,7 @@ pact_status pact_masked_allreduce(pact_comm* c, pact_ctx* ctx, const float* grad
     // setup). Measured (bench.py, NCCL transport): c2 n=4 115 vs 158 us, n=2
     // 118 vs 117 us; the bucketed pipeline is faster on plain buffers (c5 n=4
     // 1.12 vs 1.30 ms), so buckets keep ctx->packed.
-    if (c && !f16 && !buckets && nccl_sym_ok) {
+    if (c && !f16 && nccl_sym_ok) {  // buckets allreduce slices of the same window
       float* symp = nullptr;
       TRY(nccl_sym_packed(c, m->nnz * 4, s, &symp));
       if (symp && symp != packed) {
@@ -2465,8 +2491,18 @@ pact_status pact_masked_allreduce(pact_comm* c, pact_ctx* ctx, const float* grad
       // tile-aligned buckets of ~bucket_bytes packed; pack on s, NCCL on
       // aux[0], unpack on aux[1], chained by events
       const std::vector<uint32_t>& off = m->host_tile_off;
-      const std::vector<uint64_t> cuts = bucket_cuts(off, m->ntiles, nccl_bb / 4, 256);
-      nbuckets = (int)cuts.size() - 1;
+      // B = ceil(packed bytes / bucket_bytes) buckets of EQUAL chunk counts:
+      // pack and unpack cost HBM bytes of the dense range, so even ranges
+      // keep the three pipeline stages balanced (cuts by packed bytes gave
+      // VGG-19's dense classifier one bucket and the rest another)
+      const uint64_t B = std::min<uint64_t>(std::max<uint64_t>(1, (m->nnz * 4 + nccl_bb - 1) / nccl_bb),
+                                            std::min<uint64_t>(256, m->ntiles));
+      std::vector<uint64_t> cuts(B + 1);
+      for (uint64_t b = 0; b <= B; ++b) cuts[b] = m->ntiles * b / B;
+      nbuckets = (int)B;
+      // pack(b+1), the NCCL allreduce of b and unpack(b-1) run at once: the
+      // codec grids leave part of every SM to the other two
+      const float gfrac = bucket_grid_frac();
       cudaEvent_t start = pool_event(ctx, 0);
       CUDA_TRY(cudaEventRecord(start, s));
       CUDA_TRY(cudaStreamWaitEvent(ctx->aux[1], start, 0));
@@ -2474,7 +2510,7 @@ pact_status pact_masked_allreduce(pact_comm* c, pact_ctx* ctx, const float* grad
         const uint64_t tb = cuts[b], te = cuts[b + 1];
         const uint64_t o0 = off[tb], cnt = off[te] - off[tb];
         cudaEvent_t e_pack = pool_event(ctx, 1 + 2 * b), e_ar = pool_event(ctx, 2 + 2 * b);
-        pactk::launch_pack(grad, len, m->words, m->tile_off, packed, tb, te, s);
+        pactk::launch_pack(grad, len, m->words, m->tile_off, packed, tb, te, s, false, gfrac);
         CUDA_TRY(cudaEventRecord(e_pack, s));
         CUDA_TRY(cudaStreamWaitEvent(ctx->aux[0], e_pack, 0));
         if (cnt)
@@ -2483,7 +2519,7 @@ pact_status pact_masked_allreduce(pact_comm* c, pact_ctx* ctx, const float* grad
         CUDA_TRY(cudaEventRecord(e_ar, ctx->aux[0]));
         CUDA_TRY(cudaStreamWaitEvent(ctx->aux[1], e_ar, 0));
         pactk::launch_unpack(packed, len, m->words, m->tile_off, scale, scale != 1.0f, out, tb, te,
-                             ctx->aux[1]);
+                             ctx->aux[1], false, gfrac);
       }
       cudaEvent_t done = pool_event(ctx, 1 + 2 * nbuckets);
       CUDA_TRY(cudaEventRecord(done, ctx->aux[1]));
