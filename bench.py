@@ -106,6 +106,9 @@ class ClockSampler:
         self.reasons = 0
         self._stop = threading.Event()
         self.ok = False
+        if os.environ.get("PACT_BENCH_NO_NVML"):  # A/B: host-side interference of the sampler
+            self.max_mhz = None
+            return
         try:
             import pynvml
 
@@ -378,8 +381,8 @@ def main():
         comm = pb.Comm.from_process_group()
 
     model, ratio, reprune, bucket = CONFIGS[cfg]
-    if args.bucket_mb is not None:
-        bucket = int(args.bucket_mb * (1 << 20))
+    if args.bucket_mb is not None:  # < 0: one bucket whatever the size (AUTO may pick several)
+        bucket = int(args.bucket_mb * (1 << 20)) if args.bucket_mb >= 0 else (1 << 62)
     shape = synth.model_shape(model)
     n = shape.total
     ctx = pb.Context.get(local)

@@ -7,6 +7,7 @@
 // control decisions (drop count, vote rule, byte accounting, tracker).
 #include "pact_c.h"
 
+#include <cuda.h>  // green-context types (entry points fetched at run time, no libcuda link)
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -127,8 +128,22 @@ uint64_t tile_count(uint64_t len) { return (len + kTile - 1) / kTile; }
 
 }  // namespace
 
+namespace {
+// SM partition of the device for the bucketed pipeline (CUDA green
+// contexts): the exchange's NCCL kernels run on their own SMs, pack and
+// unpack on the rest, so pack(b+1) / allreduce(b) / unpack(b-1) cannot
+// starve each other of SM slots (measured: with shared SMs a persistent
+// pack grid and NCCL's symmetric kernel convoyed, 25 -> 130 us each).
+struct GreenSet {
+  int state = 0;  // 0 not tried, 1 ready, -1 unavailable
+  int nccl_sms = 0, codec_sms = 0;
+  cudaStream_t nccl = nullptr, pack = nullptr, unpack = nullptr;
+};
+}  // namespace
+
 struct pact_ctx {
   int device = 0;
+  GreenSet green;
   DevBuf ws_small;  // PruneWindow | PruneCounts | hist[2048] | digest out | changed flag
   DevBuf cand;      // prune candidates (u32 keys)
   DevBuf state;     // look-back tile states + counter
@@ -266,6 +281,88 @@ pact_status ensure_ctx_ws(pact_ctx* ctx) {
   return PACT_OK;
 }
 
+// PACT_GREEN=0 disables; PACT_NCCL_SMS (default 16) SMs for the exchange
+GreenSet* green_setup(pact_ctx* ctx, unsigned want, const char** why);
+// the partition is made on first use: PACT_NCCL_SMS, else 16 SMs for the
+// exchange at n = 2 and 8 above (tools/bucket_sweep.py green2)
+GreenSet* green_streams(pact_ctx* ctx, int n) {
+  GreenSet& g = ctx->green;
+  if (g.state) return g.state > 0 ? &g : nullptr;
+  const char* why = "";
+  const char* ns = getenv("PACT_NCCL_SMS");
+  GreenSet* r = green_setup(ctx, ns ? (unsigned)atoi(ns) : (n == 2 ? 16u : 8u), &why);
+  if (getenv("PACT_DEBUG"))
+    fprintf(stderr, "[pact] green contexts: %s (nccl %d SMs, codec %d SMs)\n", r ? "on" : why, g.nccl_sms,
+            g.codec_sms);
+  return r;
+}
+GreenSet* green_setup(pact_ctx* ctx, unsigned want, const char** why) {
+  GreenSet& g = ctx->green;
+  g.state = -1;
+  const char* en = getenv("PACT_GREEN");
+  if (en && en[0] == '0') {
+    *why = "disabled (PACT_GREEN=0)";
+    return nullptr;
+  }
+  using GetRes = CUresult (*)(CUdevice, CUdevResource*, CUdevResourceType);
+  using Split = CUresult (*)(CUdevResource*, unsigned*, const CUdevResource*, CUdevResource*, unsigned, unsigned);
+  using GenDesc = CUresult (*)(CUdevResourceDesc*, CUdevResource*, unsigned);
+  using Create = CUresult (*)(CUgreenCtx*, CUdevResourceDesc, CUdevice, unsigned);
+  using StreamCreate = CUresult (*)(CUstream*, CUgreenCtx, unsigned, int);
+  void* f[5] = {};
+  const char* names[5] = {"cuDeviceGetDevResource", "cuDevSmResourceSplitByCount", "cuDevResourceGenerateDesc",
+                          "cuGreenCtxCreate", "cuGreenCtxStreamCreate"};
+  for (int i = 0; i < 5; ++i) {
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion(names[i], &f[i], 12080, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !f[i]) {
+      cudaGetLastError();
+      *why = names[i];
+      return nullptr;
+    }
+  }
+  CUdevResource all{}, grp{}, rest{};
+  unsigned nb = 1;
+  CUresult cr = ((GetRes)f[0])((CUdevice)ctx->device, &all, CU_DEV_RESOURCE_TYPE_SM);
+  if (cr != CUDA_SUCCESS) {
+    *why = "cuDeviceGetDevResource failed";
+    return nullptr;
+  }
+  cr = ((Split)f[1])(&grp, &nb, &all, &rest, 0, want);
+  if (cr != CUDA_SUCCESS || nb != 1) {
+    *why = "cuDevSmResourceSplitByCount failed";
+    return nullptr;
+  }
+  CUdevResourceDesc d1, d2;
+  CUgreenCtx g1, g2;
+  if (((GenDesc)f[2])(&d1, &grp, 1) != CUDA_SUCCESS || ((GenDesc)f[2])(&d2, &rest, 1) != CUDA_SUCCESS) {
+    *why = "cuDevResourceGenerateDesc failed";
+    return nullptr;
+  }
+  if (((Create)f[3])(&g1, d1, (CUdevice)ctx->device, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS ||
+      ((Create)f[3])(&g2, d2, (CUdevice)ctx->device, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS) {
+    *why = "cuGreenCtxCreate failed";
+    return nullptr;
+  }
+  CUstream a, b, c;
+  static char msg[96];
+  CUresult e1 = ((StreamCreate)f[4])(&a, g1, CU_STREAM_NON_BLOCKING, 0);
+  CUresult e2 = e1 == CUDA_SUCCESS ? ((StreamCreate)f[4])(&b, g2, CU_STREAM_NON_BLOCKING, 0) : e1;
+  CUresult e3 = e2 == CUDA_SUCCESS ? ((StreamCreate)f[4])(&c, g2, CU_STREAM_NON_BLOCKING, 0) : e2;
+  if (e3 != CUDA_SUCCESS) {
+    snprintf(msg, sizeof msg, "cuGreenCtxStreamCreate failed (CUresult %d)", (int)e3);
+    *why = msg;
+    return nullptr;
+  }
+  g.nccl = (cudaStream_t)a;
+  g.pack = (cudaStream_t)b;
+  g.unpack = (cudaStream_t)c;
+  g.nccl_sms = (int)grp.sm.smCount;
+  g.codec_sms = (int)rest.sm.smCount;
+  g.state = 1;
+  return &g;
+}
+
 cudaEvent_t pool_event(pact_ctx* ctx, size_t i) {
   while (ctx->ev_pool.size() <= i) {
     cudaEvent_t e;
@@ -347,10 +444,10 @@ uint64_t link_timeout_ms() {
 // bucketed pipelines: fraction of the persistent pack/unpack grids they
 // may take, so pack(b+1), the exchange of b and unpack(b-1) run at once
 // (PACT_BUCKET_GRID_FRAC, read per call for sweeps)
-float bucket_grid_frac() {
+float bucket_grid_frac(float dflt) {
   const char* e = getenv("PACT_BUCKET_GRID_FRAC");
-  const float f = e ? (float)atof(e) : 0.75f;
-  return f > 0.f && f <= 1.f ? f : 0.75f;
+  const float f = e ? (float)atof(e) : dflt;
+  return f > 0.f && f <= 1.f ? f : dflt;
 }
 
 uint64_t drop_count_raw(float ratio, uint64_t len) {  // sparsity.cpp:38-39
@@ -2185,18 +2282,20 @@ pact_status pact_masked_allreduce(pact_comm* c, pact_ctx* ctx, const float* grad
   // P2P two-shot 148 us). PACT_TRANSPORT_P2P forces the bit-exact
   // reference-order fold at any n.
   const uint64_t pbytes = m->nnz * 4;
-  // AUTO bucketing (B200 x2 / x4, tools/bucket_sweep.py, step us single vs
-  // bucketed NCCL with 0.75 codec grids): medium and large packed vectors
-  // pipeline pack(b+1) / allreduce(b) / unpack(b-1) in EQUAL-CHUNK buckets
-  // -- c3 (28.7 MB) 3 buckets: n=4 257 -> 233, n=2 263 (P2P) -> 237;
-  // c5 (142 MB) 2 buckets: n=4 841 -> 682, n=2 742 (P2P) -> 681; c4 (219 MB)
-  // 3 buckets: n=4 752 -> 675 -- except n = 2 above 160 MB, where the P2P
-  // push (c4 535 us) wins; under 24 MB one bucket (c2: every split loses)
+  // AUTO bucketing (B200 x2 / x4, tools/bucket_sweep.py green2, host
+  // running ahead as in a training loop, step us): from 24 MB packed the
+  // step pipelines pack(b+1) / allreduce(b) / unpack(b-1) in equal-chunk
+  // buckets on an SM partition (NCCL 8 SMs at n > 2, 16 at n = 2) --
+  // n=4: c3 (28.7 MB) 3 buckets 257 -> 228, c4 (219 MB) 4 buckets 748 ->
+  // 659, c5 (142 MB) 4 buckets 840 -> 658; n=2: c3 3 buckets 261 (P2P) ->
+  // 236. At n = 2 above 64 MB packed NCCL runs its ring on a plain buffer,
+  // which needs more SMs than the partition leaves it: the P2P push stays
+  // (c4 527 us, c5 735 us). Under 24 MB one bucket (c2: every split loses).
   constexpr uint64_t kMiB = 1ull << 20;
   uint64_t auto_bb = 0;
   if (c && !f16 && pol.transport == PACT_TRANSPORT_AUTO && pol.bucket_bytes == 0 && pbytes >= 24 * kMiB &&
-      !(n == 2 && pbytes > 160 * kMiB)) {
-    const uint64_t B = pbytes < 96 * kMiB ? 3 : std::max<uint64_t>(2, (pbytes + 36 * kMiB) / (72 * kMiB));
+      (n > 2 || pbytes <= 64 * kMiB)) {
+    const uint64_t B = pbytes < 96 * kMiB ? 3 : 4;
     auto_bb = (pbytes + B - 1) / B;
   }
   const bool auto_p2p = c && n == 2 && pbytes <= (1ull << 30) && auto_bb == 0;
@@ -2226,6 +2325,24 @@ pact_status pact_masked_allreduce(pact_comm* c, pact_ctx* ctx, const float* grad
 
   int agree = 0;
   bool packed_issued = false, packed_in_sym = false;
+  // NCCL buckets: equal chunk ranges, B = ceil(packed bytes / bucket bytes)
+  // (pack and unpack cost the HBM bytes of the dense range, so even ranges
+  // keep the pipeline stages balanced; cuts by packed bytes gave VGG-19's
+  // dense classifier a bucket of its own)
+  std::vector<uint64_t> bcuts;
+  if (buckets) {
+    const uint64_t B = std::min<uint64_t>(std::max<uint64_t>(1, (m->nnz * 4 + nccl_bb - 1) / nccl_bb),
+                                          std::min<uint64_t>(256, m->ntiles));
+    bcuts.resize(B + 1);
+    for (uint64_t b = 0; b <= B; ++b) bcuts[b] = m->ntiles * b / B;
+  }
+  // bucketed pipelines run on an SM partition (green contexts) when the
+  // driver offers one: NCCL on its own SMs, pack / unpack on the rest
+  GreenSet* gr = buckets ? green_streams(ctx, n) : nullptr;
+  const cudaStream_t sp = gr ? gr->pack : s, sx = gr ? gr->nccl : ctx->aux[0], su = gr ? gr->unpack : ctx->aux[1];
+  const float gfrac = gr ? bucket_grid_frac(1.0f) * (float)gr->codec_sms / (float)sm_count_host()
+                        : bucket_grid_frac(0.75f);
+  bool bpacks_issued = false;
   if (c) {
     // speculative pack overlaps the vote (single-bucket plans): enqueued
     // first so the GPU starts while the host votes; unused on a fallback
@@ -2246,6 +2363,21 @@ pact_status pact_masked_allreduce(pact_comm* c, pact_ctx* ctx, const float* grad
         packed_issued = true;
       }
       mark(0);
+    }
+    // bucketed plans: every bucket's pack goes ahead of the vote too (into
+    // the symmetric window registered by an earlier agreed step), so a late
+    // peer at the vote board does not leave this GPU idle (measured c3 n=4:
+    // the 3-bucket step read 314 us in the bench loop without it, 229 us with
+    // the host already waiting)
+    if (stable && buckets && !f16 && m->nnz && nccl_sym_ok && c->sym && c->sym_bytes >= m->nnz * 4) {
+      packed = static_cast<float*>(c->sym);
+      CUDA_TRY(cudaEventRecord(pool_event(ctx, 0), s));
+      if (sp != s) CUDA_TRY(cudaStreamWaitEvent(sp, pool_event(ctx, 0), 0));
+      for (size_t b = 0; b + 1 < bcuts.size(); ++b) {
+        pactk::launch_pack(grad, len, m->words, m->tile_off, packed, bcuts[b], bcuts[b + 1], sp, false, gfrac);
+        CUDA_TRY(cudaEventRecord(pool_event(ctx, 1 + 2 * b), sp));
+      }
+      bpacks_issued = true;
     }
     std::vector<uint8_t> frames;
     if (c->shm) {  // host vote board: microseconds, no GPU work, no stream sync
@@ -2402,7 +2534,7 @@ pact_status pact_masked_allreduce(pact_comm* c, pact_ctx* ctx, const float* grad
     CUDA_TRY(cudaEventRecord(e_start, s));
     CUDA_TRY(cudaStreamWaitEvent(ctx->aux[0], e_start, 0));
     CUDA_TRY(cudaStreamWaitEvent(ctx->aux[1], e_start, 0));
-    const float gfrac = bucket_grid_frac();
+    const float gfrac = bucket_grid_frac(0.75f);
     for (int b = 0; b < B; ++b) {
       if (!packed_in_sym)
         pactk::launch_pack(grad, len, m->words, m->tile_off, mine, cuts[b], cuts[b + 1], s, false, gfrac);
@@ -2491,38 +2623,33 @@ pact_status pact_masked_allreduce(pact_comm* c, pact_ctx* ctx, const float* grad
       // tile-aligned buckets of ~bucket_bytes packed; pack on s, NCCL on
       // aux[0], unpack on aux[1], chained by events
       const std::vector<uint32_t>& off = m->host_tile_off;
-      // B = ceil(packed bytes / bucket_bytes) buckets of EQUAL chunk counts:
-      // pack and unpack cost HBM bytes of the dense range, so even ranges
-      // keep the three pipeline stages balanced (cuts by packed bytes gave
-      // VGG-19's dense classifier one bucket and the rest another)
-      const uint64_t B = std::min<uint64_t>(std::max<uint64_t>(1, (m->nnz * 4 + nccl_bb - 1) / nccl_bb),
-                                            std::min<uint64_t>(256, m->ntiles));
-      std::vector<uint64_t> cuts(B + 1);
-      for (uint64_t b = 0; b <= B; ++b) cuts[b] = m->ntiles * b / B;
-      nbuckets = (int)B;
+      const std::vector<uint64_t>& cuts = bcuts;
+      nbuckets = (int)cuts.size() - 1;
       // pack(b+1), the NCCL allreduce of b and unpack(b-1) run at once: the
       // codec grids leave part of every SM to the other two
-      const float gfrac = bucket_grid_frac();
       cudaEvent_t start = pool_event(ctx, 0);
-      CUDA_TRY(cudaEventRecord(start, s));
-      CUDA_TRY(cudaStreamWaitEvent(ctx->aux[1], start, 0));
+      if (!bpacks_issued) {
+        CUDA_TRY(cudaEventRecord(start, s));
+        if (sp != s) CUDA_TRY(cudaStreamWaitEvent(sp, start, 0));
+      }
+      CUDA_TRY(cudaStreamWaitEvent(su, start, 0));
       for (int b = 0; b < nbuckets; ++b) {
         const uint64_t tb = cuts[b], te = cuts[b + 1];
         const uint64_t o0 = off[tb], cnt = off[te] - off[tb];
         cudaEvent_t e_pack = pool_event(ctx, 1 + 2 * b), e_ar = pool_event(ctx, 2 + 2 * b);
-        pactk::launch_pack(grad, len, m->words, m->tile_off, packed, tb, te, s, false, gfrac);
-        CUDA_TRY(cudaEventRecord(e_pack, s));
-        CUDA_TRY(cudaStreamWaitEvent(ctx->aux[0], e_pack, 0));
-        if (cnt)
-          NCCL_TRY(ncclAllReduce(packed + o0, packed + o0, cnt, ncclFloat32, ncclSum, c->nccl,
-                                 ctx->aux[0]));
-        CUDA_TRY(cudaEventRecord(e_ar, ctx->aux[0]));
-        CUDA_TRY(cudaStreamWaitEvent(ctx->aux[1], e_ar, 0));
-        pactk::launch_unpack(packed, len, m->words, m->tile_off, scale, scale != 1.0f, out, tb, te,
-                             ctx->aux[1], false, gfrac);
+        if (!bpacks_issued) {
+          pactk::launch_pack(grad, len, m->words, m->tile_off, packed, tb, te, sp, false, gfrac);
+          CUDA_TRY(cudaEventRecord(e_pack, sp));
+        }
+        CUDA_TRY(cudaStreamWaitEvent(sx, e_pack, 0));
+        if (cnt) NCCL_TRY(ncclAllReduce(packed + o0, packed + o0, cnt, ncclFloat32, ncclSum, c->nccl, sx));
+        CUDA_TRY(cudaEventRecord(e_ar, sx));
+        CUDA_TRY(cudaStreamWaitEvent(su, e_ar, 0));
+        pactk::launch_unpack(packed, len, m->words, m->tile_off, scale, scale != 1.0f, out, tb, te, su, false,
+                             gfrac);
       }
       cudaEvent_t done = pool_event(ctx, 1 + 2 * nbuckets);
-      CUDA_TRY(cudaEventRecord(done, ctx->aux[1]));
+      CUDA_TRY(cudaEventRecord(done, su));
       CUDA_TRY(cudaStreamWaitEvent(s, done, 0));
     }
   } else {
