@@ -1280,7 +1280,7 @@ pact_status pact_prune_magnitude(pact_ctx* ctx, const float* w, uint64_t len, fl
                       h.w.T1, (unsigned long long)h.w.r1, (unsigned long long)h.w.eq1);
         out->spec_prefix_valid = h.w.straddle;
         out->nnz = h.nnz;
-        out->host_tile_off_valid = 0;
+        if ((changed & 1) || h.fix_changed) out->host_tile_off_valid = 0;
         out->digest = h.digest;  // exact for the final words whether or not they moved
         out->changed = (changed & 1) || h.fix_changed;
         out->digest_valid = 1;
@@ -1359,7 +1359,7 @@ pact_status pact_prune_magnitude(pact_ctx* ctx, const float* w, uint64_t len, fl
     CUDA_TRY(cudaStreamSynchronize(s));
     out->nnz = pin32[0];
     if (changed & 2) changed = (changed & 1) | (pin32[1] != 0);
-    out->host_tile_off_valid = 0;
+    if (changed) out->host_tile_off_valid = 0;  // same words: same offsets, the host mirror stays
   }
   out->changed = changed != 0;
   out->digest_valid = had_digest && !changed;
