@@ -390,7 +390,10 @@ def main():
 
     # inputs: identical weights on every rank (same seed) -> identical global mask
     weights = synth.weights_device(shape, 1234, synth.W_REAL, device=dev)
-    mask = pb.magnitude_prune(weights, ratio)
+    if reprune and args.prune == "per-layer":  # the A.9 recipe then keeps the per-layer mask
+        mask = pb.magnitude_prune_per_layer(weights, shape.offsets(), ratio)
+    else:
+        mask = pb.magnitude_prune(weights, ratio)
     nnz = mask.nnz()
     tracker = pb.MaskTracker(3)
     for _ in range(4):
@@ -762,7 +765,9 @@ def main():
         torch.distributed.destroy_process_group()
 
 
-SWEEP_RATIOS = (0.5, 0.6, 0.7, 0.8, 0.9, 0.95, 0.99)
+# BASELINE config 4 sweeps 50-99%; 0.05 and 0.1 (densities 0.95 / 0.9) are
+# added so the measured dense/sparse crossover is crossed inside the sweep
+SWEEP_RATIOS = (0.05, 0.1, 0.5, 0.6, 0.7, 0.8, 0.9, 0.95, 0.99)
 
 
 def run_sweep(args, pb, torch, comm, rank, world, local, dev, cfg, model, n, weights, grad, out, timed):
