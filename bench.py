@@ -92,6 +92,35 @@ def peaks():
         return 6650.0, "fallback"
 
 
+def nvlink_bytes(device: int):
+    """This GPU's cumulative NVLink data bytes (tx, rx) from the NVML field
+    counters -- hardware counters read without kernel replay, so they work
+    across ranks (ncu cannot profile a multi-rank exchange). Tries the
+    per-link byte counters first, then the aggregate KiB throughput fields;
+    None when neither is available."""
+    try:
+        import pynvml as nv
+
+        nv.nvmlInit()
+        h = nv.nvmlDeviceGetHandleByIndex(device)
+        ids = [(nv.NVML_FI_DEV_NVLINK_COUNT_XMIT_BYTES, l) for l in range(18)]
+        ids += [(nv.NVML_FI_DEV_NVLINK_COUNT_RCV_BYTES, l) for l in range(18)]
+        vals = nv.nvmlDeviceGetFieldValues(h, ids)
+        tx = [v.value.ullVal for v in vals[:18] if v.nvmlReturn == 0]
+        rx = [v.value.ullVal for v in vals[18:] if v.nvmlReturn == 0]
+        if tx and rx:
+            return {"tx": sum(tx), "rx": sum(rx), "source": "NVML_FI_DEV_NVLINK_COUNT_{XMIT,RCV}_BYTES",
+                    "links": len(tx)}
+        vals = nv.nvmlDeviceGetFieldValues(h, [nv.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX,
+                                               nv.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX])
+        if all(v.nvmlReturn == 0 for v in vals):
+            return {"tx": vals[0].value.ullVal * 1024, "rx": vals[1].value.ullVal * 1024,
+                    "source": "NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_{TX,RX} (KiB)", "links": None}
+    except Exception:
+        pass
+    return None
+
+
 class ClockSampler:
     """NVML sampling of SM clock and throttle reasons during the timed region."""
 
@@ -682,6 +711,34 @@ def main():
                  "nvlink_peak_gbs": 900.0,
                  "step_exchange_busbw_frac_of_nvlink": round(4 * nnz * f / t_x / 1e9 / 900.0, 3),
                  "dense_sync_equiv_gbs_per_rank": round(4 * n / t_dense / 1e9, 1)}
+        # NVLink hardware counters around K exchanges of the step's mask
+        # (this rank's bytes; the one-shot n = 2 push sends 4 nnz, a ring /
+        # two-shot exchange 2 (n-1)/n 4 nnz per rank)
+        nv0 = nvlink_bytes(local)
+        if nv0 is not None:
+            kx = 10
+            torch.cuda.synchronize()
+            barrier()
+            nv0 = nvlink_bytes(local)
+            for e in range(kx):
+                r = pb.masked_allreduce(grad, mask, pb.TrackerStatus.Stable, 50_000 + e, comm, policy=policy, out=out)
+            torch.cuda.synchronize()
+            nv1 = nvlink_bytes(local)
+            torch.cuda.synchronize()
+            nvd0 = nvlink_bytes(local)
+            for e in range(kx):
+                pb.full_allreduce(grad, comm, out=out)
+            torch.cuda.synchronize()
+            nvd1 = nvlink_bytes(local)
+            alg_x = 4 * nnz * (1.0 if (world == 2 and r.stats.transport == 2) else f)
+            extra["nvlink_counters"] = {
+                "source": nv0["source"], "links": nv0["links"], "steps": kx, "transport": int(r.stats.transport),
+                "tx_bytes_per_exchange": int((nv1["tx"] - nv0["tx"]) / kx),
+                "rx_bytes_per_exchange": int((nv1["rx"] - nv0["rx"]) / kx),
+                "algorithmic_bytes_per_rank": int(alg_x),
+                "tx_vs_algorithmic": round((nv1["tx"] - nv0["tx"]) / kx / alg_x, 3),
+                "dense_tx_bytes_per_allreduce": int((nvd1["tx"] - nvd0["tx"]) / kx),
+                "dense_algorithmic_bytes_per_rank": int(4 * n * f)}
         bx = stages.get("step_breakdown_us", {}).get("exchange", 0.0) * 1e-6
         if bx > 0:  # NCCL transport: the exchange timed directly inside the step (events around it)
             extra["exchange_in_step_us"] = round(bx * 1e6, 1)

@@ -404,7 +404,7 @@ __global__ void __launch_bounds__(kPuWarps * 32)
                   const uint32_t* __restrict__ chunk_off, float scale, int do_scale,
                   float* __restrict__ out, float lr, float* __restrict__ weights, uint64_t cb,
                   uint64_t ce, P2PView v, const uint64_t* __restrict__ flags, uint64_t target,
-                  P2PErr* __restrict__ err, P2PSig sg) {
+                  P2PErr* __restrict__ err, P2PSig sg, int bulk_out) {
   constexpr int kRS = kA + 1, kWS = kA + 2;  // run / word stages
   constexpr int kRun = kSrc == kSrcPair ? 2 * kRunCap : kRunCap;
   extern __shared__ __align__(16) float psm_base[];  // unpack_smem_bytes<kSrc, kA>()
@@ -456,11 +456,16 @@ __global__ void __launch_bounds__(kPuWarps * 32)
   uint32_t h = reinterpret_cast<const uint32_t*>(wsm[warp][0])[lane];
   uint32_t pos0 = warp_incl_scan((uint32_t)__popc(h)) - (uint32_t)__popc(h);
   int wi = 0, pi = 0;
+  bool bulk_pending = false;  // the previous chunk left as a bulk store from stage pa
   for (; c < ce; c += nwt) {
     const int w1 = (wi + 1) % kWS, wa = (wi + kA) % kWS, wa1 = (wi + kA + 1) % kWS, pa = (pi + kA) % kRS;
     if (c + (kA + 1) * nwt < ce) offs_words_issue(wsm[warp][wa1], words, chunk_off, c + (kA + 1) * nwt);
     cp_commit();
     asm volatile("cp.async.wait_group %0;" ::"n"(kA) : "memory");  // run(c), words(c + kA nwt) landed
+    if (bulk_pending) {  // stage pa (the previous chunk's) has been read by its bulk store
+      if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      bulk_pending = false;
+    }
     __syncwarp();
     if (c + kA * nwt < ce) {
       uint32_t b, n;
@@ -511,7 +516,37 @@ __global__ void __launch_bounds__(kPuWarps * 32)
     // term depends on j's parity only, so two per-lane bases + immediates
     const int tb0 = (lane >> 3) * 8 + ((lane & 7) ^ (lane >> 3));
     const int tb1 = (lane >> 3) * 8 + ((lane & 7) ^ ((lane >> 3) + 4));
-    if (!kSgd && !do_scale && vec_ok && (c + 1) * (uint64_t)kChunk <= len) {  // whole chunk: 8 x (LDS.128, STG.128)
+    if (!kSgd && bulk_out && vec_ok && (c + 1) * (uint64_t)kChunk <= len) {
+      // whole chunk, bulk store: the swizzled cells are read back (and
+      // scaled), rewritten linearly in place (each 128-byte row is permuted
+      // among its own 8 lanes) and leave as ONE 4 KiB cp.async.bulk from
+      // shared to global memory (the TMA engine) instead of 256 STG.128
+      float4 y[kVecPerLane];
+#pragma unroll
+      for (int j = 0; j < kVecPerLane; ++j) y[j] = T[32 * j + ((j & 1) ? tb1 : tb0)];
+      if (do_scale) {
+#pragma unroll
+        for (int j = 0; j < kVecPerLane; ++j) {
+          const uint32_t nib = (uint32_t)(wc[2 * j + (lane >> 4)] >> (4 * (lane & 15))) & 0xFu;
+          if (nib & 1) y[j].x = __fmul_rn(y[j].x, scale);
+          if (nib & 2) y[j].y = __fmul_rn(y[j].y, scale);
+          if (nib & 4) y[j].z = __fmul_rn(y[j].z, scale);
+          if (nib & 8) y[j].w = __fmul_rn(y[j].w, scale);
+        }
+      }
+      __syncwarp();
+#pragma unroll
+      for (int j = 0; j < kVecPerLane; ++j) T[32 * j + lane] = y[j];
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0)
+        asm volatile(
+            "cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n"
+            " cp.async.bulk.commit_group;" ::"l"(out + c * (uint64_t)kChunk),
+            "r"((uint32_t)__cvta_generic_to_shared(T)), "r"(kChunk * 4)
+            : "memory");
+      bulk_pending = true;
+    } else if (!kSgd && !do_scale && vec_ok && (c + 1) * (uint64_t)kChunk <= len) {  // 8 x (LDS.128, STG.128)
 #pragma unroll
       for (int j = 0; j < kVecPerLane; ++j)
         st_stream_f4(reinterpret_cast<float4*>(out + e0 + 128 * j), T[32 * j + ((j & 1) ? tb1 : tb0)]);
@@ -559,6 +594,10 @@ __global__ void __launch_bounds__(kPuWarps * 32)
     pos0 = pos0_n;
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
+  if (bulk_out) {  // the bulk stores are complete (and the stages free) before the CTA exits
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    __syncwarp();
+  }
   }
   if constexpr (kSrc != kSrcLocal) {
     p2psync::exit_signal(v, sg);  // READ: peers may reuse their buffers
@@ -818,6 +857,12 @@ void launch_pack_push(const float* g, uint64_t len, const uint64_t* words, const
 }
 
 namespace {
+// PACT_UNPACK_STG=1: whole chunks leave as 8 STG.128 per lane instead of one
+// 4 KiB bulk store per warp
+int unpack_bulk_out() {
+  static const int v = getenv("PACT_UNPACK_STG") == nullptr;
+  return v;
+}
 // chunks per warp of the one-run-ahead grid above which two runs ahead win
 constexpr uint64_t kDeepUnpackChunksPerWarp = 16;
 template <bool kSgd>
@@ -853,10 +898,10 @@ void unpack_local(const float* packed, uint64_t len, const uint64_t* words, cons
   P2PErr* ne = nullptr;
   if (deep)
     cudaLaunchKernelEx(&cfg, unpack_kernel<kSgd, kSrcLocal, 2>, packed, len, words, chunk_off, scale, do_scale, out,
-                       lr, weights, cb, ce, v, nf, (uint64_t)0, ne, sg);
+                       lr, weights, cb, ce, v, nf, (uint64_t)0, ne, sg, unpack_bulk_out());
   else
     cudaLaunchKernelEx(&cfg, unpack_kernel<kSgd, kSrcLocal, 1>, packed, len, words, chunk_off, scale, do_scale, out,
-                       lr, weights, cb, ce, v, nf, (uint64_t)0, ne, sg);
+                       lr, weights, cb, ce, v, nf, (uint64_t)0, ne, sg, unpack_bulk_out());
 }
 }  // namespace
 
@@ -886,7 +931,7 @@ void launch_unpack_p2p(const float* packed_local, uint64_t len, const uint64_t* 
     // and long grids slow down -- c3 0.26 -> 0.36 ms, c5 1.00 -> 1.21 ms.)
     unpack_kernel<false, kSrcPair, 1><<<grid_for(cap, nc, kPuWarps), kPuWarps * 32, kDyn, s>>>(
         packed_local, len, words, chunk_off, scale, do_scale, out, 0.f, nullptr, 0, nc, v, flags, target,
-        err, sg);
+        err, sg, unpack_bulk_out());
   } else {
     static DeviceCache<int> cc;
     int& cap = cc.get();
@@ -894,7 +939,7 @@ void launch_unpack_p2p(const float* packed_local, uint64_t len, const uint64_t* 
     if (!cap) cap = persistent_grid_dyn(unpack_kernel<false, kSrcOwner, 1>, kPuWarps, kDyn);
     unpack_kernel<false, kSrcOwner, 1><<<grid_for(cap, nc, kPuWarps), kPuWarps * 32, kDyn, s>>>(
         packed_local, len, words, chunk_off, scale, do_scale, out, 0.f, nullptr, 0, nc, v, flags, target,
-        err, sg);
+        err, sg, unpack_bulk_out());
   }
   note_launch();
 }

@@ -182,6 +182,7 @@ struct pact_mask {
   int ties_cur = 0;
   int spec_valid = 0;
   int spec_prefix_valid = 0;  // tie_prefix / ties[ties_cur] describe the ties at spec_T
+  int spec_drop_all = 0;      // the last result dropped every tie at spec_T (r == E)
   uint64_t spec_k = 0, spec_c_lt = 0;
   uint32_t spec_T = 0;
   // key window [win_lo, win_hi] around spec_T (about +-len/1024 ranks): the
@@ -1215,7 +1216,11 @@ pact_status pact_prune_magnitude(pact_ctx* ctx, const float* w, uint64_t len, fl
   if (out->spec_valid && out->spec_k == k) {
     const uint32_t T0 = out->spec_T;
     const uint64_t r0 = k - out->spec_c_lt;
-    const bool pv = out->spec_prefix_valid;
+    // the last result dropped every tie at T0 (e.g. A.9: the pruned weights
+    // are fresh noise, the k-th key is its maximum): drop them all in the
+    // pass too -- exact without a tie fix-up (and its second round trip)
+    // whenever that is still true, whatever the ties' positions now
+    const bool pv = out->spec_prefix_valid && !out->spec_drop_all;
     if (out->win_valid && !(out->win_lo <= T0 && T0 <= out->win_hi)) out->win_valid = 0;
     TRY(bitmap(T0, r0, pv, pv, true));
     if (hb.n_lt < k && k <= hb.n_lt + hb.n_eq) {  // threshold still the k-th key
@@ -1230,6 +1235,7 @@ pact_status pact_prune_magnitude(pact_ctx* ctx, const float* w, uint64_t len, fl
       st.c_lt = hb.n_lt;
       st.candidates = hb.n_cand;
       out->spec_c_lt = hb.n_lt;
+      out->spec_drop_all = r == hb.n_eq;
       done = true;
     } else if (out->win_valid && hb.n_cand <= ccap) {
       // (0') the threshold moved: the k-th key lies in the window when
@@ -1279,6 +1285,7 @@ pact_status pact_prune_magnitude(pact_ctx* ctx, const float* w, uint64_t len, fl
           return fail(PACT_E_RUN_FAILURE, "prune window select inconsistent (T0=%u T1=%u r1=%llu eq=%llu)", T0,
                       h.w.T1, (unsigned long long)h.w.r1, (unsigned long long)h.w.eq1);
         out->spec_prefix_valid = h.w.straddle;
+        out->spec_drop_all = !h.w.straddle;
         out->nnz = h.nnz;
         if ((changed & 1) || h.fix_changed) out->host_tile_off_valid = 0;
         out->digest = h.digest;  // exact for the final words whether or not they moved
@@ -1344,6 +1351,7 @@ pact_status pact_prune_magnitude(pact_ctx* ctx, const float* w, uint64_t len, fl
       TRY(scan(ctx, out->ties[out->ties_cur].as<uint32_t>(), nc, out->tie_prefix.as<uint32_t>(), s));
       out->spec_prefix_valid = 1;
     }
+    out->spec_drop_all = r == hb.n_eq;
     out->spec_valid = 1;
     out->spec_k = k;
     out->spec_T = T;

@@ -329,7 +329,7 @@ constexpr int kCandBuf = 64;                            // per-warp window-candi
 constexpr int kCandHistBits = 8;                        // first select digit, counted by the pass
 constexpr size_t kBitmapSmem =
     (size_t)kPruneWarps * (kKeyStages * kStageFloats * sizeof(float) + 2 * kCandBuf * sizeof(uint32_t)) +
-    (sizeof(uint32_t) << kCandHistBits);
+    (sizeof(uint32_t) << kCandHistBits) + (size_t)kPruneWarps * kKeyStages * sizeof(uint64_t);
 
 __device__ __forceinline__ void chunk_issue(float* st, const float* __restrict__ w,
                                             const uint64_t* __restrict__ words, uint64_t c) {
@@ -350,6 +350,40 @@ __device__ __forceinline__ void chunk_issue(float* st, const float* __restrict__
   }
 }
 
+// Bulk (TMA engine) variant of the chunk load: lane 0 arms the stage's
+// mbarrier with the byte count and issues two 1-D cp.async.bulk copies (the
+// 4 KiB of weights and the 128 B of old mask words) into a LINEAR stage; the
+// lanes wait on the mbarrier's phase. One instruction moves the chunk
+// instead of 264 per-lane 16-byte cp.async.
+__device__ __forceinline__ void mbar_init(uint64_t* mbar) {
+  const uint32_t a = (uint32_t)__cvta_generic_to_shared(mbar);
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(a) : "memory");
+}
+__device__ __forceinline__ void chunk_issue_bulk(float* stg, uint64_t* mbar, const float* __restrict__ w,
+                                                 const uint64_t* __restrict__ words, uint64_t c) {
+  const uint32_t sm = (uint32_t)__cvta_generic_to_shared(stg);
+  const uint32_t mb = (uint32_t)__cvta_generic_to_shared(mbar);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the lanes' reads of this stage come first
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(kChunk * 4 + kChunkWords * 8)
+               : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(sm),
+               "l"(w + c * (uint64_t)kChunk), "r"(kChunk * 4), "r"(mb)
+               : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   sm + kChunk * 4),
+               "l"(words + c * kChunkWords), "r"(kChunkWords * 8), "r"(mb)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* mbar, uint32_t phase) {
+  const uint32_t mb = (uint32_t)__cvta_generic_to_shared(mbar);
+  uint32_t done = 0;
+  while (!done)
+    asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+                 : "=r"(done)
+                 : "r"(mb), "r"(phase)
+                 : "memory");
+}
+
 // staged window candidates of one warp -> the global list (one atomic per flush)
 __device__ __forceinline__ void flush_pairs(const uint32_t* bk, const uint32_t* bi, uint32_t fill,
                                             unsigned long long* n_cand, const PruneCandBuf& cb) {
@@ -365,6 +399,7 @@ __device__ __forceinline__ void flush_pairs(const uint32_t* bk, const uint32_t* 
   __syncwarp();
 }
 
+template <bool kBulk>
 __global__ void __launch_bounds__(kPruneWarps * 32)
     prune_bitmap_kernel(const float* __restrict__ w, uint64_t len, uint32_t T, uint64_t r,
                         const uint32_t* __restrict__ tie_prefix, uint64_t* __restrict__ words,
@@ -387,6 +422,16 @@ __global__ void __launch_bounds__(kPruneWarps * 32)
     for (int b = threadIdx.x; b < (1 << kCandHistBits); b += blockDim.x) chist[b] = 0;
     __syncthreads();
   }
+  // kBulk: one mbarrier per stage per warp, after the histogram
+  uint64_t* mbars = reinterpret_cast<uint64_t*>(chist + (1 << kCandHistBits)) + warp * kKeyStages;
+  uint32_t phases = 0;  // bit s: parity of stage s's next completion
+  if constexpr (kBulk) {
+    if (lane == 0) {
+      for (int q = 0; q < kKeyStages; ++q) mbar_init(mbars + q);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+  }
   uint32_t* words32 = reinterpret_cast<uint32_t*>(words);
   uint32_t* tie32 = reinterpret_cast<uint32_t*>(tie_words);
   uint32_t* tie_old32 = reinterpret_cast<uint32_t*>(tie_old);
@@ -407,19 +452,32 @@ __global__ void __launch_bounds__(kPruneWarps * 32)
 #pragma unroll
   for (int s = 0; s < kKeyStages - 1; ++s) {
     const uint64_t cc = c0 + s * nw_total;
-    if (cc < nchunks && full(cc)) chunk_issue(ring + s * kStageFloats, w, words, cc);
-    asm volatile("cp.async.commit_group;" ::: "memory");
+    if constexpr (kBulk) {
+      if (lane == 0 && cc < nchunks && full(cc)) chunk_issue_bulk(ring + s * kStageFloats, mbars + s, w, words, cc);
+    } else {
+      if (cc < nchunks && full(cc)) chunk_issue(ring + s * kStageFloats, w, words, cc);
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    }
   }
   int slot = 0;
   for (uint64_t c = c0; c < nchunks; c += nw_total) {
+    const int cur = slot;
     {
       const uint64_t cn = c + (kKeyStages - 1) * nw_total;
       const int sn = slot == 0 ? kKeyStages - 1 : slot - 1;
       __syncwarp();  // every lane is done reading stage sn (the previous chunk)
-      if (cn < nchunks && full(cn)) chunk_issue(ring + sn * kStageFloats, w, words, cn);
-      asm volatile("cp.async.commit_group;" ::: "memory");
-      asm volatile("cp.async.wait_group %0;" ::"n"(kKeyStages - 1) : "memory");
-      __syncwarp();  // lanes read stage cells other lanes' cp.async filled
+      if constexpr (kBulk) {
+        if (lane == 0 && cn < nchunks && full(cn)) chunk_issue_bulk(ring + sn * kStageFloats, mbars + sn, w, words, cn);
+        if (full(c)) {
+          mbar_wait(mbars + cur, (phases >> cur) & 1u);
+          phases ^= 1u << cur;
+        }
+      } else {
+        if (cn < nchunks && full(cn)) chunk_issue(ring + sn * kStageFloats, w, words, cn);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        asm volatile("cp.async.wait_group %0;" ::"n"(kKeyStages - 1) : "memory");
+      }
+      __syncwarp();  // lanes read stage cells other lanes' copies filled
     }
     const float* st = ring + slot * kStageFloats;
     slot = slot == kKeyStages - 1 ? 0 : slot + 1;
@@ -431,8 +489,10 @@ __global__ void __launch_bounds__(kPruneWarps * 32)
     if (fc) {
 #pragma unroll
       for (int k = kVecPerLane - 1; k >= 0; --k) {  // elements 32*lane + 4k .. 4k+3
-        const float4 v =
-            *reinterpret_cast<const float4*>(st + 4 * (lane * 8 + (k ^ (lane & 7))));
+        // kBulk: linear stage, lane l reads its 16-byte cell (k + l) & 7 --
+        // conflict-free -- and the rotated mask is turned back below
+        const float4 v = kBulk ? *reinterpret_cast<const float4*>(st + 32 * lane + 4 * ((k + lane) & 7))
+                               : *reinterpret_cast<const float4*>(st + 4 * (lane * 8 + (k ^ (lane & 7))));
         const uint32_t k3 = mag_key(v.w), k2 = mag_key(v.z), k1 = mag_key(v.y), k0 = mag_key(v.x);
         g = __funnelshift_l(T - k3, g, 1);
         g = __funnelshift_l(T - k2, g, 1);
@@ -440,6 +500,7 @@ __global__ void __launch_bounds__(kPruneWarps * 32)
         g = __funnelshift_l(T - k0, g, 1);
         mn = min(mn, min(min(k3 - wlo, k2 - wlo), min(k1 - wlo, k0 - wlo)));
       }
+      if constexpr (kBulk) g = __funnelshift_l(g, g, 4 * (lane & 7));  // cell (k + l) & 7 sat at bits 4k
     } else {
       inr = e0 >= len ? 0u : (len - e0 >= 32 ? ~0u : (1u << (len - e0)) - 1u);
       for (int i = 31; i >= 0; --i) {
@@ -463,7 +524,7 @@ __global__ void __launch_bounds__(kPruneWarps * 32)
         bool ok = true;
         uint32_t kq;
         if (fc) {
-          kq = mag_key(st[4 * (l * 8 + ((lane >> 2) ^ (l & 7))) + (lane & 3)]);
+          kq = mag_key(kBulk ? st[32 * l + lane] : st[4 * (l * 8 + ((lane >> 2) ^ (l & 7))) + (lane & 3)]);
         } else {
           ok = el0 + lane < len;
           kq = ok ? mag_key(w[el0 + lane]) : 0u;
@@ -528,6 +589,9 @@ __global__ void __launch_bounds__(kPruneWarps * 32)
     }
     const uint32_t pc = warp_sum((uint32_t)__popc(keep));
     if (lane == 0) chunk_popc[c] = pc;
+  }
+  if constexpr (kBulk) {  // retire the mbarriers (no copy is outstanding: every issued chunk was waited on)
+    __syncwarp();
   }
   if (fill) flush_pairs(cbk, cbi, fill, &counts->n_cand, cb);
   if (cb.hist) {
@@ -763,17 +827,25 @@ void launch_prune_bitmap(const float* w, uint64_t len, uint32_t T, uint64_t r,
   cudaMemsetAsync(counts, 0, sizeof(BitmapCounts), s);
   if (cand.hist) cudaMemsetAsync(cand.hist, 0, sizeof(uint32_t) << kCandHistBits, s);
   if (!nc) return;
+  // PACT_BITMAP_CPASYNC=1: the per-lane cp.async ring instead of the bulk copies
+  static const bool bulk = getenv("PACT_BITMAP_CPASYNC") == nullptr;
   static DeviceCache<unsigned> cap;
   unsigned& cp = cap.get();
   if (!cp) {
-    cudaFuncSetAttribute(prune_bitmap_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)kBitmapSmem);
-    cp = persistent_grid(prune_bitmap_kernel, kPruneWarps * 32, kBitmapSmem, ~0ull >> 8, kPruneWarps);
+    cudaFuncSetAttribute(prune_bitmap_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBitmapSmem);
+    cudaFuncSetAttribute(prune_bitmap_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBitmapSmem);
+    cp = persistent_grid(prune_bitmap_kernel<true>, kPruneWarps * 32, kBitmapSmem, ~0ull >> 8, kPruneWarps);
   }
   const uint64_t need = (nc + kPruneWarps - 1) / kPruneWarps;
-  prune_bitmap_kernel<<<(unsigned)(need < cp ? need : cp), kPruneWarps * 32, kBitmapSmem, s>>>(
-      w, len, T, r, tie_prefix, words, (len + 63) / 64, chunk_popc, ties_out, ties_prev, tie_words, tie_old,
-      counts, nc, cand);
+  const unsigned grid = (unsigned)(need < cp ? need : cp);
+  if (bulk)
+    prune_bitmap_kernel<true><<<grid, kPruneWarps * 32, kBitmapSmem, s>>>(
+        w, len, T, r, tie_prefix, words, (len + 63) / 64, chunk_popc, ties_out, ties_prev, tie_words, tie_old,
+        counts, nc, cand);
+  else
+    prune_bitmap_kernel<false><<<grid, kPruneWarps * 32, kBitmapSmem, s>>>(
+        w, len, T, r, tie_prefix, words, (len + 63) / 64, chunk_popc, ties_out, ties_prev, tie_words, tie_old,
+        counts, nc, cand);
   note_launch();
 }
 

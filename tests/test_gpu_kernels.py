@@ -528,6 +528,23 @@ def test_reprune_sequence_paths(pb, port, cuda, n):
         assert got_paths.count(4) >= 4, paths
 
 
+def test_bitmap_cpasync_variant(cuda):
+    """prune_bitmap_kernel ships in two load variants: the default moves each
+    chunk with two cp.async.bulk copies into a linear stage (UBLKCP), the
+    PACT_BITMAP_CPASYNC=1 one with per-lane cp.async into a swizzled stage.
+    The re-prune schedule above runs bit-exact through the latter too."""
+    import os
+    import subprocess
+    import sys
+
+    env = dict(os.environ, PACT_BITMAP_CPASYNC="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
+                        f"{os.path.abspath(__file__)}::test_reprune_sequence_paths"],
+                       env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert "2 passed" in r.stdout, r.stdout[-1000:]
+
+
 def test_c5_reprune_a9_full_size(pb, port, cuda):
     """C5 (GPT-2-medium, 354,823,168) per-step re-pruning at 0.9 with the A.9
     recipe (w <- GSE(w) + delta), plus threshold moves both ways: words
