@@ -17,7 +17,8 @@
  *    (include/pact/error.hpp:10-26); 100+ are CUDA/NCCL/argument errors.
  *    No exception crosses this boundary; pact_last_error() gives the message
  *    of the calling thread's last failure.
- *  - Element counts are limited to PACT_MAX_LEN (2^30 - 1 fp32 values, 4 GiB).
+ *  - Element counts are limited to PACT_MAX_LEN (2^31 - 1 fp32 values, 8 GiB: element
+ *    indices travel as 31-bit fields, packed offsets as u32).
  */
 #ifndef PACT_C_H
 #define PACT_C_H
@@ -31,7 +32,7 @@ extern "C" {
 
 #define PACT_ABI_VERSION 1
 #define PACT_TILE 1024              /* elements per offset tile (16 words)   */
-#define PACT_MAX_LEN ((1ull << 30) - 1)
+#define PACT_MAX_LEN ((1ull << 31) - 1)
 #define PACT_HEADER_BYTES 26        /* codec.hpp:90 kHeaderSize              */
 #define PACT_UNIQUE_ID_BYTES 128    /* NCCL unique id                        */
 

@@ -6,8 +6,9 @@
 // 142-146) and F16Wire (collective.cpp:133-163): every ring hop re-rounds
 // the partial sum to binary16 before it leaves, the receiver adds it to its
 // own fp32 value, and the chunk owner rounds the final sum once more so the
-// all-gather copies identical bits. The conversions here are the same bit
-// manipulations, not the hardware cvt (whose overflow goes to Inf).
+// all-gather copies identical bits. The conversions use the hardware cvt
+// (cvt.rn.f16.f32 / cvt.f32.f16) with the reference's special-value rules
+// patched on top (overflow clamps instead of going to Inf, NaN canonical).
 //
 // Kernels: seed (first hop: encode own chunk), step (p = x + decode(recv);
 // encode p), gather (decode the owners' final chunks into the output).
@@ -18,51 +19,27 @@
 
 namespace pactk {
 
-__device__ __forceinline__ uint16_t f2h_ref(float v) {  // codec.cpp:79-111
-  const uint32_t bits = __float_as_uint(v);
-  const uint32_t sign = (bits >> 16) & 0x8000u;
-  const int32_t exp = (int32_t)((bits >> 23) & 0xffu) - 127;
-  uint32_t mant = bits & 0x7fffffu;
-  if (exp == 128) return (uint16_t)(sign | (mant ? 0x7e00u : 0x7bffu));
-  if (exp > 15) return (uint16_t)(sign | 0x7bffu);
-  if (exp >= -14) {
-    uint32_t m = mant >> 13;
-    const uint32_t rest = mant & 0x1fffu;
-    if (rest > 0x1000u || (rest == 0x1000u && (m & 1u))) ++m;
-    const uint32_t h = ((uint32_t)(exp + 15) << 10) + m;
-    return (uint16_t)(sign | (h >= 0x7c00u ? 0x7bffu : h));
-  }
-  if (exp >= -25) {
-    mant |= 0x800000u;
-    const int shift = -exp - 14 + 13;  // 14..24
-    uint32_t m = mant >> shift;
-    const uint32_t cut = mant & ((1u << shift) - 1u);
-    const uint32_t half_ulp = 1u << (shift - 1);
-    if (cut > half_ulp || (cut == half_ulp && (m & 1u))) ++m;
-    return (uint16_t)(sign | m);
-  }
-  return (uint16_t)sign;
+// The reference's conversions (codec.cpp:79-140) are RNE with three
+// departures from IEEE, so the hardware cvt does the rounding (normals and
+// subnormals alike: RNE at 2^-24 granularity, flush below 2^-25 to signed
+// zero, exactly as codec.cpp:100-110's shift-and-round) and only the
+// specials are patched: overflow (a rounded result >= 0x7c00, including
+// +-Inf inputs) clamps to +-65504 (codec.cpp:86-88, 96), NaN becomes the
+// input-signed quiet NaN 0x7e00 (codec.cpp:85).
+__device__ __forceinline__ uint16_t f2h_ref(float v) {
+  const uint16_t sign = (uint16_t)((__float_as_uint(v) >> 16) & 0x8000u);
+  uint16_t h = __half_as_ushort(__float2half_rn(v));
+  if ((h & 0x7fffu) >= 0x7c00u) h = sign | ((v != v) ? 0x7e00u : 0x7bffu);
+  return h;
 }
 
-__device__ __forceinline__ float h2f_ref(uint16_t h) {  // codec.cpp:113-140
-  const uint32_t sign = (uint32_t)(h & 0x8000u) << 16;
-  const uint32_t exp = (h >> 10) & 0x1fu;
-  const uint32_t mant = h & 0x3ffu;
-  uint32_t bits;
-  if (exp == 0) {
-    if (mant == 0) {
-      bits = sign;
-    } else {  // subnormal: normalise (leading-zero count instead of the loop)
-      const int lz = __clz(mant) - 21;  // shifts until bit 10 is set
-      const uint32_t m = mant << lz;
-      bits = sign | ((uint32_t)(1 - lz + 112) << 23) | ((m & 0x3ffu) << 13);
-    }
-  } else if (exp == 31) {
-    bits = sign | 0x7f800000u | (mant << 13);
-  } else {
-    bits = sign | ((exp + 112) << 23) | (mant << 13);
-  }
-  return __uint_as_float(bits);
+// Every binary16 value is exactly representable in fp32, so the hardware cvt
+// is the reference's decode (codec.cpp:113-140) except for NaN payloads,
+// which the reference carries through (mant << 13) and the cvt canonicalises.
+__device__ __forceinline__ float h2f_ref(uint16_t h) {
+  if ((h & 0x7c00u) == 0x7c00u)
+    return __uint_as_float(((uint32_t)(h & 0x8000u) << 16) | 0x7f800000u | ((uint32_t)(h & 0x3ffu) << 13));
+  return __half2float(__ushort_as_half(h));
 }
 
 namespace {

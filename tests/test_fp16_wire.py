@@ -77,6 +77,30 @@ def test_gpu_roundtrip_bitexact(pb, port, cuda):
 
 
 @pytest.mark.gpu
+def test_gpu_roundtrip_exhaustive_near_half_range(pb, port, cuda):
+    """The wire encode is the hardware cvt.rn.f16.f32 with the reference's
+    special-value rules patched on (f16wire.cu): every fp32 of both signs
+    with a biased exponent in [96, 145] -- below the smallest subnormal's
+    half through the clamp region, every mantissa -- plus every binary16
+    pattern decoded, bit-exact against the reference's conversions."""
+    import torch
+
+    mant = np.arange(1 << 23, dtype=np.uint32)
+    for sign in (0, 1):
+        for e in list(range(96, 146)) + [0, 1, 200, 254, 255]:
+            bits = (np.uint32(sign << 31) | np.uint32(e << 23) | mant).view(np.float32)
+            got = pb.fp16_roundtrip(torch.from_numpy(bits).cuda()).cpu().numpy()
+            want = port.half_to_float(port.float_to_half(bits))
+            bad = np.nonzero(u32(got) != u32(want))[0]
+            assert bad.size == 0, (sign, e, hex(int(u32(bits)[bad[0]])), hex(int(u32(got)[bad[0]])),
+                                   hex(int(u32(want)[bad[0]])))
+    h = np.arange(1 << 16, dtype=np.uint32)
+    f = port.half_to_float(h.astype(np.uint16))
+    got = pb.fp16_roundtrip(torch.from_numpy(f).cuda()).cpu().numpy()
+    assert np.array_equal(u32(got), u32(port.half_to_float(port.float_to_half(f))))
+
+
+@pytest.mark.gpu
 def test_gpu_fp16_single_rank_and_packed_wire(pb, port, cuda):
     import torch
 

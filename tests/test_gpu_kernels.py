@@ -662,3 +662,28 @@ def test_per_layer_prune_errors(pb, cuda):
     with pytest.raises(pb.Error) as e:
         pb.magnitude_prune_per_layer(x, [0, 100], 1.0)
     assert e.value.code == pb.Errc.InvalidRatio
+
+
+def test_max_len_prune_pack_unpack(pb, port, cuda):
+    """len = PACT_MAX_LEN = 2^31 - 1 (8 GiB of fp32, larger than GPT-2-XL's
+    1.56B; an odd length, so a ragged last word and chunk): words and digest
+    bit-exact against the oracle at 0.9, then pack -> unpack == GSE. One past
+    the limit is refused with a shape error."""
+    from paper_2505_18563_b200 import synth
+
+    n = (1 << 31) - 1
+    wd = torch.empty(n, dtype=torch.float32, device="cuda")
+    pb.synth_fill(wd, 91, synth.W_TIES, 0.25)
+    m, _ = _check_full(pb, port, wd, 0.9, n, "max_len")
+    keep = expand_bits(m.words(), n)
+    g = wd  # reuse the buffer: the gradient
+    pb.synth_fill(g, 7, synth.G_FULL)
+    p = pb.pack(g, m, 0)
+    assert p.values.numel() == m.nnz()
+    u = pb.unpack(p, m)
+    assert torch.equal(u, torch.where(keep, g, torch.zeros((), device=g.device)))
+    del u, p, keep, g, wd, m
+    torch.cuda.empty_cache()
+    with pytest.raises(pb.Error) as ei:
+        pb.SparsityMask(n + 1)
+    assert ei.value.code == pb.Errc.ShapeMismatch
