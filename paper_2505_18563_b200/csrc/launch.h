@@ -86,7 +86,9 @@ void launch_mask_gather(const uint64_t* src, uint64_t src_len, const uint64_t* s
                         uint64_t dst_words_padded, cudaStream_t s);
 // exclusive scan of n u32 -> out[0..n], out[n] = total (single pass, look-back)
 size_t scan_scratch_bytes(uint64_t n);
-void launch_scan_excl(const uint32_t* in, uint64_t n, uint32_t* out, void* scratch, cudaStream_t s);
+// gate (nullable, device): the kernel returns at once when *gate == 0
+void launch_scan_excl(const uint32_t* in, uint64_t n, uint32_t* out, void* scratch, cudaStream_t s,
+                      const int* gate = nullptr);
 // count of kernels launched by these launchers (process-wide, for gpu_launches)
 uint64_t launches();
 void note_launch(uint64_t n = 1);
@@ -189,6 +191,23 @@ struct WinReport {
   uint32_t nnz;
   int fix_changed;
 };
+// Temporal reuse resolved on the device (one host round trip): after the
+// bitmap pass at the previous (T0, r0), gate = {scan, ok, digest}: ok when
+// T0 is still the k-th key and no tie fix-up is needed (pv: the pass used
+// the previous tie prefix -- exact unless r moved or the ties did; else ties
+// all dropped -- exact when r == #ties), scan when ok and a bit changed,
+// digest when scan or force. The offsets scan and the digest are launched
+// gated on it; the report gathers the counts, gate, nnz and digest.
+struct HitReport {
+  BitmapCounts bc;
+  int gate[3], pad;
+  unsigned long long digest;
+  uint32_t nnz, pad2;
+};
+void launch_prune_hit_gate(const BitmapCounts* bc, uint64_t k, uint64_t r0, int pv, int force_digest, int* gate,
+                           cudaStream_t s);
+void launch_prune_hit_report(const BitmapCounts* bc, const int* gate, const uint64_t* digest, const uint32_t* nnz,
+                             HitReport* out, cudaStream_t s);
 void launch_prune_win_report(const WinSel* ws, const uint64_t* digest, const uint32_t* nnz,
                              const int* fix_changed, WinReport* out, cudaStream_t s);
 // Window fix-up once the true threshold T' of a moved mask is known (it lies
@@ -298,7 +317,7 @@ void launch_f16_roundtrip(const float* x, uint64_t n, float* out, cudaStream_t s
 // digest_scratch_bytes(nwords). Result written to *out_dev.
 size_t digest_scratch_bytes(uint64_t nwords);
 void launch_digest(const uint64_t* words, uint64_t nwords, void* scratch, uint64_t* out_dev,
-                   cudaStream_t s);
+                   cudaStream_t s, const int* gate = nullptr);
 
 // ---- synth.cu --------------------------------------------------------------
 void launch_synth(float* x, uint64_t len, uint64_t seed, uint64_t index_base, int recipe,

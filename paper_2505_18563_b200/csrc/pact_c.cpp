@@ -263,6 +263,8 @@ struct Small {
   pactk::WinSel win_sel;
   uint32_t cand_hist[2048];
   pactk::WinReport report;
+  int hit_gate[4];
+  pactk::HitReport hit;
 };
 
 pact_status set_device(pact_ctx* ctx) {
@@ -374,9 +376,10 @@ cudaEvent_t pool_event(pact_ctx* ctx, size_t i) {
 }
 
 // recompute tile offsets + nnz from the mask words (device), sync
-pact_status scan(pact_ctx* ctx, const uint32_t* in, uint64_t n, uint32_t* out, cudaStream_t s) {
+pact_status scan(pact_ctx* ctx, const uint32_t* in, uint64_t n, uint32_t* out, cudaStream_t s,
+                 const int* gate = nullptr) {
   TRY(ctx->state.ensure(pactk::scan_scratch_bytes(n)));
-  pactk::launch_scan_excl(in, n, out, ctx->state.p, s);
+  pactk::launch_scan_excl(in, n, out, ctx->state.p, s, gate);
   return PACT_OK;
 }
 
@@ -1154,7 +1157,8 @@ pact_status pact_prune_magnitude(pact_ctx* ctx, const float* w, uint64_t len, fl
   // one bitmap pass at (T, r); tie prefix from the previous call (spec) or
   // "all ties dropped" (prefix null); window candidates when win; returns
   // the pass's own counts
-  auto bitmap = [&](uint32_t T, uint64_t r, bool use_prefix, bool compare_prev, bool win) -> pact_status {
+  auto bitmap = [&](uint32_t T, uint64_t r, bool use_prefix, bool compare_prev, bool win,
+                    bool readback = true) -> pact_status {
     const int nxt = out->ties_cur ^ 1;
     pactk::PruneCandBuf cb;
     if (win && out->win_valid) {
@@ -1171,10 +1175,11 @@ pact_status pact_prune_magnitude(pact_ctx* ctx, const float* w, uint64_t len, fl
                                compare_prev ? out->ties[out->ties_cur].as<uint32_t>() : nullptr,
                                out->tie_words.as<uint64_t>(), bc, s, cb, out->tie_old.as<uint64_t>());
     CUDA_TRY(cudaGetLastError());
+    out->ties_cur = nxt;
+    if (!readback) return PACT_OK;
     CUDA_TRY(cudaMemcpyAsync(ctx->pin.p, bc, sizeof hb, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));
     std::memcpy(&hb, ctx->pin.p, sizeof hb);
-    out->ties_cur = nxt;
     return PACT_OK;
   };
   // exact tie bits once the true (T, r) and per-chunk tie counts are known;
@@ -1222,7 +1227,51 @@ pact_status pact_prune_magnitude(pact_ctx* ctx, const float* w, uint64_t len, fl
     // whenever that is still true, whatever the ties' positions now
     const bool pv = out->spec_prefix_valid && !out->spec_drop_all;
     if (out->win_valid && !(out->win_lo <= T0 && T0 <= out->win_hi)) out->win_valid = 0;
-    TRY(bitmap(T0, r0, pv, pv, true));
+    TRY(bitmap(T0, r0, pv, pv, true, false));
+    // the hit resolved on the device: offsets scan and digest launched gated
+    // on "T0 still the k-th key, no tie fix-up, a bit changed", one readback
+    {
+      int* gate = sm->hit_gate;
+      pactk::launch_prune_hit_gate(bc, k, r0, pv, !had_digest, gate, s);
+      TRY(scan(ctx, out->tile_popc, nc, out->tile_off, s, gate));
+      TRY(ctx->digest_scratch.ensure(pactk::digest_scratch_bytes(out->nwords)));
+      pactk::launch_digest(out->words, out->nwords, ctx->digest_scratch.p, &sm->digest, s, gate + 2);
+      pactk::launch_prune_hit_report(bc, gate, &sm->digest, out->tile_off + nc, &sm->hit, s);
+      CUDA_TRY(cudaGetLastError());
+      CUDA_TRY(cudaMemcpyAsync(ctx->pin.p, &sm->hit, sizeof(pactk::HitReport), cudaMemcpyDeviceToHost, s));
+      CUDA_TRY(cudaStreamSynchronize(s));
+      pactk::HitReport rep;
+      std::memcpy(&rep, ctx->pin.p, sizeof rep);
+      hb = rep.bc;
+      if (rep.gate[1]) {
+        const bool chg = rep.gate[0] != 0;
+        st.path = 3;
+        st.threshold = T0;
+        st.c_lt = hb.n_lt;
+        st.candidates = hb.n_cand;
+        out->spec_c_lt = hb.n_lt;
+        out->spec_drop_all = (k - hb.n_lt) == hb.n_eq;
+        // the pass resolved ties against the previous prefix (pv) or dropped
+        // them all; in the latter case that prefix no longer describes them
+        out->spec_prefix_valid = pv;
+        if (chg) {
+          out->nnz = rep.nnz;
+          out->host_tile_off_valid = 0;
+        }
+        if (rep.gate[2]) {
+          out->digest = rep.digest;
+          out->digest_valid = 1;
+        } else {
+          out->digest_valid = had_digest;
+        }
+        out->changed = chg;
+        if (out->nnz != len - k)
+          return fail(PACT_E_RUN_FAILURE, "prune kept %llu, expected %llu", (unsigned long long)out->nnz,
+                      (unsigned long long)(len - k));
+        if (stats) *stats = st;
+        return PACT_OK;
+      }
+    }
     if (hb.n_lt < k && k <= hb.n_lt + hb.n_eq) {  // threshold still the k-th key
       changed |= hb.changed | hb.changed_cand;
       const uint64_t r = k - hb.n_lt;

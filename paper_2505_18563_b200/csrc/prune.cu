@@ -859,6 +859,41 @@ __global__ void prune_win_report_kernel(const WinSel* ws, const uint64_t* digest
   *out = r;
 }
 
+namespace {
+__global__ void prune_hit_gate_kernel(const BitmapCounts* bc, uint64_t k, uint64_t r0, int pv, int force,
+                                      int* gate) {
+  const unsigned long long n_lt = bc->n_lt, n_eq = bc->n_eq;
+  const bool hit = n_lt < k && k <= n_lt + n_eq;
+  const unsigned long long r = k - n_lt;
+  const bool fix = pv ? (r != r0 || bc->tie_mismatch != 0) : (r < n_eq);
+  const bool ok = hit && !fix;
+  const bool chg = ok && (bc->changed | bc->changed_cand | bc->changed_tie) != 0;
+  gate[0] = chg;
+  gate[1] = ok;
+  gate[2] = chg || (ok && force);
+}
+__global__ void prune_hit_report_kernel(const BitmapCounts* bc, const int* gate, const uint64_t* digest,
+                                        const uint32_t* nnz, HitReport* out) {
+  out->bc = *bc;
+  out->gate[0] = gate[0];
+  out->gate[1] = gate[1];
+  out->gate[2] = gate[2];
+  out->digest = gate[2] ? *digest : 0ull;
+  out->nnz = gate[0] ? *nnz : 0u;
+}
+}  // namespace
+
+void launch_prune_hit_gate(const BitmapCounts* bc, uint64_t k, uint64_t r0, int pv, int force_digest, int* gate,
+                           cudaStream_t s) {
+  prune_hit_gate_kernel<<<1, 1, 0, s>>>(bc, k, r0, pv, force_digest, gate);
+  note_launch();
+}
+void launch_prune_hit_report(const BitmapCounts* bc, const int* gate, const uint64_t* digest, const uint32_t* nnz,
+                             HitReport* out, cudaStream_t s) {
+  prune_hit_report_kernel<<<1, 1, 0, s>>>(bc, gate, digest, nnz, out);
+  note_launch();
+}
+
 void launch_prune_win_report(const WinSel* ws, const uint64_t* digest, const uint32_t* nnz,
                              const int* fix_changed, WinReport* out, cudaStream_t s) {
   prune_win_report_kernel<<<1, 1, 0, s>>>(ws, digest, nnz, fix_changed, out);
