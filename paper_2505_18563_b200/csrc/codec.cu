@@ -1006,6 +1006,16 @@ void launch_mask_gather(const uint64_t* src, uint64_t src_len, const uint64_t* s
 
 size_t scan_scratch_bytes(uint64_t n) { return ((n + kScanItems - 1) / kScanItems + 1) * 8 + 8; }
 
+namespace {
+__global__ void gather_u32_kernel(const uint32_t* __restrict__ src, GatherIdx idx, uint32_t* __restrict__ out) {
+  if ((int)threadIdx.x < idx.n) out[threadIdx.x] = src[idx.i[threadIdx.x]];
+}
+}  // namespace
+void launch_gather_u32(const uint32_t* src, const GatherIdx& idx, uint32_t* out, cudaStream_t s) {
+  gather_u32_kernel<<<1, 96, 0, s>>>(src, idx, out);
+  note_launch();
+}
+
 void launch_scan_excl(const uint32_t* in, uint64_t n, uint32_t* out, void* scratch, cudaStream_t s,
                       const int* gate) {
   const uint64_t tiles = n ? (n + kScanItems - 1) / kScanItems : 1;

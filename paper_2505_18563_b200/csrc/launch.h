@@ -78,6 +78,14 @@ void launch_gse(const float* g, uint64_t len, const uint64_t* words, float* out,
 void launch_mask_fill(uint64_t* words, uint64_t len, int keep, uint32_t* chunk_off, cudaStream_t s);
 void launch_clear_tail(uint64_t* words, uint64_t len, cudaStream_t s);
 void launch_tile_popc(const uint64_t* words, uint64_t len, uint32_t* chunk_popc, cudaStream_t s);
+// out[j] = src[idx[j]] for j < n (n <= kGatherMax): a few chunk offsets for
+// the host in one readback (bucket boundaries of the copy-engine exchange)
+constexpr int kGatherMax = 65;
+struct GatherIdx {
+  uint64_t i[kGatherMax];
+  int n;
+};
+void launch_gather_u32(const uint32_t* src, const GatherIdx& idx, uint32_t* out, cudaStream_t s);
 // dst bits [dst_start[s], dst_start[s+1]) <- src bits from src_begin[s]
 // (device tables, nseg entries + 1 for dst_start); all dst_words_padded
 // words are written (zero past dst_len)

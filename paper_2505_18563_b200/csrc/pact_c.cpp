@@ -265,6 +265,7 @@ struct Small {
   pactk::WinReport report;
   int hit_gate[4];
   pactk::HitReport hit;
+  uint32_t gather[pactk::kGatherMax + 3];
 };
 
 pact_status set_device(pact_ctx* ctx) {
@@ -2491,6 +2492,65 @@ pact_status pact_masked_allreduce(pact_comm* c, pact_ctx* ctx, const float* grad
     const int xctas = B > 1 ? 4 * sm_count_host() : 0;  // leave SMs to pack/unpack
     const bool two = n > 2;
     if (!packed_in_sym && k1 > 2) pactk::launch_p2p_wait(myflags, pactk::kP2PRead, n, k1 - 2, err, s);
+    static const int ce_buckets = [] {  // PACT_P2P_CE=<buckets>: the copy-engine push
+      const char* e = getenv("PACT_P2P_CE");
+      return e ? std::max(1, std::min(pactk::kGatherMax - 1, atoi(e))) : 0;
+    }();
+    if (B == 1 && p2p_push && ce_buckets > 0) {
+      // copy-engine push (n = 2): the pack runs at full HBM speed over Bc
+      // chunk ranges into this rank's packed region; each range's packed
+      // values go to the peer's incoming region as one DMA copy (the copy
+      // engines, no SMs) overlapping the next range's pack; PACKED follows
+      // the last copy on the copy stream. The unpack is the push variant's.
+      const int peer = c->rank ^ 1;
+      const int Bc = (int)std::min<uint64_t>((uint64_t)ce_buckets, m->ntiles);
+      std::vector<uint64_t> tb(Bc + 1), off(Bc + 1);
+      for (int i = 0; i <= Bc; ++i) tb[i] = m->ntiles * (uint64_t)i / (uint64_t)Bc;
+      if (m->host_tile_off_valid) {
+        for (int i = 0; i <= Bc; ++i) off[i] = m->host_tile_off[tb[i]];
+      } else {  // the bucket boundaries' offsets only, one small readback
+        pactk::GatherIdx gi{};
+        gi.n = Bc + 1;
+        for (int i = 0; i <= Bc; ++i) gi.i[i] = tb[i];
+        Small* smw = ctx->ws_small.as<Small>();
+        pactk::launch_gather_u32(m->tile_off, gi, smw->gather, s);
+        CUDA_TRY(cudaMemcpyAsync(ctx->pin.p, smw->gather, 4 * (Bc + 1), cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+        for (int i = 0; i <= Bc; ++i) off[i] = ctx->pin.as<uint32_t>()[i];
+      }
+      float* remote = p2p_reduced(p, peer, par);
+      cudaStream_t xs = ctx->aux[0];
+      for (int i = 0; i < Bc; ++i) {
+        pactk::launch_pack(grad, len, m->words, m->tile_off, mine, tb[i], tb[i + 1], s);
+        cudaEvent_t e = pool_event(ctx, 1 + i);
+        CUDA_TRY(cudaEventRecord(e, s));
+        CUDA_TRY(cudaStreamWaitEvent(xs, e, 0));
+        if (off[i + 1] > off[i])
+          CUDA_TRY(cudaMemcpyAsync(remote + off[i], mine + off[i], (off[i + 1] - off[i]) * 4,
+                                   cudaMemcpyDeviceToDevice, xs));
+      }
+      mark(0);
+      pactk::launch_p2p_signal(v, pactk::kP2PPacked, fval(0), xs);
+      pactk::P2PView vin = v;
+      vin.packed[peer] = p2p_reduced(p, c->rank, par);  // this rank's incoming region
+      pactk::P2PSig sgu;
+      sgu.exit_kind = pactk::kP2PRead;
+      sgu.exit_val = k1;
+      sgu.counter = p2p_counter(p, c->rank);
+      // the caller's stream joins the copy stream (its copies are done); the
+      // unpack then waits for the peer's PACKED on the device
+      cudaEvent_t ej = pool_event(ctx, 1 + Bc);
+      CUDA_TRY(cudaEventRecord(ej, xs));
+      CUDA_TRY(cudaStreamWaitEvent(s, ej, 0));
+      mark(1);
+      pactk::launch_unpack_p2p(mine, len, m->words, m->tile_off, scale, scale != 1.0f, out, vin, 0, myflags,
+                               fval(0), err, sgu, s);
+      mark(2);
+      p.k = k1;
+      nbuckets = Bc;
+      transport = PACT_TRANSPORT_P2P;
+      goto p2p_done;
+    }
     if (B == 1 && p2p_push) {
       // push one-shot (n = 2): pack -> {own packed, peer's incoming} and
       // PACKED on exit; unpack waits for the peer's PACKED and folds the

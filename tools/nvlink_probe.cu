@@ -215,8 +215,9 @@ int main() {
     cudaStreamCreate(&s0);
     cudaEventCreate(&f0);
     cudaEventCreate(&g0);
-    const size_t mb = 20, nn = (mb << 20) / 16;
+    for (size_t mb_ : {(size_t)20, (size_t)128})
     for (int mode = 0; mode < 5; ++mode) {
+      const size_t mb = mb_, nn = (mb << 20) / 16;
       const int grids[4] = {148, 296, 592, 1184};
       float best0 = 1e9, best1 = 1e9;
       for (int it = 0; it < 10; ++it) {
@@ -249,6 +250,7 @@ int main() {
              mode < 4 ? "WRITE float4" : "cudaMemcpyPeer", mode < 4 ? grids[mode] : 0, best0 * 1e3, best1 * 1e3,
              (mb << 20) / (best0 * 1e-3) / 1e9);
     }
+    const size_t mb = 20, nn = (mb << 20) / 16;
     // bulk copy / bulk reduce-add, both directions at once; then check the sums
     for (int red = 0; red < 2; ++red) {
       float best0 = 1e9;
