@@ -435,6 +435,29 @@ pact_status mirror_tile_off(pact_mask* m, cudaStream_t s) {
   return PACT_OK;
 }
 
+// packed offsets of the given chunk boundaries on the host: from the host
+// mirror when valid, else gathered on the device and read back (a few bytes
+// instead of the whole offset table after every mask change)
+pact_status chunk_offsets(pact_mask* m, const std::vector<uint64_t>& cuts, cudaStream_t s,
+                          std::vector<uint64_t>& off) {
+  off.resize(cuts.size());
+  if (!m->host_tile_off_valid && cuts.size() <= (size_t)pactk::kGatherMax) {
+    pact_ctx* ctx = m->ctx;
+    pactk::GatherIdx gi{};
+    gi.n = (int)cuts.size();
+    for (size_t i = 0; i < cuts.size(); ++i) gi.i[i] = cuts[i];
+    Small* sm = ctx->ws_small.as<Small>();
+    pactk::launch_gather_u32(m->tile_off, gi, sm->gather, s);
+    CUDA_TRY(cudaMemcpyAsync(ctx->pin.p, sm->gather, 4 * cuts.size(), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    for (size_t i = 0; i < cuts.size(); ++i) off[i] = ctx->pin.as<uint32_t>()[i];
+    return PACT_OK;
+  }
+  TRY(mirror_tile_off(m, s));
+  for (size_t i = 0; i < cuts.size(); ++i) off[i] = m->host_tile_off[cuts[i]];
+  return PACT_OK;
+}
+
 // how long a rank waits for a peer (vote board, NVLink flags) before the
 // link is declared dead: PACT_LINK_TIMEOUT_MS, default 30 s
 uint64_t link_timeout_ms() {
@@ -2379,7 +2402,6 @@ pact_status pact_masked_allreduce(pact_comm* c, pact_ctx* ctx, const float* grad
   const uint64_t nccl_bb = pol.bucket_bytes ? pol.bucket_bytes : auto_bb;
   const bool buckets = c && !p2p_try && !f16 && nccl_bb > 0 && m->nnz * 4 > nccl_bb;
   const bool nccl_sym_ok = c && !(n == 2 && pbytes > (64ull << 20));
-  if (buckets) TRY(mirror_tile_off(m, s));
 
   int agree = 0;
   bool packed_issued = false, packed_in_sym = false;
@@ -2394,6 +2416,7 @@ pact_status pact_masked_allreduce(pact_comm* c, pact_ctx* ctx, const float* grad
     bcuts.resize(B + 1);
     for (uint64_t b = 0; b <= B; ++b) bcuts[b] = m->ntiles * b / B;
   }
+  std::vector<uint64_t> boff;  // packed offsets of the bucket cuts (after the speculative packs)
   // bucketed pipelines run on an SM partition (green contexts) when the
   // driver offers one: NCCL on its own SMs, pack / unpack on the rest
   GreenSet* gr = buckets ? green_streams(ctx, n) : nullptr;
@@ -2437,6 +2460,7 @@ pact_status pact_masked_allreduce(pact_comm* c, pact_ctx* ctx, const float* grad
       }
       bpacks_issued = true;
     }
+    if (buckets) TRY(chunk_offsets(m, bcuts, s, boff));  // s only: does not wait for the packs on sp
     std::vector<uint8_t> frames;
     if (c->shm) {  // host vote board: microseconds, no GPU work, no stream sync
       TRY(shm_vote(c, frame, frames));
@@ -2504,20 +2528,9 @@ pact_status pact_masked_allreduce(pact_comm* c, pact_ctx* ctx, const float* grad
       // the last copy on the copy stream. The unpack is the push variant's.
       const int peer = c->rank ^ 1;
       const int Bc = (int)std::min<uint64_t>((uint64_t)ce_buckets, m->ntiles);
-      std::vector<uint64_t> tb(Bc + 1), off(Bc + 1);
+      std::vector<uint64_t> tb(Bc + 1), off;
       for (int i = 0; i <= Bc; ++i) tb[i] = m->ntiles * (uint64_t)i / (uint64_t)Bc;
-      if (m->host_tile_off_valid) {
-        for (int i = 0; i <= Bc; ++i) off[i] = m->host_tile_off[tb[i]];
-      } else {  // the bucket boundaries' offsets only, one small readback
-        pactk::GatherIdx gi{};
-        gi.n = Bc + 1;
-        for (int i = 0; i <= Bc; ++i) gi.i[i] = tb[i];
-        Small* smw = ctx->ws_small.as<Small>();
-        pactk::launch_gather_u32(m->tile_off, gi, smw->gather, s);
-        CUDA_TRY(cudaMemcpyAsync(ctx->pin.p, smw->gather, 4 * (Bc + 1), cudaMemcpyDeviceToHost, s));
-        CUDA_TRY(cudaStreamSynchronize(s));
-        for (int i = 0; i <= Bc; ++i) off[i] = ctx->pin.as<uint32_t>()[i];
-      }
+      TRY(chunk_offsets(m, tb, s, off));
       float* remote = p2p_reduced(p, peer, par);
       cudaStream_t xs = ctx->aux[0];
       for (int i = 0; i < Bc; ++i) {
@@ -2739,7 +2752,6 @@ pact_status pact_masked_allreduce(pact_comm* c, pact_ctx* ctx, const float* grad
     } else {
       // tile-aligned buckets of ~bucket_bytes packed; pack on s, NCCL on
       // aux[0], unpack on aux[1], chained by events
-      const std::vector<uint32_t>& off = m->host_tile_off;
       const std::vector<uint64_t>& cuts = bcuts;
       nbuckets = (int)cuts.size() - 1;
       // pack(b+1), the NCCL allreduce of b and unpack(b-1) run at once: the
@@ -2752,7 +2764,7 @@ pact_status pact_masked_allreduce(pact_comm* c, pact_ctx* ctx, const float* grad
       CUDA_TRY(cudaStreamWaitEvent(su, start, 0));
       for (int b = 0; b < nbuckets; ++b) {
         const uint64_t tb = cuts[b], te = cuts[b + 1];
-        const uint64_t o0 = off[tb], cnt = off[te] - off[tb];
+        const uint64_t o0 = boff[b], cnt = boff[b + 1] - boff[b];
         cudaEvent_t e_pack = pool_event(ctx, 1 + 2 * b), e_ar = pool_event(ctx, 2 + 2 * b);
         if (!bpacks_issued) {
           pactk::launch_pack(grad, len, m->words, m->tile_off, packed, tb, te, sp, false, gfrac);
