@@ -858,10 +858,14 @@ void launch_pack_push(const float* g, uint64_t len, const uint64_t* words, const
 }
 
 namespace {
-// PACT_UNPACK_STG=1: whole chunks leave as 8 STG.128 per lane instead of one
-// 4 KiB bulk store per warp
+// PACT_UNPACK_BULK=1: whole chunks leave as one 4 KiB cp.async.bulk store per
+// warp instead of 8 STG.128 per lane. Measured slower (B200, unpack us, STG
+// vs bulk: c2 26.6 vs 28.7, c3 110 vs 142, c5 277 vs 357): the stage a bulk
+// store reads from is the next run's landing buffer, so every chunk waits
+// for the previous chunk's store to drain from shared memory before its
+// prefetch can be issued, where streaming STG.128s retire into the LSU.
 int unpack_bulk_out() {
-  static const int v = getenv("PACT_UNPACK_STG") == nullptr;
+  static const int v = getenv("PACT_UNPACK_BULK") != nullptr;
   return v;
 }
 // chunks per warp of the one-run-ahead grid above which two runs ahead win

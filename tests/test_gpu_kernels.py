@@ -545,6 +545,25 @@ def test_bitmap_cpasync_variant(cuda):
     assert "2 passed" in r.stdout, r.stdout[-1000:]
 
 
+def test_unpack_bulk_store_variant(cuda):
+    """The opt-in unpack variant that stores whole chunks with one 4 KiB
+    cp.async.bulk (PACT_UNPACK_BULK=1) is bit-exact through the codec tests
+    (golden, random densities, unaligned / in place, canaries, scaling)."""
+    import os
+    import subprocess
+    import sys
+
+    env = dict(os.environ, PACT_UNPACK_BULK="1")
+    sel = " or ".join(["test_codec_golden", "test_pack_unpack_random", "test_unaligned_and_inplace",
+                       "test_no_writes_outside_outputs", "test_single_gpu_masked_allreduce",
+                       "test_full_size_pack_properties"])
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
+                        os.path.abspath(__file__), "-k", sel],
+                       env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert " passed" in r.stdout and "failed" not in r.stdout, r.stdout[-1000:]
+
+
 def test_c5_reprune_a9_full_size(pb, port, cuda):
     """C5 (GPT-2-medium, 354,823,168) per-step re-pruning at 0.9 with the A.9
     recipe (w <- GSE(w) + delta), plus threshold moves both ways: words
