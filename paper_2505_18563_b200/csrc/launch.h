@@ -214,6 +214,16 @@ struct HitReport {
 };
 void launch_prune_hit_gate(const BitmapCounts* bc, uint64_t k, uint64_t r0, int pv, int force_digest, int* gate,
                            cudaStream_t s);
+// the same gate as the first node of a CUDA graph: its inputs from mapped
+// host memory (written by the host before each graph launch), its digest
+// bit the value of the graph's IF-node condition (the scan and digest run
+// inside the IF body: skipped on the device when nothing changed)
+struct HitParams {
+  unsigned long long k, r0;
+  int pv, force;
+};
+void launch_prune_hit_gate_cond(const BitmapCounts* bc, const HitParams* hp, int* gate,
+                                cudaGraphConditionalHandle h, cudaStream_t s);
 void launch_prune_hit_report(const BitmapCounts* bc, const int* gate, const uint64_t* digest, const uint32_t* nnz,
                              HitReport* out, cudaStream_t s);
 void launch_prune_win_report(const WinSel* ws, const uint64_t* digest, const uint32_t* nnz,
