@@ -419,6 +419,7 @@ __global__ void __launch_bounds__(kPuWarps * 32)
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const bool vec_ok = ((((uintptr_t)out) | (kSgd ? (uintptr_t)weights : 0)) & 15) == 0;
+  const bool uni_scale = scale > 0.0f && scale <= 3.4028235e38f;  // positive, finite
   const uint64_t nwt = (uint64_t)gridDim.x * kPuWarps;
   uint64_t c = cb + (uint64_t)blockIdx.x * kPuWarps + warp;
   if (c < ce) {
@@ -546,10 +547,21 @@ __global__ void __launch_bounds__(kPuWarps * 32)
             "r"((uint32_t)__cvta_generic_to_shared(T)), "r"(kChunk * 4)
             : "memory");
       bulk_pending = true;
-    } else if (!kSgd && !do_scale && vec_ok && (c + 1) * (uint64_t)kChunk <= len) {  // 8 x (LDS.128, STG.128)
+    } else if (!kSgd && (!do_scale || uni_scale) && vec_ok && (c + 1) * (uint64_t)kChunk <= len) {
+      // whole chunk: 8 x (LDS.128, STG.128); a positive finite scale is
+      // applied to every element (dropped ones are +0: +0 * scale == +0, the
+      // masked rule's result)
 #pragma unroll
-      for (int j = 0; j < kVecPerLane; ++j)
-        st_stream_f4(reinterpret_cast<float4*>(out + e0 + 128 * j), T[32 * j + ((j & 1) ? tb1 : tb0)]);
+      for (int j = 0; j < kVecPerLane; ++j) {
+        float4 t = T[32 * j + ((j & 1) ? tb1 : tb0)];
+        if (do_scale) {
+          t.x = __fmul_rn(t.x, scale);
+          t.y = __fmul_rn(t.y, scale);
+          t.z = __fmul_rn(t.z, scale);
+          t.w = __fmul_rn(t.w, scale);
+        }
+        st_stream_f4(reinterpret_cast<float4*>(out + e0 + 128 * j), t);
+      }
     } else
 #pragma unroll
     for (int j = 0; j < kVecPerLane; ++j) {
