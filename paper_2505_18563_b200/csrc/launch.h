@@ -199,13 +199,13 @@ struct WinReport {
   uint32_t nnz;
   int fix_changed;
 };
-// Temporal reuse resolved on the device (one host round trip): after the
-// bitmap pass at the previous (T0, r0), gate = {scan, ok, digest}: ok when
-// T0 is still the k-th key and no tie fix-up is needed (pv: the pass used
-// the previous tie prefix -- exact unless r moved or the ties did; else ties
-// all dropped -- exact when r == #ties), scan when ok and a bit changed,
-// digest when scan or force. The offsets scan and the digest are launched
-// gated on it; the report gathers the counts, gate, nnz and digest.
+// Temporal reuse decided on the device: after the bitmap pass at the
+// previous (T0, r0), gate = {changed, ok, digest}: ok when T0 is still the
+// k-th key and no tie fix-up is needed (pv: the pass used the previous tie
+// prefix -- exact unless r moved or the ties did; else ties all dropped --
+// exact when r == #ties), changed when ok and a bit moved, digest when
+// changed or force. The gate kernel writes {counts, gate} to `out`; the
+// report kernel adds the offsets' total (nnz) and the digest when they ran.
 struct HitReport {
   BitmapCounts bc;
   int gate[3], pad;
@@ -213,17 +213,7 @@ struct HitReport {
   uint32_t nnz, pad2;
 };
 void launch_prune_hit_gate(const BitmapCounts* bc, uint64_t k, uint64_t r0, int pv, int force_digest, int* gate,
-                           cudaStream_t s);
-// the same gate as the first node of a CUDA graph: its inputs from mapped
-// host memory (written by the host before each graph launch), its digest
-// bit the value of the graph's IF-node condition (the scan and digest run
-// inside the IF body: skipped on the device when nothing changed)
-struct HitParams {
-  unsigned long long k, r0;
-  int pv, force;
-};
-void launch_prune_hit_gate_cond(const BitmapCounts* bc, const HitParams* hp, int* gate,
-                                cudaGraphConditionalHandle h, cudaStream_t s);
+                           HitReport* out, cudaStream_t s);
 void launch_prune_hit_report(const BitmapCounts* bc, const int* gate, const uint64_t* digest, const uint32_t* nnz,
                              HitReport* out, cudaStream_t s);
 void launch_prune_win_report(const WinSel* ws, const uint64_t* digest, const uint32_t* nnz,

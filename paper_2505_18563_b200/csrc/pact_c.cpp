@@ -161,23 +161,10 @@ struct pact_ctx {
   std::vector<cudaEvent_t> ev_pool;
   cudaEvent_t t0 = nullptr, t1 = nullptr;
   cudaEvent_t stage[3] = {nullptr, nullptr, nullptr};
-  cudaStream_t capture = nullptr;            // graph building (stream capture)
-  pactk::HitParams* hitp = nullptr;          // mapped pinned: the hit graph's gate inputs
-  pactk::HitParams* hitp_dev = nullptr;
-};
-
-// the temporal-reuse tail of a prune as one CUDA graph (per mask): gate ->
-// IF(changed) {offsets scan, digest} -> report -> readback; rebuilt when a
-// buffer it points at moves
-struct HitGraph {
-  cudaGraph_t g = nullptr;
-  cudaGraphExec_t exec = nullptr;
-  const void* key[8] = {};
 };
 
 struct pact_mask {
   pact_ctx* ctx = nullptr;
-  HitGraph hit_graph;
   uint64_t len = 0, nwords = 0, ntiles = 0;
   uint64_t* words = nullptr;
   uint32_t* tile_off = nullptr;   // ntiles + 1
@@ -865,8 +852,6 @@ pact_status pact_ctx_destroy(pact_ctx* ctx) {
   if (ctx->t1) cudaEventDestroy(ctx->t1);
   for (auto e : ctx->stage)
     if (e) cudaEventDestroy(e);
-  if (ctx->capture) cudaStreamDestroy(ctx->capture);
-  if (ctx->hitp) cudaFreeHost(ctx->hitp);
   delete ctx;
   return PACT_OK;
 }
@@ -918,8 +903,6 @@ pact_status pact_mask_destroy(pact_mask* m) {
   m->cand_key.release();
   m->cand_idx.release();
   m->tie_old.release();
-  if (m->hit_graph.exec) cudaGraphExecDestroy(m->hit_graph.exec);
-  if (m->hit_graph.g) cudaGraphDestroy(m->hit_graph.g);
   delete m;
   return PACT_OK;
 }
@@ -1035,67 +1018,6 @@ pact_status pact_mask_digest(pact_mask* m, pact_stream_t stream, uint64_t* out) 
 // --------------------------------------------------------------- prune
 
 namespace {
-
-// the hit tail graph of mask m (see HitGraph), built on first use
-pact_status hit_graph_exec(pact_ctx* ctx, pact_mask* m, cudaGraphExec_t* out) {
-  Small* sm = ctx->ws_small.as<Small>();
-  const uint64_t nc = m->ntiles;
-  TRY(ctx->state.ensure(pactk::scan_scratch_bytes(nc)));
-  TRY(ctx->digest_scratch.ensure(pactk::digest_scratch_bytes(m->nwords)));
-  if (!ctx->hitp) {
-    void* hp = nullptr;
-    CUDA_TRY(cudaHostAlloc(&hp, sizeof(pactk::HitParams), cudaHostAllocMapped));
-    ctx->hitp = static_cast<pactk::HitParams*>(hp);
-    void* dp = nullptr;
-    CUDA_TRY(cudaHostGetDevicePointer(&dp, hp, 0));
-    ctx->hitp_dev = static_cast<pactk::HitParams*>(dp);
-  }
-  if (!ctx->capture) CUDA_TRY(cudaStreamCreateWithFlags(&ctx->capture, cudaStreamNonBlocking));
-  const void* key[8] = {m->words, m->tile_popc, m->tile_off, ctx->state.p, ctx->digest_scratch.p, sm,
-                        ctx->pin.p, ctx->hitp_dev};
-  HitGraph& hg = m->hit_graph;
-  if (hg.exec && std::memcmp(key, hg.key, sizeof key) == 0) {
-    *out = hg.exec;
-    return PACT_OK;
-  }
-  if (hg.exec) cudaGraphExecDestroy(hg.exec);
-  if (hg.g) cudaGraphDestroy(hg.g);
-  hg.exec = nullptr;
-  hg.g = nullptr;
-  cudaStream_t cs = ctx->capture;
-  cudaGraph_t g = nullptr;
-  CUDA_TRY(cudaGraphCreate(&g, 0));
-  hg.g = g;
-  cudaGraphConditionalHandle h;
-  CUDA_TRY(cudaGraphConditionalHandleCreate(&h, g, 0, cudaGraphCondAssignDefault));
-  int* gate = sm->hit_gate;
-  CUDA_TRY(cudaStreamBeginCaptureToGraph(cs, g, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
-  pactk::launch_prune_hit_gate_cond(&sm->bcounts, ctx->hitp_dev, gate, h, cs);
-  cudaStreamCaptureStatus cst;
-  const cudaGraphNode_t* deps = nullptr;
-  size_t nd = 0;
-  CUDA_TRY(cudaStreamGetCaptureInfo(cs, &cst, nullptr, nullptr, &deps, &nd));
-  cudaGraphNodeParams cp = {};
-  cp.type = cudaGraphNodeTypeConditional;
-  cp.conditional.handle = h;
-  cp.conditional.type = cudaGraphCondTypeIf;
-  cp.conditional.size = 1;
-  cudaGraphNode_t cond;
-  CUDA_TRY(cudaGraphAddNode(&cond, g, deps, nd, &cp));
-  CUDA_TRY(cudaStreamUpdateCaptureDependencies(cs, &cond, 1, cudaStreamSetCaptureDependencies));
-  pactk::launch_prune_hit_report(&sm->bcounts, gate, &sm->digest, m->tile_off + nc, &sm->hit, cs);
-  CUDA_TRY(cudaMemcpyAsync(ctx->pin.p, &sm->hit, sizeof(pactk::HitReport), cudaMemcpyDeviceToHost, cs));
-  CUDA_TRY(cudaStreamEndCapture(cs, &g));
-  cudaGraph_t body = cp.conditional.phGraph_out[0];
-  CUDA_TRY(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
-  pactk::launch_scan_excl(m->tile_popc, nc, m->tile_off, ctx->state.p, cs, gate);
-  pactk::launch_digest(m->words, m->nwords, ctx->digest_scratch.p, &sm->digest, cs);
-  CUDA_TRY(cudaStreamEndCapture(cs, &body));
-  CUDA_TRY(cudaGraphInstantiate(&hg.exec, g, 0));
-  std::memcpy(hg.key, key, sizeof key);
-  *out = hg.exec;
-  return PACT_OK;
-}
 
 // radix select of the `rank`-th smallest (1-based) key' = key - base over
 // elements with key' < 2^bits; returns key' and #(key' smaller).
@@ -1330,38 +1252,33 @@ pact_status pact_prune_magnitude(pact_ctx* ctx, const float* w, uint64_t len, fl
     const bool pv = out->spec_prefix_valid && !out->spec_drop_all;
     if (out->win_valid && !(out->win_lo <= T0 && T0 <= out->win_hi)) out->win_valid = 0;
     TRY(bitmap(T0, r0, pv, pv, true, false));
-    // the hit resolved on the device: offsets scan and digest launched gated
-    // on "T0 still the k-th key, no tie fix-up, a bit changed", one readback
+    // the hit decided on the device: one small kernel turns the pass's counts
+    // into the gate {changed, ok, digest needed} and the readback carries
+    // both. A reproduced mask (the common case) ends here; a changed one
+    // takes one more round trip for its offsets and digest. (Tried: the
+    // scan and digest launched every time, gated in-kernel, and as a CUDA
+    // graph with an IF node -- the no-op launches, the IF node and reading
+    // the gate's inputs from mapped host memory cost the reproduced mask
+    // 12-20 us, more than the changed mask's saved round trip.)
     {
-      // as one CUDA graph whose IF node skips the scan and digest on the
-      // device when nothing changed (PACT_HIT_GRAPH=0: plain gated launches)
-      static const bool use_graph = [] {
-        const char* e = getenv("PACT_HIT_GRAPH");
-        return !(e && e[0] == '0');
-      }();
       int* gate = sm->hit_gate;
-      cudaGraphExec_t ex = nullptr;
-      if (use_graph) TRY(hit_graph_exec(ctx, out, &ex));
-      if (ex) {
-        ctx->hitp->k = k;
-        ctx->hitp->r0 = r0;
-        ctx->hitp->pv = pv;
-        ctx->hitp->force = !had_digest;
-        CUDA_TRY(cudaGraphLaunch(ex, s));
-      } else {
-        pactk::launch_prune_hit_gate(bc, k, r0, pv, !had_digest, gate, s);
-        TRY(scan(ctx, out->tile_popc, nc, out->tile_off, s, gate));
-        TRY(ctx->digest_scratch.ensure(pactk::digest_scratch_bytes(out->nwords)));
-        pactk::launch_digest(out->words, out->nwords, ctx->digest_scratch.p, &sm->digest, s, gate + 2);
-        pactk::launch_prune_hit_report(bc, gate, &sm->digest, out->tile_off + nc, &sm->hit, s);
-        CUDA_TRY(cudaGetLastError());
-        CUDA_TRY(cudaMemcpyAsync(ctx->pin.p, &sm->hit, sizeof(pactk::HitReport), cudaMemcpyDeviceToHost, s));
-      }
+      pactk::launch_prune_hit_gate(bc, k, r0, pv, !had_digest, gate, &sm->hit, s);
+      CUDA_TRY(cudaGetLastError());
+      CUDA_TRY(cudaMemcpyAsync(ctx->pin.p, &sm->hit, sizeof(pactk::HitReport), cudaMemcpyDeviceToHost, s));
       CUDA_TRY(cudaStreamSynchronize(s));
       pactk::HitReport rep;
       std::memcpy(&rep, ctx->pin.p, sizeof rep);
-      if (ex) pactk::note_launch(rep.gate[2] ? 6 : 2);  // gate + report (+ scan + 3 digest kernels)
       hb = rep.bc;
+      if (rep.gate[1] && rep.gate[2]) {
+        if (rep.gate[0]) TRY(scan(ctx, out->tile_popc, nc, out->tile_off, s));
+        TRY(ctx->digest_scratch.ensure(pactk::digest_scratch_bytes(out->nwords)));
+        pactk::launch_digest(out->words, out->nwords, ctx->digest_scratch.p, &sm->digest, s);
+        pactk::launch_prune_hit_report(bc, gate, &sm->digest, out->tile_off + nc, &sm->hit, s);
+        CUDA_TRY(cudaGetLastError());
+        CUDA_TRY(cudaMemcpyAsync(ctx->pin.p, &sm->hit, sizeof(pactk::HitReport), cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+        std::memcpy(&rep, ctx->pin.p, sizeof rep);
+      }
       if (rep.gate[1]) {
         const bool chg = rep.gate[0] != 0;
         st.path = 3;

@@ -860,27 +860,19 @@ __global__ void prune_win_report_kernel(const WinSel* ws, const uint64_t* digest
 }
 
 namespace {
-__device__ __forceinline__ int hit_gate(const BitmapCounts* bc, uint64_t k, uint64_t r0, int pv, int force,
-                                        int* gate) {
+__global__ void prune_hit_gate_kernel(const BitmapCounts* bc, uint64_t k, uint64_t r0, int pv, int force,
+                                      int* gate, HitReport* out) {
   const unsigned long long n_lt = bc->n_lt, n_eq = bc->n_eq;
   const bool hit = n_lt < k && k <= n_lt + n_eq;
   const unsigned long long r = k - n_lt;
   const bool fix = pv ? (r != r0 || bc->tie_mismatch != 0) : (r < n_eq);
   const bool ok = hit && !fix;
   const bool chg = ok && (bc->changed | bc->changed_cand | bc->changed_tie) != 0;
-  gate[0] = chg;
-  gate[1] = ok;
-  gate[2] = chg || (ok && force);
-  return gate[2];
-}
-__global__ void prune_hit_gate_kernel(const BitmapCounts* bc, uint64_t k, uint64_t r0, int pv, int force,
-                                      int* gate) {
-  hit_gate(bc, k, r0, pv, force, gate);
-}
-__global__ void prune_hit_gate_cond_kernel(const BitmapCounts* bc, const HitParams* hp, int* gate,
-                                           cudaGraphConditionalHandle h) {
-  const volatile HitParams* v = hp;
-  cudaGraphSetConditional(h, (unsigned)hit_gate(bc, v->k, v->r0, v->pv, v->force, gate));
+  const int g[3] = {chg, ok, chg || (ok && force)};
+  out->bc = *bc;
+  for (int i = 0; i < 3; ++i) gate[i] = out->gate[i] = g[i];
+  out->digest = 0ull;
+  out->nnz = 0u;
 }
 __global__ void prune_hit_report_kernel(const BitmapCounts* bc, const int* gate, const uint64_t* digest,
                                         const uint32_t* nnz, HitReport* out) {
@@ -894,13 +886,9 @@ __global__ void prune_hit_report_kernel(const BitmapCounts* bc, const int* gate,
 }  // namespace
 
 void launch_prune_hit_gate(const BitmapCounts* bc, uint64_t k, uint64_t r0, int pv, int force_digest, int* gate,
-                           cudaStream_t s) {
-  prune_hit_gate_kernel<<<1, 1, 0, s>>>(bc, k, r0, pv, force_digest, gate);
+                           HitReport* out, cudaStream_t s) {
+  prune_hit_gate_kernel<<<1, 1, 0, s>>>(bc, k, r0, pv, force_digest, gate, out);
   note_launch();
-}
-void launch_prune_hit_gate_cond(const BitmapCounts* bc, const HitParams* hp, int* gate,
-                                cudaGraphConditionalHandle h, cudaStream_t s) {
-  prune_hit_gate_cond_kernel<<<1, 1, 0, s>>>(bc, hp, gate, h);
 }
 void launch_prune_hit_report(const BitmapCounts* bc, const int* gate, const uint64_t* digest, const uint32_t* nnz,
                              HitReport* out, cudaStream_t s) {

@@ -545,24 +545,6 @@ def test_bitmap_cpasync_variant(cuda):
     assert "2 passed" in r.stdout, r.stdout[-1000:]
 
 
-def test_hit_tail_plain_launch_variant(cuda):
-    """The temporal-reuse tail (gate, offsets scan, digest, report) runs as a
-    CUDA graph with an IF node by default; PACT_HIT_GRAPH=0 launches the same
-    kernels gated in-kernel. Both bit-exact through the re-prune schedule
-    and the changed-flag / digest-cache test."""
-    import os
-    import subprocess
-    import sys
-
-    env = dict(os.environ, PACT_HIT_GRAPH="0")
-    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
-                        os.path.abspath(__file__), "-k",
-                        "test_reprune_sequence_paths or test_prune_changed_flag_and_digest_cache"],
-                       env=env, capture_output=True, text=True, timeout=900)
-    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
-    assert "3 passed" in r.stdout, r.stdout[-1000:]
-
-
 def test_unpack_bulk_store_variant(cuda):
     """The opt-in unpack variant that stores whole chunks with one 4 KiB
     cp.async.bulk (PACT_UNPACK_BULK=1) is bit-exact through the codec tests
