@@ -296,15 +296,7 @@ __global__ void __launch_bounds__(kPuWarps * 32)
     pack_lm_kernel(const float* __restrict__ g, uint64_t len, const uint64_t* __restrict__ words,
                    const uint32_t* __restrict__ chunk_off, float* __restrict__ packed, uint64_t cb,
                    uint64_t ce, float* __restrict__ remote, P2PView v, P2PSig sg, int pdl_trigger) {
-  // data stages: the bulk-push variant keeps a third so that a chunk's
-  // remote copy may still be draining over NVLink while the next chunk is
-  // compacted and the one after lands (waits for the push two chunks back)
-  // (dynamic shared memory for that variant: 3 stages x 4 warps > 48 KiB)
-  constexpr int kDS = kPush == kPushTma ? 3 : 2;
-  extern __shared__ __align__(16) float pk_dyn[];
-  __shared__ __align__(16) float pk_static[kPush == kPushTma ? 4 : kPuWarps * kDS * kPkStage];
-  float* const pk_base = kPush == kPushTma ? pk_dyn : pk_static;
-  auto dsm = [&](int w, int st) { return pk_base + (w * kDS + st) * kPkStage; };
+  __shared__ __align__(16) float dsm[kPuWarps][2][kPkStage];
   __shared__ __align__(16) uint64_t wsm[kPuWarps][3][kWbuf];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const bool vec_ok = (((uintptr_t)g) & 15) == 0;
@@ -325,7 +317,7 @@ __global__ void __launch_bounds__(kPuWarps * 32)
     cp_commit();
     asm volatile("cp.async.wait_group 1;" ::: "memory");
     __syncwarp();
-    pack_data_issue(dsm(warp, 0), g, len, vec_ok, wsm[warp][0], c);
+    pack_data_issue(dsm[warp][0], g, len, vec_ok, wsm[warp][0], c);
     cp_commit();
     // lane-major rank of chunk i+1 computed during chunk i (as in unpack)
     uint32_t h = reinterpret_cast<const uint32_t*>(wsm[warp][0])[lane];
@@ -337,16 +329,15 @@ __global__ void __launch_bounds__(kPuWarps * 32)
       cp_commit();
       asm volatile("cp.async.wait_group 1;" ::: "memory");  // words(c+nwt), data(c) landed
       __syncwarp();
-      const int pn = pi + 1 == kDS ? 0 : pi + 1;
-      if constexpr (kPush == kPushTma) {  // the bulk push that read stage pn (kDS - 1 chunks back) is done
-        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(kDS - 2) : "memory");
+      if constexpr (kPush == kPushTma) {  // the bulk push of stage pi ^ 1 has read it
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         __syncwarp();
       }
-      if (c + nwt < ce) pack_data_issue(dsm(warp, pn), g, len, vec_ok, wsm[warp][w1], c + nwt);
+      if (c + nwt < ce) pack_data_issue(dsm[warp][pi ^ 1], g, len, vec_ok, wsm[warp][w1], c + nwt);
       cp_commit();
       const uint64_t* wc = wsm[warp][wi];
       const uint32_t base = reinterpret_cast<const uint32_t*>(wc + kChunkWords)[0];
-      float* st = dsm(warp, pi);
+      float* st = dsm[warp][pi];
       const uint32_t h_n = reinterpret_cast<const uint32_t*>(wsm[warp][w1])[lane];  // chunk c + nwt
       const uint32_t hc_n = __popc(h_n), incl_n = warp_incl_scan(hc_n);
       const uint32_t run = __shfl_sync(0xffffffffu, incl, 31);
@@ -379,7 +370,7 @@ __global__ void __launch_bounds__(kPuWarps * 32)
       if constexpr (kPush == kPushTma) push_run_bulk(remote + base - ph, st, ph, run);
       __syncwarp();  // stage pi and word buffer wi are refilled next
       wi = w1;
-      pi = pn;
+      pi ^= 1;
       h = h_n;
       hc = hc_n;
       incl = incl_n;
@@ -864,19 +855,17 @@ void launch_pack_push(const float* g, uint64_t len, const uint64_t* words, const
   // PACT_PUSH_STORES=1: float4 stores instead of bulk async copies (measured
   // c2 n=2 pack 61 vs 55-61 us: the exchange is NVLink-bound either way)
   static const bool stores = getenv("PACT_PUSH_STORES") != nullptr;
-  constexpr int kDynTma = kPuWarps * 3 * kPkStage * (int)sizeof(float);
-  static DeviceCache<int> cc;
-  int& cap = cc.get();
+  static int cap = 0;
   if (!cap)
     cap = stores ? persistent_grid(pack_lm_kernel<kPushStores>, kPuWarps)
-                 : persistent_grid_dyn(pack_lm_kernel<kPushTma>, kPuWarps, kDynTma);
+                 : persistent_grid(pack_lm_kernel<kPushTma>, kPuWarps);
   const unsigned grid = grid_for(cap, nc, kPuWarps);
   if (stores)
     pack_lm_kernel<kPushStores><<<grid, kPuWarps * 32, 0, s>>>(g, len, words, chunk_off, packed, 0, nc, remote,
                                                                v, sg, 0);
   else
-    pack_lm_kernel<kPushTma><<<grid, kPuWarps * 32, kDynTma, s>>>(g, len, words, chunk_off, packed, 0, nc,
-                                                                  remote, v, sg, 0);
+    pack_lm_kernel<kPushTma><<<grid, kPuWarps * 32, 0, s>>>(g, len, words, chunk_off, packed, 0, nc, remote, v,
+                                                            sg, 0);
   note_launch();
 }
 
