@@ -348,15 +348,23 @@ __global__ void __launch_bounds__(kPuWarps * 32)
       __syncwarp();
       // in-place compaction: per element a bit test, a predicated STS and a
       // predicated address increment
-      uint32_t sa = (uint32_t)__cvta_generic_to_shared(st + ph + incl - hc);
+      // (four independent address chains of 8 elements, started from byte
+      // popcounts: the chain of predicated increments is 8 deep, not 32)
+      uint32_t sa[4];
+      sa[0] = (uint32_t)__cvta_generic_to_shared(st + ph + incl - hc);
+      sa[1] = sa[0] + 4u * (uint32_t)__popc(h & 0xffu);
+      sa[2] = sa[0] + 4u * (uint32_t)__popc(h & 0xffffu);
+      sa[3] = sa[0] + 4u * (uint32_t)__popc(h & 0xffffffu);
 #pragma unroll
-      for (int e = 0; e < 32; ++e)
-        asm volatile(
-            "{\n .reg .pred p;\n setp.ne.u32 p, %2, 0;\n @p st.shared.f32 [%0], %1;\n"
-            " @p add.u32 %0, %0, 4;\n}"
-            : "+r"(sa)
-            : "f"(x[e]), "r"(h & (1u << e))
-            : "memory");
+      for (int e = 0; e < 8; ++e)
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          asm volatile(
+              "{\n .reg .pred p;\n setp.ne.u32 p, %2, 0;\n @p st.shared.f32 [%0], %1;\n"
+              " @p add.u32 %0, %0, 4;\n}"
+              : "+r"(sa[q])
+              : "f"(x[8 * q + e]), "r"(h & (1u << (8 * q + e)))
+              : "memory");
       __syncwarp();
       float* dst = packed + base;
 #pragma unroll 4
@@ -482,23 +490,35 @@ __global__ void __launch_bounds__(kPuWarps * 32)
     float x[32];
 #pragma unroll
     for (int e = 0; e < 32; ++e) x[e] = 0.0f;
+    // (four independent walking addresses of 8 elements each, started from
+    // byte popcounts: the predicated-increment chain is 8 deep, not 32)
+    const uint32_t q1 = (uint32_t)__popc(h & 0xffu), q2 = (uint32_t)__popc(h & 0xffffu),
+                   q3 = (uint32_t)__popc(h & 0xffffffu);
     if constexpr (kSrc == kSrcSlot) {  // + the peer's value at the same phase, kRunCap further
-      const float* sa = stage + pos0;
+      const float* sa[4] = {stage + pos0, stage + pos0 + q1, stage + pos0 + q2, stage + pos0 + q3};
 #pragma unroll
-      for (int e = 0; e < 32; ++e)
-        if (h & (1u << e)) {
-          x[e] = __fadd_rn(sa[0], sa[kRunCap]);
-          ++sa;
-        }
+      for (int e = 0; e < 8; ++e)
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (h & (1u << (8 * q + e))) {
+            x[8 * q + e] = __fadd_rn(sa[q][0], sa[q][kRunCap]);
+            ++sa[q];
+          }
     } else if constexpr (kSrc != kSrcPair) {
-      uint32_t sa = (uint32_t)__cvta_generic_to_shared(stage + pos0);
+      uint32_t sa[4];
+      sa[0] = (uint32_t)__cvta_generic_to_shared(stage + pos0);
+      sa[1] = sa[0] + 4u * q1;
+      sa[2] = sa[0] + 4u * q2;
+      sa[3] = sa[0] + 4u * q3;
 #pragma unroll
-      for (int e = 0; e < 32; ++e)
-        asm volatile(
-            "{\n .reg .pred p;\n setp.ne.u32 p, %2, 0;\n @p ld.shared.f32 %0, [%1];\n"
-            " @p add.u32 %1, %1, 4;\n}"
-            : "+f"(x[e]), "+r"(sa)
-            : "r"(h & (1u << e)));
+      for (int e = 0; e < 8; ++e)
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          asm volatile(
+              "{\n .reg .pred p;\n setp.ne.u32 p, %2, 0;\n @p ld.shared.f32 %0, [%1];\n"
+              " @p add.u32 %1, %1, 4;\n}"
+              : "+f"(x[8 * q + e]), "+r"(sa[q])
+              : "r"(h & (1u << (8 * q + e))));
     } else {  // + the peer's value (one-shot fold, n = 2)
       const float* sa = stage + pos0;
       const float* sp = psm(warp, pi) + kRunCap + run_phase(run_src<kSrc>(packed, v, rb, 1)) + pos0;

@@ -2,7 +2,10 @@
 step on rank 0: kernel, stream, start, duration -- shows whether pack(b+1),
 the exchange of b and unpack(b-1) actually overlap. torchrun, N ranks.
 
-    python -m torch.distributed.run --nproc-per-node 2 tools/bucket_timeline.py c3 16 0.75 [nccl|p2p]
+    python -m torch.distributed.run --nproc-per-node 2 tools/bucket_timeline.py c3 16 0.75 [nccl|p2p|auto]
+
+bucket MB 0 = the library's AUTO plan (equal-chunk buckets on the green-
+context SM partition when the packed vector is >= 24 MB).
 """
 import os
 import sys
@@ -23,7 +26,7 @@ def main():
     cfg = sys.argv[1]
     mb = float(sys.argv[2])
     os.environ["PACT_BUCKET_GRID_FRAC"] = sys.argv[3]
-    tr = {"nccl": 1, "p2p": 2}[sys.argv[4] if len(sys.argv) > 4 else "nccl"]
+    tr = {"auto": 0, "nccl": 1, "p2p": 2}[sys.argv[4] if len(sys.argv) > 4 else "nccl"]
     model, ratio = CFG[cfg]
     rank = int(os.environ["RANK"])
     torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)))
