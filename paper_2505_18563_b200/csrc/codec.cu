@@ -181,9 +181,7 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 //   kSrcOwner  NVLink two-shot all-gather: the run read straight from the
 //              owner's reduced chunk (owner = j / C, at most one owner
 //              boundary per run since C >= 1024).
-//   kSrcSlot   n = 2 push: the local run and the run the peer pushed into
-//              this rank's slot c (same 16-byte phase as the local run).
-constexpr int kSrcLocal = 0, kSrcPair = 1, kSrcOwner = 2, kSrcSlot = 3;
+constexpr int kSrcLocal = 0, kSrcPair = 1, kSrcOwner = 2;
 
 constexpr int kRunCap = kChunk + 4;  // a run plus its 16-byte phase
 
@@ -192,20 +190,15 @@ constexpr int kRunCap = kChunk + 4;  // a run plus its 16-byte phase
 template <int kSrc>
 __device__ __forceinline__ const float* run_src(const float* __restrict__ packed, const P2PView& v, uint32_t b,
                                                 int which) {
-  if constexpr (kSrc == kSrcLocal || kSrc == kSrcSlot) return packed + b;  // (slot: the local run's phase)
+  if constexpr (kSrc == kSrcLocal) return packed + b;
   else if constexpr (kSrc == kSrcPair) return (which ? v.packed[v.rank ^ 1] : packed) + b;
   else return v.reduced[b / v.C] + b;
 }
 
 template <int kSrc>
 __device__ __forceinline__ void issue_run(float* dst, const float* __restrict__ packed, const P2PView& v,
-                                          uint32_t b, uint32_t cnt, uint64_t c) {
-  if constexpr (kSrc == kSrcSlot) {
-    const float* a = packed + b;
-    const uint32_t ph = run_phase(a);
-    run_issue(dst + ph, a, cnt);
-    run_issue(dst + kRunCap + ph, v.packed[v.rank ^ 1] + c * kSlotFloats + ph, cnt);
-  } else if constexpr (kSrc == kSrcLocal) {
+                                          uint32_t b, uint32_t cnt) {
+  if constexpr (kSrc == kSrcLocal) {
     const float* src = packed + b;
     run_issue(dst + run_phase(src), src, cnt);
   } else if constexpr (kSrc == kSrcPair) {
@@ -239,20 +232,32 @@ __device__ __forceinline__ void issue_run(float* dst, const float* __restrict__ 
 // cells) at the destination's 16-byte phase and leaves as one coalesced run.
 constexpr int kPushNone = 0, kPushStores = 1, kPushTma = 2;
 
-// NVLink push of a staged run into the peer's slot for this chunk: every
-// 16-byte cell the run touches, the phase cell's leading garbage and the
-// last cell's trailing garbage included (the slot is private to the chunk),
-// as ONE bulk copy from a 128-byte aligned destination
-__device__ __forceinline__ void push_slot_bulk(float* __restrict__ slot, const float* st, uint32_t tot) {
-  if (tot == 0) return;
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the compaction's STS -> async proxy
-  __syncwarp();
-  if ((threadIdx.x & 31) == 0)
-    asm volatile(
-        "cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n"
-        " cp.async.bulk.commit_group;" ::"l"(slot),
-        "r"((uint32_t)__cvta_generic_to_shared(st)), "r"(((tot + 3) >> 2) * 16u)
-        : "memory");
+// NVLink push of a staged run as one bulk async copy (TMA engine, smem ->
+// peer global) for the whole 16-byte cells, scalar stores for the partial
+// head / tail cells (they are shared with the neighbouring chunks' runs).
+// The warp does not wait for the remote stores: the stage is recycled after
+// cp.async.bulk.wait_group.read, the kernel exit waits for completion.
+__device__ __forceinline__ void push_run_bulk(float* __restrict__ dst, const float* st, uint32_t ph, uint32_t run) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t tot = ph + run;
+  const uint32_t q0 = ph ? 1u : 0u, qe = tot >> 2;
+  if (ph) {
+    const uint32_t i = ph + lane;
+    if (i < 4 && i < tot) dst[i] = st[i];
+  }
+  const uint32_t t0 = 4 * (qe > q0 ? qe : q0);
+  if (t0 + lane < tot) dst[t0 + lane] = st[t0 + lane];
+  if (qe > q0) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the compaction's STS -> async proxy
+    __syncwarp();
+    if (lane == 0) {
+      asm volatile(
+          "cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n"
+          " cp.async.bulk.commit_group;" ::"l"(dst + 4 * q0),
+          "r"((uint32_t)__cvta_generic_to_shared(st + 4 * q0)), "r"((qe - q0) * 16u)
+          : "memory");
+    }
+  }
 }
 
 constexpr int kPkStage = kChunk + 4;  // a chunk, or a run plus its 16-byte phase
@@ -369,8 +374,8 @@ __global__ void __launch_bounds__(kPuWarps * 32)
       float* dst = packed + base;
 #pragma unroll 4
       for (uint32_t i = lane; i < run; i += 32) dst[i] = st[ph + i];
-      if constexpr (kPush == kPushStores) write_run(remote + c * kSlotFloats, st, ph, run);
-      if constexpr (kPush == kPushTma) push_slot_bulk(remote + c * kSlotFloats, st, ph + run);
+      if constexpr (kPush == kPushStores) write_run(remote + base - ph, st, ph, run);
+      if constexpr (kPush == kPushTma) push_run_bulk(remote + base - ph, st, ph, run);
       __syncwarp();  // stage pi and word buffer wi are refilled next
       wi = w1;
       pi ^= 1;
@@ -398,7 +403,7 @@ __global__ void __launch_bounds__(kPuWarps * 32)
 // per stage).
 template <int kSrc, int kA>
 __host__ __device__ constexpr int unpack_smem_bytes() {
-  return kPuWarps * (kA + 1) * (kSrc == kSrcPair || kSrc == kSrcSlot ? 2 : 1) * kRunCap * (int)sizeof(float);
+  return kPuWarps * (kA + 1) * (kSrc == kSrcPair ? 2 : 1) * kRunCap * (int)sizeof(float);
 }
 
 template <bool kSgd, int kSrc, int kA>
@@ -409,14 +414,14 @@ __global__ void __launch_bounds__(kPuWarps * 32)
                   uint64_t ce, P2PView v, const uint64_t* __restrict__ flags, uint64_t target,
                   P2PErr* __restrict__ err, P2PSig sg, int bulk_out) {
   constexpr int kRS = kA + 1, kWS = kA + 2;  // run / word stages
-  constexpr int kRun = kSrc == kSrcPair || kSrc == kSrcSlot ? 2 * kRunCap : kRunCap;
+  constexpr int kRun = kSrc == kSrcPair ? 2 * kRunCap : kRunCap;
   extern __shared__ __align__(16) float psm_base[];  // unpack_smem_bytes<kSrc, kA>()
   auto psm = [&](int w, int st) { return psm_base + (w * kRS + st) * kRun; };
   __shared__ __align__(16) uint64_t wsm[kPuWarps][kWS][kWbuf];
   if constexpr (kSrc != kSrcLocal) {  // peers' PACKED (one-shot) / REDUCED (two-shot) flags
     p2psync::entry_signal(v, sg);
     if (sg.trace && threadIdx.x == 0) atomicMin(&g_pair_trace[2], gtimer());
-    if (!p2psync::block_wait_flags(flags, kSrc == kSrcOwner ? kP2PReduced : kP2PPacked, v.n, target, err))
+    if (!p2psync::block_wait_flags(flags, kSrc == kSrcPair ? kP2PPacked : kP2PReduced, v.n, target, err))
       return;  // the exchange failed: no peer reads, no READ signal (LinkError on the host)
     if (sg.trace && threadIdx.x == 0) atomicMax(&g_pair_trace[3], gtimer());
   }
@@ -449,7 +454,7 @@ __global__ void __launch_bounds__(kPuWarps * 32)
     if (c + j * nwt < ce) {
       uint32_t b, n;
       offs(j, b, n);
-      issue_run<kSrc>(psm(warp, j), packed, v, b, n, c + j * nwt);
+      issue_run<kSrc>(psm(warp, j), packed, v, b, n);
     }
     cp_commit();
   }
@@ -474,7 +479,7 @@ __global__ void __launch_bounds__(kPuWarps * 32)
     if (c + kA * nwt < ce) {
       uint32_t b, n;
       offs(wa, b, n);
-      issue_run<kSrc>(psm(warp, pa), packed, v, b, n, c + kA * nwt);
+      issue_run<kSrc>(psm(warp, pa), packed, v, b, n);
     }
     cp_commit();
     const uint64_t* wc = wsm[warp][wi];
@@ -494,17 +499,7 @@ __global__ void __launch_bounds__(kPuWarps * 32)
     // byte popcounts: the predicated-increment chain is 8 deep, not 32)
     const uint32_t q1 = (uint32_t)__popc(h & 0xffu), q2 = (uint32_t)__popc(h & 0xffffu),
                    q3 = (uint32_t)__popc(h & 0xffffffu);
-    if constexpr (kSrc == kSrcSlot) {  // + the peer's value at the same phase, kRunCap further
-      const float* sa[4] = {stage + pos0, stage + pos0 + q1, stage + pos0 + q2, stage + pos0 + q3};
-#pragma unroll
-      for (int e = 0; e < 8; ++e)
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-          if (h & (1u << (8 * q + e))) {
-            x[8 * q + e] = __fadd_rn(sa[q][0], sa[q][kRunCap]);
-            ++sa[q];
-          }
-    } else if constexpr (kSrc != kSrcPair) {
+    if constexpr (kSrc != kSrcPair) {
       uint32_t sa[4];
       sa[0] = (uint32_t)__cvta_generic_to_shared(stage + pos0);
       sa[1] = sa[0] + 4u * q1;
@@ -520,11 +515,15 @@ __global__ void __launch_bounds__(kPuWarps * 32)
               : "+f"(x[8 * q + e]), "+r"(sa[q])
               : "r"(h & (1u << (8 * q + e))));
     } else {  // + the peer's value (one-shot fold, n = 2)
-      const float* sa = stage + pos0;
-      const float* sp = psm(warp, pi) + kRunCap + run_phase(run_src<kSrc>(packed, v, rb, 1)) + pos0;
+      const float* a0 = stage + pos0;
+      const float* b0 = psm(warp, pi) + kRunCap + run_phase(run_src<kSrc>(packed, v, rb, 1)) + pos0;
+      const float* sa[4] = {a0, a0 + q1, a0 + q2, a0 + q3};
+      const float* sp[4] = {b0, b0 + q1, b0 + q2, b0 + q3};
 #pragma unroll
-      for (int e = 0; e < 32; ++e)
-        if (h & (1u << e)) x[e] = __fadd_rn(*sa++, *sp++);
+      for (int e = 0; e < 8; ++e)
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (h & (1u << (8 * q + e))) x[8 * q + e] = __fadd_rn(*sa[q]++, *sp[q]++);
     }
     // (2) transpose through the consumed run buffer (XOR-swizzled 16-byte
     // cells: conflict-free both ways) into the coalesced layout: store j of
@@ -961,15 +960,7 @@ void launch_unpack_p2p(const float* packed_local, uint64_t len, const uint64_t* 
   if (!nc) return;
   // every CTA runs the flag wait and the exit count, so each gets >= 1 chunk
   // per warp 0 (grid <= ceil(nc / kPuWarps))
-  if (two_shot == 2) {
-    constexpr int kDyn = unpack_smem_bytes<kSrcSlot, 1>();
-    static DeviceCache<int> cc;
-    int& cap = cc.get();
-    if (!cap) cap = persistent_grid_dyn(unpack_kernel<false, kSrcSlot, 1>, kPuWarps, kDyn);
-    unpack_kernel<false, kSrcSlot, 1><<<grid_for(cap, nc, kPuWarps), kPuWarps * 32, kDyn, s>>>(
-        packed_local, len, words, chunk_off, scale, do_scale, out, 0.f, nullptr, 0, nc, v, flags, target,
-        err, sg, unpack_bulk_out());
-  } else if (!two_shot) {
+  if (!two_shot) {
     constexpr int kDyn = unpack_smem_bytes<kSrcPair, 1>();
     static DeviceCache<int> cc;
     int& cap = cc.get();

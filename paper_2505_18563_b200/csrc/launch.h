@@ -51,14 +51,8 @@ void pair_trace_read(unsigned long long out[5], cudaStream_t s);
 void launch_pack(const float* g, uint64_t len, const uint64_t* words, const uint32_t* chunk_off,
                  float* packed, uint64_t cb, uint64_t ce, cudaStream_t s, bool pdl_trigger = false,
                  float grid_frac = 0.f);
-// n = 2 push exchange, slot layout: chunk c's packed run goes to the peer's
-// incoming region at remote + c * kSlotFloats (+ the run's local 16-byte
-// phase), so every push starts at a 128-byte aligned NVLink address and is
-// ONE bulk copy of whole 16-byte cells (the slot is private to the chunk:
-// the padding cells it overwrites belong to nobody)
-constexpr int kSlotFloats = 1056;  // >= 1024 + 3, multiple of 32 floats (128 B)
-// pack into `packed` and chunk c's run into the peer's slot c (NVLink);
-// the last CTA publishes sg's exit flag
+// pack into `packed` and, with the same offsets, into `remote` (the peer's
+// incoming region, NVLink stores); the last CTA publishes sg's exit flag
 void launch_pack_push(const float* g, uint64_t len, const uint64_t* words, const uint32_t* chunk_off,
                       float* packed, float* remote, const P2PView& v, const P2PSig& sg, cudaStream_t s);
 // pdl: launched as a programmatic dependent of the kernel before it on the
@@ -68,11 +62,9 @@ void launch_pack_push(const float* g, uint64_t len, const uint64_t* words, const
 void launch_unpack(const float* packed, uint64_t len, const uint64_t* words,
                    const uint32_t* chunk_off, float scale, int do_scale, float* out, uint64_t cb,
                    uint64_t ce, cudaStream_t s, bool pdl = false, float grid_frac = 0.f);
-// unpack with the exchange fused in (NVLink P2P, B == 1): mode 0 (n == 2)
-// sums the local and the peer's packed runs (waits PACKED); mode 1
-// (two-shot) reads each run from its owner's reduced chunk (waits REDUCED;
-// needs C >= 1024); mode 2 (n == 2 push) sums the local run and the run the
-// peer pushed into this rank's slot c (v.packed[peer] = the slot region).
+// unpack with the exchange fused in (NVLink P2P, B == 1): one-shot (n == 2)
+// sums the local and the peer's packed runs (waits PACKED); two-shot reads
+// each run from its owner's reduced chunk (waits REDUCED; needs C >= 1024).
 // Publishes sg's exit flag (READ) when every CTA is done.
 void launch_unpack_p2p(const float* packed_local, uint64_t len, const uint64_t* words,
                        const uint32_t* chunk_off, float scale, int do_scale, float* out, const P2PView& v,

@@ -2400,10 +2400,7 @@ pact_status pact_masked_allreduce(pact_comm* c, pact_ctx* ctx, const float* grad
   // incoming region as well; unpack folds two LOCAL runs). No speculative
   // pack in this mode: PACKED is published by the pack itself.
   static const bool push_env = !getenv("PACT_P2P_PULL");
-  // (its slot regions hold one padded chunk each: at most 4 GiB per region,
-  // i.e. len <= ~1G elements; above, the pull fold)
-  const bool p2p_push = push_env && p2p_try && n == 2 && !p2p_buckets &&
-                        m->ntiles * (uint64_t)pactk::kSlotFloats * 4 <= (4ull << 30);
+  const bool p2p_push = push_env && p2p_try && n == 2 && !p2p_buckets;
   // NCCL buckets: bucket_bytes, or the AUTO choice above. Round 1 measured
   // bucketing losing (32 MiB buckets cut by packed bytes on full codec
   // grids: c4 n=2 0.886 vs 0.668 ms): the persistent pack/unpack grids held
@@ -2496,12 +2493,8 @@ pact_status pact_masked_allreduce(pact_comm* c, pact_ctx* ctx, const float* grad
   }
 
   int nbuckets = 0, transport = c ? PACT_TRANSPORT_NCCL : 0;
-  // the n = 2 push lands each chunk's run in a fixed slot of the peer's
-  // incoming region (pactk::kSlotFloats per chunk): size the regions for it
-  const uint64_t p2p_need = p2p_push ? std::max<uint64_t>(m->nnz, m->ntiles * (uint64_t)pactk::kSlotFloats)
-                                     : m->nnz;
-  if (agree && p2p_try) TRY(p2p_setup(c, p2p_need, s));  // collective, no-op once set up
-  if (agree && p2p_try && c->p2p.ok && c->p2p.cap >= p2p_need) {
+  if (agree && p2p_try) TRY(p2p_setup(c, m->nnz, s));  // collective, no-op once set up
+  if (agree && p2p_try && c->p2p.ok && c->p2p.cap >= m->nnz) {
     // NVLink pull exchange in the reference fold order (p2p.cu): one-shot at
     // n = 2, two-shot (reduce-scatter + all-gather by peer loads) above.
     // Regions alternate by step parity; READ(k-2) guards their reuse.
@@ -2599,13 +2592,13 @@ pact_status pact_masked_allreduce(pact_comm* c, pact_ctx* ctx, const float* grad
       mark(0);
       mark(1);
       pactk::P2PView vin = v;
-      vin.packed[peer] = p2p_reduced(p, c->rank, par);  // this rank's incoming slots
+      vin.packed[peer] = p2p_reduced(p, c->rank, par);  // this rank's incoming region
       pactk::P2PSig sgu;
       sgu.exit_kind = pactk::kP2PRead;
       sgu.exit_val = k1;
       sgu.counter = sgp.counter;
       sgu.trace = trace;
-      pactk::launch_unpack_p2p(mine, len, m->words, m->tile_off, scale, scale != 1.0f, out, vin, 2, myflags,
+      pactk::launch_unpack_p2p(mine, len, m->words, m->tile_off, scale, scale != 1.0f, out, vin, 0, myflags,
                                fval(0), err, sgu, s);
       if (trace) {
         unsigned long long t[5];
