@@ -261,6 +261,13 @@ pact_status pact_gse(pact_ctx* ctx, const float* g, uint64_t len, const pact_mas
 pact_status pact_pack(pact_ctx* ctx, const float* g, uint64_t len, const pact_mask* m,
                       float* packed, uint64_t tile_begin, uint64_t tile_end, pact_stream_t stream);
 
+/* Diagnostic (NVLink counters of the n = 2 push exchange under ncu, one
+ * process, no peer flags): pack() into `packed` and, with the same offsets,
+ * into `remote` -- memory of another GPU (peer access is enabled here) --
+ * with the push kernel the 2-rank exchange uses. No signals, no waits. */
+pact_status pact_debug_pack_push(pact_ctx* ctx, const float* g, uint64_t len, const pact_mask* m,
+                                 float* packed, float* remote, pact_stream_t stream);
+
 /* codec.cpp:27-38 unpack: PACT_E_MASK_MISMATCH if packed_digest != digest
  * (skipped when check_digest = 0), PACT_E_CORRUPT_PAYLOAD if count != nnz;
  * out[i] = bit ? packed[rank(i)] * scale : +0.0f (scale 1 => bit copy;

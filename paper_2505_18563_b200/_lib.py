@@ -84,6 +84,7 @@ SIGNATURES = {
     "pact_prune_magnitude_segmented": (C.c_int, [vp, vp, C.c_uint64, u64p, C.c_uint64, C.c_float, vp, vp]),
     "pact_gse": (C.c_int, [vp, vp, C.c_uint64, vp, vp, vp]),
     "pact_pack": (C.c_int, [vp, vp, C.c_uint64, vp, vp, C.c_uint64, C.c_uint64, vp]),
+    "pact_debug_pack_push": (C.c_int, [vp, vp, C.c_uint64, vp, vp, vp, vp]),
     "pact_unpack": (C.c_int, [vp, vp, C.c_uint64, C.c_uint64, C.c_int, vp, C.c_float, vp,
                               C.c_uint64, C.c_uint64, vp]),
     "pact_unpack_sgd": (C.c_int, [vp, vp, C.c_uint64, vp, C.c_float, C.c_float, vp, vp, vp]),

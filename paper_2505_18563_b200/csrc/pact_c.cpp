@@ -1631,6 +1631,25 @@ pact_status pact_pack(pact_ctx* ctx, const float* g, uint64_t len, const pact_ma
   return PACT_OK;
 }
 
+pact_status pact_debug_pack_push(pact_ctx* ctx, const float* g, uint64_t len, const pact_mask* m,
+                                 float* packed, float* remote, pact_stream_t stream) {
+  if (!ctx || !m || (len && (!g || !packed || !remote))) return fail(PACT_E_INVALID_ARG, "null args");
+  if (len != m->len) return fail(PACT_E_SHAPE_MISMATCH, "gradient/mask length mismatch");
+  TRY(set_device(ctx));
+  cudaPointerAttributes a{};
+  CUDA_TRY(cudaPointerGetAttributes(&a, remote));
+  if (a.type == cudaMemoryTypeDevice && a.device != ctx->device) {
+    const cudaError_t e = cudaDeviceEnablePeerAccess(a.device, 0);
+    if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) CUDA_TRY(e);
+    cudaGetLastError();
+  }
+  pactk::P2PView v{};
+  pactk::P2PSig sg;  // no entry / exit signal
+  pactk::launch_pack_push(g, len, m->words, m->tile_off, packed, remote, v, sg, stream);
+  CUDA_TRY(cudaGetLastError());
+  return PACT_OK;
+}
+
 pact_status pact_unpack(pact_ctx* ctx, const float* packed, uint64_t count, uint64_t packed_digest,
                         int check_digest, const pact_mask* m, float scale, float* out,
                         uint64_t tb, uint64_t te, pact_stream_t stream) {
