@@ -17,7 +17,7 @@ import sys
 import pytest
 
 from conftest import ROOT
-from test_multi_gpu import _free_port
+from test_multi_gpu import _free_port, _torchrun
 
 
 def _planning_worker(rank, world, port, q):
@@ -142,9 +142,6 @@ def test_ddp_hook_multi_gpu(pb):
     n = torch.cuda.device_count()
     if n < 2:
         pytest.skip("needs >= 2 GPUs (run with gpurun --gpus 2)")
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
-           "--master-addr=127.0.0.1", f"--master-port={_free_port()}",
-           os.path.join(ROOT, "tests", "ddp_worker.py")]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    r = _torchrun(2, os.path.join(ROOT, "tests", "ddp_worker.py"))
     print(r.stdout[-4000:], r.stderr[-4000:])
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]

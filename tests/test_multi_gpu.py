@@ -25,6 +25,19 @@ def _free_port():
     return p
 
 
+def _torchrun(nproc, script, env=None, timeout=600):
+    """torchrun on 127.0.0.1 with a fresh port; retried (new port) when the
+    rendezvous store cannot bind it (EADDRINUSE: a port probed free can be
+    taken, or in TIME_WAIT, by the time torchrun listens)."""
+    for _ in range(4):
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+               "--master-addr=127.0.0.1", f"--master-port={_free_port()}", script]
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, cwd=ROOT, env=env)
+        if r.returncode == 0 or "EADDRINUSE" not in r.stderr:
+            return r
+    return r
+
+
 def _gloo_vote_worker(rank, world, port, q):
     import torch.distributed as dist
 
@@ -96,14 +109,10 @@ def test_nccl_masked_allreduce_multi_gpu(pb):
     if n < 2:
         pytest.skip("needs >= 2 GPUs (run with gpurun --gpus 2)")
     world = min(n, 4)
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
-           "--master-addr=127.0.0.1", f"--master-port={_free_port()}",
-           os.path.join(ROOT, "tests", "mp_masked_worker.py")]
     # default exchange, then the opt-in unpack-fused P2P consumer (PACT_P2P_FUSED)
     for extra in ({}, {"PACT_P2P_FUSED": "1"}):
         env = dict(os.environ, **extra)
-        cmd[6] = f"--master-port={_free_port()}"
-        r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
+        r = _torchrun(world, os.path.join(ROOT, "tests", "mp_masked_worker.py"), env=env)
         print(r.stdout[-4000:], r.stderr[-4000:])
         assert r.returncode == 0, str(extra) + r.stdout[-2000:] + r.stderr[-2000:]
 
