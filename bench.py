@@ -591,7 +591,11 @@ def main():
     if br and br[0][1] > 0:
         med = [statistics.median(x[k] for x in br) * 1e6 for k in range(4)]
         stages["step_breakdown_us"] = {"total": round(med[0], 1), "pack": round(med[1], 1),
-                                       "exchange": round(med[2], 1), "unpack": round(med[3], 1)}
+                                       "exchange": round(med[2], 1), "unpack": round(med[3], 1),
+                                       "transport": ["none", "nccl", "nvlink-p2p"][rr.stats.transport]}
+        if rr.stats.transport == 2:  # the NVLink exchange is fused into pack and unpack: no stage of its own
+            stages["step_breakdown_us"]["note"] = ("nvlink-p2p: the push is inside 'pack', the peer wait "
+                                                   "and fold inside 'unpack'")
     if reprune:
         # the prune paths on their own (prune.cu; DESIGN 3a): threshold reuse,
         # A.9 (the headline's), a dense drift that moves the threshold and
@@ -739,7 +743,8 @@ def main():
                 "tx_vs_algorithmic": round((nv1["tx"] - nv0["tx"]) / kx / alg_x, 3),
                 "dense_tx_bytes_per_allreduce": int((nvd1["tx"] - nvd0["tx"]) / kx),
                 "dense_algorithmic_bytes_per_rank": int(4 * n * f)}
-        bx = stages.get("step_breakdown_us", {}).get("exchange", 0.0) * 1e-6
+        sb = stages.get("step_breakdown_us", {})
+        bx = sb.get("exchange", 0.0) * 1e-6 if sb.get("transport") == "nccl" else 0.0
         if bx > 0:  # NCCL transport: the exchange timed directly inside the step (events around it)
             extra["exchange_in_step_us"] = round(bx * 1e6, 1)
             extra["exchange_in_step_busbw_gbs"] = round(4 * nnz * f / bx / 1e9, 1)
