@@ -230,11 +230,7 @@ __device__ __forceinline__ void issue_run(float* dst, const float* __restrict__ 
 // cp.async writes and the lane-major LDS.128 reads are conflict-free; the
 // compacted run is written back in place (after every lane has read its
 // cells) at the destination's 16-byte phase and leaves as one coalesced run.
-// kPushSeg: no peer writes in the kernel; after each chunk's run is stored
-// locally the warp bumps seg_cnt[iteration] (release), and a concurrent
-// copier kernel streams every completed iteration's packed range to the peer
-// with coalesced stores (push_copy_kernel)
-constexpr int kPushNone = 0, kPushStores = 1, kPushTma = 2, kPushSeg = 3;
+constexpr int kPushNone = 0, kPushStores = 1, kPushTma = 2;
 
 // NVLink push of a staged run as one bulk async copy (TMA engine, smem ->
 // peer global) for the whole 16-byte cells, scalar stores for the partial
@@ -299,8 +295,7 @@ template <int kPush>
 __global__ void __launch_bounds__(kPuWarps * 32)
     pack_lm_kernel(const float* __restrict__ g, uint64_t len, const uint64_t* __restrict__ words,
                    const uint32_t* __restrict__ chunk_off, float* __restrict__ packed, uint64_t cb,
-                   uint64_t ce, float* __restrict__ remote, P2PView v, P2PSig sg, int pdl_trigger,
-                   unsigned* __restrict__ seg_cnt) {
+                   uint64_t ce, float* __restrict__ remote, P2PView v, P2PSig sg, int pdl_trigger) {
   __shared__ __align__(16) float dsm[kPuWarps][2][kPkStage];
   __shared__ __align__(16) uint64_t wsm[kPuWarps][3][kWbuf];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -312,9 +307,8 @@ __global__ void __launch_bounds__(kPuWarps * 32)
   // `packed`. Only when the caller launches one: a PDL-capable successor of
   // another kind (e.g. a collective kernel) must not be let in early.
   if (pdl_trigger) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  if constexpr (kPush != kPushNone && kPush != kPushSeg)
+  if constexpr (kPush != kPushNone)
     if (sg.trace && threadIdx.x == 0) atomicMin(&g_pair_trace[0], gtimer());
-  uint32_t iter = 0;  // kPushSeg: the warp's loop iteration (chunks c0 + iter * nwt)
   if (c < ce) {
     // prologue: words(c0), words(c1), data(c0)
     offs_words_issue(wsm[warp][0], words, chunk_off, c);
@@ -383,10 +377,6 @@ __global__ void __launch_bounds__(kPuWarps * 32)
       if constexpr (kPush == kPushStores) write_run(remote + base - ph, st, ph, run);
       if constexpr (kPush == kPushTma) push_run_bulk(remote + base - ph, st, ph, run);
       __syncwarp();  // stage pi and word buffer wi are refilled next
-      if constexpr (kPush == kPushSeg) {  // the run is stored: publish it to the copier
-        if (lane == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(seg_cnt + iter) : "memory");
-        ++iter;
-      }
       wi = w1;
       pi ^= 1;
       h = h_n;
@@ -399,7 +389,7 @@ __global__ void __launch_bounds__(kPuWarps * 32)
       __syncwarp();
     }
   }
-  if constexpr (kPush == kPushStores || kPush == kPushTma) {
+  if constexpr (kPush != kPushNone) {
     p2psync::exit_signal(v, sg);  // PACKED: every CTA's remote stores are done
     if (sg.trace && threadIdx.x == 0) atomicMax(&g_pair_trace[1], gtimer());
   }
@@ -876,95 +866,7 @@ void launch_pack(const float* g, uint64_t len, const uint64_t* words, const uint
   if (!cap) cap = persistent_grid(pack_lm_kernel<kPushNone>, kPuWarps);
   const int c = grid_frac > 0.f ? std::max(1, (int)(cap * grid_frac)) : cap;
   pack_lm_kernel<kPushNone><<<grid_for(c, ce - cb, kPuWarps), kPuWarps * 32, 0, s>>>(
-      g, len, words, chunk_off, packed, cb, ce, nullptr, P2PView{}, P2PSig{}, pdl_trigger ? 1 : 0, nullptr);
-  note_launch();
-}
-
-namespace {
-// Streams the pack's completed iterations to the peer: iteration k of the
-// persistent pack covers chunks [k nwt, (k+1) nwt), whose packed values are
-// the contiguous range [chunk_off[k nwt], chunk_off[(k+1) nwt]). All copier
-// CTAs wait for seg_cnt[k] to reach the number of warps with a chunk in it,
-// then each copies its slice with 16-byte L2 loads and peer stores (same
-// 16-byte phase on both sides: both buffers are region bases + offset).
-// The last CTA publishes PACKED (sg exit) after every CTA's peer stores.
-__global__ void __launch_bounds__(256)
-    push_copy_kernel(const float* __restrict__ packed, float* __restrict__ remote,
-                     const uint32_t* __restrict__ chunk_off, uint64_t nc, uint64_t nwt,
-                     const unsigned* __restrict__ seg_cnt, P2PView v, P2PSig sg, P2PErr* __restrict__ err) {
-  __shared__ int s_ok;
-  const uint64_t K = (nc + nwt - 1) / nwt;
-  const uint64_t G = gridDim.x, gt = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x, stride = G * blockDim.x;
-  bool ok = true;
-  for (uint64_t k = 0; k < K && ok; ++k) {
-    const uint64_t c0 = k * nwt, c1 = c0 + nwt < nc ? c0 + nwt : nc;
-    if (threadIdx.x == 0) {
-      const unsigned want = (unsigned)(c1 - c0);
-      const uint64_t t0 = p2psync::globaltimer();
-      int good = 1;
-      while (true) {
-        unsigned x;
-        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(x) : "l"(seg_cnt + k) : "memory");
-        if (x >= want) break;
-        if (p2psync::globaltimer() - t0 > err->timeout_ns) {  // the pack stalled: fail the exchange
-          atomicExch(&err->flag, 1);
-          if (err->host) *err->host = 1;
-          __threadfence_system();
-          good = 0;
-          break;
-        }
-        __nanosleep(32);
-      }
-      s_ok = good;
-    }
-    __syncthreads();
-    ok = s_ok != 0;
-    if (!ok) break;
-    const uint64_t o0 = __ldcg(chunk_off + c0), o1 = __ldcg(chunk_off + c1);
-    const uint64_t a0 = (o0 + 3) & ~3ull, a1 = o1 & ~3ull;
-    if (a0 >= a1) {  // short range: scalar
-      for (uint64_t i = o0 + gt; i < o1; i += stride) remote[i] = __ldcg(packed + i);
-    } else {
-      for (uint64_t i = o0 + gt; i < a0; i += stride) remote[i] = __ldcg(packed + i);
-      const float4* s4 = reinterpret_cast<const float4*>(packed + a0);
-      float4* d4 = reinterpret_cast<float4*>(remote + a0);
-      const uint64_t n4 = (a1 - a0) >> 2;
-      for (uint64_t i = gt; i < n4; i += stride) d4[i] = __ldcg(s4 + i);
-      for (uint64_t i = a1 + gt; i < o1; i += stride) remote[i] = __ldcg(packed + i);
-    }
-    __syncthreads();
-  }
-  if (ok) p2psync::exit_signal(v, sg);
-}
-}  // namespace
-
-unsigned pack_seg_warps(uint64_t len, float grid_frac) {
-  const uint64_t nc = (len + kChunk - 1) / kChunk;
-  if (!nc) return 0;
-  static DeviceCache<int> cc;
-  int& cap = cc.get();
-  if (!cap) cap = persistent_grid(pack_lm_kernel<kPushSeg>, kPuWarps);
-  const int c = std::max(1, (int)(cap * grid_frac));
-  return grid_for(c, nc, kPuWarps) * kPuWarps;
-}
-
-unsigned launch_pack_seg(const float* g, uint64_t len, const uint64_t* words, const uint32_t* chunk_off,
-                         float* packed, unsigned* seg_cnt, float grid_frac, cudaStream_t s) {
-  const uint64_t nc = (len + kChunk - 1) / kChunk;
-  if (!nc) return 0;
-  const unsigned grid = pack_seg_warps(len, grid_frac) / kPuWarps;
-  pack_lm_kernel<kPushSeg><<<grid, kPuWarps * 32, 0, s>>>(g, len, words, chunk_off, packed, 0, nc, nullptr,
-                                                          P2PView{}, P2PSig{}, 0, seg_cnt);
-  note_launch();
-  return grid * kPuWarps;
-}
-
-void launch_push_copy(const float* packed, float* remote, const uint32_t* chunk_off, uint64_t len, uint64_t nwt,
-                      const unsigned* seg_cnt, const P2PView& v, const P2PSig& sg, P2PErr* err, int ctas,
-                      cudaStream_t s) {
-  const uint64_t nc = (len + kChunk - 1) / kChunk;
-  if (!nc || !nwt) return;
-  push_copy_kernel<<<ctas, 256, 0, s>>>(packed, remote, chunk_off, nc, nwt, seg_cnt, v, sg, err);
+      g, len, words, chunk_off, packed, cb, ce, nullptr, P2PView{}, P2PSig{}, pdl_trigger ? 1 : 0);
   note_launch();
 }
 
@@ -982,10 +884,10 @@ void launch_pack_push(const float* g, uint64_t len, const uint64_t* words, const
   const unsigned grid = grid_for(cap, nc, kPuWarps);
   if (stores)
     pack_lm_kernel<kPushStores><<<grid, kPuWarps * 32, 0, s>>>(g, len, words, chunk_off, packed, 0, nc, remote,
-                                                               v, sg, 0, nullptr);
+                                                               v, sg, 0);
   else
     pack_lm_kernel<kPushTma><<<grid, kPuWarps * 32, 0, s>>>(g, len, words, chunk_off, packed, 0, nc, remote, v,
-                                                            sg, 0, nullptr);
+                                                            sg, 0);
   note_launch();
 }
 

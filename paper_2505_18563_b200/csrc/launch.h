@@ -55,18 +55,6 @@ void launch_pack(const float* g, uint64_t len, const uint64_t* words, const uint
 // incoming region, NVLink stores); the last CTA publishes sg's exit flag
 void launch_pack_push(const float* g, uint64_t len, const uint64_t* words, const uint32_t* chunk_off,
                       float* packed, float* remote, const P2PView& v, const P2PSig& sg, cudaStream_t s);
-// n = 2 push with a separate copier (PACT_P2P_COPIER=<ctas>): the pack on
-// grid_frac of its persistent grid bumps seg_cnt[k] (zeroed by the caller,
-// ceil(nchunks / nwt) counters) as its warps store iteration k's runs, and
-// returns nwt (warps in the grid); the copier streams each completed
-// iteration's packed range into `remote` (same offsets) with coalesced
-// stores, then publishes sg's exit flag (PACKED).
-unsigned pack_seg_warps(uint64_t len, float grid_frac);  // nwt the launch below will use
-unsigned launch_pack_seg(const float* g, uint64_t len, const uint64_t* words, const uint32_t* chunk_off,
-                         float* packed, unsigned* seg_cnt, float grid_frac, cudaStream_t s);
-void launch_push_copy(const float* packed, float* remote, const uint32_t* chunk_off, uint64_t len, uint64_t nwt,
-                      const unsigned* seg_cnt, const P2PView& v, const P2PSig& sg, P2PErr* err, int ctas,
-                      cudaStream_t s);
 // pdl: launched as a programmatic dependent of the kernel before it on the
 // stream (which must not write words / chunk_off): its CTAs start while the
 // predecessor drains and load their first mask words, then wait

@@ -154,7 +154,6 @@ struct pact_ctx {
   DevBuf tern;      // ternary: [smax u32][err i32][pad][own block][n gathered blocks]
   DevBuf f16;       // binary16 ring: send x2, recv, n gathered chunks
   DevBuf topk;      // TopK: [own idx k][own val k][n gathered blocks] + f64 accumulator
-  DevBuf seg_cnt;   // n = 2 copier push: per-iteration completion counters of the pack
   pact_mask* topk_sel = nullptr;  // TopK selection bitmap (prune machinery)
   pact_mask* topk_union = nullptr;  // TopK aggregate: union of the ranks' selections
   HostBuf pin;      // small pinned readbacks
@@ -841,7 +840,7 @@ pact_status pact_ctx_destroy(pact_ctx* ctx) {
   cudaSetDevice(ctx->device);
   cudaDeviceSynchronize();
   for (DevBuf* b : {&ctx->ws_small, &ctx->cand, &ctx->state, &ctx->seg_ws, &ctx->digest_scratch, &ctx->packed,
-                    &ctx->grad_stage, &ctx->out_stage, &ctx->tern, &ctx->f16, &ctx->topk, &ctx->seg_cnt})
+                    &ctx->grad_stage, &ctx->out_stage, &ctx->tern, &ctx->f16, &ctx->topk})
     b->release();
   if (ctx->topk_sel) pact_mask_destroy(ctx->topk_sel);
   if (ctx->topk_union) pact_mask_destroy(ctx->topk_union);
@@ -2593,54 +2592,6 @@ pact_status pact_masked_allreduce(pact_comm* c, pact_ctx* ctx, const float* grad
       mark(2);
       p.k = k1;
       nbuckets = Bc;
-      transport = PACT_TRANSPORT_P2P;
-      goto p2p_done;
-    }
-    static const int copier_ctas = [] {  // PACT_P2P_COPIER=<ctas>: push by a concurrent copier kernel
-      const char* e = getenv("PACT_P2P_COPIER");
-      return e ? std::max(0, std::min(148, atoi(e))) : 0;
-    }();
-    if (B == 1 && p2p_push && copier_ctas > 0) {
-      // the pack runs at full speed on most of the SMs into this rank's
-      // packed region and counts finished iterations; a copier on a few SMs
-      // (launched first, so its CTAs are resident) streams each finished
-      // iteration's packed range to the peer's incoming region with
-      // coalesced 16-byte stores and publishes PACKED; the caller's stream
-      // joins the copier before the pair unpack (which then only waits for
-      // the peer's PACKED)
-      const int peer = c->rank ^ 1;
-      const float frac = 1.0f - (float)(copier_ctas + 4) / (float)sm_count_host();
-      const unsigned nwt = pactk::pack_seg_warps(len, frac);
-      const uint64_t K = nwt ? (m->ntiles + nwt - 1) / nwt : 0;
-      TRY(ctx->seg_cnt.ensure(std::max<uint64_t>(1, K) * 4));
-      unsigned* segc = ctx->seg_cnt.as<unsigned>();
-      CUDA_TRY(cudaMemsetAsync(segc, 0, std::max<uint64_t>(1, K) * 4, s));
-      cudaStream_t xs = ctx->aux[0];
-      cudaEvent_t e0 = pool_event(ctx, 1), e1 = pool_event(ctx, 2);
-      CUDA_TRY(cudaEventRecord(e0, s));
-      CUDA_TRY(cudaStreamWaitEvent(xs, e0, 0));
-      pactk::P2PSig sgc;
-      sgc.exit_kind = pactk::kP2PPacked;
-      sgc.exit_val = fval(0);
-      sgc.counter = p2p_counter(p, c->rank);
-      pactk::launch_push_copy(mine, p2p_reduced(p, peer, par), m->tile_off, len, nwt, segc, v, sgc, err,
-                              copier_ctas, xs);
-      CUDA_TRY(cudaEventRecord(e1, xs));
-      pactk::launch_pack_seg(grad, len, m->words, m->tile_off, mine, segc, frac, s);
-      mark(0);
-      CUDA_TRY(cudaStreamWaitEvent(s, e1, 0));
-      mark(1);
-      pactk::P2PView vin = v;
-      vin.packed[peer] = p2p_reduced(p, c->rank, par);  // this rank's incoming region
-      pactk::P2PSig sgu;
-      sgu.exit_kind = pactk::kP2PRead;
-      sgu.exit_val = k1;
-      sgu.counter = p2p_counter(p, c->rank);
-      pactk::launch_unpack_p2p(mine, len, m->words, m->tile_off, scale, scale != 1.0f, out, vin, 0, myflags,
-                               fval(0), err, sgu, s);
-      mark(2);
-      p.k = k1;
-      nbuckets = 1;
       transport = PACT_TRANSPORT_P2P;
       goto p2p_done;
     }
