@@ -120,6 +120,13 @@ int main() {
   run("remote READ float4 ld.cg  (GPU1 -> GPU0)", [&] { rd4<<<grid, blk>>>((float4*)a1, (float4*)b0, n / 4); });
   run("remote WRITE float4        (GPU0 -> GPU1)", [&] { wr4<<<grid, blk>>>((float4*)a0, (float4*)a1, n / 4); });
   run("remote WRITE f32 coalesced (GPU0 -> GPU1)", [&] { wr1<<<grid, blk>>>(a0, a1, n); });
+  // how few SMs saturate a one-way NVLink push (float4 stores, 256 MB)
+  for (int g : {8, 16, 32, 64})
+    for (int per : {1, 4}) {
+      char nm[96];
+      snprintf(nm, sizeof nm, "remote WRITE float4, %d SMs x %d CTAs", g, per);
+      run(nm, [&] { wr4<<<g * per, 1024 / per, 0>>>((float4*)a0, (float4*)a1, n / 4); });
+    }
   run("remote WRITE f32 x4/thread strided", [&] { wr1x4<<<grid, blk>>>(a0, a1, n / 4); });
   run("remote WRITE f32 coalesced, +4B offset", [&] { wr1_off<<<grid, blk>>>(a0, a1, n); });
   run("cudaMemcpyPeer GPU0 -> GPU1", [&] { cudaMemcpyPeerAsync(a1, 1, a0, 0, bytes); });
