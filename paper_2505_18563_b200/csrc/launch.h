@@ -290,6 +290,10 @@ void launch_seg_select(const SegInfo* info, SegState* st, uint32_t nseg, const u
 // per-chunk tie counts and kept counts, per-layer b_lt / b_eq
 void launch_seg_bitmap(const float* w, uint64_t len, const SegInfo* info, SegState* st, const uint32_t* chunk_seg,
                        uint64_t* words, uint64_t* tie_words, uint32_t* ties, uint32_t* chunk_popc, cudaStream_t s);
+// per-layer temporal reuse: after a bitmap pass at the previous thresholds,
+// every non-trivial layer whose T is still its k-th key (b_lt < k <= b_lt +
+// b_eq) takes c_lt = b_lt, r = k - b_lt; any other sets *miss
+void launch_seg_verify(const SegInfo* info, SegState* st, uint32_t nseg, int* miss, cudaStream_t s);
 void launch_seg_tiebase(const SegInfo* info, SegState* st, uint32_t nseg, const uint64_t* tie_words,
                         const uint32_t* ties, const uint32_t* tie_prefix, cudaStream_t s);
 void launch_seg_tiefix(uint64_t len, const SegInfo* info, const SegState* st, const uint32_t* chunk_seg,

@@ -165,6 +165,11 @@ struct pact_ctx {
 
 struct pact_mask {
   pact_ctx* ctx = nullptr;
+  // per-layer temporal reuse: the last segmented prune's layer table and
+  // resolved per-layer thresholds (valid while the table and ratio repeat)
+  std::vector<uint64_t> seg_key;
+  float seg_ratio = -1.0f;
+  std::vector<pactk::SegState> seg_states;
   uint64_t len = 0, nwords = 0, ntiles = 0;
   uint64_t* words = nullptr;
   uint32_t* tile_off = nullptr;   // ntiles + 1
@@ -1541,9 +1546,51 @@ pact_status pact_prune_magnitude_segmented(pact_ctx* ctx, const float* w, uint64
   auto* d_tiles = reinterpret_cast<pactk::SegTile*>(ws + o_tiles);
   auto* d_cand = reinterpret_cast<uint32_t*>(ws + o_cand);
   CUDA_TRY(cudaMemcpyAsync(d_info, info.data(), nseg * sizeof(pactk::SegInfo), cudaMemcpyHostToDevice, s));
+  CUDA_TRY(cudaMemcpyAsync(d_cs, chunk_seg.data(), chunk_seg.size() * 4, cudaMemcpyHostToDevice, s));
+  uint32_t* ties = out->ties[0].as<uint32_t>();
+  uint32_t* pin32 = ctx->pin.as<uint32_t>();
+  std::vector<pactk::SegState> hst(nseg);
+  // (0) temporal reuse (same layer table and ratio as the last call): one
+  // bitmap pass at every layer's previous threshold verifies all of them
+  // at once; the tie ranks and offsets follow as in (5)-(6) below. Any
+  // layer whose k-th key moved sends the whole call down the full path.
+  const std::vector<uint64_t> key(seg, seg + nseg + 1);
+  if (out->seg_ratio == ratio && out->seg_key == key && out->seg_states.size() == nseg) {
+    std::vector<pactk::SegState> prev = out->seg_states;
+    for (auto& x : prev) x.b_lt = x.b_eq = 0;
+    int* miss = &ctx->ws_small.as<Small>()->changed;
+    CUDA_TRY(cudaMemcpyAsync(d_st, prev.data(), nseg * sizeof(pactk::SegState), cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaMemsetAsync(miss, 0, 4, s));
+    pactk::launch_seg_bitmap(w, len, d_info, d_st, d_cs, out->words, out->tie_words.as<uint64_t>(), ties,
+                             out->tile_popc, s);
+    pactk::launch_seg_verify(d_info, d_st, (uint32_t)nseg, miss, s);
+    TRY(scan(ctx, ties, nc, out->tie_prefix.as<uint32_t>(), s));
+    pactk::launch_seg_tiebase(d_info, d_st, (uint32_t)nseg, out->tie_words.as<uint64_t>(), ties,
+                              out->tie_prefix.as<uint32_t>(), s);
+    pactk::launch_seg_tiefix(len, d_info, d_st, d_cs, out->words, out->tie_words.as<uint64_t>(), ties,
+                             out->tie_prefix.as<uint32_t>(), out->tile_popc, s);
+    TRY(scan(ctx, out->tile_popc, nc, out->tile_off, s));
+    CUDA_TRY(cudaMemcpyAsync(pin32, out->tile_off + nc, 4, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaMemcpyAsync(pin32 + 1, miss, 4, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaMemcpyAsync(hst.data(), d_st, nseg * sizeof(pactk::SegState), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaStreamSynchronize(s));
+    if (pin32[1] == 0) {
+      out->nnz = pin32[0];
+      out->host_tile_off_valid = 0;
+      out->changed = 1;  // (no per-bit change record on this path: the digest decides)
+      out->digest_valid = 0;
+      out->spec_valid = 0;
+      out->seg_states = hst;
+      if (out->nnz != kept)
+        return fail(PACT_E_RUN_FAILURE, "per-layer prune kept %llu, expected %llu",
+                    (unsigned long long)out->nnz, (unsigned long long)kept);
+      return PACT_OK;
+    }
+  }
+  out->seg_states.clear();
   CUDA_TRY(cudaMemcpyAsync(d_st, st0.data(), nseg * sizeof(pactk::SegState), cudaMemcpyHostToDevice, s));
   CUDA_TRY(cudaMemsetAsync(d_fill, 0, nseg * 8, s));
-  CUDA_TRY(cudaMemcpyAsync(d_cs, chunk_seg.data(), chunk_seg.size() * 4, cudaMemcpyHostToDevice, s));
   if (!tiles.empty())
     CUDA_TRY(cudaMemcpyAsync(d_tiles, tiles.data(), tiles.size() * sizeof(pactk::SegTile), cudaMemcpyHostToDevice,
                              s));
@@ -1552,7 +1599,6 @@ pact_status pact_prune_magnitude_segmented(pact_ctx* ctx, const float* w, uint64
   pactk::launch_seg_count(w, d_info, d_st, d_tiles, (uint32_t)tiles.size(), d_cand, d_fill, s);
   pactk::launch_seg_select(d_info, d_st, (uint32_t)nseg, d_cand, d_fill, s);
   CUDA_TRY(cudaGetLastError());
-  std::vector<pactk::SegState> hst(nseg);
   CUDA_TRY(cudaMemcpyAsync(hst.data(), d_st, nseg * sizeof(pactk::SegState), cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaStreamSynchronize(s));
   // layers whose sampled window missed: the exact global select on the slice
@@ -1573,7 +1619,6 @@ pact_status pact_prune_magnitude_segmented(pact_ctx* ctx, const float* w, uint64
   if (patched)
     CUDA_TRY(cudaMemcpyAsync(d_st, hst.data(), nseg * sizeof(pactk::SegState), cudaMemcpyHostToDevice, s));
   // (4) bitmap with ties dropped, (5) per-layer tie ranks, (6) offsets
-  uint32_t* ties = out->ties[0].as<uint32_t>();
   pactk::launch_seg_bitmap(w, len, d_info, d_st, d_cs, out->words, out->tie_words.as<uint64_t>(), ties,
                            out->tile_popc, s);
   TRY(scan(ctx, ties, nc, out->tie_prefix.as<uint32_t>(), s));
@@ -1582,7 +1627,6 @@ pact_status pact_prune_magnitude_segmented(pact_ctx* ctx, const float* w, uint64
   pactk::launch_seg_tiefix(len, d_info, d_st, d_cs, out->words, out->tie_words.as<uint64_t>(), ties,
                            out->tie_prefix.as<uint32_t>(), out->tile_popc, s);
   TRY(scan(ctx, out->tile_popc, nc, out->tile_off, s));
-  uint32_t* pin32 = ctx->pin.as<uint32_t>();
   CUDA_TRY(cudaMemcpyAsync(pin32, out->tile_off + nc, 4, cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaMemcpyAsync(hst.data(), d_st, nseg * sizeof(pactk::SegState), cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaGetLastError());
@@ -1601,6 +1645,9 @@ pact_status pact_prune_magnitude_segmented(pact_ctx* ctx, const float* w, uint64
   if (out->nnz != kept)
     return fail(PACT_E_RUN_FAILURE, "per-layer prune kept %llu, expected %llu",
                 (unsigned long long)out->nnz, (unsigned long long)kept);
+  out->seg_key = key;
+  out->seg_ratio = ratio;
+  out->seg_states = hst;
   return PACT_OK;
 }
 

@@ -596,6 +596,28 @@ void launch_seg_tiebase(const SegInfo* info, SegState* st, uint32_t nseg, const 
   note_launch();
 }
 
+namespace {
+__global__ void seg_verify_kernel(const SegInfo* __restrict__ info, SegState* __restrict__ st, uint32_t nseg,
+                                  int* __restrict__ miss) {
+  for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < nseg; q += gridDim.x * blockDim.x) {
+    if (info[q].trivial) continue;
+    const unsigned long long k = info[q].k, lt = st[q].b_lt, eq = st[q].b_eq;
+    if (lt < k && k <= lt + eq) {
+      st[q].c_lt = lt;
+      st[q].r = k - lt;
+    } else {
+      atomicExch(miss, 1);
+    }
+  }
+}
+}  // namespace
+
+void launch_seg_verify(const SegInfo* info, SegState* st, uint32_t nseg, int* miss, cudaStream_t s) {
+  if (!nseg) return;
+  seg_verify_kernel<<<(nseg + 255) / 256, 256, 0, s>>>(info, st, nseg, miss);
+  note_launch();
+}
+
 void launch_seg_tiefix(uint64_t len, const SegInfo* info, const SegState* st, const uint32_t* chunk_seg,
                        uint64_t* words, const uint64_t* tie_words, const uint32_t* ties, const uint32_t* tie_prefix,
                        uint32_t* chunk_popc, cudaStream_t s) {

@@ -653,6 +653,40 @@ def test_per_layer_prune_model_shapes(pb, port, cuda):
         assert m.digest() == port.mask_digest(ref, shape.total)
 
 
+def test_per_layer_reprune_sequence(pb, port, cuda):
+    """Per-layer re-pruning into the same mask (temporal reuse: one bitmap
+    pass at every layer's previous threshold, verified per layer, else the
+    full path): words bit-exact against the oracle's per-slice rule at every
+    step of a schedule that keeps, moves (both ways) and scrambles the
+    thresholds, with tie-heavy weights, and across a ratio change and a
+    changed layer table (the cache is keyed on both)."""
+    from paper_2505_18563_b200 import synth
+
+    shape = synth.model_shape("resnet18")
+    n = shape.total
+    offs = shape.offsets()
+    cuts = np.array(offs, np.uint64)
+    for recipe in (synth.W_REAL, synth.W_TIES):
+        rng = np.random.default_rng(7 + recipe)
+        w = synth.weights_host(shape, 17 + recipe, recipe)
+        m = pb.SparsityMask(n)
+        prev = None
+        for t, kind in enumerate(["same", "same", "up", "a9", "a9ties", "down", "same", "new", "same"]):
+            if prev is not None:
+                w = _perturb(kind, w, bits_from_words(prev, n), rng, synth, t)
+            pb.magnitude_prune_per_layer(dev(w), offs, 0.9, out=m)
+            ref = port.magnitude_prune_segmented(w, cuts, 0.9)
+            assert np.array_equal(m.words_host(), ref), (recipe, t, kind)
+            assert m.nnz() == port.mask_nnz(ref, n)
+            assert m.digest() == port.mask_digest(ref, n)
+            prev = ref
+        for ratio, table in ((0.8, offs), (0.8, [0, 5000] + [o for o in offs[1:] if o > 5000])):
+            pb.magnitude_prune_per_layer(dev(w), table, ratio, out=m)
+            pb.magnitude_prune_per_layer(dev(w), table, ratio, out=m)  # the reuse of the new key
+            ref = port.magnitude_prune_segmented(w, np.array(table, np.uint64), ratio)
+            assert np.array_equal(m.words_host(), ref), (recipe, ratio, len(table))
+
+
 @pytest.mark.parametrize("model", ["gpt2-medium", "bert-base"])
 def test_per_layer_prune_full_size(pb, port, cuda, model):
     """Per-layer mode (north_star (1)) at C5 / C4 size: every
