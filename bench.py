@@ -638,8 +638,13 @@ def main():
         p_full = pr.pop("paths")
         # per-layer thresholds: every layer's own k-th key, all
         # layers at once (prune_seg.cu), against the global first-time prune
+        fill = lambda i: pb.api._call(pb.api.lib.pact_mask_fill, scratch.handle, 0, pb.api._stream())  # noqa: E731
         t_layer = statistics.median(timed(lambda i: pb.magnitude_prune_per_layer(w_cur, layer_offs, ratio,
-                                                                                 out=scratch), 3))
+                                                                                 out=scratch), 3, pre=fill))
+        # per-layer temporal reuse: every layer's previous threshold verified by one pass
+        pb.magnitude_prune_per_layer(w_cur, layer_offs, ratio, out=scratch)
+        t_layer_reuse = statistics.median(timed(lambda i: pb.magnitude_prune_per_layer(w_cur, layer_offs, ratio,
+                                                                                       out=scratch), 5))
         del scratch
         # a whole step whose mask changed (regrowth), on the packed path
         # (the tracker would fall back to dense for K steps; this is the cost
@@ -651,10 +656,11 @@ def main():
         t_step_change = statistics.median(timed(step_stable, 5, pre=lambda i: perturb(50_000 + i, "regrow")))
         t_step_hit = statistics.median(timed(step_stable, 5))
         if world > 1:
-            tt = torch.tensor([t_hit, t_a9, t_drift, t_regrow, t_full, t_step_change, t_step_hit, t_layer],
+            tt = torch.tensor([t_hit, t_a9, t_drift, t_regrow, t_full, t_step_change, t_step_hit, t_layer,
+                               t_layer_reuse],
                               dtype=torch.float64, device=dev)
             torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-            t_hit, t_a9, t_drift, t_regrow, t_full, t_step_change, t_step_hit, t_layer = tt.tolist()
+            t_hit, t_a9, t_drift, t_regrow, t_full, t_step_change, t_step_hit, t_layer, t_layer_reuse = tt.tolist()
         stages["prune"] = {
             "reuse_hit_us": round(t_hit * 1e6, 1), "reuse_hit_gbs": round(alg_prune / t_hit / 1e9, 1),
             "a9_us": round(t_a9 * 1e6, 1), "a9_paths": p_a9,
@@ -662,6 +668,7 @@ def main():
             "regrowth_change_plus_digest_us": round(t_regrow * 1e6, 1), "regrowth_paths": p_regrow,
             "first_time_sampled_us": round(t_full * 1e6, 1), "first_time_paths": p_full,
             "per_layer_us": round(t_layer * 1e6, 1), "per_layer_layers": len(layer_offs) - 1,
+            "per_layer_reuse_us": round(t_layer_reuse * 1e6, 1),
             "per_layer_vs_global_first_time": round(t_layer / t_full, 3),
             "paths_legend": "1 sampled window, 2 full radix, 3 threshold reuse, 4 moved threshold from window candidates",
         }

@@ -937,6 +937,7 @@ pact_status pact_mask_fill(pact_mask* m, int keep, pact_stream_t stream) {
   m->nnz = want;
   m->digest_valid = 0;
   m->spec_valid = 0;
+  m->seg_states.clear();  // the per-layer reuse restarts from the full path
   m->host_tile_off_valid = 0;
   return PACT_OK;
 }
@@ -957,6 +958,7 @@ pact_status pact_mask_set_words(pact_mask* m, const uint64_t* words_dev, pact_st
   m->changed = 1;
   m->digest_valid = 0;
   m->spec_valid = 0;
+  m->seg_states.clear();  // the per-layer reuse restarts from the full path
   return PACT_OK;
 }
 
@@ -998,6 +1000,7 @@ pact_status pact_mask_gather(const pact_mask* src, uint64_t nseg, const uint64_t
   dst->changed = 1;
   dst->digest_valid = 0;
   dst->spec_valid = 0;
+  dst->seg_states.clear();  // the per-layer reuse restarts from the full path
   return PACT_OK;
 }
 
@@ -2075,6 +2078,7 @@ pact_status topk_mask(pact_ctx* ctx, const float* g, uint64_t len, uint64_t k, c
   m->changed = 1;
   m->digest_valid = 0;
   m->spec_valid = 0;
+  m->seg_states.clear();  // the per-layer reuse restarts from the full path
   const uint64_t kd = len - k;
   if (kd == 0 || len == 0) {
     if (nnz_pin) *nnz_pin = (uint32_t)k;
