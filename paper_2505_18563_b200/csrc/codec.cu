@@ -1024,6 +1024,30 @@ void launch_clear_tail(uint64_t* words, uint64_t len, cudaStream_t s) {
   note_launch();
 }
 
+namespace {
+__global__ void words_differ_kernel(const uint4* __restrict__ a, const uint4* __restrict__ b, uint64_t n16,
+                                    int* __restrict__ flag) {
+  bool d = false;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n16;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint4 x = __ldcs(a + i), y = __ldcs(b + i);
+    d |= (x.x != y.x) | (x.y != y.y) | (x.z != y.z) | (x.w != y.w);
+  }
+  if (__any_sync(0xffffffffu, d) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+}
+}  // namespace
+
+void launch_words_differ(const uint64_t* a, const uint64_t* b, uint64_t nwords, int* flag, cudaStream_t s) {
+  const uint64_t n16 = (nwords + 1) / 2;  // both padded to whole 16-word chunks
+  if (!n16) return;
+  uint64_t blocks = (n16 + 255) / 256;
+  const uint64_t cap = (uint64_t)sm_count() * 8;
+  if (blocks > cap) blocks = cap;
+  words_differ_kernel<<<(unsigned)blocks, 256, 0, s>>>(reinterpret_cast<const uint4*>(a),
+                                                       reinterpret_cast<const uint4*>(b), n16, flag);
+  note_launch();
+}
+
 void launch_tile_popc(const uint64_t* words, uint64_t len, uint32_t* popc, cudaStream_t s) {
   const uint64_t nc = (len + kChunk - 1) / kChunk;
   if (!nc) return;

@@ -78,6 +78,8 @@ void launch_gse(const float* g, uint64_t len, const uint64_t* words, float* out,
 void launch_mask_fill(uint64_t* words, uint64_t len, int keep, uint32_t* chunk_off, cudaStream_t s);
 void launch_clear_tail(uint64_t* words, uint64_t len, cudaStream_t s);
 void launch_tile_popc(const uint64_t* words, uint64_t len, uint32_t* chunk_popc, cudaStream_t s);
+// *flag |= 1 when the two word arrays differ (nwords rounded up to pairs)
+void launch_words_differ(const uint64_t* a, const uint64_t* b, uint64_t nwords, int* flag, cudaStream_t s);
 // out[j] = src[idx[j]] for j < n (n <= kGatherMax): a few chunk offsets for
 // the host in one readback (bucket boundaries of the copy-engine exchange)
 constexpr int kGatherMax = 65;

@@ -170,6 +170,7 @@ struct pact_mask {
   std::vector<uint64_t> seg_key;
   float seg_ratio = -1.0f;
   std::vector<pactk::SegState> seg_states;
+  DevBuf seg_prev;  // the words before a per-layer reuse pass (exact `changed`)
   uint64_t len = 0, nwords = 0, ntiles = 0;
   uint64_t* words = nullptr;
   uint32_t* tile_off = nullptr;   // ntiles + 1
@@ -908,6 +909,7 @@ pact_status pact_mask_destroy(pact_mask* m) {
   m->cand_key.release();
   m->cand_idx.release();
   m->tie_old.release();
+  m->seg_prev.release();
   delete m;
   return PACT_OK;
 }
@@ -1562,8 +1564,12 @@ pact_status pact_prune_magnitude_segmented(pact_ctx* ctx, const float* w, uint64
     std::vector<pactk::SegState> prev = out->seg_states;
     for (auto& x : prev) x.b_lt = x.b_eq = 0;
     int* miss = &ctx->ws_small.as<Small>()->changed;
+    int* differ = miss + 1;  // Small::pad1[0]
+    const size_t wbytes = (size_t)((nw + 15) / 16) * 16 * 8;  // words are padded to whole chunks
+    TRY(out->seg_prev.ensure(wbytes));
+    CUDA_TRY(cudaMemcpyAsync(out->seg_prev.p, out->words, wbytes, cudaMemcpyDeviceToDevice, s));
     CUDA_TRY(cudaMemcpyAsync(d_st, prev.data(), nseg * sizeof(pactk::SegState), cudaMemcpyHostToDevice, s));
-    CUDA_TRY(cudaMemsetAsync(miss, 0, 4, s));
+    CUDA_TRY(cudaMemsetAsync(miss, 0, 8, s));
     pactk::launch_seg_bitmap(w, len, d_info, d_st, d_cs, out->words, out->tie_words.as<uint64_t>(), ties,
                              out->tile_popc, s);
     pactk::launch_seg_verify(d_info, d_st, (uint32_t)nseg, miss, s);
@@ -1573,16 +1579,22 @@ pact_status pact_prune_magnitude_segmented(pact_ctx* ctx, const float* w, uint64
     pactk::launch_seg_tiefix(len, d_info, d_st, d_cs, out->words, out->tie_words.as<uint64_t>(), ties,
                              out->tie_prefix.as<uint32_t>(), out->tile_popc, s);
     TRY(scan(ctx, out->tile_popc, nc, out->tile_off, s));
+    pactk::launch_words_differ(out->words, out->seg_prev.as<uint64_t>(), (wbytes / 8), differ, s);
     CUDA_TRY(cudaMemcpyAsync(pin32, out->tile_off + nc, 4, cudaMemcpyDeviceToHost, s));
-    CUDA_TRY(cudaMemcpyAsync(pin32 + 1, miss, 4, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaMemcpyAsync(pin32 + 1, miss, 8, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaMemcpyAsync(hst.data(), d_st, nseg * sizeof(pactk::SegState), cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cudaStreamSynchronize(s));
     if (pin32[1] == 0) {
+      // `changed` exact from a word compare with the words before the pass: an
+      // unchanged mask keeps its digest and host offsets
+      const bool chg = pin32[2] != 0;
       out->nnz = pin32[0];
-      out->host_tile_off_valid = 0;
-      out->changed = 1;  // (no per-bit change record on this path: the digest decides)
-      out->digest_valid = 0;
+      if (chg) {
+        out->host_tile_off_valid = 0;
+        out->digest_valid = 0;
+      }
+      out->changed = chg;
       out->spec_valid = 0;
       out->seg_states = hst;
       if (out->nnz != kept)

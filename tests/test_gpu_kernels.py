@@ -678,6 +678,8 @@ def test_per_layer_reprune_sequence(pb, port, cuda):
             ref = port.magnitude_prune_segmented(w, cuts, 0.9)
             assert np.array_equal(m.words_host(), ref), (recipe, t, kind)
             assert m.nnz() == port.mask_nnz(ref, n)
+            if prev is not None and not m.changed:  # an unchanged mask keeps its digest
+                assert np.array_equal(ref, prev), (recipe, t, kind, "change missed")
             assert m.digest() == port.mask_digest(ref, n)
             prev = ref
         for ratio, table in ((0.8, offs), (0.8, [0, 5000] + [o for o in offs[1:] if o > 5000])):
