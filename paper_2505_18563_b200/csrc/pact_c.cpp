@@ -148,6 +148,7 @@ struct pact_ctx {
   DevBuf cand;      // prune candidates (u32 keys)
   DevBuf state;     // look-back tile states + counter
   DevBuf seg_ws;    // per-layer prune: segment table, thresholds, tie prefixes
+  DevBuf seg_ws2;   // per-layer reuse: the re-selected layers' sub-problem
   DevBuf digest_scratch;
   DevBuf packed;    // packed gradient for masked_allreduce
   DevBuf grad_stage, out_stage;  // e2e host path staging
@@ -845,7 +846,7 @@ pact_status pact_ctx_destroy(pact_ctx* ctx) {
   if (!ctx) return PACT_OK;
   cudaSetDevice(ctx->device);
   cudaDeviceSynchronize();
-  for (DevBuf* b : {&ctx->ws_small, &ctx->cand, &ctx->state, &ctx->seg_ws, &ctx->digest_scratch, &ctx->packed,
+  for (DevBuf* b : {&ctx->ws_small, &ctx->cand, &ctx->state, &ctx->seg_ws, &ctx->seg_ws2, &ctx->digest_scratch, &ctx->packed,
                     &ctx->grad_stage, &ctx->out_stage, &ctx->tern, &ctx->f16, &ctx->topk})
     b->release();
   if (ctx->topk_sel) pact_mask_destroy(ctx->topk_sel);
@@ -1556,9 +1557,12 @@ pact_status pact_prune_magnitude_segmented(pact_ctx* ctx, const float* w, uint64
   uint32_t* pin32 = ctx->pin.as<uint32_t>();
   std::vector<pactk::SegState> hst(nseg);
   // (0) temporal reuse (same layer table and ratio as the last call): one
-  // bitmap pass at every layer's previous threshold verifies all of them
-  // at once; the tie ranks and offsets follow as in (5)-(6) below. Any
-  // layer whose k-th key moved sends the whole call down the full path.
+  // bitmap pass at every layer's previous threshold verifies all of them at
+  // once on the device. Layers whose k-th key moved (typically small layers
+  // whose regrowth noise re-draws it every step) are re-selected as a batch
+  // of their own -- the same sample / count / select kernels on those layers
+  // only -- and a second bitmap pass applies every layer's threshold; then
+  // the tie ranks and offsets as in (5)-(6) below.
   const std::vector<uint64_t> key(seg, seg + nseg + 1);
   if (out->seg_ratio == ratio && out->seg_key == key && out->seg_states.size() == nseg) {
     std::vector<pactk::SegState> prev = out->seg_states;
@@ -1573,6 +1577,75 @@ pact_status pact_prune_magnitude_segmented(pact_ctx* ctx, const float* w, uint64
     pactk::launch_seg_bitmap(w, len, d_info, d_st, d_cs, out->words, out->tie_words.as<uint64_t>(), ties,
                              out->tile_popc, s);
     pactk::launch_seg_verify(d_info, d_st, (uint32_t)nseg, miss, s);
+    CUDA_TRY(cudaMemcpyAsync(pin32 + 1, miss, 4, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaMemcpyAsync(hst.data(), d_st, nseg * sizeof(pactk::SegState), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaStreamSynchronize(s));
+    if (pin32[1] != 0) {
+      std::vector<uint32_t> ml;  // the layers whose threshold moved
+      for (uint64_t q = 0; q < nseg; ++q) {
+        if (info[q].trivial) continue;
+        const uint64_t k = info[q].k;
+        if (!(hst[q].b_lt < k && k <= hst[q].b_lt + hst[q].b_eq)) ml.push_back((uint32_t)q);
+      }
+      const uint32_t nm = (uint32_t)ml.size();
+      std::vector<pactk::SegInfo> im(nm);
+      std::vector<pactk::SegState> sm0(nm);
+      std::vector<pactk::SegTile> tm;
+      uint64_t cm = 0;
+      for (uint32_t j = 0; j < nm; ++j) {
+        const uint32_t q = ml[j];
+        im[j] = info[q];
+        im[j].cand_off = cm;
+        cm += info[q].cand_cap;
+        for (uint64_t b = seg[q]; b < seg[q + 1]; b += kTileElems)
+          tm.push_back({j, 0, b, std::min(seg[q + 1], b + kTileElems)});
+      }
+      const size_t m_info = 0, m_st = m_info + al(nm * sizeof(pactk::SegInfo)),
+                   m_fill = m_st + al(nm * sizeof(pactk::SegState)), m_tiles = m_fill + al(nm * 8),
+                   m_cand = m_tiles + al(std::max<size_t>(1, tm.size()) * sizeof(pactk::SegTile)),
+                   m_total = m_cand + al(std::max<uint64_t>(1, cm) * 4);
+      TRY(ctx->seg_ws2.ensure(m_total));
+      char* ws2 = ctx->seg_ws2.as<char>();
+      auto* e_info = reinterpret_cast<pactk::SegInfo*>(ws2 + m_info);
+      auto* e_st = reinterpret_cast<pactk::SegState*>(ws2 + m_st);
+      auto* e_fill = reinterpret_cast<unsigned long long*>(ws2 + m_fill);
+      auto* e_tiles = reinterpret_cast<pactk::SegTile*>(ws2 + m_tiles);
+      auto* e_cand = reinterpret_cast<uint32_t*>(ws2 + m_cand);
+      CUDA_TRY(cudaMemcpyAsync(e_info, im.data(), nm * sizeof(pactk::SegInfo), cudaMemcpyHostToDevice, s));
+      CUDA_TRY(cudaMemcpyAsync(e_st, sm0.data(), nm * sizeof(pactk::SegState), cudaMemcpyHostToDevice, s));
+      CUDA_TRY(cudaMemsetAsync(e_fill, 0, nm * 8, s));
+      if (!tm.empty())
+        CUDA_TRY(cudaMemcpyAsync(e_tiles, tm.data(), tm.size() * sizeof(pactk::SegTile), cudaMemcpyHostToDevice, s));
+      pactk::launch_seg_sample(w, e_info, e_st, nm, s);
+      pactk::launch_seg_count(w, e_info, e_st, e_tiles, (uint32_t)tm.size(), e_cand, e_fill, s);
+      pactk::launch_seg_select(e_info, e_st, nm, e_cand, e_fill, s);
+      std::vector<pactk::SegState> hm(nm);
+      CUDA_TRY(cudaMemcpyAsync(hm.data(), e_st, nm * sizeof(pactk::SegState), cudaMemcpyDeviceToHost, s));
+      CUDA_TRY(cudaGetLastError());
+      CUDA_TRY(cudaStreamSynchronize(s));
+      for (uint32_t j = 0; j < nm; ++j) {
+        const uint32_t q = ml[j];
+        if (hm[j].mode != 0) {  // the sampled window missed: the exact select on the slice
+          const uint64_t ls = info[q].end - info[q].begin;
+          uint32_t T = 0;
+          uint64_t c_lt = 0;
+          pact_prune_stats pst{};
+          TRY(find_threshold(ctx, w + info[q].begin, ls, info[q].k, s, &T, &c_lt, &pst));
+          hm[j].T = T;
+          hm[j].c_lt = c_lt;
+          hm[j].r = info[q].k - c_lt;
+        }
+        hst[q].T = hm[j].T;
+        hst[q].c_lt = hm[j].c_lt;
+        hst[q].r = hm[j].r;
+        hst[q].mode = 0;
+      }
+      for (auto& x : hst) x.b_lt = x.b_eq = 0;
+      CUDA_TRY(cudaMemcpyAsync(d_st, hst.data(), nseg * sizeof(pactk::SegState), cudaMemcpyHostToDevice, s));
+      pactk::launch_seg_bitmap(w, len, d_info, d_st, d_cs, out->words, out->tie_words.as<uint64_t>(), ties,
+                               out->tile_popc, s);
+    }
     TRY(scan(ctx, ties, nc, out->tie_prefix.as<uint32_t>(), s));
     pactk::launch_seg_tiebase(d_info, d_st, (uint32_t)nseg, out->tie_words.as<uint64_t>(), ties,
                               out->tie_prefix.as<uint32_t>(), s);
@@ -1581,27 +1654,31 @@ pact_status pact_prune_magnitude_segmented(pact_ctx* ctx, const float* w, uint64
     TRY(scan(ctx, out->tile_popc, nc, out->tile_off, s));
     pactk::launch_words_differ(out->words, out->seg_prev.as<uint64_t>(), (wbytes / 8), differ, s);
     CUDA_TRY(cudaMemcpyAsync(pin32, out->tile_off + nc, 4, cudaMemcpyDeviceToHost, s));
-    CUDA_TRY(cudaMemcpyAsync(pin32 + 1, miss, 8, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaMemcpyAsync(pin32 + 2, differ, 4, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaMemcpyAsync(hst.data(), d_st, nseg * sizeof(pactk::SegState), cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cudaStreamSynchronize(s));
-    if (pin32[1] == 0) {
-      // `changed` exact from a word compare with the words before the pass: an
-      // unchanged mask keeps its digest and host offsets
-      const bool chg = pin32[2] != 0;
-      out->nnz = pin32[0];
-      if (chg) {
-        out->host_tile_off_valid = 0;
-        out->digest_valid = 0;
-      }
-      out->changed = chg;
-      out->spec_valid = 0;
-      out->seg_states = hst;
-      if (out->nnz != kept)
-        return fail(PACT_E_RUN_FAILURE, "per-layer prune kept %llu, expected %llu",
-                    (unsigned long long)out->nnz, (unsigned long long)kept);
-      return PACT_OK;
+    for (uint64_t q = 0; q < nseg; ++q) {  // every threshold verified by the final pass's own counts
+      if (info[q].trivial) continue;
+      if (hst[q].b_lt != hst[q].c_lt || !(hst[q].c_lt < info[q].k && info[q].k <= hst[q].b_lt + hst[q].b_eq))
+        return fail(PACT_E_RUN_FAILURE, "per-layer threshold inconsistent at layer %llu (reuse)",
+                    (unsigned long long)q);
     }
+    // `changed` exact from a word compare with the words before the call:
+    // an unchanged mask keeps its digest and host offsets
+    const bool chg = pin32[2] != 0;
+    out->nnz = pin32[0];
+    if (chg) {
+      out->host_tile_off_valid = 0;
+      out->digest_valid = 0;
+    }
+    out->changed = chg;
+    out->spec_valid = 0;
+    out->seg_states = hst;
+    if (out->nnz != kept)
+      return fail(PACT_E_RUN_FAILURE, "per-layer prune kept %llu, expected %llu", (unsigned long long)out->nnz,
+                  (unsigned long long)kept);
+    return PACT_OK;
   }
   out->seg_states.clear();
   CUDA_TRY(cudaMemcpyAsync(d_st, st0.data(), nseg * sizeof(pactk::SegState), cudaMemcpyHostToDevice, s));
