@@ -721,8 +721,7 @@ constexpr int kScanItems = 1024 * kScanPerThread;
 __global__ void __launch_bounds__(1024) scan_excl_kernel(const uint32_t* __restrict__ in, uint64_t n,
                                                          uint32_t* __restrict__ out,
                                                          uint64_t* __restrict__ state,
-                                                         unsigned* __restrict__ ticket, const int* gate) {
-  if (gate && *gate == 0) return;
+                                                         unsigned* __restrict__ ticket) {
   __shared__ uint32_t warp_tot[33];
   __shared__ uint32_t s_tile;
   __shared__ uint64_t s_prefix;
@@ -1078,13 +1077,12 @@ void launch_gather_u32(const uint32_t* src, const GatherIdx& idx, uint32_t* out,
   note_launch();
 }
 
-void launch_scan_excl(const uint32_t* in, uint64_t n, uint32_t* out, void* scratch, cudaStream_t s,
-                      const int* gate) {
+void launch_scan_excl(const uint32_t* in, uint64_t n, uint32_t* out, void* scratch, cudaStream_t s) {
   const uint64_t tiles = n ? (n + kScanItems - 1) / kScanItems : 1;
   cudaMemsetAsync(scratch, 0, tiles * 8 + 8, s);
   uint64_t* state = static_cast<uint64_t*>(scratch);
   scan_excl_kernel<<<(unsigned)tiles, 1024, 0, s>>>(in, n, out, state,
-                                                    reinterpret_cast<unsigned*>(state + tiles), gate);
+                                                    reinterpret_cast<unsigned*>(state + tiles));
   note_launch();
 }
 

@@ -187,9 +187,7 @@ __device__ __forceinline__ int seg_words(uint64_t nwords, uint64_t seg) {
 // (1) low-nibble maps of every segment; tile maps; last CTA: tile starts
 __global__ void __launch_bounds__(kDThreads)
     digest_low_kernel(const uint64_t* __restrict__ words, uint64_t nwords, uint4* __restrict__ seg_low,
-                      uint4* __restrict__ tile_low, uint32_t* __restrict__ tile_tin, unsigned* cnt,
-                      const int* gate) {
-  if (gate && *gate == 0) return;
+                      uint4* __restrict__ tile_low, uint32_t* __restrict__ tile_tin, unsigned* cnt) {
   __shared__ MapScratch sh;
   const uint64_t seg = (uint64_t)blockIdx.x * kDThreads + threadIdx.x;
   const int nw = seg_words(nwords, seg);
@@ -228,9 +226,7 @@ __global__ void __launch_bounds__(kDThreads)
     digest_high_kernel(const uint64_t* __restrict__ words, uint64_t nwords,
                        const uint4* __restrict__ seg_low, const uint32_t* __restrict__ tile_tin,
                        uint4* __restrict__ seg_high, uint8_t* __restrict__ seg_tin,
-                       uint4* __restrict__ tile_high, uint32_t* __restrict__ tile_hin, unsigned* cnt,
-                       const int* gate) {
-  if (gate && *gate == 0) return;
+                       uint4* __restrict__ tile_high, uint32_t* __restrict__ tile_hin, unsigned* cnt) {
   __shared__ MapScratch sh;
   const uint64_t seg = (uint64_t)blockIdx.x * kDThreads + threadIdx.x;
   const int nw = seg_words(nwords, seg);
@@ -276,8 +272,7 @@ __global__ void __launch_bounds__(kDThreads)
     digest_affine_kernel(const uint64_t* __restrict__ words, uint64_t nwords,
                          const uint4* __restrict__ seg_high, const uint8_t* __restrict__ seg_tin,
                          const uint32_t* __restrict__ tile_hin, Aff* __restrict__ tile_aff,
-                         uint64_t p_full, unsigned* cnt, uint64_t* __restrict__ out, const int* gate) {
-  if (gate && *gate == 0) return;
+                         uint64_t p_full, unsigned* cnt, uint64_t* __restrict__ out) {
   __shared__ MapScratch sh;
   __shared__ Aff warp_aff[kDThreads / 32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -362,7 +357,7 @@ DigestLayout digest_layout(uint64_t nwords) {
 size_t digest_scratch_bytes(uint64_t nwords) { return digest_layout(nwords).total; }
 
 void launch_digest(const uint64_t* words, uint64_t nwords, void* scratch, uint64_t* out_dev,
-                   cudaStream_t s, const int* gate) {
+                   cudaStream_t s) {
   if (nwords == 0) {  // fnv1a64 of zero bytes is the offset basis
     static const uint64_t basis = kFnvBasis;
     cudaMemcpyAsync(out_dev, &basis, 8, cudaMemcpyHostToDevice, s);
@@ -377,15 +372,15 @@ void launch_digest(const uint64_t* words, uint64_t nwords, void* scratch, uint64
   cudaMemsetAsync(cnt, 0, 16, s);
   const unsigned grid = (unsigned)L.ntiles;
   digest_low_kernel<<<grid, kDThreads, 0, s>>>(words, nwords, u4(L.o_seg_low), u4(L.o_tile_low),
-                                               u32p(L.o_tile_tin), cnt, gate);
+                                               u32p(L.o_tile_tin), cnt);
   digest_high_kernel<<<grid, kDThreads, 0, s>>>(words, nwords, u4(L.o_seg_low), u32p(L.o_tile_tin),
                                                 u4(L.o_seg_high),
                                                 reinterpret_cast<uint8_t*>(b + L.o_seg_tin),
-                                                u4(L.o_tile_high), u32p(L.o_tile_hin), cnt + 1, gate);
+                                                u4(L.o_tile_high), u32p(L.o_tile_hin), cnt + 1);
   digest_affine_kernel<<<grid, kDThreads, 0, s>>>(
       words, nwords, u4(L.o_seg_high), reinterpret_cast<const uint8_t*>(b + L.o_seg_tin),
       u32p(L.o_tile_hin), reinterpret_cast<Aff*>(b + L.o_tile_aff), pow_p(8ull * kSegWords), cnt + 2,
-      out_dev, gate);
+      out_dev);
   note_launch(3);
 }
 

@@ -96,9 +96,7 @@ void launch_mask_gather(const uint64_t* src, uint64_t src_len, const uint64_t* s
                         uint64_t dst_words_padded, cudaStream_t s);
 // exclusive scan of n u32 -> out[0..n], out[n] = total (single pass, look-back)
 size_t scan_scratch_bytes(uint64_t n);
-// gate (nullable, device): the kernel returns at once when *gate == 0
-void launch_scan_excl(const uint32_t* in, uint64_t n, uint32_t* out, void* scratch, cudaStream_t s,
-                      const int* gate = nullptr);
+void launch_scan_excl(const uint32_t* in, uint64_t n, uint32_t* out, void* scratch, cudaStream_t s);
 // count of kernels launched by these launchers (process-wide, for gpu_launches)
 uint64_t launches();
 void note_launch(uint64_t n = 1);
@@ -331,7 +329,7 @@ void launch_f16_roundtrip(const float* x, uint64_t n, float* out, cudaStream_t s
 // digest_scratch_bytes(nwords). Result written to *out_dev.
 size_t digest_scratch_bytes(uint64_t nwords);
 void launch_digest(const uint64_t* words, uint64_t nwords, void* scratch, uint64_t* out_dev,
-                   cudaStream_t s, const int* gate = nullptr);
+                   cudaStream_t s);
 
 // ---- synth.cu --------------------------------------------------------------
 void launch_synth(float* x, uint64_t len, uint64_t seed, uint64_t index_base, int recipe,

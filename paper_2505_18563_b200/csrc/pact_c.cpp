@@ -384,10 +384,9 @@ cudaEvent_t pool_event(pact_ctx* ctx, size_t i) {
 }
 
 // recompute tile offsets + nnz from the mask words (device), sync
-pact_status scan(pact_ctx* ctx, const uint32_t* in, uint64_t n, uint32_t* out, cudaStream_t s,
-                 const int* gate = nullptr) {
+pact_status scan(pact_ctx* ctx, const uint32_t* in, uint64_t n, uint32_t* out, cudaStream_t s) {
   TRY(ctx->state.ensure(pactk::scan_scratch_bytes(n)));
-  pactk::launch_scan_excl(in, n, out, ctx->state.p, s, gate);
+  pactk::launch_scan_excl(in, n, out, ctx->state.p, s);
   return PACT_OK;
 }
 
