@@ -28,6 +28,7 @@ that process never maps the product library (asserted).
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import math
 import os
@@ -500,6 +501,10 @@ def main():
         the flush re-aligns the ranks on the device, so no step is
         charged for a peer's flush."""
         evs = []
+        # no cyclic-GC pause inside a step: the prune's readback makes the
+        # host part of the device timeline (collected before, re-enabled after)
+        gc.collect()
+        gc.disable()
         for i in range(k):
             if pre is not None:
                 pre(i)
@@ -518,6 +523,7 @@ def main():
             b.record(stream)
             evs.append((a, b))
         torch.cuda.synchronize()
+        gc.enable()
         return [a.elapsed_time(b) * 1e-3 for a, b in evs]
 
     if args.path == "sweep":

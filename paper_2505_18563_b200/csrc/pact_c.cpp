@@ -172,6 +172,7 @@ struct pact_mask {
   float seg_ratio = -1.0f;
   std::vector<pactk::SegState> seg_states;
   DevBuf seg_prev;  // the words before a per-layer reuse pass (exact `changed`)
+  int seg_skip = 0;  // calls left before the reuse is tried again after a heavy miss
   uint64_t len = 0, nwords = 0, ntiles = 0;
   uint64_t* words = nullptr;
   uint32_t* tile_off = nullptr;   // ntiles + 1
@@ -1563,11 +1564,17 @@ pact_status pact_prune_magnitude_segmented(pact_ctx* ctx, const float* w, uint64
   // only -- and a second bitmap pass applies every layer's threshold; then
   // the tie ranks and offsets as in (5)-(6) below.
   const std::vector<uint64_t> key(seg, seg + nseg + 1);
-  if (out->seg_ratio == ratio && out->seg_key == key && out->seg_states.size() == nseg) {
+  // (when more than a quarter of the elements sit in layers whose threshold
+  // moved, the re-select costs about the full path: the call takes it, and
+  // the next 7 calls skip the verify pass -- e.g. SURVEY A.9's regrowth
+  // noise re-draws every layer's k-th key each step)
+  bool reuse = out->seg_ratio == ratio && out->seg_key == key && out->seg_states.size() == nseg &&
+               out->seg_skip == 0;
+  if (out->seg_skip > 0) --out->seg_skip;
+  if (reuse) {
     std::vector<pactk::SegState> prev = out->seg_states;
     for (auto& x : prev) x.b_lt = x.b_eq = 0;
     int* miss = &ctx->ws_small.as<Small>()->changed;
-    int* differ = miss + 1;  // Small::pad1[0]
     const size_t wbytes = (size_t)((nw + 15) / 16) * 16 * 8;  // words are padded to whole chunks
     TRY(out->seg_prev.ensure(wbytes));
     CUDA_TRY(cudaMemcpyAsync(out->seg_prev.p, out->words, wbytes, cudaMemcpyDeviceToDevice, s));
@@ -1580,13 +1587,23 @@ pact_status pact_prune_magnitude_segmented(pact_ctx* ctx, const float* w, uint64
     CUDA_TRY(cudaMemcpyAsync(hst.data(), d_st, nseg * sizeof(pactk::SegState), cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cudaStreamSynchronize(s));
+    std::vector<uint32_t> ml;  // the layers whose threshold moved
+    uint64_t moved = 0;
     if (pin32[1] != 0) {
-      std::vector<uint32_t> ml;  // the layers whose threshold moved
       for (uint64_t q = 0; q < nseg; ++q) {
         if (info[q].trivial) continue;
         const uint64_t k = info[q].k;
-        if (!(hst[q].b_lt < k && k <= hst[q].b_lt + hst[q].b_eq)) ml.push_back((uint32_t)q);
+        if (!(hst[q].b_lt < k && k <= hst[q].b_lt + hst[q].b_eq)) {
+          ml.push_back((uint32_t)q);
+          moved += info[q].end - info[q].begin;
+        }
       }
+      if (moved * 4 > len) {
+        reuse = false;
+        out->seg_skip = 7;
+      }
+    }
+    if (reuse && !ml.empty()) {
       const uint32_t nm = (uint32_t)ml.size();
       std::vector<pactk::SegInfo> im(nm);
       std::vector<pactk::SegState> sm0(nm);
@@ -1645,6 +1662,10 @@ pact_status pact_prune_magnitude_segmented(pact_ctx* ctx, const float* w, uint64
       pactk::launch_seg_bitmap(w, len, d_info, d_st, d_cs, out->words, out->tie_words.as<uint64_t>(), ties,
                                out->tile_popc, s);
     }
+  }
+  if (reuse) {
+    int* differ = &ctx->ws_small.as<Small>()->changed + 1;  // Small::pad1[0]
+    const size_t wbytes = (size_t)((nw + 15) / 16) * 16 * 8;
     TRY(scan(ctx, ties, nc, out->tie_prefix.as<uint32_t>(), s));
     pactk::launch_seg_tiebase(d_info, d_st, (uint32_t)nseg, out->tie_words.as<uint64_t>(), ties,
                               out->tie_prefix.as<uint32_t>(), s);

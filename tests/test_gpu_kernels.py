@@ -671,8 +671,15 @@ def test_per_layer_reprune_sequence(pb, port, cuda):
         w = synth.weights_host(shape, 17 + recipe, recipe)
         m = pb.SparsityMask(n)
         prev = None
-        for t, kind in enumerate(["same", "same", "up", "a9", "a9ties", "down", "same", "new", "same"]):
-            if prev is not None:
+        sizes = np.diff(np.array(offs))
+        small = [i for i in range(len(sizes)) if 4096 <= sizes[i] <= n // 16]
+        for t, kind in enumerate(["same", "same", "layer", "same", "layer", "up", "a9", "a9ties", "down", "same",
+                                  "new", "same"]):
+            if kind == "layer":  # one layer's weights re-drawn: only its threshold moves (partial re-select)
+                i = small[(t * 7) % len(small)]
+                w = w.copy()
+                w[offs[i]:offs[i + 1]] = rng.standard_normal(sizes[i]).astype(np.float32) * np.float32(0.05)
+            elif prev is not None:
                 w = _perturb(kind, w, bits_from_words(prev, n), rng, synth, t)
             pb.magnitude_prune_per_layer(dev(w), offs, 0.9, out=m)
             ref = port.magnitude_prune_segmented(w, cuts, 0.9)
