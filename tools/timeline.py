@@ -2,7 +2,7 @@
 kernel name, start offset, duration and the idle gap before it, so host
 round trips show up as gaps. nsys is not in this image.
 
-    python tools/timeline.py [model] [ratio] [scenario: hit|drift|regrow|step]
+    python tools/timeline.py [model] [ratio] [scenario: hit|drift|regrow|step|a9|a9step]
 """
 import os
 import sys
@@ -40,7 +40,7 @@ def main():
         if scen == "drift" or scen == "step":
             pb.synth_fill(noise, 900 + t, synth.W_REAL, 2.0 ** -17)
             w.add_(noise)
-        elif scen == "a9":  # bench.py's A.9 perturbation
+        elif scen in ("a9", "a9step"):  # bench.py's A.9 perturbation
             kb = keep_of(m)
             pb.synth_fill(noise, 700 + t, synth.W_REAL, 2.0 ** -14)
             wd = w + noise
@@ -50,7 +50,7 @@ def main():
     def run(t):
         pb.magnitude_prune(w, ratio, out=m)
         m.digest()
-        if scen == "step":
+        if scen in ("step", "a9step"):
             pb.masked_allreduce(g, m, pb.TrackerStatus.Stable, t, None, out=out)
 
     for t in range(3):
