@@ -66,7 +66,15 @@ def _call(fn, *args):
         raise Error(code, msg, st)
 
 
+_raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+_cur_dev = getattr(torch._C, "_cuda_getDevice", None)
+
+
 def _stream() -> C.c_void_p:
+    # the raw handle of torch's current stream without building a Stream
+    # object (this sits between the prune's readback and the next launch)
+    if _raw_stream is not None and _cur_dev is not None:
+        return C.c_void_p(_raw_stream(_cur_dev()))
     return C.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
