@@ -327,9 +327,11 @@ constexpr int kKeyStages = 2;
 constexpr int kStageFloats = kChunk + 2 * kChunkWords;  // keys, then the 16 old mask words
 constexpr int kCandBuf = 64;                            // per-warp window-candidate staging
 constexpr int kCandHistBits = 8;                        // first select digit, counted by the pass
-constexpr size_t kBitmapSmem =
-    (size_t)kPruneWarps * (kKeyStages * kStageFloats * sizeof(float) + 2 * kCandBuf * sizeof(uint32_t)) +
-    (sizeof(uint32_t) << kCandHistBits) + (size_t)kPruneWarps * kKeyStages * sizeof(uint64_t);
+constexpr size_t bitmap_smem(int stages) {
+  return (size_t)kPruneWarps * (stages * kStageFloats * sizeof(float) + 2 * kCandBuf * sizeof(uint32_t)) +
+         (sizeof(uint32_t) << kCandHistBits) + (size_t)kPruneWarps * stages * sizeof(uint64_t);
+}
+constexpr size_t kBitmapSmem = bitmap_smem(kKeyStages);
 
 __device__ __forceinline__ void chunk_issue(float* st, const float* __restrict__ w,
                                             const uint64_t* __restrict__ words, uint64_t c) {
@@ -399,7 +401,7 @@ __device__ __forceinline__ void flush_pairs(const uint32_t* bk, const uint32_t* 
   __syncwarp();
 }
 
-template <bool kBulk>
+template <bool kBulk, int kS>
 __global__ void __launch_bounds__(kPruneWarps * 32)
     prune_bitmap_kernel(const float* __restrict__ w, uint64_t len, uint32_t T, uint64_t r,
                         const uint32_t* __restrict__ tie_prefix, uint64_t* __restrict__ words,
@@ -409,25 +411,25 @@ __global__ void __launch_bounds__(kPruneWarps * 32)
                         BitmapCounts* __restrict__ counts, uint64_t nchunks, PruneCandBuf cb) {
   extern __shared__ __align__(16) float ring_all[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  float* ring = ring_all + (size_t)warp * kKeyStages * kStageFloats;
-  uint32_t* cbk = reinterpret_cast<uint32_t*>(ring_all + (size_t)kPruneWarps * kKeyStages * kStageFloats) +
+  float* ring = ring_all + (size_t)warp * kS * kStageFloats;
+  uint32_t* cbk = reinterpret_cast<uint32_t*>(ring_all + (size_t)kPruneWarps * kS * kStageFloats) +
                   warp * 2 * kCandBuf;
   uint32_t* cbi = cbk + kCandBuf;
   // CTA histogram of the candidates' top digit (warp-aggregated smem
   // atomics; a window whose lower end is crowded sends most to one bin),
   // added to the global one once at the end
-  uint32_t* chist = reinterpret_cast<uint32_t*>(ring_all + (size_t)kPruneWarps * kKeyStages * kStageFloats) +
+  uint32_t* chist = reinterpret_cast<uint32_t*>(ring_all + (size_t)kPruneWarps * kS * kStageFloats) +
                     kPruneWarps * 2 * kCandBuf;
   if (cb.hist) {
     for (int b = threadIdx.x; b < (1 << kCandHistBits); b += blockDim.x) chist[b] = 0;
     __syncthreads();
   }
   // kBulk: one mbarrier per stage per warp, after the histogram
-  uint64_t* mbars = reinterpret_cast<uint64_t*>(chist + (1 << kCandHistBits)) + warp * kKeyStages;
+  uint64_t* mbars = reinterpret_cast<uint64_t*>(chist + (1 << kCandHistBits)) + warp * kS;
   uint32_t phases = 0;  // bit s: parity of stage s's next completion
   if constexpr (kBulk) {
     if (lane == 0) {
-      for (int q = 0; q < kKeyStages; ++q) mbar_init(mbars + q);
+      for (int q = 0; q < kS; ++q) mbar_init(mbars + q);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncwarp();
@@ -450,7 +452,7 @@ __global__ void __launch_bounds__(kPruneWarps * 32)
   const uint64_t nw_total = (uint64_t)gridDim.x * kPruneWarps;
   const uint64_t c0 = (uint64_t)blockIdx.x * kPruneWarps + warp;
 #pragma unroll
-  for (int s = 0; s < kKeyStages - 1; ++s) {
+  for (int s = 0; s < kS - 1; ++s) {
     const uint64_t cc = c0 + s * nw_total;
     if constexpr (kBulk) {
       if (lane == 0 && cc < nchunks && full(cc)) chunk_issue_bulk(ring + s * kStageFloats, mbars + s, w, words, cc);
@@ -463,8 +465,8 @@ __global__ void __launch_bounds__(kPruneWarps * 32)
   for (uint64_t c = c0; c < nchunks; c += nw_total) {
     const int cur = slot;
     {
-      const uint64_t cn = c + (kKeyStages - 1) * nw_total;
-      const int sn = slot == 0 ? kKeyStages - 1 : slot - 1;
+      const uint64_t cn = c + (kS - 1) * nw_total;
+      const int sn = slot == 0 ? kS - 1 : slot - 1;
       __syncwarp();  // every lane is done reading stage sn (the previous chunk)
       if constexpr (kBulk) {
         if (lane == 0 && cn < nchunks && full(cn)) chunk_issue_bulk(ring + sn * kStageFloats, mbars + sn, w, words, cn);
@@ -475,12 +477,12 @@ __global__ void __launch_bounds__(kPruneWarps * 32)
       } else {
         if (cn < nchunks && full(cn)) chunk_issue(ring + sn * kStageFloats, w, words, cn);
         asm volatile("cp.async.commit_group;" ::: "memory");
-        asm volatile("cp.async.wait_group %0;" ::"n"(kKeyStages - 1) : "memory");
+        asm volatile("cp.async.wait_group %0;" ::"n"(kS - 1) : "memory");
       }
       __syncwarp();  // lanes read stage cells other lanes' copies filled
     }
     const float* st = ring + slot * kStageFloats;
-    slot = slot == kKeyStages - 1 ? 0 : slot + 1;
+    slot = slot == kS - 1 ? 0 : slot + 1;
     const bool fc = full(c);
     const uint64_t e0 = c * (uint64_t)kChunk + 32 * lane;
     // per element: one compare against T (funnel-shifted sign) and the
@@ -827,23 +829,36 @@ void launch_prune_bitmap(const float* w, uint64_t len, uint32_t T, uint64_t r,
   cudaMemsetAsync(counts, 0, sizeof(BitmapCounts), s);
   if (cand.hist) cudaMemsetAsync(cand.hist, 0, sizeof(uint32_t) << kCandHistBits, s);
   if (!nc) return;
-  // PACT_BITMAP_CPASYNC=1: the per-lane cp.async ring instead of the bulk copies
+  // PACT_BITMAP_CPASYNC=1: the per-lane cp.async ring instead of the bulk
+  // copies; PACT_BITMAP_STAGES=3: three bulk stages per warp (two chunks in
+  // flight, 2 CTAs per SM instead of 3)
   static const bool bulk = getenv("PACT_BITMAP_CPASYNC") == nullptr;
+  static const bool three = bulk && getenv("PACT_BITMAP_STAGES") && atoi(getenv("PACT_BITMAP_STAGES")) == 3;
+  constexpr size_t kSmem3 = bitmap_smem(3);
   static DeviceCache<unsigned> cap;
   unsigned& cp = cap.get();
   if (!cp) {
-    cudaFuncSetAttribute(prune_bitmap_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBitmapSmem);
-    cudaFuncSetAttribute(prune_bitmap_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBitmapSmem);
-    cp = persistent_grid(prune_bitmap_kernel<true>, kPruneWarps * 32, kBitmapSmem, ~0ull >> 8, kPruneWarps);
+    cudaFuncSetAttribute(prune_bitmap_kernel<true, kKeyStages>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kBitmapSmem);
+    cudaFuncSetAttribute(prune_bitmap_kernel<false, kKeyStages>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kBitmapSmem);
+    cudaFuncSetAttribute(prune_bitmap_kernel<true, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem3);
+    cp = three ? persistent_grid(prune_bitmap_kernel<true, 3>, kPruneWarps * 32, kSmem3, ~0ull >> 8, kPruneWarps)
+               : persistent_grid(prune_bitmap_kernel<true, kKeyStages>, kPruneWarps * 32, kBitmapSmem, ~0ull >> 8,
+                                 kPruneWarps);
   }
   const uint64_t need = (nc + kPruneWarps - 1) / kPruneWarps;
   const unsigned grid = (unsigned)(need < cp ? need : cp);
-  if (bulk)
-    prune_bitmap_kernel<true><<<grid, kPruneWarps * 32, kBitmapSmem, s>>>(
+  if (three)
+    prune_bitmap_kernel<true, 3><<<grid, kPruneWarps * 32, kSmem3, s>>>(
+        w, len, T, r, tie_prefix, words, (len + 63) / 64, chunk_popc, ties_out, ties_prev, tie_words, tie_old,
+        counts, nc, cand);
+  else if (bulk)
+    prune_bitmap_kernel<true, kKeyStages><<<grid, kPruneWarps * 32, kBitmapSmem, s>>>(
         w, len, T, r, tie_prefix, words, (len + 63) / 64, chunk_popc, ties_out, ties_prev, tie_words, tie_old,
         counts, nc, cand);
   else
-    prune_bitmap_kernel<false><<<grid, kPruneWarps * 32, kBitmapSmem, s>>>(
+    prune_bitmap_kernel<false, kKeyStages><<<grid, kPruneWarps * 32, kBitmapSmem, s>>>(
         w, len, T, r, tie_prefix, words, (len + 63) / 64, chunk_popc, ties_out, ties_prev, tie_words, tie_old,
         counts, nc, cand);
   note_launch();
