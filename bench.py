@@ -682,7 +682,7 @@ def main():
             "per_layer_us": round(t_layer * 1e6, 1), "per_layer_layers": len(layer_offs) - 1,
             "per_layer_reuse_us": round(t_layer_reuse * 1e6, 1),
             "per_layer_vs_global_first_time": round(t_layer / t_full, 3),
-            "paths_legend": "1 sampled window + counting pass, 2 full radix, 3 threshold reuse, 4 moved threshold from window candidates, 5 first time: one windowed pass seeded by the sample",
+            "paths_legend": "1 sampled window, 2 full radix, 3 threshold reuse, 4 moved threshold from window candidates",
         }
         stages["mask_change_step_us"] = round(t_step_change * 1e6, 1)
         stages["mask_reuse_step_us"] = round(t_step_hit * 1e6, 1)

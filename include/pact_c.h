@@ -157,9 +157,7 @@ typedef struct pact_prune_stats {
   uint64_t k;           /* drop count (sparsity.cpp:33-40) */
   uint32_t threshold;   /* k-th smallest |w| key (bits & 0x7fffffff) */
   uint64_t c_lt;        /* #(key < threshold) */
-  int path;             /* 0 trivial, 1 sampled window + counting pass, 2 full radix fallback,
-                           3 previous threshold reused, 4 moved threshold from the window
-                           candidates, 5 first time: one windowed pass seeded by the sample */
+  int path;             /* 0 trivial, 1 sampled window, 2 full radix fallback */
   uint64_t candidates;  /* window candidates compacted */
 } pact_prune_stats;
 

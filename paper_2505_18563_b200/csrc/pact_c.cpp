@@ -1175,45 +1175,14 @@ pact_status pact_prune_magnitude(pact_ctx* ctx, const float* w, uint64_t len, fl
   TRY(out->ties[0].ensure(nc * 4));
   TRY(out->ties[1].ensure(nc * 4));
   TRY(out->tie_prefix.ensure((nc + 1) * 4));
-  Small* sm = ctx->ws_small.as<Small>();
-  // first-time prune (no previous threshold for this k): seed the reuse
-  // machinery with the sampled window instead of running the counting pass
-  // -- one windowed bitmap pass at the window's upper end compacts every
-  // element of the window, and the moved-threshold fix-ups below finish the
-  // mask (one read of the weights instead of two). The window's candidates
-  // are ~1.4% of the elements (a 16384-key sample, +-6 sigma), so the
-  // candidate buffers are sized for 4% on this call; a window that misses
-  // the k-th key falls through to the counting path. (PACT_PRUNE_COUNT_PASS=1:
-  // the counting path always.)
-  static const bool seed_env = getenv("PACT_PRUNE_COUNT_PASS") == nullptr;
-  bool seeded = false;
-  if (seed_env && !(out->spec_valid && out->spec_k == k) && len >= (1u << 20)) {
-    pactk::launch_prune_sample(w, len, k, &sm->win, s);
-    CUDA_TRY(cudaGetLastError());
-    CUDA_TRY(cudaMemcpyAsync(ctx->pin.p, &sm->win, sizeof(pactk::PruneWindow), cudaMemcpyDeviceToHost, s));
-    CUDA_TRY(cudaStreamSynchronize(s));
-    pactk::PruneWindow wn;
-    std::memcpy(&wn, ctx->pin.p, sizeof wn);
-    if (wn.lo < wn.hi) {
-      out->spec_valid = 1;
-      out->spec_k = k;
-      out->spec_T = wn.hi;
-      out->spec_c_lt = 0;
-      out->spec_prefix_valid = 0;
-      out->spec_drop_all = 1;  // ties at the seed all dropped by the pass
-      out->win_lo = wn.lo;
-      out->win_hi = wn.hi;
-      out->win_valid = 1;
-      seeded = true;
-    }
-  }
   // window half-width (ranks) and candidate capacity
   const uint64_t mwin = std::max<uint64_t>(4096, len >> 11);
-  const uint64_t ccap = seeded ? std::max<uint64_t>(4 * mwin + 65536, len / 25 + 65536) : 4 * mwin + 65536;
+  const uint64_t ccap = 4 * mwin + 65536;
   TRY(out->cand_key.ensure(ccap * 4));
   TRY(out->cand_idx.ensure(ccap * 4));
   uint32_t* ckey = out->cand_key.as<uint32_t>();
   uint32_t* cidx = out->cand_idx.as<uint32_t>();
+  Small* sm = ctx->ws_small.as<Small>();
   pactk::BitmapCounts* bc = &sm->bcounts;
   pactk::BitmapCounts hb{};
   const int had_digest = out->digest_valid;
@@ -1323,8 +1292,7 @@ pact_status pact_prune_magnitude(pact_ctx* ctx, const float* w, uint64_t len, fl
       }
       if (rep.gate[1]) {
         const bool chg = rep.gate[0] != 0;
-        st.path = seeded ? 5 : 3;
-        if (seeded) out->win_valid = 0;  // the k-th key was the seed itself: no window around it yet
+        st.path = 3;
         st.threshold = T0;
         st.c_lt = hb.n_lt;
         st.candidates = hb.n_cand;
@@ -1358,8 +1326,7 @@ pact_status pact_prune_magnitude(pact_ctx* ctx, const float* w, uint64_t len, fl
         TRY(fix_ties(r));
       else
         changed |= hb.changed_tie;
-      st.path = seeded ? 5 : 3;
-      if (seeded) out->win_valid = 0;
+      st.path = 3;
       st.threshold = T0;
       st.c_lt = hb.n_lt;
       st.candidates = hb.n_cand;
@@ -1422,13 +1389,13 @@ pact_status pact_prune_magnitude(pact_ctx* ctx, const float* w, uint64_t len, fl
         out->digest_valid = 1;
         out->spec_T = h.w.T1;
         out->spec_c_lt = h.w.c_lt1;
-        st.path = seeded ? 5 : 4;
+        st.path = 4;
         st.threshold = h.w.T1;
         st.c_lt = h.w.c_lt1;
         st.candidates = ncand;
         // re-centre the window when T' sits near one of its ends
         const uint64_t pos = h.w.below + 1;  // T's rank among the candidates
-        if (seeded || pos < mwin / 2 || ncand - std::min(ncand, pos) < mwin / 2)  // (a seed's window is wide)
+        if (pos < mwin / 2 || ncand - std::min(ncand, pos) < mwin / 2)
           TRY(set_window(ckey, ncand, base, out->win_hi, (int64_t)pos - (int64_t)mwin, (int64_t)pos + (int64_t)mwin,
                          h.w.T1));
         if (out->nnz != len - k)
