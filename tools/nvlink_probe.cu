@@ -56,6 +56,31 @@ __global__ void fold2(const float4* __restrict__ loc, const float4* __restrict__
 // smem-staged bulk copy / bulk reduce-add to a (peer) global buffer: 4 KiB
 // per warp-iteration, issued by lane 0 (the n = 2 reduce-push candidate)
 template <bool kReduce>
+// one-way push of `seg` floats per bulk op (each warp: load a segment into
+// smem, bulk-copy it to the peer at the same offset; two smem slots so a
+// segment's copy drains while the next one loads -- the pack's pattern)
+__global__ void bulk_push_seg(const float* __restrict__ src, float* __restrict__ dst, size_t n, int seg) {
+  __shared__ __align__(128) float st[8][2][4096];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int slot = 0;
+  for (size_t c = (size_t)blockIdx.x * 8 + warp; c * seg < n; c += (size_t)gridDim.x * 8) {
+    float* b = st[warp][slot];
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+    __syncwarp();
+    for (int i = lane; i < seg / 4; i += 32)
+      reinterpret_cast<float4*>(b)[i] = reinterpret_cast<const float4*>(src + c * seg)[i];
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    if (lane == 0) {
+      const uint32_t sa = (uint32_t)__cvta_generic_to_shared(b);
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n"
+                   " cp.async.bulk.commit_group;" ::"l"(dst + c * seg), "r"(sa), "r"(seg * 4) : "memory");
+    }
+    slot ^= 1;
+  }
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 __global__ void bulk_push(const float* __restrict__ src, float* __restrict__ dst, size_t n) {
   __shared__ __align__(128) float st[8][1024];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -120,6 +145,13 @@ int main() {
   run("remote READ float4 ld.cg  (GPU1 -> GPU0)", [&] { rd4<<<grid, blk>>>((float4*)a1, (float4*)b0, n / 4); });
   run("remote WRITE float4        (GPU0 -> GPU1)", [&] { wr4<<<grid, blk>>>((float4*)a0, (float4*)a1, n / 4); });
   run("remote WRITE f32 coalesced (GPU0 -> GPU1)", [&] { wr1<<<grid, blk>>>(a0, a1, n); });
+  // one-way bulk pushes by op size (the pack pushes ~400-byte runs)
+  for (int seg : {100, 256, 1024, 4096})
+    for (int g : {148 * 2, 148 * 6}) {
+      char nm[96];
+      snprintf(nm, sizeof nm, "bulk push %5d B ops, %d CTAs", seg * 4, g);
+      run(nm, [&] { bulk_push_seg<<<g, 256>>>(a0, a1, n, seg); });
+    }
   // how few SMs saturate a one-way NVLink push (float4 stores, 256 MB)
   for (int g : {8, 16, 32, 64})
     for (int per : {1, 4}) {
