@@ -55,7 +55,6 @@ __global__ void fold2(const float4* __restrict__ loc, const float4* __restrict__
 
 // smem-staged bulk copy / bulk reduce-add to a (peer) global buffer: 4 KiB
 // per warp-iteration, issued by lane 0 (the n = 2 reduce-push candidate)
-template <bool kReduce>
 // one-way push of `seg` floats per bulk op (each warp: load a segment into
 // smem, bulk-copy it to the peer at the same offset; two smem slots so a
 // segment's copy drains while the next one loads -- the pack's pattern)
@@ -81,6 +80,7 @@ __global__ void bulk_push_seg(const float* __restrict__ src, float* __restrict__
   if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+template <bool kReduce>
 __global__ void bulk_push(const float* __restrict__ src, float* __restrict__ dst, size_t n) {
   __shared__ __align__(128) float st[8][1024];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
