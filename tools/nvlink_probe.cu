@@ -59,10 +59,10 @@ __global__ void fold2(const float4* __restrict__ loc, const float4* __restrict__
 // smem, bulk-copy it to the peer at the same offset; two smem slots so a
 // segment's copy drains while the next one loads -- the pack's pattern)
 __global__ void bulk_push_seg(const float* __restrict__ src, float* __restrict__ dst, size_t n, int seg) {
-  __shared__ __align__(128) float st[8][2][4096];
+  __shared__ __align__(128) float st[4][2][1024];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int slot = 0;
-  for (size_t c = (size_t)blockIdx.x * 8 + warp; c * seg < n; c += (size_t)gridDim.x * 8) {
+  for (size_t c = (size_t)blockIdx.x * 4 + warp; c * seg < n; c += (size_t)gridDim.x * 4) {
     float* b = st[warp][slot];
     if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
     __syncwarp();
@@ -146,11 +146,11 @@ int main() {
   run("remote WRITE float4        (GPU0 -> GPU1)", [&] { wr4<<<grid, blk>>>((float4*)a0, (float4*)a1, n / 4); });
   run("remote WRITE f32 coalesced (GPU0 -> GPU1)", [&] { wr1<<<grid, blk>>>(a0, a1, n); });
   // one-way bulk pushes by op size (the pack pushes ~400-byte runs)
-  for (int seg : {100, 256, 1024, 4096})
-    for (int g : {148 * 2, 148 * 6}) {
+  for (int seg : {100, 256, 1024})
+    for (int g : {148 * 4, 148 * 6}) {
       char nm[96];
-      snprintf(nm, sizeof nm, "bulk push %5d B ops, %d CTAs", seg * 4, g);
-      run(nm, [&] { bulk_push_seg<<<g, 256>>>(a0, a1, n, seg); });
+      snprintf(nm, sizeof nm, "bulk push %5d B ops, %d CTAs x 4 warps", seg * 4, g);
+      run(nm, [&] { bulk_push_seg<<<g, 128>>>(a0, a1, n, seg); });
     }
   // how few SMs saturate a one-way NVLink push (float4 stores, 256 MB)
   for (int g : {8, 16, 32, 64})
