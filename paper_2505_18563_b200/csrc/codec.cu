@@ -230,13 +230,7 @@ __device__ __forceinline__ void issue_run(float* dst, const float* __restrict__ 
 // cp.async writes and the lane-major LDS.128 reads are conflict-free; the
 // compacted run is written back in place (after every lane has read its
 // cells) at the destination's 16-byte phase and leaves as one coalesced run.
-// kPushBatch: each warp packs a contiguous block of chunks, so its runs are
-// consecutive in the packed vector, and pushes them in ~3 KiB batches (one
-// bulk copy each, from one of two per-warp batch buffers) instead of one
-// ~400-byte bulk copy and two scalar partial-cell stores per run (measured
-// one-way NVLink: 400-byte bulk ops 547-576 GB/s, 1 KiB 655-680, 4 KiB 696)
-constexpr int kPushNone = 0, kPushStores = 1, kPushTma = 2, kPushBatch = 3;
-constexpr int kBatchFlush = 768;  // floats buffered before a batch leaves
+constexpr int kPushNone = 0, kPushStores = 1, kPushTma = 2;
 
 // NVLink push of a staged run as one bulk async copy (TMA engine, smem ->
 // peer global) for the whole 16-byte cells, scalar stores for the partial
@@ -304,21 +298,10 @@ __global__ void __launch_bounds__(kPuWarps * 32)
                    uint64_t ce, float* __restrict__ remote, P2PView v, P2PSig sg, int pdl_trigger) {
   __shared__ __align__(16) float dsm[kPuWarps][2][kPkStage];
   __shared__ __align__(16) uint64_t wsm[kPuWarps][3][kWbuf];
-  extern __shared__ __align__(16) float pk_batch[];  // kPushBatch: [kPuWarps][2][kPkStage]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const bool vec_ok = (((uintptr_t)g) & 15) == 0;
   const uint64_t nwt = (uint64_t)gridDim.x * kPuWarps;
-  // chunk order: round robin (c, c + nwt, ...), or for kPushBatch a
-  // contiguous block per warp
-  const uint64_t gw = (uint64_t)blockIdx.x * kPuWarps + warp;
-  const uint64_t per = (ce - cb + nwt - 1) / nwt;
-  uint64_t c = kPush == kPushBatch ? cb + gw * per : cb + gw;
-  const uint64_t cend = kPush == kPushBatch ? (c + per < ce ? c + per : ce) : ce;
-  const uint64_t stride = kPush == kPushBatch ? 1 : nwt;
-  float* const pbuf = pk_batch + (size_t)warp * 2 * kPkStage;
-  int pb = 0;
-  uint32_t pb_len = 0, pb_ph = 0, pb_base = 0;
-  bool pb_wait = false;
+  uint64_t c = cb + (uint64_t)blockIdx.x * kPuWarps + warp;
   // a programmatic dependent (the single-GPU unpack) may be scheduled as soon
   // as SMs free up; it waits for this grid's completion before reading
   // `packed`. Only when the caller launches one: a PDL-capable successor of
@@ -326,11 +309,11 @@ __global__ void __launch_bounds__(kPuWarps * 32)
   if (pdl_trigger) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if constexpr (kPush != kPushNone)
     if (sg.trace && threadIdx.x == 0) atomicMin(&g_pair_trace[0], gtimer());
-  if (c < cend) {
+  if (c < ce) {
     // prologue: words(c0), words(c1), data(c0)
     offs_words_issue(wsm[warp][0], words, chunk_off, c);
     cp_commit();
-    if (c + stride < cend) offs_words_issue(wsm[warp][1], words, chunk_off, c + stride);
+    if (c + nwt < ce) offs_words_issue(wsm[warp][1], words, chunk_off, c + nwt);
     cp_commit();
     asm volatile("cp.async.wait_group 1;" ::: "memory");
     __syncwarp();
@@ -340,22 +323,22 @@ __global__ void __launch_bounds__(kPuWarps * 32)
     uint32_t h = reinterpret_cast<const uint32_t*>(wsm[warp][0])[lane];
     uint32_t hc = __popc(h), incl = warp_incl_scan(hc);
     int wi = 0, pi = 0;
-    for (; c < cend; c += stride) {
+    for (; c < ce; c += nwt) {
       const int w1 = wi == 2 ? 0 : wi + 1, w2 = w1 == 2 ? 0 : w1 + 1;
-      if (c + 2 * stride < cend) offs_words_issue(wsm[warp][w2], words, chunk_off, c + 2 * stride);
+      if (c + 2 * nwt < ce) offs_words_issue(wsm[warp][w2], words, chunk_off, c + 2 * nwt);
       cp_commit();
-      asm volatile("cp.async.wait_group 1;" ::: "memory");  // words(c+stride), data(c) landed
+      asm volatile("cp.async.wait_group 1;" ::: "memory");  // words(c+nwt), data(c) landed
       __syncwarp();
       if constexpr (kPush == kPushTma) {  // the bulk push of stage pi ^ 1 has read it
         if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         __syncwarp();
       }
-      if (c + stride < cend) pack_data_issue(dsm[warp][pi ^ 1], g, len, vec_ok, wsm[warp][w1], c + stride);
+      if (c + nwt < ce) pack_data_issue(dsm[warp][pi ^ 1], g, len, vec_ok, wsm[warp][w1], c + nwt);
       cp_commit();
       const uint64_t* wc = wsm[warp][wi];
       const uint32_t base = reinterpret_cast<const uint32_t*>(wc + kChunkWords)[0];
       float* st = dsm[warp][pi];
-      const uint32_t h_n = reinterpret_cast<const uint32_t*>(wsm[warp][w1])[lane];  // chunk c + stride
+      const uint32_t h_n = reinterpret_cast<const uint32_t*>(wsm[warp][w1])[lane];  // chunk c + nwt
       const uint32_t hc_n = __popc(h_n), incl_n = warp_incl_scan(hc_n);
       const uint32_t run = __shfl_sync(0xffffffffu, incl, 31);
       const uint32_t ph = (uint32_t)(((uintptr_t)(packed + base) >> 2) & 3u);
@@ -393,35 +376,6 @@ __global__ void __launch_bounds__(kPuWarps * 32)
       for (uint32_t i = lane; i < run; i += 32) dst[i] = st[ph + i];
       if constexpr (kPush == kPushStores) write_run(remote + base - ph, st, ph, run);
       if constexpr (kPush == kPushTma) push_run_bulk(remote + base - ph, st, ph, run);
-      if constexpr (kPush == kPushBatch) {
-        // append the run to the batch (consecutive chunks: consecutive runs)
-        if (pb_len && pb_ph + pb_len + run > (uint32_t)kPkStage) {
-          __syncwarp();
-          push_run_bulk(remote + pb_base - pb_ph, pbuf + pb * kPkStage, pb_ph, pb_len);
-          pb ^= 1;
-          pb_len = 0;
-          pb_wait = true;
-        }
-        if (pb_wait) {  // the other batch buffer's copy has read it
-          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-          __syncwarp();
-          pb_wait = false;
-        }
-        if (pb_len == 0) {
-          pb_base = base;
-          pb_ph = ph;
-        }
-        float* bq = pbuf + pb * kPkStage + pb_ph + pb_len;
-        for (uint32_t i = lane; i < run; i += 32) bq[i] = st[ph + i];
-        pb_len += run;
-        if (pb_ph + pb_len >= (uint32_t)kBatchFlush) {
-          __syncwarp();
-          push_run_bulk(remote + pb_base - pb_ph, pbuf + pb * kPkStage, pb_ph, pb_len);
-          pb ^= 1;
-          pb_len = 0;
-          pb_wait = true;
-        }
-      }
       __syncwarp();  // stage pi and word buffer wi are refilled next
       wi = w1;
       pi ^= 1;
@@ -430,13 +384,7 @@ __global__ void __launch_bounds__(kPuWarps * 32)
       incl = incl_n;
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
-    if constexpr (kPush == kPushBatch) {
-      if (pb_len) {
-        __syncwarp();
-        push_run_bulk(remote + pb_base - pb_ph, pbuf + pb * kPkStage, pb_ph, pb_len);
-      }
-    }
-    if constexpr (kPush == kPushTma || kPush == kPushBatch) {  // the bulk stores have landed in the peer's memory
+    if constexpr (kPush == kPushTma) {  // the bulk stores have landed in the peer's memory
       if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;\n fence.proxy.async.global;" ::: "memory");
       __syncwarp();
     }
@@ -928,20 +876,12 @@ void launch_pack_push(const float* g, uint64_t len, const uint64_t* words, const
   // PACT_PUSH_STORES=1: float4 stores instead of bulk async copies (measured
   // c2 n=2 pack 61 vs 55-61 us: the exchange is NVLink-bound either way)
   static const bool stores = getenv("PACT_PUSH_STORES") != nullptr;
-  // PACT_PUSH_BATCH=1: contiguous chunk blocks per warp, runs pushed in batches
-  static const bool batch = !stores && getenv("PACT_PUSH_BATCH") != nullptr;
-  constexpr int kDynBatch = kPuWarps * 2 * kPkStage * (int)sizeof(float);
-  static DeviceCache<int> cc;
-  int& cap = cc.get();
+  static int cap = 0;
   if (!cap)
     cap = stores ? persistent_grid(pack_lm_kernel<kPushStores>, kPuWarps)
-                 : batch ? persistent_grid_dyn(pack_lm_kernel<kPushBatch>, kPuWarps, kDynBatch)
-                         : persistent_grid(pack_lm_kernel<kPushTma>, kPuWarps);
+                 : persistent_grid(pack_lm_kernel<kPushTma>, kPuWarps);
   const unsigned grid = grid_for(cap, nc, kPuWarps);
-  if (batch)
-    pack_lm_kernel<kPushBatch><<<grid, kPuWarps * 32, kDynBatch, s>>>(g, len, words, chunk_off, packed, 0, nc,
-                                                                      remote, v, sg, 0);
-  else if (stores)
+  if (stores)
     pack_lm_kernel<kPushStores><<<grid, kPuWarps * 32, 0, s>>>(g, len, words, chunk_off, packed, 0, nc, remote,
                                                                v, sg, 0);
   else
